@@ -1,0 +1,783 @@
+// capi.cpp -- implementation of the C-ABI in include/paraplan_cuda.h.
+//
+// Host side of Planner::plan_step (src/planner.cpp:238-351 in the reference):
+//   * validation with the reference's messages,
+//   * snapshot staging (pinned host -> HBM, one copy per tick),
+//   * the restart x iteration schedule: with n_iter_max == 1 every candidate
+//     of every restart is independent (each restart re-centres on the warm
+//     start, :271-277) and the whole tick is ONE kernel launch; iterations
+//     >= 1 centre on the incumbent and run as dependent rounds,
+//   * the ordered, strict-better merge of round winners (:310-330),
+//   * the FP64 epilogue (:339-350) on the host, bit-identical to the
+//     reference because best_theta is regenerated with the host KeyedRng and
+//     re-simulated through the same FP64 primitives.
+// Compiled with -ffp-contract=off -fno-math-errno.
+#include "paraplan_cuda.h"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <exception>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../cuda/device_api.h"
+#include "paraplan/geometry.hpp"
+#include "paraplan/planner.hpp"
+#include "paraplan/policy.hpp"
+#include "paraplan/rng.hpp"
+
+namespace {
+
+thread_local std::string g_error;
+
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct NoDevice : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) {
+    throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+  }
+}
+
+template <class F>
+pp_status guarded(F&& f) {
+  try {
+    f();
+    return PP_OK;
+  } catch (const std::invalid_argument& e) {
+    g_error = e.what();
+    return PP_INVALID_ARGUMENT;
+  } catch (const NoDevice& e) {
+    g_error = e.what();
+    return PP_NO_DEVICE;
+  } catch (const CudaError& e) {
+    g_error = e.what();
+    return PP_CUDA_ERROR;
+  } catch (const std::exception& e) {
+    g_error = e.what();
+    return PP_RUNTIME_ERROR;
+  }
+}
+
+// Device buffer that only grows.
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  // Returns true when the buffer was (re)allocated.
+  bool reserve(size_t bytes, const char* what) {
+    if (bytes <= cap) return false;
+    if (p != nullptr) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    ck(cudaMalloc(&p, bytes), what);
+    cap = bytes;
+    return true;
+  }
+  void release() {
+    if (p != nullptr) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+};
+
+struct HostBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  void reserve(size_t bytes, const char* what) {
+    if (bytes <= cap) return;
+    if (p != nullptr) cudaFreeHost(p);
+    p = nullptr;
+    cap = 0;
+    ck(cudaMallocHost(&p, bytes), what);
+    cap = bytes;
+  }
+  void release() {
+    if (p != nullptr) cudaFreeHost(p);
+    p = nullptr;
+    cap = 0;
+  }
+};
+
+paraplan::VehicleParams params_of(const pp_vehicle& v) {
+  paraplan::VehicleParams p;
+  p.l_f = v.l_f;
+  p.l_r = v.l_r;
+  p.delta_max = v.delta_max;
+  p.delta_rate_max = v.delta_rate_max;
+  p.u_v_min = v.u_v_min;
+  p.u_v_max = v.u_v_max;
+  p.overhang_front = v.overhang_front;
+  p.overhang_rear = v.overhang_rear;
+  p.half_width = v.half_width;
+  p.T_s = v.T_s;
+  return p;
+}
+
+paraplan::PlannerConfig config_of(const pp_config& c) {
+  paraplan::PlannerConfig cfg;
+  cfg.H = c.H;
+  cfg.n_restarts = c.n_restarts;
+  cfg.n_iter_max = c.n_iter_max;
+  cfg.n_candidates = c.n_candidates;
+  cfg.n_obst_pts = c.n_obst_pts;
+  cfg.tol = {c.eps_xi, c.eps_eta, c.eps_phi, c.eps_v};
+  cfg.sigma_log_low = c.sigma_log_low;
+  cfg.sigma_log_high = c.sigma_log_high;
+  cfg.master_seed = c.master_seed;
+  cfg.early_exit = c.early_exit != 0;
+  cfg.threads = c.threads;
+  cfg.precision = c.precision;
+  cfg.device = c.device;
+  cfg.refine = c.refine != 0;
+  return cfg;
+}
+
+struct Key {
+  int cls = 0;
+  double k1 = 0.0, k2 = 0.0;
+};
+
+bool key_better(const Key& a, const Key& b) {  // src/planner.cpp:40-44
+  if (a.cls != b.cls) return a.cls > b.cls;
+  if (a.k1 != b.k1) return a.k1 > b.k1;
+  return a.k2 > b.k2;
+}
+
+}  // namespace
+
+struct pp_handle {
+  pp_model model{};
+  std::vector<int32_t> sizes;
+  paraplan::VehicleParams params;
+  paraplan::PlannerConfig cfg;
+  paraplan::NormConstants norm;
+  std::unique_ptr<paraplan::MlpPolicy> policy;
+  paraplan::ChassisPolytope chassis;
+  int P = 0;
+  ppdev::NetKind kind = ppdev::NetKind::kGeneric;
+  int device = 0;
+  bool fp64 = false;
+
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  DevBuf d_field, d_params, d_result, d_tiles, d_counters, d_samples, d_scratch, d_injected;
+  HostBuf h_field, h_params, h_result;
+
+  // resident snapshot
+  bool snap_valid = false;
+  ppdev::RoundArgs base{};
+  int field_smem_bytes = 0;
+
+  pp_timing timing{};
+};
+
+namespace {
+
+// Goal transform and constants of a snapshot (src/planner.cpp:70-81).
+void upload_snapshot(pp_handle* h, const pp_snapshot& s) {
+  const auto& cfg = h->cfg;
+  if (s.n_points < 0 || s.field_H < 0) throw std::invalid_argument("malformed obstacle field");
+  if (s.n_points > 0 && s.field_H < cfg.H) {
+    // The reference would read past the field (geometry.hpp:82-85).
+    throw std::invalid_argument("obstacle field shorter than the planning horizon");
+  }
+  if (s.n_points > 0 && s.field_xy == nullptr) throw std::invalid_argument("null obstacle field");
+  ppdev::RoundArgs& a = h->base;
+  a = ppdev::RoundArgs{};
+  const paraplan::Pose2 anchor{s.ev_x, s.ev_y, s.ev_phi};
+  const paraplan::Vec2 g = paraplan::to_ev_frame(anchor, {s.goal_x, s.goal_y});
+  a.gx = g.x;
+  a.gy = g.y;
+  a.gphi = s.goal_phi - anchor.phi;
+  a.gv = s.goal_v;
+  a.gcos = std::cos(a.gphi);
+  a.gsin = std::sin(a.gphi);
+  a.v0 = s.ev_v;
+  a.act0 = s.actuator_delta;
+  a.pa0 = s.prev_a0;
+  a.d_xi = h->norm.d_xi;
+  a.d_eta = h->norm.d_eta;
+  a.d_phi = h->norm.d_phi;
+  a.d_v = h->norm.d_v;
+  a.eps_xi = cfg.tol.eps_xi;
+  a.eps_eta = cfg.tol.eps_eta;
+  a.eps_phi = cfg.tol.eps_phi;
+  a.eps_v = cfg.tol.eps_v;
+  const auto& p = h->params;
+  a.delta_max = p.delta_max;
+  a.window = p.delta_rate_max * p.T_s;
+  a.l_r = p.l_r;
+  a.wheelbase = p.l_f + p.l_r;
+  a.T_s = p.T_s;
+  a.u_v_min = p.u_v_min;
+  a.u_v_max = p.u_v_max;
+  a.fe = p.front_extent();
+  a.re = p.rear_extent();
+  a.hw = p.half_width;
+  const double radius = h->chassis.bounding_radius();
+  a.r2 = radius * radius;
+  a.sig_lo = cfg.sigma_log_low;
+  a.sig_span = cfg.sigma_log_high - cfg.sigma_log_low;
+  a.H = cfg.H;
+  a.n_params = h->P;
+  a.n_layers = static_cast<int32_t>(h->sizes.size());
+  for (size_t i = 0; i < h->sizes.size(); ++i) a.sizes[i] = h->sizes[i];
+
+  // Only rows 0..H are ever read; ship those, in the compute precision.
+  const int N = s.n_points;
+  a.n_points = N;
+  const size_t count = static_cast<size_t>(cfg.H + 1) * static_cast<size_t>(N);
+  const size_t elem = h->fp64 ? sizeof(double) : sizeof(float);
+  const size_t bytes = 2 * count * elem;
+  if (count > 0) {
+    h->h_field.reserve(bytes, "pinned field");
+    h->d_field.reserve(bytes, "device field");
+    if (h->fp64) {
+      std::memcpy(h->h_field.p, s.field_xy, bytes);
+    } else {
+      float* dst = static_cast<float*>(h->h_field.p);
+      for (size_t i = 0; i < 2 * count; ++i) dst[i] = static_cast<float>(s.field_xy[i]);
+    }
+    ck(cudaMemcpyAsync(h->d_field.p, h->h_field.p, bytes, cudaMemcpyHostToDevice, h->stream),
+       "field H2D");
+    h->timing.h2d_bytes += static_cast<int64_t>(bytes);
+  }
+  a.field = h->d_field.p;
+  h->field_smem_bytes = bytes <= 32 * 1024 ? static_cast<int>(bytes) : 0;
+  h->snap_valid = true;
+}
+
+// key prefix fold^4(seed, t, restart, iter) (src/rng.cpp:26-34 minus the
+// candidate fold, which the kernel applies).
+uint64_t key_prefix(uint64_t seed, uint64_t t, uint64_t r, uint64_t i) {
+  // KeyedRng's state after four folds == prefix; reuse the public class on a
+  // dummy candidate would fold a fifth time, so recompute here.
+  constexpr uint64_t G = 0x9E3779B97F4A7C15ULL;
+  auto mix = [](uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+  };
+  auto fold = [&](uint64_t hh, uint64_t f) { return mix(hh ^ (mix(f) + G + (hh << 6) + (hh >> 2))); };
+  uint64_t hh = mix(seed + G);
+  hh = fold(hh, t);
+  hh = fold(hh, r);
+  hh = fold(hh, i);
+  return hh;
+}
+
+struct RoundOut {
+  std::vector<pp_record> recs;
+};
+
+// One sampling round on the device: restarts [r0, r0+rc), candidates
+// [c0, c1) of each, iteration `iter`, centred on `center` (or injected theta).
+void run_round(pp_handle* h, uint64_t t, int iter, int r0, int rc, const double* center,
+               int64_t c0, int64_t c1, const double* injected, pp_record* out,
+               pp_rollout_stats* per_sample) {
+  if (!h->snap_valid) throw std::invalid_argument("no snapshot uploaded");
+  if (rc < 1 || c1 < c0) throw std::invalid_argument("empty sampling round");
+  const int64_t count = c1 - c0;
+  ppdev::RoundArgs a = h->base;
+  const int block = 128;
+  const int64_t tpr64 = (count + block - 1) / block;
+  if (tpr64 * rc > (int64_t{1} << 30)) throw std::invalid_argument("sampling round too large");
+  a.restart_count = rc;
+  a.cand_begin = c0;
+  a.count = count;
+  a.tiles_per_restart = static_cast<int32_t>(tpr64);
+  a.n_tiles = static_cast<int32_t>(tpr64 * rc);
+
+  ppdev::LaunchShape shape{};
+  const int rcode = h->fp64 ? ppdev::shape_f64(h->kind, h->device, h->field_smem_bytes, &shape)
+                            : ppdev::shape_f32(h->kind, h->device, h->field_smem_bytes, &shape);
+  ck(static_cast<cudaError_t>(rcode), "occupancy query");
+  a.block = block;
+  a.grid = std::max(1, std::min(shape.grid, a.n_tiles));
+  a.field_smem_bytes = h->field_smem_bytes;
+
+  // params block: [prefix u64 x rc][center f64 x P]
+  const size_t pbytes = sizeof(uint64_t) * rc + sizeof(double) * h->P;
+  h->h_params.reserve(pbytes, "pinned params");
+  h->d_params.reserve(pbytes, "device params");
+  uint64_t* hp = static_cast<uint64_t*>(h->h_params.p);
+  for (int r = 0; r < rc; ++r) {
+    hp[r] = key_prefix(h->cfg.master_seed, t, static_cast<uint64_t>(r0 + r),
+                       static_cast<uint64_t>(iter));
+  }
+  double* hc = reinterpret_cast<double*>(hp + rc);
+  if (center != nullptr) {
+    std::memcpy(hc, center, sizeof(double) * h->P);
+  } else {
+    std::fill(hc, hc + h->P, 0.0);
+  }
+  ck(cudaMemcpyAsync(h->d_params.p, h->h_params.p, pbytes, cudaMemcpyHostToDevice, h->stream),
+     "params H2D");
+  h->timing.h2d_bytes += static_cast<int64_t>(pbytes);
+  a.key_prefix = static_cast<const uint64_t*>(h->d_params.p);
+  a.center = reinterpret_cast<const double*>(static_cast<uint64_t*>(h->d_params.p) + rc);
+
+  if (injected != nullptr) {
+    const size_t ib = sizeof(double) * h->P * static_cast<size_t>(count);
+    h->d_injected.reserve(ib, "device theta");
+    ck(cudaMemcpyAsync(h->d_injected.p, injected, ib, cudaMemcpyHostToDevice, h->stream),
+       "theta H2D");
+    h->timing.h2d_bytes += static_cast<int64_t>(ib);
+    a.injected = static_cast<const double*>(h->d_injected.p);
+  }
+
+  h->d_tiles.reserve(sizeof(ppdev::Rec) * a.n_tiles, "tile records");
+  a.tile_recs = static_cast<ppdev::Rec*>(h->d_tiles.p);
+  const size_t rbytes = 32 + sizeof(ppdev::Rec) * rc;
+  if (h->d_result.reserve(rbytes, "result block")) {
+    ck(cudaMemsetAsync(h->d_result.p, 0, rbytes, h->stream), "result block");
+  }
+  h->h_result.reserve(rbytes, "pinned result");
+  a.exec = static_cast<unsigned long long*>(h->d_result.p);
+  a.out = reinterpret_cast<ppdev::Rec*>(static_cast<char*>(h->d_result.p) + 32);
+  a.counters = static_cast<uint32_t*>(h->d_counters.p);
+  if (per_sample != nullptr) {
+    h->d_samples.reserve(sizeof(ppdev::SampleOut) * rc * static_cast<size_t>(count),
+                         "per-sample buffer");
+    a.per_sample = static_cast<ppdev::SampleOut*>(h->d_samples.p);
+  }
+  if (h->kind == ppdev::NetKind::kGeneric) {
+    const size_t elems = static_cast<size_t>(h->P) * a.grid * a.block;
+    h->d_scratch.reserve(elems * (h->fp64 ? sizeof(double) : sizeof(float)), "theta scratch");
+    a.theta_scratch = static_cast<float*>(h->d_scratch.p);
+    a.theta_scratch64 = static_cast<double*>(h->d_scratch.p);
+  }
+
+  ck(cudaEventRecord(h->ev0, h->stream), "event");
+  const int lcode = h->fp64 ? ppdev::launch_round_f64(h->kind, a, h->stream)
+                            : ppdev::launch_round_f32(h->kind, a, h->stream);
+  ck(static_cast<cudaError_t>(lcode), "sampling kernel launch");
+  ck(cudaEventRecord(h->ev1, h->stream), "event");
+  ck(cudaMemcpyAsync(h->h_result.p, h->d_result.p, rbytes, cudaMemcpyDeviceToHost, h->stream),
+     "result D2H");
+  h->timing.d2h_bytes += static_cast<int64_t>(rbytes);
+  if (per_sample != nullptr) {
+    const size_t sb = sizeof(ppdev::SampleOut) * rc * static_cast<size_t>(count);
+    ck(cudaMemcpyAsync(per_sample, h->d_samples.p, sb, cudaMemcpyDeviceToHost, h->stream),
+       "per-sample D2H");
+    h->timing.d2h_bytes += static_cast<int64_t>(sb);
+  }
+  ck(cudaStreamSynchronize(h->stream), "sampling kernel");
+  float ms = 0.f;
+  ck(cudaEventElapsedTime(&ms, h->ev0, h->ev1), "event timing");
+  h->timing.kernel_ms += ms;
+  h->timing.launches += 1;
+  h->timing.samples += count * rc;
+  const unsigned long long* ex = static_cast<const unsigned long long*>(h->h_result.p);
+  h->timing.executed_steps += static_cast<int64_t>(ex[2]);
+  h->timing.checked_states += static_cast<int64_t>(ex[3]);
+  const ppdev::Rec* recs =
+      reinterpret_cast<const ppdev::Rec*>(static_cast<const char*>(h->h_result.p) + 32);
+  for (int r = 0; r < rc; ++r) {
+    out[r].cls = recs[r].cls;
+    out[r].candidate = recs[r].cand;
+    out[r].restart = r0 + r;
+    out[r].iter = iter;
+    out[r].k1 = recs[r].k1;
+    out[r].k2 = recs[r].k2;
+  }
+}
+
+paraplan::PlanningSnapshot to_snapshot(const pp_snapshot& s) {
+  paraplan::PlanningSnapshot snap;
+  snap.ev_state = {s.ev_x, s.ev_y, s.ev_phi, s.ev_v};
+  snap.actuator.delta = s.actuator_delta;
+  snap.prev_action = {s.prev_a0, s.prev_a1};
+  snap.goal = {s.goal_x, s.goal_y, s.goal_phi, s.goal_v};
+  return snap;
+}
+
+// Host FP64 rollout: src/planner.cpp:66-191 expressed through the public
+// primitives (bit-identical under -ffp-contract=off; the reference's own
+// selfcheck::resimulate_rollout relies on the same equivalence).
+void host_rollout(const pp_handle* h, const pp_snapshot& s, const double* theta,
+                  pp_rollout_stats* out, double* traj, int32_t cap, int32_t* traj_len) {
+  using namespace paraplan;
+  const auto& p = h->params;
+  const auto& cfg = h->cfg;
+  const Pose2 anchor{s.ev_x, s.ev_y, s.ev_phi};
+  const Vec2 gp = to_ev_frame(anchor, {s.goal_x, s.goal_y});
+  const GoalSetpoint goal{gp.x, gp.y, s.goal_phi - anchor.phi, s.goal_v};
+  const double gc = std::cos(goal.phi), gs = std::sin(goal.phi);
+  const std::span<const double> th(theta, h->P);
+  const int N = s.n_points;
+  if (N > 0 && s.field_H < cfg.H) {
+    throw std::invalid_argument("obstacle field shorter than the planning horizon");
+  }
+
+  VehicleState z{0.0, 0.0, 0.0, s.ev_v};
+  ActuatorState act{s.actuator_delta};
+  double prev_a0 = s.prev_a0;
+  std::memset(out, 0, sizeof(*out));
+  out->t_goal = -1;
+  int32_t n = 0;
+  auto push = [&](const VehicleState& st) {
+    if (traj != nullptr && n < cap) {
+      traj[4 * n + 0] = st.x;
+      traj[4 * n + 1] = st.y;
+      traj[4 * n + 2] = st.phi;
+      traj[4 * n + 3] = st.v;
+    }
+    ++n;
+  };
+  push(z);
+  const ControlAction first = h->policy->forward(th, build_features(z, goal, prev_a0, h->norm));
+  out->first_a0 = first.a0;
+  out->first_a1 = first.a1;
+  double path = 0.0;
+  for (int k = 0;; ++k) {
+    if (N > 0) {
+      const std::span<const Vec2> row(
+          reinterpret_cast<const Vec2*>(s.field_xy) + static_cast<size_t>(k) * N, N);
+      if (collision({z.x, z.y, z.phi}, row, h->chassis)) {
+        out->collided = 1;
+        break;
+      }
+    }
+    const double gdx = goal.x - z.x, gdy = goal.y - z.y;
+    if (std::abs(gc * gdx + gs * gdy) <= cfg.tol.eps_xi &&
+        std::abs(-gs * gdx + gc * gdy) <= cfg.tol.eps_eta &&
+        std::abs(wrap_angle(goal.phi - z.phi)) <= cfg.tol.eps_phi &&
+        std::abs(goal.v - z.v) <= cfg.tol.eps_v) {
+      out->reached = 1;
+      out->t_goal = k;
+      break;
+    }
+    if (k == cfg.H) break;
+    const ControlAction a =
+        k == 0 ? first : h->policy->forward(th, build_features(z, goal, prev_a0, h->norm));
+    const Controls u = map_controls(a, act, p);
+    const VehicleState nz = step(z, u.delta, u.u_v, p);
+    const double dx = nz.x - z.x, dy = nz.y - z.y;
+    path += std::sqrt(dx * dx + dy * dy);
+    z = nz;
+    act.delta = u.delta;
+    prev_a0 = a.a0;
+    push(z);
+  }
+  out->path_length = path;
+  out->terminal_cost = std::abs(goal.x - z.x) / h->norm.d_xi +
+                       std::abs(goal.y - z.y) / h->norm.d_eta +
+                       std::abs(wrap_angle(goal.phi - z.phi)) / h->norm.d_phi +
+                       std::abs(goal.v - z.v) / h->norm.d_v;
+  out->steps = n - 1;
+  if (traj_len != nullptr) *traj_len = n;
+}
+
+void host_sample(const pp_handle* h, const double* center, uint64_t t, int restart, int iter,
+                 int cand, double* out, int len = -1) {
+  if (len < 0) len = h->P;
+  if (cand == 0) {
+    std::memcpy(out, center, sizeof(double) * len);
+    return;
+  }
+  paraplan::KeyedRng rng(h->cfg.master_seed, t, static_cast<uint64_t>(restart),
+                         static_cast<uint64_t>(iter), static_cast<uint64_t>(cand));
+  const double sigma = std::pow(
+      10.0, h->cfg.sigma_log_low + rng.next_unit() * (h->cfg.sigma_log_high - h->cfg.sigma_log_low));
+  for (int i = 0; i < len; ++i) out[i] = center[i] + sigma * rng.next_normal();
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t pp_abi_version(void) { return PP_ABI_VERSION; }
+
+const char* pp_last_error(void) { return g_error.c_str(); }
+
+int32_t pp_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+pp_status pp_create(const pp_model* m, pp_handle** out) {
+  if (out != nullptr) *out = nullptr;
+  pp_handle* h = nullptr;
+  const pp_status st = guarded([&] {
+    if (m == nullptr || out == nullptr) throw std::invalid_argument("null argument");
+    auto hp = std::make_unique<pp_handle>();
+    hp->model = *m;
+    hp->sizes.assign(m->layer_sizes, m->layer_sizes + std::max(0, m->n_layers));
+    hp->model.layer_sizes = hp->sizes.data();
+    hp->params = params_of(m->vehicle);
+    hp->cfg = config_of(m->config);
+    hp->norm = {m->norm.d_xi, m->norm.d_eta, m->norm.d_phi, m->norm.d_v};
+    paraplan::MlpArchitecture arch;
+    arch.layer_sizes.assign(hp->sizes.begin(), hp->sizes.end());
+    if (static_cast<int>(arch.layer_sizes.size()) > ppdev::kMaxLayers) {
+      throw std::invalid_argument("at most 16 layers are supported");
+    }
+    // Same validation order as the reference constructor (planner.cpp:46-58).
+    hp->policy = std::make_unique<paraplan::MlpPolicy>(arch);
+    hp->params.validate();
+    hp->cfg.validate();
+    hp->chassis = paraplan::ChassisPolytope::rectangle(hp->params);
+    hp->P = hp->policy->param_count();
+    hp->kind = ppdev::classify(hp->sizes.data(), static_cast<int32_t>(hp->sizes.size()));
+    hp->fp64 = hp->cfg.precision == 64;
+    hp->device = hp->cfg.device;
+
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+      cudaGetLastError();
+      throw NoDevice("no CUDA device: the paraplan B200 planner has no CPU fallback");
+    }
+    if (hp->device >= n) throw std::invalid_argument("CUDA device ordinal out of range");
+    cudaDeviceProp prop{};
+    ck(cudaGetDeviceProperties(&prop, hp->device), "device query");
+    if (prop.major != 10) {
+      throw NoDevice(std::string("device ") + prop.name +
+                     " is not sm_100 (B200); kernels are built for sm_100a only");
+    }
+    ck(cudaSetDevice(hp->device), "cudaSetDevice");
+    ck(cudaStreamCreateWithFlags(&hp->stream, cudaStreamNonBlocking), "stream");
+    ck(cudaEventCreate(&hp->ev0), "event");
+    ck(cudaEventCreate(&hp->ev1), "event");
+    hp->d_counters.reserve(64, "counters");
+    ck(cudaMemsetAsync(hp->d_counters.p, 0, 64, hp->stream), "counters");
+    hp->d_result.reserve(4096, "result block");
+    ck(cudaMemsetAsync(hp->d_result.p, 0, 4096, hp->stream), "result block");
+    ck(cudaStreamSynchronize(hp->stream), "init");
+    h = hp.release();
+  });
+  if (st == PP_OK) *out = h;
+  return st;
+}
+
+void pp_destroy(pp_handle* h) {
+  if (h == nullptr) return;
+  cudaSetDevice(h->device);
+  if (h->stream != nullptr) cudaStreamSynchronize(h->stream);
+  for (DevBuf* b : {&h->d_field, &h->d_params, &h->d_result, &h->d_tiles, &h->d_counters,
+                    &h->d_samples, &h->d_scratch, &h->d_injected}) {
+    b->release();
+  }
+  for (HostBuf* b : {&h->h_field, &h->h_params, &h->h_result}) b->release();
+  if (h->ev0 != nullptr) cudaEventDestroy(h->ev0);
+  if (h->ev1 != nullptr) cudaEventDestroy(h->ev1);
+  if (h->stream != nullptr) cudaStreamDestroy(h->stream);
+  delete h;
+}
+
+int32_t pp_param_count(const pp_handle* h) { return h == nullptr ? 0 : h->P; }
+
+void* pp_stream(const pp_handle* h) { return h == nullptr ? nullptr : h->stream; }
+
+pp_status pp_last_timing(const pp_handle* h, pp_timing* out) {
+  if (h == nullptr || out == nullptr) return PP_INVALID_ARGUMENT;
+  *out = h->timing;
+  return PP_OK;
+}
+
+pp_status pp_upload_snapshot(pp_handle* h, const pp_snapshot* snap) {
+  return guarded([&] {
+    if (h == nullptr || snap == nullptr) throw std::invalid_argument("null argument");
+    ck(cudaSetDevice(h->device), "cudaSetDevice");
+    upload_snapshot(h, *snap);
+    ck(cudaStreamSynchronize(h->stream), "snapshot H2D");
+  });
+}
+
+pp_status pp_evaluate(pp_handle* h, const pp_snapshot* snap, uint64_t t, int32_t iter,
+                      int32_t restart_begin, int32_t restart_count, const double* center,
+                      int64_t cand_begin, int64_t cand_end, pp_record* out,
+                      pp_rollout_stats* per_sample) {
+  return guarded([&] {
+    if (h == nullptr || out == nullptr) throw std::invalid_argument("null argument");
+    if (cand_begin < 0 || cand_end > h->cfg.n_candidates || restart_begin < 0 ||
+        restart_begin + restart_count > h->cfg.n_restarts || iter < 0 ||
+        iter >= h->cfg.n_iter_max) {
+      throw std::invalid_argument("sampling round outside the configured budget");
+    }
+    ck(cudaSetDevice(h->device), "cudaSetDevice");
+    h->timing = pp_timing{};
+    if (snap != nullptr) upload_snapshot(h, *snap);
+    if (cand_end <= cand_begin) {
+      for (int r = 0; r < restart_count; ++r) {
+        out[r] = pp_record{-1, -1, restart_begin + r, iter, 0.0, 0.0};
+      }
+      return;
+    }
+    run_round(h, t, iter, restart_begin, restart_count, center, cand_begin, cand_end, nullptr,
+              out, per_sample);
+  });
+}
+
+pp_status pp_eval_theta(pp_handle* h, const pp_snapshot* snap, const double* theta, int64_t n,
+                        pp_rollout_stats* out) {
+  return guarded([&] {
+    if (h == nullptr || theta == nullptr || out == nullptr) {
+      throw std::invalid_argument("null argument");
+    }
+    ck(cudaSetDevice(h->device), "cudaSetDevice");
+    h->timing = pp_timing{};
+    if (snap != nullptr) upload_snapshot(h, *snap);
+    if (n <= 0) return;
+    pp_record rec{};
+    run_round(h, 0, 0, 0, 1, nullptr, 0, n, theta, &rec, out);
+  });
+}
+
+pp_status pp_rollout(const pp_handle* h, const pp_snapshot* snap, const double* theta,
+                     int32_t theta_len, pp_rollout_stats* out, double* traj, int32_t traj_cap,
+                     int32_t* traj_len) {
+  return guarded([&] {
+    if (h == nullptr || snap == nullptr || theta == nullptr || out == nullptr) {
+      throw std::invalid_argument("null argument");
+    }
+    if (theta_len != h->P) throw std::invalid_argument("parameter vector size mismatch");
+    host_rollout(h, *snap, theta, out, traj, traj_cap, traj_len);
+  });
+}
+
+pp_status pp_sample_candidate(const pp_handle* h, const double* center, int32_t len, uint64_t t,
+                              int32_t restart, int32_t iter, int32_t candidate, double* out) {
+  return guarded([&] {
+    if (h == nullptr || center == nullptr || out == nullptr) {
+      throw std::invalid_argument("null argument");
+    }
+    if (len < 0) throw std::invalid_argument("candidate buffer size mismatch");
+    host_sample(h, center, t, restart, iter, candidate, out, len);
+  });
+}
+
+double pp_perturbation_sigma(const pp_handle* h, uint64_t t, int32_t restart, int32_t iter,
+                             int32_t candidate) {
+  paraplan::KeyedRng rng(h->cfg.master_seed, t, static_cast<uint64_t>(restart),
+                         static_cast<uint64_t>(iter), static_cast<uint64_t>(candidate));
+  return std::pow(10.0, h->cfg.sigma_log_low +
+                            rng.next_unit() * (h->cfg.sigma_log_high - h->cfg.sigma_log_low));
+}
+
+int32_t pp_key_better(int32_t cls_a, double k1_a, double k2_a, int32_t cls_b, double k1_b,
+                      double k2_b) {
+  return key_better({cls_a, k1_a, k2_a}, {cls_b, k1_b, k2_b}) ? 1 : 0;
+}
+
+// Ordered merge (src/planner.cpp:310-321): records come from disjoint,
+// increasing index ranges, so a strict-better scan keeps the lowest index.
+pp_status pp_merge_records(const pp_record* recs, int32_t n, pp_record* out) {
+  if (out == nullptr || (n > 0 && recs == nullptr)) return PP_INVALID_ARGUMENT;
+  pp_record m{-1, -1, -1, -1, 0.0, 0.0};
+  for (int32_t i = 0; i < n; ++i) {
+    if (recs[i].candidate < 0) continue;
+    if (m.candidate < 0 ||
+        key_better({recs[i].cls, recs[i].k1, recs[i].k2}, {m.cls, m.k1, m.k2})) {
+      m = recs[i];
+    }
+  }
+  *out = m;
+  return PP_OK;
+}
+
+pp_status pp_plan_step(pp_handle* h, const pp_snapshot* snap, uint64_t t, pp_plan_output* out) {
+  return guarded([&] {
+    if (h == nullptr || snap == nullptr || out == nullptr) {
+      throw std::invalid_argument("null argument");
+    }
+    const int P = h->P;
+    const auto& cfg = h->cfg;
+    if (snap->warm_theta_len != 0 && snap->warm_theta_len != P) {
+      throw std::invalid_argument("warm start vector size mismatch");  // :240-244
+    }
+    ck(cudaSetDevice(h->device), "cudaSetDevice");
+    h->timing = pp_timing{};
+    upload_snapshot(h, *snap);
+
+    std::vector<double> init_center(P, 0.0);
+    if (snap->warm_theta_len == P) init_center.assign(snap->warm_theta, snap->warm_theta + P);
+
+    const int R = cfg.n_restarts, I = cfg.n_iter_max, n = cfg.n_candidates;
+    // Iteration 0 of every restart centres on the warm start: one launch.
+    std::vector<pp_record> first(R);
+    run_round(h, t, 0, 0, R, init_center.data(), 0, n, nullptr, first.data(), nullptr);
+
+    Key best;
+    bool best_valid = false, any_free = false;
+    std::vector<double> best_theta(P, 0.0), center(P, 0.0), theta(P);
+    pp_record win{-1, -1, -1, -1, 0.0, 0.0};
+    int64_t evaluated = 0;
+    bool done = false;
+    for (int r = 0; r < R && !done; ++r) {
+      for (int it = 0; it < I; ++it) {
+        pp_record rec;
+        if (it == 0) {
+          center = init_center;
+          rec = first[r];
+        } else {
+          if (best_valid) center = best_theta;  // :275-276
+          run_round(h, t, it, r, 1, center.data(), 0, n, nullptr, &rec, nullptr);
+        }
+        evaluated += n;
+        any_free = any_free || rec.cls >= 1;
+        const Key k{rec.cls, rec.k1, rec.k2};
+        if (!best_valid || key_better(k, best)) {  // :324-330
+          host_sample(h, center.data(), t, r, it, rec.candidate, theta.data());
+          best = k;
+          best_theta = theta;
+          best_valid = true;
+          win = rec;
+        }
+        if (cfg.early_exit && best_valid && best.cls == 2) {  // :332-334
+          done = true;
+          break;
+        }
+      }
+    }
+
+    // FP64 epilogue (:339-350).
+    out->evaluated = evaluated;
+    if (out->best_theta != nullptr) std::memcpy(out->best_theta, best_theta.data(), sizeof(double) * P);
+    int32_t len = 0;
+    host_rollout(h, *snap, best_theta.data(), &out->predicted, out->trajectory, cfg.H + 1, &len);
+    out->trajectory_len = len;
+    out->success = out->predicted.reached && !out->predicted.collided;
+    if (any_free) {
+      out->action_a0 = out->predicted.first_a0;
+      out->action_a1 = out->predicted.first_a1;
+    } else {
+      out->action_a0 = snap->actuator_delta / h->params.delta_max;
+      out->action_a1 = -1.0;
+    }
+    out->winner = win;
+  });
+}
+
+pp_status pp_measure_fp32_peak(int32_t device, double* tflops, double* sm_mhz) {
+  return guarded([&] {
+    if (tflops == nullptr || sm_mhz == nullptr) throw std::invalid_argument("null argument");
+    if (pp_device_count() <= device) throw NoDevice("no such CUDA device");
+    ck(static_cast<cudaError_t>(ppdev::measure_ffma(device, tflops, sm_mhz)), "ffma probe");
+  });
+}
+
+}  // extern "C"
+
+namespace ppdev {
+NetKind classify(const int32_t* s, int32_t n) {
+  if (n == 3 && s[0] == 5 && s[2] == 2) {
+    if (s[1] == 2) return NetKind::k5_2_2;
+    if (s[1] == 10) return NetKind::k5_10_2;
+  }
+  return NetKind::kGeneric;
+}
+}  // namespace ppdev

@@ -1,0 +1,89 @@
+// device_api.h -- host-visible interface of the sm_100a kernels (no CUDA
+// types; streams are passed as void*). Implemented in rollout_f32.cu /
+// rollout_f64.cu (one instantiation of rollout.cuh each) and peak.cu.
+#pragma once
+
+#include <cstdint>
+
+namespace ppdev {
+
+constexpr int kMaxLayers = 16;
+
+// Per-sample output of the parity/debug path (same layout as pp_rollout_stats).
+struct SampleOut {
+  int32_t reached, t_goal, collided, steps;
+  double path_length, terminal_cost, first_a0, first_a1;
+};
+
+// Winner of a tile / of a restart segment. cls = -1 marks "no candidate".
+struct Rec {
+  int32_t cls;
+  int32_t cand;  // index within the restart
+  double k1, k2;
+};
+
+// Everything one sampling round needs. Scalars are FP64 here; the FP32
+// kernel rounds them once at kernel entry.
+struct RoundArgs {
+  // goal in the anchor frame (planner.cpp:70-81)
+  double gx, gy, gphi, gv, gcos, gsin;
+  // initial carry (planner.cpp:123-125)
+  double v0, act0, pa0;
+  // NormConstants
+  double d_xi, d_eta, d_phi, d_v;
+  // GoalTolerance
+  double eps_xi, eps_eta, eps_phi, eps_v;
+  // VehicleParams-derived
+  double delta_max, window, l_r, wheelbase, T_s, u_v_min, u_v_max;
+  double fe, re, hw, r2;  // chassis half-planes and squared bounding radius
+  // sigma = 10^(lo + u * span)
+  double sig_lo, sig_span;
+  int32_t H;
+  int32_t n_points;  // 0 disables the collision test (planner.cpp:74)
+  int32_t n_params;
+  int32_t n_layers;
+  int32_t sizes[kMaxLayers];
+  // sampling round: restarts [0, restart_count) of this call, candidates
+  // [cand_begin, cand_begin + count) of each restart
+  int32_t restart_count;
+  int64_t cand_begin;
+  int64_t count;
+  const uint64_t* key_prefix;  // device [restart_count]: fold^4(seed, t, r, iter)
+  const double* center;        // device [n_params]
+  const double* injected;      // device [count * n_params] or null (RNG off)
+  const void* field;           // device Real2 [(H+1) * n_points], row-major in h
+  // scratch / outputs (device)
+  Rec* tile_recs;              // [n_tiles]
+  Rec* out;                    // [restart_count]
+  uint32_t* counters;          // [2]: tile ticket, done ticket (self-resetting)
+  unsigned long long* exec;    // [4]: accumulators (steps, states), published totals
+  SampleOut* per_sample;       // [restart_count * count] or null
+  float* theta_scratch;        // generic-arch path: [n_params * grid_threads]
+  double* theta_scratch64;
+  int32_t grid;                // blocks launched (persistent)
+  int32_t block;               // threads per block
+  int32_t tiles_per_restart;
+  int32_t n_tiles;
+  int32_t field_smem_bytes;    // 0 = read the field from global/L2
+};
+
+// Architecture dispatch of the specialised kernels.
+enum class NetKind : int { kGeneric = 0, k5_2_2 = 1, k5_10_2 = 2 };
+NetKind classify(const int32_t* sizes, int32_t n_layers);
+
+// Grid sizing: persistent blocks = min(n_tiles, SMs x resident blocks/SM).
+struct LaunchShape {
+  int32_t grid, block, smem_limit;
+};
+// Returns 0 or a cudaError_t.
+int shape_f32(NetKind k, int device, int smem_bytes, LaunchShape* out);
+int shape_f64(NetKind k, int device, int smem_bytes, LaunchShape* out);
+
+// Enqueue one sampling round on `stream`. Returns 0 or a cudaError_t.
+int launch_round_f32(NetKind k, const RoundArgs& a, void* stream);
+int launch_round_f64(NetKind k, const RoundArgs& a, void* stream);
+
+// FFMA throughput probe (the FP32 roofline denominator).
+int measure_ffma(int device, double* tflops, double* sm_mhz);
+
+}  // namespace ppdev

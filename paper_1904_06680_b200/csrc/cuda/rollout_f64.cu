@@ -1,0 +1,28 @@
+// rollout_f64.cu -- double instantiation of the fused sampler (rollout.cuh).
+#include "rollout.cuh"
+
+namespace ppdev {
+
+int shape_f64(NetKind k, int device, int smem_bytes, LaunchShape* out) {
+  switch (k) {
+    case NetKind::k5_2_2:
+      return shape_impl<double, NetReg<double, 2>>(device, smem_bytes, out);
+    case NetKind::k5_10_2:
+      return shape_impl<double, NetReg<double, 10>>(device, smem_bytes, out);
+    default:
+      return shape_impl<double, NetGlobal<double>>(device, smem_bytes, out);
+  }
+}
+
+int launch_round_f64(NetKind k, const RoundArgs& a, void* stream) {
+  switch (k) {
+    case NetKind::k5_2_2:
+      return launch_impl<double, NetReg<double, 2>>(a, stream);
+    case NetKind::k5_10_2:
+      return launch_impl<double, NetReg<double, 10>>(a, stream);
+    default:
+      return launch_impl<double, NetGlobal<double>>(a, stream);
+  }
+}
+
+}  // namespace ppdev
