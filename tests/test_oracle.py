@@ -1,0 +1,126 @@
+"""Pin the CPU checkers before trusting them.
+
+The plain-C restatement (oracle/paraplan_oracle.c) must reproduce, bit for
+bit, (a) the golden vectors generated from the reference itself
+(tests/golden/reference_vectors.json) and (b) the reference compiled from its
+own sources (oracle/_ref/libparaplan_ref.so) on randomized inputs.
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import pytest
+
+from conftest import golden_snapshot, golden_stats, unhex
+from oracle.oracle import Port, Ref
+from paper_1904_06680_b200 import abi
+
+
+def test_rng_streams_match_golden(gold):
+    for g in gold["rng"]:
+        k = tuple(g["key"])
+        assert [format(int(x), "016x") for x in Port.rng_stream(k, 0, 8)] == g["u64"]
+        assert np.array_equal(Port.rng_stream(k, 1, 8), unhex(g["unit"]))
+        assert np.array_equal(Port.rng_stream(k, 2, 9), unhex(g["normal"]))
+
+
+def test_rng_known_answer():
+    # KeyedRng(1, 2, 3, 4, 5): first three u64 draws (SURVEY.md Appendix C values)
+    got = {format(int(x), "016x") for x in Port.rng_stream((1, 2, 3, 4, 5), 0, 3)}
+    assert got == {"f210f3dff76f35a3", "19c67b98c2dd443f", "93cef386c5d90e84"}
+
+
+def test_rng_unit_range_and_normal_moments():
+    # rng_test.cpp:45-71
+    u = Port.rng_stream((1, 2, 3, 4, 5), 1, 10000)
+    assert (u >= 0).all() and (u < 1).all()
+    x = Port.rng_stream((11, 0, 0, 0, 0), 2, 200000)
+    assert abs(x.mean()) < 0.01 and abs(x.var() - 1.0) < 0.02
+
+
+def test_sample_candidate_matches_golden(gold):
+    for g in gold["sample_candidate"]:
+        m = abi.Model(layer_sizes=g["sizes"], master_seed=g["seed"])
+        th = Port(m).sample_candidate(unhex(g["center"]), g["t"], g["restart"], g["iter"],
+                                      g["cand"])
+        assert np.array_equal(th, unhex(g["theta"]))
+        if g["cand"] == 0:
+            assert np.array_equal(th, unhex(g["center"]))
+
+
+@pytest.mark.parametrize("idx", range(4))
+def test_round_stats_match_golden(gold, idx):
+    g = gold["rounds"][idx]
+    snap, H = golden_snapshot(gold, g["snapshot"])
+    m = abi.Model(H=H, n_restarts=1, n_candidates=g["n"], master_seed=g["seed"])
+    got = Port(m).eval_candidates(snap, g["t"], 0, 0, np.zeros(m.param_count()), 0, g["n"])
+    want = golden_stats(g["stats"])
+    assert got.tobytes() == want.tobytes()
+
+
+@pytest.mark.parametrize("idx", range(6))
+def test_plan_step_matches_golden(gold, idx):
+    g = gold["plans"][idx]
+    snap, H = golden_snapshot(gold, g["snapshot"])
+    m = abi.Model(H=H, **g["config"])
+    o, theta, traj = Port(m).plan_step(snap, g["t"])
+    assert np.array_equal(theta, unhex(g["best_theta"]))
+    assert np.array_equal(traj.ravel(), unhex(g["trajectory"]))
+    assert np.array_equal([o.action_a0, o.action_a1], unhex(g["action"]))
+    assert bool(o.success) == g["success"]
+    assert o.evaluated == g["evaluated"]
+
+
+def _random_snapshot(rng, H, n_params):
+    # the reference's selfcheck generator shape (selfcheck.cpp:107-135)
+    ev = (rng.uniform(-20, 20), rng.uniform(-20, 20), 2 * rng.uniform(-math.pi, math.pi),
+          rng.uniform(-8, 12))
+    pts = np.array([[ev[0] + rng.uniform(-20, 20), ev[1] + rng.uniform(-20, 20),
+                     rng.uniform(-math.pi, math.pi), abs(rng.uniform(-8, 12))]
+                    for _ in range(rng.integers(0, 11))]).reshape(-1, 4)
+    c, s = math.cos(ev[2]), math.sin(ev[2])
+    local = pts.copy()
+    if len(pts):
+        dx, dy = pts[:, 0] - ev[0], pts[:, 1] - ev[1]
+        local[:, 0] = c * dx + s * dy
+        local[:, 1] = -s * dx + c * dy
+        local[:, 2] = pts[:, 2] - ev[2]
+    warm = rng.uniform(-1, 1, n_params) if rng.random() > 0.5 else None
+    return abi.Snapshot(ev=ev, actuator_delta=0.6 * rng.uniform(-1, 1),
+                        prev_action=(0.9 * rng.uniform(-1, 1), 0.9 * rng.uniform(-1, 1)),
+                        goal=(ev[0] + rng.uniform(-20, 20), ev[1] + rng.uniform(-20, 20),
+                              rng.uniform(-math.pi, math.pi), rng.uniform(-8, 12)),
+                        field=abi.extrapolate(local, H), warm_theta=warm)
+
+
+@pytest.mark.parametrize("sizes", [[5, 2, 2], [5, 10, 2], [5, 4, 3, 2]])
+def test_port_equals_reference_on_random_snapshots(sizes):
+    rng = np.random.default_rng(4242)
+    for trial in range(6):
+        m = abi.Model(layer_sizes=sizes, H=40, n_restarts=2, n_iter_max=1 + trial % 2,
+                      n_candidates=48, master_seed=77 + trial)
+        snap = _random_snapshot(rng, m.H, m.param_count())
+        o1, th1, tr1 = Ref(m).plan_step(snap, trial)
+        o2, th2, tr2 = Port(m).plan_step(snap, trial)
+        assert np.array_equal(th1, th2) and np.array_equal(tr1, tr2)
+        assert (o1.action_a0, o1.action_a1, o1.evaluated) == (o2.action_a0, o2.action_a1,
+                                                              o2.evaluated)
+        st1 = Ref(m).eval_candidates(snap, trial, 0, 1, np.zeros(m.param_count()), 0, 48)
+        st2 = Port(m).eval_candidates(snap, trial, 0, 1, np.zeros(m.param_count()), 0, 48)
+        assert st1.tobytes() == st2.tobytes()
+
+
+def test_port_threads_are_bit_identical():
+    # planner_test.cpp:209-241 on the restatement's OpenMP path
+    snap = Ref.builtin_snapshot("exp3_explicit", 0, 30)
+    m = abi.Model(H=30, n_restarts=3, n_candidates=96, master_seed=5)
+    outs = [Port(m).plan_step(snap, 7, threads=t) for t in (1, 2, 8)]
+    for o, th, tr in outs[1:]:
+        assert np.array_equal(th, outs[0][1]) and np.array_equal(tr, outs[0][2])
+
+
+def test_reference_selfchecks_pass():
+    failed, text = Ref.selfchecks()
+    assert failed == 0, text
+    assert text.count(":PASS:") == 7
