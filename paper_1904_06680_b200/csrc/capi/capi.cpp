@@ -169,7 +169,8 @@ struct pp_handle {
 
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-  DevBuf d_field, d_params, d_result, d_tiles, d_counters, d_samples, d_scratch, d_injected;
+  DevBuf d_field, d_params, d_result, d_tiles, d_counters, d_samples, d_scratch, d_injected,
+      d_theta;
   HostBuf h_field, h_params, h_result;
 
   // resident snapshot
@@ -181,6 +182,44 @@ struct pp_handle {
 };
 
 namespace {
+
+// Round constants in the compute precision (rounded once from FP64).
+template <typename Real>
+void fill_consts(const ppdev::RoundArgs& a, ppdev::ConstsT<Real>* k) {
+  k->gx = Real(a.gx);
+  k->gy = Real(a.gy);
+  k->gphi = Real(a.gphi);
+  k->gv = Real(a.gv);
+  k->gcos = Real(a.gcos);
+  k->gsin = Real(a.gsin);
+  k->v0 = Real(a.v0);
+  k->act0 = Real(a.act0);
+  k->pa0 = Real(a.pa0);
+  k->inv_xi = Real(1.0 / a.d_xi);
+  k->inv_eta = Real(1.0 / a.d_eta);
+  k->inv_phi = Real(1.0 / a.d_phi);
+  k->inv_v = Real(1.0 / a.d_v);
+  k->d_xi = a.d_xi;
+  k->d_eta = a.d_eta;
+  k->d_phi = a.d_phi;
+  k->d_v = a.d_v;
+  k->eps_xi = Real(a.eps_xi);
+  k->eps_eta = Real(a.eps_eta);
+  k->eps_phi = Real(a.eps_phi);
+  k->eps_v = Real(a.eps_v);
+  k->dmax = Real(a.delta_max);
+  k->window = Real(a.window);
+  k->l_r = Real(a.l_r);
+  k->wb = Real(a.wheelbase);
+  k->Ts = Real(a.T_s);
+  k->umin = Real(a.u_v_min);
+  k->umax = Real(a.u_v_max);
+  k->fe = Real(a.fe);
+  k->re = Real(a.re);
+  k->hw = Real(a.hw);
+  k->r2 = Real(a.r2);
+  k->cull = Real(std::sqrt(a.r2) + 1e-3);
+}
 
 // Goal transform and constants of a snapshot (src/planner.cpp:70-81).
 void upload_snapshot(pp_handle* h, const pp_snapshot& s) {
@@ -227,32 +266,59 @@ void upload_snapshot(pp_handle* h, const pp_snapshot& s) {
   a.r2 = radius * radius;
   a.sig_lo = cfg.sigma_log_low;
   a.sig_span = cfg.sigma_log_high - cfg.sigma_log_low;
+  fill_consts(a, &a.kf);
+  fill_consts(a, &a.kd);
   a.H = cfg.H;
   a.n_params = h->P;
   a.n_layers = static_cast<int32_t>(h->sizes.size());
   for (size_t i = 0; i < h->sizes.size(); ++i) a.sizes[i] = h->sizes[i];
 
-  // Only rows 0..H are ever read; ship those, in the compute precision.
+  // Only rows 0..H are ever read; ship those, in the compute precision, each
+  // row sorted by x so the kernel can window its collision scan (the verdict
+  // is an OR over the row's points, independent of their order).
   const int N = s.n_points;
   a.n_points = N;
   const size_t count = static_cast<size_t>(cfg.H + 1) * static_cast<size_t>(N);
   const size_t elem = h->fp64 ? sizeof(double) : sizeof(float);
-  const size_t bytes = 2 * count * elem;
+  const size_t pts_off = (count * elem + 15) & ~size_t(15);
+  const size_t bytes = pts_off + 2 * count * elem;
   if (count > 0) {
     h->h_field.reserve(bytes, "pinned field");
     h->d_field.reserve(bytes, "device field");
-    if (h->fp64) {
-      std::memcpy(h->h_field.p, s.field_xy, bytes);
-    } else {
-      float* dst = static_cast<float*>(h->h_field.p);
-      for (size_t i = 0; i < 2 * count; ++i) dst[i] = static_cast<float>(s.field_xy[i]);
+    unsigned char* base = static_cast<unsigned char*>(h->h_field.p);
+    std::vector<int32_t> order(N);
+    for (int row = 0; row <= cfg.H; ++row) {
+      const double* src = s.field_xy + 2 * static_cast<size_t>(row) * N;
+      for (int j = 0; j < N; ++j) order[j] = j;
+      std::stable_sort(order.begin(), order.end(),
+                       [&](int32_t p, int32_t q) { return src[2 * p] < src[2 * q]; });
+      const size_t o = static_cast<size_t>(row) * N;
+      if (h->fp64) {
+        double* xs = reinterpret_cast<double*>(base) + o;
+        double* pts = reinterpret_cast<double*>(base + pts_off) + 2 * o;
+        for (int j = 0; j < N; ++j) {
+          xs[j] = src[2 * order[j]];
+          pts[2 * j] = src[2 * order[j]];
+          pts[2 * j + 1] = src[2 * order[j] + 1];
+        }
+      } else {
+        float* xs = reinterpret_cast<float*>(base) + o;
+        float* pts = reinterpret_cast<float*>(base + pts_off) + 2 * o;
+        for (int j = 0; j < N; ++j) {
+          xs[j] = static_cast<float>(src[2 * order[j]]);
+          pts[2 * j] = static_cast<float>(src[2 * order[j]]);
+          pts[2 * j + 1] = static_cast<float>(src[2 * order[j] + 1]);
+        }
+      }
     }
     ck(cudaMemcpyAsync(h->d_field.p, h->h_field.p, bytes, cudaMemcpyHostToDevice, h->stream),
        "field H2D");
     h->timing.h2d_bytes += static_cast<int64_t>(bytes);
   }
   a.field = h->d_field.p;
-  h->field_smem_bytes = bytes <= 32 * 1024 ? static_cast<int>(bytes) : 0;
+  // stage the field in shared memory when it fits comfortably next to the
+  // theta queues; larger fields are read through L1/L2
+  h->field_smem_bytes = (count > 0 && bytes <= 40 * 1024) ? static_cast<int>(bytes) : 0;
   h->snap_valid = true;
 }
 
@@ -275,35 +341,34 @@ uint64_t key_prefix(uint64_t seed, uint64_t t, uint64_t r, uint64_t i) {
   return hh;
 }
 
-struct RoundOut {
-  std::vector<pp_record> recs;
-};
+constexpr int ppdev_warps() { return 4; }  // warps per CTA (rollout.cuh kBlock / 32)
 
 // One sampling round on the device: restarts [r0, r0+rc), candidates
 // [c0, c1) of each, iteration `iter`, centred on `center` (or injected theta).
-void run_round(pp_handle* h, uint64_t t, int iter, int r0, int rc, const double* center,
-               int64_t c0, int64_t c1, const double* injected, pp_record* out,
-               pp_rollout_stats* per_sample) {
-  if (!h->snap_valid) throw std::invalid_argument("no snapshot uploaded");
-  if (rc < 1 || c1 < c0) throw std::invalid_argument("empty sampling round");
+void run_round_launch(pp_handle* h, uint64_t t, int iter, int r0, int rc, const double* center,
+                      int64_t c0, int64_t c1, const double* injected, pp_record* out,
+                      pp_rollout_stats* per_sample) {
   const int64_t count = c1 - c0;
   ppdev::RoundArgs a = h->base;
-  const int block = 128;
-  const int64_t tpr64 = (count + block - 1) / block;
+  ppdev::LaunchShape shape{};
+  const int rcode = h->fp64 ? ppdev::shape_f64(h->kind, h->device, h->field_smem_bytes, &shape)
+                            : ppdev::shape_f32(h->kind, h->device, h->field_smem_bytes, &shape);
+  ck(static_cast<cudaError_t>(rcode), "occupancy query");
+  // refill: 32-candidate batches; lockstep: one tile of `block` candidates
+  const int unit = shape.refill ? 32 : shape.block;
+  const int64_t tpr64 = (count + unit - 1) / unit;
   if (tpr64 * rc > (int64_t{1} << 30)) throw std::invalid_argument("sampling round too large");
   a.restart_count = rc;
   a.cand_begin = c0;
   a.count = count;
   a.tiles_per_restart = static_cast<int32_t>(tpr64);
   a.n_tiles = static_cast<int32_t>(tpr64 * rc);
-
-  ppdev::LaunchShape shape{};
-  const int rcode = h->fp64 ? ppdev::shape_f64(h->kind, h->device, h->field_smem_bytes, &shape)
-                            : ppdev::shape_f32(h->kind, h->device, h->field_smem_bytes, &shape);
-  ck(static_cast<cudaError_t>(rcode), "occupancy query");
-  a.block = block;
-  a.grid = std::max(1, std::min(shape.grid, a.n_tiles));
+  a.block = shape.block;
+  a.grid = std::max(1, std::min(shape.grid, shape.refill ? (a.n_tiles + ppdev_warps() - 1) /
+                                                               ppdev_warps()
+                                                         : a.n_tiles));
   a.field_smem_bytes = h->field_smem_bytes;
+  a.queue_bytes = shape.queue_bytes;
 
   // params block: [prefix u64 x rc][center f64 x P]
   const size_t pbytes = sizeof(uint64_t) * rc + sizeof(double) * h->P;
@@ -335,7 +400,8 @@ void run_round(pp_handle* h, uint64_t t, int iter, int r0, int rc, const double*
     a.injected = static_cast<const double*>(h->d_injected.p);
   }
 
-  h->d_tiles.reserve(sizeof(ppdev::Rec) * a.n_tiles, "tile records");
+  const size_t n_recs = shape.refill ? static_cast<size_t>(rc) * a.grid : a.n_tiles;
+  h->d_tiles.reserve(sizeof(ppdev::Rec) * n_recs, "tile records");
   a.tile_recs = static_cast<ppdev::Rec*>(h->d_tiles.p);
   const size_t rbytes = 32 + sizeof(ppdev::Rec) * rc;
   if (h->d_result.reserve(rbytes, "result block")) {
@@ -349,6 +415,13 @@ void run_round(pp_handle* h, uint64_t t, int iter, int r0, int rc, const double*
     h->d_samples.reserve(sizeof(ppdev::SampleOut) * rc * static_cast<size_t>(count),
                          "per-sample buffer");
     a.per_sample = static_cast<ppdev::SampleOut*>(h->d_samples.p);
+  }
+  if (shape.refill) {
+    const size_t total = static_cast<size_t>(count) * rc;
+    const size_t esz = h->fp64 ? sizeof(double) : sizeof(float);
+    h->d_theta.reserve(total * shape.theta_elem * esz, "theta buffer");
+    a.theta_buf = h->d_theta.p;
+    a.first_buf = static_cast<char*>(h->d_theta.p) + total * (shape.theta_elem - 2) * esz;
   }
   if (h->kind == ppdev::NetKind::kGeneric) {
     const size_t elems = static_cast<size_t>(h->P) * a.grid * a.block;
@@ -375,7 +448,7 @@ void run_round(pp_handle* h, uint64_t t, int iter, int r0, int rc, const double*
   float ms = 0.f;
   ck(cudaEventElapsedTime(&ms, h->ev0, h->ev1), "event timing");
   h->timing.kernel_ms += ms;
-  h->timing.launches += 1;
+  h->timing.launches += shape.refill ? 2 : 1;
   h->timing.samples += count * rc;
   const unsigned long long* ex = static_cast<const unsigned long long*>(h->h_result.p);
   h->timing.executed_steps += static_cast<int64_t>(ex[2]);
@@ -389,6 +462,19 @@ void run_round(pp_handle* h, uint64_t t, int iter, int r0, int rc, const double*
     out[r].iter = iter;
     out[r].k1 = recs[r].k1;
     out[r].k2 = recs[r].k2;
+  }
+}
+
+void run_round(pp_handle* h, uint64_t t, int iter, int r0, int rc, const double* center,
+               int64_t c0, int64_t c1, const double* injected, pp_record* out,
+               pp_rollout_stats* per_sample) {
+  if (!h->snap_valid) throw std::invalid_argument("no snapshot uploaded");
+  if (rc < 1 || c1 < c0) throw std::invalid_argument("empty sampling round");
+  // the refill kernel keeps per-restart tables in shared memory: chunk
+  for (int done = 0; done < rc; done += ppdev::kMaxRestartsPerLaunch) {
+    const int n = std::min(ppdev::kMaxRestartsPerLaunch, rc - done);
+    run_round_launch(h, t, iter, r0 + done, n, center, c0, c1, injected, out + done,
+                     per_sample == nullptr ? nullptr : per_sample + done * (c1 - c0));
   }
 }
 
@@ -568,7 +654,7 @@ void pp_destroy(pp_handle* h) {
   cudaSetDevice(h->device);
   if (h->stream != nullptr) cudaStreamSynchronize(h->stream);
   for (DevBuf* b : {&h->d_field, &h->d_params, &h->d_result, &h->d_tiles, &h->d_counters,
-                    &h->d_samples, &h->d_scratch, &h->d_injected}) {
+                    &h->d_samples, &h->d_scratch, &h->d_injected, &h->d_theta}) {
     b->release();
   }
   for (HostBuf* b : {&h->h_field, &h->h_params, &h->h_result}) b->release();

@@ -8,6 +8,7 @@
 namespace ppdev {
 
 constexpr int kMaxLayers = 16;
+constexpr int kMaxRestartsPerLaunch = 64;  // per-warp restart tables of the refill kernel
 
 // Per-sample output of the parity/debug path (same layout as pp_rollout_stats).
 struct SampleOut {
@@ -20,6 +21,21 @@ struct Rec {
   int32_t cls;
   int32_t cand;  // index within the restart
   double k1, k2;
+};
+
+// Round constants in the compute precision, filled once per snapshot on the
+// host and read by the kernels straight from the parameter (constant) bank,
+// so they cost no registers.
+template <typename Real>
+struct ConstsT {
+  Real gx, gy, gphi, gv, gcos, gsin;  // goal in the anchor frame (planner.cpp:70-81)
+  Real v0, act0, pa0;                 // initial carry (planner.cpp:123-125)
+  Real inv_xi, inv_eta, inv_phi, inv_v;
+  double d_xi, d_eta, d_phi, d_v;     // NormConstants (FP64 path divides)
+  Real eps_xi, eps_eta, eps_phi, eps_v;
+  Real dmax, window, l_r, wb, Ts, umin, umax;
+  Real fe, re, hw, r2;  // chassis half-planes, squared bounding radius
+  Real cull;            // collision x-window half width: bounding radius + 1e-3
 };
 
 // Everything one sampling round needs. Scalars are FP64 here; the FP32
@@ -38,6 +54,8 @@ struct RoundArgs {
   double fe, re, hw, r2;  // chassis half-planes and squared bounding radius
   // sigma = 10^(lo + u * span)
   double sig_lo, sig_span;
+  ConstsT<float> kf;
+  ConstsT<double> kd;
   int32_t H;
   int32_t n_points;  // 0 disables the collision test (planner.cpp:74)
   int32_t n_params;
@@ -51,9 +69,9 @@ struct RoundArgs {
   const uint64_t* key_prefix;  // device [restart_count]: fold^4(seed, t, r, iter)
   const double* center;        // device [n_params]
   const double* injected;      // device [count * n_params] or null (RNG off)
-  const void* field;           // device Real2 [(H+1) * n_points], row-major in h
+  const void* field;           // device [xs Real (H+1)N][pad16][pts Real2 (H+1)N], rows sorted by x
   // scratch / outputs (device)
-  Rec* tile_recs;              // [n_tiles]
+  Rec* tile_recs;              // restart-major: [r][tile] (lockstep) or [r][CTA] (refill)
   Rec* out;                    // [restart_count]
   uint32_t* counters;          // [2]: tile ticket, done ticket (self-resetting)
   unsigned long long* exec;    // [4]: accumulators (steps, states), published totals
@@ -65,6 +83,9 @@ struct RoundArgs {
   int32_t tiles_per_restart;
   int32_t n_tiles;
   int32_t field_smem_bytes;    // 0 = read the field from global/L2
+  int32_t queue_bytes;         // unused (0)
+  void* theta_buf;             // refill schedule: [P][total] theta in Real
+  void* first_buf;             // refill schedule: [2][total] first action in Real
 };
 
 // Architecture dispatch of the specialised kernels.
@@ -74,10 +95,14 @@ NetKind classify(const int32_t* sizes, int32_t n_layers);
 // Grid sizing: persistent blocks = min(n_tiles, SMs x resident blocks/SM).
 struct LaunchShape {
   int32_t grid, block, smem_limit;
+  int32_t refill;       // 1: refill_kernel (32-candidate batches), 0: lockstep tiles
+  int32_t queue_bytes;  // unused (0)
+  int32_t theta_elem;   // refill: Real elements per candidate in theta_buf + first_buf
 };
+// field_bytes = shared-memory image of the field (0 = read from L2).
 // Returns 0 or a cudaError_t.
-int shape_f32(NetKind k, int device, int smem_bytes, LaunchShape* out);
-int shape_f64(NetKind k, int device, int smem_bytes, LaunchShape* out);
+int shape_f32(NetKind k, int device, int field_bytes, LaunchShape* out);
+int shape_f64(NetKind k, int device, int field_bytes, LaunchShape* out);
 
 // Enqueue one sampling round on `stream`. Returns 0 or a cudaError_t.
 int launch_round_f32(NetKind k, const RoundArgs& a, void* stream);

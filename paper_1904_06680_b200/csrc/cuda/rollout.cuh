@@ -1,28 +1,45 @@
-// rollout.cuh -- the fused per-control-step sampler kernel (sm_100a).
+// rollout.cuh -- the fused per-control-step sampler kernels (sm_100a).
 //
-// One thread per candidate. Per candidate it
+// One lane per candidate. Per candidate a lane
 //   1. derives the keyed SplitMix64 stream in closed form and draws
 //      theta = center + sigma * N(0,1) (src/rng.cpp:26-58,
-//      src/planner.cpp:207-226) into registers,
+//      src/planner.cpp:207-226), in FP64, rounded once to Real,
 //   2. rolls the kinematic bicycle over the horizon with the reference's
-//      exact check order (src/planner.cpp:66-191): collision vs the obstacle
-//      row h (field staged once per CTA in shared memory, read as a warp
-//      broadcast), inclusive goal box in the goal frame, horizon stop, tanh
-//      MLP -> map_controls -> explicit Euler,
-//   3. scores the rollout (src/planner.cpp:27-44) and reduces to the
+//      exact check order (src/planner.cpp:66-191): collision vs obstacle row h,
+//      inclusive goal box in the goal frame, horizon stop, tanh MLP ->
+//      map_controls -> explicit Euler,
+//   3. scores the rollout (src/planner.cpp:27-44); lanes reduce to the
 //      lexicographically best candidate, ties to the lowest index.
-// CTAs are persistent and pull 1-restart tiles from an atomic ticket; the last
-// CTA to finish reduces the tile winners per restart (the ordered merge of
-// src/planner.cpp:310-321) and resets the tickets, so a round is ONE launch.
 //
-// Real = float is the throughput path (FMA contraction on); Real = double is
-// the parity path (compiled with --fmad=false so every add/mul rounds like
-// the reference's -ffp-contract=off build).
+// Obstacle rows arrive sorted by x (host, capi.cpp) and are staged once per
+// CTA in shared memory. A lane only tests the points of its row whose x lies
+// within (r + margin) of its own x, found by binary search: every skipped
+// point satisfies |dx| > r, so the reference's bounding-circle prefilter
+// (src/geometry.cpp:71, dx^2 + dy^2 >= r^2 -> skip) would have skipped it
+// too and the collision verdict is unchanged.
+//
+// Two schedules:
+//   generate_kernel + refill_kernel (theta in registers, [5,2,2] /
+//     [5,10,2]): the generator draws theta and the first action of every
+//     candidate at full SIMT width into an L2-sized buffer; in the rollout
+//     kernel persistent warps claim restart-aligned 32-candidate batches and
+//     a lane whose rollout ends loads the next candidate at once, so lanes
+//     never idle behind the longest rollout of their warp. Lane bests flush
+//     into per-warp, per-restart shared tables, CTAs write per-restart
+//     records, the last CTA reduces them.
+//   lockstep_kernel (any architecture, theta in a global column per lane):
+//     one candidate per lane per tile, 1-restart tiles, last-CTA reduction.
+//
+// Real = float: throughput path (FMA contraction on). Real = double: parity
+// path (rollout_f64.cu is compiled with --fmad=false so each add/mul rounds
+// like the reference's -ffp-contract=off build).
 #pragma once
 
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
+#include <cstring>
 
 #include "device_api.h"
 
@@ -31,6 +48,9 @@ namespace ppdev {
 constexpr uint64_t kGamma = 0x9E3779B97F4A7C15ull;
 constexpr double kPi = 3.141592653589793;
 constexpr double kTwoPi = 6.283185307179586;
+constexpr unsigned kFull = 0xffffffffu;
+constexpr int kBlock = 128;
+constexpr int kWarps = kBlock / 32;
 
 // src/rng.cpp:11-18
 __device__ __forceinline__ uint64_t mix64(uint64_t z) {
@@ -77,15 +97,15 @@ struct M<float> {
   static __device__ __forceinline__ void sc(float x, float* s, float* c) { sincosf(x, s, c); }
   static __device__ __forceinline__ float sq(float x) { return sqrtf(x); }
   static __device__ __forceinline__ float ab(float x) { return fabsf(x); }
-  // wrap_angle (src/geometry.cpp:9-13): remainder by 2*pi (Cody-Waite in two
-  // parts), lower boundary folded onto +pi.
+  // wrap_angle (src/geometry.cpp:9-13): remainder by 2*pi (two-part
+  // Cody-Waite), lower boundary folded onto +pi.
   static __device__ __forceinline__ float wrap(float a) {
     const float n = rintf(a * 0.15915494309189535f);
     float r = fmaf(-n, 6.28318548202514648f, a);
     r = fmaf(-n, -1.7484555314695172e-07f, r);
     return r <= -3.14159274101257324f ? r + 6.28318548202514648f : r;
   }
-  static __device__ __forceinline__ float ndiv(float a, double d, float inv) { return a * inv; }
+  static __device__ __forceinline__ float ndiv(float a, double, float inv) { return a * inv; }
 };
 
 template <>
@@ -99,6 +119,7 @@ struct M<double> {
     const double r = remainder(a, kTwoPi);  // exact, identical to glibc
     return r <= -kPi ? r + kTwoPi : r;
   }
+  // true division, as the reference (src/planner.cpp:117-120, 186-189)
   static __device__ __forceinline__ double ndiv(double a, double d, double) { return a / d; }
 };
 
@@ -107,68 +128,66 @@ __device__ __forceinline__ Real clampr(Real v, Real lo, Real hi) {
   return v < lo ? lo : (hi < v ? hi : v);  // std::clamp
 }
 
-// Kernel-entry copy of the round constants in the compute precision.
+// Round constants live in the kernel parameter bank (RoundArgs::kf / kd).
 template <typename Real>
-struct Consts {
-  Real gx, gy, gphi, gv, gcos, gsin;
-  Real v0, act0, pa0;
-  Real inv_xi, inv_eta, inv_phi, inv_v;
-  double d_xi, d_eta, d_phi, d_v;  // FP64 path divides (src/planner.cpp:117-120)
-  Real eps_xi, eps_eta, eps_phi, eps_v;
-  Real dmax, window, l_r, wb, Ts, umin, umax;
-  Real fe, re, hw, r2;
-  __device__ __forceinline__ void load(const RoundArgs& a) {
-    gx = Real(a.gx); gy = Real(a.gy); gphi = Real(a.gphi); gv = Real(a.gv);
-    gcos = Real(a.gcos); gsin = Real(a.gsin);
-    v0 = Real(a.v0); act0 = Real(a.act0); pa0 = Real(a.pa0);
-    inv_xi = Real(1.0 / a.d_xi); inv_eta = Real(1.0 / a.d_eta);
-    inv_phi = Real(1.0 / a.d_phi); inv_v = Real(1.0 / a.d_v);
-    d_xi = a.d_xi; d_eta = a.d_eta; d_phi = a.d_phi; d_v = a.d_v;
-    eps_xi = Real(a.eps_xi); eps_eta = Real(a.eps_eta);
-    eps_phi = Real(a.eps_phi); eps_v = Real(a.eps_v);
-    dmax = Real(a.delta_max); window = Real(a.window); l_r = Real(a.l_r);
-    wb = Real(a.wheelbase); Ts = Real(a.T_s); umin = Real(a.u_v_min); umax = Real(a.u_v_max);
-    fe = Real(a.fe); re = Real(a.re); hw = Real(a.hw); r2 = Real(a.r2);
-  }
-};
+using Consts = ConstsT<Real>;
+
+template <typename Real>
+__device__ __forceinline__ const Consts<Real>& consts_of(const RoundArgs& a);
+template <>
+__device__ __forceinline__ const Consts<float>& consts_of<float>(const RoundArgs& a) {
+  return a.kf;
+}
+template <>
+__device__ __forceinline__ const Consts<double>& consts_of<double>(const RoundArgs& a) {
+  return a.kd;
+}
 
 // ----------------------------------------------------------- networks ----
-// [5, H1, 2], theta in registers; layout per layer W (out x in, row-major)
-// then b (include/paraplan/policy.hpp:50-53, src/policy.cpp:53-80).
+// [5, H1, 2] forward pass over any weight accessor w(i); layout per layer W
+// (out x in, row-major) then b (include/paraplan/policy.hpp:50-53,
+// src/policy.cpp:53-80): acc = b, acc += W[o][i] * x[i] ascending, tanh.
+template <typename Real, int H1, class W>
+__device__ __forceinline__ void mlp_5h2(W&& w, const Real s[5], Real& a0, Real& a1) {
+  Real hdn[H1];
+#pragma unroll
+  for (int o = 0; o < H1; ++o) {
+    Real acc = w(5 * H1 + o);
+#pragma unroll
+    for (int i = 0; i < 5; ++i) acc += w(o * 5 + i) * s[i];
+    hdn[o] = M<Real>::th(acc);
+  }
+  constexpr int off = 6 * H1;
+  Real out[2];
+#pragma unroll
+  for (int o = 0; o < 2; ++o) {
+    Real acc = w(off + 2 * H1 + o);
+#pragma unroll
+    for (int i = 0; i < H1; ++i) acc += w(off + o * H1 + i) * hdn[i];
+    out[o] = M<Real>::th(acc);
+  }
+  a0 = out[0];
+  a1 = out[1];
+}
+
+// [5, H1, 2], theta in registers.
 template <typename Real, int H1>
 struct NetReg {
   static constexpr int P = 6 * H1 + (H1 + 1) * 2;
-  static constexpr int kP = P;  // compile-time parameter count
+  static constexpr int kP = P;
+  static constexpr int kH1 = H1;
   Real w[P];
   __device__ __forceinline__ void set(int i, Real v) { w[i] = v; }
   __device__ __forceinline__ void eval(const Real s[5], Real& a0, Real& a1) const {
-    Real hdn[H1];
-#pragma unroll
-    for (int o = 0; o < H1; ++o) {
-      Real acc = w[5 * H1 + o];
-#pragma unroll
-      for (int i = 0; i < 5; ++i) acc += w[o * 5 + i] * s[i];
-      hdn[o] = M<Real>::th(acc);
-    }
-    constexpr int off = 6 * H1;
-    Real out[2];
-#pragma unroll
-    for (int o = 0; o < 2; ++o) {
-      Real acc = w[off + 2 * H1 + o];
-#pragma unroll
-      for (int i = 0; i < H1; ++i) acc += w[off + o * H1 + i] * hdn[i];
-      out[o] = M<Real>::th(acc);
-    }
-    a0 = out[0];
-    a1 = out[1];
+    mlp_5h2<Real, H1>([&](int i) { return w[i]; }, s, a0, a1);
   }
 };
 
-// Any architecture (sizes <= 256): theta in a per-thread column of a global
+// Any architecture (sizes <= 256): theta in a per-lane column of a global
 // scratch buffer (coalesced across the warp), activations in local memory.
 template <typename Real>
 struct NetGlobal {
-  static constexpr int kP = 0;  // runtime parameter count
+  static constexpr int kP = 0;
   Real* col;  // element i at col[i * stride]
   int stride;
   const int32_t* sizes;
@@ -197,19 +216,24 @@ struct NetGlobal {
 };
 
 // ------------------------------------------------------------- sample ----
-// theta for candidate c of restart r (src/planner.cpp:207-226): c == 0 is the
-// centre; otherwise sigma first, then Box-Muller pairs (cos value first).
-// The stream is always evaluated in FP64, then rounded to Real.
-template <typename Real, class Net>
-__device__ __forceinline__ void draw_theta(Net& net, const RoundArgs& a, uint64_t prefix,
-                                           int64_t c) {
-  // KP > 0: fully unrolled so theta stays in registers.
-  constexpr int KP = Net::kP;
-  const int P = KP > 0 ? KP : a.n_params;
+// theta for candidate c of a restart (src/planner.cpp:207-226): c == 0 is the
+// centre; otherwise sigma first, then Box-Muller pairs (cos value first). The
+// stream is evaluated in FP64, then rounded to Real; `put(i, v)` stores it.
+// In injected mode row `c` of the injected matrix is used instead.
+template <typename Real, int KP, class Put>
+__device__ __forceinline__ void draw_theta(const RoundArgs& a, uint64_t prefix, int64_t c,
+                                           int Pdyn, Put&& put) {
+  const int P = KP > 0 ? KP : Pdyn;
   const double* center = a.center;
+  if (a.injected != nullptr) {
+    const double* src = a.injected + c * P;
+#pragma unroll
+    for (int i = 0; i < P; ++i) put(i, Real(src[i]));
+    return;
+  }
   if (c == 0) {
 #pragma unroll
-    for (int i = 0; i < P; ++i) net.set(i, Real(__ldg(center + i)));
+    for (int i = 0; i < P; ++i) put(i, Real(__ldg(center + i)));
     return;
   }
   Stream g{fold(prefix, static_cast<uint64_t>(c))};
@@ -222,180 +246,219 @@ __device__ __forceinline__ void draw_theta(Net& net, const RoundArgs& a, uint64_
     const double t = kTwoPi * u2;
     double sn, cs;
     sincos(t, &sn, &cs);
-    net.set(i, Real(__ldg(center + i) + sigma * (r * cs)));
-    if (i + 1 < P) net.set(i + 1, Real(__ldg(center + i + 1) + sigma * (r * sn)));
+    put(i, Real(__ldg(center + i) + sigma * (r * cs)));
+    if (i + 1 < P) put(i + 1, Real(__ldg(center + i + 1) + sigma * (r * sn)));
   }
 }
 
-template <typename Real, class Net>
-__device__ __forceinline__ void load_theta(Net& net, const double* src, int Pdyn) {
-  constexpr int KP = Net::kP;
-  const int P = KP > 0 ? KP : Pdyn;
-#pragma unroll
-  for (int i = 0; i < P; ++i) net.set(i, Real(src[i]));
-}
-
+// Sorted obstacle field: per row h, xs[h*N + j] ascending and pts[h*N + j].
 template <typename Real>
-struct Outcome {
-  int cls;  // 2 reached, 1 free, 0 collided
-  int t_goal;
-  int steps;
-  Real path, terminal, f0, f1;
+struct Field {
+  const Real* xs;
+  const typename Vec2T<Real>::type* pts;
+  int N;
+  int top;  // largest power of two <= N (binary-search stride)
 };
 
-// src/planner.cpp:66-191 (simulate<false>) in Real arithmetic.
-template <typename Real, class Net>
-__device__ __forceinline__ Outcome<Real> simulate(const Net& net, const Consts<Real>& K,
-                                                  const typename Vec2T<Real>::type* field,
-                                                  int N, int H) {
-  using R2 = typename Vec2T<Real>::type;
-  Real x = Real(0), y = Real(0), phi = Real(0), v = K.v0;
-  Real act = K.act0, pa0 = K.pa0;
-  Real path = Real(0);
-  int status = 1;
-  int t_goal = -1;
-  int h = 0;
-
-  Real ephi = M<Real>::wrap(K.gphi - phi);
-  Real s[5] = {M<Real>::ndiv(K.gx - x, K.d_xi, K.inv_xi), M<Real>::ndiv(K.gy - y, K.d_eta, K.inv_eta),
-               M<Real>::ndiv(ephi, K.d_phi, K.inv_phi), M<Real>::ndiv(K.gv - v, K.d_v, K.inv_v), pa0};
-  Real f0, f1;
-  net.eval(s, f0, f1);  // first action exists even if the rollout ends at h = 0
-
-  for (;; ++h) {
-    Real sphi, cphi;
-    M<Real>::sc(phi, &sphi, &cphi);
-    if (N > 0) {
-      // src/geometry.cpp:63-76 against row h; strict half-planes
-      const R2* row = field + static_cast<size_t>(h) * N;
-      bool hit = false;
-      for (int j = 0; j < N; ++j) {
-        const R2 m = row[j];
-        const Real dx = m.x - x, dy = m.y - y;
-        if (dx * dx + dy * dy < K.r2) {
-          const Real bx = cphi * dx + sphi * dy;
-          const Real by = -sphi * dx + cphi * dy;
-          hit |= (bx < K.fe) & (-bx < K.re) & (by < K.hw) & (-by < K.hw);
-        }
-      }
-      if (hit) {
-        status = 0;
-        break;
-      }
-    }
-    ephi = M<Real>::wrap(K.gphi - phi);
-    {
-      const Real gdx = K.gx - x, gdy = K.gy - y;
-      if (M<Real>::ab(K.gcos * gdx + K.gsin * gdy) <= K.eps_xi &&
-          M<Real>::ab(-K.gsin * gdx + K.gcos * gdy) <= K.eps_eta &&
-          M<Real>::ab(ephi) <= K.eps_phi && M<Real>::ab(K.gv - v) <= K.eps_v) {
-        status = 2;
-        t_goal = h;
-        break;
-      }
-    }
-    if (h == H) break;
-
-    Real a0, a1;
-    if (h == 0) {
-      a0 = f0;
-      a1 = f1;
-    } else {
-      s[0] = M<Real>::ndiv(K.gx - x, K.d_xi, K.inv_xi);
-      s[1] = M<Real>::ndiv(K.gy - y, K.d_eta, K.inv_eta);
-      s[2] = M<Real>::ndiv(ephi, K.d_phi, K.inv_phi);
-      s[3] = M<Real>::ndiv(K.gv - v, K.d_v, K.inv_v);
-      s[4] = pa0;
-      net.eval(s, a0, a1);
-    }
-    // map_controls (src/dynamics.cpp:30-43)
-    const Real c0 = clampr(a0, Real(-1), Real(1));
-    const Real c1 = clampr(a1, Real(-1), Real(1));
-    Real delta = clampr(K.dmax * c0, act - K.window, act + K.window);
-    delta = clampr(delta, -K.dmax, K.dmax);
-    const Real w = Real(0.5) * (c1 + Real(1));
-    const Real u_v = (Real(1) - w) * K.umin + w * K.umax;
-    // explicit Euler (src/dynamics.cpp:45-62)
-    const Real tan_d = M<Real>::tn(delta);
-    const Real tb = K.l_r * tan_d / K.wb;
-    const Real tv = K.Ts * v;
-    const Real nx = x + tv * (cphi - tb * sphi);
-    const Real ny = y + tv * (sphi + tb * cphi);
-    const Real nphi = phi + tv * tan_d / K.wb;
-    const Real nv = v + K.Ts * u_v;
-    const Real dx = nx - x, dy = ny - y;
-    path += M<Real>::sq(dx * dx + dy * dy);
-    x = nx;
-    y = ny;
-    phi = nphi;
-    v = nv;
-    act = delta;
-    pa0 = a0;
+// Number of row entries < v (lower_bound) with a warp-uniform trip count.
+template <typename Real>
+__device__ __forceinline__ int count_below(const Real* xs, int N, int top, Real v) {
+  int pos = 0;
+  for (int step = top; step > 0; step >>= 1) {
+    const int probe = pos + step;
+    if (probe <= N && xs[probe - 1] < v) pos = probe;
   }
-  if (status == 0) ephi = M<Real>::wrap(K.gphi - phi);
-  Outcome<Real> o;
-  o.cls = status;
-  o.t_goal = t_goal;
-  o.steps = h;  // states 0..h were checked; h dynamics steps simulated
-  o.path = path;
-  o.terminal = M<Real>::ndiv(M<Real>::ab(K.gx - x), K.d_xi, K.inv_xi) +
-               M<Real>::ndiv(M<Real>::ab(K.gy - y), K.d_eta, K.inv_eta) +
-               M<Real>::ndiv(M<Real>::ab(ephi), K.d_phi, K.inv_phi) +
-               M<Real>::ndiv(M<Real>::ab(K.gv - v), K.d_v, K.inv_v);
-  o.f0 = f0;
-  o.f1 = f1;
-  return o;
+  return pos;
 }
 
+// Collision of the chassis at (x, y, phi) with row h (src/geometry.cpp:63-76):
+// bounding-circle prefilter, strict half-planes. Only the points with
+// x - cull <= px < x + cull are visited (the rest fail the prefilter).
+// Warp-synchronous: all 32 lanes call it; every loop has a warp-uniform trip
+// count so the warp stays converged.
+template <typename Real>
+__device__ __forceinline__ bool collides(const Field<Real>& f, const Consts<Real>& K, int h,
+                                         Real x, Real y, Real c, Real s) {
+  const int N = f.N;
+  const Real* xs = f.xs + static_cast<size_t>(h) * N;
+  const auto* pts = f.pts + static_cast<size_t>(h) * N;
+  const int top = f.top;
+  const int lo = count_below(xs, N, top, x - K.cull);
+  const int hi = count_below(xs, N, top, x + K.cull);
+  const int cnt = hi - lo;
+  const int rounds = __reduce_max_sync(kFull, cnt);
+  bool hit = false;
+  for (int j = 0; j < rounds; ++j) {
+    if (j < cnt) {
+      const auto m = pts[lo + j];
+      const Real dx = m.x - x, dy = m.y - y;
+      const Real bx = c * dx + s * dy;
+      const Real by = -s * dx + c * dy;
+      hit |= (dx * dx + dy * dy < K.r2) & (bx < K.fe) & (-bx < K.re) & (by < K.hw) &
+             (-by < K.hw);
+    }
+  }
+  return hit;
+}
+
+// One candidate's rollout state (src/planner.cpp:123-125, 130-132).
+template <typename Real>
+struct Lane {
+  Real x, y, phi, v, act, pa0, path, f0, f1, ephi;
+  int h;
+  __device__ __forceinline__ void start(const Consts<Real>& K, Real first0, Real first1) {
+    x = y = phi = Real(0);
+    v = K.v0;
+    act = K.act0;
+    pa0 = K.pa0;
+    path = Real(0);
+    f0 = first0;
+    f1 = first1;
+    h = 0;
+  }
+};
+
+// Features of the EV-at-start state: identical for every candidate.
+template <typename Real>
+__device__ __forceinline__ void start_features(const Consts<Real>& K, Real s[5]) {
+  s[0] = M<Real>::ndiv(K.gx - Real(0), K.d_xi, K.inv_xi);
+  s[1] = M<Real>::ndiv(K.gy - Real(0), K.d_eta, K.inv_eta);
+  s[2] = M<Real>::ndiv(M<Real>::wrap(K.gphi - Real(0)), K.d_phi, K.inv_phi);
+  s[3] = M<Real>::ndiv(K.gv - K.v0, K.d_v, K.inv_v);
+  s[4] = K.pa0;
+}
+
+// One state of the rollout loop (src/planner.cpp:137-183). Returns -1 while
+// running, else the class (0 collided, 1 horizon, 2 reached at state h).
+// Warp-synchronous and branch-free: the checks and the next state are
+// computed for every lane and committed only by the lanes still running,
+// so the warp never splits into per-outcome paths.
+template <typename Real, class Net>
+__device__ __forceinline__ int advance(Lane<Real>& L, const Net& net, const Consts<Real>& K,
+                                       const Field<Real>& f, int H) {
+  Real sphi, cphi;
+  M<Real>::sc(L.phi, &sphi, &cphi);
+  L.ephi = M<Real>::wrap(K.gphi - L.phi);
+  const bool hit = f.N > 0 && collides(f, K, L.h, L.x, L.y, cphi, sphi);
+  const Real gdx = K.gx - L.x, gdy = K.gy - L.y;
+  const bool reached = (M<Real>::ab(K.gcos * gdx + K.gsin * gdy) <= K.eps_xi) &
+                       (M<Real>::ab(-K.gsin * gdx + K.gcos * gdy) <= K.eps_eta) &
+                       (M<Real>::ab(L.ephi) <= K.eps_phi) & (M<Real>::ab(K.gv - L.v) <= K.eps_v);
+  const int cls = hit ? 0 : (reached ? 2 : (L.h == H ? 1 : -1));
+
+  Real s[5];
+  s[0] = M<Real>::ndiv(gdx, K.d_xi, K.inv_xi);
+  s[1] = M<Real>::ndiv(gdy, K.d_eta, K.inv_eta);
+  s[2] = M<Real>::ndiv(L.ephi, K.d_phi, K.inv_phi);
+  s[3] = M<Real>::ndiv(K.gv - L.v, K.d_v, K.inv_v);
+  s[4] = L.pa0;
+  Real a0, a1;
+  net.eval(s, a0, a1);
+  if (L.h == 0) {  // the first action was computed before the loop
+    a0 = L.f0;
+    a1 = L.f1;
+  }
+  // map_controls (src/dynamics.cpp:30-43)
+  const Real c0 = clampr(a0, Real(-1), Real(1));
+  const Real c1 = clampr(a1, Real(-1), Real(1));
+  Real delta = clampr(K.dmax * c0, L.act - K.window, L.act + K.window);
+  delta = clampr(delta, -K.dmax, K.dmax);
+  const Real w = Real(0.5) * (c1 + Real(1));
+  const Real u_v = (Real(1) - w) * K.umin + w * K.umax;
+  // explicit Euler (src/dynamics.cpp:45-62)
+  const Real tan_d = M<Real>::tn(delta);
+  const Real tb = K.l_r * tan_d / K.wb;
+  const Real tv = K.Ts * L.v;
+  const Real nx = L.x + tv * (cphi - tb * sphi);
+  const Real ny = L.y + tv * (sphi + tb * cphi);
+  const Real nphi = L.phi + tv * tan_d / K.wb;
+  const Real nv = L.v + K.Ts * u_v;
+  const Real dx = nx - L.x, dy = ny - L.y;
+  const Real seg = M<Real>::sq(dx * dx + dy * dy);
+  if (cls < 0) {
+    L.path += seg;
+    L.x = nx;
+    L.y = ny;
+    L.phi = nphi;
+    L.v = nv;
+    L.act = delta;
+    L.pa0 = a0;
+    ++L.h;
+  }
+  return cls;
+}
+
+// src/planner.cpp:186-189 at the final state (L.ephi is that state's).
+template <typename Real>
+__device__ __forceinline__ Real terminal_cost(const Lane<Real>& L, const Consts<Real>& K) {
+  return M<Real>::ndiv(M<Real>::ab(K.gx - L.x), K.d_xi, K.inv_xi) +
+         M<Real>::ndiv(M<Real>::ab(K.gy - L.y), K.d_eta, K.inv_eta) +
+         M<Real>::ndiv(M<Real>::ab(L.ephi), K.d_phi, K.inv_phi) +
+         M<Real>::ndiv(M<Real>::ab(K.gv - L.v), K.d_v, K.inv_v);
+}
 
 // ---------------------------------------------------------- reduction ----
 // Lexicographic (cls, k1, k2) descending, index ascending: a total order, so
-// any reduction tree gives the reference's "strict better, lowest index wins"
-// result (src/planner.cpp:40-44, 295, 316).
-template <typename K>
+// any reduction tree gives the reference's "strict better, lowest index
+// wins" result (src/planner.cpp:40-44, 295, 316).
 struct Key {
   int cls;
   int idx;
-  K k1, k2;
+  double k1, k2;
 };
 
-template <typename K>
-__device__ __forceinline__ bool prefer(const Key<K>& a, const Key<K>& b) {
+__device__ __forceinline__ Key empty_key() { return Key{-1, -1, 0.0, 0.0}; }
+
+__device__ __forceinline__ bool prefer(const Key& a, const Key& b) {
   if (a.cls != b.cls) return a.cls > b.cls;
   if (a.k1 != b.k1) return a.k1 > b.k1;
   if (a.k2 != b.k2) return a.k2 > b.k2;
   return static_cast<unsigned>(a.idx) < static_cast<unsigned>(b.idx);
 }
 
-template <typename K>
-__device__ __forceinline__ Key<K> shfl_key(const Key<K>& k, int src) {
-  Key<K> o;
-  o.cls = __shfl_down_sync(0xffffffffu, k.cls, src);
-  o.idx = __shfl_down_sync(0xffffffffu, k.idx, src);
-  o.k1 = __shfl_down_sync(0xffffffffu, k.k1, src);
-  o.k2 = __shfl_down_sync(0xffffffffu, k.k2, src);
+template <typename Real>
+__device__ __forceinline__ Key make_key(int cls, int h, Real path, Real term, int idx) {
+  Key k;  // src/planner.cpp:27-38
+  k.cls = cls;
+  k.idx = idx;
+  if (cls == 2) {
+    k.k1 = -static_cast<double>(h);
+    k.k2 = -static_cast<double>(path);
+  } else {
+    k.k1 = -static_cast<double>(term);
+    k.k2 = 0.0;
+  }
+  return k;
+}
+
+__device__ __forceinline__ Key shfl_key(const Key& k, int off) {
+  Key o;
+  o.cls = __shfl_down_sync(kFull, k.cls, off);
+  o.idx = __shfl_down_sync(kFull, k.idx, off);
+  o.k1 = __shfl_down_sync(kFull, k.k1, off);
+  o.k2 = __shfl_down_sync(kFull, k.k2, off);
   return o;
 }
 
-// Block argmin; result valid in thread 0. `scratch` holds >= 32 keys.
-template <typename K>
-__device__ __forceinline__ Key<K> block_best(Key<K> k, Key<K>* scratch) {
+// Warp argmin; result valid in lane 0.
+__device__ __forceinline__ Key warp_best(Key k) {
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) {
-    const Key<K> o = shfl_key(k, off);
+    const Key o = shfl_key(k, off);
     if (prefer(o, k)) k = o;
   }
+  return k;
+}
+
+// Block argmin; result valid in thread 0. `scratch` holds >= 32 keys.
+__device__ __forceinline__ Key block_best(Key k, Key* scratch) {
+  k = warp_best(k);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (lane == 0) scratch[warp] = k;
   __syncthreads();
   if (warp == 0) {
-    const int nw = (blockDim.x + 31) >> 5;
-    k = lane < nw ? scratch[lane] : Key<K>{-1, -1, K(0), K(0)};
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-      const Key<K> o = shfl_key(k, off);
-      if (prefer(o, k)) k = o;
-    }
+    k = lane < static_cast<int>(blockDim.x >> 5) ? scratch[lane] : empty_key();
+    k = warp_best(k);
   }
   __syncthreads();
   return k;
@@ -404,28 +467,266 @@ __device__ __forceinline__ Key<K> block_best(Key<K> k, Key<K>* scratch) {
 __device__ __forceinline__ unsigned long long block_sum(unsigned long long v,
                                                         unsigned long long* scratch) {
 #pragma unroll
-  for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off);
+  for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(kFull, v, off);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (lane == 0) scratch[warp] = v;
   __syncthreads();
   if (warp == 0) {
-    const int nw = (blockDim.x + 31) >> 5;
-    v = lane < nw ? scratch[lane] : 0ull;
+    v = lane < static_cast<int>(blockDim.x >> 5) ? scratch[lane] : 0ull;
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off);
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(kFull, v, off);
   }
   __syncthreads();
   return v;
 }
 
-// ------------------------------------------------------------- kernel ----
+__device__ __forceinline__ Key load_rec_cg(const Rec* src) {
+  // written by other CTAs: read through L2 (ld.global.cg), never L1
+  return Key{__ldcg(&src->cls), __ldcg(&src->cand), __ldcg(&src->k1), __ldcg(&src->k2)};
+}
+
+// Shared-memory image of the sorted field: [xs (H+1)N][pad 16][pts (H+1)N].
+template <typename Real>
+__device__ __forceinline__ Field<Real> stage_field(const RoundArgs& a, unsigned char* smem) {
+  using R2 = typename Vec2T<Real>::type;
+  const int N = a.n_points;
+  const size_t count = static_cast<size_t>(a.H + 1) * N;
+  const Real* gxs = static_cast<const Real*>(a.field);
+  const size_t pts_off = (count * sizeof(Real) + 15) & ~size_t(15);
+  const R2* gpts =
+      reinterpret_cast<const R2*>(static_cast<const unsigned char*>(a.field) + pts_off);
+  int top = 1;
+  while (top * 2 <= N) top *= 2;
+  Field<Real> f{gxs, gpts, N, N > 0 ? top : 0};
+  if (a.field_smem_bytes > 0 && N > 0) {
+    Real* sxs = reinterpret_cast<Real*>(smem);
+    R2* spts = reinterpret_cast<R2*>(smem + pts_off);
+    for (size_t i = threadIdx.x; i < count; i += blockDim.x) {
+      sxs[i] = gxs[i];
+      spts[i] = gpts[i];
+    }
+    f.xs = sxs;
+    f.pts = spts;
+  }
+  __syncthreads();
+  return f;
+}
+
+// Per-sample debug/parity record.
+template <typename Real>
+__device__ __forceinline__ void write_sample(const RoundArgs& a, int64_t slot, int cls,
+                                             const Lane<Real>& L, Real term) {
+  SampleOut& so = a.per_sample[slot];
+  so.reached = cls == 2;
+  so.t_goal = cls == 2 ? L.h : -1;
+  so.collided = cls == 0;
+  so.steps = L.h;
+  so.path_length = static_cast<double>(L.path);
+  so.terminal_cost = static_cast<double>(term);
+  so.first_a0 = static_cast<double>(L.f0);
+  so.first_a1 = static_cast<double>(L.f1);
+}
+
+// Last CTA: per-restart reduction of `n_src` records per restart (laid out
+// restart-major), publish the work counters, re-arm the tickets.
+__device__ __forceinline__ void finish_round(const RoundArgs& a, const Rec* recs, int n_src,
+                                             Key* red) {
+  __shared__ int s_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(&a.counters[1], 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  for (int r = 0; r < a.restart_count; ++r) {
+    Key k = empty_key();
+    for (int t = threadIdx.x; t < n_src; t += blockDim.x) {
+      const Key o = load_rec_cg(recs + static_cast<size_t>(r) * n_src + t);
+      if (o.cls >= 0 && (k.cls < 0 || prefer(o, k))) k = o;
+    }
+    const Key best = block_best(k, red);
+    if (threadIdx.x == 0) a.out[r] = Rec{best.cls, best.idx, best.k1, best.k2};
+  }
+  if (threadIdx.x == 0) {
+    a.exec[2] = atomicExch(&a.exec[0], 0ull);
+    a.exec[3] = atomicExch(&a.exec[1], 0ull);
+    a.counters[0] = 0;
+    a.counters[1] = 0;
+  }
+}
+
+// Warp-cooperative flush of the lanes' best keys (flagged by `flush`) into
+// the warp's per-restart shared table, one restart at a time.
+__device__ __forceinline__ void flush_bests(bool& flush, Key& best, int best_r, Key* table_w,
+                                            int lane) {
+  unsigned pend = __ballot_sync(kFull, flush);
+  while (pend != 0u) {
+    const int r0 = __shfl_sync(kFull, best_r, __ffs(pend) - 1);
+    const bool mine = flush && best_r == r0;
+    const Key k = warp_best(mine ? best : empty_key());
+    if (lane == 0 && (table_w[r0].cls < 0 || prefer(k, table_w[r0]))) table_w[r0] = k;
+    if (mine) {
+      flush = false;
+      best = empty_key();
+    }
+    pend = __ballot_sync(kFull, flush);
+  }
+}
+
+// --------------------------------------------------- generate kernel ----
+// theta (rounded to Real) and the first action of every candidate of the
+// round, one thread per candidate at full SIMT width: the FP64 RNG lives here
+// and not in the rollout kernel, so the rollout kernel stays register-light.
+// Layout: theta_buf[i * total + s], first_buf[k * total + s], with the flat
+// index s = r * count + local (restart-major).
+template <typename Real, int H1>
+__global__ void __launch_bounds__(256) generate_kernel(const RoundArgs a) {
+  constexpr int P = NetReg<Real, H1>::P;
+  const Consts<Real>& K = consts_of<Real>(a);
+  Real s0[5];
+  start_features(K, s0);
+  Real* theta = static_cast<Real*>(a.theta_buf);
+  Real* first = static_cast<Real*>(a.first_buf);
+  const int64_t total = a.count * a.restart_count;
+  for (int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; s < total;
+       s += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int r = static_cast<int>(s / a.count);
+    const int64_t local = s - static_cast<int64_t>(r) * a.count;
+    NetReg<Real, H1> n;
+    draw_theta<Real, P>(a, __ldg(a.key_prefix + r), a.injected ? local : a.cand_begin + local, P,
+                        [&](int i, Real v) {
+                          n.w[i] = v;
+                          theta[static_cast<int64_t>(i) * total + s] = v;
+                        });
+    Real f0, f1;
+    n.eval(s0, f0, f1);  // first action (src/planner.cpp:130-132)
+    first[s] = f0;
+    first[total + s] = f1;
+  }
+}
+
+// ------------------------------------------------------ refill kernel ----
+template <typename Real, class Net>
+__global__ void __launch_bounds__(kBlock) refill_kernel(const RoundArgs a) {
+  constexpr int P = Net::kP;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ Key table[kWarps][kMaxRestartsPerLaunch];
+  __shared__ Key red[32];
+  __shared__ unsigned long long red_sum[32];
+
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const Consts<Real>& K = consts_of<Real>(a);
+  const int H = a.H;
+  for (int i = threadIdx.x; i < kWarps * kMaxRestartsPerLaunch; i += blockDim.x) {
+    (&table[0][0])[i] = empty_key();
+  }
+  const Field<Real> f = stage_field<Real>(a, smem_raw);
+
+  const int bpr = a.tiles_per_restart;  // 32-candidate batches per restart
+  const unsigned total_batches = static_cast<unsigned>(a.n_tiles);
+  const int64_t total = a.count * a.restart_count;
+  const Real* theta = static_cast<const Real*>(a.theta_buf);
+  const Real* first = static_cast<const Real*>(a.first_buf);
+
+  Net net;
+#pragma unroll
+  for (int i = 0; i < P; ++i) net.w[i] = Real(0);
+  Lane<Real> L;
+  L.start(K, Real(0), Real(0));  // idle lanes step a valid (discarded) state
+  bool active = false;
+  int my_r = 0;
+  int my_c = 0;  // local candidate index within [0, count)
+  Key best = empty_key();
+  int best_r = -1;
+  int q_head = 32, q_count = 0, q_r = 0, q_c0 = 0;
+  bool exhausted = false;
+  unsigned long long n_steps = 0, n_states = 0;
+
+  for (;;) {
+    // -------- hand the warp's current batch to idle lanes --------
+    const unsigned need = __ballot_sync(kFull, !active);
+    if (need != 0u) {
+      if (q_head >= q_count && !exhausted) {
+        unsigned b = 0;
+        if (lane == 0) b = atomicAdd(&a.counters[0], 1u);
+        b = __shfl_sync(kFull, b, 0);
+        if (b >= total_batches) {
+          exhausted = true;
+        } else {
+          q_r = static_cast<int>(b) / bpr;
+          q_c0 = (static_cast<int>(b) - q_r * bpr) * 32;
+          const int64_t left = a.count - q_c0;
+          q_count = left < 32 ? static_cast<int>(left) : 32;
+          q_head = 0;
+        }
+      }
+      const int avail = q_count - q_head;
+      if (avail > 0) {
+        const int rank = __popc(need & ((1u << lane) - 1u));
+        if (!active && rank < avail) {
+          my_r = q_r;
+          my_c = q_c0 + q_head + rank;
+          const int64_t sidx = static_cast<int64_t>(my_r) * a.count + my_c;
+#pragma unroll
+          for (int i = 0; i < P; ++i) net.w[i] = theta[static_cast<int64_t>(i) * total + sidx];
+          L.start(K, first[sidx], first[total + sidx]);
+          active = true;
+        }
+        q_head += __popc(need) < avail ? __popc(need) : avail;
+      }
+    }
+    if (!__any_sync(kFull, active)) break;  // stream exhausted, all lanes done
+
+    // -------- one rollout state per lane --------
+    // every lane steps (idle lanes only at the stream tail, results unused)
+    const int cls = advance<Real>(L, net, K, f, H);
+    const bool done = active && cls >= 0;
+    // lane bests are per restart: flush the old one before crossing over
+    bool flush = done && best.cls >= 0 && best_r != my_r;
+    if (__any_sync(kFull, flush)) flush_bests(flush, best, best_r, table[warp], lane);
+    if (done) {
+      const Real term = terminal_cost(L, K);
+      const Key k = make_key<Real>(cls, L.h, L.path, term, static_cast<int>(a.cand_begin + my_c));
+      if (best.cls < 0 || prefer(k, best)) {
+        best = k;
+        best_r = my_r;
+      }
+      n_steps += static_cast<unsigned long long>(L.h);
+      n_states += static_cast<unsigned long long>(L.h + 1);
+      if (a.per_sample != nullptr) {
+        write_sample(a, static_cast<int64_t>(my_r) * a.count + my_c, cls, L, term);
+      }
+      active = false;
+    }
+  }
+
+  // -------- flush lane bests, combine warps, publish CTA records --------
+  bool flush = best.cls >= 0;
+  flush_bests(flush, best, best_r, table[warp], lane);
+  __syncthreads();
+  for (int r = threadIdx.x; r < a.restart_count; r += blockDim.x) {
+    Key k = table[0][r];
+    for (int w = 1; w < kWarps; ++w) {
+      if (table[w][r].cls >= 0 && (k.cls < 0 || prefer(table[w][r], k))) k = table[w][r];
+    }
+    a.tile_recs[static_cast<size_t>(r) * gridDim.x + blockIdx.x] = Rec{k.cls, k.idx, k.k1, k.k2};
+  }
+  const unsigned long long steps = block_sum(n_steps, red_sum);
+  const unsigned long long states = block_sum(n_states, red_sum);
+  if (threadIdx.x == 0) {
+    atomicAdd(&a.exec[0], steps);
+    atomicAdd(&a.exec[1], states);
+  }
+  finish_round(a, a.tile_recs, static_cast<int>(gridDim.x), red);
+}
+
+// ---------------------------------------------------- lockstep kernel ----
 template <typename Real, class Net>
 struct NetFactory;
 
 template <typename Real, int H1>
 struct NetFactory<Real, NetReg<Real, H1>> {
   static __device__ __forceinline__ NetReg<Real, H1> make(const RoundArgs&) { return {}; }
-  static constexpr bool kStaticP = true;
 };
 
 template <typename Real>
@@ -449,37 +750,24 @@ struct NetFactory<Real, NetGlobal<Real>> {
     n.n_layers = a.n_layers;
     return n;
   }
-  static constexpr bool kStaticP = false;
 };
 
 template <typename Real, class Net>
-__global__ void __launch_bounds__(128) round_kernel(const RoundArgs a) {
-  using R2 = typename Vec2T<Real>::type;
+__global__ void __launch_bounds__(kBlock) lockstep_kernel(const RoundArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  __shared__ Key<double> red[32];
+  __shared__ Key red[32];
   __shared__ unsigned long long red_sum[32];
   __shared__ int s_tile;
 
-  Consts<Real> K;
-  K.load(a);
-  const int N = a.n_points;
+  const Consts<Real>& K = consts_of<Real>(a);
   const int H = a.H;
   const int P = a.n_params;
-
-  // Stage the obstacle field once per persistent CTA (read by every warp as
-  // a broadcast); large fields stay in L2 and are read through the RO path.
-  const R2* field = static_cast<const R2*>(a.field);
-  if (a.field_smem_bytes > 0) {
-    R2* dst = reinterpret_cast<R2*>(smem_raw);
-    const int total = (H + 1) * N;
-    for (int i = threadIdx.x; i < total; i += blockDim.x) dst[i] = field[i];
-    field = dst;
-    __syncthreads();
-  }
+  const Field<Real> f = stage_field<Real>(a, smem_raw);
+  Real s0[5];
+  start_features(K, s0);
 
   Net net = NetFactory<Real, Net>::make(a);
-  unsigned long long my_steps = 0, my_states = 0;
-
+  unsigned long long n_steps = 0, n_states = 0;
   for (;;) {
     if (threadIdx.x == 0) s_tile = static_cast<int>(atomicAdd(&a.counters[0], 1u));
     __syncthreads();
@@ -487,109 +775,110 @@ __global__ void __launch_bounds__(128) round_kernel(const RoundArgs a) {
     __syncthreads();
     if (tile >= a.n_tiles) break;
     const int r = tile / a.tiles_per_restart;
-    const int64_t local = static_cast<int64_t>(tile - r * a.tiles_per_restart) * blockDim.x +
-                          threadIdx.x;
-    Key<double> key{-1, -1, 0.0, 0.0};
-    if (local < a.count) {
-      const int64_t c = a.cand_begin + local;
-      if (a.injected != nullptr) {
-        load_theta<Real>(net, a.injected + local * P, P);
-      } else {
-        draw_theta<Real>(net, a, __ldg(a.key_prefix + r), c);
-      }
-      const Outcome<Real> o = simulate<Real>(net, K, field, N, H);
-      key.cls = o.cls;
-      key.idx = static_cast<int>(c);
-      if (o.cls == 2) {  // src/planner.cpp:27-38
-        key.k1 = -static_cast<double>(o.t_goal);
-        key.k2 = -static_cast<double>(o.path);
-      } else {
-        key.k1 = -static_cast<double>(o.terminal);
-        key.k2 = 0.0;
-      }
-      my_steps += static_cast<unsigned long long>(o.steps);
-      my_states += static_cast<unsigned long long>(o.steps + 1);
+    const int64_t local =
+        static_cast<int64_t>(tile - r * a.tiles_per_restart) * blockDim.x + threadIdx.x;
+    Key key = empty_key();
+    const bool valid = local < a.count;
+    const int64_t c = a.cand_begin + (valid ? local : 0);
+    draw_theta<Real, Net::kP>(a, __ldg(a.key_prefix + r), a.injected ? (valid ? local : 0) : c,
+                              P, [&](int i, Real v) { net.set(i, v); });
+    Real f0, f1;
+    net.eval(s0, f0, f1);
+    Lane<Real> L;
+    L.start(K, f0, f1);
+    int cls = -1;
+    // lanes keep stepping (and discarding) until the whole warp is done
+    while (__any_sync(kFull, cls < 0)) {
+      const int k = advance<Real>(L, net, K, f, H);
+      if (cls < 0) cls = k;
+    }
+    if (valid) {
+      const Real term = terminal_cost(L, K);
+      key = make_key<Real>(cls, L.h, L.path, term, static_cast<int>(c));
+      n_steps += static_cast<unsigned long long>(L.h);
+      n_states += static_cast<unsigned long long>(L.h + 1);
       if (a.per_sample != nullptr) {
-        SampleOut& so = a.per_sample[static_cast<int64_t>(r) * a.count + local];
-        so.reached = o.cls == 2;
-        so.t_goal = o.t_goal;
-        so.collided = o.cls == 0;
-        so.steps = o.steps;
-        so.path_length = static_cast<double>(o.path);
-        so.terminal_cost = static_cast<double>(o.terminal);
-        so.first_a0 = static_cast<double>(o.f0);
-        so.first_a1 = static_cast<double>(o.f1);
+        write_sample(a, static_cast<int64_t>(r) * a.count + local, cls, L, term);
       }
     }
-    const Key<double> best = block_best(key, red);
+    const Key best = block_best(key, red);
+    // tile records are restart-major: [r][tile within restart]
     if (threadIdx.x == 0) a.tile_recs[tile] = Rec{best.cls, best.idx, best.k1, best.k2};
   }
-
-  // Work accounting, one atomic per CTA.
-  const unsigned long long steps = block_sum(my_steps, red_sum);
-  const unsigned long long states = block_sum(my_states, red_sum);
+  const unsigned long long steps = block_sum(n_steps, red_sum);
+  const unsigned long long states = block_sum(n_states, red_sum);
   if (threadIdx.x == 0) {
     atomicAdd(&a.exec[0], steps);
     atomicAdd(&a.exec[1], states);
   }
-
-  // Last CTA reduces the tile winners of every restart (ordered merge).
-  __threadfence();
-  if (threadIdx.x == 0) s_tile = static_cast<int>(atomicAdd(&a.counters[1], 1u));
-  __syncthreads();
-  if (s_tile != static_cast<int>(gridDim.x) - 1) return;
-  __threadfence();
-  for (int r = 0; r < a.restart_count; ++r) {
-    Key<double> k{-1, -1, 0.0, 0.0};
-    for (int t = threadIdx.x; t < a.tiles_per_restart; t += blockDim.x) {
-      // written by other CTAs: read through L2 (ld.global.cg), never L1
-      const Rec* src = a.tile_recs + r * a.tiles_per_restart + t;
-      const Key<double> o{__ldcg(&src->cls), __ldcg(&src->cand), __ldcg(&src->k1),
-                          __ldcg(&src->k2)};
-      if (o.cls >= 0 && (k.cls < 0 || prefer(o, k))) k = o;
-    }
-    const Key<double> best = block_best(k, red);
-    if (threadIdx.x == 0) a.out[r] = Rec{best.cls, best.idx, best.k1, best.k2};
-  }
-  if (threadIdx.x == 0) {
-    // publish the work counters and re-arm everything for the next round
-    a.exec[2] = atomicExch(&a.exec[0], 0ull);
-    a.exec[3] = atomicExch(&a.exec[1], 0ull);
-    a.counters[0] = 0;
-    a.counters[1] = 0;
-  }
+  finish_round(a, a.tile_recs, a.tiles_per_restart, red);
 }
 
 // ------------------------------------------------------------ launch ----
+// Register-resident nets use the refill schedule; PARAPLAN_SCHEDULE=lockstep
+// forces the lockstep schedule (A/B measurements only).
+inline bool force_lockstep() {
+  static const bool v = [] {
+    const char* e = std::getenv("PARAPLAN_SCHEDULE");
+    return e != nullptr && std::strcmp(e, "lockstep") == 0;
+  }();
+  return v;
+}
+
+template <class Net>
+bool refill_schedule() {
+  return Net::kP > 0 && !force_lockstep();
+}
+
+template <typename Real, class Net>
+void (*kernel_of())(const RoundArgs) {
+  if constexpr (Net::kP > 0) {
+    if (refill_schedule<Net>()) return refill_kernel<Real, Net>;
+  }
+  return lockstep_kernel<Real, Net>;
+}
+
 template <typename Real, class Net>
 int launch_impl(const RoundArgs& a, void* stream) {
-  const size_t smem = static_cast<size_t>(a.field_smem_bytes);
-  if (smem > 48 * 1024) {
-    cudaFuncSetAttribute(round_kernel<Real, Net>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(smem));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if constexpr (Net::kP > 0) {
+    if (refill_schedule<Net>()) {
+      const int64_t total = a.count * a.restart_count;
+      const int gen_blocks = static_cast<int>((total + 255) / 256);
+      generate_kernel<Real, Net::kH1><<<gen_blocks, 256, 0, st>>>(a);
+    }
   }
-  round_kernel<Real, Net><<<a.grid, a.block, smem, static_cast<cudaStream_t>(stream)>>>(a);
+  auto k = kernel_of<Real, Net>();
+  const size_t smem = static_cast<size_t>(a.field_smem_bytes);
+  if (smem > 32 * 1024) {
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  }
+  k<<<a.grid, a.block, smem, st>>>(a);
   return static_cast<int>(cudaGetLastError());
 }
 
 template <typename Real, class Net>
-int shape_impl(int device, int smem_bytes, LaunchShape* out) {
+int shape_impl(int device, int field_bytes, LaunchShape* out) {
+  auto k = kernel_of<Real, Net>();
+  const bool refill = refill_schedule<Net>();
+  const int smem_bytes = field_bytes;
+  out->queue_bytes = 0;
+  out->theta_elem = refill ? Net::kP + 2 : 0;  // theta + first action per candidate
   int sms = 0, blocks = 0;
   cudaError_t e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
   if (e != cudaSuccess) return static_cast<int>(e);
-  if (smem_bytes > 48 * 1024) {
-    e = cudaFuncSetAttribute(round_kernel<Real, Net>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
+  if (smem_bytes > 32 * 1024) {
+    e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
     if (e != cudaSuccess) return static_cast<int>(e);
   }
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, round_kernel<Real, Net>, 128,
-                                                    smem_bytes);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k, kBlock, smem_bytes);
   if (e != cudaSuccess) return static_cast<int>(e);
   int smem_optin = 0;
   cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
-  out->block = 128;
+  out->block = kBlock;
   out->grid = sms * (blocks > 0 ? blocks : 1);
   out->smem_limit = smem_optin;
+  out->refill = refill ? 1 : 0;
   return 0;
 }
 
