@@ -218,7 +218,11 @@ void fill_consts(const ppdev::RoundArgs& a, ppdev::ConstsT<Real>* k) {
   k->re = Real(a.re);
   k->hw = Real(a.hw);
   k->r2 = Real(a.r2);
-  k->cull = Real(std::sqrt(a.r2) + 1e-3);
+  const double cull = std::sqrt(a.r2) + 1e-3;
+  k->cull = Real(cull);
+  k->bx0 = Real(a.bucket_x0);
+  k->binv = Real(1.0 / a.bucket_w);
+  k->qpad = Real(cull + a.bucket_w / 8.0);
 }
 
 // Goal transform and constants of a snapshot (src/planner.cpp:70-81).
@@ -266,48 +270,74 @@ void upload_snapshot(pp_handle* h, const pp_snapshot& s) {
   a.r2 = radius * radius;
   a.sig_lo = cfg.sigma_log_low;
   a.sig_span = cfg.sigma_log_high - cfg.sigma_log_low;
-  fill_consts(a, &a.kf);
-  fill_consts(a, &a.kd);
   a.H = cfg.H;
   a.n_params = h->P;
   a.n_layers = static_cast<int32_t>(h->sizes.size());
   for (size_t i = 0; i < h->sizes.size(); ++i) a.sizes[i] = h->sizes[i];
 
-  // Only rows 0..H are ever read; ship those, in the compute precision, each
-  // row sorted by x so the kernel can window its collision scan (the verdict
-  // is an OR over the row's points, independent of their order).
+  // Only rows 0..H are ever read; ship those, in the compute precision,
+  // each row ordered by x-bucket with per-bucket start offsets so the kernel
+  // visits only the points near its own x (the collision verdict is an OR
+  // over the row's points, independent of their order).
   const int N = s.n_points;
   a.n_points = N;
-  const size_t count = static_cast<size_t>(cfg.H + 1) * static_cast<size_t>(N);
+  const size_t rows = static_cast<size_t>(cfg.H + 1);
+  const size_t count = rows * static_cast<size_t>(N);
   const size_t elem = h->fp64 ? sizeof(double) : sizeof(float);
-  const size_t pts_off = (count * elem + 15) & ~size_t(15);
-  const size_t bytes = pts_off + 2 * count * elem;
+  double xmin = 0.0, xmax = 0.0;
+  for (size_t i = 0; i < count; ++i) {
+    const double x = s.field_xy[2 * i];
+    if (i == 0 || x < xmin) xmin = x;
+    if (i == 0 || x > xmax) xmax = x;
+  }
+  const double cull = std::sqrt(a.r2) + 1e-3;
+  double width = 0.5 * cull;
+  int B = 1;
+  if (count > 0) {
+    if (!(std::isfinite(xmin) && std::isfinite(xmax))) {
+      throw std::invalid_argument("obstacle field has non-finite coordinates");
+    }
+    width = std::max(width, (xmax - xmin) / 4095.0);
+    B = static_cast<int>(std::floor((xmax - xmin) / width)) + 1;
+    B = std::min(std::max(B, 1), 4096);
+  }
+  a.n_buckets = B;
+  a.bucket_x0 = xmin;
+  a.bucket_w = width;
+  const size_t pts_bytes = 2 * count * elem;
+  const size_t bytes = pts_bytes + rows * (B + 1) * sizeof(int32_t);
   if (count > 0) {
     h->h_field.reserve(bytes, "pinned field");
     h->d_field.reserve(bytes, "device field");
     unsigned char* base = static_cast<unsigned char*>(h->h_field.p);
-    std::vector<int32_t> order(N);
-    for (int row = 0; row <= cfg.H; ++row) {
-      const double* src = s.field_xy + 2 * static_cast<size_t>(row) * N;
-      for (int j = 0; j < N; ++j) order[j] = j;
+    int32_t* starts = reinterpret_cast<int32_t*>(base + pts_bytes);
+    std::vector<int32_t> order(N), bucket(N);
+    for (size_t row = 0; row < rows; ++row) {
+      const double* src = s.field_xy + 2 * row * N;
+      for (int j = 0; j < N; ++j) {
+        order[j] = j;
+        bucket[j] = std::min(B - 1, std::max(0, static_cast<int>(std::floor(
+                                                    (src[2 * j] - xmin) / width))));
+      }
       std::stable_sort(order.begin(), order.end(),
-                       [&](int32_t p, int32_t q) { return src[2 * p] < src[2 * q]; });
-      const size_t o = static_cast<size_t>(row) * N;
-      if (h->fp64) {
-        double* xs = reinterpret_cast<double*>(base) + o;
-        double* pts = reinterpret_cast<double*>(base + pts_off) + 2 * o;
-        for (int j = 0; j < N; ++j) {
-          xs[j] = src[2 * order[j]];
-          pts[2 * j] = src[2 * order[j]];
-          pts[2 * j + 1] = src[2 * order[j] + 1];
-        }
-      } else {
-        float* xs = reinterpret_cast<float*>(base) + o;
-        float* pts = reinterpret_cast<float*>(base + pts_off) + 2 * o;
-        for (int j = 0; j < N; ++j) {
-          xs[j] = static_cast<float>(src[2 * order[j]]);
-          pts[2 * j] = static_cast<float>(src[2 * order[j]]);
-          pts[2 * j + 1] = static_cast<float>(src[2 * order[j] + 1]);
+                       [&](int32_t p, int32_t q) { return bucket[p] < bucket[q]; });
+      int32_t* st = starts + row * (B + 1);
+      int next = 0;
+      for (int b = 0; b <= B; ++b) {
+        while (next < N && bucket[order[next]] < b) ++next;
+        st[b] = next;
+      }
+      const size_t o = row * N;
+      for (int j = 0; j < N; ++j) {
+        const double px = src[2 * order[j]], py = src[2 * order[j] + 1];
+        if (h->fp64) {
+          double* pts = reinterpret_cast<double*>(base) + 2 * (o + j);
+          pts[0] = px;
+          pts[1] = py;
+        } else {
+          float* pts = reinterpret_cast<float*>(base) + 2 * (o + j);
+          pts[0] = static_cast<float>(px);
+          pts[1] = static_cast<float>(py);
         }
       }
     }
@@ -315,9 +345,11 @@ void upload_snapshot(pp_handle* h, const pp_snapshot& s) {
        "field H2D");
     h->timing.h2d_bytes += static_cast<int64_t>(bytes);
   }
+  fill_consts(a, &a.kf);
+  fill_consts(a, &a.kd);
   a.field = h->d_field.p;
-  // stage the field in shared memory when it fits comfortably next to the
-  // theta queues; larger fields are read through L1/L2
+  // stage the field in shared memory when it fits; larger fields are read
+  // through L1/L2
   h->field_smem_bytes = (count > 0 && bytes <= 40 * 1024) ? static_cast<int>(bytes) : 0;
   h->snap_valid = true;
 }

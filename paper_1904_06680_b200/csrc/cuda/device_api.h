@@ -36,6 +36,8 @@ struct ConstsT {
   Real dmax, window, l_r, wb, Ts, umin, umax;
   Real fe, re, hw, r2;  // chassis half-planes, squared bounding radius
   Real cull;            // collision x-window half width: bounding radius + 1e-3
+  Real bx0, binv;       // x-bucket grid of the field: origin, 1 / bucket width
+  Real qpad;            // bucket query half width: cull + bucket width / 8
 };
 
 // Everything one sampling round needs. Scalars are FP64 here; the FP32
@@ -69,7 +71,10 @@ struct RoundArgs {
   const uint64_t* key_prefix;  // device [restart_count]: fold^4(seed, t, r, iter)
   const double* center;        // device [n_params]
   const double* injected;      // device [count * n_params] or null (RNG off)
-  const void* field;           // device [xs Real (H+1)N][pad16][pts Real2 (H+1)N], rows sorted by x
+  const void* field;           // device [pts Real2 (H+1)N][starts int32 (H+1)(B+1)], rows
+                               // sorted by x-bucket; starts[h][b] = first point of bucket b
+  int32_t n_buckets;           // B
+  double bucket_x0, bucket_w;  // x-bucket grid (host side; kf/kd carry bx0 and 1/w)
   // scratch / outputs (device)
   Rec* tile_recs;              // restart-major: [r][tile] (lockstep) or [r][CTA] (refill)
   Rec* out;                    // [restart_count]

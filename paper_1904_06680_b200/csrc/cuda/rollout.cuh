@@ -237,55 +237,67 @@ __device__ __forceinline__ void draw_theta(const RoundArgs& a, uint64_t prefix, 
     return;
   }
   Stream g{fold(prefix, static_cast<uint64_t>(c))};
-  const double sigma = pow(10.0, a.sig_lo + unit53(g.next()) * a.sig_span);
+  if constexpr (sizeof(Real) == sizeof(float)) {
+    // FP32 path: the integer stream is exact; the Box-Muller transform runs in
+    // float (theta agrees with the FP64 draw to a few float ulps, well inside
+    // the FP32 parity tolerance; the host regenerates the winner in FP64).
+    const float sigma =
+        exp10f(static_cast<float>(a.sig_lo + unit53(g.next()) * a.sig_span));
 #pragma unroll
-  for (int i = 0; i < P; i += 2) {
-    const double u1 = 1.0 - unit53(g.next());
-    const double u2 = unit53(g.next());
-    const double r = sqrt(-2.0 * log(u1));
-    const double t = kTwoPi * u2;
-    double sn, cs;
-    sincos(t, &sn, &cs);
-    put(i, Real(__ldg(center + i) + sigma * (r * cs)));
-    if (i + 1 < P) put(i + 1, Real(__ldg(center + i + 1) + sigma * (r * sn)));
+    for (int i = 0; i < P; i += 2) {
+      const float u1 = static_cast<float>(1.0 - unit53(g.next()));
+      const float u2 = static_cast<float>(unit53(g.next()));
+      const float r = sqrtf(-2.0f * logf(u1));
+      float sn, cs;
+      sincospif(2.0f * u2, &sn, &cs);
+      put(i, Real(static_cast<float>(__ldg(center + i)) + sigma * (r * cs)));
+      if (i + 1 < P) put(i + 1, Real(static_cast<float>(__ldg(center + i + 1)) + sigma * (r * sn)));
+    }
+  } else {
+    const double sigma = pow(10.0, a.sig_lo + unit53(g.next()) * a.sig_span);
+#pragma unroll
+    for (int i = 0; i < P; i += 2) {
+      const double u1 = 1.0 - unit53(g.next());
+      const double u2 = unit53(g.next());
+      const double r = sqrt(-2.0 * log(u1));
+      const double t = kTwoPi * u2;
+      double sn, cs;
+      sincos(t, &sn, &cs);
+      put(i, Real(__ldg(center + i) + sigma * (r * cs)));
+      if (i + 1 < P) put(i + 1, Real(__ldg(center + i + 1) + sigma * (r * sn)));
+    }
   }
 }
 
-// Sorted obstacle field: per row h, xs[h*N + j] ascending and pts[h*N + j].
+// Bucketed obstacle field: per row h the points sorted by x-bucket
+// (bucket b = floor((px - bx0) * binv), same grid for all rows) and
+// starts[h * (B+1) + b] = index of the first point of bucket b.
 template <typename Real>
 struct Field {
-  const Real* xs;
   const typename Vec2T<Real>::type* pts;
+  const int* starts;
   int N;
-  int top;  // largest power of two <= N (binary-search stride)
+  int B;
 };
 
-// Number of row entries < v (lower_bound) with a warp-uniform trip count.
-template <typename Real>
-__device__ __forceinline__ int count_below(const Real* xs, int N, int top, Real v) {
-  int pos = 0;
-  for (int step = top; step > 0; step >>= 1) {
-    const int probe = pos + step;
-    if (probe <= N && xs[probe - 1] < v) pos = probe;
-  }
-  return pos;
-}
-
 // Collision of the chassis at (x, y, phi) with row h (src/geometry.cpp:63-76):
-// bounding-circle prefilter, strict half-planes. Only the points with
-// x - cull <= px < x + cull are visited (the rest fail the prefilter).
-// Warp-synchronous: all 32 lanes call it; every loop has a warp-uniform trip
-// count so the warp stays converged.
+// bounding-circle prefilter, strict half-planes. Only the buckets covering
+// [x - qpad, x + qpad] are visited; every point outside them has
+// |px - x| > cull > r and fails the prefilter. Warp-synchronous: all 32
+// lanes call it and the candidate loop has a warp-uniform trip count.
 template <typename Real>
 __device__ __forceinline__ bool collides(const Field<Real>& f, const Consts<Real>& K, int h,
                                          Real x, Real y, Real c, Real s) {
-  const int N = f.N;
-  const Real* xs = f.xs + static_cast<size_t>(h) * N;
-  const auto* pts = f.pts + static_cast<size_t>(h) * N;
-  const int top = f.top;
-  const int lo = count_below(xs, N, top, x - K.cull);
-  const int hi = count_below(xs, N, top, x + K.cull);
-  const int cnt = hi - lo;
+  const int B = f.B;
+  const int* st = f.starts + static_cast<size_t>(h) * (B + 1);
+  const auto* pts = f.pts + static_cast<size_t>(h) * f.N;
+  const Real top = Real(B - 1);
+  const Real flo = (x - K.qpad - K.bx0) * K.binv;
+  const Real fhi = (x + K.qpad - K.bx0) * K.binv;
+  const int blo = static_cast<int>(floor(fmin(fmax(flo, Real(0)), top)));
+  const int bhi = static_cast<int>(floor(fmin(fmax(fhi, Real(0)), top)));
+  const int lo = st[blo];
+  const int cnt = st[bhi + 1] - lo;
   const int rounds = __reduce_max_sync(kFull, cnt);
   bool hit = false;
   for (int j = 0; j < rounds; ++j) {
@@ -485,28 +497,23 @@ __device__ __forceinline__ Key load_rec_cg(const Rec* src) {
   return Key{__ldcg(&src->cls), __ldcg(&src->cand), __ldcg(&src->k1), __ldcg(&src->k2)};
 }
 
-// Shared-memory image of the sorted field: [xs (H+1)N][pad 16][pts (H+1)N].
+// Shared-memory image of the bucketed field: [pts (H+1)N][starts (H+1)(B+1)].
 template <typename Real>
 __device__ __forceinline__ Field<Real> stage_field(const RoundArgs& a, unsigned char* smem) {
   using R2 = typename Vec2T<Real>::type;
-  const int N = a.n_points;
+  const int N = a.n_points, B = a.n_buckets;
   const size_t count = static_cast<size_t>(a.H + 1) * N;
-  const Real* gxs = static_cast<const Real*>(a.field);
-  const size_t pts_off = (count * sizeof(Real) + 15) & ~size_t(15);
-  const R2* gpts =
-      reinterpret_cast<const R2*>(static_cast<const unsigned char*>(a.field) + pts_off);
-  int top = 1;
-  while (top * 2 <= N) top *= 2;
-  Field<Real> f{gxs, gpts, N, N > 0 ? top : 0};
+  const size_t nst = static_cast<size_t>(a.H + 1) * (B + 1);
+  const R2* gpts = static_cast<const R2*>(a.field);
+  const int* gst = reinterpret_cast<const int*>(gpts + count);
+  Field<Real> f{gpts, gst, N, B};
   if (a.field_smem_bytes > 0 && N > 0) {
-    Real* sxs = reinterpret_cast<Real*>(smem);
-    R2* spts = reinterpret_cast<R2*>(smem + pts_off);
-    for (size_t i = threadIdx.x; i < count; i += blockDim.x) {
-      sxs[i] = gxs[i];
-      spts[i] = gpts[i];
-    }
-    f.xs = sxs;
+    R2* spts = reinterpret_cast<R2*>(smem);
+    int* sst = reinterpret_cast<int*>(spts + count);
+    for (size_t i = threadIdx.x; i < count; i += blockDim.x) spts[i] = gpts[i];
+    for (size_t i = threadIdx.x; i < nst; i += blockDim.x) sst[i] = gst[i];
     f.pts = spts;
+    f.starts = sst;
   }
   __syncthreads();
   return f;
