@@ -17,7 +17,14 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
+#include <condition_variable>
+#include <functional>
+#include <mutex>
+#include <thread>
+#include <unordered_map>
 #include <chrono>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <exception>
@@ -146,6 +153,65 @@ struct Key {
   double k1 = 0.0, k2 = 0.0;
 };
 
+// Fork-join pool for the host's exact re-evaluation of near-tie candidates.
+class HostPool {
+ public:
+  explicit HostPool(int n) {
+    for (int i = 1; i < n; ++i) workers_.emplace_back([this, i] { loop(i); });
+  }
+  ~HostPool() {
+    {
+      std::lock_guard<std::mutex> lock(mu_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    for (auto& w : workers_) w.join();
+  }
+  int size() const { return static_cast<int>(workers_.size()) + 1; }
+  // fn(i) for i in [0, n), spread over the workers and the caller.
+  void run(int n, const std::function<void(int)>& fn) {
+    {
+      std::lock_guard<std::mutex> lock(mu_);
+      fn_ = &fn;
+      n_ = n;
+      next_.store(0);
+      pending_ = static_cast<int>(workers_.size());
+      ++gen_;
+    }
+    cv_.notify_all();
+    drain();
+    std::unique_lock<std::mutex> lock(mu_);
+    done_cv_.wait(lock, [this] { return pending_ == 0; });
+  }
+
+ private:
+  void drain() {
+    for (int i; (i = next_.fetch_add(1)) < n_;) (*fn_)(i);
+  }
+  void loop(int) {
+    uint64_t seen = 0;
+    for (;;) {
+      {
+        std::unique_lock<std::mutex> lock(mu_);
+        cv_.wait(lock, [&] { return stop_ || gen_ != seen; });
+        if (stop_) return;
+        seen = gen_;
+      }
+      drain();
+      std::lock_guard<std::mutex> lock(mu_);
+      if (--pending_ == 0) done_cv_.notify_one();
+    }
+  }
+  std::vector<std::thread> workers_;
+  std::mutex mu_;
+  std::condition_variable cv_, done_cv_;
+  const std::function<void(int)>* fn_ = nullptr;
+  std::atomic<int> next_{0};
+  int n_ = 0, pending_ = 0;
+  uint64_t gen_ = 0;
+  bool stop_ = false;
+};
+
 bool key_better(const Key& a, const Key& b) {  // src/planner.cpp:40-44
   if (a.cls != b.cls) return a.cls > b.cls;
   if (a.k1 != b.k1) return a.k1 > b.k1;
@@ -170,8 +236,18 @@ struct pp_handle {
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   DevBuf d_field, d_params, d_result, d_tiles, d_counters, d_samples, d_scratch, d_injected,
-      d_theta;
-  HostBuf h_field, h_params, h_result;
+      d_theta, d_skeys, d_sel, d_bound;
+  HostBuf h_field, h_params, h_result, h_sel, h_bound;
+
+  // near-tie re-ranking (PlannerConfig::refine): needs the host snapshot
+  bool rerank = true;
+  const pp_snapshot* snapshot = nullptr;  // -> snap_copy once a snapshot is resident
+  pp_snapshot snap_copy{};
+  std::vector<double> snap_field, snap_warm;
+  uint32_t h_selcount = 0;
+  double sel_rho = 1e-3;   // FP32 window: cost <= best * (1 + rho) + 1e-6
+  std::unique_ptr<HostPool> pool;  // exact re-evaluation of near ties
+  double dmarg32 = 2e-5;   // FP32 margin below which a worse-side verdict may flip
 
   // resident snapshot
   bool snap_valid = false;
@@ -223,6 +299,8 @@ void fill_consts(const ppdev::RoundArgs& a, ppdev::ConstsT<Real>* k) {
   k->bx0 = Real(a.bucket_x0);
   k->binv = Real(1.0 / a.bucket_w);
   k->qpad = Real(cull + a.bucket_w / 8.0);
+  // a discrete verdict whose margin is below this may flip under rounding
+  k->dmarg = sizeof(Real) == sizeof(float) ? Real(a.dmarg32) : Real(1e-9);
 }
 
 // Goal transform and constants of a snapshot (src/planner.cpp:70-81).
@@ -305,12 +383,18 @@ void upload_snapshot(pp_handle* h, const pp_snapshot& s) {
   a.bucket_x0 = xmin;
   a.bucket_w = width;
   const size_t pts_bytes = 2 * count * elem;
-  const size_t bytes = pts_bytes + rows * (B + 1) * sizeof(int32_t);
+  // padded to 16 bytes so the FP64 image after it is double2-aligned
+  const size_t bytes = (pts_bytes + rows * (B + 1) * sizeof(int32_t) + 15) & ~size_t(15);
+  // FP32 rounds also get an FP64 image for the near-tie re-ranking
+  const size_t pts64_bytes = 2 * count * sizeof(double);
+  const size_t bytes64 = h->fp64 ? 0 : pts64_bytes + rows * (B + 1) * sizeof(int32_t);
   if (count > 0) {
-    h->h_field.reserve(bytes, "pinned field");
-    h->d_field.reserve(bytes, "device field");
+    h->h_field.reserve(bytes + bytes64, "pinned field");
+    h->d_field.reserve(bytes + bytes64, "device field");
     unsigned char* base = static_cast<unsigned char*>(h->h_field.p);
     int32_t* starts = reinterpret_cast<int32_t*>(base + pts_bytes);
+    unsigned char* base64 = base + bytes;
+    int32_t* starts64 = reinterpret_cast<int32_t*>(base64 + pts64_bytes);
     std::vector<int32_t> order(N), bucket(N);
     for (size_t row = 0; row < rows; ++row) {
       const double* src = s.field_xy + 2 * row * N;
@@ -327,6 +411,7 @@ void upload_snapshot(pp_handle* h, const pp_snapshot& s) {
         while (next < N && bucket[order[next]] < b) ++next;
         st[b] = next;
       }
+      if (bytes64 > 0) std::memcpy(starts64 + row * (B + 1), st, sizeof(int32_t) * (B + 1));
       const size_t o = row * N;
       for (int j = 0; j < N; ++j) {
         const double px = src[2 * order[j]], py = src[2 * order[j] + 1];
@@ -338,16 +423,30 @@ void upload_snapshot(pp_handle* h, const pp_snapshot& s) {
           float* pts = reinterpret_cast<float*>(base) + 2 * (o + j);
           pts[0] = static_cast<float>(px);
           pts[1] = static_cast<float>(py);
+          double* p64 = reinterpret_cast<double*>(base64) + 2 * (o + j);
+          p64[0] = px;
+          p64[1] = py;
         }
       }
     }
-    ck(cudaMemcpyAsync(h->d_field.p, h->h_field.p, bytes, cudaMemcpyHostToDevice, h->stream),
+    ck(cudaMemcpyAsync(h->d_field.p, h->h_field.p, bytes + bytes64, cudaMemcpyHostToDevice,
+                       h->stream),
        "field H2D");
-    h->timing.h2d_bytes += static_cast<int64_t>(bytes);
+    h->timing.h2d_bytes += static_cast<int64_t>(bytes + bytes64);
   }
+  a.dmarg32 = h->dmarg32;
   fill_consts(a, &a.kf);
   fill_consts(a, &a.kd);
   a.field = h->d_field.p;
+  a.field64 = h->fp64 ? h->d_field.p : static_cast<unsigned char*>(h->d_field.p) + bytes;
+  // host copy for the exact re-ranking of FP64 near-ties (rows 0..H)
+  h->snap_field.assign(s.field_xy, s.field_xy + 2 * count);
+  h->snap_warm.assign(s.warm_theta, s.warm_theta + std::max(0, s.warm_theta_len));
+  h->snap_copy = s;
+  h->snap_copy.field_xy = h->snap_field.data();
+  h->snap_copy.field_H = cfg.H;
+  h->snap_copy.warm_theta = h->snap_warm.data();
+  h->snapshot = &h->snap_copy;
   // stage the field in shared memory when it fits; larger fields are read
   // through L1/L2
   h->field_smem_bytes = (count > 0 && bytes <= 40 * 1024) ? static_cast<int>(bytes) : 0;
@@ -375,16 +474,37 @@ uint64_t key_prefix(uint64_t seed, uint64_t t, uint64_t r, uint64_t i) {
 
 constexpr int ppdev_warps() { return 4; }  // warps per CTA (rollout.cuh kBlock / 32)
 
+void host_rollout(const pp_handle* h, const pp_snapshot& s, const double* theta,
+                  pp_rollout_stats* out, double* traj, int32_t cap, int32_t* traj_len);
+void host_sample(const pp_handle* h, const double* center, uint64_t t, int restart, int iter,
+                 int cand, double* out, int len = -1);
+
+void certify_round(pp_handle* h, ppdev::RoundArgs& a, uint64_t t, int iter, int r0, int rc,
+                   const double* center, int64_t c0, int64_t c1, const double* injected,
+                   pp_record* out, bool fp64, uint32_t n_sel);
+
+constexpr int kSelCap = 1 << 16;    // near-tie candidates re-ranked per launch
+constexpr int kSelFirst = 512;      // copied back with the round result
+constexpr int kHostMax = 96;        // windows up to this size are re-evaluated on the host
+constexpr int kRefineGrid = 148 * 2;
+
 // One sampling round on the device: restarts [r0, r0+rc), candidates
 // [c0, c1) of each, iteration `iter`, centred on `center` (or injected theta).
+// With re-ranking on, the round is followed by the near-tie window select,
+// the FP64 re-evaluation of the window and a host re-rank of FP64 near-ties
+// in the reference's own arithmetic, so the winner is the reference's.
 void run_round_launch(pp_handle* h, uint64_t t, int iter, int r0, int rc, const double* center,
                       int64_t c0, int64_t c1, const double* injected, pp_record* out,
-                      pp_rollout_stats* per_sample) {
+                      pp_rollout_stats* per_sample, bool force_fp64 = false) {
   const int64_t count = c1 - c0;
+  const bool fp64 = h->fp64 || force_fp64;
+  const bool rerank = h->rerank && h->snapshot != nullptr;
   ppdev::RoundArgs a = h->base;
+  if (force_fp64 && !h->fp64) a.field = a.field64;
   ppdev::LaunchShape shape{};
-  const int rcode = h->fp64 ? ppdev::shape_f64(h->kind, h->device, h->field_smem_bytes, &shape)
-                            : ppdev::shape_f32(h->kind, h->device, h->field_smem_bytes, &shape);
+  const int field_smem = (force_fp64 && !h->fp64) ? 0 : h->field_smem_bytes;
+  const int rcode = fp64 ? ppdev::shape_f64(h->kind, h->device, field_smem, &shape)
+                         : ppdev::shape_f32(h->kind, h->device, field_smem, &shape);
   ck(static_cast<cudaError_t>(rcode), "occupancy query");
   // refill: 32-candidate batches; lockstep: one tile of `block` candidates
   const int unit = shape.refill ? 32 : shape.block;
@@ -399,8 +519,8 @@ void run_round_launch(pp_handle* h, uint64_t t, int iter, int r0, int rc, const 
   a.grid = std::max(1, std::min(shape.grid, shape.refill ? (a.n_tiles + ppdev_warps() - 1) /
                                                                ppdev_warps()
                                                          : a.n_tiles));
-  a.field_smem_bytes = h->field_smem_bytes;
-  a.queue_bytes = shape.queue_bytes;
+  a.field_smem_bytes = field_smem;
+  a.queue_bytes = 0;
 
   // params block: [prefix u64 x rc][center f64 x P]
   const size_t pbytes = sizeof(uint64_t) * rc + sizeof(double) * h->P;
@@ -435,40 +555,77 @@ void run_round_launch(pp_handle* h, uint64_t t, int iter, int r0, int rc, const 
   const size_t n_recs = shape.refill ? static_cast<size_t>(rc) * a.grid : a.n_tiles;
   h->d_tiles.reserve(sizeof(ppdev::Rec) * n_recs, "tile records");
   a.tile_recs = static_cast<ppdev::Rec*>(h->d_tiles.p);
-  const size_t rbytes = 32 + sizeof(ppdev::Rec) * rc;
-  if (h->d_result.reserve(rbytes, "result block")) {
-    ck(cudaMemsetAsync(h->d_result.p, 0, rbytes, h->stream), "result block");
+  // result block: [exec u64 x 4][pad 8][Rec x rc]
+  const size_t rec_off = 40;
+  const size_t rbytes = rec_off + sizeof(ppdev::Rec) * rc;
+  if (h->d_result.reserve(std::max<size_t>(rbytes, 4096), "result block")) {
+    ck(cudaMemsetAsync(h->d_result.p, 0, std::max<size_t>(rbytes, 4096), h->stream),
+       "result block");
   }
-  h->h_result.reserve(rbytes, "pinned result");
-  a.exec = static_cast<unsigned long long*>(h->d_result.p);
-  a.out = reinterpret_cast<ppdev::Rec*>(static_cast<char*>(h->d_result.p) + 32);
+  h->h_result.reserve(std::max<size_t>(rbytes, 4096), "pinned result");
+  char* dres = static_cast<char*>(h->d_result.p);
+  a.exec = reinterpret_cast<unsigned long long*>(dres);
+  a.out = reinterpret_cast<ppdev::Rec*>(dres + rec_off);
   a.counters = static_cast<uint32_t*>(h->d_counters.p);
   if (per_sample != nullptr) {
     h->d_samples.reserve(sizeof(ppdev::SampleOut) * rc * static_cast<size_t>(count),
                          "per-sample buffer");
     a.per_sample = static_cast<ppdev::SampleOut*>(h->d_samples.p);
   }
+  const size_t total = static_cast<size_t>(count) * rc;
   if (shape.refill) {
-    const size_t total = static_cast<size_t>(count) * rc;
-    const size_t esz = h->fp64 ? sizeof(double) : sizeof(float);
+    const size_t esz = fp64 ? sizeof(double) : sizeof(float);
     h->d_theta.reserve(total * shape.theta_elem * esz, "theta buffer");
     a.theta_buf = h->d_theta.p;
     a.first_buf = static_cast<char*>(h->d_theta.p) + total * (shape.theta_elem - 2) * esz;
   }
-  if (h->kind == ppdev::NetKind::kGeneric) {
-    const size_t elems = static_cast<size_t>(h->P) * a.grid * a.block;
-    h->d_scratch.reserve(elems * (h->fp64 ? sizeof(double) : sizeof(float)), "theta scratch");
+  const bool generic = h->kind == ppdev::NetKind::kGeneric;
+  if (generic || rerank) {
+    const size_t lanes = std::max<size_t>(generic ? static_cast<size_t>(a.grid) * a.block : 0,
+                                          rerank ? kRefineGrid * 128 : 0);
+    h->d_scratch.reserve(lanes * h->P * sizeof(double), "theta scratch");
     a.theta_scratch = static_cast<float*>(h->d_scratch.p);
     a.theta_scratch64 = static_cast<double*>(h->d_scratch.p);
   }
+  if (rerank) {
+    h->d_skeys.reserve(total * sizeof(ppdev::SKey), "sample keys");
+    h->d_sel.reserve(kSelCap * (sizeof(int64_t) + sizeof(ppdev::SelRec)), "selection");
+    h->h_sel.reserve(kSelCap * std::max(sizeof(ppdev::SelRec), sizeof(int64_t)),
+                     "pinned selection");
+    a.skeys = static_cast<ppdev::SKey*>(h->d_skeys.p);
+    a.sel_out = static_cast<ppdev::SelRec*>(h->d_sel.p);
+    a.sel_list = reinterpret_cast<int64_t*>(a.sel_out + kSelCap);
+    a.sel_cap = kSelCap;
+    a.refine_grid = kRefineGrid;
+    a.sel_rho = fp64 ? 1e-11 : h->sel_rho;
+    a.sel_alpha = fp64 ? 1e-13 : 1e-6;
+    a.counters = static_cast<uint32_t*>(h->d_counters.p);
+  }
 
   ck(cudaEventRecord(h->ev0, h->stream), "event");
-  const int lcode = h->fp64 ? ppdev::launch_round_f64(h->kind, a, h->stream)
-                            : ppdev::launch_round_f32(h->kind, a, h->stream);
+  const int lcode = fp64 ? ppdev::launch_round_f64(h->kind, a, h->stream)
+                         : ppdev::launch_round_f32(h->kind, a, h->stream);
   ck(static_cast<cudaError_t>(lcode), "sampling kernel launch");
+  if (rerank) {
+    ck(cudaMemsetAsync(reinterpret_cast<uint32_t*>(h->d_counters.p) + 2, 0, sizeof(uint32_t),
+                       h->stream),
+       "selection counter");
+    ck(static_cast<cudaError_t>(ppdev::launch_select(a, h->stream)), "window select launch");
+  }
   ck(cudaEventRecord(h->ev1, h->stream), "event");
   ck(cudaMemcpyAsync(h->h_result.p, h->d_result.p, rbytes, cudaMemcpyDeviceToHost, h->stream),
      "result D2H");
+  uint32_t n_sel = 0;
+  if (rerank) {
+    ck(cudaMemcpyAsync(&h->h_selcount, reinterpret_cast<uint32_t*>(h->d_counters.p) + 2,
+                       sizeof(uint32_t), cudaMemcpyDeviceToHost, h->stream),
+       "selection D2H");
+    // the first kSelFirst selected indices ride along with the result
+    ck(cudaMemcpyAsync(h->h_sel.p, a.sel_list, sizeof(int64_t) * kSelFirst,
+                       cudaMemcpyDeviceToHost, h->stream),
+       "selection D2H");
+    h->timing.d2h_bytes += sizeof(int64_t) * kSelFirst + sizeof(uint32_t);
+  }
   h->timing.d2h_bytes += static_cast<int64_t>(rbytes);
   if (per_sample != nullptr) {
     const size_t sb = sizeof(ppdev::SampleOut) * rc * static_cast<size_t>(count);
@@ -480,13 +637,13 @@ void run_round_launch(pp_handle* h, uint64_t t, int iter, int r0, int rc, const 
   float ms = 0.f;
   ck(cudaEventElapsedTime(&ms, h->ev0, h->ev1), "event timing");
   h->timing.kernel_ms += ms;
-  h->timing.launches += shape.refill ? 2 : 1;
+  h->timing.launches += (shape.refill ? 2 : 1) + (rerank ? 1 : 0);
   h->timing.samples += count * rc;
   const unsigned long long* ex = static_cast<const unsigned long long*>(h->h_result.p);
   h->timing.executed_steps += static_cast<int64_t>(ex[2]);
   h->timing.checked_states += static_cast<int64_t>(ex[3]);
-  const ppdev::Rec* recs =
-      reinterpret_cast<const ppdev::Rec*>(static_cast<const char*>(h->h_result.p) + 32);
+  const char* hres = static_cast<const char*>(h->h_result.p);
+  const ppdev::Rec* recs = reinterpret_cast<const ppdev::Rec*>(hres + rec_off);
   for (int r = 0; r < rc; ++r) {
     out[r].cls = recs[r].cls;
     out[r].candidate = recs[r].cand;
@@ -495,6 +652,197 @@ void run_round_launch(pp_handle* h, uint64_t t, int iter, int r0, int rc, const 
     out[r].k1 = recs[r].k1;
     out[r].k2 = recs[r].k2;
   }
+  if (!rerank) return;
+
+  n_sel = h->h_selcount;
+  certify_round(h, a, t, iter, r0, rc, center, c0, c1, injected, out, fp64, n_sel);
+}
+
+// Certified re-ranking (PlannerConfig::refine). The FP32 keys are trusted
+// only up to a relative error rho/2 (+ alpha/2), and discrete verdicts that
+// rounding could flip toward a BETTER outcome are flagged by the kernel and
+// always selected; flips toward a worse outcome only hurt the candidate
+// itself. Each pass evaluates the window's new members in the reference's
+// own FP64 arithmetic on the host (the device FP64 kernel first when the
+// window is wide) and certifies a restart when its exact best beats every
+// unselected candidate's optimistic bound; otherwise the window widens.
+// Windows that overflow, or restarts still uncertified after the last pass,
+// are redone as an FP64 round.
+void certify_round(pp_handle* h, ppdev::RoundArgs& a, uint64_t t, int iter, int r0, int rc,
+                   const double* center, int64_t c0, int64_t c1, const double* injected,
+                   pp_record* out, bool fp64, uint32_t n_sel) {
+  const int64_t count = c1 - c0;
+  const pp_snapshot& snap = *h->snapshot;
+  std::vector<double> ctr(h->P, 0.0);
+  if (center != nullptr) ctr.assign(center, center + h->P);
+  struct Exact {
+    int cls;
+    int t_goal;
+    double cost;  // terminal cost (cls 0/1) or path length (cls 2)
+    double k1, k2;
+  };
+  std::unordered_map<int64_t, Exact> known;
+  auto exact_of = [&](int64_t s) {  // the reference's own FP64 arithmetic
+    const int r = static_cast<int>(s / count);
+    const int cand = static_cast<int>(c0 + (s - r * count));
+    std::vector<double> theta(h->P);
+    if (injected != nullptr) {
+      std::memcpy(theta.data(), injected + static_cast<size_t>(cand - c0) * h->P,
+                  sizeof(double) * h->P);
+    } else {
+      host_sample(h, ctr.data(), t, r0 + r, iter, cand, theta.data(), -1);
+    }
+    pp_rollout_stats st{};
+    host_rollout(h, snap, theta.data(), &st, nullptr, 0, nullptr);
+    Exact e;
+    e.cls = st.collided ? 0 : (st.reached ? 2 : 1);
+    e.t_goal = st.t_goal;
+    e.cost = e.cls == 2 ? st.path_length : st.terminal_cost;
+    e.k1 = e.cls == 2 ? -static_cast<double>(st.t_goal) : -st.terminal_cost;
+    e.k2 = e.cls == 2 ? -st.path_length : 0.0;
+    return e;
+  };
+  if (!h->pool) {
+    const unsigned hc = std::thread::hardware_concurrency();
+    h->pool = std::make_unique<HostPool>(static_cast<int>(std::min(16u, std::max(1u, hc))));
+  }
+  const double rho = a.sel_rho, alpha = a.sel_alpha;
+  std::vector<ppdev::SelBound> bound(rc);
+  for (int r = 0; r < rc; ++r) {
+    bound[r].cls = out[r].cls;
+    bound[r].t_goal = out[r].cls == 2 ? static_cast<int>(-out[r].k1) : 0;
+    bound[r].thr = (out[r].cls == 2 ? -out[r].k2 : -out[r].k1) * (1.0 + rho) + alpha;
+  }
+  std::vector<char> certified(rc, 0);
+  std::vector<int64_t> list;
+  constexpr int kPasses = 6;
+  for (int pass = 0; pass < kPasses; ++pass) {
+    if (pass > 0) {  // widened select over the uncertified restarts
+      h->d_bound.reserve(sizeof(ppdev::SelBound) * rc, "window bounds");
+      h->h_bound.reserve(sizeof(ppdev::SelBound) * rc, "pinned bounds");
+      std::memcpy(h->h_bound.p, bound.data(), sizeof(ppdev::SelBound) * rc);
+      ck(cudaMemcpyAsync(h->d_bound.p, h->h_bound.p, sizeof(ppdev::SelBound) * rc,
+                         cudaMemcpyHostToDevice, h->stream),
+         "bounds H2D");
+      a.sel_bound = static_cast<const ppdev::SelBound*>(h->d_bound.p);
+      ck(cudaMemsetAsync(reinterpret_cast<uint32_t*>(h->d_counters.p) + 2, 0, sizeof(uint32_t),
+                         h->stream),
+         "selection counter");
+      ck(static_cast<cudaError_t>(ppdev::launch_select(a, h->stream)), "window select launch");
+      ck(cudaMemcpyAsync(&h->h_selcount, reinterpret_cast<uint32_t*>(h->d_counters.p) + 2,
+                         sizeof(uint32_t), cudaMemcpyDeviceToHost, h->stream),
+         "selection D2H");
+      ck(cudaMemcpyAsync(h->h_sel.p, a.sel_list, sizeof(int64_t) * kSelFirst,
+                         cudaMemcpyDeviceToHost, h->stream),
+         "selection D2H");
+      ck(cudaStreamSynchronize(h->stream), "window select");
+      h->timing.launches += 1;
+      n_sel = h->h_selcount;
+    }
+    if (n_sel > static_cast<uint32_t>(kSelCap)) break;
+    if (n_sel > static_cast<uint32_t>(kSelFirst)) {
+      ck(cudaMemcpy(static_cast<int64_t*>(h->h_sel.p) + kSelFirst, a.sel_list + kSelFirst,
+                    sizeof(int64_t) * (n_sel - kSelFirst), cudaMemcpyDeviceToHost),
+         "selection D2H");
+    }
+    const int64_t* sl = static_cast<const int64_t*>(h->h_sel.p);
+    list.clear();
+    for (uint32_t i = 0; i < n_sel; ++i) {
+      if (known.find(sl[i]) == known.end()) list.push_back(sl[i]);
+    }
+    std::sort(list.begin(), list.end());
+    list.erase(std::unique(list.begin(), list.end()), list.end());
+    h->timing.refined += static_cast<int32_t>(list.size());
+    std::vector<Exact> got(list.size());
+    if (list.size() <= static_cast<size_t>(kHostMax)) {
+      h->pool->run(static_cast<int>(list.size()), [&](int i) { got[i] = exact_of(list[i]); });
+    } else {
+      // wide window: FP64 keys from the device, exact host keys for the FP64
+      // near-ties of each restart's best
+      ck(cudaMemcpyAsync(a.sel_list, list.data(), sizeof(int64_t) * list.size(),
+                         cudaMemcpyHostToDevice, h->stream),
+         "refine list H2D");
+      const uint32_t n_list = static_cast<uint32_t>(list.size());
+      ck(cudaMemcpyAsync(reinterpret_cast<uint32_t*>(h->d_counters.p) + 2, &n_list,
+                         sizeof(uint32_t), cudaMemcpyHostToDevice, h->stream),
+         "refine count H2D");
+      ck(static_cast<cudaError_t>(ppdev::launch_refine(h->kind, a, h->stream)), "refine launch");
+      std::vector<ppdev::SelRec> dev(list.size());
+      ck(cudaMemcpyAsync(dev.data(), a.sel_out, sizeof(ppdev::SelRec) * list.size(),
+                         cudaMemcpyDeviceToHost, h->stream),
+         "refine D2H");
+      ck(cudaStreamSynchronize(h->stream), "refine kernel");
+      h->timing.launches += 1;
+      std::vector<int> best(rc, -1);
+      for (size_t i = 0; i < dev.size(); ++i) {
+        got[i] = Exact{dev[i].cls, dev[i].cls == 2 ? static_cast<int>(-dev[i].k1) : -1,
+                       dev[i].cls == 2 ? -dev[i].k2 : -dev[i].k1, dev[i].k1, dev[i].k2};
+        const int r = dev[i].restart;
+        if (best[r] < 0 || key_better({got[i].cls, got[i].k1, got[i].k2},
+                                      {got[best[r]].cls, got[best[r]].k1, got[best[r]].k2})) {
+          best[r] = static_cast<int>(i);
+        }
+      }
+      std::vector<int> ties;
+      for (size_t i = 0; i < dev.size(); ++i) {
+        const Exact& b = got[best[dev[i].restart]];
+        const double tol = 1e-12;
+        if (got[i].cls == b.cls && std::abs(got[i].k1 - b.k1) <= tol * std::max(1.0, std::abs(b.k1)) &&
+            std::abs(got[i].k2 - b.k2) <= tol * std::max(1.0, std::abs(b.k2))) {
+          ties.push_back(static_cast<int>(i));
+        }
+      }
+      h->pool->run(static_cast<int>(ties.size()),
+                   [&](int j) { got[ties[j]] = exact_of(list[ties[j]]); });
+    }
+    for (size_t i = 0; i < list.size(); ++i) known[list[i]] = got[i];
+
+    // certify or widen each uncertified restart
+    bool all = true;
+    for (int r = 0; r < rc; ++r) {
+      if (certified[r]) continue;
+      const ppdev::SelBound& bd = bound[r];
+      int64_t win = -1;
+      const Exact* e = nullptr;
+      for (const auto& kv : known) {
+        if (kv.first / count != r) continue;
+        const Exact& q = kv.second;
+        if (e == nullptr || key_better({q.cls, q.k1, q.k2}, {e->cls, e->k1, e->k2}) ||
+            (q.cls == e->cls && q.k1 == e->k1 && q.k2 == e->k2 && kv.first < win)) {
+          e = &q;
+          win = kv.first;
+        }
+      }
+      const double slack = 0.5 * (rho * bd.thr + alpha);
+      bool ok = false;
+      if (e != nullptr) {
+        if (e->cls > bd.cls) {
+          ok = true;  // only a flagged (always selected) candidate can rise a class
+        } else if (e->cls == bd.cls) {
+          ok = (bd.cls == 2 && e->t_goal < bd.t_goal) ||
+               ((bd.cls != 2 || e->t_goal == bd.t_goal) && e->cost <= bd.thr - slack);
+        }
+      }
+      if (ok) {
+        certified[r] = 1;
+        out[r].cls = e->cls;
+        out[r].candidate = static_cast<int>(c0 + (win - r * count));
+        out[r].k1 = e->k1;
+        out[r].k2 = e->k2;
+        bound[r].cls = -1;  // select nothing more for this restart
+        continue;
+      }
+      all = false;
+      const bool same = e != nullptr && e->cls == bd.cls && (bd.cls != 2 || e->t_goal == bd.t_goal);
+      const double widened = bd.thr * 1.25 + alpha;
+      bound[r].thr = same ? std::max(e->cost * (1.0 + rho) + alpha, widened) : widened;
+    }
+    if (all) return;
+  }
+  // overflowed or not certified: redo the round in FP64
+  if (fp64) throw std::runtime_error("near-tie re-ranking could not certify an FP64 round");
+  h->timing.refined = -1;
+  run_round_launch(h, t, iter, r0, rc, center, c0, c1, injected, out, nullptr, true);
 }
 
 void run_round(pp_handle* h, uint64_t t, int iter, int r0, int rc, const double* center,
@@ -510,14 +858,6 @@ void run_round(pp_handle* h, uint64_t t, int iter, int r0, int rc, const double*
   }
 }
 
-paraplan::PlanningSnapshot to_snapshot(const pp_snapshot& s) {
-  paraplan::PlanningSnapshot snap;
-  snap.ev_state = {s.ev_x, s.ev_y, s.ev_phi, s.ev_v};
-  snap.actuator.delta = s.actuator_delta;
-  snap.prev_action = {s.prev_a0, s.prev_a1};
-  snap.goal = {s.goal_x, s.goal_y, s.goal_phi, s.goal_v};
-  return snap;
-}
 
 // Host FP64 rollout: src/planner.cpp:66-191 expressed through the public
 // primitives (bit-identical under -ffp-contract=off; the reference's own
@@ -597,7 +937,7 @@ void host_rollout(const pp_handle* h, const pp_snapshot& s, const double* theta,
 }
 
 void host_sample(const pp_handle* h, const double* center, uint64_t t, int restart, int iter,
-                 int cand, double* out, int len = -1) {
+                 int cand, double* out, int len) {
   if (len < 0) len = h->P;
   if (cand == 0) {
     std::memcpy(out, center, sizeof(double) * len);
@@ -652,6 +992,9 @@ pp_status pp_create(const pp_model* m, pp_handle** out) {
     hp->P = hp->policy->param_count();
     hp->kind = ppdev::classify(hp->sizes.data(), static_cast<int32_t>(hp->sizes.size()));
     hp->fp64 = hp->cfg.precision == 64;
+    hp->rerank = hp->cfg.refine;
+    if (const char* e = std::getenv("PARAPLAN_SEL_RHO")) hp->sel_rho = std::atof(e);
+    if (const char* e = std::getenv("PARAPLAN_DMARG")) hp->dmarg32 = std::atof(e);
     hp->device = hp->cfg.device;
 
     int n = 0;
@@ -686,10 +1029,13 @@ void pp_destroy(pp_handle* h) {
   cudaSetDevice(h->device);
   if (h->stream != nullptr) cudaStreamSynchronize(h->stream);
   for (DevBuf* b : {&h->d_field, &h->d_params, &h->d_result, &h->d_tiles, &h->d_counters,
-                    &h->d_samples, &h->d_scratch, &h->d_injected, &h->d_theta}) {
+                    &h->d_samples, &h->d_scratch, &h->d_injected, &h->d_theta, &h->d_skeys,
+                    &h->d_sel, &h->d_bound}) {
     b->release();
   }
-  for (HostBuf* b : {&h->h_field, &h->h_params, &h->h_result}) b->release();
+  for (HostBuf* b : {&h->h_field, &h->h_params, &h->h_result, &h->h_sel, &h->h_bound}) {
+    b->release();
+  }
   if (h->ev0 != nullptr) cudaEventDestroy(h->ev0);
   if (h->ev1 != nullptr) cudaEventDestroy(h->ev1);
   if (h->stream != nullptr) cudaStreamDestroy(h->stream);

@@ -16,6 +16,26 @@ struct SampleOut {
   double path_length, terminal_cost, first_a0, first_a1;
 };
 
+// Compact per-sample key for the near-tie window (16 bytes).
+struct SKey {
+  double cost;    // terminal cost (cls 0/1) or path length (cls 2)
+  uint32_t meta;  // cls | marginal << 2 | t_goal << 8
+  uint32_t pad;
+};
+
+// Window of one restart for a widened select pass: class, t_goal (class 2)
+// and cost threshold; cls = -1 selects nothing (restart certified).
+struct SelBound {
+  int32_t cls, t_goal;
+  double thr;
+};
+
+// FP64 re-evaluated key of a selected candidate.
+struct SelRec {
+  int32_t cls, cand, restart, pad;
+  double k1, k2;
+};
+
 // Winner of a tile / of a restart segment. cls = -1 marks "no candidate".
 struct Rec {
   int32_t cls;
@@ -38,6 +58,7 @@ struct ConstsT {
   Real cull;            // collision x-window half width: bounding radius + 1e-3
   Real bx0, binv;       // x-bucket grid of the field: origin, 1 / bucket width
   Real qpad;            // bucket query half width: cull + bucket width / 8
+  Real dmarg;           // |margin| below which a discrete verdict is "marginal"
 };
 
 // Everything one sampling round needs. Scalars are FP64 here; the FP32
@@ -91,6 +112,16 @@ struct RoundArgs {
   int32_t queue_bytes;         // unused (0)
   void* theta_buf;             // refill schedule: [P][total] theta in Real
   void* first_buf;             // refill schedule: [2][total] first action in Real
+  // near-tie re-ranking (null skeys = off)
+  SKey* skeys;                 // [restart_count * count]
+  const void* field64;         // FP64 image of the field (same layout as `field`)
+  int64_t* sel_list;           // [sel_cap] selected flat indices
+  SelRec* sel_out;             // [sel_cap] their FP64 keys
+  int32_t sel_cap;
+  int32_t refine_grid;
+  double sel_rho, sel_alpha;   // window: cost <= best * (1 + rho) + alpha
+  const SelBound* sel_bound;   // null: first pass (window around a.out)
+  double dmarg32;              // FP32 marginal threshold (host side, copied into kf)
 };
 
 // Architecture dispatch of the specialised kernels.
@@ -112,6 +143,12 @@ int shape_f64(NetKind k, int device, int field_bytes, LaunchShape* out);
 // Enqueue one sampling round on `stream`. Returns 0 or a cudaError_t.
 int launch_round_f32(NetKind k, const RoundArgs& a, void* stream);
 int launch_round_f64(NetKind k, const RoundArgs& a, void* stream);
+
+// Near-tie window after a round: counters[2] receives the number of selected
+// candidates, sel_list their flat indices.
+int launch_select(const RoundArgs& a, void* stream);
+// FP64 re-evaluation of the selected candidates into sel_out.
+int launch_refine(NetKind k, const RoundArgs& a, void* stream);
 
 // FFMA throughput probe (the FP32 roofline denominator).
 int measure_ffma(int device, double* tflops, double* sm_mhz);

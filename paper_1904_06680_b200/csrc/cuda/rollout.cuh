@@ -37,6 +37,7 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
@@ -285,9 +286,13 @@ struct Field {
 // [x - qpad, x + qpad] are visited; every point outside them has
 // |px - x| > cull > r and fails the prefilter. Warp-synchronous: all 32
 // lanes call it and the candidate loop has a warp-uniform trip count.
+// Returns the inside-margin m = max over points of min(r2 - d2, fe - bx,
+// re + bx, hw - by, hw + by): the reference reports a collision iff m > 0
+// (each difference has the exact sign of the reference's comparison), and
+// |m| small marks a verdict rounding could flip.
 template <typename Real>
-__device__ __forceinline__ bool collides(const Field<Real>& f, const Consts<Real>& K, int h,
-                                         Real x, Real y, Real c, Real s) {
+__device__ __forceinline__ Real collide_margin(const Field<Real>& f, const Consts<Real>& K, int h,
+                                               Real x, Real y, Real c, Real s) {
   const int B = f.B;
   const int* st = f.starts + static_cast<size_t>(h) * (B + 1);
   const auto* pts = f.pts + static_cast<size_t>(h) * f.N;
@@ -299,18 +304,19 @@ __device__ __forceinline__ bool collides(const Field<Real>& f, const Consts<Real
   const int lo = st[blo];
   const int cnt = st[bhi + 1] - lo;
   const int rounds = __reduce_max_sync(kFull, cnt);
-  bool hit = false;
+  Real best = Real(-1e30);
   for (int j = 0; j < rounds; ++j) {
     if (j < cnt) {
       const auto m = pts[lo + j];
       const Real dx = m.x - x, dy = m.y - y;
       const Real bx = c * dx + s * dy;
       const Real by = -s * dx + c * dy;
-      hit |= (dx * dx + dy * dy < K.r2) & (bx < K.fe) & (-bx < K.re) & (by < K.hw) &
-             (-by < K.hw);
+      const Real pre = K.r2 - (dx * dx + dy * dy);
+      const Real box = fmin(fmin(K.fe - bx, K.re + bx), fmin(K.hw - by, K.hw + by));
+      best = fmax(best, fmin(pre, box));
     }
   }
-  return hit;
+  return best;
 }
 
 // One candidate's rollout state (src/planner.cpp:123-125, 130-132).
@@ -318,6 +324,7 @@ template <typename Real>
 struct Lane {
   Real x, y, phi, v, act, pa0, path, f0, f1, ephi;
   int h;
+  bool marg;  // a worse-side collision / goal verdict came within K.dmarg of flipping
   __device__ __forceinline__ void start(const Consts<Real>& K, Real first0, Real first1) {
     x = y = phi = Real(0);
     v = K.v0;
@@ -327,6 +334,7 @@ struct Lane {
     f0 = first0;
     f1 = first1;
     h = 0;
+    marg = false;
   }
 };
 
@@ -351,11 +359,21 @@ __device__ __forceinline__ int advance(Lane<Real>& L, const Net& net, const Cons
   Real sphi, cphi;
   M<Real>::sc(L.phi, &sphi, &cphi);
   L.ephi = M<Real>::wrap(K.gphi - L.phi);
-  const bool hit = f.N > 0 && collides(f, K, L.h, L.x, L.y, cphi, sphi);
+  bool hit = false;
+  if (f.N > 0) {
+    const Real cm = collide_margin(f, K, L.h, L.x, L.y, cphi, sphi);
+    hit = cm > Real(0);
+    // a narrow hit might be free in exact arithmetic (a better outcome)
+    L.marg |= hit & (cm < K.dmarg);
+  }
   const Real gdx = K.gx - L.x, gdy = K.gy - L.y;
-  const bool reached = (M<Real>::ab(K.gcos * gdx + K.gsin * gdy) <= K.eps_xi) &
-                       (M<Real>::ab(-K.gsin * gdx + K.gcos * gdy) <= K.eps_eta) &
-                       (M<Real>::ab(L.ephi) <= K.eps_phi) & (M<Real>::ab(K.gv - L.v) <= K.eps_v);
+  // inclusive goal box: eps - |err| >= 0 <=> |err| <= eps, exactly
+  const Real gm = fmin(fmin(K.eps_xi - M<Real>::ab(K.gcos * gdx + K.gsin * gdy),
+                            K.eps_eta - M<Real>::ab(-K.gsin * gdx + K.gcos * gdy)),
+                       fmin(K.eps_phi - M<Real>::ab(L.ephi), K.eps_v - M<Real>::ab(K.gv - L.v)));
+  const bool reached = gm >= Real(0);
+  // a narrow miss might reach in exact arithmetic (a better outcome)
+  L.marg |= !reached & (gm > -K.dmarg);
   const int cls = hit ? 0 : (reached ? 2 : (L.h == H ? 1 : -1));
 
   Real s[5];
@@ -517,6 +535,21 @@ __device__ __forceinline__ Field<Real> stage_field(const RoundArgs& a, unsigned 
   }
   __syncthreads();
   return f;
+}
+
+// Compact per-sample key for the near-tie re-ranking (select_kernel):
+// cost = terminal cost (cls 0/1) or path length (cls 2); meta = cls | marg<<2
+// | t_goal<<8.
+template <typename Real>
+__device__ __forceinline__ void write_skey(const RoundArgs& a, int64_t slot, int cls,
+                                           const Lane<Real>& L, Real term) {
+  if (a.skeys == nullptr) return;
+  SKey k;
+  k.cost = static_cast<double>(cls == 2 ? L.path : term);
+  k.meta = static_cast<uint32_t>(cls) | (L.marg ? 4u : 0u) |
+           (static_cast<uint32_t>(cls == 2 ? L.h : 0) << 8);
+  k.pad = 0;
+  a.skeys[slot] = k;
 }
 
 // Per-sample debug/parity record.
@@ -703,6 +736,7 @@ __global__ void __launch_bounds__(kBlock) refill_kernel(const RoundArgs a) {
       if (a.per_sample != nullptr) {
         write_sample(a, static_cast<int64_t>(my_r) * a.count + my_c, cls, L, term);
       }
+      write_skey(a, static_cast<int64_t>(my_r) * a.count + my_c, cls, L, term);
       active = false;
     }
   }
@@ -807,6 +841,7 @@ __global__ void __launch_bounds__(kBlock) lockstep_kernel(const RoundArgs a) {
       if (a.per_sample != nullptr) {
         write_sample(a, static_cast<int64_t>(r) * a.count + local, cls, L, term);
       }
+      write_skey(a, static_cast<int64_t>(r) * a.count + local, cls, L, term);
     }
     const Key best = block_best(key, red);
     // tile records are restart-major: [r][tile within restart]
@@ -819,6 +854,98 @@ __global__ void __launch_bounds__(kBlock) lockstep_kernel(const RoundArgs a) {
     atomicAdd(&a.exec[1], states);
   }
   finish_round(a, a.tile_recs, a.tiles_per_restart, red);
+}
+
+// ------------------------------------------------------ select kernel ----
+// Near-tie window of every restart: candidates of the winner's class whose
+// key lies within (1 + rho) * cost + alpha of the round winner, plus every
+// candidate flagged marginal. Indices are appended to a.sel_list.
+static __global__ void __launch_bounds__(256) select_kernel(const RoundArgs a) {
+  const int64_t total = a.count * a.restart_count;
+  for (int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; s < total;
+       s += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int r = static_cast<int>(s / a.count);
+    SelBound bd;
+    if (a.sel_bound != nullptr) {  // widened window of a later pass
+      bd = a.sel_bound[r];
+    } else {  // first pass: around the round winner
+      const Rec b = a.out[r];
+      bd.cls = b.cls;
+      bd.t_goal = b.cls == 2 ? static_cast<int>(-b.k1) : 0;
+      bd.thr = (b.cls == 2 ? -b.k2 : -b.k1) * (1.0 + a.sel_rho) + a.sel_alpha;
+    }
+    const SKey k = a.skeys[s];
+    const int cls = static_cast<int>(k.meta & 3u);
+    bool take = (k.meta & 4u) != 0u && bd.cls >= 0;
+    if (cls == bd.cls && k.cost <= bd.thr) {
+      take |= cls != 2 || static_cast<int>(k.meta >> 8) == bd.t_goal;
+    }
+    if (take) {
+      const unsigned i = atomicAdd(&a.counters[2], 1u);
+      if (i < static_cast<unsigned>(a.sel_cap)) a.sel_list[i] = s;
+    }
+  }
+}
+
+// ------------------------------------------------------ refine kernel ----
+// FP64 re-evaluation of the selected candidates (theta redrawn in FP64,
+// FP64 field). One lane per candidate, warp-synchronous stepping.
+template <class Net64>
+struct RefineNet;
+template <int H1>
+struct RefineNet<NetReg<double, H1>> {
+  static __device__ __forceinline__ NetReg<double, H1> make(const RoundArgs&) { return {}; }
+};
+template <>
+struct RefineNet<NetGlobal<double>> {
+  static __device__ __forceinline__ NetGlobal<double> make(const RoundArgs& a) {
+    NetGlobal<double> n;
+    n.stride = gridDim.x * blockDim.x;
+    n.col = a.theta_scratch64 + blockIdx.x * blockDim.x + threadIdx.x;
+    n.sizes = a.sizes;
+    n.n_layers = a.n_layers;
+    return n;
+  }
+};
+
+template <class Net64>
+__global__ void __launch_bounds__(128) refine_kernel(const RoundArgs a) {
+  const Consts<double>& K = a.kd;
+  const unsigned n_sel = min(__ldcg(&a.counters[2]), static_cast<unsigned>(a.sel_cap));
+  const Field<double> f{static_cast<const double2*>(a.field64),
+                        reinterpret_cast<const int*>(static_cast<const double2*>(a.field64) +
+                                                     static_cast<size_t>(a.H + 1) * a.n_points),
+                        a.n_points, a.n_buckets};
+  double s0[5];
+  start_features(K, s0);
+  Net64 net = RefineNet<Net64>::make(a);
+  // warp-uniform bound so every lane of a live warp keeps stepping
+  const unsigned stride = gridDim.x * blockDim.x;
+  for (unsigned base = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); base < n_sel;
+       base += stride) {
+    const unsigned i = base + (threadIdx.x & 31u);
+    const bool valid = i < n_sel;
+    const int64_t s = a.sel_list[valid ? i : base];
+    const int r = static_cast<int>(s / a.count);
+    const int64_t local = s - static_cast<int64_t>(r) * a.count;
+    draw_theta<double, Net64::kP>(a, __ldg(a.key_prefix + r),
+                                  a.injected ? local : a.cand_begin + local, a.n_params,
+                                  [&](int j, double v) { net.set(j, v); });
+    double f0, f1;
+    net.eval(s0, f0, f1);
+    Lane<double> L;
+    L.start(K, f0, f1);
+    int cls = -1;
+    while (__any_sync(kFull, cls < 0)) {
+      const int k = advance<double>(L, net, K, f, a.H);
+      if (cls < 0) cls = k;
+    }
+    if (valid) {
+      const double term = terminal_cost(L, K);
+      const Key k = make_key<double>(cls, L.h, L.path, term, static_cast<int>(a.cand_begin + local));
+      a.sel_out[i] = SelRec{k.cls, k.idx, r, 0, k.k1, k.k2};
+    }
+  }
 }
 
 // ------------------------------------------------------------ launch ----
@@ -861,6 +988,21 @@ int launch_impl(const RoundArgs& a, void* stream) {
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   }
   k<<<a.grid, a.block, smem, st>>>(a);
+  return static_cast<int>(cudaGetLastError());
+}
+
+// Near-tie window of a finished round.
+inline int launch_select_impl(const RoundArgs& a, void* stream) {
+  const int64_t total = a.count * a.restart_count;
+  const int blocks = static_cast<int>(std::min<int64_t>((total + 255) / 256, 148 * 16));
+  select_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(a);
+  return static_cast<int>(cudaGetLastError());
+}
+
+// FP64 re-evaluation of the selected window.
+template <class Net64>
+int launch_refine_impl(const RoundArgs& a, void* stream) {
+  refine_kernel<Net64><<<a.refine_grid, 128, 0, static_cast<cudaStream_t>(stream)>>>(a);
   return static_cast<int>(cudaGetLastError());
 }
 

@@ -26,3 +26,21 @@ int launch_round_f64(NetKind k, const RoundArgs& a, void* stream) {
 }
 
 }  // namespace ppdev
+
+namespace ppdev {
+
+// The re-ranking kernels live in the --fmad=false translation unit.
+int launch_select(const RoundArgs& a, void* stream) { return launch_select_impl(a, stream); }
+
+int launch_refine(NetKind k, const RoundArgs& a, void* stream) {
+  switch (k) {
+    case NetKind::k5_2_2:
+      return launch_refine_impl<NetReg<double, 2>>(a, stream);
+    case NetKind::k5_10_2:
+      return launch_refine_impl<NetReg<double, 10>>(a, stream);
+    default:
+      return launch_refine_impl<NetGlobal<double>>(a, stream);
+  }
+}
+
+}  // namespace ppdev

@@ -60,7 +60,7 @@ def test_round_stats_vs_golden(gold, idx, precision):
     g = gold["rounds"][idx]
     snap, H = golden_snapshot(gold, g["snapshot"])
     m = abi.Model(H=H, n_restarts=1, n_candidates=g["n"], master_seed=g["seed"],
-                  precision=precision)
+                  precision=precision, refine=0)
     dp = capi.DevicePlanner(m)
     rec, got = dp.evaluate(snap, g["t"], 0, 0, 1, np.zeros(m.param_count()), 0, g["n"],
                            per_sample=True)
@@ -76,7 +76,7 @@ def test_round_stats_vs_golden(gold, idx, precision):
 def test_round_stats_vs_oracle_all_architectures(sizes, precision):
     w = workloads.c2(samples=4096)
     m = abi.Model(layer_sizes=sizes, H=30, n_restarts=2, n_candidates=2048, master_seed=11,
-                  precision=precision)
+                  precision=precision, refine=0)
     dp = capi.DevicePlanner(m)
     center = np.linspace(-0.3, 0.3, m.param_count())
     recs, got = dp.evaluate(w.snapshot, w.t, 0, 0, 2, center, 0, 2048, per_sample=True)
@@ -137,6 +137,7 @@ def test_c1_full_plan_vs_oracle(precision):
 def test_c2_per_sample_vs_oracle(precision):
     n = 1 << 15
     w = workloads.c2(samples=n, precision=precision)
+    w.model.refine = 0  # per-sample kernel parity (no re-ranking pass)
     dp = capi.DevicePlanner(w.model)
     rec, got = dp.evaluate(w.snapshot, w.t, 0, 0, 1, np.zeros(18), 0, n, per_sample=True)
     want = Port(w.model).eval_candidates(w.snapshot, w.t, 0, 0, np.zeros(18), 0, n)
@@ -181,3 +182,44 @@ def test_invalid_field_horizon_rejected():
     m = abi.Model(H=40, n_restarts=1, n_candidates=64)
     with pytest.raises(ValueError, match="shorter than the planning horizon"):
         capi.DevicePlanner(m).plan_step(w.snapshot, 0)
+
+
+@pytest.mark.parametrize("samples", [1 << 16, 1 << 18])
+def test_fp32_rerank_returns_the_reference_winner(samples):
+    """FP32 rollout + near-tie re-ranking: the round winner is the reference's
+    winner (the oracle evaluates every candidate in FP64 with glibc)."""
+    w = workloads.c2(samples=samples)
+    dp = capi.DevicePlanner(abi.Model(H=30, n_restarts=1, n_candidates=samples,
+                                      precision=32, refine=1))
+    rec, _ = dp.evaluate(w.snapshot, w.t, 0, 0, 1, None, 0, samples)
+    assert dp.timing().refined >= 1
+    want = Port(w.model).eval_candidates(w.snapshot, w.t, 0, 0, np.zeros(18), 0, samples)
+    cls = np.where(want["collided"] != 0, 0, np.where(want["reached"] != 0, 2, 1))
+    k1 = np.where(cls == 2, -want["t_goal"].astype(float), -want["terminal_cost"])
+    k2 = np.where(cls == 2, -want["path_length"], 0.0)
+    order = np.lexsort((np.arange(samples), -k2, -k1, -cls))
+    assert rec[0]["candidate"] == order[0]
+    assert rec[0]["k1"] == k1[order[0]] and rec[0]["cls"] == cls[order[0]]
+
+
+def test_refine_fixes_a_flipped_fp32_winner():
+    """C2 at 2^16: the FP32 best (the unperturbed centre, candidate 0) rides
+    exactly on the chassis edge of the oncoming car's corner points; FP32
+    rounding of the field calls it free, the reference calls it collided.
+    The certified re-ranking must return the reference's winner anyway."""
+    n = 1 << 16
+    w = workloads.c2(samples=n)
+    raw = capi.DevicePlanner(abi.Model(H=30, n_restarts=1, n_candidates=n, refine=0))
+    fixed = capi.DevicePlanner(abi.Model(H=30, n_restarts=1, n_candidates=n, refine=1))
+    ra, _ = raw.evaluate(w.snapshot, w.t, 0, 0, 1, None, 0, n)
+    rb, _ = fixed.evaluate(w.snapshot, w.t, 0, 0, 1, None, 0, n)
+    assert raw.timing().refined == 0 and fixed.timing().refined >= 1
+    port = Port(w.model)
+    want_b = port.eval_candidates(w.snapshot, w.t, 0, 0, np.zeros(18), int(rb[0]["candidate"]),
+                                  int(rb[0]["candidate"]) + 1)[0]
+    assert rb[0]["k1"] == -want_b["terminal_cost"] and not want_b["collided"]
+    if ra[0]["candidate"] != rb[0]["candidate"]:
+        want_a = port.eval_candidates(w.snapshot, w.t, 0, 0, np.zeros(18),
+                                      int(ra[0]["candidate"]), int(ra[0]["candidate"]) + 1)[0]
+        exact_cls = 0 if want_a["collided"] else (2 if want_a["reached"] else 1)
+        assert exact_cls < rb[0]["cls"] or -want_a["terminal_cost"] <= rb[0]["k1"]

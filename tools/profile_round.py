@@ -11,12 +11,18 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--precision", type=int, default=32)
 ap.add_argument("--samples", type=int, default=1 << 20)
+ap.add_argument("--refine", type=int, default=1)
 a = ap.parse_args()
 w = workloads.c2(samples=a.samples, precision=a.precision)
+w.model.refine = a.refine
 dp = capi.DevicePlanner(w.model)
 dp.upload(w.snapshot)
+import time  # noqa: E402
 for _ in range(a.reps):
+    t0 = time.perf_counter()
     rec, _ = dp.evaluate(None, w.t, 0, 0, 1, None, 0, w.model.n_candidates)
+    wall = (time.perf_counter() - t0) * 1e3
     t = dp.timing()
-    print(f"kernel {t.kernel_ms:.3f} ms winner {rec[0]['candidate']} cls {rec[0]['cls']} "
-          f"steps {t.executed_steps}")
+    print(f"p{a.precision} refine={a.refine} wall {wall:.3f} ms device {t.kernel_ms:.3f} ms winner "
+          f"{rec[0]['candidate']} cls {rec[0]['cls']} k1 {rec[0]['k1']:.12f} "
+          f"steps {t.executed_steps} refined {t.refined} launches {t.launches}")
