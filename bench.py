@@ -201,7 +201,7 @@ def run_b200(a):
     center = np.zeros(model.param_count())
     for _ in range(a.warmup):
         dp.evaluate(None, w.t, 0, 0, 1, center, c0, c1)
-    dev_ms, kern_ms, steps_exec, states, launches = [], [], 0, 0, 0
+    dev_ms, kern_ms, steps_exec, states, launches, refined = [], [], 0, 0, 0, 0
     barrier()
     with ClockSampler(local) as clocks:
         for _ in range(a.steps):
@@ -219,6 +219,7 @@ def run_b200(a):
             steps_exec += tm.executed_steps
             states += tm.checked_states
             launches += tm.launches
+            refined += max(tm.refined, 0)
         barrier()
         total_ms = sum(dev_ms)
         if dist is not None:
@@ -308,7 +309,14 @@ def run_b200(a):
                        "samples_per_gpu": per_gpu, "samples_total": model.n_candidates,
                        "H": H, "n_points": N, "moving_points": 4, "arch": [5, 2, 2],
                        "restarts": 1, "parallelism": f"candidate shards x{world}",
+                       "rollout_precision": "fp32" if a.precision == 32 else "fp64",
+                       "winner": "certified: FP32 window re-ranked in the reference's FP64 "
+                                 "arithmetic (PlannerConfig.refine)",
                        "l2": "flushed (256 MiB write) between timed steps"},
+            "value_timing": "CUDA events on the planner stream around each sampling round "
+                            "(generate + rollout + window-select kernels and the host "
+                            "certification between them), snapshot resident in HBM",
+            "near_tie_candidates_per_step": refined // a.steps,
             "e2e": {"value": e2e_value, "unit": UNIT, "ms_per_step": e2e_s / a.steps * 1e3,
                     "h2d_bytes_per_step": h2d // a.steps, "d2h_bytes_per_step": d2h // a.steps,
                     "api": "paraplan.Planner.plan_step" if world == 1 else
