@@ -301,6 +301,9 @@ void fill_consts(const ppdev::RoundArgs& a, ppdev::ConstsT<Real>* k) {
   k->qpad = Real(cull + a.bucket_w / 8.0);
   // a discrete verdict whose margin is below this may flip under rounding
   k->dmarg = sizeof(Real) == sizeof(float) ? Real(a.dmarg32) : Real(1e-9);
+  k->bcx = Real(0.5 * (a.fe - a.re));
+  k->bhx = Real(0.5 * (a.fe + a.re));
+  k->tan_small = a.delta_max <= 0.785 ? 1 : 0;
 }
 
 // Goal transform and constants of a snapshot (src/planner.cpp:70-81).

@@ -59,6 +59,8 @@ struct ConstsT {
   Real bx0, binv;       // x-bucket grid of the field: origin, 1 / bucket width
   Real qpad;            // bucket query half width: cull + bucket width / 8
   Real dmarg;           // |margin| below which a discrete verdict is "marginal"
+  Real bcx, bhx;        // rectangle centre offset (fe - re)/2 and half length (fe + re)/2
+  int32_t tan_small;    // delta_max <= pi/4: tan by polynomial ratio (FP32)
 };
 
 // Everything one sampling round needs. Scalars are FP64 here; the FP32

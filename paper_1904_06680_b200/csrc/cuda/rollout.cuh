@@ -91,11 +91,49 @@ struct Vec2T<double> {
 template <typename Real>
 struct M;
 
+// FP32 sin/cos kernels on [-pi/4, pi/4] (minimax, ~1 ulp; Cephes-style
+// coefficients) and the quadrant reduction used by the FP32 rollout.
+__device__ __forceinline__ float sin_poly(float r) {
+  const float r2 = r * r;
+  float p = fmaf(r2, -1.9515295891e-4f, 8.3321608736e-3f);
+  p = fmaf(r2, p, -1.6666654611e-1f);
+  return fmaf(r * r2, p, r);
+}
+__device__ __forceinline__ float cos_poly(float r) {
+  const float r2 = r * r;
+  float p = fmaf(r2, 2.443315711809948e-5f, -1.388731625493765e-3f);
+  p = fmaf(r2, p, 4.166664568298827e-2f);
+  return fmaf(r2 * r2, p, fmaf(-0.5f, r2, 1.0f));
+}
+// sincos for the rollout's headings (|x| well below 2^7 * pi/2, where the
+// three-part pi/2 products stay exact).
+__device__ __forceinline__ void fast_sincosf(float x, float* s, float* c) {
+  const float q = rintf(x * 0.636619772367581343f);
+  float r = fmaf(-q, 1.5703125f, x);
+  r = fmaf(-q, 4.837512969970703125e-4f, r);
+  r = fmaf(-q, 7.54978995489188216e-8f, r);
+  const float sp = sin_poly(r), cp = cos_poly(r);
+  const int qi = static_cast<int>(q);
+  const bool swap = (qi & 1) != 0;
+  float sv = swap ? cp : sp;
+  float cv = swap ? sp : cp;
+  sv = (qi & 2) ? -sv : sv;
+  cv = ((qi + 1) & 2) ? -cv : cv;
+  *s = sv;
+  *c = cv;
+}
+
 template <>
 struct M<float> {
   static __device__ __forceinline__ float th(float x) { return tanhf(x); }
   static __device__ __forceinline__ float tn(float x) { return tanf(x); }
-  static __device__ __forceinline__ void sc(float x, float* s, float* c) { sincosf(x, s, c); }
+  // tan for |x| <= pi/4 (the steering range when delta_max <= pi/4)
+  static __device__ __forceinline__ float tn_small(float x) {
+    return sin_poly(x) * __frcp_rn(cos_poly(x));
+  }
+  static __device__ __forceinline__ void sc(float x, float* s, float* c) {
+    fast_sincosf(x, s, c);
+  }
   static __device__ __forceinline__ float sq(float x) { return sqrtf(x); }
   static __device__ __forceinline__ float ab(float x) { return fabsf(x); }
   // wrap_angle (src/geometry.cpp:9-13): remainder by 2*pi (two-part
@@ -113,6 +151,7 @@ template <>
 struct M<double> {
   static __device__ __forceinline__ double th(double x) { return tanh(x); }
   static __device__ __forceinline__ double tn(double x) { return tan(x); }
+  static __device__ __forceinline__ double tn_small(double x) { return tan(x); }
   static __device__ __forceinline__ void sc(double x, double* s, double* c) { sincos(x, s, c); }
   static __device__ __forceinline__ double sq(double x) { return sqrt(x); }
   static __device__ __forceinline__ double ab(double x) { return fabs(x); }
@@ -319,6 +358,41 @@ __device__ __forceinline__ Real collide_margin(const Field<Real>& f, const Const
   return best;
 }
 
+// FP32 specialisation: points in the vehicle frame via the pre-rotated
+// vehicle position (b = R(-phi) p - R(-phi) z), the rectangle tested around
+// its centre (|bx - cx| < hx, |by| < hw) and no separate circle prefilter
+// (the rectangle lies inside the bounding circle, so the prefilter can only
+// matter at the rear corners within rounding -- a narrow hit, which the
+// marginal flag sends to the exact re-ranking).
+template <>
+__device__ __forceinline__ float collide_margin<float>(const Field<float>& f,
+                                                       const Consts<float>& K, int h, float x,
+                                                       float y, float c, float s) {
+  const int B = f.B;
+  const int* st = f.starts + static_cast<size_t>(h) * (B + 1);
+  const float2* pts = f.pts + static_cast<size_t>(h) * f.N;
+  const float top = static_cast<float>(B - 1);
+  const float flo = (x - K.qpad - K.bx0) * K.binv;
+  const float fhi = (x + K.qpad - K.bx0) * K.binv;
+  const int blo = static_cast<int>(fminf(fmaxf(flo, 0.0f), top));
+  const int bhi = static_cast<int>(fminf(fmaxf(fhi, 0.0f), top));
+  const int lo = st[blo];
+  const int cnt = st[bhi + 1] - lo;
+  const int rounds = __reduce_max_sync(kFull, cnt);
+  const float kx = fmaf(c, x, fmaf(s, y, K.bcx));  // vehicle (+ box centre) rotated
+  const float ky = fmaf(-s, x, c * y);
+  float best = -1e30f;
+  for (int j = 0; j < rounds; ++j) {
+    if (j < cnt) {
+      const float2 m = pts[lo + j];
+      const float bx = fmaf(c, m.x, fmaf(s, m.y, -kx));
+      const float by = fmaf(-s, m.x, fmaf(c, m.y, -ky));
+      best = fmaxf(best, fminf(K.bhx - fabsf(bx), K.hw - fabsf(by)));
+    }
+  }
+  return best;
+}
+
 // One candidate's rollout state (src/planner.cpp:123-125, 130-132).
 template <typename Real>
 struct Lane {
@@ -396,7 +470,7 @@ __device__ __forceinline__ int advance(Lane<Real>& L, const Net& net, const Cons
   const Real w = Real(0.5) * (c1 + Real(1));
   const Real u_v = (Real(1) - w) * K.umin + w * K.umax;
   // explicit Euler (src/dynamics.cpp:45-62)
-  const Real tan_d = M<Real>::tn(delta);
+  const Real tan_d = K.tan_small ? M<Real>::tn_small(delta) : M<Real>::tn(delta);
   const Real tb = K.l_r * tan_d / K.wb;
   const Real tv = K.Ts * L.v;
   const Real nx = L.x + tv * (cphi - tb * sphi);
