@@ -28,8 +28,8 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 INC = ROOT / "include"
-BUILD = PKG / "_build"
-LIB = PKG / "lib" / "libparaplan.so"
+BUILD = Path(os.environ.get("PARAPLAN_BUILD_DIR", PKG / "_build"))
+LIB = Path(os.environ.get("PARAPLAN_BUILD_LIB", PKG / "lib" / "libparaplan.so"))
 PYPKG = PKG / "python" / "paraplan"
 CORE = PYPKG / ("_core" + sysconfig.get_config_var("EXT_SUFFIX"))
 
@@ -44,7 +44,7 @@ JSON_DIRS = [
 HOST_FLAGS = ["-std=c++20", "-O3", "-fPIC", "-fno-math-errno", "-ffp-contract=off", "-pthread",
               "-Wall", "-Wno-unused-parameter"]
 NVCC_FLAGS = ["-std=c++17", "-O3", "-lineinfo", "-Xptxas", "-v", "-Xcompiler", "-fPIC",
-              "--expt-relaxed-constexpr"] + ARCH
+              "--expt-relaxed-constexpr"] + ARCH + os.environ.get("PARAPLAN_NVCC_DEFS", "").split()
 
 
 def _json_dir() -> Path:
@@ -107,6 +107,8 @@ def build(force: bool = False, verbose: bool = False) -> Path:
               f"-L{CUDA_HOME / 'lib64'}", "-lcudart_static", "-ldl", "-lrt", "-lpthread",
               "-Wl,--no-undefined"], verbose)
 
+    if "PARAPLAN_BUILD_LIB" in os.environ:  # variant library only (A/B experiments)
+        return LIB
     import pybind11
     bind = CSRC / "python" / "bindings.cpp"
     if force or _stale(CORE, [bind, LIB] + hdrs):

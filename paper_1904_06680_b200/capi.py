@@ -7,13 +7,16 @@ when it is missing -- there is no CPU fallback anywhere on the product path.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
 import numpy as np
 
 from . import abi
 
-LIB_PATH = Path(__file__).resolve().parent / "lib" / "libparaplan.so"
+# PARAPLAN_LIB selects an alternative build (A/B experiments only)
+LIB_PATH = Path(os.environ.get("PARAPLAN_LIB",
+                               Path(__file__).resolve().parent / "lib" / "libparaplan.so"))
 _lib = None
 
 

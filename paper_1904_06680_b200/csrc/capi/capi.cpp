@@ -303,6 +303,8 @@ void fill_consts(const ppdev::RoundArgs& a, ppdev::ConstsT<Real>* k) {
   k->dmarg = sizeof(Real) == sizeof(float) ? Real(a.dmarg32) : Real(1e-9);
   k->bcx = Real(0.5 * (a.fe - a.re));
   k->bhx = Real(0.5 * (a.fe + a.re));
+  k->inv_wb = Real(1.0 / a.wheelbase);
+  k->wb_d = a.wheelbase;
   k->tan_small = a.delta_max <= 0.785 ? 1 : 0;
 }
 

@@ -60,6 +60,8 @@ struct ConstsT {
   Real qpad;            // bucket query half width: cull + bucket width / 8
   Real dmarg;           // |margin| below which a discrete verdict is "marginal"
   Real bcx, bhx;        // rectangle centre offset (fe - re)/2 and half length (fe + re)/2
+  Real inv_wb;          // 1 / wheelbase (FP32 path multiplies)
+  double wb_d;          // wheelbase (FP64 path divides, src/dynamics.cpp:52-55)
   int32_t tan_small;    // delta_max <= pi/4: tan by polynomial ratio (FP32)
 };
 

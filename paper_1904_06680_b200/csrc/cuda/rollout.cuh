@@ -52,6 +52,9 @@ constexpr double kTwoPi = 6.283185307179586;
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kBlock = 128;
 constexpr int kWarps = kBlock / 32;
+#ifndef PARAPLAN_REFILL_MINB
+#define PARAPLAN_REFILL_MINB 1
+#endif
 
 // src/rng.cpp:11-18
 __device__ __forceinline__ uint64_t mix64(uint64_t z) {
@@ -471,11 +474,11 @@ __device__ __forceinline__ int advance(Lane<Real>& L, const Net& net, const Cons
   const Real u_v = (Real(1) - w) * K.umin + w * K.umax;
   // explicit Euler (src/dynamics.cpp:45-62)
   const Real tan_d = K.tan_small ? M<Real>::tn_small(delta) : M<Real>::tn(delta);
-  const Real tb = K.l_r * tan_d / K.wb;
+  const Real tb = M<Real>::ndiv(K.l_r * tan_d, K.wb_d, K.inv_wb);
   const Real tv = K.Ts * L.v;
   const Real nx = L.x + tv * (cphi - tb * sphi);
   const Real ny = L.y + tv * (sphi + tb * cphi);
-  const Real nphi = L.phi + tv * tan_d / K.wb;
+  const Real nphi = L.phi + M<Real>::ndiv(tv * tan_d, K.wb_d, K.inv_wb);
   const Real nv = L.v + K.Ts * u_v;
   const Real dx = nx - L.x, dy = ny - L.y;
   const Real seg = M<Real>::sq(dx * dx + dy * dy);
@@ -721,7 +724,7 @@ __global__ void __launch_bounds__(256) generate_kernel(const RoundArgs a) {
 
 // ------------------------------------------------------ refill kernel ----
 template <typename Real, class Net>
-__global__ void __launch_bounds__(kBlock) refill_kernel(const RoundArgs a) {
+__global__ void __launch_bounds__(kBlock, PARAPLAN_REFILL_MINB) refill_kernel(const RoundArgs a) {
   constexpr int P = Net::kP;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ Key table[kWarps][kMaxRestartsPerLaunch];
