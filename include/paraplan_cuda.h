@@ -161,6 +161,7 @@ typedef struct pp_timing {
   int32_t launches;        /* kernels launched by the call */
   int32_t refined;         /* FP32 candidates re-ranked in FP64 */
   int64_t h2d_bytes, d2h_bytes;
+  double certify_ms;       /* host time of the certified re-ranking (wall) */
 } pp_timing;
 
 typedef struct pp_handle pp_handle;

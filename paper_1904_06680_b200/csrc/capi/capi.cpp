@@ -154,62 +154,80 @@ struct Key {
 };
 
 // Fork-join pool for the host's exact re-evaluation of near-tie candidates.
+// prewarm() is called when a round is launched: the workers wake and spin
+// for the job (up to a few ms) while the GPU works, so the fork itself costs
+// no thread wake-up latency.
 class HostPool {
  public:
   explicit HostPool(int n) {
-    for (int i = 1; i < n; ++i) workers_.emplace_back([this, i] { loop(i); });
+    for (int i = 1; i < n; ++i) workers_.emplace_back([this] { loop(); });
   }
   ~HostPool() {
     {
       std::lock_guard<std::mutex> lock(mu_);
-      stop_ = true;
+      stop_.store(true);
     }
     cv_.notify_all();
     for (auto& w : workers_) w.join();
   }
   int size() const { return static_cast<int>(workers_.size()) + 1; }
-  // fn(i) for i in [0, n), spread over the workers and the caller.
-  void run(int n, const std::function<void(int)>& fn) {
+  void prewarm() {
     {
       std::lock_guard<std::mutex> lock(mu_);
-      fn_ = &fn;
-      n_ = n;
-      next_.store(0);
-      pending_ = static_cast<int>(workers_.size());
-      ++gen_;
+      warm_.fetch_add(1);
+    }
+    cv_.notify_all();
+  }
+  // fn(i) for i in [0, n), spread over the workers and the caller.
+  void run(int n, const std::function<void(int)>& fn) {
+    fn_ = &fn;
+    n_ = n;
+    next_.store(0);
+    done_.store(0);
+    {
+      std::lock_guard<std::mutex> lock(mu_);
+      job_.fetch_add(1, std::memory_order_release);
     }
     cv_.notify_all();
     drain();
-    std::unique_lock<std::mutex> lock(mu_);
-    done_cv_.wait(lock, [this] { return pending_ == 0; });
+    const int workers = static_cast<int>(workers_.size());
+    while (done_.load(std::memory_order_acquire) < workers) std::this_thread::yield();
   }
 
  private:
   void drain() {
     for (int i; (i = next_.fetch_add(1)) < n_;) (*fn_)(i);
   }
-  void loop(int) {
-    uint64_t seen = 0;
+  void loop() {
+    uint64_t seen_job = 0, seen_warm = 0;
     for (;;) {
       {
         std::unique_lock<std::mutex> lock(mu_);
-        cv_.wait(lock, [&] { return stop_ || gen_ != seen; });
-        if (stop_) return;
-        seen = gen_;
+        cv_.wait(lock, [&] {
+          return stop_.load() || job_.load() != seen_job || warm_.load() != seen_warm;
+        });
+        if (stop_.load()) return;
+        seen_warm = warm_.load();
       }
-      drain();
-      std::lock_guard<std::mutex> lock(mu_);
-      if (--pending_ == 0) done_cv_.notify_one();
+      const auto t0 = std::chrono::steady_clock::now();
+      while (job_.load(std::memory_order_acquire) == seen_job && !stop_.load() &&
+             std::chrono::steady_clock::now() - t0 < std::chrono::milliseconds(5)) {
+      }
+      if (job_.load(std::memory_order_acquire) != seen_job) {
+        seen_job = job_.load(std::memory_order_acquire);
+        drain();
+        done_.fetch_add(1, std::memory_order_release);
+      }
     }
   }
   std::vector<std::thread> workers_;
   std::mutex mu_;
-  std::condition_variable cv_, done_cv_;
+  std::condition_variable cv_;
   const std::function<void(int)>* fn_ = nullptr;
-  std::atomic<int> next_{0};
-  int n_ = 0, pending_ = 0;
-  uint64_t gen_ = 0;
-  bool stop_ = false;
+  std::atomic<int> next_{0}, done_{0};
+  int n_ = 0;
+  std::atomic<uint64_t> job_{0}, warm_{0};
+  std::atomic<bool> stop_{false};
 };
 
 bool key_better(const Key& a, const Key& b) {  // src/planner.cpp:40-44
@@ -581,8 +599,8 @@ void run_round_launch(pp_handle* h, uint64_t t, int iter, int r0, int rc, const 
   if (shape.refill) {
     const size_t esz = fp64 ? sizeof(double) : sizeof(float);
     h->d_theta.reserve(total * shape.theta_elem * esz, "theta buffer");
-    a.theta_buf = h->d_theta.p;
-    a.first_buf = static_cast<char*>(h->d_theta.p) + total * (shape.theta_elem - 2) * esz;
+    a.theta_buf = h->d_theta.p;  // [total][theta_elem]: theta, first action, pad
+    a.first_buf = nullptr;
   }
   const bool generic = h->kind == ppdev::NetKind::kGeneric;
   if (generic || rerank) {
@@ -616,6 +634,11 @@ void run_round_launch(pp_handle* h, uint64_t t, int iter, int r0, int rc, const 
                        h->stream),
        "selection counter");
     ck(static_cast<cudaError_t>(ppdev::launch_select(a, h->stream)), "window select launch");
+    if (!h->pool) {
+      const unsigned hc = std::thread::hardware_concurrency();
+      h->pool = std::make_unique<HostPool>(static_cast<int>(std::min(16u, std::max(1u, hc))));
+    }
+    h->pool->prewarm();  // workers spin while the GPU samples
   }
   ck(cudaEventRecord(h->ev1, h->stream), "event");
   ck(cudaMemcpyAsync(h->h_result.p, h->d_result.p, rbytes, cudaMemcpyDeviceToHost, h->stream),
@@ -660,7 +683,10 @@ void run_round_launch(pp_handle* h, uint64_t t, int iter, int r0, int rc, const 
   if (!rerank) return;
 
   n_sel = h->h_selcount;
+  const auto c_t0 = std::chrono::steady_clock::now();
   certify_round(h, a, t, iter, r0, rc, center, c0, c1, injected, out, fp64, n_sel);
+  h->timing.certify_ms +=
+      std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - c_t0).count();
 }
 
 // Certified re-ranking (PlannerConfig::refine). The FP32 keys are trusted

@@ -39,6 +39,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <type_traits>
 #include <cstdlib>
 #include <cstring>
 
@@ -53,7 +54,7 @@ constexpr unsigned kFull = 0xffffffffu;
 constexpr int kBlock = 128;
 constexpr int kWarps = kBlock / 32;
 #ifndef PARAPLAN_REFILL_MINB
-#define PARAPLAN_REFILL_MINB 1
+#define PARAPLAN_REFILL_MINB 6  // <= 85 registers: 6 CTAs (24 warps) per SM, no spills
 #endif
 
 // src/rng.cpp:11-18
@@ -694,31 +695,44 @@ __device__ __forceinline__ void flush_bests(bool& flush, Key& best, int best_r, 
 // theta (rounded to Real) and the first action of every candidate of the
 // round, one thread per candidate at full SIMT width: the FP64 RNG lives here
 // and not in the rollout kernel, so the rollout kernel stays register-light.
-// Layout: theta_buf[i * total + s], first_buf[k * total + s], with the flat
-// index s = r * count + local (restart-major).
+// Layout: one record of kRecW(P) Reals per candidate, [theta 0..P-1][f0][f1]
+// [pad], so a refilling lane loads it with 16-byte vector loads; the flat
+// index is s = r * count + local (restart-major).
+template <typename Real>
+constexpr int rec_width(int P) {
+  return ((P + 2) * static_cast<int>(sizeof(Real)) + 15) / 16 * 16 / static_cast<int>(sizeof(Real));
+}
+template <typename Real>
+using Vec16 = typename std::conditional<sizeof(Real) == 4, float4, double2>::type;
+
 template <typename Real, int H1>
 __global__ void __launch_bounds__(256) generate_kernel(const RoundArgs a) {
   constexpr int P = NetReg<Real, H1>::P;
+  constexpr int W = rec_width<Real>(P);
+  constexpr int V = W * static_cast<int>(sizeof(Real)) / 16;
   const Consts<Real>& K = consts_of<Real>(a);
   Real s0[5];
   start_features(K, s0);
-  Real* theta = static_cast<Real*>(a.theta_buf);
-  Real* first = static_cast<Real*>(a.first_buf);
+  Vec16<Real>* recs = static_cast<Vec16<Real>*>(a.theta_buf);
   const int64_t total = a.count * a.restart_count;
   for (int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; s < total;
        s += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int r = static_cast<int>(s / a.count);
     const int64_t local = s - static_cast<int64_t>(r) * a.count;
-    NetReg<Real, H1> n;
+    union {
+      Real v[W];
+      Vec16<Real> q[V];
+    } rec;
     draw_theta<Real, P>(a, __ldg(a.key_prefix + r), a.injected ? local : a.cand_begin + local, P,
-                        [&](int i, Real v) {
-                          n.w[i] = v;
-                          theta[static_cast<int64_t>(i) * total + s] = v;
-                        });
-    Real f0, f1;
-    n.eval(s0, f0, f1);  // first action (src/planner.cpp:130-132)
-    first[s] = f0;
-    first[total + s] = f1;
+                        [&](int i, Real v) { rec.v[i] = v; });
+    NetReg<Real, H1> n;
+#pragma unroll
+    for (int i = 0; i < P; ++i) n.w[i] = rec.v[i];
+    n.eval(s0, rec.v[P], rec.v[P + 1]);  // first action (src/planner.cpp:130-132)
+#pragma unroll
+    for (int i = P + 2; i < W; ++i) rec.v[i] = Real(0);
+#pragma unroll
+    for (int j = 0; j < V; ++j) recs[s * V + j] = rec.q[j];
   }
 }
 
@@ -741,9 +755,9 @@ __global__ void __launch_bounds__(kBlock, PARAPLAN_REFILL_MINB) refill_kernel(co
 
   const int bpr = a.tiles_per_restart;  // 32-candidate batches per restart
   const unsigned total_batches = static_cast<unsigned>(a.n_tiles);
-  const int64_t total = a.count * a.restart_count;
-  const Real* theta = static_cast<const Real*>(a.theta_buf);
-  const Real* first = static_cast<const Real*>(a.first_buf);
+  constexpr int W = rec_width<Real>(P);
+  constexpr int V = W * static_cast<int>(sizeof(Real)) / 16;
+  const Vec16<Real>* recs = static_cast<const Vec16<Real>*>(a.theta_buf);
 
   Net net;
 #pragma unroll
@@ -784,9 +798,11 @@ __global__ void __launch_bounds__(kBlock, PARAPLAN_REFILL_MINB) refill_kernel(co
           my_r = q_r;
           my_c = q_c0 + q_head + rank;
           const int64_t sidx = static_cast<int64_t>(my_r) * a.count + my_c;
+          // contiguous record: one address, immediate offsets, no extra registers
+          const Real* rp = reinterpret_cast<const Real*>(recs + sidx * V);
 #pragma unroll
-          for (int i = 0; i < P; ++i) net.w[i] = theta[static_cast<int64_t>(i) * total + sidx];
-          L.start(K, first[sidx], first[total + sidx]);
+          for (int i = 0; i < P; ++i) net.w[i] = __ldg(rp + i);
+          L.start(K, __ldg(rp + P), __ldg(rp + P + 1));
           active = true;
         }
         q_head += __popc(need) < avail ? __popc(need) : avail;
@@ -1089,7 +1105,7 @@ int shape_impl(int device, int field_bytes, LaunchShape* out) {
   const bool refill = refill_schedule<Net>();
   const int smem_bytes = field_bytes;
   out->queue_bytes = 0;
-  out->theta_elem = refill ? Net::kP + 2 : 0;  // theta + first action per candidate
+  out->theta_elem = refill ? rec_width<Real>(Net::kP) : 0;  // Reals per candidate record
   int sms = 0, blocks = 0;
   cudaError_t e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
   if (e != cudaSuccess) return static_cast<int>(e);

@@ -25,4 +25,5 @@ for _ in range(a.reps):
     t = dp.timing()
     print(f"p{a.precision} refine={a.refine} wall {wall:.3f} ms device {t.kernel_ms:.3f} ms winner "
           f"{rec[0]['candidate']} cls {rec[0]['cls']} k1 {rec[0]['k1']:.12f} "
-          f"steps {t.executed_steps} refined {t.refined} launches {t.launches}")
+          f"steps {t.executed_steps} refined {t.refined} launches {t.launches} "
+          f"certify {t.certify_ms:.3f} ms")
