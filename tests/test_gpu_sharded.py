@@ -1,0 +1,57 @@
+"""The multi-GPU plan_step on real device rounds: two ranks (gloo for the
+record exchange) each run the sm_100a kernels on their candidate shard of the
+same GPU -- no kernel waits on another rank, the ranks only exchange winner
+records on the host -- and must return the single-GPU plan bit for bit."""
+from __future__ import annotations
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_1904_06680_b200 import abi, capi, workloads
+
+pytestmark = pytest.mark.gpu
+
+CFGS = [dict(H=30, n_restarts=1, n_candidates=1 << 16),
+        dict(H=30, n_restarts=3, n_candidates=5000, master_seed=4),
+        dict(H=30, n_restarts=2, n_iter_max=2, n_candidates=3000, master_seed=8)]
+
+
+def _worker(rank, world, port, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1904_06680_b200.distributed import ShardedPlanner
+    w = workloads.c2(samples=1 << 10)
+    for k, cfg in enumerate(CFGS):
+        sp = ShardedPlanner.on_device(abi.Model(**cfg), rank, world)
+        r = sp.plan_step(w.snapshot, w.t)
+        out[(rank, k)] = (r.best_theta.tobytes(), r.trajectory.tobytes(), r.action, r.evaluated,
+                          r.winner[:2])
+        sp.device_planner.close()
+    dist.destroy_process_group()
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def test_two_ranks_equal_one_gpu_plan():
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_worker, args=(2, _port(), out), nprocs=2, join=True)
+    w = workloads.c2(samples=1 << 10)
+    for k, cfg in enumerate(CFGS):
+        o, theta, traj = capi.DevicePlanner(abi.Model(**cfg)).plan_step(w.snapshot, w.t)
+        for rank in range(2):
+            bt, tr, action, evaluated, win = out[(rank, k)]
+            assert bt == theta.tobytes() and tr == traj.tobytes(), (k, rank)
+            assert action == (o.action_a0, o.action_a1) and evaluated == o.evaluated
