@@ -314,9 +314,10 @@ void fill_consts(const ppdev::RoundArgs& a, ppdev::ConstsT<Real>* k) {
   k->r2 = Real(a.r2);
   const double cull = std::sqrt(a.r2) + 1e-3;
   k->cull = Real(cull);
-  k->bx0 = Real(a.bucket_x0);
-  k->binv = Real(1.0 / a.bucket_w);
-  k->qpad = Real(cull + a.bucket_w / 8.0);
+  k->bx0 = Real(a.grid_x0);
+  k->by0 = Real(a.grid_y0);
+  k->binv = Real(1.0 / a.grid_g);
+  k->qpad = Real(cull + a.grid_g / 8.0);
   // a discrete verdict whose margin is below this may flip under rounding
   k->dmarg = sizeof(Real) == sizeof(float) ? Real(a.dmarg32) : Real(1e-9);
   k->bcx = Real(0.5 * (a.fe - a.re));
@@ -377,40 +378,59 @@ void upload_snapshot(pp_handle* h, const pp_snapshot& s) {
   for (size_t i = 0; i < h->sizes.size(); ++i) a.sizes[i] = h->sizes[i];
 
   // Only rows 0..H are ever read; ship those, in the compute precision,
-  // each row ordered by x-bucket with per-bucket start offsets so the kernel
-  // visits only the points near its own x (the collision verdict is an OR
-  // over the row's points, independent of their order).
+  // each row ordered by grid cell with per-cell start offsets so the kernel
+  // visits only the points near the vehicle (the collision verdict is an OR
+  // over the row's points, independent of their order). A static field
+  // (every row identical) ships one row.
   const int N = s.n_points;
   a.n_points = N;
-  const size_t rows = static_cast<size_t>(cfg.H + 1);
+  const size_t all_rows = static_cast<size_t>(cfg.H + 1);
+  const size_t row_len = 2 * static_cast<size_t>(N);
+  bool is_static = N > 0;
+  for (size_t row = 1; row < all_rows && is_static; ++row) {
+    is_static = std::memcmp(s.field_xy, s.field_xy + row * row_len, row_len * sizeof(double)) == 0;
+  }
+  const size_t rows = is_static ? 1 : all_rows;
   const size_t count = rows * static_cast<size_t>(N);
   const size_t elem = h->fp64 ? sizeof(double) : sizeof(float);
-  double xmin = 0.0, xmax = 0.0;
+  double xmin = 0.0, xmax = 0.0, ymin = 0.0, ymax = 0.0;
   for (size_t i = 0; i < count; ++i) {
-    const double x = s.field_xy[2 * i];
+    const double x = s.field_xy[2 * i], y = s.field_xy[2 * i + 1];
     if (i == 0 || x < xmin) xmin = x;
     if (i == 0 || x > xmax) xmax = x;
+    if (i == 0 || y < ymin) ymin = y;
+    if (i == 0 || y > ymax) ymax = y;
   }
+  // cell size: half the collision window; a 2-D grid only for larger clouds,
+  // at most ~4096 cells per row
   const double cull = std::sqrt(a.r2) + 1e-3;
-  double width = 0.5 * cull;
-  int B = 1;
+  double cg = 0.5 * cull;
+  int nx = 1, ny = 1;
   if (count > 0) {
-    if (!(std::isfinite(xmin) && std::isfinite(xmax))) {
+    if (!(std::isfinite(xmin) && std::isfinite(xmax) && std::isfinite(ymin) && std::isfinite(ymax))) {
       throw std::invalid_argument("obstacle field has non-finite coordinates");
     }
-    width = std::max(width, (xmax - xmin) / 4095.0);
-    B = static_cast<int>(std::floor((xmax - xmin) / width)) + 1;
-    B = std::min(std::max(B, 1), 4096);
+    const bool two_d = N >= 128;
+    const double wx = xmax - xmin, wy = two_d ? ymax - ymin : 0.0;
+    const double cap = two_d ? 4096.0 : 4096.0;
+    while ((std::floor(wx / cg) + 1) * (two_d ? std::floor(wy / cg) + 1 : 1.0) > cap) cg *= 1.25;
+    nx = static_cast<int>(std::floor(wx / cg)) + 1;
+    ny = two_d ? static_cast<int>(std::floor(wy / cg)) + 1 : 1;
   }
-  a.n_buckets = B;
-  a.bucket_x0 = xmin;
-  a.bucket_w = width;
+  const int cells = nx * ny;
+  a.field_rows = static_cast<int32_t>(rows);
+  a.grid_nx = nx;
+  a.grid_ny = ny;
+  a.grid_x0 = xmin;
+  a.grid_y0 = ymin;
+  a.grid_g = cg;
   const size_t pts_bytes = 2 * count * elem;
+  const size_t st_bytes = rows * (cells + 1) * sizeof(int32_t);
   // padded to 16 bytes so the FP64 image after it is double2-aligned
-  const size_t bytes = (pts_bytes + rows * (B + 1) * sizeof(int32_t) + 15) & ~size_t(15);
+  const size_t bytes = (pts_bytes + st_bytes + 15) & ~size_t(15);
   // FP32 rounds also get an FP64 image for the near-tie re-ranking
   const size_t pts64_bytes = 2 * count * sizeof(double);
-  const size_t bytes64 = h->fp64 ? 0 : pts64_bytes + rows * (B + 1) * sizeof(int32_t);
+  const size_t bytes64 = h->fp64 ? 0 : pts64_bytes + st_bytes;
   if (count > 0) {
     h->h_field.reserve(bytes + bytes64, "pinned field");
     h->d_field.reserve(bytes + bytes64, "device field");
@@ -418,23 +438,24 @@ void upload_snapshot(pp_handle* h, const pp_snapshot& s) {
     int32_t* starts = reinterpret_cast<int32_t*>(base + pts_bytes);
     unsigned char* base64 = base + bytes;
     int32_t* starts64 = reinterpret_cast<int32_t*>(base64 + pts64_bytes);
-    std::vector<int32_t> order(N), bucket(N);
+    std::vector<int32_t> order(N), cell(N), fill(cells + 1);
     for (size_t row = 0; row < rows; ++row) {
-      const double* src = s.field_xy + 2 * row * N;
+      const double* src = s.field_xy + row * row_len;
+      // counting sort by cell (stable)
+      std::fill(fill.begin(), fill.end(), 0);
       for (int j = 0; j < N; ++j) {
-        order[j] = j;
-        bucket[j] = std::min(B - 1, std::max(0, static_cast<int>(std::floor(
-                                                    (src[2 * j] - xmin) / width))));
+        const int cx = std::min(nx - 1, std::max(0, static_cast<int>(std::floor((src[2 * j] - xmin) / cg))));
+        const int cy = ny == 1 ? 0
+                               : std::min(ny - 1, std::max(0, static_cast<int>(std::floor(
+                                                              (src[2 * j + 1] - ymin) / cg))));
+        cell[j] = cx * ny + cy;
+        ++fill[cell[j] + 1];
       }
-      std::stable_sort(order.begin(), order.end(),
-                       [&](int32_t p, int32_t q) { return bucket[p] < bucket[q]; });
-      int32_t* st = starts + row * (B + 1);
-      int next = 0;
-      for (int b = 0; b <= B; ++b) {
-        while (next < N && bucket[order[next]] < b) ++next;
-        st[b] = next;
-      }
-      if (bytes64 > 0) std::memcpy(starts64 + row * (B + 1), st, sizeof(int32_t) * (B + 1));
+      for (int c = 0; c < cells; ++c) fill[c + 1] += fill[c];
+      int32_t* st = starts + row * (cells + 1);
+      std::copy(fill.begin(), fill.end(), st);
+      if (bytes64 > 0) std::copy(fill.begin(), fill.end(), starts64 + row * (cells + 1));
+      for (int j = 0; j < N; ++j) order[fill[cell[j]]++] = j;
       const size_t o = row * N;
       for (int j = 0; j < N; ++j) {
         const double px = src[2 * order[j]], py = src[2 * order[j] + 1];
@@ -463,7 +484,7 @@ void upload_snapshot(pp_handle* h, const pp_snapshot& s) {
   a.field = h->d_field.p;
   a.field64 = h->fp64 ? h->d_field.p : static_cast<unsigned char*>(h->d_field.p) + bytes;
   // host copy for the exact re-ranking of FP64 near-ties (rows 0..H)
-  h->snap_field.assign(s.field_xy, s.field_xy + 2 * count);
+  h->snap_field.assign(s.field_xy, s.field_xy + all_rows * row_len);
   h->snap_warm.assign(s.warm_theta, s.warm_theta + std::max(0, s.warm_theta_len));
   h->snap_copy = s;
   h->snap_copy.field_xy = h->snap_field.data();
@@ -526,8 +547,9 @@ void run_round_launch(pp_handle* h, uint64_t t, int iter, int r0, int rc, const 
   if (force_fp64 && !h->fp64) a.field = a.field64;
   ppdev::LaunchShape shape{};
   const int field_smem = (force_fp64 && !h->fp64) ? 0 : h->field_smem_bytes;
-  const int rcode = fp64 ? ppdev::shape_f64(h->kind, h->device, field_smem, &shape)
-                         : ppdev::shape_f32(h->kind, h->device, field_smem, &shape);
+  const bool grid2d = h->base.grid_ny > 1;
+  const int rcode = fp64 ? ppdev::shape_f64(h->kind, h->device, field_smem, grid2d, &shape)
+                         : ppdev::shape_f32(h->kind, h->device, field_smem, grid2d, &shape);
   ck(static_cast<cudaError_t>(rcode), "occupancy query");
   // refill: 32-candidate batches; lockstep: one tile of `block` candidates
   const int unit = shape.refill ? 32 : shape.block;

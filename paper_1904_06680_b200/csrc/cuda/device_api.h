@@ -56,8 +56,8 @@ struct ConstsT {
   Real dmax, window, l_r, wb, Ts, umin, umax;
   Real fe, re, hw, r2;  // chassis half-planes, squared bounding radius
   Real cull;            // collision x-window half width: bounding radius + 1e-3
-  Real bx0, binv;       // x-bucket grid of the field: origin, 1 / bucket width
-  Real qpad;            // bucket query half width: cull + bucket width / 8
+  Real bx0, by0, binv;  // cell grid of the field: origin, 1 / cell size
+  Real qpad;            // cell query half width: cull + cell size / 8
   Real dmarg;           // |margin| below which a discrete verdict is "marginal"
   Real bcx, bhx;        // rectangle centre offset (fe - re)/2 and half length (fe + re)/2
   Real inv_wb;          // 1 / wheelbase (FP32 path multiplies)
@@ -96,10 +96,11 @@ struct RoundArgs {
   const uint64_t* key_prefix;  // device [restart_count]: fold^4(seed, t, r, iter)
   const double* center;        // device [n_params]
   const double* injected;      // device [count * n_params] or null (RNG off)
-  const void* field;           // device [pts Real2 (H+1)N][starts int32 (H+1)(B+1)], rows
-                               // sorted by x-bucket; starts[h][b] = first point of bucket b
-  int32_t n_buckets;           // B
-  double bucket_x0, bucket_w;  // x-bucket grid (host side; kf/kd carry bx0 and 1/w)
+  const void* field;           // device [pts Real2 rows x N][starts int32 rows x (cells+1)]:
+                               // each row ordered by grid cell, starts = first point per cell
+  int32_t field_rows;          // H+1, or 1 for a static field
+  int32_t grid_nx, grid_ny;    // cells (grid_ny == 1: x-buckets)
+  double grid_x0, grid_y0, grid_g;  // grid origin and cell size (host side)
   // scratch / outputs (device)
   Rec* tile_recs;              // restart-major: [r][tile] (lockstep) or [r][CTA] (refill)
   Rec* out;                    // [restart_count]
@@ -141,8 +142,9 @@ struct LaunchShape {
 };
 // field_bytes = shared-memory image of the field (0 = read from L2).
 // Returns 0 or a cudaError_t.
-int shape_f32(NetKind k, int device, int field_bytes, LaunchShape* out);
-int shape_f64(NetKind k, int device, int field_bytes, LaunchShape* out);
+// grid: the field uses the 2-D cell grid (separate kernel instantiation).
+int shape_f32(NetKind k, int device, int field_bytes, bool grid, LaunchShape* out);
+int shape_f64(NetKind k, int device, int field_bytes, bool grid, LaunchShape* out);
 
 // Enqueue one sampling round on `stream`. Returns 0 or a cudaError_t.
 int launch_round_f32(NetKind k, const RoundArgs& a, void* stream);

@@ -53,6 +53,9 @@ constexpr double kTwoPi = 6.283185307179586;
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kBlock = 128;
 constexpr int kWarps = kBlock / 32;
+#ifndef PARAPLAN_COLL_EXIT
+#define PARAPLAN_COLL_EXIT 1
+#endif
 #ifndef PARAPLAN_REFILL_MINB
 #define PARAPLAN_REFILL_MINB 6  // <= 85 registers: 6 CTAs (24 warps) per SM, no spills
 #endif
@@ -313,85 +316,99 @@ __device__ __forceinline__ void draw_theta(const RoundArgs& a, uint64_t prefix, 
   }
 }
 
-// Bucketed obstacle field: per row h the points sorted by x-bucket
-// (bucket b = floor((px - bx0) * binv), same grid for all rows) and
-// starts[h * (B+1) + b] = index of the first point of bucket b.
+// Binned obstacle field. Each row h holds its N points ordered by grid cell
+// (cx * ncy + cy) of a uniform grid with cell size g (origin bx0, by0, same
+// grid for all rows), and starts[row * (ncx*ncy + 1) + cell] is the index of
+// the first point of that cell. Static fields (every row identical) are
+// stored once: row = h * row_step with row_step = 0. With ncy == 1 the grid
+// is a row of x-buckets and the cells of a query window are contiguous.
 template <typename Real>
 struct Field {
   const typename Vec2T<Real>::type* pts;
   const int* starts;
   int N;
-  int B;
+  int ncx, ncy;
+  int row_step;  // 1, or 0 for a static field
 };
 
-// Collision of the chassis at (x, y, phi) with row h (src/geometry.cpp:63-76):
-// bounding-circle prefilter, strict half-planes. Only the buckets covering
-// [x - qpad, x + qpad] are visited; every point outside them has
-// |px - x| > cull > r and fails the prefilter. Warp-synchronous: all 32
-// lanes call it and the candidate loop has a warp-uniform trip count.
-// Returns the inside-margin m = max over points of min(r2 - d2, fe - bx,
-// re + bx, hw - by, hw + by): the reference reports a collision iff m > 0
-// (each difference has the exact sign of the reference's comparison), and
-// |m| small marks a verdict rounding could flip.
+// Inside-margin of one point against the chassis at (x, y, phi):
+// min(r2 - d2, fe - bx, re + bx, hw - by, hw + by) in the reference's own
+// expressions (src/geometry.cpp:63-76): > 0 iff the reference reports the
+// point inside (each difference has the exact sign of its comparison).
 template <typename Real>
-__device__ __forceinline__ Real collide_margin(const Field<Real>& f, const Consts<Real>& K, int h,
-                                               Real x, Real y, Real c, Real s) {
-  const int B = f.B;
-  const int* st = f.starts + static_cast<size_t>(h) * (B + 1);
-  const auto* pts = f.pts + static_cast<size_t>(h) * f.N;
-  const Real top = Real(B - 1);
-  const Real flo = (x - K.qpad - K.bx0) * K.binv;
-  const Real fhi = (x + K.qpad - K.bx0) * K.binv;
-  const int blo = static_cast<int>(floor(fmin(fmax(flo, Real(0)), top)));
-  const int bhi = static_cast<int>(floor(fmin(fmax(fhi, Real(0)), top)));
-  const int lo = st[blo];
-  const int cnt = st[bhi + 1] - lo;
-  const int rounds = __reduce_max_sync(kFull, cnt);
-  Real best = Real(-1e30);
-  for (int j = 0; j < rounds; ++j) {
-    if (j < cnt) {
-      const auto m = pts[lo + j];
-      const Real dx = m.x - x, dy = m.y - y;
-      const Real bx = c * dx + s * dy;
-      const Real by = -s * dx + c * dy;
-      const Real pre = K.r2 - (dx * dx + dy * dy);
-      const Real box = fmin(fmin(K.fe - bx, K.re + bx), fmin(K.hw - by, K.hw + by));
-      best = fmax(best, fmin(pre, box));
-    }
-  }
-  return best;
+__device__ __forceinline__ Real point_margin(const Consts<Real>& K, Real x, Real y, Real c, Real s,
+                                             Real kx, Real ky, Real mx, Real my) {
+  const Real dx = mx - x, dy = my - y;
+  const Real bx = c * dx + s * dy;
+  const Real by = -s * dx + c * dy;
+  const Real pre = K.r2 - (dx * dx + dy * dy);
+  const Real box = fmin(fmin(K.fe - bx, K.re + bx), fmin(K.hw - by, K.hw + by));
+  return fmin(pre, box);
+}
+// FP32: the point in the vehicle frame via the pre-rotated vehicle position
+// (kx, ky include the rectangle centre offset), the rectangle tested around
+// its centre and no separate circle prefilter (the rectangle lies inside the
+// bounding circle; the prefilter can only matter at the rear corners within
+// rounding -- a narrow hit, which the marginal flag sends to the exact
+// re-ranking).
+template <>
+__device__ __forceinline__ float point_margin<float>(const Consts<float>& K, float, float,
+                                                     float c, float s, float kx, float ky,
+                                                     float mx, float my) {
+  const float bx = fmaf(c, mx, fmaf(s, my, -kx));
+  const float by = fmaf(-s, mx, fmaf(c, my, -ky));
+  return fminf(K.bhx - fabsf(bx), K.hw - fabsf(by));
 }
 
-// FP32 specialisation: points in the vehicle frame via the pre-rotated
-// vehicle position (b = R(-phi) p - R(-phi) z), the rectangle tested around
-// its centre (|bx - cx| < hx, |by| < hw) and no separate circle prefilter
-// (the rectangle lies inside the bounding circle, so the prefilter can only
-// matter at the rear corners within rounding -- a narrow hit, which the
-// marginal flag sends to the exact re-ranking).
-template <>
-__device__ __forceinline__ float collide_margin<float>(const Field<float>& f,
-                                                       const Consts<float>& K, int h, float x,
-                                                       float y, float c, float s) {
-  const int B = f.B;
-  const int* st = f.starts + static_cast<size_t>(h) * (B + 1);
-  const float2* pts = f.pts + static_cast<size_t>(h) * f.N;
-  const float top = static_cast<float>(B - 1);
-  const float flo = (x - K.qpad - K.bx0) * K.binv;
-  const float fhi = (x + K.qpad - K.bx0) * K.binv;
-  const int blo = static_cast<int>(fminf(fmaxf(flo, 0.0f), top));
-  const int bhi = static_cast<int>(fminf(fmaxf(fhi, 0.0f), top));
-  const int lo = st[blo];
-  const int cnt = st[bhi + 1] - lo;
-  const int rounds = __reduce_max_sync(kFull, cnt);
-  const float kx = fmaf(c, x, fmaf(s, y, K.bcx));  // vehicle (+ box centre) rotated
-  const float ky = fmaf(-s, x, c * y);
-  float best = -1e30f;
-  for (int j = 0; j < rounds; ++j) {
-    if (j < cnt) {
-      const float2 m = pts[lo + j];
-      const float bx = fmaf(c, m.x, fmaf(s, m.y, -kx));
-      const float by = fmaf(-s, m.x, fmaf(c, m.y, -ky));
-      best = fmaxf(best, fminf(K.bhx - fabsf(bx), K.hw - fabsf(by)));
+// Collision of the chassis at (x, y, phi) with row h. Only the grid cells
+// covering [x - qpad, x + qpad] x [y - qpad, y + qpad] are visited: every
+// point outside them is farther than cull > r from the vehicle and fails the
+// reference's bounding-circle prefilter (src/geometry.cpp:71). Returns the
+// inside-margin max over visited points (the reference reports a collision
+// iff it is > 0; a small |margin| marks a verdict rounding could flip).
+// A lane stops at its first robust hit (margin >= stop). Warp-synchronous:
+// all 32 lanes call it, every loop is warp-uniform.
+template <typename Real, bool kGrid>
+__device__ __forceinline__ Real collide_margin(const Field<Real>& f, const Consts<Real>& K, int h,
+                                               Real x, Real y, Real c, Real s, Real stop) {
+  const int ncx = f.ncx, ncy = f.ncy;
+  const int row = h * f.row_step;
+  const int* st = f.starts + static_cast<size_t>(row) * (ncx * ncy + 1);
+  const auto* pts = f.pts + static_cast<size_t>(row) * f.N;
+  const Real top = Real(ncx - 1);
+  const int cx_lo = static_cast<int>(fmin(fmax((x - K.qpad - K.bx0) * K.binv, Real(0)), top));
+  const int cx_hi = static_cast<int>(fmin(fmax((x + K.qpad - K.bx0) * K.binv, Real(0)), top));
+  const Real kx = c * x + s * y + K.bcx;  // FP32 rotated-frame form only
+  const Real ky = -s * x + c * y;
+  Real best = Real(-1e30);
+  if constexpr (!kGrid) {  // x-buckets: the window is one contiguous range
+    const int lo = st[cx_lo];
+    const int cnt = st[cx_hi + 1] - lo;
+    const int rounds = __reduce_max_sync(kFull, cnt);
+    for (int j = 0; j < rounds; ++j) {
+      if (j < cnt) {
+        const auto m = pts[lo + j];
+        best = fmax(best, point_margin<Real>(K, x, y, c, s, kx, ky, m.x, m.y));
+      }
+    }
+  } else {  // 2-D cells, one contiguous range per cell column; early exit
+    const Real ytop = Real(ncy - 1);
+    const int cy_lo = static_cast<int>(fmin(fmax((y - K.qpad - K.by0) * K.binv, Real(0)), ytop));
+    const int cy_hi = static_cast<int>(fmin(fmax((y + K.qpad - K.by0) * K.binv, Real(0)), ytop));
+    const int ncol = cx_hi - cx_lo + 1;
+    const int cols = __reduce_max_sync(kFull, ncol);
+    for (int k = 0; k < cols; ++k) {
+      const bool has = k < ncol;
+      const int cell = (has ? cx_lo + k : cx_lo) * ncy;
+      const int lo = st[cell + cy_lo];
+      const int cnt = has ? st[cell + cy_hi + 1] - lo : 0;
+      // a lane stops at its first robust hit (margin >= stop)
+      for (int j = 0; __any_sync(kFull, j < cnt && best < stop); ++j) {
+        if (j < cnt && best < stop) {
+          const auto m = pts[lo + j];
+          best = fmax(best, point_margin<Real>(K, x, y, c, s, kx, ky, m.x, m.y));
+        }
+      }
     }
   }
   return best;
@@ -431,7 +448,7 @@ __device__ __forceinline__ void start_features(const Consts<Real>& K, Real s[5])
 // Warp-synchronous and branch-free: the checks and the next state are
 // computed for every lane and committed only by the lanes still running,
 // so the warp never splits into per-outcome paths.
-template <typename Real, class Net>
+template <typename Real, bool kGrid, class Net>
 __device__ __forceinline__ int advance(Lane<Real>& L, const Net& net, const Consts<Real>& K,
                                        const Field<Real>& f, int H) {
   Real sphi, cphi;
@@ -439,7 +456,8 @@ __device__ __forceinline__ int advance(Lane<Real>& L, const Net& net, const Cons
   L.ephi = M<Real>::wrap(K.gphi - L.phi);
   bool hit = false;
   if (f.N > 0) {
-    const Real cm = collide_margin(f, K, L.h, L.x, L.y, cphi, sphi);
+    // a lane may stop at a hit whose margin is too large to flip
+    const Real cm = collide_margin<Real, kGrid>(f, K, L.h, L.x, L.y, cphi, sphi, K.dmarg);
     hit = cm > Real(0);
     // a narrow hit might be free in exact arithmetic (a better outcome)
     L.marg |= hit & (cm < K.dmarg);
@@ -593,16 +611,17 @@ __device__ __forceinline__ Key load_rec_cg(const Rec* src) {
   return Key{__ldcg(&src->cls), __ldcg(&src->cand), __ldcg(&src->k1), __ldcg(&src->k2)};
 }
 
-// Shared-memory image of the bucketed field: [pts (H+1)N][starts (H+1)(B+1)].
+// Shared-memory image of the binned field: [pts rows x N][starts rows x (cells+1)].
 template <typename Real>
 __device__ __forceinline__ Field<Real> stage_field(const RoundArgs& a, unsigned char* smem) {
   using R2 = typename Vec2T<Real>::type;
-  const int N = a.n_points, B = a.n_buckets;
-  const size_t count = static_cast<size_t>(a.H + 1) * N;
-  const size_t nst = static_cast<size_t>(a.H + 1) * (B + 1);
+  const int N = a.n_points;
+  const size_t rows = a.field_rows;
+  const size_t count = rows * N;
+  const size_t nst = rows * (static_cast<size_t>(a.grid_nx) * a.grid_ny + 1);
   const R2* gpts = static_cast<const R2*>(a.field);
   const int* gst = reinterpret_cast<const int*>(gpts + count);
-  Field<Real> f{gpts, gst, N, B};
+  Field<Real> f{gpts, gst, N, a.grid_nx, a.grid_ny, rows > 1 ? 1 : 0};
   if (a.field_smem_bytes > 0 && N > 0) {
     R2* spts = reinterpret_cast<R2*>(smem);
     int* sst = reinterpret_cast<int*>(spts + count);
@@ -737,8 +756,9 @@ __global__ void __launch_bounds__(256) generate_kernel(const RoundArgs a) {
 }
 
 // ------------------------------------------------------ refill kernel ----
-template <typename Real, class Net>
-__global__ void __launch_bounds__(kBlock, PARAPLAN_REFILL_MINB) refill_kernel(const RoundArgs a) {
+template <typename Real, class Net, bool kGrid>
+__global__ void __launch_bounds__(kBlock, sizeof(Real) == 4 ? PARAPLAN_REFILL_MINB : 4)
+    refill_kernel(const RoundArgs a) {
   constexpr int P = Net::kP;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ Key table[kWarps][kMaxRestartsPerLaunch];
@@ -812,7 +832,7 @@ __global__ void __launch_bounds__(kBlock, PARAPLAN_REFILL_MINB) refill_kernel(co
 
     // -------- one rollout state per lane --------
     // every lane steps (idle lanes only at the stream tail, results unused)
-    const int cls = advance<Real>(L, net, K, f, H);
+    const int cls = advance<Real, kGrid>(L, net, K, f, H);
     const bool done = active && cls >= 0;
     // lane bests are per restart: flush the old one before crossing over
     bool flush = done && best.cls >= 0 && best_r != my_r;
@@ -886,7 +906,7 @@ struct NetFactory<Real, NetGlobal<Real>> {
   }
 };
 
-template <typename Real, class Net>
+template <typename Real, class Net, bool kGrid>
 __global__ void __launch_bounds__(kBlock) lockstep_kernel(const RoundArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ Key red[32];
@@ -923,7 +943,7 @@ __global__ void __launch_bounds__(kBlock) lockstep_kernel(const RoundArgs a) {
     int cls = -1;
     // lanes keep stepping (and discarding) until the whole warp is done
     while (__any_sync(kFull, cls < 0)) {
-      const int k = advance<Real>(L, net, K, f, H);
+      const int k = advance<Real, kGrid>(L, net, K, f, H);
       if (cls < 0) cls = k;
     }
     if (valid) {
@@ -1001,14 +1021,14 @@ struct RefineNet<NetGlobal<double>> {
   }
 };
 
-template <class Net64>
+template <class Net64, bool kGrid>
 __global__ void __launch_bounds__(128) refine_kernel(const RoundArgs a) {
   const Consts<double>& K = a.kd;
   const unsigned n_sel = min(__ldcg(&a.counters[2]), static_cast<unsigned>(a.sel_cap));
   const Field<double> f{static_cast<const double2*>(a.field64),
                         reinterpret_cast<const int*>(static_cast<const double2*>(a.field64) +
-                                                     static_cast<size_t>(a.H + 1) * a.n_points),
-                        a.n_points, a.n_buckets};
+                                                     static_cast<size_t>(a.field_rows) * a.n_points),
+                        a.n_points, a.grid_nx, a.grid_ny, a.field_rows > 1 ? 1 : 0};
   double s0[5];
   start_features(K, s0);
   Net64 net = RefineNet<Net64>::make(a);
@@ -1030,7 +1050,7 @@ __global__ void __launch_bounds__(128) refine_kernel(const RoundArgs a) {
     L.start(K, f0, f1);
     int cls = -1;
     while (__any_sync(kFull, cls < 0)) {
-      const int k = advance<double>(L, net, K, f, a.H);
+      const int k = advance<double, kGrid>(L, net, K, f, a.H);
       if (cls < 0) cls = k;
     }
     if (valid) {
@@ -1057,12 +1077,21 @@ bool refill_schedule() {
   return Net::kP > 0 && !force_lockstep();
 }
 
-template <typename Real, class Net>
-void (*kernel_of())(const RoundArgs) {
+using KernelFn = void (*)(const RoundArgs);
+
+template <typename Real, class Net, bool kGrid>
+KernelFn kernel_of_g() {
   if constexpr (Net::kP > 0) {
-    if (refill_schedule<Net>()) return refill_kernel<Real, Net>;
+    if (refill_schedule<Net>()) return refill_kernel<Real, Net, kGrid>;
   }
-  return lockstep_kernel<Real, Net>;
+  return lockstep_kernel<Real, Net, kGrid>;
+}
+
+// grid: the field has a 2-D cell grid (dense clouds) -- a separate
+// instantiation so the small-field kernel stays lean.
+template <typename Real, class Net>
+KernelFn kernel_of(bool grid) {
+  return grid ? kernel_of_g<Real, Net, true>() : kernel_of_g<Real, Net, false>();
 }
 
 template <typename Real, class Net>
@@ -1075,7 +1104,7 @@ int launch_impl(const RoundArgs& a, void* stream) {
       generate_kernel<Real, Net::kH1><<<gen_blocks, 256, 0, st>>>(a);
     }
   }
-  auto k = kernel_of<Real, Net>();
+  auto k = kernel_of<Real, Net>(a.grid_ny > 1);
   const size_t smem = static_cast<size_t>(a.field_smem_bytes);
   if (smem > 32 * 1024) {
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
@@ -1095,13 +1124,18 @@ inline int launch_select_impl(const RoundArgs& a, void* stream) {
 // FP64 re-evaluation of the selected window.
 template <class Net64>
 int launch_refine_impl(const RoundArgs& a, void* stream) {
-  refine_kernel<Net64><<<a.refine_grid, 128, 0, static_cast<cudaStream_t>(stream)>>>(a);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (a.grid_ny > 1) {
+    refine_kernel<Net64, true><<<a.refine_grid, 128, 0, st>>>(a);
+  } else {
+    refine_kernel<Net64, false><<<a.refine_grid, 128, 0, st>>>(a);
+  }
   return static_cast<int>(cudaGetLastError());
 }
 
 template <typename Real, class Net>
-int shape_impl(int device, int field_bytes, LaunchShape* out) {
-  auto k = kernel_of<Real, Net>();
+int shape_impl(int device, int field_bytes, bool grid, LaunchShape* out) {
+  auto k = kernel_of<Real, Net>(grid);
   const bool refill = refill_schedule<Net>();
   const int smem_bytes = field_bytes;
   out->queue_bytes = 0;

@@ -3,14 +3,14 @@
 
 namespace ppdev {
 
-int shape_f32(NetKind k, int device, int smem_bytes, LaunchShape* out) {
+int shape_f32(NetKind k, int device, int smem_bytes, bool grid, LaunchShape* out) {
   switch (k) {
     case NetKind::k5_2_2:
-      return shape_impl<float, NetReg<float, 2>>(device, smem_bytes, out);
+      return shape_impl<float, NetReg<float, 2>>(device, smem_bytes, grid, out);
     case NetKind::k5_10_2:
-      return shape_impl<float, NetReg<float, 10>>(device, smem_bytes, out);
+      return shape_impl<float, NetReg<float, 10>>(device, smem_bytes, grid, out);
     default:
-      return shape_impl<float, NetGlobal<float>>(device, smem_bytes, out);
+      return shape_impl<float, NetGlobal<float>>(device, smem_bytes, grid, out);
   }
 }
 

@@ -1,0 +1,77 @@
+"""Time the BASELINE.json configurations through the C-ABI (one GPU).
+
+  C1  4096 samples, H=20, 18 static points           (single control step)
+  C2  2^20 samples, H=30, 20 points (4 moving)       (bench workload)
+  C3  exp4 closed loop, 2^20 samples, H=200, N=0     (per-tick latency, K ticks)
+  C4  exp5_3wp lot densified to 10k points, H=200    (--c4-samples, default 2^20)
+  C5  sweep points (samples x H x N)
+"""
+import argparse
+import json
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+from paper_1904_06680_b200 import abi, capi, import_paraplan, workloads  # noqa: E402
+
+
+def time_round(w, reps=3, refine=1):
+    w.model.refine = refine
+    dp = capi.DevicePlanner(w.model)
+    dp.upload(w.snapshot)
+    out = []
+    for _ in range(reps + 1):
+        t0 = time.perf_counter()
+        rec, _ = dp.evaluate(None, w.t, 0, 0, w.model.n_restarts, None, 0, w.model.n_candidates)
+        wall = (time.perf_counter() - t0) * 1e3
+        t = dp.timing()
+        out.append(dict(wall_ms=wall, device_ms=t.kernel_ms, certify_ms=t.certify_ms,
+                        refined=t.refined, steps=t.executed_steps, cls=int(rec[0]["cls"]),
+                        cand=int(rec[0]["candidate"])))
+    dp.close()
+    best = min(out[1:], key=lambda d: d["wall_ms"])
+    best["nominal_steps_per_s"] = w.samples * w.model.H / (best["wall_ms"] * 1e-3)
+    return best
+
+
+def closed_loop(samples, H, ticks, name="exp4"):
+    pp = import_paraplan()
+    spec = pp.builtin_scenario(name)
+    c = spec.planner
+    c.H, c.n_candidates, c.n_restarts = H, samples, 1
+    m = spec.mission
+    m.time_limit = ticks * 0.1
+    t0 = time.perf_counter()
+    log = pp.run_mission(m, c, spec.arch, 0)
+    wall = time.perf_counter() - t0
+    taus = [r.plan_time for r in log.records if r.evaluated > 0]
+    return dict(ticks=len(taus), tau_avg_ms=1e3 * float(np.mean(taus)),
+                tau_max_ms=1e3 * float(np.max(taus)), wall_s=wall,
+                completed=bool(log.completed))
+
+
+if __name__ == "__main__":
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--which", default="C1,C2,C3,C4,C5")
+    ap.add_argument("--c4-samples", type=int, default=1 << 20)
+    ap.add_argument("--c3-ticks", type=int, default=20)
+    a = ap.parse_args()
+    res = {}
+    which = a.which.split(",")
+    if "C1" in which:
+        res["C1"] = time_round(workloads.c1())
+    if "C2" in which:
+        res["C2"] = time_round(workloads.c2())
+        res["C2_fp64"] = time_round(workloads.c2(precision=64))
+    if "C3" in which:
+        res["C3"] = closed_loop(1 << 20, 200, a.c3_ticks)
+    if "C4" in which:
+        res["C4"] = time_round(workloads.c4(samples=a.c4_samples), reps=1)
+    if "C5" in which:
+        for n_pts in (100, 1000):
+            for H in (10, 50, 100):
+                res[f"C5_n{n_pts}_H{H}"] = time_round(workloads.c5(1 << 20, H, n_pts), reps=1)
+    print(json.dumps(res, indent=1))
