@@ -77,7 +77,7 @@ def _free_port():
 
 @pytest.mark.parametrize("world", [2, 3])
 def test_sharded_plan_matches_single_process(world):
-    mgr = mp.Manager()
+    mgr = mp.get_context("spawn").Manager()
     results = mgr.dict()
     mp.spawn(_worker, args=(world, _free_port(), results), nprocs=world, join=True)
     for name, t_snap, cfg, t in CASES:

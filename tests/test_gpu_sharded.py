@@ -45,7 +45,7 @@ def _port():
 
 
 def test_two_ranks_equal_one_gpu_plan():
-    mgr = mp.Manager()
+    mgr = mp.get_context("spawn").Manager()
     out = mgr.dict()
     mp.spawn(_worker, args=(2, _port(), out), nprocs=2, join=True)
     w = workloads.c2(samples=1 << 10)
