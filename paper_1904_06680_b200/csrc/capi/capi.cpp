@@ -238,6 +238,18 @@ bool key_better(const Key& a, const Key& b) {  // src/planner.cpp:40-44
 
 }  // namespace
 
+// Host-side cell index of the resident obstacle field, used by the exact FP64
+// rollouts (epilogue, certification) for large clouds: same visiting rule as
+// the device (only points within cull > r of the vehicle in x and y), so the
+// verdict equals the reference's brute-force scan (src/geometry.cpp:63-76).
+struct HostGrid {
+  bool on = false;
+  int rows = 0, nx = 0, ny = 0, N = 0;
+  double x0 = 0, y0 = 0, g = 1, cull = 0;
+  std::vector<int32_t> starts;  // rows x (nx*ny + 1)
+  std::vector<double> pts;      // rows x N x 2, cell order
+};
+
 struct pp_handle {
   pp_model model{};
   std::vector<int32_t> sizes;
@@ -273,6 +285,7 @@ struct pp_handle {
   int field_smem_bytes = 0;
 
   pp_timing timing{};
+  HostGrid hgrid;
 };
 
 namespace {
@@ -491,6 +504,46 @@ void upload_snapshot(pp_handle* h, const pp_snapshot& s) {
   h->snap_copy.field_H = cfg.H;
   h->snap_copy.warm_theta = h->snap_warm.data();
   h->snapshot = &h->snap_copy;
+  // host cell index for the exact rollouts of large clouds
+  HostGrid& hg = h->hgrid;
+  hg.on = N >= 64;
+  if (hg.on) {
+    hg.rows = static_cast<int>(rows);
+    hg.N = N;
+    hg.cull = cull;
+    hg.g = cull;
+    hg.x0 = xmin;
+    hg.y0 = ymin;
+    hg.nx = static_cast<int>(std::floor((xmax - xmin) / hg.g)) + 1;
+    hg.ny = static_cast<int>(std::floor((ymax - ymin) / hg.g)) + 1;
+    while (static_cast<double>(hg.nx) * hg.ny > 65536.0) {
+      hg.g *= 1.5;
+      hg.nx = static_cast<int>(std::floor((xmax - xmin) / hg.g)) + 1;
+      hg.ny = static_cast<int>(std::floor((ymax - ymin) / hg.g)) + 1;
+    }
+    const int cells = hg.nx * hg.ny;
+    hg.starts.assign(static_cast<size_t>(hg.rows) * (cells + 1), 0);
+    hg.pts.resize(static_cast<size_t>(hg.rows) * N * 2);
+    std::vector<int32_t> cellof(N), fillv(cells + 1);
+    for (int row = 0; row < hg.rows; ++row) {
+      const double* src = s.field_xy + static_cast<size_t>(row) * row_len;
+      std::fill(fillv.begin(), fillv.end(), 0);
+      for (int j = 0; j < N; ++j) {
+        const int cx = std::min(hg.nx - 1, std::max(0, static_cast<int>(std::floor((src[2 * j] - hg.x0) / hg.g))));
+        const int cy = std::min(hg.ny - 1, std::max(0, static_cast<int>(std::floor((src[2 * j + 1] - hg.y0) / hg.g))));
+        cellof[j] = cx * hg.ny + cy;
+        ++fillv[cellof[j] + 1];
+      }
+      for (int c = 0; c < cells; ++c) fillv[c + 1] += fillv[c];
+      std::copy(fillv.begin(), fillv.end(), hg.starts.begin() + static_cast<size_t>(row) * (cells + 1));
+      double* dst = hg.pts.data() + static_cast<size_t>(row) * N * 2;
+      for (int j = 0; j < N; ++j) {
+        const int at = fillv[cellof[j]]++;
+        dst[2 * at] = src[2 * j];
+        dst[2 * at + 1] = src[2 * j + 1];
+      }
+    }
+  }
   // stage the field in shared memory when it fits; larger fields are read
   // through L1/L2
   h->field_smem_bytes = (count > 0 && bytes <= 40 * 1024) ? static_cast<int>(bytes) : 0;
@@ -915,6 +968,32 @@ void run_round(pp_handle* h, uint64_t t, int iter, int r0, int rc, const double*
 // Host FP64 rollout: src/planner.cpp:66-191 expressed through the public
 // primitives (bit-identical under -ffp-contract=off; the reference's own
 // selfcheck::resimulate_rollout relies on the same equivalence).
+// Collision at state k against the resident field through the cell index:
+// the reference's own per-point test (src/geometry.cpp:63-76), points
+// farther than cull > r in x or y skipped (they fail its prefilter).
+bool grid_collision(const HostGrid& hg, const paraplan::ChassisPolytope& ch, int k, double x,
+                    double y, double phi) {
+  const int row = hg.rows > 1 ? k : 0;
+  const int cells = hg.nx * hg.ny;
+  const int32_t* st = hg.starts.data() + static_cast<size_t>(row) * (cells + 1);
+  const double* pts = hg.pts.data() + static_cast<size_t>(row) * hg.N * 2;
+  const auto cell = [&](double v, double v0, int n) {
+    return std::min(n - 1, std::max(0, static_cast<int>(std::floor((v - v0) / hg.g))));
+  };
+  const int cx0 = cell(x - hg.cull, hg.x0, hg.nx), cx1 = cell(x + hg.cull, hg.x0, hg.nx);
+  const int cy0 = cell(y - hg.cull, hg.y0, hg.ny), cy1 = cell(y + hg.cull, hg.y0, hg.ny);
+  const double c = std::cos(phi), s = std::sin(phi);
+  const double r2 = ch.bounding_radius() * ch.bounding_radius();
+  for (int cx = cx0; cx <= cx1; ++cx) {
+    for (int j = st[cx * hg.ny + cy0]; j < st[cx * hg.ny + cy1 + 1]; ++j) {
+      const double dx = pts[2 * j] - x, dy = pts[2 * j + 1] - y;
+      if (dx * dx + dy * dy >= r2) continue;
+      if (ch.contains({c * dx + s * dy, -s * dx + c * dy})) return true;
+    }
+  }
+  return false;
+}
+
 void host_rollout(const pp_handle* h, const pp_snapshot& s, const double* theta,
                   pp_rollout_stats* out, double* traj, int32_t cap, int32_t* traj_len) {
   using namespace paraplan;
@@ -952,9 +1031,12 @@ void host_rollout(const pp_handle* h, const pp_snapshot& s, const double* theta,
   double path = 0.0;
   for (int k = 0;; ++k) {
     if (N > 0) {
+      // the resident snapshot's large clouds go through the cell index
+      const bool indexed = h->hgrid.on && s.field_xy == h->snap_copy.field_xy;
       const std::span<const Vec2> row(
           reinterpret_cast<const Vec2*>(s.field_xy) + static_cast<size_t>(k) * N, N);
-      if (collision({z.x, z.y, z.phi}, row, h->chassis)) {
+      if (indexed ? grid_collision(h->hgrid, h->chassis, k, z.x, z.y, z.phi)
+                  : collision({z.x, z.y, z.phi}, row, h->chassis)) {
         out->collided = 1;
         break;
       }
@@ -1265,7 +1347,7 @@ pp_status pp_plan_step(pp_handle* h, const pp_snapshot* snap, uint64_t t, pp_pla
     out->evaluated = evaluated;
     if (out->best_theta != nullptr) std::memcpy(out->best_theta, best_theta.data(), sizeof(double) * P);
     int32_t len = 0;
-    host_rollout(h, *snap, best_theta.data(), &out->predicted, out->trajectory, cfg.H + 1, &len);
+    host_rollout(h, *h->snapshot, best_theta.data(), &out->predicted, out->trajectory, cfg.H + 1, &len);
     out->trajectory_len = len;
     out->success = out->predicted.reached && !out->predicted.collided;
     if (any_free) {

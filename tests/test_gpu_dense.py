@@ -1,0 +1,44 @@
+"""Dense obstacle clouds: the 2-D cell grid, static-row dedup, early exit and
+the host cell index must give the reference's verdicts exactly (the oracle
+scans every point of every row)."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from oracle.oracle import Port
+from paper_1904_06680_b200 import abi, capi, workloads
+
+pytestmark = pytest.mark.gpu
+
+
+def _plan_equal(w):
+    o1, th1, tr1 = Port(w.model).plan_step(w.snapshot, w.t)
+    o2, th2, tr2 = capi.DevicePlanner(w.model).plan_step(w.snapshot, w.t)
+    assert np.array_equal(th1, th2) and np.array_equal(tr1, tr2)
+    assert (o1.action_a0, o1.action_a1, o1.success) == (o2.action_a0, o2.action_a1, o2.success)
+
+
+@pytest.mark.parametrize("n_points", [200, 1000])
+@pytest.mark.parametrize("precision", [32, 64])
+def test_c5_cloud_plan_matches_oracle(n_points, precision):
+    w = workloads.c5(4096, 30, n_points, precision=precision)
+    _plan_equal(w)
+
+
+def test_c4_lot_plan_matches_oracle():
+    w = workloads.c4(samples=2048, H=60)
+    _plan_equal(w)
+
+
+@pytest.mark.parametrize("precision", [32, 64])
+def test_c4_lot_per_sample_stats(precision):
+    w = workloads.c4(samples=1024, H=40, precision=precision)
+    w.model.refine = 0
+    dp = capi.DevicePlanner(w.model)
+    _, got = dp.evaluate(w.snapshot, w.t, 0, 0, 1, None, 0, 1024, per_sample=True)
+    want = Port(w.model).eval_candidates(w.snapshot, w.t, 0, 0, np.zeros(18), 0, 1024)
+    flips = np.count_nonzero(got["collided"] != want["collided"])
+    assert flips <= (0 if precision == 64 else 5)
+    same = got["steps"] == want["steps"]
+    assert same.mean() >= 0.99
