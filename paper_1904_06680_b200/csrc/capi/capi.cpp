@@ -33,6 +33,7 @@
 #include <vector>
 
 #include "../cuda/device_api.h"
+#include "field.hpp"
 #include "paraplan/geometry.hpp"
 #include "paraplan/planner.hpp"
 #include "paraplan/policy.hpp"
@@ -238,18 +239,6 @@ bool key_better(const Key& a, const Key& b) {  // src/planner.cpp:40-44
 
 }  // namespace
 
-// Host-side cell index of the resident obstacle field, used by the exact FP64
-// rollouts (epilogue, certification) for large clouds: same visiting rule as
-// the device (only points within cull > r of the vehicle in x and y), so the
-// verdict equals the reference's brute-force scan (src/geometry.cpp:63-76).
-struct HostGrid {
-  bool on = false;
-  int rows = 0, nx = 0, ny = 0, N = 0;
-  double x0 = 0, y0 = 0, g = 1, cull = 0;
-  std::vector<int32_t> starts;  // rows x (nx*ny + 1)
-  std::vector<double> pts;      // rows x N x 2, cell order
-};
-
 struct pp_handle {
   pp_model model{};
   std::vector<int32_t> sizes;
@@ -273,7 +262,7 @@ struct pp_handle {
   bool rerank = true;
   const pp_snapshot* snapshot = nullptr;  // -> snap_copy once a snapshot is resident
   pp_snapshot snap_copy{};
-  std::vector<double> snap_field, snap_warm;
+  std::vector<double> snap_warm;
   uint32_t h_selcount = 0;
   double sel_rho = 1e-3;   // FP32 window: cost <= best * (1 + rho) + 1e-6
   std::unique_ptr<HostPool> pool;  // exact re-evaluation of near ties
@@ -285,7 +274,11 @@ struct pp_handle {
   int field_smem_bytes = 0;
 
   pp_timing timing{};
-  HostGrid hgrid;
+  // resident obstacle field: FP64 binned image (host) + device images
+  ppfield::Binned field;
+  bool field64_ready = false;
+  DevBuf d_field64;
+  HostBuf h_field64;
 };
 
 namespace {
@@ -340,6 +333,65 @@ void fill_consts(const ppdev::RoundArgs& a, ppdev::ConstsT<Real>* k) {
   k->tan_small = a.delta_max <= 0.785 ? 1 : 0;
 }
 
+// Device image of h->field in the compute precision (one H2D); the FP64 image
+// for the near-tie re-ranking is uploaded only when a round needs it.
+void finish_field(pp_handle* h, ppdev::RoundArgs& a) {
+  const ppfield::Binned& b = h->field;
+  a.field_ns = b.Ns;
+  a.field_nd = b.Nd;
+  a.grid_nx = b.nx;
+  a.grid_ny = b.ny;
+  a.grid_x0 = b.x0;
+  a.grid_y0 = b.y0;
+  a.grid_g = b.g;
+  const size_t elem = h->fp64 ? sizeof(double) : sizeof(float);
+  const ppfield::Layout l = ppfield::layout(b, elem), l64 = ppfield::layout(b, sizeof(double));
+  a.lay = {static_cast<int64_t>(l.dpts), static_cast<int64_t>(l.sst), static_cast<int64_t>(l.dst),
+           static_cast<int64_t>(l.bytes)};
+  a.lay64 = {static_cast<int64_t>(l64.dpts), static_cast<int64_t>(l64.sst),
+             static_cast<int64_t>(l64.dst), static_cast<int64_t>(l64.bytes)};
+  a.field = nullptr;
+  a.field64 = nullptr;
+  h->field64_ready = false;
+  if (b.points() > 0) {
+    h->h_field.reserve(l.bytes, "pinned field");
+    h->d_field.reserve(l.bytes, "device field");
+    ppfield::pack(b, h->fp64, h->h_field.p);
+    ck(cudaMemcpyAsync(h->d_field.p, h->h_field.p, l.bytes, cudaMemcpyHostToDevice, h->stream),
+       "field H2D");
+    h->timing.h2d_bytes += static_cast<int64_t>(l.bytes);
+    a.field = h->d_field.p;
+    if (h->fp64) {
+      a.field64 = h->d_field.p;
+      h->field64_ready = true;
+    }
+  }
+  a.dmarg32 = h->dmarg32;
+  fill_consts(a, &a.kf);
+  fill_consts(a, &a.kd);
+  // stage the field in shared memory when it fits; larger fields are read
+  // through L1/L2
+  h->field_smem_bytes = (b.points() > 0 && l.bytes <= 40 * 1024) ? static_cast<int>(l.bytes) : 0;
+}
+
+// FP64 field image on the device (FP32 rounds that need the FP64 refine or
+// the FP64 fallback).
+const void* ensure_field64(pp_handle* h) {
+  if (h->field.points() == 0) return nullptr;
+  if (!h->field64_ready) {
+    const ppfield::Layout l64 = ppfield::layout(h->field, sizeof(double));
+    h->h_field64.reserve(l64.bytes, "pinned field64");
+    h->d_field64.reserve(l64.bytes, "device field64");
+    ppfield::pack(h->field, true, h->h_field64.p);
+    ck(cudaMemcpyAsync(h->d_field64.p, h->h_field64.p, l64.bytes, cudaMemcpyHostToDevice,
+                       h->stream),
+       "field64 H2D");
+    h->timing.h2d_bytes += static_cast<int64_t>(l64.bytes);
+    h->field64_ready = true;
+  }
+  return h->d_field64.p;
+}
+
 // Goal transform and constants of a snapshot (src/planner.cpp:70-81).
 void upload_snapshot(pp_handle* h, const pp_snapshot& s) {
   const auto& cfg = h->cfg;
@@ -390,163 +442,26 @@ void upload_snapshot(pp_handle* h, const pp_snapshot& s) {
   a.n_layers = static_cast<int32_t>(h->sizes.size());
   for (size_t i = 0; i < h->sizes.size(); ++i) a.sizes[i] = h->sizes[i];
 
-  // Only rows 0..H are ever read; ship those, in the compute precision,
-  // each row ordered by grid cell with per-cell start offsets so the kernel
-  // visits only the points near the vehicle (the collision verdict is an OR
-  // over the row's points, independent of their order). A static field
-  // (every row identical) ships one row.
+  // Only rows 0..H are ever read (src/planner.cpp:139 at h <= H): split
+  // into static and dynamic points and bin them (csrc/capi/field.hpp).
   const int N = s.n_points;
   a.n_points = N;
-  const size_t all_rows = static_cast<size_t>(cfg.H + 1);
-  const size_t row_len = 2 * static_cast<size_t>(N);
-  bool is_static = N > 0;
-  for (size_t row = 1; row < all_rows && is_static; ++row) {
-    is_static = std::memcmp(s.field_xy, s.field_xy + row * row_len, row_len * sizeof(double)) == 0;
-  }
-  const size_t rows = is_static ? 1 : all_rows;
-  const size_t count = rows * static_cast<size_t>(N);
-  const size_t elem = h->fp64 ? sizeof(double) : sizeof(float);
-  double xmin = 0.0, xmax = 0.0, ymin = 0.0, ymax = 0.0;
-  for (size_t i = 0; i < count; ++i) {
-    const double x = s.field_xy[2 * i], y = s.field_xy[2 * i + 1];
-    if (i == 0 || x < xmin) xmin = x;
-    if (i == 0 || x > xmax) xmax = x;
-    if (i == 0 || y < ymin) ymin = y;
-    if (i == 0 || y > ymax) ymax = y;
-  }
-  // cell size: half the collision window; a 2-D grid only for larger clouds,
-  // at most ~4096 cells per row
   const double cull = std::sqrt(a.r2) + 1e-3;
-  double cg = 0.5 * cull;
-  int nx = 1, ny = 1;
-  if (count > 0) {
-    if (!(std::isfinite(xmin) && std::isfinite(xmax) && std::isfinite(ymin) && std::isfinite(ymax))) {
-      throw std::invalid_argument("obstacle field has non-finite coordinates");
-    }
-    const bool two_d = N >= 128;
-    const double wx = xmax - xmin, wy = two_d ? ymax - ymin : 0.0;
-    const double cap = two_d ? 4096.0 : 4096.0;
-    while ((std::floor(wx / cg) + 1) * (two_d ? std::floor(wy / cg) + 1 : 1.0) > cap) cg *= 1.25;
-    nx = static_cast<int>(std::floor(wx / cg)) + 1;
-    ny = two_d ? static_cast<int>(std::floor(wy / cg)) + 1 : 1;
+  if (N > 0) {
+    ppfield::from_rows(h->field, s.field_xy, cfg.H + 1, N, cull);
+  } else {
+    h->field = ppfield::Binned{};
+    h->field.rows = cfg.H + 1;
+    h->field.cull = cull;
   }
-  const int cells = nx * ny;
-  a.field_rows = static_cast<int32_t>(rows);
-  a.grid_nx = nx;
-  a.grid_ny = ny;
-  a.grid_x0 = xmin;
-  a.grid_y0 = ymin;
-  a.grid_g = cg;
-  const size_t pts_bytes = 2 * count * elem;
-  const size_t st_bytes = rows * (cells + 1) * sizeof(int32_t);
-  // padded to 16 bytes so the FP64 image after it is double2-aligned
-  const size_t bytes = (pts_bytes + st_bytes + 15) & ~size_t(15);
-  // FP32 rounds also get an FP64 image for the near-tie re-ranking
-  const size_t pts64_bytes = 2 * count * sizeof(double);
-  const size_t bytes64 = h->fp64 ? 0 : pts64_bytes + st_bytes;
-  if (count > 0) {
-    h->h_field.reserve(bytes + bytes64, "pinned field");
-    h->d_field.reserve(bytes + bytes64, "device field");
-    unsigned char* base = static_cast<unsigned char*>(h->h_field.p);
-    int32_t* starts = reinterpret_cast<int32_t*>(base + pts_bytes);
-    unsigned char* base64 = base + bytes;
-    int32_t* starts64 = reinterpret_cast<int32_t*>(base64 + pts64_bytes);
-    std::vector<int32_t> order(N), cell(N), fill(cells + 1);
-    for (size_t row = 0; row < rows; ++row) {
-      const double* src = s.field_xy + row * row_len;
-      // counting sort by cell (stable)
-      std::fill(fill.begin(), fill.end(), 0);
-      for (int j = 0; j < N; ++j) {
-        const int cx = std::min(nx - 1, std::max(0, static_cast<int>(std::floor((src[2 * j] - xmin) / cg))));
-        const int cy = ny == 1 ? 0
-                               : std::min(ny - 1, std::max(0, static_cast<int>(std::floor(
-                                                              (src[2 * j + 1] - ymin) / cg))));
-        cell[j] = cx * ny + cy;
-        ++fill[cell[j] + 1];
-      }
-      for (int c = 0; c < cells; ++c) fill[c + 1] += fill[c];
-      int32_t* st = starts + row * (cells + 1);
-      std::copy(fill.begin(), fill.end(), st);
-      if (bytes64 > 0) std::copy(fill.begin(), fill.end(), starts64 + row * (cells + 1));
-      for (int j = 0; j < N; ++j) order[fill[cell[j]]++] = j;
-      const size_t o = row * N;
-      for (int j = 0; j < N; ++j) {
-        const double px = src[2 * order[j]], py = src[2 * order[j] + 1];
-        if (h->fp64) {
-          double* pts = reinterpret_cast<double*>(base) + 2 * (o + j);
-          pts[0] = px;
-          pts[1] = py;
-        } else {
-          float* pts = reinterpret_cast<float*>(base) + 2 * (o + j);
-          pts[0] = static_cast<float>(px);
-          pts[1] = static_cast<float>(py);
-          double* p64 = reinterpret_cast<double*>(base64) + 2 * (o + j);
-          p64[0] = px;
-          p64[1] = py;
-        }
-      }
-    }
-    ck(cudaMemcpyAsync(h->d_field.p, h->h_field.p, bytes + bytes64, cudaMemcpyHostToDevice,
-                       h->stream),
-       "field H2D");
-    h->timing.h2d_bytes += static_cast<int64_t>(bytes + bytes64);
-  }
-  a.dmarg32 = h->dmarg32;
-  fill_consts(a, &a.kf);
-  fill_consts(a, &a.kd);
-  a.field = h->d_field.p;
-  a.field64 = h->fp64 ? h->d_field.p : static_cast<unsigned char*>(h->d_field.p) + bytes;
-  // host copy for the exact re-ranking of FP64 near-ties (rows 0..H)
-  h->snap_field.assign(s.field_xy, s.field_xy + all_rows * row_len);
-  h->snap_warm.assign(s.warm_theta, s.warm_theta + std::max(0, s.warm_theta_len));
+  finish_field(h, a);
+  // host copy of the reference snapshot (rows 0..H) for pp_rollout-style use
   h->snap_copy = s;
-  h->snap_copy.field_xy = h->snap_field.data();
+  h->snap_copy.field_xy = nullptr;
   h->snap_copy.field_H = cfg.H;
+  h->snap_warm.assign(s.warm_theta, s.warm_theta + std::max(0, s.warm_theta_len));
   h->snap_copy.warm_theta = h->snap_warm.data();
   h->snapshot = &h->snap_copy;
-  // host cell index for the exact rollouts of large clouds
-  HostGrid& hg = h->hgrid;
-  hg.on = N >= 64;
-  if (hg.on) {
-    hg.rows = static_cast<int>(rows);
-    hg.N = N;
-    hg.cull = cull;
-    hg.g = cull;
-    hg.x0 = xmin;
-    hg.y0 = ymin;
-    hg.nx = static_cast<int>(std::floor((xmax - xmin) / hg.g)) + 1;
-    hg.ny = static_cast<int>(std::floor((ymax - ymin) / hg.g)) + 1;
-    while (static_cast<double>(hg.nx) * hg.ny > 65536.0) {
-      hg.g *= 1.5;
-      hg.nx = static_cast<int>(std::floor((xmax - xmin) / hg.g)) + 1;
-      hg.ny = static_cast<int>(std::floor((ymax - ymin) / hg.g)) + 1;
-    }
-    const int cells = hg.nx * hg.ny;
-    hg.starts.assign(static_cast<size_t>(hg.rows) * (cells + 1), 0);
-    hg.pts.resize(static_cast<size_t>(hg.rows) * N * 2);
-    std::vector<int32_t> cellof(N), fillv(cells + 1);
-    for (int row = 0; row < hg.rows; ++row) {
-      const double* src = s.field_xy + static_cast<size_t>(row) * row_len;
-      std::fill(fillv.begin(), fillv.end(), 0);
-      for (int j = 0; j < N; ++j) {
-        const int cx = std::min(hg.nx - 1, std::max(0, static_cast<int>(std::floor((src[2 * j] - hg.x0) / hg.g))));
-        const int cy = std::min(hg.ny - 1, std::max(0, static_cast<int>(std::floor((src[2 * j + 1] - hg.y0) / hg.g))));
-        cellof[j] = cx * hg.ny + cy;
-        ++fillv[cellof[j] + 1];
-      }
-      for (int c = 0; c < cells; ++c) fillv[c + 1] += fillv[c];
-      std::copy(fillv.begin(), fillv.end(), hg.starts.begin() + static_cast<size_t>(row) * (cells + 1));
-      double* dst = hg.pts.data() + static_cast<size_t>(row) * N * 2;
-      for (int j = 0; j < N; ++j) {
-        const int at = fillv[cellof[j]]++;
-        dst[2 * at] = src[2 * j];
-        dst[2 * at + 1] = src[2 * j + 1];
-      }
-    }
-  }
-  // stage the field in shared memory when it fits; larger fields are read
-  // through L1/L2
-  h->field_smem_bytes = (count > 0 && bytes <= 40 * 1024) ? static_cast<int>(bytes) : 0;
   h->snap_valid = true;
 }
 
@@ -597,7 +512,10 @@ void run_round_launch(pp_handle* h, uint64_t t, int iter, int r0, int rc, const 
   const bool fp64 = h->fp64 || force_fp64;
   const bool rerank = h->rerank && h->snapshot != nullptr;
   ppdev::RoundArgs a = h->base;
-  if (force_fp64 && !h->fp64) a.field = a.field64;
+  if (force_fp64 && !h->fp64) {
+    a.field = ensure_field64(h);
+    a.lay = a.lay64;
+  }
   ppdev::LaunchShape shape{};
   const int field_smem = (force_fp64 && !h->fp64) ? 0 : h->field_smem_bytes;
   const bool grid2d = h->base.grid_ny > 1;
@@ -872,6 +790,7 @@ void certify_round(pp_handle* h, ppdev::RoundArgs& a, uint64_t t, int iter, int 
       ck(cudaMemcpyAsync(reinterpret_cast<uint32_t*>(h->d_counters.p) + 2, &n_list,
                          sizeof(uint32_t), cudaMemcpyHostToDevice, h->stream),
          "refine count H2D");
+      a.field64 = ensure_field64(h);
       ck(static_cast<cudaError_t>(ppdev::launch_refine(h->kind, a, h->stream)), "refine launch");
       std::vector<ppdev::SelRec> dev(list.size());
       ck(cudaMemcpyAsync(dev.data(), a.sel_out, sizeof(ppdev::SelRec) * list.size(),
@@ -968,32 +887,6 @@ void run_round(pp_handle* h, uint64_t t, int iter, int r0, int rc, const double*
 // Host FP64 rollout: src/planner.cpp:66-191 expressed through the public
 // primitives (bit-identical under -ffp-contract=off; the reference's own
 // selfcheck::resimulate_rollout relies on the same equivalence).
-// Collision at state k against the resident field through the cell index:
-// the reference's own per-point test (src/geometry.cpp:63-76), points
-// farther than cull > r in x or y skipped (they fail its prefilter).
-bool grid_collision(const HostGrid& hg, const paraplan::ChassisPolytope& ch, int k, double x,
-                    double y, double phi) {
-  const int row = hg.rows > 1 ? k : 0;
-  const int cells = hg.nx * hg.ny;
-  const int32_t* st = hg.starts.data() + static_cast<size_t>(row) * (cells + 1);
-  const double* pts = hg.pts.data() + static_cast<size_t>(row) * hg.N * 2;
-  const auto cell = [&](double v, double v0, int n) {
-    return std::min(n - 1, std::max(0, static_cast<int>(std::floor((v - v0) / hg.g))));
-  };
-  const int cx0 = cell(x - hg.cull, hg.x0, hg.nx), cx1 = cell(x + hg.cull, hg.x0, hg.nx);
-  const int cy0 = cell(y - hg.cull, hg.y0, hg.ny), cy1 = cell(y + hg.cull, hg.y0, hg.ny);
-  const double c = std::cos(phi), s = std::sin(phi);
-  const double r2 = ch.bounding_radius() * ch.bounding_radius();
-  for (int cx = cx0; cx <= cx1; ++cx) {
-    for (int j = st[cx * hg.ny + cy0]; j < st[cx * hg.ny + cy1 + 1]; ++j) {
-      const double dx = pts[2 * j] - x, dy = pts[2 * j + 1] - y;
-      if (dx * dx + dy * dy >= r2) continue;
-      if (ch.contains({c * dx + s * dy, -s * dx + c * dy})) return true;
-    }
-  }
-  return false;
-}
-
 void host_rollout(const pp_handle* h, const pp_snapshot& s, const double* theta,
                   pp_rollout_stats* out, double* traj, int32_t cap, int32_t* traj_len) {
   using namespace paraplan;
@@ -1005,7 +898,7 @@ void host_rollout(const pp_handle* h, const pp_snapshot& s, const double* theta,
   const double gc = std::cos(goal.phi), gs = std::sin(goal.phi);
   const std::span<const double> th(theta, h->P);
   const int N = s.n_points;
-  if (N > 0 && s.field_H < cfg.H) {
+  if (N > 0 && s.field_xy != nullptr && s.field_H < cfg.H) {
     throw std::invalid_argument("obstacle field shorter than the planning horizon");
   }
 
@@ -1031,12 +924,17 @@ void host_rollout(const pp_handle* h, const pp_snapshot& s, const double* theta,
   double path = 0.0;
   for (int k = 0;; ++k) {
     if (N > 0) {
-      // the resident snapshot's large clouds go through the cell index
-      const bool indexed = h->hgrid.on && s.field_xy == h->snap_copy.field_xy;
-      const std::span<const Vec2> row(
-          reinterpret_cast<const Vec2*>(s.field_xy) + static_cast<size_t>(k) * N, N);
-      if (indexed ? grid_collision(h->hgrid, h->chassis, k, z.x, z.y, z.phi)
-                  : collision({z.x, z.y, z.phi}, row, h->chassis)) {
+      // the resident snapshot (field_xy == nullptr) goes through the binned
+      // field; a caller's snapshot is scanned point by point
+      bool hit;
+      if (s.field_xy == nullptr) {
+        hit = ppfield::collides(h->field, h->chassis, k, z.x, z.y, z.phi);
+      } else {
+        const std::span<const Vec2> row(
+            reinterpret_cast<const Vec2*>(s.field_xy) + static_cast<size_t>(k) * N, N);
+        hit = collision({z.x, z.y, z.phi}, row, h->chassis);
+      }
+      if (hit) {
         out->collided = 1;
         break;
       }
@@ -1165,10 +1063,11 @@ void pp_destroy(pp_handle* h) {
   if (h->stream != nullptr) cudaStreamSynchronize(h->stream);
   for (DevBuf* b : {&h->d_field, &h->d_params, &h->d_result, &h->d_tiles, &h->d_counters,
                     &h->d_samples, &h->d_scratch, &h->d_injected, &h->d_theta, &h->d_skeys,
-                    &h->d_sel, &h->d_bound}) {
+                    &h->d_sel, &h->d_bound, &h->d_field64}) {
     b->release();
   }
-  for (HostBuf* b : {&h->h_field, &h->h_params, &h->h_result, &h->h_sel, &h->h_bound}) {
+  for (HostBuf* b : {&h->h_field, &h->h_params, &h->h_result, &h->h_sel, &h->h_bound,
+                     &h->h_field64}) {
     b->release();
   }
   if (h->ev0 != nullptr) cudaEventDestroy(h->ev0);

@@ -1,0 +1,64 @@
+// field.hpp -- the obstacle field of one planning tick, split and binned.
+//
+// The reference hands the planner an ExtrapolatedField: (H+1) rows of N
+// anchor-frame points, point j of row h at x_j + h*step_x, y_j + h*step_y
+// (src/geometry.cpp:43-61), and tests every point of row h at state h
+// (src/geometry.cpp:63-76, src/planner.cpp:138-142). Here the points are
+// split into a static part (identical in every row: stored once) and a
+// dynamic part (one row per state), and both are binned on a uniform cell
+// grid so a collision query visits only the cells within cull > r of the
+// vehicle. The collision verdict is an OR over points, so neither the split
+// nor the cell order changes it; skipped points fail the reference's own
+// bounding-circle prefilter.
+//
+// `Binned` is the FP64 image (kept on the host for the exact rollouts of the
+// certification and the epilogue); the device images (FP32 or FP64) are
+// packed from it with the same layout.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <vector>
+
+#include "paraplan/geometry.hpp"
+
+namespace ppfield {
+
+struct Binned {
+  int Ns = 0, Nd = 0, rows = 0;  // static points, dynamic points per row, rows (H+1)
+  int nx = 1, ny = 1;            // cells; ny == 1: x-buckets (small clouds)
+  double x0 = 0.0, y0 = 0.0, g = 1.0, cull = 0.0;
+  std::vector<double> spts;      // Ns x 2, cell order
+  std::vector<double> dpts;      // rows x Nd x 2, per row cell order
+  std::vector<int32_t> sst;      // cells + 1
+  std::vector<int32_t> dst;      // rows x (cells + 1)
+  int cells() const { return nx * ny; }
+  int points() const { return Ns + Nd; }
+};
+
+// Device image layout: byte offsets of [spts][dpts][sst][dst] (16-aligned).
+struct Layout {
+  size_t dpts = 0, sst = 0, dst = 0, bytes = 0;
+};
+Layout layout(const Binned& b, size_t elem);
+
+// From a reference field (rows x N points, rows >= 1): a point whose position
+// is identical in every row is static.
+void from_rows(Binned& b, const double* xy, int rows, int N, double cull);
+
+// From raw anchor-frame points (x, y, heading, speed) x N: the reference's
+// extrapolate (src/geometry.cpp:43-61) evaluated for rows 0..rows-1; points
+// with a zero step in x and y are static.
+void from_points(Binned& b, const double* pts4, int N, int rows, double T_s, double cull);
+
+// Device image in the compute precision (fp64: the binned doubles as-is).
+void pack(const Binned& b, bool fp64, void* out);
+
+// Exact collision at state k (the reference's per-point test).
+bool collides(const Binned& b, const paraplan::ChassisPolytope& ch, int k, double x, double y,
+              double phi);
+
+// The full (rows x N) position of point j of row k in the reference's order
+// is not needed by anyone: the field is only ever queried by state.
+
+}  // namespace ppfield

@@ -65,6 +65,11 @@ struct ConstsT {
   int32_t tan_small;    // delta_max <= pi/4: tan by polynomial ratio (FP32)
 };
 
+// Byte offsets of the parts of a field image.
+struct FieldLayout {
+  int64_t dpts, sst, dst, bytes;
+};
+
 // Everything one sampling round needs. Scalars are FP64 here; the FP32
 // kernel rounds them once at kernel entry.
 struct RoundArgs {
@@ -96,11 +101,15 @@ struct RoundArgs {
   const uint64_t* key_prefix;  // device [restart_count]: fold^4(seed, t, r, iter)
   const double* center;        // device [n_params]
   const double* injected;      // device [count * n_params] or null (RNG off)
-  const void* field;           // device [pts Real2 rows x N][starts int32 rows x (cells+1)]:
-                               // each row ordered by grid cell, starts = first point per cell
-  int32_t field_rows;          // H+1, or 1 for a static field
+  // Obstacle field image (see csrc/capi/field.hpp): [static pts Real2 x Ns]
+  // [dynamic pts Real2 x (H+1) x Nd][static starts int32 x (cells+1)]
+  // [dynamic starts int32 x (H+1) x (cells+1)], points in cell order.
+  const void* field;
+  int32_t field_ns, field_nd;  // static points, dynamic points per row
   int32_t grid_nx, grid_ny;    // cells (grid_ny == 1: x-buckets)
   double grid_x0, grid_y0, grid_g;  // grid origin and cell size (host side)
+  FieldLayout lay;             // byte offsets of the compute-precision image
+  FieldLayout lay64;           // byte offsets of the FP64 image (field64)
   // scratch / outputs (device)
   Rec* tile_recs;              // restart-major: [r][tile] (lockstep) or [r][CTA] (refill)
   Rec* out;                    // [restart_count]

@@ -316,20 +316,30 @@ __device__ __forceinline__ void draw_theta(const RoundArgs& a, uint64_t prefix, 
   }
 }
 
-// Binned obstacle field. Each row h holds its N points ordered by grid cell
-// (cx * ncy + cy) of a uniform grid with cell size g (origin bx0, by0, same
-// grid for all rows), and starts[row * (ncx*ncy + 1) + cell] is the index of
-// the first point of that cell. Static fields (every row identical) are
-// stored once: row = h * row_step with row_step = 0. With ncy == 1 the grid
-// is a row of x-buckets and the cells of a query window are contiguous.
+// Binned obstacle field (csrc/capi/field.hpp): static points stored once,
+// dynamic points once per state row, both in cell order of one uniform grid
+// (cell size g, origin bx0/by0); starts[cell] = first point of the cell.
+// With ncy == 1 the grid is a row of x-buckets.
 template <typename Real>
 struct Field {
-  const typename Vec2T<Real>::type* pts;
-  const int* starts;
-  int N;
+  const typename Vec2T<Real>::type* spts;
+  const typename Vec2T<Real>::type* dpts;
+  const int* sst;
+  const int* dst;
+  int Ns, Nd;
   int ncx, ncy;
-  int row_step;  // 1, or 0 for a static field
 };
+
+template <typename Real>
+__device__ __forceinline__ Field<Real> field_at(const RoundArgs& a, const void* base,
+                                                const FieldLayout& l) {
+  using R2 = typename Vec2T<Real>::type;
+  const unsigned char* p = static_cast<const unsigned char*>(base);
+  return Field<Real>{reinterpret_cast<const R2*>(p), reinterpret_cast<const R2*>(p + l.dpts),
+                     reinterpret_cast<const int*>(p + l.sst),
+                     reinterpret_cast<const int*>(p + l.dst), a.field_ns, a.field_nd,
+                     a.grid_nx, a.grid_ny};
+}
 
 // Inside-margin of one point against the chassis at (x, y, phi):
 // min(r2 - d2, fe - bx, re + bx, hw - by, hw + by) in the reference's own
@@ -368,19 +378,13 @@ __device__ __forceinline__ float point_margin<float>(const Consts<float>& K, flo
 // iff it is > 0; a small |margin| marks a verdict rounding could flip).
 // A lane stops at its first robust hit (margin >= stop). Warp-synchronous:
 // all 32 lanes call it, every loop is warp-uniform.
+// Points of one part (static, or the dynamic row of state h) in the cells
+// covering the query window; updates the inside-margin `best`.
 template <typename Real, bool kGrid>
-__device__ __forceinline__ Real collide_margin(const Field<Real>& f, const Consts<Real>& K, int h,
-                                               Real x, Real y, Real c, Real s, Real stop) {
-  const int ncx = f.ncx, ncy = f.ncy;
-  const int row = h * f.row_step;
-  const int* st = f.starts + static_cast<size_t>(row) * (ncx * ncy + 1);
-  const auto* pts = f.pts + static_cast<size_t>(row) * f.N;
-  const Real top = Real(ncx - 1);
-  const int cx_lo = static_cast<int>(fmin(fmax((x - K.qpad - K.bx0) * K.binv, Real(0)), top));
-  const int cx_hi = static_cast<int>(fmin(fmax((x + K.qpad - K.bx0) * K.binv, Real(0)), top));
-  const Real kx = c * x + s * y + K.bcx;  // FP32 rotated-frame form only
-  const Real ky = -s * x + c * y;
-  Real best = Real(-1e30);
+__device__ __forceinline__ void scan_part(const typename Vec2T<Real>::type* pts, const int* st,
+                                          int ncy, int cx_lo, int cx_hi, int cy_lo, int cy_hi,
+                                          const Consts<Real>& K, Real x, Real y, Real c, Real s,
+                                          Real kx, Real ky, Real stop, Real& best) {
   if constexpr (!kGrid) {  // x-buckets: the window is one contiguous range
     const int lo = st[cx_lo];
     const int cnt = st[cx_hi + 1] - lo;
@@ -392,9 +396,6 @@ __device__ __forceinline__ Real collide_margin(const Field<Real>& f, const Const
       }
     }
   } else {  // 2-D cells, one contiguous range per cell column; early exit
-    const Real ytop = Real(ncy - 1);
-    const int cy_lo = static_cast<int>(fmin(fmax((y - K.qpad - K.by0) * K.binv, Real(0)), ytop));
-    const int cy_hi = static_cast<int>(fmin(fmax((y + K.qpad - K.by0) * K.binv, Real(0)), ytop));
     const int ncol = cx_hi - cx_lo + 1;
     const int cols = __reduce_max_sync(kFull, ncol);
     for (int k = 0; k < cols; ++k) {
@@ -410,6 +411,43 @@ __device__ __forceinline__ Real collide_margin(const Field<Real>& f, const Const
         }
       }
     }
+  }
+}
+
+// Collision of the chassis at (x, y, phi) with the field at state h. Only the
+// cells covering [x - qpad, x + qpad] (x [y - qpad, y + qpad] with a 2-D
+// grid) are visited: every other point is farther than cull > r from the
+// vehicle and fails the reference's bounding-circle prefilter
+// (src/geometry.cpp:71). Returns the inside-margin max over visited points
+// (the reference reports a collision iff it is > 0; a small |margin| marks a
+// verdict rounding could flip). Warp-synchronous: all 32 lanes call it,
+// every loop is warp-uniform.
+template <typename Real, bool kGrid>
+__device__ __forceinline__ Real collide_margin(const Field<Real>& f, const Consts<Real>& K, int h,
+                                               Real x, Real y, Real c, Real s, Real stop) {
+  const int ncx = f.ncx, ncy = f.ncy;
+  const Real top = Real(ncx - 1);
+  const int cx_lo = static_cast<int>(fmin(fmax((x - K.qpad - K.bx0) * K.binv, Real(0)), top));
+  const int cx_hi = static_cast<int>(fmin(fmax((x + K.qpad - K.bx0) * K.binv, Real(0)), top));
+  int cy_lo = 0, cy_hi = 0;
+  if constexpr (kGrid) {
+    const Real ytop = Real(ncy - 1);
+    cy_lo = static_cast<int>(fmin(fmax((y - K.qpad - K.by0) * K.binv, Real(0)), ytop));
+    cy_hi = static_cast<int>(fmin(fmax((y + K.qpad - K.by0) * K.binv, Real(0)), ytop));
+  }
+  const Real kx = c * x + s * y + K.bcx;  // FP32 rotated-frame form only
+  const Real ky = -s * x + c * y;
+  Real best = Real(-1e30);
+  // part 0: static points; part 1: the dynamic row of state h (one copy of
+  // the scan code, warp-uniform part loop)
+#pragma unroll 1
+  for (int part = 0; part < 2; ++part) {
+    const bool dyn = part == 1;
+    if ((dyn ? f.Nd : f.Ns) == 0) continue;
+    const auto* pts = dyn ? f.dpts + static_cast<size_t>(h) * f.Nd : f.spts;
+    const int* st = dyn ? f.dst + static_cast<size_t>(h) * (ncx * ncy + 1) : f.sst;
+    scan_part<Real, kGrid>(pts, st, ncy, cx_lo, cx_hi, cy_lo, cy_hi, K, x, y, c, s, kx, ky, stop,
+                           best);
   }
   return best;
 }
@@ -455,7 +493,7 @@ __device__ __forceinline__ int advance(Lane<Real>& L, const Net& net, const Cons
   M<Real>::sc(L.phi, &sphi, &cphi);
   L.ephi = M<Real>::wrap(K.gphi - L.phi);
   bool hit = false;
-  if (f.N > 0) {
+  if (f.Ns + f.Nd > 0) {
     // a lane may stop at a hit whose margin is too large to flip
     const Real cm = collide_margin<Real, kGrid>(f, K, L.h, L.x, L.y, cphi, sphi, K.dmarg);
     hit = cm > Real(0);
@@ -611,27 +649,20 @@ __device__ __forceinline__ Key load_rec_cg(const Rec* src) {
   return Key{__ldcg(&src->cls), __ldcg(&src->cand), __ldcg(&src->k1), __ldcg(&src->k2)};
 }
 
-// Shared-memory image of the binned field: [pts rows x N][starts rows x (cells+1)].
+// Field of the round, staged whole into shared memory when it fits
+// (a.field_smem_bytes > 0), else read through L1/L2.
 template <typename Real>
 __device__ __forceinline__ Field<Real> stage_field(const RoundArgs& a, unsigned char* smem) {
-  using R2 = typename Vec2T<Real>::type;
-  const int N = a.n_points;
-  const size_t rows = a.field_rows;
-  const size_t count = rows * N;
-  const size_t nst = rows * (static_cast<size_t>(a.grid_nx) * a.grid_ny + 1);
-  const R2* gpts = static_cast<const R2*>(a.field);
-  const int* gst = reinterpret_cast<const int*>(gpts + count);
-  Field<Real> f{gpts, gst, N, a.grid_nx, a.grid_ny, rows > 1 ? 1 : 0};
-  if (a.field_smem_bytes > 0 && N > 0) {
-    R2* spts = reinterpret_cast<R2*>(smem);
-    int* sst = reinterpret_cast<int*>(spts + count);
-    for (size_t i = threadIdx.x; i < count; i += blockDim.x) spts[i] = gpts[i];
-    for (size_t i = threadIdx.x; i < nst; i += blockDim.x) sst[i] = gst[i];
-    f.pts = spts;
-    f.starts = sst;
+  if (a.field_smem_bytes > 0 && a.n_points > 0) {
+    const int4* src = static_cast<const int4*>(a.field);
+    int4* dst = reinterpret_cast<int4*>(smem);
+    const int n16 = a.field_smem_bytes / 16;
+    for (int i = threadIdx.x; i < n16; i += blockDim.x) dst[i] = src[i];
+    __syncthreads();
+    return field_at<Real>(a, smem, a.lay);
   }
   __syncthreads();
-  return f;
+  return field_at<Real>(a, a.field, a.lay);
 }
 
 // Compact per-sample key for the near-tie re-ranking (select_kernel):
@@ -756,8 +787,15 @@ __global__ void __launch_bounds__(256) generate_kernel(const RoundArgs a) {
 }
 
 // ------------------------------------------------------ refill kernel ----
+// Resident CTAs per SM the register allocation must allow: [5,2,2] in FP32
+// fits 6 (<= 85 registers), wider nets and FP64 need more registers.
+template <typename Real, class Net>
+constexpr int refill_min_blocks() {
+  return sizeof(Real) == 4 ? (Net::kP <= 24 ? PARAPLAN_REFILL_MINB : 3) : (Net::kP <= 24 ? 4 : 2);
+}
+
 template <typename Real, class Net, bool kGrid>
-__global__ void __launch_bounds__(kBlock, sizeof(Real) == 4 ? PARAPLAN_REFILL_MINB : 4)
+__global__ void __launch_bounds__(kBlock, refill_min_blocks<Real, Net>())
     refill_kernel(const RoundArgs a) {
   constexpr int P = Net::kP;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1025,10 +1063,7 @@ template <class Net64, bool kGrid>
 __global__ void __launch_bounds__(128) refine_kernel(const RoundArgs a) {
   const Consts<double>& K = a.kd;
   const unsigned n_sel = min(__ldcg(&a.counters[2]), static_cast<unsigned>(a.sel_cap));
-  const Field<double> f{static_cast<const double2*>(a.field64),
-                        reinterpret_cast<const int*>(static_cast<const double2*>(a.field64) +
-                                                     static_cast<size_t>(a.field_rows) * a.n_points),
-                        a.n_points, a.grid_nx, a.grid_ny, a.field_rows > 1 ? 1 : 0};
+  const Field<double> f = field_at<double>(a, a.field64, a.lay64);
   double s0[5];
   start_features(K, s0);
   Net64 net = RefineNet<Net64>::make(a);
