@@ -12,6 +12,7 @@
  *   pp_create / pp_destroy      Planner::Planner / ~Planner
  *                               (src/planner.cpp:46-58, include/paraplan/planner.hpp:90-92)
  *   pp_plan_step                Planner::plan_step        (src/planner.cpp:238-351)
+ *   pp_plan_step_points         plan_step of extrapolate(points) (src/mission.cpp:142-158)
  *   pp_rollout                  Planner::rollout          (src/planner.cpp:193-205)
  *   pp_sample_candidate         Planner::sample_candidate (src/planner.cpp:207-226)
  *   pp_perturbation_sigma       Planner::perturbation_sigma (src/planner.cpp:228-236)
@@ -116,6 +117,26 @@ typedef struct pp_snapshot {
   int32_t _pad;
 } pp_snapshot;
 
+/* Snapshot with raw obstacle points instead of an extrapolated field: the
+ * anchor-frame points sense() returns (x, y, heading, speed) x n_points. The
+ * planner extrapolates them exactly as extrapolate(points, H, T_s)
+ * (src/geometry.cpp:43-61) would, so results equal pp_plan_step on that
+ * field; static points are stored once and nothing (H+1) x N crosses the
+ * boundary. */
+typedef struct pp_snapshot_points {
+  double ev_x, ev_y, ev_phi, ev_v;
+  double actuator_delta;
+  double prev_a0, prev_a1;
+  double goal_x, goal_y, goal_phi, goal_v;
+  const double* points;
+  int32_t n_points;
+  int32_t _pad;
+  double T_s;
+  const double* warm_theta;
+  int32_t warm_theta_len;
+  int32_t _pad2;
+} pp_snapshot_points;
+
 /* RolloutResult without the trajectory (include/paraplan/planner.hpp:48-56).
  * steps = dynamics steps simulated (trajectory length - 1). */
 typedef struct pp_rollout_stats {
@@ -180,6 +201,12 @@ int32_t pp_abi_version(void);
  * in FP64. */
 pp_status pp_plan_step(pp_handle* h, const pp_snapshot* snap, uint64_t t,
                        pp_plan_output* out);
+
+/* pp_plan_step on a raw-points snapshot (same results as on the
+ * extrapolated field); run_mission's tick uses it. */
+pp_status pp_plan_step_points(pp_handle* h, const pp_snapshot_points* snap, uint64_t t,
+                              pp_plan_output* out);
+pp_status pp_upload_points(pp_handle* h, const pp_snapshot_points* snap);
 
 /* Planner::rollout (host FP64, bit-identical to the reference). traj may be
  * NULL; otherwise it holds traj_cap states of 4 doubles. */

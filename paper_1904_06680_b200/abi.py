@@ -54,6 +54,17 @@ class pp_snapshot(C.Structure):
     ]
 
 
+class pp_snapshot_points(C.Structure):
+    _fields_ = [
+        ("ev_x", C.c_double), ("ev_y", C.c_double), ("ev_phi", C.c_double), ("ev_v", C.c_double),
+        ("actuator_delta", C.c_double), ("prev_a0", C.c_double), ("prev_a1", C.c_double),
+        ("goal_x", C.c_double), ("goal_y", C.c_double), ("goal_phi", C.c_double),
+        ("goal_v", C.c_double), ("points", C.POINTER(C.c_double)), ("n_points", C.c_int32),
+        ("_pad", C.c_int32), ("T_s", C.c_double), ("warm_theta", C.POINTER(C.c_double)),
+        ("warm_theta_len", C.c_int32), ("_pad2", C.c_int32),
+    ]
+
+
 class pp_rollout_stats(C.Structure):
     _fields_ = [("reached", C.c_int32), ("t_goal", C.c_int32), ("collided", C.c_int32),
                 ("steps", C.c_int32), ("path_length", C.c_double),
@@ -183,6 +194,28 @@ class Snapshot:
             keep.append(w)
         s._keep = keep
         return s
+
+
+def points_snapshot(snap: Snapshot, points: np.ndarray, T_s: float = 0.1) -> pp_snapshot_points:
+    """pp_snapshot_points of `snap` (its field ignored) with raw anchor-frame
+    points (N, 4): x, y, heading, speed."""
+    p = pp_snapshot_points()
+    p.ev_x, p.ev_y, p.ev_phi, p.ev_v = map(float, snap.ev)
+    p.actuator_delta = float(snap.actuator_delta)
+    p.prev_a0, p.prev_a1 = map(float, snap.prev_action)
+    p.goal_x, p.goal_y, p.goal_phi, p.goal_v = map(float, snap.goal)
+    pts = np.ascontiguousarray(np.asarray(points, dtype=np.float64).reshape(-1, 4))
+    p.points = pts.ctypes.data_as(C.POINTER(C.c_double))
+    p.n_points = len(pts)
+    p.T_s = T_s
+    keep = [pts]
+    if snap.warm_theta is not None and len(snap.warm_theta) > 0:
+        w = np.ascontiguousarray(snap.warm_theta, dtype=np.float64)
+        p.warm_theta = w.ctypes.data_as(C.POINTER(C.c_double))
+        p.warm_theta_len = len(w)
+        keep.append(w)
+    p._keep = keep
+    return p
 
 
 def extrapolate(points: np.ndarray, H: int, T_s: float = 0.1) -> np.ndarray:

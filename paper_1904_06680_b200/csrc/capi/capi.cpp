@@ -392,6 +392,46 @@ const void* ensure_field64(pp_handle* h) {
   return h->d_field64.p;
 }
 
+void set_round_constants(pp_handle* h, const pp_snapshot& s);
+void upload_field_rows(pp_handle* h, const pp_snapshot& s, ppdev::RoundArgs& a);
+
+// Snapshot with raw anchor-frame obstacle points: the field is the
+// reference's extrapolate(points, H, T_s) (src/geometry.cpp:43-61), built
+// straight into the binned static/dynamic form.
+void upload_points(pp_handle* h, const pp_snapshot_points& p) {
+  const auto& cfg = h->cfg;
+  if (p.n_points < 0) throw std::invalid_argument("malformed obstacle points");
+  if (p.n_points > 0 && p.points == nullptr) throw std::invalid_argument("null obstacle points");
+  pp_snapshot s{};
+  s.ev_x = p.ev_x;
+  s.ev_y = p.ev_y;
+  s.ev_phi = p.ev_phi;
+  s.ev_v = p.ev_v;
+  s.actuator_delta = p.actuator_delta;
+  s.prev_a0 = p.prev_a0;
+  s.prev_a1 = p.prev_a1;
+  s.goal_x = p.goal_x;
+  s.goal_y = p.goal_y;
+  s.goal_phi = p.goal_phi;
+  s.goal_v = p.goal_v;
+  s.field_xy = nullptr;
+  s.field_H = cfg.H;
+  s.n_points = p.n_points;
+  s.warm_theta = p.warm_theta;
+  s.warm_theta_len = p.warm_theta_len;
+  set_round_constants(h, s);
+  ppdev::RoundArgs& a = h->base;
+  a.n_points = p.n_points;
+  const double cull = std::sqrt(a.r2) + 1e-3;
+  ppfield::from_points(h->field, p.points, p.n_points, cfg.H + 1, p.T_s, cull);
+  finish_field(h, a);
+  h->snap_copy = s;
+  h->snap_warm.assign(s.warm_theta, s.warm_theta + std::max(0, s.warm_theta_len));
+  h->snap_copy.warm_theta = h->snap_warm.data();
+  h->snapshot = &h->snap_copy;
+  h->snap_valid = true;
+}
+
 // Goal transform and constants of a snapshot (src/planner.cpp:70-81).
 void upload_snapshot(pp_handle* h, const pp_snapshot& s) {
   const auto& cfg = h->cfg;
@@ -401,6 +441,13 @@ void upload_snapshot(pp_handle* h, const pp_snapshot& s) {
     throw std::invalid_argument("obstacle field shorter than the planning horizon");
   }
   if (s.n_points > 0 && s.field_xy == nullptr) throw std::invalid_argument("null obstacle field");
+  set_round_constants(h, s);
+  ppdev::RoundArgs& a = h->base;
+  upload_field_rows(h, s, a);
+}
+
+void set_round_constants(pp_handle* h, const pp_snapshot& s) {
+  const auto& cfg = h->cfg;
   ppdev::RoundArgs& a = h->base;
   a = ppdev::RoundArgs{};
   const paraplan::Pose2 anchor{s.ev_x, s.ev_y, s.ev_phi};
@@ -442,6 +489,10 @@ void upload_snapshot(pp_handle* h, const pp_snapshot& s) {
   a.n_layers = static_cast<int32_t>(h->sizes.size());
   for (size_t i = 0; i < h->sizes.size(); ++i) a.sizes[i] = h->sizes[i];
 
+}
+
+void upload_field_rows(pp_handle* h, const pp_snapshot& s, ppdev::RoundArgs& a) {
+  const auto& cfg = h->cfg;
   // Only rows 0..H are ever read (src/planner.cpp:139 at h <= H): split
   // into static and dynamic points and bin them (csrc/capi/field.hpp).
   const int N = s.n_points;
@@ -1187,76 +1238,116 @@ pp_status pp_merge_records(const pp_record* recs, int32_t n, pp_record* out) {
   return PP_OK;
 }
 
+}  // extern "C"
+
+namespace {
+
+// Planner::plan_step after the snapshot is resident (src/planner.cpp:238-351).
+void plan_step_resident(pp_handle* h, uint64_t t, pp_plan_output* out) {
+  const int P = h->P;
+  const auto& cfg = h->cfg;
+  const pp_snapshot& snap = *h->snapshot;
+  std::vector<double> init_center(P, 0.0);
+  if (snap.warm_theta_len == P) init_center.assign(snap.warm_theta, snap.warm_theta + P);
+
+  const int R = cfg.n_restarts, I = cfg.n_iter_max, n = cfg.n_candidates;
+  // Iteration 0 of every restart centres on the warm start: one launch.
+  std::vector<pp_record> first(R);
+  run_round(h, t, 0, 0, R, init_center.data(), 0, n, nullptr, first.data(), nullptr);
+
+  Key best;
+  bool best_valid = false, any_free = false;
+  std::vector<double> best_theta(P, 0.0), center(P, 0.0), theta(P);
+  pp_record win{-1, -1, -1, -1, 0.0, 0.0};
+  int64_t evaluated = 0;
+  bool done = false;
+  for (int r = 0; r < R && !done; ++r) {
+    for (int it = 0; it < I; ++it) {
+      pp_record rec;
+      if (it == 0) {
+        center = init_center;
+        rec = first[r];
+      } else {
+        if (best_valid) center = best_theta;  // :275-276
+        run_round(h, t, it, r, 1, center.data(), 0, n, nullptr, &rec, nullptr);
+      }
+      evaluated += n;
+      any_free = any_free || rec.cls >= 1;
+      const Key k{rec.cls, rec.k1, rec.k2};
+      if (!best_valid || key_better(k, best)) {  // :324-330
+        host_sample(h, center.data(), t, r, it, rec.candidate, theta.data());
+        best = k;
+        best_theta = theta;
+        best_valid = true;
+        win = rec;
+      }
+      if (cfg.early_exit && best_valid && best.cls == 2) {  // :332-334
+        done = true;
+        break;
+      }
+    }
+  }
+
+  // FP64 epilogue (:339-350).
+  out->evaluated = evaluated;
+  if (out->best_theta != nullptr) std::memcpy(out->best_theta, best_theta.data(), sizeof(double) * P);
+  int32_t len = 0;
+  host_rollout(h, snap, best_theta.data(), &out->predicted, out->trajectory, cfg.H + 1, &len);
+  out->trajectory_len = len;
+  out->success = out->predicted.reached && !out->predicted.collided;
+  if (any_free) {
+    out->action_a0 = out->predicted.first_a0;
+    out->action_a1 = out->predicted.first_a1;
+  } else {
+    out->action_a0 = snap.actuator_delta / h->params.delta_max;
+    out->action_a1 = -1.0;
+  }
+  out->winner = win;
+}
+
+void check_warm(const pp_handle* h, int32_t len) {
+  if (len != 0 && len != h->P) {
+    throw std::invalid_argument("warm start vector size mismatch");  // :240-244
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
 pp_status pp_plan_step(pp_handle* h, const pp_snapshot* snap, uint64_t t, pp_plan_output* out) {
   return guarded([&] {
     if (h == nullptr || snap == nullptr || out == nullptr) {
       throw std::invalid_argument("null argument");
     }
-    const int P = h->P;
-    const auto& cfg = h->cfg;
-    if (snap->warm_theta_len != 0 && snap->warm_theta_len != P) {
-      throw std::invalid_argument("warm start vector size mismatch");  // :240-244
-    }
+    check_warm(h, snap->warm_theta_len);
     ck(cudaSetDevice(h->device), "cudaSetDevice");
     h->timing = pp_timing{};
     upload_snapshot(h, *snap);
+    plan_step_resident(h, t, out);
+  });
+}
 
-    std::vector<double> init_center(P, 0.0);
-    if (snap->warm_theta_len == P) init_center.assign(snap->warm_theta, snap->warm_theta + P);
+pp_status pp_upload_points(pp_handle* h, const pp_snapshot_points* snap) {
+  return guarded([&] {
+    if (h == nullptr || snap == nullptr) throw std::invalid_argument("null argument");
+    ck(cudaSetDevice(h->device), "cudaSetDevice");
+    upload_points(h, *snap);
+    ck(cudaStreamSynchronize(h->stream), "snapshot H2D");
+  });
+}
 
-    const int R = cfg.n_restarts, I = cfg.n_iter_max, n = cfg.n_candidates;
-    // Iteration 0 of every restart centres on the warm start: one launch.
-    std::vector<pp_record> first(R);
-    run_round(h, t, 0, 0, R, init_center.data(), 0, n, nullptr, first.data(), nullptr);
-
-    Key best;
-    bool best_valid = false, any_free = false;
-    std::vector<double> best_theta(P, 0.0), center(P, 0.0), theta(P);
-    pp_record win{-1, -1, -1, -1, 0.0, 0.0};
-    int64_t evaluated = 0;
-    bool done = false;
-    for (int r = 0; r < R && !done; ++r) {
-      for (int it = 0; it < I; ++it) {
-        pp_record rec;
-        if (it == 0) {
-          center = init_center;
-          rec = first[r];
-        } else {
-          if (best_valid) center = best_theta;  // :275-276
-          run_round(h, t, it, r, 1, center.data(), 0, n, nullptr, &rec, nullptr);
-        }
-        evaluated += n;
-        any_free = any_free || rec.cls >= 1;
-        const Key k{rec.cls, rec.k1, rec.k2};
-        if (!best_valid || key_better(k, best)) {  // :324-330
-          host_sample(h, center.data(), t, r, it, rec.candidate, theta.data());
-          best = k;
-          best_theta = theta;
-          best_valid = true;
-          win = rec;
-        }
-        if (cfg.early_exit && best_valid && best.cls == 2) {  // :332-334
-          done = true;
-          break;
-        }
-      }
+pp_status pp_plan_step_points(pp_handle* h, const pp_snapshot_points* snap, uint64_t t,
+                              pp_plan_output* out) {
+  return guarded([&] {
+    if (h == nullptr || snap == nullptr || out == nullptr) {
+      throw std::invalid_argument("null argument");
     }
-
-    // FP64 epilogue (:339-350).
-    out->evaluated = evaluated;
-    if (out->best_theta != nullptr) std::memcpy(out->best_theta, best_theta.data(), sizeof(double) * P);
-    int32_t len = 0;
-    host_rollout(h, *h->snapshot, best_theta.data(), &out->predicted, out->trajectory, cfg.H + 1, &len);
-    out->trajectory_len = len;
-    out->success = out->predicted.reached && !out->predicted.collided;
-    if (any_free) {
-      out->action_a0 = out->predicted.first_a0;
-      out->action_a1 = out->predicted.first_a1;
-    } else {
-      out->action_a0 = snap->actuator_delta / h->params.delta_max;
-      out->action_a1 = -1.0;
-    }
-    out->winner = win;
+    check_warm(h, snap->warm_theta_len);
+    ck(cudaSetDevice(h->device), "cudaSetDevice");
+    h->timing = pp_timing{};
+    upload_points(h, *snap);
+    plan_step_resident(h, t, out);
   });
 }
 

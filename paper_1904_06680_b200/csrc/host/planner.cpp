@@ -102,19 +102,65 @@ Planner::Planner(const VehicleParams& params, const MlpArchitecture& arch,
 
 Planner::~Planner() { pp_destroy(handle_); }
 
+namespace {
+PlannerOutput unpack(const pp_plan_output& o, const std::vector<double>& traj,
+                     std::vector<double> best_theta);
+}
+
 PlannerOutput Planner::plan_step(const PlanningSnapshot& snap, std::uint64_t t) const {
   const int np = param_count();
   if (!snap.warm_theta.empty() && static_cast<int>(snap.warm_theta.size()) != np) {
     throw std::invalid_argument("warm start vector size mismatch");
   }
   const pp_snapshot s = pack(snap);
-  PlannerOutput out;
-  out.best_theta.assign(np, 0.0);
+  std::vector<double> theta(np, 0.0);
   std::vector<double> traj(static_cast<std::size_t>(cfg_.H + 1) * 4);
   pp_plan_output o{};
-  o.best_theta = out.best_theta.data();
+  o.best_theta = theta.data();
   o.trajectory = traj.data();
   throw_status(pp_plan_step(handle_, &s, t, &o));
+  return unpack(o, traj, std::move(theta));
+}
+
+PlannerOutput Planner::plan_step_points(const PlanningSnapshot& snap,
+                                        std::span<const ObstaclePoint> points,
+                                        std::uint64_t t) const {
+  const int np = param_count();
+  if (!snap.warm_theta.empty() && static_cast<int>(snap.warm_theta.size()) != np) {
+    throw std::invalid_argument("warm start vector size mismatch");
+  }
+  static_assert(sizeof(ObstaclePoint) == 4 * sizeof(double), "ObstaclePoint must be 4 doubles");
+  pp_snapshot_points s{};
+  s.ev_x = snap.ev_state.x;
+  s.ev_y = snap.ev_state.y;
+  s.ev_phi = snap.ev_state.phi;
+  s.ev_v = snap.ev_state.v;
+  s.actuator_delta = snap.actuator.delta;
+  s.prev_a0 = snap.prev_action.a0;
+  s.prev_a1 = snap.prev_action.a1;
+  s.goal_x = snap.goal.x;
+  s.goal_y = snap.goal.y;
+  s.goal_phi = snap.goal.phi;
+  s.goal_v = snap.goal.v;
+  s.points = points.empty() ? nullptr : reinterpret_cast<const double*>(points.data());
+  s.n_points = static_cast<int32_t>(points.size());
+  s.T_s = params_.T_s;
+  s.warm_theta = snap.warm_theta.empty() ? nullptr : snap.warm_theta.data();
+  s.warm_theta_len = static_cast<int32_t>(snap.warm_theta.size());
+  std::vector<double> theta(np, 0.0);
+  std::vector<double> traj(static_cast<std::size_t>(cfg_.H + 1) * 4);
+  pp_plan_output o{};
+  o.best_theta = theta.data();
+  o.trajectory = traj.data();
+  throw_status(pp_plan_step_points(handle_, &s, t, &o));
+  return unpack(o, traj, std::move(theta));
+}
+
+namespace {
+PlannerOutput unpack(const pp_plan_output& o, const std::vector<double>& traj,
+                     std::vector<double> best_theta) {
+  PlannerOutput out;
+  out.best_theta = std::move(best_theta);
   out.evaluated = o.evaluated;
   out.success = o.success != 0;
   out.action = {o.action_a0, o.action_a1};
@@ -131,6 +177,7 @@ PlannerOutput Planner::plan_step(const PlanningSnapshot& snap, std::uint64_t t) 
   }
   return out;
 }
+}  // namespace
 
 RolloutResult Planner::rollout(std::span<const double> theta, const PlanningSnapshot& snap) const {
   if (static_cast<int>(theta.size()) != param_count()) {

@@ -42,3 +42,38 @@ def test_c4_lot_per_sample_stats(precision):
     assert flips <= (0 if precision == 64 else 5)
     same = got["steps"] == want["steps"]
     assert same.mean() >= 0.99
+
+
+@pytest.mark.parametrize("which", ["c2", "c5_mixed", "c5_static"])
+def test_raw_points_path_equals_extrapolated_field(which):
+    """pp_plan_step_points(points) == pp_plan_step(extrapolate(points)),
+    bit for bit (the field is built by the planner)."""
+    import math
+    rng = np.random.default_rng(7)
+    if which == "c2":
+        w = workloads.c2(samples=1 << 14)
+        from paper_1904_06680_b200 import import_paraplan
+        pp = import_paraplan()
+        m = workloads.c2_mission()
+        pts = np.array([(q.x, q.y, q.heading, q.speed)
+                        for q in pp.sense(m, m.initial_state, w.t, 20, 0.1)])
+    else:
+        n = 500
+        pts = np.zeros((n, 4))
+        pts[:, 0] = rng.uniform(-10, 30, n)
+        pts[:, 1] = rng.uniform(2.5, 10, n) * rng.choice([-1, 1], n)
+        if which == "c5_mixed":
+            dyn = rng.random(n) < 0.25
+            pts[dyn, 2] = rng.choice([0.0, math.pi], dyn.sum())
+            pts[dyn, 3] = rng.uniform(0, 15, dyn.sum())
+        w = workloads.c5(1 << 14, 30, n)
+    snap = abi.Snapshot(ev=w.snapshot.ev, actuator_delta=w.snapshot.actuator_delta,
+                        prev_action=w.snapshot.prev_action, goal=w.snapshot.goal,
+                        field=abi.extrapolate(pts, w.model.H))
+    dp = capi.DevicePlanner(w.model)
+    o1, th1, tr1 = dp.plan_step(snap, w.t)
+    o2, th2, tr2 = dp.plan_step_points(snap, pts, w.t)
+    assert np.array_equal(th1, th2) and np.array_equal(tr1, tr2)
+    assert (o1.action_a0, o1.action_a1, o1.evaluated) == (o2.action_a0, o2.action_a1, o2.evaluated)
+    o3, th3, tr3 = Port(w.model).plan_step(snap, w.t)
+    assert np.array_equal(th1, th3) and np.array_equal(tr1, tr3)

@@ -40,7 +40,7 @@ def test_library_exports_every_declared_symbol():
 
 def test_struct_layout_matches_c(tmp_path: Path):
     src = tmp_path / "probe.c"
-    names = ["pp_vehicle", "pp_norm", "pp_config", "pp_model", "pp_snapshot",
+    names = ["pp_vehicle", "pp_norm", "pp_config", "pp_model", "pp_snapshot", "pp_snapshot_points",
              "pp_rollout_stats", "pp_record", "pp_plan_output", "pp_timing"]
     src.write_text('#include <stdio.h>\n#include <stddef.h>\n#include "paraplan_cuda.h"\n'
                    "int main(void){\n" +
