@@ -100,7 +100,8 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     with cf.ThreadPoolExecutor(max_workers=os.cpu_count() or 4) as ex:
         for out in ex.map(lambda c: _run(c, verbose), jobs):
             logs.append(out)
-    (BUILD / "ptxas.log").write_text("\n".join(logs))
+    if jobs:  # keep the last compile log when nothing was stale
+        (BUILD / "ptxas.log").write_text("\n".join(logs))
 
     if force or _stale(LIB, objs):
         _run(["g++", "-shared", "-o", str(LIB), *map(str, objs),

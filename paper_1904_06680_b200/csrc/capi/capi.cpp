@@ -247,6 +247,7 @@ struct pp_handle {
   paraplan::NormConstants norm;
   std::unique_ptr<paraplan::MlpPolicy> policy;
   paraplan::ChassisPolytope chassis;
+  ppfield::Box box;  // the same rectangle as (front, rear, half width)
   int P = 0;
   ppdev::NetKind kind = ppdev::NetKind::kGeneric;
   int device = 0;
@@ -323,7 +324,7 @@ void fill_consts(const ppdev::RoundArgs& a, ppdev::ConstsT<Real>* k) {
   k->bx0 = Real(a.grid_x0);
   k->by0 = Real(a.grid_y0);
   k->binv = Real(1.0 / a.grid_g);
-  k->qpad = Real(cull + a.grid_g / 8.0);
+  k->qpad = Real(a.grid_g / 8.0);
   // a discrete verdict whose margin is below this may flip under rounding
   k->dmarg = sizeof(Real) == sizeof(float) ? Real(a.dmarg32) : Real(1e-9);
   k->bcx = Real(0.5 * (a.fe - a.re));
@@ -344,12 +345,14 @@ void finish_field(pp_handle* h, ppdev::RoundArgs& a) {
   a.grid_x0 = b.x0;
   a.grid_y0 = b.y0;
   a.grid_g = b.g;
+  a.grid_mode = b.mode();
   const size_t elem = h->fp64 ? sizeof(double) : sizeof(float);
   const ppfield::Layout l = ppfield::layout(b, elem), l64 = ppfield::layout(b, sizeof(double));
   a.lay = {static_cast<int64_t>(l.dpts), static_cast<int64_t>(l.sst), static_cast<int64_t>(l.dst),
-           static_cast<int64_t>(l.bytes)};
+           static_cast<int64_t>(l.sbox), static_cast<int64_t>(l.bytes)};
   a.lay64 = {static_cast<int64_t>(l64.dpts), static_cast<int64_t>(l64.sst),
-             static_cast<int64_t>(l64.dst), static_cast<int64_t>(l64.bytes)};
+             static_cast<int64_t>(l64.dst), static_cast<int64_t>(l64.sbox),
+             static_cast<int64_t>(l64.bytes)};
   a.field = nullptr;
   a.field64 = nullptr;
   h->field64_ready = false;
@@ -548,8 +551,17 @@ void certify_round(pp_handle* h, ppdev::RoundArgs& a, uint64_t t, int iter, int 
 
 constexpr int kSelCap = 1 << 16;    // near-tie candidates re-ranked per launch
 constexpr int kSelFirst = 512;      // copied back with the round result
-constexpr int kHostMax = 96;        // windows up to this size are re-evaluated on the host
 constexpr int kRefineGrid = 148 * 2;
+
+// Windows up to this size are re-evaluated on the host pool (exact FP64
+// rollouts, 16 workers); wider ones get the FP64 device kernel first.
+int host_max() {
+  static const int v = [] {
+    const char* e = std::getenv("PARAPLAN_HOST_MAX");
+    return e != nullptr ? std::atoi(e) : 1024;
+  }();
+  return v;
+}
 
 // One sampling round on the device: restarts [r0, r0+rc), candidates
 // [c0, c1) of each, iteration `iter`, centred on `center` (or injected theta).
@@ -569,7 +581,7 @@ void run_round_launch(pp_handle* h, uint64_t t, int iter, int r0, int rc, const 
   }
   ppdev::LaunchShape shape{};
   const int field_smem = (force_fp64 && !h->fp64) ? 0 : h->field_smem_bytes;
-  const bool grid2d = h->base.grid_ny > 1;
+  const int grid2d = h->base.grid_mode;
   const int rcode = fp64 ? ppdev::shape_f64(h->kind, h->device, field_smem, grid2d, &shape)
                          : ppdev::shape_f32(h->kind, h->device, field_smem, grid2d, &shape);
   ck(static_cast<cudaError_t>(rcode), "occupancy query");
@@ -829,7 +841,7 @@ void certify_round(pp_handle* h, ppdev::RoundArgs& a, uint64_t t, int iter, int 
     list.erase(std::unique(list.begin(), list.end()), list.end());
     h->timing.refined += static_cast<int32_t>(list.size());
     std::vector<Exact> got(list.size());
-    if (list.size() <= static_cast<size_t>(kHostMax)) {
+    if (list.size() <= static_cast<size_t>(host_max())) {
       h->pool->run(static_cast<int>(list.size()), [&](int i) { got[i] = exact_of(list[i]); });
     } else {
       // wide window: FP64 keys from the device, exact host keys for the FP64
@@ -979,7 +991,7 @@ void host_rollout(const pp_handle* h, const pp_snapshot& s, const double* theta,
       // field; a caller's snapshot is scanned point by point
       bool hit;
       if (s.field_xy == nullptr) {
-        hit = ppfield::collides(h->field, h->chassis, k, z.x, z.y, z.phi);
+        hit = ppfield::collides(h->field, h->chassis, h->box, k, z.x, z.y, z.phi);
       } else {
         const std::span<const Vec2> row(
             reinterpret_cast<const Vec2*>(s.field_xy) + static_cast<size_t>(k) * N, N);
@@ -1073,6 +1085,7 @@ pp_status pp_create(const pp_model* m, pp_handle** out) {
     hp->params.validate();
     hp->cfg.validate();
     hp->chassis = paraplan::ChassisPolytope::rectangle(hp->params);
+    hp->box = {hp->params.front_extent(), hp->params.rear_extent(), hp->params.half_width};
     hp->P = hp->policy->param_count();
     hp->kind = ppdev::classify(hp->sizes.data(), static_cast<int32_t>(hp->sizes.size()));
     hp->fp64 = hp->cfg.precision == 64;

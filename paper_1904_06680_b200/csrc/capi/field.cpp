@@ -1,12 +1,19 @@
 // field.cpp -- static/dynamic split and cell binning of the obstacle field
 // (see field.hpp). Compiled with -ffp-contract=off: positions of the raw-
 // points path are x + h * step exactly as the reference's extrapolate.
+//
+// Dense clouds put (H+1) x Nd dynamic positions through the binning (2.5M at
+// N = 100k, 25% moving, H = 100): rows are binned in parallel on the host
+// cores, each row independent.
 #include "field.hpp"
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <stdexcept>
+#include <thread>
 
 namespace ppfield {
 
@@ -18,79 +25,184 @@ size_t align16(size_t v) { return (v + 15) & ~size_t(15); }
 // state beats a static and a dynamic scan of a handful of points each).
 constexpr int kSmall = 64;
 
-// Common grid over every point of every row: cell size half the query
-// window (g = cull / 2), a 2-D grid only for larger clouds, <= 4096 cells.
-void choose_grid(Binned& b, double xmin, double xmax, double ymin, double ymax) {
-  double g = 0.5 * b.cull;
-  const bool two_d = b.points() >= 128;
-  const double wx = xmax - xmin, wy = two_d ? ymax - ymin : 0.0;
+double env_or(const char* name, double dflt) {
+  const char* v = std::getenv(name);
+  return v != nullptr ? std::atof(v) : dflt;
+}
+
+// f(i) for i in [0, n), on up to 16 host threads when `work` is large.
+template <class F>
+void par_for(int n, size_t work, F&& f) {
+  const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+  const unsigned T = std::min<unsigned>({16u, hw, static_cast<unsigned>(std::max(n, 1))});
+  if (work < (size_t(1) << 17) || T <= 1) {
+    for (int i = 0; i < n; ++i) f(i);
+    return;
+  }
+  std::atomic<int> next{0};
+  const auto body = [&] {
+    for (int i; (i = next.fetch_add(1)) < n;) f(i);
+  };
+  std::vector<std::thread> th;
+  th.reserve(T - 1);
+  for (unsigned t = 1; t < T; ++t) th.emplace_back(body);
+  body();
+  for (auto& t : th) t.join();
+}
+
+struct BBox {
+  double xmin = 0, xmax = 0, ymin = 0, ymax = 0;
+  bool any = false;
+  bool finite = true;
+  void see(double x, double y) {
+    if (!(std::isfinite(x) && std::isfinite(y))) {
+      finite = false;
+      return;
+    }
+    if (!any || x < xmin) xmin = x;
+    if (!any || x > xmax) xmax = x;
+    if (!any || y < ymin) ymin = y;
+    if (!any || y > ymax) ymax = y;
+    any = true;
+  }
+  void merge(const BBox& o) {
+    finite &= o.finite;
+    if (!o.any) return;
+    see(o.xmin, o.ymin);
+    see(o.xmax, o.ymax);
+  }
+};
+
+// Common grid over every point of every row: cell size a fraction of the
+// bounding radius (the query window is the chassis bounding box, about
+// 2r x r), a 2-D grid only for larger clouds, <= 4096 cells.
+void choose_grid(Binned& b, const BBox& box) {
+  if (!box.finite) throw std::invalid_argument("obstacle field has non-finite coordinates");
+  // tuning knobs (defaults measured on B200)
+  static const double frac = env_or("PARAPLAN_GRID_FRAC", 0.25);
+  static const double min2d = env_or("PARAPLAN_GRID2D_MIN", 128);
+  double g = frac * b.cull;
+  const bool two_d = b.points() >= min2d;
+  const double wx = box.xmax - box.xmin, wy = two_d ? box.ymax - box.ymin : 0.0;
   while ((std::floor(wx / g) + 1) * (two_d ? std::floor(wy / g) + 1 : 1.0) > 4096.0) g *= 1.25;
   b.g = g;
-  b.x0 = xmin;
-  b.y0 = ymin;
+  b.x0 = box.xmin;
+  b.y0 = box.ymin;
   b.nx = static_cast<int>(std::floor(wx / g)) + 1;
   b.ny = two_d ? static_cast<int>(std::floor(wy / g)) + 1 : 1;
 }
 
-int cell_of(const Binned& b, double x, double y) {
-  const int cx = std::min(b.nx - 1, std::max(0, static_cast<int>(std::floor((x - b.x0) / b.g))));
-  const int cy =
-      b.ny == 1 ? 0 : std::min(b.ny - 1, std::max(0, static_cast<int>(std::floor((y - b.y0) / b.g))));
-  return cx * b.ny + cy;
-}
+// Cell of a point (x-major). Queries cover the chassis box + g/8, so a point
+// near a cell edge may land on either side of it.
+struct CellOf {
+  double x0, y0, inv;
+  int nx, ny;
+  explicit CellOf(const Binned& b) : x0(b.x0), y0(b.y0), inv(1.0 / b.g), nx(b.nx), ny(b.ny) {}
+  static int clampi(double t, int n) { return t <= 0.0 ? 0 : std::min(n - 1, static_cast<int>(t)); }
+  int operator()(double x, double y) const {
+    return clampi((x - x0) * inv, nx) * ny + (ny == 1 ? 0 : clampi((y - y0) * inv, ny));
+  }
+};
 
 // Stable counting sort of n points (xy) into `out` (cell order) + starts.
 void bin(const Binned& b, const double* xy, int n, double* out, int32_t* starts,
-         std::vector<int32_t>& cell, std::vector<int32_t>& fill) {
+         std::vector<int32_t>& cell) {
   const int cells = b.cells();
+  const CellOf cell_of(b);
   cell.resize(n);
-  fill.assign(cells + 1, 0);
+  std::fill(starts, starts + cells + 1, 0);
   for (int j = 0; j < n; ++j) {
-    cell[j] = cell_of(b, xy[2 * j], xy[2 * j + 1]);
-    ++fill[cell[j] + 1];
+    cell[j] = cell_of(xy[2 * j], xy[2 * j + 1]);
+    ++starts[cell[j] + 1];
   }
-  for (int c = 0; c < cells; ++c) fill[c + 1] += fill[c];
-  std::copy(fill.begin(), fill.end(), starts);
+  for (int c = 0; c < cells; ++c) starts[c + 1] += starts[c];
+  // scatter with starts[c] as the running cursor, then shift back
   for (int j = 0; j < n; ++j) {
-    const int at = fill[cell[j]]++;
+    const int at = starts[cell[j]]++;
     out[2 * at] = xy[2 * j];
     out[2 * at + 1] = xy[2 * j + 1];
   }
+  for (int c = cells; c > 0; --c) starts[c] = starts[c - 1];
+  starts[0] = 0;
 }
 
-void finish(Binned& b, const std::vector<double>& s_xy, const std::vector<double>& d_xy) {
-  double xmin = 0, xmax = 0, ymin = 0, ymax = 0;
-  bool first = true;
-  const auto see = [&](const std::vector<double>& v) {
-    for (size_t i = 0; i + 1 < v.size(); i += 2) {
-      const double x = v[i], y = v[i + 1];
-      if (!(std::isfinite(x) && std::isfinite(y))) {
-        throw std::invalid_argument("obstacle field has non-finite coordinates");
-      }
-      if (first || x < xmin) xmin = x;
-      if (first || x > xmax) xmax = x;
-      if (first || y < ymin) ymin = y;
-      if (first || y > ymax) ymax = y;
-      first = false;
-    }
-  };
-  see(s_xy);
-  see(d_xy);
-  choose_grid(b, xmin, xmax, ymin, ymax);
+// Tight point boxes of the static cells, kept when the static part is dense
+// (mean points per occupied cell >= PARAPLAN_CELL_BOX_MIN) and structured
+// (mean box area below half a cell: lines and walls rather than a uniform
+// fill, which a box test cannot thin out). There a box test per visited cell
+// is cheaper than scanning its points.
+void cell_boxes(Binned& b) {
+  static const double min_fill = env_or("PARAPLAN_CELL_BOX_MIN", 8);
+  static const double max_area = env_or("PARAPLAN_CELL_BOX_AREA", 0.5);
+  b.boxes = false;
+  if (b.ny <= 1 || b.Ns == 0) return;
   const int cells = b.cells();
-  std::vector<int32_t> cell, fill;
+  int occupied = 0;
+  for (int c = 0; c < cells; ++c) occupied += b.sst[c + 1] > b.sst[c];
+  if (static_cast<double>(b.Ns) < min_fill * occupied) return;
+  b.sbox.resize(4 * static_cast<size_t>(cells));
+  double area = 0.0;
+  for (int c = 0; c < cells; ++c) {
+    double x0 = 0, x1 = -1, y0 = 0, y1 = -1;  // empty: negative half extents
+    for (int j = b.sst[c]; j < b.sst[c + 1]; ++j) {
+      const double x = b.spts[2 * j], y = b.spts[2 * j + 1];
+      if (j == b.sst[c]) {
+        x0 = x1 = x;
+        y0 = y1 = y;
+      } else {
+        x0 = std::min(x0, x);
+        x1 = std::max(x1, x);
+        y0 = std::min(y0, y);
+        y1 = std::max(y1, y);
+      }
+    }
+    double* o = b.sbox.data() + 4 * static_cast<size_t>(c);
+    o[0] = 0.5 * (x0 + x1);
+    o[1] = 0.5 * (y0 + y1);
+    o[2] = 0.5 * (x1 - x0);
+    o[3] = 0.5 * (y1 - y0);
+    if (x1 >= x0) area += (x1 - x0) * (y1 - y0);
+  }
+  b.boxes = area < max_area * occupied * b.g * b.g;
+}
+
+// Grid + static bins + dynamic rows: row(r, xy) writes the Nd positions of
+// dynamic row r.
+template <class Row>
+void finish(Binned& b, const std::vector<double>& s_xy, const BBox& box, Row&& row) {
+  choose_grid(b, box);
+  const int cells = b.cells();
+  std::vector<int32_t> cell;
   b.spts.resize(2 * static_cast<size_t>(b.Ns));
   b.sst.assign(cells + 1, 0);
-  if (b.Ns > 0) bin(b, s_xy.data(), b.Ns, b.spts.data(), b.sst.data(), cell, fill);
+  if (b.Ns > 0) bin(b, s_xy.data(), b.Ns, b.spts.data(), b.sst.data(), cell);
+  cell_boxes(b);
   b.dpts.resize(2 * static_cast<size_t>(b.Nd) * b.rows);
   b.dst.assign(static_cast<size_t>(b.rows) * (cells + 1), 0);
   if (b.Nd > 0) {
-    for (int r = 0; r < b.rows; ++r) {
+    par_for(b.rows, static_cast<size_t>(b.rows) * b.Nd, [&](int r) {
+      thread_local std::vector<double> xy;
+      thread_local std::vector<int32_t> tcell;
+      xy.resize(2 * static_cast<size_t>(b.Nd));
+      row(r, xy.data());
       const size_t o = static_cast<size_t>(r) * b.Nd * 2;
-      bin(b, d_xy.data() + o, b.Nd, b.dpts.data() + o, b.dst.data() + static_cast<size_t>(r) * (cells + 1),
-          cell, fill);
-    }
+      bin(b, xy.data(), b.Nd, b.dpts.data() + o, b.dst.data() + static_cast<size_t>(r) * (cells + 1),
+          tcell);
+    });
   }
+}
+
+// Scalars back to their defaults; the vectors keep their storage, so a
+// planner re-binning a field of the same shape every tick neither allocates
+// nor faults pages in.
+void reset(Binned& b, int rows, double cull) {
+  b.Ns = b.Nd = 0;
+  b.boxes = false;
+  b.nx = b.ny = 1;
+  b.x0 = b.y0 = 0.0;
+  b.g = 1.0;
+  b.rows = rows;
+  b.cull = cull;
 }
 
 }  // namespace
@@ -100,57 +212,59 @@ Layout layout(const Binned& b, size_t elem) {
   l.dpts = align16(2 * elem * b.Ns);
   l.sst = align16(l.dpts + 2 * elem * static_cast<size_t>(b.Nd) * b.rows);
   l.dst = align16(l.sst + sizeof(int32_t) * (b.cells() + 1));
-  l.bytes = align16(l.dst + sizeof(int32_t) * static_cast<size_t>(b.rows) * (b.cells() + 1));
+  l.sbox = align16(l.dst + sizeof(int32_t) * static_cast<size_t>(b.rows) * (b.cells() + 1));
+  l.bytes = align16(l.sbox + (b.boxes ? 4 * elem * static_cast<size_t>(b.cells()) : 0));
   return l;
 }
 
 void from_rows(Binned& b, const double* xy, int rows, int N, double cull) {
-  b = Binned{};
-  b.rows = rows;
-  b.cull = cull;
-  std::vector<char> moving(N, 0);
+  reset(b, rows, cull);
   const size_t len = 2 * static_cast<size_t>(N);
+  std::vector<char> moving(N, 0);
   for (int r = 1; r < rows; ++r) {
     const double* row = xy + r * len;
     for (int j = 0; j < N; ++j) {
-      if (!moving[j] && (std::memcmp(row + 2 * j, xy + 2 * j, 2 * sizeof(double)) != 0)) {
-        moving[j] = 1;
-      }
+      moving[j] |= std::memcmp(row + 2 * j, xy + 2 * j, 2 * sizeof(double)) != 0;
     }
   }
   // small mixed clouds stay one scan per state: every point dynamic
   if (N <= kSmall && std::count(moving.begin(), moving.end(), 1) > 0) {
     std::fill(moving.begin(), moving.end(), 1);
   }
-  std::vector<double> s_xy, d_xy;
+  std::vector<double> s_xy;
   std::vector<int> dyn;
+  BBox box;
   for (int j = 0; j < N; ++j) {
     if (moving[j]) {
       dyn.push_back(j);
     } else {
       s_xy.push_back(xy[2 * j]);
       s_xy.push_back(xy[2 * j + 1]);
+      box.see(xy[2 * j], xy[2 * j + 1]);
     }
   }
   b.Ns = N - static_cast<int>(dyn.size());
   b.Nd = static_cast<int>(dyn.size());
-  d_xy.resize(2 * static_cast<size_t>(b.Nd) * rows);
-  for (int r = 0; r < rows; ++r) {
-    for (int k = 0; k < b.Nd; ++k) {
-      d_xy[(static_cast<size_t>(r) * b.Nd + k) * 2] = xy[r * len + 2 * dyn[k]];
-      d_xy[(static_cast<size_t>(r) * b.Nd + k) * 2 + 1] = xy[r * len + 2 * dyn[k] + 1];
-    }
+  if (b.Nd > 0) {  // rows are arbitrary: every dynamic position joins the box
+    std::vector<BBox> rb(rows);
+    par_for(rows, static_cast<size_t>(rows) * b.Nd, [&](int r) {
+      const double* row = xy + r * len;
+      for (int k = 0; k < b.Nd; ++k) rb[r].see(row[2 * dyn[k]], row[2 * dyn[k] + 1]);
+    });
+    for (const BBox& o : rb) box.merge(o);
   }
-  finish(b, s_xy, d_xy);
+  finish(b, s_xy, box, [&](int r, double* out) {
+    const double* row = xy + r * len;
+    for (int k = 0; k < b.Nd; ++k) {
+      out[2 * k] = row[2 * dyn[k]];
+      out[2 * k + 1] = row[2 * dyn[k] + 1];
+    }
+  });
 }
 
 void from_points(Binned& b, const double* pts4, int N, int rows, double T_s, double cull) {
-  b = Binned{};
-  b.rows = rows;
-  b.cull = cull;
-  std::vector<double> s_xy, d_xy;
-  std::vector<int> dyn;
-  std::vector<double> stepx, stepy;
+  reset(b, rows, cull);
+  std::vector<double> s_xy, base, step;
   bool any_moving = false;
   for (int j = 0; j < N; ++j) {
     const double* p = pts4 + 4 * j;
@@ -158,6 +272,7 @@ void from_points(Binned& b, const double* pts4, int N, int rows, double T_s, dou
   }
   // small mixed clouds stay one scan per state: every point dynamic
   const bool all_dynamic = N <= kSmall && any_moving;
+  BBox box;
   for (int j = 0; j < N; ++j) {
     const double* p = pts4 + 4 * j;
     // src/geometry.cpp:51-52
@@ -166,24 +281,27 @@ void from_points(Binned& b, const double* pts4, int N, int rows, double T_s, dou
     if (!all_dynamic && sx == 0.0 && sy == 0.0) {  // x + h * (+-0) == x: identical rows
       s_xy.push_back(p[0]);
       s_xy.push_back(p[1]);
+      box.see(p[0], p[1]);
     } else {
-      dyn.push_back(j);
-      stepx.push_back(sx);
-      stepy.push_back(sy);
+      base.push_back(p[0]);
+      base.push_back(p[1]);
+      step.push_back(sx);
+      step.push_back(sy);
+      // x + r * step is monotone in r (rounding is monotone): rows 0 and
+      // rows - 1 bound every position of the point
+      box.see(p[0], p[1]);
+      box.see(p[0] + (rows - 1) * sx, p[1] + (rows - 1) * sy);
     }
   }
   b.Ns = static_cast<int>(s_xy.size() / 2);
-  b.Nd = static_cast<int>(dyn.size());
-  d_xy.resize(2 * static_cast<size_t>(b.Nd) * rows);
-  for (int r = 0; r < rows; ++r) {
+  b.Nd = static_cast<int>(base.size() / 2);
+  finish(b, s_xy, box, [&](int r, double* out) {
+    // src/geometry.cpp:53-57: x + h * step (int h promoted to double)
     for (int k = 0; k < b.Nd; ++k) {
-      const double* p = pts4 + 4 * dyn[k];
-      // src/geometry.cpp:53-57: x + h * step (int h promoted to double)
-      d_xy[(static_cast<size_t>(r) * b.Nd + k) * 2] = p[0] + r * stepx[k];
-      d_xy[(static_cast<size_t>(r) * b.Nd + k) * 2 + 1] = p[1] + r * stepy[k];
+      out[2 * k] = base[2 * k] + r * step[2 * k];
+      out[2 * k + 1] = base[2 * k + 1] + r * step[2 * k + 1];
     }
-  }
-  finish(b, s_xy, d_xy);
+  });
 }
 
 void pack(const Binned& b, bool fp64, void* out) {
@@ -191,21 +309,44 @@ void pack(const Binned& b, bool fp64, void* out) {
   const Layout l = layout(b, elem);
   unsigned char* base = static_cast<unsigned char*>(out);
   const auto put = [&](size_t off, const std::vector<double>& v) {
-    if (fp64) {
-      std::memcpy(base + off, v.data(), v.size() * sizeof(double));
-    } else {
-      float* f = reinterpret_cast<float*>(base + off);
-      for (size_t i = 0; i < v.size(); ++i) f[i] = static_cast<float>(v[i]);
-    }
+    constexpr size_t kChunk = size_t(1) << 16;
+    const int chunks = static_cast<int>((v.size() + kChunk - 1) / kChunk);
+    par_for(chunks, v.size(), [&](int c) {
+      const size_t lo = c * kChunk, hi = std::min(v.size(), lo + kChunk);
+      if (fp64) {
+        std::memcpy(base + off + lo * sizeof(double), v.data() + lo, (hi - lo) * sizeof(double));
+      } else {
+        float* f = reinterpret_cast<float*>(base + off);
+        for (size_t i = lo; i < hi; ++i) f[i] = static_cast<float>(v[i]);
+      }
+    });
   };
   put(0, b.spts);
   put(l.dpts, b.dpts);
   std::memcpy(base + l.sst, b.sst.data(), b.sst.size() * sizeof(int32_t));
   std::memcpy(base + l.dst, b.dst.data(), b.dst.size() * sizeof(int32_t));
+  if (b.boxes) put(l.sbox, b.sbox);
 }
 
-bool collides(const Binned& b, const paraplan::ChassisPolytope& ch, int k, double x, double y,
-              double phi) {
+namespace {
+bool box_separated(const double* bx, double c, double s, double kx, double ky, double bh, double hw,
+                   double pad) {
+  // separating axes: the rectangle's own (u = (c, s), v = (-s, c)); the
+  // world axes are covered by the query window
+  const double ac = std::abs(c), as = std::abs(s);
+  const double du = c * bx[0] + s * bx[1] - kx, dv = -s * bx[0] + c * bx[1] - ky;
+  return std::abs(du) > bh + bx[2] * ac + bx[3] * as + pad ||
+         std::abs(dv) > hw + bx[2] * as + bx[3] * ac + pad;
+}
+}  // namespace
+
+namespace {
+bool box_separated(const double* bx, double c, double s, double kx, double ky, double bh, double hw,
+                   double pad);
+}
+
+bool collides(const Binned& b, const paraplan::ChassisPolytope& ch, const Box& box, int k, double x,
+              double y, double phi) {
   if (b.points() == 0) return false;
   const auto cx_of = [&](double v) {
     return std::min(b.nx - 1, std::max(0, static_cast<int>(std::floor((v - b.x0) / b.g))));
@@ -214,22 +355,48 @@ bool collides(const Binned& b, const paraplan::ChassisPolytope& ch, int k, doubl
     return b.ny == 1 ? 0
                      : std::min(b.ny - 1, std::max(0, static_cast<int>(std::floor((v - b.y0) / b.g))));
   };
-  const int cx0 = cx_of(x - b.cull), cx1 = cx_of(x + b.cull);
-  const int cy0 = cy_of(y - b.cull), cy1 = cy_of(y + b.cull);
   // src/geometry.cpp:63-76, expression by expression
   const double c = std::cos(phi), s = std::sin(phi);
+  // world bounding box of the rectangle (+ g/8): points outside it are
+  // outside the rectangle, a miss in the reference's test
+  const double bc = 0.5 * (box.front - box.rear), bh = 0.5 * (box.front + box.rear);
+  const double pad = b.g / 8.0;
+  const double ox = x + bc * c, oy = y + bc * s;
+  const double ex = bh * std::abs(c) + box.half_width * std::abs(s) + pad;
+  const double ey = bh * std::abs(s) + box.half_width * std::abs(c) + pad;
+  const int cx0 = cx_of(ox - ex), cx1 = cx_of(ox + ex);
+  const int cy0 = cy_of(oy - ey), cy1 = cy_of(oy + ey);
   const double r2 = ch.bounding_radius() * ch.bounding_radius();
-  const auto scan = [&](const double* pts, const int32_t* st) {
-    for (int cx = cx0; cx <= cx1; ++cx) {
-      for (int j = st[cx * b.ny + cy0]; j < st[cx * b.ny + cy1 + 1]; ++j) {
-        const double dx = pts[2 * j] - x, dy = pts[2 * j + 1] - y;
-        if (dx * dx + dy * dy >= r2) continue;
-        if (ch.contains({c * dx + s * dy, -s * dx + c * dy})) return true;
-      }
+  const auto test = [&](const double* pts, int j0, int j1) {
+    for (int j = j0; j < j1; ++j) {
+      const double dx = pts[2 * j] - x, dy = pts[2 * j + 1] - y;
+      if (dx * dx + dy * dy >= r2) continue;
+      if (ch.contains({c * dx + s * dy, -s * dx + c * dy})) return true;
     }
     return false;
   };
-  if (b.Ns > 0 && scan(b.spts.data(), b.sst.data())) return true;
+  const auto scan = [&](const double* pts, const int32_t* st) {
+    for (int cx = cx0; cx <= cx1; ++cx) {
+      if (test(pts, st[cx * b.ny + cy0], st[cx * b.ny + cy1 + 1])) return true;
+    }
+    return false;
+  };
+  if (b.Ns > 0 && b.boxes) {  // cell by cell, skipping cells whose box is clear of the rectangle
+    const double kx = c * x + s * y + bc, ky = -s * x + c * y;
+    for (int cx = cx0; cx <= cx1; ++cx) {
+      for (int cy = cy0; cy <= cy1; ++cy) {
+        const int cell = cx * b.ny + cy;
+        if (b.sst[cell + 1] == b.sst[cell]) continue;
+        if (box_separated(b.sbox.data() + 4 * static_cast<size_t>(cell), c, s, kx, ky, bh,
+                          box.half_width, pad)) {
+          continue;
+        }
+        if (test(b.spts.data(), b.sst[cell], b.sst[cell + 1])) return true;
+      }
+    }
+  } else if (b.Ns > 0 && scan(b.spts.data(), b.sst.data())) {
+    return true;
+  }
   if (b.Nd > 0) {
     const int cells = b.cells();
     return scan(b.dpts.data() + static_cast<size_t>(k) * b.Nd * 2,

@@ -32,13 +32,21 @@ struct Binned {
   std::vector<double> dpts;      // rows x Nd x 2, per row cell order
   std::vector<int32_t> sst;      // cells + 1
   std::vector<int32_t> dst;      // rows x (cells + 1)
+  // Dense static clouds: per cell the tight bounding box of its points as
+  // (centre x, centre y, half width, half height); a query skips a cell whose
+  // box is separated from the chassis rectangle.
+  bool boxes = false;
+  std::vector<double> sbox;      // cells x 4 (when boxes)
   int cells() const { return nx * ny; }
+  // 0: x-buckets, 1: 2-D cells scanned by column, 2: 2-D cells with boxes
+  int mode() const { return boxes ? 2 : (ny > 1 ? 1 : 0); }
   int points() const { return Ns + Nd; }
 };
 
-// Device image layout: byte offsets of [spts][dpts][sst][dst] (16-aligned).
+// Device image layout: byte offsets of [spts][dpts][sst][dst][sbox]
+// (16-aligned).
 struct Layout {
-  size_t dpts = 0, sst = 0, dst = 0, bytes = 0;
+  size_t dpts = 0, sst = 0, dst = 0, sbox = 0, bytes = 0;
 };
 Layout layout(const Binned& b, size_t elem);
 
@@ -54,9 +62,15 @@ void from_points(Binned& b, const double* pts4, int N, int rows, double T_s, dou
 // Device image in the compute precision (fp64: the binned doubles as-is).
 void pack(const Binned& b, bool fp64, void* out);
 
-// Exact collision at state k (the reference's per-point test).
-bool collides(const Binned& b, const paraplan::ChassisPolytope& ch, int k, double x, double y,
-              double phi);
+// The chassis rectangle in the body frame: -rear < x < front, |y| < half_width.
+struct Box {
+  double front = 0.0, rear = 0.0, half_width = 0.0;
+};
+
+// Exact collision at state k (the reference's per-point test) over the cells
+// covering the world bounding box of `box` at (x, y, phi) + g/8.
+bool collides(const Binned& b, const paraplan::ChassisPolytope& ch, const Box& box, int k, double x,
+              double y, double phi);
 
 // The full (rows x N) position of point j of row k in the reference's order
 // is not needed by anyone: the field is only ever queried by state.

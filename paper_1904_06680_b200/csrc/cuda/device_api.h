@@ -57,7 +57,7 @@ struct ConstsT {
   Real fe, re, hw, r2;  // chassis half-planes, squared bounding radius
   Real cull;            // collision x-window half width: bounding radius + 1e-3
   Real bx0, by0, binv;  // cell grid of the field: origin, 1 / cell size
-  Real qpad;            // cell query half width: cull + cell size / 8
+  Real qpad;            // pad of the chassis bounding box query: cell size / 8
   Real dmarg;           // |margin| below which a discrete verdict is "marginal"
   Real bcx, bhx;        // rectangle centre offset (fe - re)/2 and half length (fe + re)/2
   Real inv_wb;          // 1 / wheelbase (FP32 path multiplies)
@@ -67,7 +67,7 @@ struct ConstsT {
 
 // Byte offsets of the parts of a field image.
 struct FieldLayout {
-  int64_t dpts, sst, dst, bytes;
+  int64_t dpts, sst, dst, sbox, bytes;
 };
 
 // Everything one sampling round needs. Scalars are FP64 here; the FP32
@@ -103,10 +103,13 @@ struct RoundArgs {
   const double* injected;      // device [count * n_params] or null (RNG off)
   // Obstacle field image (see csrc/capi/field.hpp): [static pts Real2 x Ns]
   // [dynamic pts Real2 x (H+1) x Nd][static starts int32 x (cells+1)]
-  // [dynamic starts int32 x (H+1) x (cells+1)], points in cell order.
+  // [dynamic starts int32 x (H+1) x (cells+1)][static cell boxes Real4 x
+  // cells, grid_mode 2 only], points in cell order.
   const void* field;
   int32_t field_ns, field_nd;  // static points, dynamic points per row
   int32_t grid_nx, grid_ny;    // cells (grid_ny == 1: x-buckets)
+  int32_t grid_mode;           // 0 x-buckets, 1 2-D by column, 2 2-D with static cell boxes
+  int32_t _pad_mode;
   double grid_x0, grid_y0, grid_g;  // grid origin and cell size (host side)
   FieldLayout lay;             // byte offsets of the compute-precision image
   FieldLayout lay64;           // byte offsets of the FP64 image (field64)
@@ -152,8 +155,8 @@ struct LaunchShape {
 // field_bytes = shared-memory image of the field (0 = read from L2).
 // Returns 0 or a cudaError_t.
 // grid: the field uses the 2-D cell grid (separate kernel instantiation).
-int shape_f32(NetKind k, int device, int field_bytes, bool grid, LaunchShape* out);
-int shape_f64(NetKind k, int device, int field_bytes, bool grid, LaunchShape* out);
+int shape_f32(NetKind k, int device, int field_bytes, int grid, LaunchShape* out);
+int shape_f64(NetKind k, int device, int field_bytes, int grid, LaunchShape* out);
 
 // Enqueue one sampling round on `stream`. Returns 0 or a cudaError_t.
 int launch_round_f32(NetKind k, const RoundArgs& a, void* stream);

@@ -326,6 +326,7 @@ struct Field {
   const typename Vec2T<Real>::type* dpts;
   const int* sst;
   const int* dst;
+  const typename Vec2T<Real>::type* sbox;  // per cell: (centre), (half extents)
   int Ns, Nd;
   int ncx, ncy;
 };
@@ -337,8 +338,9 @@ __device__ __forceinline__ Field<Real> field_at(const RoundArgs& a, const void* 
   const unsigned char* p = static_cast<const unsigned char*>(base);
   return Field<Real>{reinterpret_cast<const R2*>(p), reinterpret_cast<const R2*>(p + l.dpts),
                      reinterpret_cast<const int*>(p + l.sst),
-                     reinterpret_cast<const int*>(p + l.dst), a.field_ns, a.field_nd,
-                     a.grid_nx, a.grid_ny};
+                     reinterpret_cast<const int*>(p + l.dst),
+                     reinterpret_cast<const R2*>(p + l.sbox), a.field_ns, a.field_nd, a.grid_nx,
+                     a.grid_ny};
 }
 
 // Inside-margin of one point against the chassis at (x, y, phi):
@@ -380,12 +382,12 @@ __device__ __forceinline__ float point_margin<float>(const Consts<float>& K, flo
 // all 32 lanes call it, every loop is warp-uniform.
 // Points of one part (static, or the dynamic row of state h) in the cells
 // covering the query window; updates the inside-margin `best`.
-template <typename Real, bool kGrid>
+template <typename Real, int kGrid>
 __device__ __forceinline__ void scan_part(const typename Vec2T<Real>::type* pts, const int* st,
                                           int ncy, int cx_lo, int cx_hi, int cy_lo, int cy_hi,
                                           const Consts<Real>& K, Real x, Real y, Real c, Real s,
                                           Real kx, Real ky, Real stop, Real& best) {
-  if constexpr (!kGrid) {  // x-buckets: the window is one contiguous range
+  if constexpr (kGrid == 0) {  // x-buckets: the window is one contiguous range
     const int lo = st[cx_lo];
     const int cnt = st[cx_hi + 1] - lo;
     const int rounds = __reduce_max_sync(kFull, cnt);
@@ -414,26 +416,91 @@ __device__ __forceinline__ void scan_part(const typename Vec2T<Real>::type* pts,
   }
 }
 
+// Dense static part (grid_mode 2), column by column. A column holding more
+// than kDenseCol points in the window is visited cell by cell: a cell whose
+// tight point box is separated from the rectangle along the rectangle's own
+// axes (by more than the pad) holds no point the reference could report
+// inside, and is skipped without reading its points. Sparser columns are
+// scanned as one range, as in grid_mode 1.
+constexpr int kDenseCol = 16;
+
+template <typename Real>
+__device__ __forceinline__ void scan_boxed(const typename Vec2T<Real>::type* pts, const int* st,
+                                           const typename Vec2T<Real>::type* box, int ncy,
+                                           int cx_lo, int cx_hi, int cy_lo, int cy_hi,
+                                           const Consts<Real>& K, Real x, Real y, Real c, Real s,
+                                           Real kx, Real ky, Real stop, Real& best) {
+  const Real ac = fabs(c), as = fabs(s);
+  const int nrow = cy_hi - cy_lo + 1;
+  const int ncol = cx_hi - cx_lo + 1;
+  const int cols = __reduce_max_sync(kFull, ncol);
+  for (int k = 0; k < cols; ++k) {
+    const bool has = k < ncol;
+    const int cell0 = (has ? cx_lo + k : cx_lo) * ncy + cy_lo;
+    const int lo = st[cell0];
+    const int n = has ? st[cell0 + nrow] - lo : 0;
+    const bool dense = n > kDenseCol;
+    // dense columns: cell by cell behind the box test
+    const int rows = __reduce_max_sync(kFull, dense ? nrow : 0);
+    for (int q = 0; q < rows; ++q) {
+      int clo = 0, cnt = 0;
+      if (dense && q < nrow && best < stop) {
+        const int cell = cell0 + q;
+        clo = st[cell];
+        cnt = st[cell + 1] - clo;
+        if (cnt > 0) {
+          const auto m = box[2 * cell], e = box[2 * cell + 1];
+          const Real du = fabs(c * m.x + s * m.y - kx), dv = fabs(-s * m.x + c * m.y - ky);
+          if (du > K.bhx + e.x * ac + e.y * as + K.qpad ||
+              dv > K.hw + e.x * as + e.y * ac + K.qpad) {
+            cnt = 0;
+          }
+        }
+      }
+      for (int j = 0; __any_sync(kFull, j < cnt && best < stop); ++j) {
+        if (j < cnt && best < stop) {
+          const auto m = pts[clo + j];
+          best = fmax(best, point_margin<Real>(K, x, y, c, s, kx, ky, m.x, m.y));
+        }
+      }
+    }
+    // sparse columns: one range
+    const int cnt = dense ? 0 : n;
+    for (int j = 0; __any_sync(kFull, j < cnt && best < stop); ++j) {
+      if (j < cnt && best < stop) {
+        const auto m = pts[lo + j];
+        best = fmax(best, point_margin<Real>(K, x, y, c, s, kx, ky, m.x, m.y));
+      }
+    }
+  }
+}
+
 // Collision of the chassis at (x, y, phi) with the field at state h. Only the
-// cells covering [x - qpad, x + qpad] (x [y - qpad, y + qpad] with a 2-D
-// grid) are visited: every other point is farther than cull > r from the
-// vehicle and fails the reference's bounding-circle prefilter
-// (src/geometry.cpp:71). Returns the inside-margin max over visited points
-// (the reference reports a collision iff it is > 0; a small |margin| marks a
-// verdict rounding could flip). Warp-synchronous: all 32 lanes call it,
-// every loop is warp-uniform.
-template <typename Real, bool kGrid>
+// cells covering the world-frame bounding box of the chassis rectangle (+ a
+// pad of an eighth of a cell) are visited: the reference reports a point
+// inside only if it lies strictly inside the rectangle (src/geometry.cpp:
+// 63-76), so every point outside that box is a miss whatever the rounding.
+// Returns the inside-margin max over visited points (the reference reports a
+// collision iff it is > 0; a small |margin| marks a verdict rounding could
+// flip). Warp-synchronous: all 32 lanes call it, every loop is warp-uniform.
+template <typename Real, int kGrid>
 __device__ __forceinline__ Real collide_margin(const Field<Real>& f, const Consts<Real>& K, int h,
                                                Real x, Real y, Real c, Real s, Real stop) {
   const int ncx = f.ncx, ncy = f.ncy;
+  const Real ac = fabs(c), as = fabs(s);
   const Real top = Real(ncx - 1);
-  const int cx_lo = static_cast<int>(fmin(fmax((x - K.qpad - K.bx0) * K.binv, Real(0)), top));
-  const int cx_hi = static_cast<int>(fmin(fmax((x + K.qpad - K.bx0) * K.binv, Real(0)), top));
+  // rectangle centre (x, y) + bcx (c, s); half extents bhx |c| + hw |s| (x)
+  const Real ox = x + K.bcx * c - K.bx0;
+  const Real ex = K.bhx * ac + K.hw * as + K.qpad;
+  const int cx_lo = static_cast<int>(fmin(fmax((ox - ex) * K.binv, Real(0)), top));
+  const int cx_hi = static_cast<int>(fmin(fmax((ox + ex) * K.binv, Real(0)), top));
   int cy_lo = 0, cy_hi = 0;
   if constexpr (kGrid) {
     const Real ytop = Real(ncy - 1);
-    cy_lo = static_cast<int>(fmin(fmax((y - K.qpad - K.by0) * K.binv, Real(0)), ytop));
-    cy_hi = static_cast<int>(fmin(fmax((y + K.qpad - K.by0) * K.binv, Real(0)), ytop));
+    const Real oy = y + K.bcx * s - K.by0;
+    const Real ey = K.bhx * as + K.hw * ac + K.qpad;
+    cy_lo = static_cast<int>(fmin(fmax((oy - ey) * K.binv, Real(0)), ytop));
+    cy_hi = static_cast<int>(fmin(fmax((oy + ey) * K.binv, Real(0)), ytop));
   }
   const Real kx = c * x + s * y + K.bcx;  // FP32 rotated-frame form only
   const Real ky = -s * x + c * y;
@@ -446,6 +513,13 @@ __device__ __forceinline__ Real collide_margin(const Field<Real>& f, const Const
     if ((dyn ? f.Nd : f.Ns) == 0) continue;
     const auto* pts = dyn ? f.dpts + static_cast<size_t>(h) * f.Nd : f.spts;
     const int* st = dyn ? f.dst + static_cast<size_t>(h) * (ncx * ncy + 1) : f.sst;
+    if constexpr (kGrid == 2) {
+      if (!dyn) {
+        scan_boxed<Real>(pts, st, f.sbox, ncy, cx_lo, cx_hi, cy_lo, cy_hi, K, x, y, c, s, kx, ky,
+                         stop, best);
+        continue;
+      }
+    }
     scan_part<Real, kGrid>(pts, st, ncy, cx_lo, cx_hi, cy_lo, cy_hi, K, x, y, c, s, kx, ky, stop,
                            best);
   }
@@ -486,7 +560,7 @@ __device__ __forceinline__ void start_features(const Consts<Real>& K, Real s[5])
 // Warp-synchronous and branch-free: the checks and the next state are
 // computed for every lane and committed only by the lanes still running,
 // so the warp never splits into per-outcome paths.
-template <typename Real, bool kGrid, class Net>
+template <typename Real, int kGrid, class Net>
 __device__ __forceinline__ int advance(Lane<Real>& L, const Net& net, const Consts<Real>& K,
                                        const Field<Real>& f, int H) {
   Real sphi, cphi;
@@ -794,7 +868,7 @@ constexpr int refill_min_blocks() {
   return sizeof(Real) == 4 ? (Net::kP <= 24 ? PARAPLAN_REFILL_MINB : 3) : (Net::kP <= 24 ? 4 : 2);
 }
 
-template <typename Real, class Net, bool kGrid>
+template <typename Real, class Net, int kGrid>
 __global__ void __launch_bounds__(kBlock, refill_min_blocks<Real, Net>())
     refill_kernel(const RoundArgs a) {
   constexpr int P = Net::kP;
@@ -944,7 +1018,7 @@ struct NetFactory<Real, NetGlobal<Real>> {
   }
 };
 
-template <typename Real, class Net, bool kGrid>
+template <typename Real, class Net, int kGrid>
 __global__ void __launch_bounds__(kBlock) lockstep_kernel(const RoundArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ Key red[32];
@@ -1059,7 +1133,7 @@ struct RefineNet<NetGlobal<double>> {
   }
 };
 
-template <class Net64, bool kGrid>
+template <class Net64, int kGrid>
 __global__ void __launch_bounds__(128) refine_kernel(const RoundArgs a) {
   const Consts<double>& K = a.kd;
   const unsigned n_sel = min(__ldcg(&a.counters[2]), static_cast<unsigned>(a.sel_cap));
@@ -1114,7 +1188,7 @@ bool refill_schedule() {
 
 using KernelFn = void (*)(const RoundArgs);
 
-template <typename Real, class Net, bool kGrid>
+template <typename Real, class Net, int kGrid>
 KernelFn kernel_of_g() {
   if constexpr (Net::kP > 0) {
     if (refill_schedule<Net>()) return refill_kernel<Real, Net, kGrid>;
@@ -1122,11 +1196,12 @@ KernelFn kernel_of_g() {
   return lockstep_kernel<Real, Net, kGrid>;
 }
 
-// grid: the field has a 2-D cell grid (dense clouds) -- a separate
-// instantiation so the small-field kernel stays lean.
+// grid mode of the field (0 x-buckets, 1 2-D, 2 2-D with cell boxes) -- a
+// separate instantiation each, so the small-field kernel stays lean.
 template <typename Real, class Net>
-KernelFn kernel_of(bool grid) {
-  return grid ? kernel_of_g<Real, Net, true>() : kernel_of_g<Real, Net, false>();
+KernelFn kernel_of(int mode) {
+  return mode == 2 ? kernel_of_g<Real, Net, 2>()
+                   : (mode == 1 ? kernel_of_g<Real, Net, 1>() : kernel_of_g<Real, Net, 0>());
 }
 
 template <typename Real, class Net>
@@ -1139,7 +1214,7 @@ int launch_impl(const RoundArgs& a, void* stream) {
       generate_kernel<Real, Net::kH1><<<gen_blocks, 256, 0, st>>>(a);
     }
   }
-  auto k = kernel_of<Real, Net>(a.grid_ny > 1);
+  auto k = kernel_of<Real, Net>(a.grid_mode);
   const size_t smem = static_cast<size_t>(a.field_smem_bytes);
   if (smem > 32 * 1024) {
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
@@ -1160,16 +1235,18 @@ inline int launch_select_impl(const RoundArgs& a, void* stream) {
 template <class Net64>
 int launch_refine_impl(const RoundArgs& a, void* stream) {
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (a.grid_ny > 1) {
-    refine_kernel<Net64, true><<<a.refine_grid, 128, 0, st>>>(a);
+  if (a.grid_mode == 2) {
+    refine_kernel<Net64, 2><<<a.refine_grid, 128, 0, st>>>(a);
+  } else if (a.grid_mode == 1) {
+    refine_kernel<Net64, 1><<<a.refine_grid, 128, 0, st>>>(a);
   } else {
-    refine_kernel<Net64, false><<<a.refine_grid, 128, 0, st>>>(a);
+    refine_kernel<Net64, 0><<<a.refine_grid, 128, 0, st>>>(a);
   }
   return static_cast<int>(cudaGetLastError());
 }
 
 template <typename Real, class Net>
-int shape_impl(int device, int field_bytes, bool grid, LaunchShape* out) {
+int shape_impl(int device, int field_bytes, int grid, LaunchShape* out) {
   auto k = kernel_of<Real, Net>(grid);
   const bool refill = refill_schedule<Net>();
   const int smem_bytes = field_bytes;

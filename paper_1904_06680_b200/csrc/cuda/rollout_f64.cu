@@ -3,7 +3,7 @@
 
 namespace ppdev {
 
-int shape_f64(NetKind k, int device, int smem_bytes, bool grid, LaunchShape* out) {
+int shape_f64(NetKind k, int device, int smem_bytes, int grid, LaunchShape* out) {
   switch (k) {
     case NetKind::k5_2_2:
       return shape_impl<double, NetReg<double, 2>>(device, smem_bytes, grid, out);

@@ -138,10 +138,14 @@ def c4(precision: int = abi.PP_FP32, samples: int = 1 << 22, n_points: int = 100
     m = spec.mission
     m.static_points = [pp.ObstaclePoint(*row) for row in densified_lot(n_points)]
     snap = snapshot_from_mission(m, m.initial_state, 0, H, n_points)
+    ev = m.initial_state
+    pts = np.array([(q.x, q.y, q.heading, q.speed) for q in
+                    pp.sense(m, ev, 0, n_points, pp.VehicleParams().T_s)], dtype=np.float64)
     model = abi.Model(H=H, n_restarts=1, n_candidates=samples, n_obst_pts=n_points,
                       precision=precision)
     return Workload("C4", model, snap, 0,
-                    f"reverse parking, {n_points} static lot points, H={H}, {samples} samples")
+                    f"reverse parking, {n_points} static lot points, H={H}, {samples} samples",
+                    extra={"points": pts})
 
 
 def c5(samples: int, H: int, n_points: int, precision: int = abi.PP_FP32,
@@ -160,7 +164,8 @@ def c5(samples: int, H: int, n_points: int, precision: int = abi.PP_FP32,
                         goal=(30.0, 0.0, 0.0, 50.0 / 3.6), field=abi.extrapolate(pts, H))
     model = abi.Model(H=H, n_restarts=1, n_candidates=samples, n_obst_pts=n_points,
                       precision=precision)
-    return Workload("C5", model, snap, 0, f"sweep point: {samples} samples, H={H}, N={n_points}")
+    return Workload("C5", model, snap, 0, f"sweep point: {samples} samples, H={H}, N={n_points}",
+                    extra={"points": pts})
 
 
 def algorithmic_flops(layer_sizes, n_points: int, executed_steps: int, checked_states: int) -> int:

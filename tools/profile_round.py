@@ -1,4 +1,4 @@
-"""One C2 sampling round (2^20 candidates, H=30, 20 points) repeated --reps
+"""One sampling round (default C2 (2^20 candidates, H=30, 20 points) repeated --reps
 times through the C-ABI: the command profiled under ncu (profiles/)."""
 import argparse
 import sys
@@ -12,8 +12,15 @@ ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--precision", type=int, default=32)
 ap.add_argument("--samples", type=int, default=1 << 20)
 ap.add_argument("--refine", type=int, default=1)
+ap.add_argument("--workload", default="c2", help="c2 | c4 | c5:N:H")
 a = ap.parse_args()
-w = workloads.c2(samples=a.samples, precision=a.precision)
+if a.workload == "c2":
+    w = workloads.c2(samples=a.samples, precision=a.precision)
+elif a.workload == "c4":
+    w = workloads.c4(samples=a.samples, precision=a.precision)
+else:
+    _, n_pts, H = a.workload.split(":")
+    w = workloads.c5(a.samples, int(H), int(n_pts), precision=a.precision)
 w.model.refine = a.refine
 dp = capi.DevicePlanner(w.model)
 dp.upload(w.snapshot)

@@ -31,9 +31,22 @@ def time_round(w, reps=3, refine=1):
         out.append(dict(wall_ms=wall, device_ms=t.kernel_ms, certify_ms=t.certify_ms,
                         refined=t.refined, steps=t.executed_steps, cls=int(rec[0]["cls"]),
                         cand=int(rec[0]["candidate"])))
-    dp.close()
     best = min(out[1:], key=lambda d: d["wall_ms"])
     best["nominal_steps_per_s"] = w.samples * w.model.H / (best["wall_ms"] * 1e-3)
+    # end to end through the C-ABI with host buffers: the (H+1) x N field, and
+    # (C4/C5) the raw sensed points the planner extrapolates itself
+    legs = [("e2e_field_ms", lambda: dp.plan_step(w.snapshot, w.t))]
+    if "points" in w.extra:
+        legs.append(("e2e_points_ms",
+                     lambda: dp.plan_step_points(w.snapshot, w.extra["points"], w.t)))
+    for name, call in legs:
+        ts = []
+        for _ in range(reps + 1):
+            t0 = time.perf_counter()
+            call()
+            ts.append((time.perf_counter() - t0) * 1e3)
+        best[name] = min(ts[1:])
+    dp.close()
     return best
 
 
@@ -58,6 +71,9 @@ if __name__ == "__main__":
     ap.add_argument("--which", default="C1,C2,C3,C4,C5")
     ap.add_argument("--c4-samples", type=int, default=1 << 20)
     ap.add_argument("--c3-ticks", type=int, default=20)
+    ap.add_argument("--fp64", type=int, default=1)
+    ap.add_argument("--c5-n", default="100,1000,10000,100000")
+    ap.add_argument("--c5-H", default="10,30,100")
     a = ap.parse_args()
     res = {}
     which = a.which.split(",")
@@ -65,13 +81,14 @@ if __name__ == "__main__":
         res["C1"] = time_round(workloads.c1())
     if "C2" in which:
         res["C2"] = time_round(workloads.c2())
-        res["C2_fp64"] = time_round(workloads.c2(precision=64))
+        if a.fp64:
+            res["C2_fp64"] = time_round(workloads.c2(precision=64))
     if "C3" in which:
         res["C3"] = closed_loop(1 << 20, 200, a.c3_ticks)
     if "C4" in which:
         res["C4"] = time_round(workloads.c4(samples=a.c4_samples), reps=1)
     if "C5" in which:
-        for n_pts in (100, 1000):
-            for H in (10, 50, 100):
+        for n_pts in map(int, a.c5_n.split(",")):
+            for H in map(int, a.c5_H.split(",")):
                 res[f"C5_n{n_pts}_H{H}"] = time_round(workloads.c5(1 << 20, H, n_pts), reps=1)
     print(json.dumps(res, indent=1))
