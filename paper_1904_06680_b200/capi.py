@@ -15,8 +15,8 @@ import numpy as np
 from . import abi
 
 # PARAPLAN_LIB selects an alternative build (A/B experiments only)
-LIB_PATH = Path(os.environ.get("PARAPLAN_LIB",
-                               Path(__file__).resolve().parent / "lib" / "libparaplan.so"))
+LIB_PATH = Path(os.environ.get("PARAPLAN_LIB")
+                or Path(__file__).resolve().parent / "lib" / "libparaplan.so")
 _lib = None
 
 

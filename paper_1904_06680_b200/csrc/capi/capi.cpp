@@ -20,10 +20,12 @@
 #include <atomic>
 #include <condition_variable>
 #include <functional>
+#include <map>
 #include <mutex>
 #include <thread>
 #include <unordered_map>
 #include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <cmath>
 #include <cstring>
@@ -271,6 +273,7 @@ struct pp_handle {
 
   // resident snapshot
   bool snap_valid = false;
+  std::map<int64_t, ppdev::LaunchShape> shapes;  // occupancy per (smem, grid mode, precision)
   ppdev::RoundArgs base{};
   int field_smem_bytes = 0;
 
@@ -553,6 +556,15 @@ constexpr int kSelCap = 1 << 16;    // near-tie candidates re-ranked per launch
 constexpr int kSelFirst = 512;      // copied back with the round result
 constexpr int kRefineGrid = 148 * 2;
 
+// PARAPLAN_TRACE=1: one stderr line per certification pass (diagnostics).
+bool trace_on() {
+  static const bool v = [] {
+    const char* e = std::getenv("PARAPLAN_TRACE");
+    return e != nullptr && std::atoi(e) != 0;
+  }();
+  return v;
+}
+
 // Windows up to this size are re-evaluated on the host pool (exact FP64
 // rollouts, 16 workers); wider ones get the FP64 device kernel first.
 int host_max() {
@@ -579,12 +591,20 @@ void run_round_launch(pp_handle* h, uint64_t t, int iter, int r0, int rc, const 
     a.field = ensure_field64(h);
     a.lay = a.lay64;
   }
-  ppdev::LaunchShape shape{};
   const int field_smem = (force_fp64 && !h->fp64) ? 0 : h->field_smem_bytes;
   const int grid2d = h->base.grid_mode;
-  const int rcode = fp64 ? ppdev::shape_f64(h->kind, h->device, field_smem, grid2d, &shape)
-                         : ppdev::shape_f32(h->kind, h->device, field_smem, grid2d, &shape);
-  ck(static_cast<cudaError_t>(rcode), "occupancy query");
+  // occupancy of the kernel for this (precision, staged field size, grid
+  // mode), queried once per handle
+  const int64_t skey = (static_cast<int64_t>(field_smem) << 8) | (grid2d << 1) | (fp64 ? 1 : 0);
+  auto found = h->shapes.find(skey);
+  if (found == h->shapes.end()) {
+    ppdev::LaunchShape sh{};
+    const int rcode = fp64 ? ppdev::shape_f64(h->kind, h->device, field_smem, grid2d, &sh)
+                           : ppdev::shape_f32(h->kind, h->device, field_smem, grid2d, &sh);
+    ck(static_cast<cudaError_t>(rcode), "occupancy query");
+    found = h->shapes.emplace(skey, sh).first;
+  }
+  const ppdev::LaunchShape shape = found->second;
   // refill: 32-candidate batches; lockstep: one tile of `block` candidates
   const int unit = shape.refill ? 32 : shape.block;
   const int64_t tpr64 = (count + unit - 1) / unit;
@@ -826,7 +846,13 @@ void certify_round(pp_handle* h, ppdev::RoundArgs& a, uint64_t t, int iter, int 
       h->timing.launches += 1;
       n_sel = h->h_selcount;
     }
-    if (n_sel > static_cast<uint32_t>(kSelCap)) break;
+    if (n_sel > static_cast<uint32_t>(kSelCap)) {
+      if (trace_on()) {
+        std::fprintf(stderr, "[paraplan] t=%llu iter=%d pass=%d selected=%u: window overflow\n",
+                     static_cast<unsigned long long>(t), iter, pass, n_sel);
+      }
+      break;
+    }
     if (n_sel > static_cast<uint32_t>(kSelFirst)) {
       ck(cudaMemcpy(static_cast<int64_t*>(h->h_sel.p) + kSelFirst, a.sel_list + kSelFirst,
                     sizeof(int64_t) * (n_sel - kSelFirst), cudaMemcpyDeviceToHost),
@@ -925,9 +951,18 @@ void certify_round(pp_handle* h, ppdev::RoundArgs& a, uint64_t t, int iter, int 
       const double widened = bd.thr * 1.25 + alpha;
       bound[r].thr = same ? std::max(e->cost * (1.0 + rho) + alpha, widened) : widened;
     }
+    if (trace_on()) {
+      std::fprintf(stderr, "[paraplan] t=%llu iter=%d pass=%d selected=%u new=%zu certified=%s\n",
+                   static_cast<unsigned long long>(t), iter, pass, n_sel, list.size(),
+                   all ? "all" : "no");
+    }
     if (all) return;
   }
   // overflowed or not certified: redo the round in FP64
+  if (trace_on()) {
+    std::fprintf(stderr, "[paraplan] t=%llu iter=%d: FP64 fallback round\n",
+                 static_cast<unsigned long long>(t), iter);
+  }
   if (fp64) throw std::runtime_error("near-tie re-ranking could not certify an FP64 round");
   h->timing.refined = -1;
   run_round_launch(h, t, iter, r0, rc, center, c0, c1, injected, out, nullptr, true);
@@ -1063,6 +1098,38 @@ int32_t pp_device_count(void) {
   return n;
 }
 
+// Warm-up at construction (the reference starts its thread pool in its
+// constructor as well): one obstacle-free round at the configured size
+// allocates the round buffers, loads the kernels and starts the host pool,
+// and the 2-D field kernels are loaded too, so the first plan_step pays for
+// none of it. Failures here are left for the first real call to report.
+void prewarm(pp_handle* h) {
+  if (const char* e = std::getenv("PARAPLAN_PREWARM"); e != nullptr && std::atoi(e) == 0) return;
+  try {
+    pp_snapshot s{};
+    s.goal_x = 1e3;
+    s.field_H = h->cfg.H;
+    upload_snapshot(h, s);
+    const int rc = std::min(h->cfg.n_restarts, 64);
+    std::vector<pp_record> rec(rc);
+    run_round(h, 0, 0, 0, rc, nullptr, 0, h->cfg.n_candidates, nullptr, rec.data(), nullptr);
+    for (int mode = 1; mode <= 2; ++mode) {
+      ppdev::LaunchShape sh{};
+      if (h->fp64) {
+        ppdev::shape_f64(h->kind, h->device, 0, mode, &sh);
+      } else {
+        ppdev::shape_f32(h->kind, h->device, 0, mode, &sh);
+      }
+    }
+    ck(cudaStreamSynchronize(h->stream), "warm-up");
+  } catch (...) {
+    cudaGetLastError();
+  }
+  h->snap_valid = false;
+  h->snapshot = nullptr;
+  h->timing = pp_timing{};
+}
+
 pp_status pp_create(const pp_model* m, pp_handle** out) {
   if (out != nullptr) *out = nullptr;
   pp_handle* h = nullptr;
@@ -1117,7 +1184,10 @@ pp_status pp_create(const pp_model* m, pp_handle** out) {
     ck(cudaStreamSynchronize(hp->stream), "init");
     h = hp.release();
   });
-  if (st == PP_OK) *out = h;
+  if (st == PP_OK) {
+    prewarm(h);
+    *out = h;
+  }
   return st;
 }
 

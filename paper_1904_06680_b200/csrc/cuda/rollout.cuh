@@ -292,11 +292,22 @@ __device__ __forceinline__ void draw_theta(const RoundArgs& a, uint64_t prefix, 
         exp10f(static_cast<float>(a.sig_lo + unit53(g.next()) * a.sig_span));
 #pragma unroll
     for (int i = 0; i < P; i += 2) {
-      const float u1 = static_cast<float>(1.0 - unit53(g.next()));
-      const float u2 = static_cast<float>(unit53(g.next()));
+      // float(1 - unit53) and float(unit53) straight from the integers:
+      // 1 - m 2^-53 = (2^53 - m) 2^-53 exactly, and scaling by 2^-53 commutes
+      // with rounding to float
+      const uint64_t m1 = g.next() >> 11, m2 = g.next() >> 11;
+      const float u1 = __ull2float_rn((1ull << 53) - m1) * 0x1.0p-53f;
+      const float u2 = __ull2float_rn(m2) * 0x1.0p-53f;
       const float r = sqrtf(-2.0f * logf(u1));
-      float sn, cs;
-      sincospif(2.0f * u2, &sn, &cs);
+      // sincos(2 pi u2): quarter-turn reduction t = 4 u2 - q is exact
+      const float q = rintf(4.0f * u2);
+      const float t = fmaf(4.0f, u2, -q) * 1.57079632679489662f;
+      const float sp = sin_poly(t), cp = cos_poly(t);
+      const int qi = static_cast<int>(q);
+      float sn = (qi & 1) ? cp : sp;
+      float cs = (qi & 1) ? sp : cp;
+      sn = (qi & 2) ? -sn : sn;
+      cs = ((qi + 1) & 2) ? -cs : cs;
       put(i, Real(static_cast<float>(__ldg(center + i)) + sigma * (r * cs)));
       if (i + 1 < P) put(i + 1, Real(static_cast<float>(__ldg(center + i + 1)) + sigma * (r * sn)));
     }
@@ -841,7 +852,10 @@ __global__ void __launch_bounds__(256) generate_kernel(const RoundArgs a) {
   const int64_t total = a.count * a.restart_count;
   for (int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; s < total;
        s += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int r = static_cast<int>(s / a.count);
+    // restart of flat index s (32-bit division when the round is small)
+    const int r = total <= 0x7fffffff
+                      ? static_cast<int>(static_cast<uint32_t>(s) / static_cast<uint32_t>(a.count))
+                      : static_cast<int>(s / a.count);
     const int64_t local = s - static_cast<int64_t>(r) * a.count;
     union {
       Real v[W];
