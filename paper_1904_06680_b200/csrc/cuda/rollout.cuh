@@ -735,15 +735,40 @@ __device__ __forceinline__ Key load_rec_cg(const Rec* src) {
 }
 
 // Field of the round, staged whole into shared memory when it fits
-// (a.field_smem_bytes > 0), else read through L1/L2.
+// (a.field_smem_bytes > 0), else read through L1/L2. The staging is one TMA
+// bulk copy (cp.async.bulk, global -> shared) issued by thread 0 and
+// completed on an mbarrier (transaction count = the image size, a multiple
+// of 16 bytes, <= 40 KB); every thread waits on the barrier's phase 0.
+__device__ __forceinline__ void bulk_stage(unsigned char* dst, const void* src, uint32_t bytes,
+                                           uint64_t* mbar) {
+  const uint32_t bar = static_cast<uint32_t>(__cvta_generic_to_shared(mbar));
+  if (threadIdx.x == 0) {
+    const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+                 : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(d),
+        "l"(src), "r"(bytes), "r"(bar)
+        : "memory");
+  }
+  __syncthreads();  // the barrier is initialised before anyone polls it
+  asm volatile(
+      "{\n"
+      ".reg .pred done;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], 0;\n"
+      "@!done bra WAIT_%=;\n"
+      "}\n" ::"r"(bar)
+      : "memory");
+}
+
 template <typename Real>
 __device__ __forceinline__ Field<Real> stage_field(const RoundArgs& a, unsigned char* smem) {
+  __shared__ __align__(8) uint64_t stage_bar;
   if (a.field_smem_bytes > 0 && a.n_points > 0) {
-    const int4* src = static_cast<const int4*>(a.field);
-    int4* dst = reinterpret_cast<int4*>(smem);
-    const int n16 = a.field_smem_bytes / 16;
-    for (int i = threadIdx.x; i < n16; i += blockDim.x) dst[i] = src[i];
-    __syncthreads();
+    bulk_stage(smem, a.field, static_cast<uint32_t>(a.field_smem_bytes), &stage_bar);
     return field_at<Real>(a, smem, a.lay);
   }
   __syncthreads();
