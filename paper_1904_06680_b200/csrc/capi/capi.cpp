@@ -257,16 +257,15 @@ struct pp_handle {
 
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-  DevBuf d_field, d_params, d_result, d_tiles, d_counters, d_samples, d_scratch, d_injected,
-      d_theta, d_skeys, d_sel, d_bound;
-  HostBuf h_field, h_params, h_result, h_sel, h_bound;
+  DevBuf d_field, d_params, d_round, d_tiles, d_samples, d_scratch, d_injected, d_theta, d_skeys,
+      d_sel, d_bound;
+  HostBuf h_field, h_params, h_round, h_bound;
 
   // near-tie re-ranking (PlannerConfig::refine): needs the host snapshot
   bool rerank = true;
   const pp_snapshot* snapshot = nullptr;  // -> snap_copy once a snapshot is resident
   pp_snapshot snap_copy{};
   std::vector<double> snap_warm;
-  uint32_t h_selcount = 0;
   double sel_rho = 1e-3;   // FP32 window: cost <= best * (1 + rho) + 1e-6
   std::unique_ptr<HostPool> pool;  // exact re-evaluation of near ties
   double dmarg32 = 2e-5;   // FP32 margin below which a worse-side verdict may flip
@@ -554,15 +553,43 @@ void certify_round(pp_handle* h, ppdev::RoundArgs& a, uint64_t t, int iter, int 
 
 constexpr int kSelCap = 1 << 16;    // near-tie candidates re-ranked per launch
 constexpr int kSelFirst = 512;      // copied back with the round result
+// Round block (device, one allocation; its head is copied back in ONE D2H):
+// [counters u32 x 16][exec u64 x 4 + pad][Rec x kMaxRestartsPerLaunch][selected indices int64 x kSelCap]
+constexpr size_t kExecOff = 64;
+constexpr size_t kRecOff = 128;
+constexpr size_t kSelOff =
+    (kRecOff + sizeof(ppdev::Rec) * ppdev::kMaxRestartsPerLaunch + 63) / 64 * 64;
+constexpr size_t kRoundBytes = kSelOff + sizeof(int64_t) * kSelCap;
 constexpr int kRefineGrid = 148 * 2;
 
-// PARAPLAN_TRACE=1: one stderr line per certification pass (diagnostics).
-bool trace_on() {
-  static const bool v = [] {
+// PARAPLAN_TRACE=1: one stderr line per certification pass; 2: also the
+// host-side phase times of every plan step (diagnostics).
+int trace_level() {
+  static const int v = [] {
     const char* e = std::getenv("PARAPLAN_TRACE");
-    return e != nullptr && std::atoi(e) != 0;
+    return e != nullptr ? std::atoi(e) : 0;
   }();
   return v;
+}
+bool trace_on() { return trace_level() > 0; }
+
+struct PhaseClock {
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  char buf[256];
+  int len = 0;
+  void mark(const char* what) {
+    if (trace_level() < 2) return;
+    const double us =
+        std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
+    len += std::snprintf(buf + len, sizeof(buf) - len, " %s=%.1f", what, us);
+  }
+  void flush() {
+    if (trace_level() >= 2) std::fprintf(stderr, "[paraplan] plan_step us:%s\n", buf);
+  }
+};
+PhaseClock* g_clock = nullptr;  // the plan step being traced (one driver thread per handle)
+void phase(const char* what) {
+  if (g_clock != nullptr) g_clock->mark(what);
 }
 
 // Windows up to this size are re-evaluated on the host pool (exact FP64
@@ -654,18 +681,14 @@ void run_round_launch(pp_handle* h, uint64_t t, int iter, int r0, int rc, const 
   const size_t n_recs = shape.refill ? static_cast<size_t>(rc) * a.grid : a.n_tiles;
   h->d_tiles.reserve(sizeof(ppdev::Rec) * n_recs, "tile records");
   a.tile_recs = static_cast<ppdev::Rec*>(h->d_tiles.p);
-  // result block: [exec u64 x 4][pad 8][Rec x rc]
-  const size_t rec_off = 40;
-  const size_t rbytes = rec_off + sizeof(ppdev::Rec) * rc;
-  if (h->d_result.reserve(std::max<size_t>(rbytes, 4096), "result block")) {
-    ck(cudaMemsetAsync(h->d_result.p, 0, std::max<size_t>(rbytes, 4096), h->stream),
-       "result block");
-  }
-  h->h_result.reserve(std::max<size_t>(rbytes, 4096), "pinned result");
-  char* dres = static_cast<char*>(h->d_result.p);
-  a.exec = reinterpret_cast<unsigned long long*>(dres);
-  a.out = reinterpret_cast<ppdev::Rec*>(dres + rec_off);
-  a.counters = static_cast<uint32_t*>(h->d_counters.p);
+  // the round block: counters, work counters, per-restart winners and the
+  // selected window, copied back together
+  char* dres = static_cast<char*>(h->d_round.p);
+  a.counters = reinterpret_cast<uint32_t*>(dres);
+  a.exec = reinterpret_cast<unsigned long long*>(dres + kExecOff);
+  a.out = reinterpret_cast<ppdev::Rec*>(dres + kRecOff);
+  const size_t rbytes = rerank ? kSelOff + sizeof(int64_t) * kSelFirst
+                               : kRecOff + sizeof(ppdev::Rec) * rc;
   if (per_sample != nullptr) {
     h->d_samples.reserve(sizeof(ppdev::SampleOut) * rc * static_cast<size_t>(count),
                          "per-sample buffer");
@@ -688,17 +711,14 @@ void run_round_launch(pp_handle* h, uint64_t t, int iter, int r0, int rc, const 
   }
   if (rerank) {
     h->d_skeys.reserve(total * sizeof(ppdev::SKey), "sample keys");
-    h->d_sel.reserve(kSelCap * (sizeof(int64_t) + sizeof(ppdev::SelRec)), "selection");
-    h->h_sel.reserve(kSelCap * std::max(sizeof(ppdev::SelRec), sizeof(int64_t)),
-                     "pinned selection");
+    h->d_sel.reserve(kSelCap * sizeof(ppdev::SelRec), "selection");
     a.skeys = static_cast<ppdev::SKey*>(h->d_skeys.p);
     a.sel_out = static_cast<ppdev::SelRec*>(h->d_sel.p);
-    a.sel_list = reinterpret_cast<int64_t*>(a.sel_out + kSelCap);
+    a.sel_list = reinterpret_cast<int64_t*>(dres + kSelOff);
     a.sel_cap = kSelCap;
     a.refine_grid = kRefineGrid;
     a.sel_rho = fp64 ? 1e-11 : h->sel_rho;
     a.sel_alpha = fp64 ? 1e-13 : 1e-6;
-    a.counters = static_cast<uint32_t*>(h->d_counters.p);
   }
 
   ck(cudaEventRecord(h->ev0, h->stream), "event");
@@ -706,9 +726,7 @@ void run_round_launch(pp_handle* h, uint64_t t, int iter, int r0, int rc, const 
                          : ppdev::launch_round_f32(h->kind, a, h->stream);
   ck(static_cast<cudaError_t>(lcode), "sampling kernel launch");
   if (rerank) {
-    ck(cudaMemsetAsync(reinterpret_cast<uint32_t*>(h->d_counters.p) + 2, 0, sizeof(uint32_t),
-                       h->stream),
-       "selection counter");
+    // the selection counter was re-armed by the rollout kernel's last CTA
     ck(static_cast<cudaError_t>(ppdev::launch_select(a, h->stream)), "window select launch");
     if (!h->pool) {
       const unsigned hc = std::thread::hardware_concurrency();
@@ -717,19 +735,12 @@ void run_round_launch(pp_handle* h, uint64_t t, int iter, int r0, int rc, const 
     h->pool->prewarm();  // workers spin while the GPU samples
   }
   ck(cudaEventRecord(h->ev1, h->stream), "event");
-  ck(cudaMemcpyAsync(h->h_result.p, h->d_result.p, rbytes, cudaMemcpyDeviceToHost, h->stream),
+  // one D2H: counters (selection count), work counters, winners and the
+  // first kSelFirst selected indices
+  ck(cudaMemcpyAsync(h->h_round.p, h->d_round.p, rbytes, cudaMemcpyDeviceToHost, h->stream),
      "result D2H");
+  phase("enqueued");
   uint32_t n_sel = 0;
-  if (rerank) {
-    ck(cudaMemcpyAsync(&h->h_selcount, reinterpret_cast<uint32_t*>(h->d_counters.p) + 2,
-                       sizeof(uint32_t), cudaMemcpyDeviceToHost, h->stream),
-       "selection D2H");
-    // the first kSelFirst selected indices ride along with the result
-    ck(cudaMemcpyAsync(h->h_sel.p, a.sel_list, sizeof(int64_t) * kSelFirst,
-                       cudaMemcpyDeviceToHost, h->stream),
-       "selection D2H");
-    h->timing.d2h_bytes += sizeof(int64_t) * kSelFirst + sizeof(uint32_t);
-  }
   h->timing.d2h_bytes += static_cast<int64_t>(rbytes);
   if (per_sample != nullptr) {
     const size_t sb = sizeof(ppdev::SampleOut) * rc * static_cast<size_t>(count);
@@ -738,16 +749,17 @@ void run_round_launch(pp_handle* h, uint64_t t, int iter, int r0, int rc, const 
     h->timing.d2h_bytes += static_cast<int64_t>(sb);
   }
   ck(cudaStreamSynchronize(h->stream), "sampling kernel");
+  phase("synced");
   float ms = 0.f;
   ck(cudaEventElapsedTime(&ms, h->ev0, h->ev1), "event timing");
   h->timing.kernel_ms += ms;
   h->timing.launches += (shape.refill ? 2 : 1) + (rerank ? 1 : 0);
   h->timing.samples += count * rc;
-  const unsigned long long* ex = static_cast<const unsigned long long*>(h->h_result.p);
+  const char* hres = static_cast<const char*>(h->h_round.p);
+  const unsigned long long* ex = reinterpret_cast<const unsigned long long*>(hres + kExecOff);
   h->timing.executed_steps += static_cast<int64_t>(ex[2]);
   h->timing.checked_states += static_cast<int64_t>(ex[3]);
-  const char* hres = static_cast<const char*>(h->h_result.p);
-  const ppdev::Rec* recs = reinterpret_cast<const ppdev::Rec*>(hres + rec_off);
+  const ppdev::Rec* recs = reinterpret_cast<const ppdev::Rec*>(hres + kRecOff);
   for (int r = 0; r < rc; ++r) {
     out[r].cls = recs[r].cls;
     out[r].candidate = recs[r].cand;
@@ -758,9 +770,10 @@ void run_round_launch(pp_handle* h, uint64_t t, int iter, int r0, int rc, const 
   }
   if (!rerank) return;
 
-  n_sel = h->h_selcount;
+  n_sel = reinterpret_cast<const uint32_t*>(hres)[2];
   const auto c_t0 = std::chrono::steady_clock::now();
   certify_round(h, a, t, iter, r0, rc, center, c0, c1, injected, out, fp64, n_sel);
+  phase("certified");
   h->timing.certify_ms +=
       std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - c_t0).count();
 }
@@ -832,19 +845,14 @@ void certify_round(pp_handle* h, ppdev::RoundArgs& a, uint64_t t, int iter, int 
                          cudaMemcpyHostToDevice, h->stream),
          "bounds H2D");
       a.sel_bound = static_cast<const ppdev::SelBound*>(h->d_bound.p);
-      ck(cudaMemsetAsync(reinterpret_cast<uint32_t*>(h->d_counters.p) + 2, 0, sizeof(uint32_t),
-                         h->stream),
-         "selection counter");
+      ck(cudaMemsetAsync(a.counters + 2, 0, sizeof(uint32_t), h->stream), "selection counter");
       ck(static_cast<cudaError_t>(ppdev::launch_select(a, h->stream)), "window select launch");
-      ck(cudaMemcpyAsync(&h->h_selcount, reinterpret_cast<uint32_t*>(h->d_counters.p) + 2,
-                         sizeof(uint32_t), cudaMemcpyDeviceToHost, h->stream),
-         "selection D2H");
-      ck(cudaMemcpyAsync(h->h_sel.p, a.sel_list, sizeof(int64_t) * kSelFirst,
+      ck(cudaMemcpyAsync(h->h_round.p, h->d_round.p, kSelOff + sizeof(int64_t) * kSelFirst,
                          cudaMemcpyDeviceToHost, h->stream),
          "selection D2H");
       ck(cudaStreamSynchronize(h->stream), "window select");
       h->timing.launches += 1;
-      n_sel = h->h_selcount;
+      n_sel = static_cast<const uint32_t*>(h->h_round.p)[2];
     }
     if (n_sel > static_cast<uint32_t>(kSelCap)) {
       if (trace_on()) {
@@ -854,11 +862,13 @@ void certify_round(pp_handle* h, ppdev::RoundArgs& a, uint64_t t, int iter, int 
       break;
     }
     if (n_sel > static_cast<uint32_t>(kSelFirst)) {
-      ck(cudaMemcpy(static_cast<int64_t*>(h->h_sel.p) + kSelFirst, a.sel_list + kSelFirst,
-                    sizeof(int64_t) * (n_sel - kSelFirst), cudaMemcpyDeviceToHost),
+      ck(cudaMemcpy(reinterpret_cast<int64_t*>(static_cast<char*>(h->h_round.p) + kSelOff) + kSelFirst,
+                    a.sel_list + kSelFirst, sizeof(int64_t) * (n_sel - kSelFirst),
+                    cudaMemcpyDeviceToHost),
          "selection D2H");
     }
-    const int64_t* sl = static_cast<const int64_t*>(h->h_sel.p);
+    const int64_t* sl =
+        reinterpret_cast<const int64_t*>(static_cast<const char*>(h->h_round.p) + kSelOff);
     list.clear();
     for (uint32_t i = 0; i < n_sel; ++i) {
       if (known.find(sl[i]) == known.end()) list.push_back(sl[i]);
@@ -876,8 +886,8 @@ void certify_round(pp_handle* h, ppdev::RoundArgs& a, uint64_t t, int iter, int 
                          cudaMemcpyHostToDevice, h->stream),
          "refine list H2D");
       const uint32_t n_list = static_cast<uint32_t>(list.size());
-      ck(cudaMemcpyAsync(reinterpret_cast<uint32_t*>(h->d_counters.p) + 2, &n_list,
-                         sizeof(uint32_t), cudaMemcpyHostToDevice, h->stream),
+      ck(cudaMemcpyAsync(a.counters + 2, &n_list, sizeof(uint32_t), cudaMemcpyHostToDevice,
+                         h->stream),
          "refine count H2D");
       a.field64 = ensure_field64(h);
       ck(static_cast<cudaError_t>(ppdev::launch_refine(h->kind, a, h->stream)), "refine launch");
@@ -1177,10 +1187,9 @@ pp_status pp_create(const pp_model* m, pp_handle** out) {
     ck(cudaStreamCreateWithFlags(&hp->stream, cudaStreamNonBlocking), "stream");
     ck(cudaEventCreate(&hp->ev0), "event");
     ck(cudaEventCreate(&hp->ev1), "event");
-    hp->d_counters.reserve(64, "counters");
-    ck(cudaMemsetAsync(hp->d_counters.p, 0, 64, hp->stream), "counters");
-    hp->d_result.reserve(4096, "result block");
-    ck(cudaMemsetAsync(hp->d_result.p, 0, 4096, hp->stream), "result block");
+    hp->d_round.reserve(kRoundBytes, "round block");
+    ck(cudaMemsetAsync(hp->d_round.p, 0, kRoundBytes, hp->stream), "round block");
+    hp->h_round.reserve(kRoundBytes, "pinned round block");
     ck(cudaStreamSynchronize(hp->stream), "init");
     h = hp.release();
   });
@@ -1195,12 +1204,12 @@ void pp_destroy(pp_handle* h) {
   if (h == nullptr) return;
   cudaSetDevice(h->device);
   if (h->stream != nullptr) cudaStreamSynchronize(h->stream);
-  for (DevBuf* b : {&h->d_field, &h->d_params, &h->d_result, &h->d_tiles, &h->d_counters,
+  for (DevBuf* b : {&h->d_field, &h->d_params, &h->d_round, &h->d_tiles,
                     &h->d_samples, &h->d_scratch, &h->d_injected, &h->d_theta, &h->d_skeys,
                     &h->d_sel, &h->d_bound, &h->d_field64}) {
     b->release();
   }
-  for (HostBuf* b : {&h->h_field, &h->h_params, &h->h_result, &h->h_sel, &h->h_bound,
+  for (HostBuf* b : {&h->h_field, &h->h_params, &h->h_round, &h->h_bound,
                      &h->h_field64}) {
     b->release();
   }
@@ -1372,6 +1381,7 @@ void plan_step_resident(pp_handle* h, uint64_t t, pp_plan_output* out) {
   }
 
   // FP64 epilogue (:339-350).
+  phase("merged");
   out->evaluated = evaluated;
   if (out->best_theta != nullptr) std::memcpy(out->best_theta, best_theta.data(), sizeof(double) * P);
   int32_t len = 0;
@@ -1406,8 +1416,14 @@ pp_status pp_plan_step(pp_handle* h, const pp_snapshot* snap, uint64_t t, pp_pla
     check_warm(h, snap->warm_theta_len);
     ck(cudaSetDevice(h->device), "cudaSetDevice");
     h->timing = pp_timing{};
+    PhaseClock clock;
+    g_clock = &clock;
     upload_snapshot(h, *snap);
+    phase("upload");
     plan_step_resident(h, t, out);
+    phase("done");
+    g_clock = nullptr;
+    clock.flush();
   });
 }
 
@@ -1429,8 +1445,14 @@ pp_status pp_plan_step_points(pp_handle* h, const pp_snapshot_points* snap, uint
     check_warm(h, snap->warm_theta_len);
     ck(cudaSetDevice(h->device), "cudaSetDevice");
     h->timing = pp_timing{};
+    PhaseClock clock;
+    g_clock = &clock;
     upload_points(h, *snap);
+    phase("upload");
     plan_step_resident(h, t, out);
+    phase("done");
+    g_clock = nullptr;
+    clock.flush();
   });
 }
 

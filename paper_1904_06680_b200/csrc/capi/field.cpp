@@ -33,12 +33,12 @@ double env_or(const char* name, double dflt) {
 // f(i) for i in [0, n), on up to 16 host threads when `work` is large.
 template <class F>
 void par_for(int n, size_t work, F&& f) {
-  const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
-  const unsigned T = std::min<unsigned>({16u, hw, static_cast<unsigned>(std::max(n, 1))});
-  if (work < (size_t(1) << 17) || T <= 1) {
+  if (work < (size_t(1) << 17) || n <= 1) {
     for (int i = 0; i < n; ++i) f(i);
     return;
   }
+  static const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+  const unsigned T = std::min<unsigned>({16u, hw, static_cast<unsigned>(n)});
   std::atomic<int> next{0};
   const auto body = [&] {
     for (int i; (i = next.fetch_add(1)) < n;) f(i);

@@ -734,6 +734,14 @@ __device__ __forceinline__ Key load_rec_cg(const Rec* src) {
   return Key{__ldcg(&src->cls), __ldcg(&src->cand), __ldcg(&src->k1), __ldcg(&src->k2)};
 }
 
+// Programmatic dependent launch: a kernel launched with programmatic stream
+// serialization may start while its predecessor drains; it waits here (the
+// predecessor has completed and its writes are visible) before reading what
+// the predecessor wrote. A no-op for an ordinary launch.
+__device__ __forceinline__ void wait_prior_grid() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
 // Field of the round, staged whole into shared memory when it fits
 // (a.field_smem_bytes > 0), else read through L1/L2. The staging is one TMA
 // bulk copy (cp.async.bulk, global -> shared) issued by thread 0 and
@@ -830,6 +838,7 @@ __device__ __forceinline__ void finish_round(const RoundArgs& a, const Rec* recs
     a.exec[3] = atomicExch(&a.exec[1], 0ull);
     a.counters[0] = 0;
     a.counters[1] = 0;
+    a.counters[2] = 0;  // the window selection that follows counts from zero
   }
 }
 
@@ -923,6 +932,7 @@ __global__ void __launch_bounds__(kBlock, refill_min_blocks<Real, Net>())
     (&table[0][0])[i] = empty_key();
   }
   const Field<Real> f = stage_field<Real>(a, smem_raw);
+  wait_prior_grid();  // the generator's theta records
 
   const int bpr = a.tiles_per_restart;  // 32-candidate batches per restart
   const unsigned total_batches = static_cast<unsigned>(a.n_tiles);
@@ -1125,6 +1135,7 @@ __global__ void __launch_bounds__(kBlock) lockstep_kernel(const RoundArgs a) {
 // key lies within (1 + rho) * cost + alpha of the round winner, plus every
 // candidate flagged marginal. Indices are appended to a.sel_list.
 static __global__ void __launch_bounds__(256) select_kernel(const RoundArgs a) {
+  wait_prior_grid();  // the rollout's keys and winners
   const int64_t total = a.count * a.restart_count;
   for (int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; s < total;
        s += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -1227,6 +1238,23 @@ bool refill_schedule() {
 
 using KernelFn = void (*)(const RoundArgs);
 
+// Launch with programmatic stream serialization when `pdl` (the kernel calls
+// wait_prior_grid() before reading its predecessor's output).
+inline cudaError_t launch_dependent(KernelFn k, int grid, int block, size_t smem, cudaStream_t st,
+                                    bool pdl, const RoundArgs& a) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(grid));
+  cfg.blockDim = dim3(static_cast<unsigned>(block));
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, k, a);
+}
+
 template <typename Real, class Net, int kGrid>
 KernelFn kernel_of_g() {
   if constexpr (Net::kP > 0) {
@@ -1258,16 +1286,18 @@ int launch_impl(const RoundArgs& a, void* stream) {
   if (smem > 32 * 1024) {
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   }
-  k<<<a.grid, a.block, smem, st>>>(a);
-  return static_cast<int>(cudaGetLastError());
+  // after the generator: dependent launch (the rollout CTAs stage the field
+  // while the generator drains, then wait for its records)
+  const bool after_generate = Net::kP > 0 && refill_schedule<Net>();
+  return static_cast<int>(launch_dependent(k, a.grid, a.block, smem, st, after_generate, a));
 }
 
-// Near-tie window of a finished round.
+// Near-tie window of a finished round (a dependent launch after the rollout).
 inline int launch_select_impl(const RoundArgs& a, void* stream) {
   const int64_t total = a.count * a.restart_count;
   const int blocks = static_cast<int>(std::min<int64_t>((total + 255) / 256, 148 * 16));
-  select_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(a);
-  return static_cast<int>(cudaGetLastError());
+  return static_cast<int>(
+      launch_dependent(select_kernel, blocks, 256, 0, static_cast<cudaStream_t>(stream), true, a));
 }
 
 // FP64 re-evaluation of the selected window.
