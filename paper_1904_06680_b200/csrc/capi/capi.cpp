@@ -257,6 +257,12 @@ struct pp_handle {
 
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  // a deferred field goes up on `side` while the generator runs on `stream`;
+  // the rollout waits on ev_field (the dependent launch of the rollout after
+  // the generator stays intact)
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_field = nullptr;
+  bool field_via_side = false, field_event = false;
   DevBuf d_field, d_params, d_round, d_tiles, d_samples, d_scratch, d_injected, d_theta, d_skeys,
       d_sel, d_bound;
   HostBuf h_field, h_params, h_round, h_bound;
@@ -273,6 +279,9 @@ struct pp_handle {
   // resident snapshot
   bool snap_valid = false;
   std::map<int64_t, ppdev::LaunchShape> shapes;  // occupancy per (smem, grid mode, precision)
+  // plan_step: the field of the snapshot is binned and uploaded while the
+  // theta generator runs (consumed by the first round of the step)
+  std::function<void()> pending_field;
   ppdev::RoundArgs base{};
   int field_smem_bytes = 0;
 
@@ -362,8 +371,13 @@ void finish_field(pp_handle* h, ppdev::RoundArgs& a) {
     h->h_field.reserve(l.bytes, "pinned field");
     h->d_field.reserve(l.bytes, "device field");
     ppfield::pack(b, h->fp64, h->h_field.p);
-    ck(cudaMemcpyAsync(h->d_field.p, h->h_field.p, l.bytes, cudaMemcpyHostToDevice, h->stream),
+    cudaStream_t st = h->field_via_side ? h->side : h->stream;
+    ck(cudaMemcpyAsync(h->d_field.p, h->h_field.p, l.bytes, cudaMemcpyHostToDevice, st),
        "field H2D");
+    if (h->field_via_side) {
+      ck(cudaEventRecord(h->ev_field, h->side), "field event");
+      h->field_event = true;
+    }
     h->timing.h2d_bytes += static_cast<int64_t>(l.bytes);
     a.field = h->d_field.p;
     if (h->fp64) {
@@ -400,10 +414,22 @@ const void* ensure_field64(pp_handle* h) {
 void set_round_constants(pp_handle* h, const pp_snapshot& s);
 void upload_field_rows(pp_handle* h, const pp_snapshot& s, ppdev::RoundArgs& a);
 
+// Host copy of the snapshot scalars (+ warm start) for the epilogue and the
+// certification; the field lives in h->field.
+void keep_snapshot(pp_handle* h, const pp_snapshot& s) {
+  h->snap_copy = s;
+  h->snap_copy.field_xy = nullptr;
+  h->snap_copy.field_H = h->cfg.H;
+  h->snap_warm.assign(s.warm_theta, s.warm_theta + std::max(0, s.warm_theta_len));
+  h->snap_copy.warm_theta = h->snap_warm.data();
+  h->snapshot = &h->snap_copy;
+  h->snap_valid = true;
+}
+
 // Snapshot with raw anchor-frame obstacle points: the field is the
 // reference's extrapolate(points, H, T_s) (src/geometry.cpp:43-61), built
 // straight into the binned static/dynamic form.
-void upload_points(pp_handle* h, const pp_snapshot_points& p) {
+void upload_points(pp_handle* h, const pp_snapshot_points& p, bool defer = false) {
   const auto& cfg = h->cfg;
   if (p.n_points < 0) throw std::invalid_argument("malformed obstacle points");
   if (p.n_points > 0 && p.points == nullptr) throw std::invalid_argument("null obstacle points");
@@ -425,20 +451,23 @@ void upload_points(pp_handle* h, const pp_snapshot_points& p) {
   s.warm_theta = p.warm_theta;
   s.warm_theta_len = p.warm_theta_len;
   set_round_constants(h, s);
-  ppdev::RoundArgs& a = h->base;
-  a.n_points = p.n_points;
-  const double cull = std::sqrt(a.r2) + 1e-3;
-  ppfield::from_points(h->field, p.points, p.n_points, cfg.H + 1, p.T_s, cull);
-  finish_field(h, a);
-  h->snap_copy = s;
-  h->snap_warm.assign(s.warm_theta, s.warm_theta + std::max(0, s.warm_theta_len));
-  h->snap_copy.warm_theta = h->snap_warm.data();
-  h->snapshot = &h->snap_copy;
-  h->snap_valid = true;
+  keep_snapshot(h, s);
+  auto field = [h, p] {
+    ppdev::RoundArgs& a = h->base;
+    a.n_points = p.n_points;
+    const double cull = std::sqrt(a.r2) + 1e-3;
+    ppfield::from_points(h->field, p.points, p.n_points, h->cfg.H + 1, p.T_s, cull);
+    finish_field(h, a);
+  };
+  if (defer) {
+    h->pending_field = field;
+  } else {
+    field();
+  }
 }
 
 // Goal transform and constants of a snapshot (src/planner.cpp:70-81).
-void upload_snapshot(pp_handle* h, const pp_snapshot& s) {
+void upload_snapshot(pp_handle* h, const pp_snapshot& s, bool defer = false) {
   const auto& cfg = h->cfg;
   if (s.n_points < 0 || s.field_H < 0) throw std::invalid_argument("malformed obstacle field");
   if (s.n_points > 0 && s.field_H < cfg.H) {
@@ -447,8 +476,12 @@ void upload_snapshot(pp_handle* h, const pp_snapshot& s) {
   }
   if (s.n_points > 0 && s.field_xy == nullptr) throw std::invalid_argument("null obstacle field");
   set_round_constants(h, s);
-  ppdev::RoundArgs& a = h->base;
-  upload_field_rows(h, s, a);
+  keep_snapshot(h, s);
+  if (defer) {
+    h->pending_field = [h, s] { upload_field_rows(h, s, h->base); };
+  } else {
+    upload_field_rows(h, s, h->base);
+  }
 }
 
 void set_round_constants(pp_handle* h, const pp_snapshot& s) {
@@ -493,7 +526,10 @@ void set_round_constants(pp_handle* h, const pp_snapshot& s) {
   a.n_params = h->P;
   a.n_layers = static_cast<int32_t>(h->sizes.size());
   for (size_t i = 0; i < h->sizes.size(); ++i) a.sizes[i] = h->sizes[i];
-
+  // the generator's start features need the constants before the field
+  a.dmarg32 = h->dmarg32;
+  fill_consts(a, &a.kf);
+  fill_consts(a, &a.kd);
 }
 
 void upload_field_rows(pp_handle* h, const pp_snapshot& s, ppdev::RoundArgs& a) {
@@ -511,14 +547,6 @@ void upload_field_rows(pp_handle* h, const pp_snapshot& s, ppdev::RoundArgs& a) 
     h->field.cull = cull;
   }
   finish_field(h, a);
-  // host copy of the reference snapshot (rows 0..H) for pp_rollout-style use
-  h->snap_copy = s;
-  h->snap_copy.field_xy = nullptr;
-  h->snap_copy.field_H = cfg.H;
-  h->snap_warm.assign(s.warm_theta, s.warm_theta + std::max(0, s.warm_theta_len));
-  h->snap_copy.warm_theta = h->snap_warm.data();
-  h->snapshot = &h->snap_copy;
-  h->snap_valid = true;
 }
 
 // key prefix fold^4(seed, t, restart, iter) (src/rng.cpp:26-34 minus the
@@ -602,6 +630,40 @@ int host_max() {
   return v;
 }
 
+// Occupancy of the rollout kernel for (precision, staged field size, grid
+// mode), queried once per handle.
+ppdev::LaunchShape launch_shape(pp_handle* h, bool fp64, int field_smem, int grid_mode) {
+  const int64_t key = (static_cast<int64_t>(field_smem) << 8) | (grid_mode << 1) | (fp64 ? 1 : 0);
+  auto found = h->shapes.find(key);
+  if (found == h->shapes.end()) {
+    ppdev::LaunchShape sh{};
+    const int rcode = fp64 ? ppdev::shape_f64(h->kind, h->device, field_smem, grid_mode, &sh)
+                           : ppdev::shape_f32(h->kind, h->device, field_smem, grid_mode, &sh);
+    ck(static_cast<cudaError_t>(rcode), "occupancy query");
+    found = h->shapes.emplace(key, sh).first;
+  }
+  return found->second;
+}
+
+void consume_pending_field(pp_handle* h, bool side = false) {
+  std::function<void()> f = std::move(h->pending_field);
+  h->pending_field = nullptr;
+  h->field_via_side = side;
+  h->field_event = false;
+  try {
+    f();
+  } catch (...) {
+    h->field_via_side = false;
+    throw;
+  }
+  h->field_via_side = false;
+  if (h->field_event) {
+    ck(cudaStreamWaitEvent(h->stream, h->ev_field, 0), "field wait");
+    h->field_event = false;
+  }
+  phase("field");
+}
+
 // One sampling round on the device: restarts [r0, r0+rc), candidates
 // [c0, c1) of each, iteration `iter`, centred on `center` (or injected theta).
 // With re-ranking on, the round is followed by the near-tie window select,
@@ -613,39 +675,20 @@ void run_round_launch(pp_handle* h, uint64_t t, int iter, int r0, int rc, const 
   const int64_t count = c1 - c0;
   const bool fp64 = h->fp64 || force_fp64;
   const bool rerank = h->rerank && h->snapshot != nullptr;
+  // the schedule (refill: generator + rollout) and the theta record width do
+  // not depend on the field
+  const ppdev::LaunchShape shape0 = launch_shape(h, fp64, 0, 0);
+  // a pending field is binned while the generator runs; without a generator
+  // (lockstep) or for an FP64 redo it is needed now
+  if (h->pending_field && (!shape0.refill || force_fp64)) consume_pending_field(h);
   ppdev::RoundArgs a = h->base;
   if (force_fp64 && !h->fp64) {
     a.field = ensure_field64(h);
     a.lay = a.lay64;
   }
-  const int field_smem = (force_fp64 && !h->fp64) ? 0 : h->field_smem_bytes;
-  const int grid2d = h->base.grid_mode;
-  // occupancy of the kernel for this (precision, staged field size, grid
-  // mode), queried once per handle
-  const int64_t skey = (static_cast<int64_t>(field_smem) << 8) | (grid2d << 1) | (fp64 ? 1 : 0);
-  auto found = h->shapes.find(skey);
-  if (found == h->shapes.end()) {
-    ppdev::LaunchShape sh{};
-    const int rcode = fp64 ? ppdev::shape_f64(h->kind, h->device, field_smem, grid2d, &sh)
-                           : ppdev::shape_f32(h->kind, h->device, field_smem, grid2d, &sh);
-    ck(static_cast<cudaError_t>(rcode), "occupancy query");
-    found = h->shapes.emplace(skey, sh).first;
-  }
-  const ppdev::LaunchShape shape = found->second;
-  // refill: 32-candidate batches; lockstep: one tile of `block` candidates
-  const int unit = shape.refill ? 32 : shape.block;
-  const int64_t tpr64 = (count + unit - 1) / unit;
-  if (tpr64 * rc > (int64_t{1} << 30)) throw std::invalid_argument("sampling round too large");
   a.restart_count = rc;
   a.cand_begin = c0;
   a.count = count;
-  a.tiles_per_restart = static_cast<int32_t>(tpr64);
-  a.n_tiles = static_cast<int32_t>(tpr64 * rc);
-  a.block = shape.block;
-  a.grid = std::max(1, std::min(shape.grid, shape.refill ? (a.n_tiles + ppdev_warps() - 1) /
-                                                               ppdev_warps()
-                                                         : a.n_tiles));
-  a.field_smem_bytes = field_smem;
   a.queue_bytes = 0;
 
   // params block: [prefix u64 x rc][center f64 x P]
@@ -678,9 +721,6 @@ void run_round_launch(pp_handle* h, uint64_t t, int iter, int r0, int rc, const 
     a.injected = static_cast<const double*>(h->d_injected.p);
   }
 
-  const size_t n_recs = shape.refill ? static_cast<size_t>(rc) * a.grid : a.n_tiles;
-  h->d_tiles.reserve(sizeof(ppdev::Rec) * n_recs, "tile records");
-  a.tile_recs = static_cast<ppdev::Rec*>(h->d_tiles.p);
   // the round block: counters, work counters, per-restart winners and the
   // selected window, copied back together
   char* dres = static_cast<char*>(h->d_round.p);
@@ -695,19 +735,11 @@ void run_round_launch(pp_handle* h, uint64_t t, int iter, int r0, int rc, const 
     a.per_sample = static_cast<ppdev::SampleOut*>(h->d_samples.p);
   }
   const size_t total = static_cast<size_t>(count) * rc;
-  if (shape.refill) {
+  if (shape0.refill) {
     const size_t esz = fp64 ? sizeof(double) : sizeof(float);
-    h->d_theta.reserve(total * shape.theta_elem * esz, "theta buffer");
+    h->d_theta.reserve(total * shape0.theta_elem * esz, "theta buffer");
     a.theta_buf = h->d_theta.p;  // [total][theta_elem]: theta, first action, pad
     a.first_buf = nullptr;
-  }
-  const bool generic = h->kind == ppdev::NetKind::kGeneric;
-  if (generic || rerank) {
-    const size_t lanes = std::max<size_t>(generic ? static_cast<size_t>(a.grid) * a.block : 0,
-                                          rerank ? kRefineGrid * 128 : 0);
-    h->d_scratch.reserve(lanes * h->P * sizeof(double), "theta scratch");
-    a.theta_scratch = static_cast<float*>(h->d_scratch.p);
-    a.theta_scratch64 = static_cast<double*>(h->d_scratch.p);
   }
   if (rerank) {
     h->d_skeys.reserve(total * sizeof(ppdev::SKey), "sample keys");
@@ -722,9 +754,55 @@ void run_round_launch(pp_handle* h, uint64_t t, int iter, int r0, int rc, const 
   }
 
   ck(cudaEventRecord(h->ev0, h->stream), "event");
-  const int lcode = fp64 ? ppdev::launch_round_f64(h->kind, a, h->stream)
-                         : ppdev::launch_round_f32(h->kind, a, h->stream);
-  ck(static_cast<cudaError_t>(lcode), "sampling kernel launch");
+  ck(static_cast<cudaError_t>(fp64 ? ppdev::launch_generate_f64(h->kind, a, h->stream)
+                                   : ppdev::launch_generate_f32(h->kind, a, h->stream)),
+     "theta generator launch");
+  if (h->pending_field) {  // bin + upload the field while the generator runs
+    consume_pending_field(h, true);
+    const ppdev::RoundArgs& b = h->base;
+    a.field = b.field;
+    a.field64 = b.field64;
+    a.n_points = b.n_points;
+    a.field_ns = b.field_ns;
+    a.field_nd = b.field_nd;
+    a.grid_nx = b.grid_nx;
+    a.grid_ny = b.grid_ny;
+    a.grid_mode = b.grid_mode;
+    a.grid_x0 = b.grid_x0;
+    a.grid_y0 = b.grid_y0;
+    a.grid_g = b.grid_g;
+    a.lay = b.lay;
+    a.lay64 = b.lay64;
+    a.kf = b.kf;
+    a.kd = b.kd;
+  }
+  const int field_smem = (force_fp64 && !h->fp64) ? 0 : h->field_smem_bytes;
+  const ppdev::LaunchShape shape = launch_shape(h, fp64, field_smem, a.grid_mode);
+  // refill: 32-candidate batches; lockstep: one tile of `block` candidates
+  const int unit = shape.refill ? 32 : shape.block;
+  const int64_t tpr64 = (count + unit - 1) / unit;
+  if (tpr64 * rc > (int64_t{1} << 30)) throw std::invalid_argument("sampling round too large");
+  a.tiles_per_restart = static_cast<int32_t>(tpr64);
+  a.n_tiles = static_cast<int32_t>(tpr64 * rc);
+  a.block = shape.block;
+  a.grid = std::max(1, std::min(shape.grid, shape.refill ? (a.n_tiles + ppdev_warps() - 1) /
+                                                               ppdev_warps()
+                                                         : a.n_tiles));
+  a.field_smem_bytes = field_smem;
+  const size_t n_recs = shape.refill ? static_cast<size_t>(rc) * a.grid : a.n_tiles;
+  h->d_tiles.reserve(sizeof(ppdev::Rec) * n_recs, "tile records");
+  a.tile_recs = static_cast<ppdev::Rec*>(h->d_tiles.p);
+  const bool generic = h->kind == ppdev::NetKind::kGeneric;
+  if (generic || rerank) {
+    const size_t lanes = std::max<size_t>(generic ? static_cast<size_t>(a.grid) * a.block : 0,
+                                          rerank ? kRefineGrid * 128 : 0);
+    h->d_scratch.reserve(lanes * h->P * sizeof(double), "theta scratch");
+    a.theta_scratch = static_cast<float*>(h->d_scratch.p);
+    a.theta_scratch64 = static_cast<double*>(h->d_scratch.p);
+  }
+  ck(static_cast<cudaError_t>(fp64 ? ppdev::launch_rollout_f64(h->kind, a, h->stream)
+                                   : ppdev::launch_rollout_f32(h->kind, a, h->stream)),
+     "sampling kernel launch");
   if (rerank) {
     // the selection counter was re-armed by the rollout kernel's last CTA
     ck(static_cast<cudaError_t>(ppdev::launch_select(a, h->stream)), "window select launch");
@@ -1187,6 +1265,8 @@ pp_status pp_create(const pp_model* m, pp_handle** out) {
     ck(cudaStreamCreateWithFlags(&hp->stream, cudaStreamNonBlocking), "stream");
     ck(cudaEventCreate(&hp->ev0), "event");
     ck(cudaEventCreate(&hp->ev1), "event");
+    ck(cudaStreamCreateWithFlags(&hp->side, cudaStreamNonBlocking), "stream");
+    ck(cudaEventCreateWithFlags(&hp->ev_field, cudaEventDisableTiming), "event");
     hp->d_round.reserve(kRoundBytes, "round block");
     ck(cudaMemsetAsync(hp->d_round.p, 0, kRoundBytes, hp->stream), "round block");
     hp->h_round.reserve(kRoundBytes, "pinned round block");
@@ -1213,6 +1293,9 @@ void pp_destroy(pp_handle* h) {
                      &h->h_field64}) {
     b->release();
   }
+  if (h->side != nullptr) cudaStreamSynchronize(h->side);
+  if (h->ev_field != nullptr) cudaEventDestroy(h->ev_field);
+  if (h->side != nullptr) cudaStreamDestroy(h->side);
   if (h->ev0 != nullptr) cudaEventDestroy(h->ev0);
   if (h->ev1 != nullptr) cudaEventDestroy(h->ev1);
   if (h->stream != nullptr) cudaStreamDestroy(h->stream);
@@ -1398,6 +1481,17 @@ void plan_step_resident(pp_handle* h, uint64_t t, pp_plan_output* out) {
   out->winner = win;
 }
 
+// A deferred field never outlives its plan step (its source is the caller's
+// snapshot), nor does the phase clock.
+struct PendingGuard {
+  pp_handle* h;
+  explicit PendingGuard(pp_handle* hh) : h(hh) {}
+  ~PendingGuard() {
+    h->pending_field = nullptr;
+    g_clock = nullptr;
+  }
+};
+
 void check_warm(const pp_handle* h, int32_t len) {
   if (len != 0 && len != h->P) {
     throw std::invalid_argument("warm start vector size mismatch");  // :240-244
@@ -1418,7 +1512,8 @@ pp_status pp_plan_step(pp_handle* h, const pp_snapshot* snap, uint64_t t, pp_pla
     h->timing = pp_timing{};
     PhaseClock clock;
     g_clock = &clock;
-    upload_snapshot(h, *snap);
+    PendingGuard pending(h);
+    upload_snapshot(h, *snap, true);  // field binned while the generator runs
     phase("upload");
     plan_step_resident(h, t, out);
     phase("done");
@@ -1447,7 +1542,8 @@ pp_status pp_plan_step_points(pp_handle* h, const pp_snapshot_points* snap, uint
     h->timing = pp_timing{};
     PhaseClock clock;
     g_clock = &clock;
-    upload_points(h, *snap);
+    PendingGuard pending(h);
+    upload_points(h, *snap, true);  // field binned while the generator runs
     phase("upload");
     plan_step_resident(h, t, out);
     phase("done");

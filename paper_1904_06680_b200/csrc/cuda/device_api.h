@@ -158,9 +158,13 @@ struct LaunchShape {
 int shape_f32(NetKind k, int device, int field_bytes, int grid, LaunchShape* out);
 int shape_f64(NetKind k, int device, int field_bytes, int grid, LaunchShape* out);
 
-// Enqueue one sampling round on `stream`. Returns 0 or a cudaError_t.
-int launch_round_f32(NetKind k, const RoundArgs& a, void* stream);
-int launch_round_f64(NetKind k, const RoundArgs& a, void* stream);
+// Enqueue one sampling round on `stream` in two stages: the theta generator
+// (needs no field), then the rollout (needs the field). Returns 0 or a
+// cudaError_t.
+int launch_generate_f32(NetKind k, const RoundArgs& a, void* stream);
+int launch_generate_f64(NetKind k, const RoundArgs& a, void* stream);
+int launch_rollout_f32(NetKind k, const RoundArgs& a, void* stream);
+int launch_rollout_f64(NetKind k, const RoundArgs& a, void* stream);
 
 // Near-tie window after a round: counters[2] receives the number of selected
 // candidates, sel_list their flat indices.

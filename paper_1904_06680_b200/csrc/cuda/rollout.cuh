@@ -1271,24 +1271,34 @@ KernelFn kernel_of(int mode) {
                    : (mode == 1 ? kernel_of_g<Real, Net, 1>() : kernel_of_g<Real, Net, 0>());
 }
 
+// Stage 1 of a round: the theta generator (refill schedule only; a no-op
+// for the lockstep schedule, which draws theta itself).
 template <typename Real, class Net>
-int launch_impl(const RoundArgs& a, void* stream) {
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
+int launch_generate_impl(const RoundArgs& a, void* stream) {
   if constexpr (Net::kP > 0) {
     if (refill_schedule<Net>()) {
       const int64_t total = a.count * a.restart_count;
       const int gen_blocks = static_cast<int>((total + 255) / 256);
-      generate_kernel<Real, Net::kH1><<<gen_blocks, 256, 0, st>>>(a);
+      generate_kernel<Real, Net::kH1><<<gen_blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(a);
+      return static_cast<int>(cudaGetLastError());
     }
   }
+  return 0;
+}
+
+// Stage 2: the rollout. After the generator it is a dependent launch (the
+// rollout CTAs stage the field while the generator drains, then wait for its
+// records).
+template <typename Real, class Net>
+int launch_rollout_impl(const RoundArgs& a, void* stream) {
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
   auto k = kernel_of<Real, Net>(a.grid_mode);
   const size_t smem = static_cast<size_t>(a.field_smem_bytes);
   if (smem > 32 * 1024) {
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   }
-  // after the generator: dependent launch (the rollout CTAs stage the field
-  // while the generator drains, then wait for its records)
-  const bool after_generate = Net::kP > 0 && refill_schedule<Net>();
+  bool after_generate = false;
+  if constexpr (Net::kP > 0) after_generate = refill_schedule<Net>();
   return static_cast<int>(launch_dependent(k, a.grid, a.block, smem, st, after_generate, a));
 }
 

@@ -14,14 +14,25 @@ int shape_f32(NetKind k, int device, int smem_bytes, int grid, LaunchShape* out)
   }
 }
 
-int launch_round_f32(NetKind k, const RoundArgs& a, void* stream) {
+int launch_generate_f32(NetKind k, const RoundArgs& a, void* stream) {
   switch (k) {
     case NetKind::k5_2_2:
-      return launch_impl<float, NetReg<float, 2>>(a, stream);
+      return launch_generate_impl<float, NetReg<float, 2>>(a, stream);
     case NetKind::k5_10_2:
-      return launch_impl<float, NetReg<float, 10>>(a, stream);
+      return launch_generate_impl<float, NetReg<float, 10>>(a, stream);
     default:
-      return launch_impl<float, NetGlobal<float>>(a, stream);
+      return launch_generate_impl<float, NetGlobal<float>>(a, stream);
+  }
+}
+
+int launch_rollout_f32(NetKind k, const RoundArgs& a, void* stream) {
+  switch (k) {
+    case NetKind::k5_2_2:
+      return launch_rollout_impl<float, NetReg<float, 2>>(a, stream);
+    case NetKind::k5_10_2:
+      return launch_rollout_impl<float, NetReg<float, 10>>(a, stream);
+    default:
+      return launch_rollout_impl<float, NetGlobal<float>>(a, stream);
   }
 }
 
