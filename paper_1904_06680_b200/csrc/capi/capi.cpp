@@ -742,9 +742,10 @@ void run_round_launch(pp_handle* h, uint64_t t, int iter, int r0, int rc, const 
     a.first_buf = nullptr;
   }
   if (rerank) {
-    h->d_skeys.reserve(total * sizeof(ppdev::SKey), "sample keys");
+    h->d_skeys.reserve(total * (fp64 ? sizeof(ppdev::SKey) : sizeof(ppdev::SKey32)), "sample keys");
     h->d_sel.reserve(kSelCap * sizeof(ppdev::SelRec), "selection");
-    a.skeys = static_cast<ppdev::SKey*>(h->d_skeys.p);
+    a.skeys = h->d_skeys.p;
+    a.skey32 = fp64 ? 0 : 1;
     a.sel_out = static_cast<ppdev::SelRec*>(h->d_sel.p);
     a.sel_list = reinterpret_cast<int64_t*>(dres + kSelOff);
     a.sel_cap = kSelCap;

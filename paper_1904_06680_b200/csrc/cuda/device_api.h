@@ -16,11 +16,16 @@ struct SampleOut {
   double path_length, terminal_cost, first_a0, first_a1;
 };
 
-// Compact per-sample key for the near-tie window (16 bytes).
+// Compact per-sample key for the near-tie window: 16 bytes for FP64 rounds,
+// 8 bytes (SKey32) for FP32 rounds, whose costs are floats anyway.
 struct SKey {
   double cost;    // terminal cost (cls 0/1) or path length (cls 2)
   uint32_t meta;  // cls | marginal << 2 | t_goal << 8
   uint32_t pad;
+};
+struct SKey32 {
+  float cost;
+  uint32_t meta;
 };
 
 // Window of one restart for a widened select pass: class, t_goal (class 2)
@@ -130,7 +135,9 @@ struct RoundArgs {
   void* theta_buf;             // refill schedule: [P][total] theta in Real
   void* first_buf;             // refill schedule: [2][total] first action in Real
   // near-tie re-ranking (null skeys = off)
-  SKey* skeys;                 // [restart_count * count]
+  void* skeys;                 // [restart_count * count] SKey (FP64) or SKey32 (FP32)
+  int32_t skey32;              // skeys holds SKey32
+  int32_t _pad_skey;
   const void* field64;         // FP64 image of the field (same layout as `field`)
   int64_t* sel_list;           // [sel_cap] selected flat indices
   SelRec* sel_out;             // [sel_cap] their FP64 keys

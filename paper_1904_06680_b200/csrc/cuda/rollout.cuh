@@ -790,12 +790,13 @@ template <typename Real>
 __device__ __forceinline__ void write_skey(const RoundArgs& a, int64_t slot, int cls,
                                            const Lane<Real>& L, Real term) {
   if (a.skeys == nullptr) return;
-  SKey k;
-  k.cost = static_cast<double>(cls == 2 ? L.path : term);
-  k.meta = static_cast<uint32_t>(cls) | (L.marg ? 4u : 0u) |
-           (static_cast<uint32_t>(cls == 2 ? L.h : 0) << 8);
-  k.pad = 0;
-  a.skeys[slot] = k;
+  const uint32_t meta = static_cast<uint32_t>(cls) | (L.marg ? 4u : 0u) |
+                        (static_cast<uint32_t>(cls == 2 ? L.h : 0) << 8);
+  if constexpr (sizeof(Real) == sizeof(float)) {
+    static_cast<SKey32*>(a.skeys)[slot] = SKey32{cls == 2 ? L.path : term, meta};
+  } else {
+    static_cast<SKey*>(a.skeys)[slot] = SKey{cls == 2 ? L.path : term, meta, 0u};
+  }
 }
 
 // Per-sample debug/parity record.
@@ -1149,7 +1150,14 @@ static __global__ void __launch_bounds__(256) select_kernel(const RoundArgs a) {
       bd.t_goal = b.cls == 2 ? static_cast<int>(-b.k1) : 0;
       bd.thr = (b.cls == 2 ? -b.k2 : -b.k1) * (1.0 + a.sel_rho) + a.sel_alpha;
     }
-    const SKey k = a.skeys[s];
+    SKey k;
+    if (a.skey32) {
+      const SKey32 k32 = static_cast<const SKey32*>(a.skeys)[s];
+      k.cost = static_cast<double>(k32.cost);
+      k.meta = k32.meta;
+    } else {
+      k = static_cast<const SKey*>(a.skeys)[s];
+    }
     const int cls = static_cast<int>(k.meta & 3u);
     bool take = (k.meta & 4u) != 0u && bd.cls >= 0;
     if (cls == bd.cls && k.cost <= bd.thr) {
