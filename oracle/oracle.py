@@ -84,6 +84,10 @@ class Ref(_Base):
                                                   C.c_int32, C.c_double, C.c_uint64,
                                                   C.c_int32, C.POINTER(C.c_double), C.c_int32,
                                                   C.POINTER(C.c_double)]
+            L.ref_run_sweep_builtin.argtypes = [C.c_char_p, C.c_int32, C.c_int32, C.c_int32,
+                                                C.c_double, C.POINTER(C.c_uint64), C.c_int32,
+                                                C.c_int32, C.c_char_p]
+            L.ref_serialize_builtin.argtypes = [C.c_char_p, C.c_char_p, C.c_int32]
             cls._lib = L
         return cls._lib
 

@@ -335,4 +335,36 @@ int ref_run_mission_builtin(const char* name, int32_t H, int32_t n_candidates,
   return count;
 }
 
+// The reference's serialize_scenario of a builtin scenario into buf (the
+// length is returned; -1 on error).
+int ref_serialize_builtin(const char* name, char* buf, int32_t cap) {
+  int n = -1;
+  guarded([&] {
+    const std::string text = serialize_scenario(builtin_scenario(name));
+    n = static_cast<int>(text.size());
+    if (n < cap) std::memcpy(buf, text.data(), text.size() + 1);
+  });
+  return n;
+}
+
+// The reference's run_sweep on a builtin scenario with a reduced budget:
+// every output file (scenario JSON, report JSON, per-seed CSV and xy) is
+// written to out_dir exactly as the reference writes it.
+int ref_run_sweep_builtin(const char* name, int32_t H, int32_t n_candidates, int32_t n_restarts,
+                          double time_limit, const uint64_t* seeds, int32_t n_seeds,
+                          int32_t threads, const char* out_dir) {
+  int ok = -1;
+  guarded([&] {
+    ScenarioSpec spec = builtin_scenario(name);
+    spec.planner.H = H;
+    spec.planner.n_candidates = n_candidates;
+    spec.planner.n_restarts = n_restarts;
+    if (time_limit >= 0) spec.mission.time_limit = time_limit;
+    spec.seeds.assign(seeds, seeds + n_seeds);
+    run_sweep(spec, out_dir, threads);
+    ok = 0;
+  });
+  return ok;
+}
+
 }  // extern "C"

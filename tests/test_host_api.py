@@ -190,6 +190,18 @@ def test_builtin_scenarios(pp, tmp_path):  # test_smoke.py, scenario_test.cpp
         assert pp.serialize_scenario(back) == pp.serialize_scenario(spec)
 
 
+def test_serialized_scenarios_match_reference_text(pp):
+    """serialize_scenario (scenario.cpp:204-266) writes the reference's text,
+    provenance comments included, for every builtin scenario."""
+    import ctypes as C
+    from oracle.oracle import Ref
+    for n in pp.builtin_scenario_names():
+        buf = C.create_string_buffer(1 << 20)
+        size = Ref.lib().ref_serialize_builtin(n.encode(), buf, len(buf))
+        assert 0 < size < len(buf)
+        assert pp.serialize_scenario(pp.builtin_scenario(n)) == buf.value.decode(), n
+
+
 def test_no_gpu_fails_loudly(pp):
     """Without a device the planner must refuse, never fall back to the CPU."""
     from conftest import has_gpu
