@@ -264,8 +264,8 @@ struct pp_handle {
   cudaEvent_t ev_field = nullptr;
   bool field_via_side = false, field_event = false;
   DevBuf d_field, d_params, d_round, d_tiles, d_samples, d_scratch, d_injected, d_theta, d_skeys,
-      d_sel, d_bound;
-  HostBuf h_field, h_params, h_round, h_bound;
+      d_sel, d_bound, d_movers, d_bin;
+  HostBuf h_field, h_params, h_round, h_bound, h_movers;
 
   // near-tie re-ranking (PlannerConfig::refine): needs the host snapshot
   bool rerank = true;
@@ -370,15 +370,55 @@ void finish_field(pp_handle* h, ppdev::RoundArgs& a) {
   if (b.points() > 0) {
     h->h_field.reserve(l.bytes, "pinned field");
     h->d_field.reserve(l.bytes, "device field");
-    ppfield::pack(b, h->fp64, h->h_field.p);
     cudaStream_t st = h->field_via_side ? h->side : h->stream;
-    ck(cudaMemcpyAsync(h->d_field.p, h->h_field.p, l.bytes, cudaMemcpyHostToDevice, st),
-       "field H2D");
+    if (b.dyn_deferred) {
+      // the device bins the movers itself: upload the static parts and the
+      // raw movers only (csrc/cuda/binning_f64.cu)
+      ppfield::pack(b, h->fp64, h->h_field.p, false);
+      unsigned char* hf = static_cast<unsigned char*>(h->h_field.p);
+      unsigned char* df = static_cast<unsigned char*>(h->d_field.p);
+      const auto part = [&](size_t lo, size_t hi) {
+        if (hi > lo) {
+          ck(cudaMemcpyAsync(df + lo, hf + lo, hi - lo, cudaMemcpyHostToDevice, st), "field H2D");
+          h->timing.h2d_bytes += static_cast<int64_t>(hi - lo);
+        }
+      };
+      part(0, l.dpts);       // static points
+      part(l.sst, l.dst);    // static starts
+      part(l.sbox, l.bytes); // static cell boxes
+      const size_t mb = sizeof(double) * b.dbase.size();
+      h->h_movers.reserve(mb, "pinned movers");
+      h->d_movers.reserve(mb, "device movers");
+      std::memcpy(h->h_movers.p, b.dbase.data(), mb);
+      ck(cudaMemcpyAsync(h->d_movers.p, h->h_movers.p, mb, cudaMemcpyHostToDevice, st),
+         "movers H2D");
+      h->timing.h2d_bytes += static_cast<int64_t>(mb);
+      h->d_bin.reserve(sizeof(int32_t) * static_cast<size_t>(b.rows) * b.cells(), "bin cursors");
+      ppdev::BinArgs ba{};
+      ba.movers = static_cast<const double*>(h->d_movers.p);
+      ba.Nd = b.Nd;
+      ba.rows = b.rows;
+      ba.nx = b.nx;
+      ba.ny = b.ny;
+      ba.x0 = b.x0;
+      ba.y0 = b.y0;
+      ba.inv_g = 1.0 / b.g;
+      ba.dpts = df + l.dpts;
+      ba.dst = reinterpret_cast<int32_t*>(df + l.dst);
+      ba.cursor = static_cast<int32_t*>(h->d_bin.p);
+      ba.fp64 = h->fp64 ? 1 : 0;
+      ck(static_cast<cudaError_t>(ppdev::bin_movers(ba, st)), "mover binning");
+      h->timing.launches += 3;
+    } else {
+      ppfield::pack(b, h->fp64, h->h_field.p);
+      ck(cudaMemcpyAsync(h->d_field.p, h->h_field.p, l.bytes, cudaMemcpyHostToDevice, st),
+         "field H2D");
+      h->timing.h2d_bytes += static_cast<int64_t>(l.bytes);
+    }
     if (h->field_via_side) {
       ck(cudaEventRecord(h->ev_field, h->side), "field event");
       h->field_event = true;
     }
-    h->timing.h2d_bytes += static_cast<int64_t>(l.bytes);
     a.field = h->d_field.p;
     if (h->fp64) {
       a.field64 = h->d_field.p;
@@ -397,6 +437,7 @@ void finish_field(pp_handle* h, ppdev::RoundArgs& a) {
 // the FP64 fallback).
 const void* ensure_field64(pp_handle* h) {
   if (h->field.points() == 0) return nullptr;
+  ppfield::bin_dynamic(h->field);
   if (!h->field64_ready) {
     const ppfield::Layout l64 = ppfield::layout(h->field, sizeof(double));
     h->h_field64.reserve(l64.bytes, "pinned field64");
@@ -413,6 +454,16 @@ const void* ensure_field64(pp_handle* h) {
 
 void set_round_constants(pp_handle* h, const pp_snapshot& s);
 void upload_field_rows(pp_handle* h, const pp_snapshot& s, ppdev::RoundArgs& a);
+
+// Mover sets of at least this many positions (rows x movers) are binned on
+// the device in a plan step.
+int64_t device_bin_min() {
+  static const int64_t v = [] {
+    const char* e = std::getenv("PARAPLAN_DEVICE_BIN_MIN");
+    return e != nullptr ? std::atoll(e) : int64_t{1} << 16;
+  }();
+  return v;
+}
 
 // Host copy of the snapshot scalars (+ warm start) for the epilogue and the
 // certification; the field lives in h->field.
@@ -452,11 +503,17 @@ void upload_points(pp_handle* h, const pp_snapshot_points& p, bool defer = false
   s.warm_theta_len = p.warm_theta_len;
   set_round_constants(h, s);
   keep_snapshot(h, s);
-  auto field = [h, p] {
+  // In a plan step the device bins large mover sets itself and the host
+  // bins its exact FP64 image while the round runs.
+  auto field = [h, p, defer] {
     ppdev::RoundArgs& a = h->base;
     a.n_points = p.n_points;
     const double cull = std::sqrt(a.r2) + 1e-3;
-    ppfield::from_points(h->field, p.points, p.n_points, h->cfg.H + 1, p.T_s, cull);
+    ppfield::from_points(h->field, p.points, p.n_points, h->cfg.H + 1, p.T_s, cull, defer);
+    if (h->field.dyn_deferred &&
+        static_cast<int64_t>(h->field.Nd) * h->field.rows < device_bin_min()) {
+      ppfield::bin_dynamic(h->field);  // small: the host bins it at once
+    }
     finish_field(h, a);
   };
   if (defer) {
@@ -819,6 +876,11 @@ void run_round_launch(pp_handle* h, uint64_t t, int iter, int r0, int rc, const 
   ck(cudaMemcpyAsync(h->h_round.p, h->d_round.p, rbytes, cudaMemcpyDeviceToHost, h->stream),
      "result D2H");
   phase("enqueued");
+  // the host's exact image of device-binned movers, while the round runs
+  if (h->field.dyn_deferred) {
+    ppfield::bin_dynamic(h->field);
+    phase("host-binned");
+  }
   uint32_t n_sel = 0;
   h->timing.d2h_bytes += static_cast<int64_t>(rbytes);
   if (per_sample != nullptr) {
@@ -1085,6 +1147,9 @@ void host_rollout(const pp_handle* h, const pp_snapshot& s, const double* theta,
   const double gc = std::cos(goal.phi), gs = std::sin(goal.phi);
   const std::span<const double> th(theta, h->P);
   const int N = s.n_points;
+  if (s.field_xy == nullptr && h->field.dyn_deferred) {
+    throw std::logic_error("obstacle field used before its moving points were binned");
+  }
   if (N > 0 && s.field_xy != nullptr && s.field_H < cfg.H) {
     throw std::invalid_argument("obstacle field shorter than the planning horizon");
   }
@@ -1285,12 +1350,12 @@ void pp_destroy(pp_handle* h) {
   if (h == nullptr) return;
   cudaSetDevice(h->device);
   if (h->stream != nullptr) cudaStreamSynchronize(h->stream);
-  for (DevBuf* b : {&h->d_field, &h->d_params, &h->d_round, &h->d_tiles,
+  for (DevBuf* b : {&h->d_field, &h->d_params, &h->d_round, &h->d_tiles, &h->d_movers, &h->d_bin,
                     &h->d_samples, &h->d_scratch, &h->d_injected, &h->d_theta, &h->d_skeys,
                     &h->d_sel, &h->d_bound, &h->d_field64}) {
     b->release();
   }
-  for (HostBuf* b : {&h->h_field, &h->h_params, &h->h_round, &h->h_bound,
+  for (HostBuf* b : {&h->h_field, &h->h_params, &h->h_round, &h->h_bound, &h->h_movers,
                      &h->h_field64}) {
     b->release();
   }

@@ -166,10 +166,8 @@ void cell_boxes(Binned& b) {
   b.boxes = area < max_area * occupied * b.g * b.g;
 }
 
-// Grid + static bins + dynamic rows: row(r, xy) writes the Nd positions of
-// dynamic row r.
-template <class Row>
-void finish(Binned& b, const std::vector<double>& s_xy, const BBox& box, Row&& row) {
+// Grid + static bins (+ boxes).
+void finish_static(Binned& b, const std::vector<double>& s_xy, const BBox& box) {
   choose_grid(b, box);
   const int cells = b.cells();
   std::vector<int32_t> cell;
@@ -177,6 +175,12 @@ void finish(Binned& b, const std::vector<double>& s_xy, const BBox& box, Row&& r
   b.sst.assign(cells + 1, 0);
   if (b.Ns > 0) bin(b, s_xy.data(), b.Ns, b.spts.data(), b.sst.data(), cell);
   cell_boxes(b);
+}
+
+// Dynamic rows: row(r, xy) writes the Nd positions of dynamic row r.
+template <class Row>
+void finish_dynamic(Binned& b, Row&& row) {
+  const int cells = b.cells();
   b.dpts.resize(2 * static_cast<size_t>(b.Nd) * b.rows);
   b.dst.assign(static_cast<size_t>(b.rows) * (cells + 1), 0);
   if (b.Nd > 0) {
@@ -192,12 +196,30 @@ void finish(Binned& b, const std::vector<double>& s_xy, const BBox& box, Row&& r
   }
 }
 
+template <class Row>
+void finish(Binned& b, const std::vector<double>& s_xy, const BBox& box, Row&& row) {
+  finish_static(b, s_xy, box);
+  finish_dynamic(b, row);
+}
+
+// src/geometry.cpp:53-57: row r of the movers, x + h * step (int h promoted
+// to double).
+void mover_row(const Binned& b, int r, double* out) {
+  const double* q = b.dbase.data();
+  for (int k = 0; k < b.Nd; ++k) {
+    out[2 * k] = q[4 * k] + r * q[4 * k + 2];
+    out[2 * k + 1] = q[4 * k + 1] + r * q[4 * k + 3];
+  }
+}
+
 // Scalars back to their defaults; the vectors keep their storage, so a
 // planner re-binning a field of the same shape every tick neither allocates
 // nor faults pages in.
 void reset(Binned& b, int rows, double cull) {
   b.Ns = b.Nd = 0;
   b.boxes = false;
+  b.dyn_deferred = false;
+  b.dbase.clear();
   b.nx = b.ny = 1;
   b.x0 = b.y0 = 0.0;
   b.g = 1.0;
@@ -262,49 +284,80 @@ void from_rows(Binned& b, const double* xy, int rows, int N, double cull) {
   });
 }
 
-void from_points(Binned& b, const double* pts4, int N, int rows, double T_s, double cull) {
+void from_points(Binned& b, const double* pts4, int N, int rows, double T_s, double cull,
+                 bool defer_dynamic) {
   reset(b, rows, cull);
-  std::vector<double> s_xy, base, step;
+  // src/geometry.cpp:51-52, once per point
+  std::vector<double> steps(2 * static_cast<size_t>(N));
+  par_for((N + 4095) / 4096, static_cast<size_t>(N) * 8, [&](int c) {
+    for (int j = c * 4096; j < std::min(N, (c + 1) * 4096); ++j) {
+      const double* p = pts4 + 4 * j;
+      steps[2 * j] = T_s * p[3] * std::cos(p[2]);
+      steps[2 * j + 1] = T_s * p[3] * std::sin(p[2]);
+    }
+  });
   bool any_moving = false;
-  for (int j = 0; j < N; ++j) {
-    const double* p = pts4 + 4 * j;
-    any_moving |= !(T_s * p[3] * std::cos(p[2]) == 0.0 && T_s * p[3] * std::sin(p[2]) == 0.0);
+  for (int j = 0; j < N && !any_moving; ++j) {
+    any_moving = !(steps[2 * j] == 0.0 && steps[2 * j + 1] == 0.0);
   }
   // small mixed clouds stay one scan per state: every point dynamic
   const bool all_dynamic = N <= kSmall && any_moving;
-  BBox box;
+  std::vector<double> s_xy(2 * static_cast<size_t>(N));
+  b.dbase.resize(4 * static_cast<size_t>(N));
+  size_t ns = 0, nd = 0;
+  double xmin = INFINITY, xmax = -INFINITY, ymin = INFINITY, ymax = -INFINITY;
+  bool finite = true;
+  const auto see = [&](double x, double y) {
+    finite &= std::isfinite(x) && std::isfinite(y);
+    xmin = std::min(xmin, x);
+    xmax = std::max(xmax, x);
+    ymin = std::min(ymin, y);
+    ymax = std::max(ymax, y);
+  };
   for (int j = 0; j < N; ++j) {
     const double* p = pts4 + 4 * j;
-    // src/geometry.cpp:51-52
-    const double sx = T_s * p[3] * std::cos(p[2]);
-    const double sy = T_s * p[3] * std::sin(p[2]);
+    const double sx = steps[2 * j], sy = steps[2 * j + 1];
+    see(p[0], p[1]);
     if (!all_dynamic && sx == 0.0 && sy == 0.0) {  // x + h * (+-0) == x: identical rows
-      s_xy.push_back(p[0]);
-      s_xy.push_back(p[1]);
-      box.see(p[0], p[1]);
+      s_xy[2 * ns] = p[0];
+      s_xy[2 * ns + 1] = p[1];
+      ++ns;
     } else {
-      base.push_back(p[0]);
-      base.push_back(p[1]);
-      step.push_back(sx);
-      step.push_back(sy);
+      double* q = b.dbase.data() + 4 * nd++;
+      q[0] = p[0];
+      q[1] = p[1];
+      q[2] = sx;
+      q[3] = sy;
       // x + r * step is monotone in r (rounding is monotone): rows 0 and
       // rows - 1 bound every position of the point
-      box.see(p[0], p[1]);
-      box.see(p[0] + (rows - 1) * sx, p[1] + (rows - 1) * sy);
+      see(p[0] + (rows - 1) * sx, p[1] + (rows - 1) * sy);
     }
   }
+  s_xy.resize(2 * ns);
+  b.dbase.resize(4 * nd);
+  BBox box;
+  box.finite = finite;
+  if (N > 0 && finite) {
+    box.see(xmin, ymin);
+    box.see(xmax, ymax);
+  }
   b.Ns = static_cast<int>(s_xy.size() / 2);
-  b.Nd = static_cast<int>(base.size() / 2);
-  finish(b, s_xy, box, [&](int r, double* out) {
-    // src/geometry.cpp:53-57: x + h * step (int h promoted to double)
-    for (int k = 0; k < b.Nd; ++k) {
-      out[2 * k] = base[2 * k] + r * step[2 * k];
-      out[2 * k + 1] = base[2 * k + 1] + r * step[2 * k + 1];
-    }
-  });
+  b.Nd = static_cast<int>(b.dbase.size() / 4);
+  finish_static(b, s_xy, box);
+  if (defer_dynamic && b.Nd > 0) {
+    b.dyn_deferred = true;
+    return;
+  }
+  finish_dynamic(b, [&](int r, double* out) { mover_row(b, r, out); });
 }
 
-void pack(const Binned& b, bool fp64, void* out) {
+void bin_dynamic(Binned& b) {
+  if (!b.dyn_deferred) return;
+  finish_dynamic(b, [&](int r, double* out) { mover_row(b, r, out); });
+  b.dyn_deferred = false;
+}
+
+void pack(const Binned& b, bool fp64, void* out, bool with_dynamic) {
   const size_t elem = fp64 ? sizeof(double) : sizeof(float);
   const Layout l = layout(b, elem);
   unsigned char* base = static_cast<unsigned char*>(out);
@@ -322,9 +375,11 @@ void pack(const Binned& b, bool fp64, void* out) {
     });
   };
   put(0, b.spts);
-  put(l.dpts, b.dpts);
   std::memcpy(base + l.sst, b.sst.data(), b.sst.size() * sizeof(int32_t));
-  std::memcpy(base + l.dst, b.dst.data(), b.dst.size() * sizeof(int32_t));
+  if (with_dynamic) {
+    put(l.dpts, b.dpts);
+    std::memcpy(base + l.dst, b.dst.data(), b.dst.size() * sizeof(int32_t));
+  }
   if (b.boxes) put(l.sbox, b.sbox);
 }
 

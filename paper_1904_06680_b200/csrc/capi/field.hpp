@@ -37,6 +37,12 @@ struct Binned {
   // box is separated from the chassis rectangle.
   bool boxes = false;
   std::vector<double> sbox;      // cells x 4 (when boxes)
+  // Raw movers of a points field (x, y, step x, step y) x Nd. With
+  // `dyn_deferred` the dynamic rows (dpts, dst) are not binned yet: the
+  // device bins its own image from these, and bin_dynamic() fills the host
+  // image later (overlapped with the device round).
+  std::vector<double> dbase;
+  bool dyn_deferred = false;
   int cells() const { return nx * ny; }
   // 0: x-buckets, 1: 2-D cells scanned by column, 2: 2-D cells with boxes
   int mode() const { return boxes ? 2 : (ny > 1 ? 1 : 0); }
@@ -56,11 +62,18 @@ void from_rows(Binned& b, const double* xy, int rows, int N, double cull);
 
 // From raw anchor-frame points (x, y, heading, speed) x N: the reference's
 // extrapolate (src/geometry.cpp:43-61) evaluated for rows 0..rows-1; points
-// with a zero step in x and y are static.
-void from_points(Binned& b, const double* pts4, int N, int rows, double T_s, double cull);
+// with a zero step in x and y are static. defer_dynamic: leave the dynamic
+// rows unbinned (dyn_deferred) -- see bin_dynamic.
+void from_points(Binned& b, const double* pts4, int N, int rows, double T_s, double cull,
+                 bool defer_dynamic = false);
+
+// Bins the deferred dynamic rows on the host (no-op when not deferred).
+void bin_dynamic(Binned& b);
 
 // Device image in the compute precision (fp64: the binned doubles as-is).
-void pack(const Binned& b, bool fp64, void* out);
+// with_dynamic = false leaves the dynamic parts of the image untouched (the
+// device bins them).
+void pack(const Binned& b, bool fp64, void* out, bool with_dynamic = true);
 
 // The chassis rectangle in the body frame: -rear < x < front, |y| < half_width.
 struct Box {

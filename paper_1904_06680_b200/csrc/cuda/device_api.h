@@ -179,6 +179,22 @@ int launch_select(const RoundArgs& a, void* stream);
 // FP64 re-evaluation of the selected candidates into sel_out.
 int launch_refine(NetKind k, const RoundArgs& a, void* stream);
 
+// Device binning of the dynamic rows of a raw-points field (field.hpp's
+// layout): row r of mover k sits at x + r * step (FP64, no contraction: the
+// host's positions bit for bit), rounded to the image precision, in the
+// cell order of the host's grid. Counts, per-row scan, scatter.
+struct BinArgs {
+  const double* movers;  // Nd x 4: x, y, step x, step y
+  int32_t Nd, rows, nx, ny;
+  double x0, y0, inv_g;
+  void* dpts;            // rows x Nd: float2 (fp64 == 0) or double2
+  int32_t* dst;          // rows x (cells + 1) starts
+  int32_t* cursor;       // rows x cells scratch
+  int32_t fp64;
+  int32_t _pad;
+};
+int bin_movers(const BinArgs& a, void* stream);
+
 // FFMA throughput probe (the FP32 roofline denominator).
 int measure_ffma(int device, double* tflops, double* sm_mhz);
 

@@ -44,7 +44,7 @@ def test_c4_lot_per_sample_stats(precision):
     assert same.mean() >= 0.99
 
 
-@pytest.mark.parametrize("which", ["c2", "c5_mixed", "c5_static"])
+@pytest.mark.parametrize("which", ["c2", "c5_mixed", "c5_static", "c5_dense"])
 def test_raw_points_path_equals_extrapolated_field(which):
     """pp_plan_step_points(points) == pp_plan_step(extrapolate(points)),
     bit for bit (the field is built by the planner)."""
@@ -58,11 +58,11 @@ def test_raw_points_path_equals_extrapolated_field(which):
         pts = np.array([(q.x, q.y, q.heading, q.speed)
                         for q in pp.sense(m, m.initial_state, w.t, 20, 0.1)])
     else:
-        n = 500
+        n = 10000 if which == "c5_dense" else 500  # c5_dense: movers binned on the device
         pts = np.zeros((n, 4))
         pts[:, 0] = rng.uniform(-10, 30, n)
         pts[:, 1] = rng.uniform(2.5, 10, n) * rng.choice([-1, 1], n)
-        if which == "c5_mixed":
+        if which in ("c5_mixed", "c5_dense"):
             dyn = rng.random(n) < 0.25
             pts[dyn, 2] = rng.choice([0.0, math.pi], dyn.sum())
             pts[dyn, 3] = rng.uniform(0, 15, dyn.sum())
