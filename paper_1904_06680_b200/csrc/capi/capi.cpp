@@ -850,7 +850,10 @@ void run_round_launch(pp_handle* h, uint64_t t, int iter, int r0, int rc, const 
   const size_t n_recs = shape.refill ? static_cast<size_t>(rc) * a.grid : a.n_tiles;
   h->d_tiles.reserve(sizeof(ppdev::Rec) * n_recs, "tile records");
   a.tile_recs = static_cast<ppdev::Rec*>(h->d_tiles.p);
-  const bool generic = h->kind == ppdev::NetKind::kGeneric;
+  // theta in a global per-lane column (NetGlobal): any architecture without
+  // a register specialisation in this precision ([5,10,10,2] has one in FP32)
+  const bool generic = h->kind == ppdev::NetKind::kGeneric ||
+                       (fp64 && h->kind == ppdev::NetKind::k5_10_10_2);
   if (generic || rerank) {
     const size_t lanes = std::max<size_t>(generic ? static_cast<size_t>(a.grid) * a.block : 0,
                                           rerank ? kRefineGrid * 128 : 0);
@@ -1634,6 +1637,7 @@ NetKind classify(const int32_t* s, int32_t n) {
     if (s[1] == 2) return NetKind::k5_2_2;
     if (s[1] == 10) return NetKind::k5_10_2;
   }
+  if (n == 4 && s[0] == 5 && s[1] == 10 && s[2] == 10 && s[3] == 2) return NetKind::k5_10_10_2;
   return NetKind::kGeneric;
 }
 }  // namespace ppdev

@@ -149,7 +149,7 @@ struct RoundArgs {
 };
 
 // Architecture dispatch of the specialised kernels.
-enum class NetKind : int { kGeneric = 0, k5_2_2 = 1, k5_10_2 = 2 };
+enum class NetKind : int { kGeneric = 0, k5_2_2 = 1, k5_10_2 = 2, k5_10_10_2 = 3 };
 NetKind classify(const int32_t* sizes, int32_t n_layers);
 
 // Grid sizing: persistent blocks = min(n_tiles, SMs x resident blocks/SM).

@@ -230,6 +230,45 @@ struct NetReg {
   }
 };
 
+// [5, A, B, 2], theta in registers (FP32 [5,10,10,2]: 192 parameters, two
+// CTAs of 128 threads per SM at <= 255 registers).
+template <typename Real, int A, int B>
+struct NetReg3 {
+  static constexpr int P = 6 * A + (A + 1) * B + (B + 1) * 2;
+  static constexpr int kP = P;
+  Real w[P];
+  __device__ __forceinline__ void set(int i, Real v) { w[i] = v; }
+  __device__ __forceinline__ void eval(const Real s[5], Real& a0, Real& a1) const {
+    Real h1[A], h2[B];
+#pragma unroll
+    for (int o = 0; o < A; ++o) {
+      Real acc = w[5 * A + o];
+#pragma unroll
+      for (int i = 0; i < 5; ++i) acc += w[o * 5 + i] * s[i];
+      h1[o] = M<Real>::th(acc);
+    }
+    constexpr int off2 = 6 * A;
+#pragma unroll
+    for (int o = 0; o < B; ++o) {
+      Real acc = w[off2 + A * B + o];
+#pragma unroll
+      for (int i = 0; i < A; ++i) acc += w[off2 + o * A + i] * h1[i];
+      h2[o] = M<Real>::th(acc);
+    }
+    constexpr int off3 = off2 + (A + 1) * B;
+    Real out[2];
+#pragma unroll
+    for (int o = 0; o < 2; ++o) {
+      Real acc = w[off3 + 2 * B + o];
+#pragma unroll
+      for (int i = 0; i < B; ++i) acc += w[off3 + o * B + i] * h2[i];
+      out[o] = M<Real>::th(acc);
+    }
+    a0 = out[0];
+    a1 = out[1];
+  }
+};
+
 // Any architecture (sizes <= 256): theta in a per-lane column of a global
 // scratch buffer (coalesced across the warp), activations in local memory.
 template <typename Real>
@@ -875,9 +914,9 @@ constexpr int rec_width(int P) {
 template <typename Real>
 using Vec16 = typename std::conditional<sizeof(Real) == 4, float4, double2>::type;
 
-template <typename Real, int H1>
+template <typename Real, class Net>
 __global__ void __launch_bounds__(256) generate_kernel(const RoundArgs a) {
-  constexpr int P = NetReg<Real, H1>::P;
+  constexpr int P = Net::P;
   constexpr int W = rec_width<Real>(P);
   constexpr int V = W * static_cast<int>(sizeof(Real)) / 16;
   const Consts<Real>& K = consts_of<Real>(a);
@@ -898,7 +937,7 @@ __global__ void __launch_bounds__(256) generate_kernel(const RoundArgs a) {
     } rec;
     draw_theta<Real, P>(a, __ldg(a.key_prefix + r), a.injected ? local : a.cand_begin + local, P,
                         [&](int i, Real v) { rec.v[i] = v; });
-    NetReg<Real, H1> n;
+    Net n;
 #pragma unroll
     for (int i = 0; i < P; ++i) n.w[i] = rec.v[i];
     n.eval(s0, rec.v[P], rec.v[P + 1]);  // first action (src/planner.cpp:130-132)
@@ -914,7 +953,8 @@ __global__ void __launch_bounds__(256) generate_kernel(const RoundArgs a) {
 // fits 6 (<= 85 registers), wider nets and FP64 need more registers.
 template <typename Real, class Net>
 constexpr int refill_min_blocks() {
-  return sizeof(Real) == 4 ? (Net::kP <= 24 ? PARAPLAN_REFILL_MINB : 3) : (Net::kP <= 24 ? 4 : 2);
+  return sizeof(Real) == 4 ? (Net::kP <= 24 ? PARAPLAN_REFILL_MINB : (Net::kP <= 100 ? 3 : 2))
+                           : (Net::kP <= 24 ? 4 : 2);
 }
 
 template <typename Real, class Net, int kGrid>
@@ -1043,6 +1083,10 @@ struct NetFactory;
 template <typename Real, int H1>
 struct NetFactory<Real, NetReg<Real, H1>> {
   static __device__ __forceinline__ NetReg<Real, H1> make(const RoundArgs&) { return {}; }
+};
+template <typename Real, int A, int B>
+struct NetFactory<Real, NetReg3<Real, A, B>> {
+  static __device__ __forceinline__ NetReg3<Real, A, B> make(const RoundArgs&) { return {}; }
 };
 
 template <typename Real>
@@ -1287,7 +1331,7 @@ int launch_generate_impl(const RoundArgs& a, void* stream) {
     if (refill_schedule<Net>()) {
       const int64_t total = a.count * a.restart_count;
       const int gen_blocks = static_cast<int>((total + 255) / 256);
-      generate_kernel<Real, Net::kH1><<<gen_blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(a);
+      generate_kernel<Real, Net><<<gen_blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(a);
       return static_cast<int>(cudaGetLastError());
     }
   }

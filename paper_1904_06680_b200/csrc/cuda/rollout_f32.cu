@@ -7,6 +7,8 @@ int shape_f32(NetKind k, int device, int smem_bytes, int grid, LaunchShape* out)
   switch (k) {
     case NetKind::k5_2_2:
       return shape_impl<float, NetReg<float, 2>>(device, smem_bytes, grid, out);
+    case NetKind::k5_10_10_2:
+      return shape_impl<float, NetReg3<float, 10, 10>>(device, smem_bytes, grid, out);
     case NetKind::k5_10_2:
       return shape_impl<float, NetReg<float, 10>>(device, smem_bytes, grid, out);
     default:
@@ -18,6 +20,8 @@ int launch_generate_f32(NetKind k, const RoundArgs& a, void* stream) {
   switch (k) {
     case NetKind::k5_2_2:
       return launch_generate_impl<float, NetReg<float, 2>>(a, stream);
+    case NetKind::k5_10_10_2:
+      return launch_generate_impl<float, NetReg3<float, 10, 10>>(a, stream);
     case NetKind::k5_10_2:
       return launch_generate_impl<float, NetReg<float, 10>>(a, stream);
     default:
@@ -29,6 +33,8 @@ int launch_rollout_f32(NetKind k, const RoundArgs& a, void* stream) {
   switch (k) {
     case NetKind::k5_2_2:
       return launch_rollout_impl<float, NetReg<float, 2>>(a, stream);
+    case NetKind::k5_10_10_2:
+      return launch_rollout_impl<float, NetReg3<float, 10, 10>>(a, stream);
     case NetKind::k5_10_2:
       return launch_rollout_impl<float, NetReg<float, 10>>(a, stream);
     default:
