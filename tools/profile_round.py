@@ -1,9 +1,12 @@
 """One sampling round (default C2 (2^20 candidates, H=30, 20 points) repeated --reps
 times through the C-ABI: the command profiled under ncu (profiles/)."""
 import argparse
+import os
 import sys
 from pathlib import Path
 
+# the construction warm-up round would be the first launches ncu captures
+os.environ.setdefault("PARAPLAN_PREWARM", "0")
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 from paper_1904_06680_b200 import capi, workloads  # noqa: E402
 
