@@ -798,11 +798,16 @@ void run_round_launch(pp_handle* h, uint64_t t, int iter, int r0, int rc, const 
     a.theta_buf = h->d_theta.p;  // [total][theta_elem]: theta, first action, pad
     a.first_buf = nullptr;
   }
-  if (rerank) {
+  // several restarts on the refill schedule: winners from the sample keys
+  const bool keys_only = shape0.refill && rc > 1;
+  a.keys_only = keys_only ? 1 : 0;
+  if (rerank || keys_only) {
     h->d_skeys.reserve(total * (fp64 ? sizeof(ppdev::SKey) : sizeof(ppdev::SKey32)), "sample keys");
-    h->d_sel.reserve(kSelCap * sizeof(ppdev::SelRec), "selection");
     a.skeys = h->d_skeys.p;
     a.skey32 = fp64 ? 0 : 1;
+  }
+  if (rerank) {
+    h->d_sel.reserve(kSelCap * sizeof(ppdev::SelRec), "selection");
     a.sel_out = static_cast<ppdev::SelRec*>(h->d_sel.p);
     a.sel_list = reinterpret_cast<int64_t*>(dres + kSelOff);
     a.sel_cap = kSelCap;
@@ -847,7 +852,8 @@ void run_round_launch(pp_handle* h, uint64_t t, int iter, int r0, int rc, const 
                                                                ppdev_warps()
                                                          : a.n_tiles));
   a.field_smem_bytes = field_smem;
-  const size_t n_recs = shape.refill ? static_cast<size_t>(rc) * a.grid : a.n_tiles;
+  const size_t n_recs = shape.refill ? static_cast<size_t>(rc) * std::max(a.grid, 148 * 4)
+                                    : static_cast<size_t>(a.n_tiles);
   h->d_tiles.reserve(sizeof(ppdev::Rec) * n_recs, "tile records");
   a.tile_recs = static_cast<ppdev::Rec*>(h->d_tiles.p);
   // theta in a global per-lane column (NetGlobal): any architecture without
@@ -897,7 +903,7 @@ void run_round_launch(pp_handle* h, uint64_t t, int iter, int r0, int rc, const 
   float ms = 0.f;
   ck(cudaEventElapsedTime(&ms, h->ev0, h->ev1), "event timing");
   h->timing.kernel_ms += ms;
-  h->timing.launches += (shape.refill ? 2 : 1) + (rerank ? 1 : 0);
+  h->timing.launches += (shape.refill ? 2 : 1) + (rerank ? 1 : 0) + (keys_only ? 1 : 0);
   h->timing.samples += count * rc;
   const char* hres = static_cast<const char*>(h->h_round.p);
   const unsigned long long* ex = reinterpret_cast<const unsigned long long*>(hres + kExecOff);

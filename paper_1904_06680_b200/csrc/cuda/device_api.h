@@ -137,7 +137,10 @@ struct RoundArgs {
   // near-tie re-ranking (null skeys = off)
   void* skeys;                 // [restart_count * count] SKey (FP64) or SKey32 (FP32)
   int32_t skey32;              // skeys holds SKey32
-  int32_t _pad_skey;
+  // several restarts (refill schedule): the rollout only writes the sample
+  // keys, and reduce_keys_kernel forms the per-restart winners from them
+  // (lanes crossing restarts would otherwise flush their bests every batch)
+  int32_t keys_only;
   const void* field64;         // FP64 image of the field (same layout as `field`)
   int64_t* sel_list;           // [sel_cap] selected flat indices
   SelRec* sel_out;             // [sel_cap] their FP64 keys

@@ -860,7 +860,8 @@ __device__ __forceinline__ void finish_round(const RoundArgs& a, const Rec* recs
   __shared__ int s_last;
   __threadfence();
   __syncthreads();
-  if (threadIdx.x == 0) s_last = atomicAdd(&a.counters[1], 1u) == gridDim.x - 1;
+  const unsigned n_blocks = gridDim.x * gridDim.y;
+  if (threadIdx.x == 0) s_last = atomicAdd(&a.counters[1], 1u) == n_blocks - 1;
   __syncthreads();
   if (!s_last) return;
   __threadfence();
@@ -992,25 +993,43 @@ __global__ void __launch_bounds__(kBlock, refill_min_blocks<Real, Net>())
   Key best = empty_key();
   int best_r = -1;
   int q_head = 32, q_count = 0, q_r = 0, q_c0 = 0;
+  // claimed batch range [qb, qe): with several restarts a warp claims runs of
+  // consecutive batches, so its lanes rarely cross restarts (each crossing
+  // flushes lane bests into the per-restart tables); single batches near the
+  // end of the round keep the tail balanced
+  unsigned qb = 0, qe = 0;
+  const unsigned run = a.restart_count > 1 ? 8u : 1u;
+  const unsigned tail = static_cast<unsigned>(gridDim.x) * kWarps * 2u * run;
   bool exhausted = false;
   unsigned long long n_steps = 0, n_states = 0;
+  const bool track = a.keys_only == 0;  // lane bests (one restart) or keys only
 
   for (;;) {
     // -------- hand the warp's current batch to idle lanes --------
     const unsigned need = __ballot_sync(kFull, !active);
     if (need != 0u) {
       if (q_head >= q_count && !exhausted) {
-        unsigned b = 0;
-        if (lane == 0) b = atomicAdd(&a.counters[0], 1u);
-        b = __shfl_sync(kFull, b, 0);
-        if (b >= total_batches) {
+        if (qb >= qe) {
+          unsigned b = 0;
+          if (lane == 0) {
+            const unsigned seen = __ldcg(&a.counters[0]);
+            const unsigned k = seen + tail < total_batches ? run : 1u;
+            b = atomicAdd(&a.counters[0], k);
+            qe = min(b + k, total_batches);
+          }
+          b = __shfl_sync(kFull, b, 0);
+          qe = __shfl_sync(kFull, qe, 0);
+          qb = b;
+        }
+        if (qb >= total_batches) {
           exhausted = true;
         } else {
-          q_r = static_cast<int>(b) / bpr;
-          q_c0 = (static_cast<int>(b) - q_r * bpr) * 32;
+          q_r = static_cast<int>(qb) / bpr;
+          q_c0 = (static_cast<int>(qb) - q_r * bpr) * 32;
           const int64_t left = a.count - q_c0;
           q_count = left < 32 ? static_cast<int>(left) : 32;
           q_head = 0;
+          ++qb;
         }
       }
       const int avail = q_count - q_head;
@@ -1037,14 +1056,17 @@ __global__ void __launch_bounds__(kBlock, refill_min_blocks<Real, Net>())
     const int cls = advance<Real, kGrid>(L, net, K, f, H);
     const bool done = active && cls >= 0;
     // lane bests are per restart: flush the old one before crossing over
-    bool flush = done && best.cls >= 0 && best_r != my_r;
+    bool flush = track && done && best.cls >= 0 && best_r != my_r;
     if (__any_sync(kFull, flush)) flush_bests(flush, best, best_r, table[warp], lane);
     if (done) {
       const Real term = terminal_cost(L, K);
-      const Key k = make_key<Real>(cls, L.h, L.path, term, static_cast<int>(a.cand_begin + my_c));
-      if (best.cls < 0 || prefer(k, best)) {
-        best = k;
-        best_r = my_r;
+      if (track) {
+        const Key k =
+            make_key<Real>(cls, L.h, L.path, term, static_cast<int>(a.cand_begin + my_c));
+        if (best.cls < 0 || prefer(k, best)) {
+          best = k;
+          best_r = my_r;
+        }
       }
       n_steps += static_cast<unsigned long long>(L.h);
       n_states += static_cast<unsigned long long>(L.h + 1);
@@ -1057,6 +1079,13 @@ __global__ void __launch_bounds__(kBlock, refill_min_blocks<Real, Net>())
   }
 
   // -------- flush lane bests, combine warps, publish CTA records --------
+  const unsigned long long steps = block_sum(n_steps, red_sum);
+  const unsigned long long states = block_sum(n_states, red_sum);
+  if (threadIdx.x == 0) {
+    atomicAdd(&a.exec[0], steps);
+    atomicAdd(&a.exec[1], states);
+  }
+  if (!track) return;  // reduce_keys_kernel forms the winners
   bool flush = best.cls >= 0;
   flush_bests(flush, best, best_r, table[warp], lane);
   __syncthreads();
@@ -1067,11 +1096,49 @@ __global__ void __launch_bounds__(kBlock, refill_min_blocks<Real, Net>())
     }
     a.tile_recs[static_cast<size_t>(r) * gridDim.x + blockIdx.x] = Rec{k.cls, k.idx, k.k1, k.k2};
   }
-  const unsigned long long steps = block_sum(n_steps, red_sum);
-  const unsigned long long states = block_sum(n_states, red_sum);
+  finish_round(a, a.tile_recs, static_cast<int>(gridDim.x), red);
+}
+
+// Per-restart winners from the sample keys (RoundArgs::keys_only): block
+// (x, r) reduces chunk x of restart r; the last block reduces the chunks.
+// The keys are the rollout's own: (cls, t_goal, FP32 cost) give the same
+// (cls, k1, k2) as make_key, and the index is the slot's.
+static __global__ void __launch_bounds__(256) reduce_keys_kernel(const RoundArgs a) {
+  __shared__ Key red[32];
+  wait_prior_grid();  // the rollout's keys
+  const int r = blockIdx.y;
+  const int64_t chunk = (a.count + gridDim.x - 1) / gridDim.x;
+  const int64_t lo = static_cast<int64_t>(blockIdx.x) * chunk;
+  const int64_t hi = lo + chunk < a.count ? lo + chunk : a.count;
+  Key k = empty_key();
+  for (int64_t c = lo + threadIdx.x; c < hi; c += blockDim.x) {
+    const int64_t slot = static_cast<int64_t>(r) * a.count + c;
+    double cost;
+    uint32_t meta;
+    if (a.skey32) {
+      const SKey32 q = static_cast<const SKey32*>(a.skeys)[slot];
+      cost = static_cast<double>(q.cost);
+      meta = q.meta;
+    } else {
+      const SKey q = static_cast<const SKey*>(a.skeys)[slot];
+      cost = q.cost;
+      meta = q.meta;
+    }
+    Key o;
+    o.cls = static_cast<int>(meta & 3u);
+    o.idx = static_cast<int>(a.cand_begin + c);
+    if (o.cls == 2) {
+      o.k1 = -static_cast<double>(meta >> 8);
+      o.k2 = -cost;
+    } else {
+      o.k1 = -cost;
+      o.k2 = 0.0;
+    }
+    if (k.cls < 0 || prefer(o, k)) k = o;
+  }
+  k = block_best(k, red);
   if (threadIdx.x == 0) {
-    atomicAdd(&a.exec[0], steps);
-    atomicAdd(&a.exec[1], states);
+    a.tile_recs[static_cast<size_t>(r) * gridDim.x + blockIdx.x] = Rec{k.cls, k.idx, k.k1, k.k2};
   }
   finish_round(a, a.tile_recs, static_cast<int>(gridDim.x), red);
 }
@@ -1351,7 +1418,23 @@ int launch_rollout_impl(const RoundArgs& a, void* stream) {
   }
   bool after_generate = false;
   if constexpr (Net::kP > 0) after_generate = refill_schedule<Net>();
-  return static_cast<int>(launch_dependent(k, a.grid, a.block, smem, st, after_generate, a));
+  cudaError_t e = launch_dependent(k, a.grid, a.block, smem, st, after_generate, a);
+  if (e == cudaSuccess && a.keys_only) {
+    // about four blocks per SM over all restarts
+    const int64_t per = std::max<int64_t>(1, std::min<int64_t>((a.count + 2047) / 2048,
+                                                              148 * 4 / a.restart_count));
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(static_cast<unsigned>(per), static_cast<unsigned>(a.restart_count));
+    cfg.blockDim = dim3(256);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, reduce_keys_kernel, a);
+  }
+  return static_cast<int>(e);
 }
 
 // Near-tie window of a finished round (a dependent launch after the rollout).
