@@ -639,11 +639,14 @@ void certify_round(pp_handle* h, ppdev::RoundArgs& a, uint64_t t, int iter, int 
 constexpr int kSelCap = 1 << 16;    // near-tie candidates re-ranked per launch
 constexpr int kSelFirst = 512;      // copied back with the round result
 // Round block (device, one allocation; its head is copied back in ONE D2H):
-// [counters u32 x 16][exec u64 x 4 + pad][Rec x kMaxRestartsPerLaunch][selected indices int64 x kSelCap]
+// [counters u32 x 16][exec u64 x 4 + pad][Rec x kMaxRestartsPerLaunch]
+// [unflagged Rec x kMaxRestartsPerLaunch][selected indices int64 x kSelCap]
 constexpr size_t kExecOff = 64;
 constexpr size_t kRecOff = 128;
+// [Rec x kMaxRestartsPerLaunch] best unflagged per restart (keys_only rounds)
+constexpr size_t kFreeOff = kRecOff + sizeof(ppdev::Rec) * ppdev::kMaxRestartsPerLaunch;
 constexpr size_t kSelOff =
-    (kRecOff + sizeof(ppdev::Rec) * ppdev::kMaxRestartsPerLaunch + 63) / 64 * 64;
+    (kFreeOff + sizeof(ppdev::Rec) * ppdev::kMaxRestartsPerLaunch + 63) / 64 * 64;
 constexpr size_t kRoundBytes = kSelOff + sizeof(int64_t) * kSelCap;
 constexpr int kRefineGrid = 148 * 2;
 
@@ -801,6 +804,7 @@ void run_round_launch(pp_handle* h, uint64_t t, int iter, int r0, int rc, const 
   // several restarts on the refill schedule: winners from the sample keys
   const bool keys_only = shape0.refill && rc > 1;
   a.keys_only = keys_only ? 1 : 0;
+  a.out_free = keys_only && rerank ? reinterpret_cast<ppdev::Rec*>(dres + kFreeOff) : nullptr;
   if (rerank || keys_only) {
     h->d_skeys.reserve(total * (fp64 ? sizeof(ppdev::SKey) : sizeof(ppdev::SKey32)), "sample keys");
     a.skeys = h->d_skeys.p;
@@ -852,7 +856,8 @@ void run_round_launch(pp_handle* h, uint64_t t, int iter, int r0, int rc, const 
                                                                ppdev_warps()
                                                          : a.n_tiles));
   a.field_smem_bytes = field_smem;
-  const size_t n_recs = shape.refill ? static_cast<size_t>(rc) * std::max(a.grid, 148 * 4)
+  // tile records (x2 for keys_only: best and best unflagged)
+  const size_t n_recs = shape.refill ? 2 * static_cast<size_t>(rc) * std::max(a.grid, 148 * 4)
                                     : static_cast<size_t>(a.n_tiles);
   h->d_tiles.reserve(sizeof(ppdev::Rec) * n_recs, "tile records");
   a.tile_recs = static_cast<ppdev::Rec*>(h->d_tiles.p);
@@ -978,10 +983,22 @@ void certify_round(pp_handle* h, ppdev::RoundArgs& a, uint64_t t, int iter, int 
   }
   const double rho = a.sel_rho, alpha = a.sel_alpha;
   std::vector<ppdev::SelBound> bound(rc);
+  // the first window is built around each restart's best unflagged
+  // candidate when the round reports it (keys_only), else its winner
+  const ppdev::Rec* free_recs =
+      a.out_free != nullptr
+          ? reinterpret_cast<const ppdev::Rec*>(static_cast<const char*>(h->h_round.p) + kFreeOff)
+          : nullptr;
   for (int r = 0; r < rc; ++r) {
-    bound[r].cls = out[r].cls;
-    bound[r].t_goal = out[r].cls == 2 ? static_cast<int>(-out[r].k1) : 0;
-    bound[r].thr = (out[r].cls == 2 ? -out[r].k2 : -out[r].k1) * (1.0 + rho) + alpha;
+    pp_record o = out[r];
+    if (free_recs != nullptr && free_recs[r].cls >= 0) {
+      o.cls = free_recs[r].cls;
+      o.k1 = free_recs[r].k1;
+      o.k2 = free_recs[r].k2;
+    }
+    bound[r].cls = o.cls;
+    bound[r].t_goal = o.cls == 2 ? static_cast<int>(-o.k1) : 0;
+    bound[r].thr = (o.cls == 2 ? -o.k2 : -o.k1) * (1.0 + rho) + alpha;
   }
   std::vector<char> certified(rc, 0);
   std::vector<int64_t> list;
@@ -1107,6 +1124,13 @@ void certify_round(pp_handle* h, ppdev::RoundArgs& a, uint64_t t, int iter, int 
         continue;
       }
       all = false;
+      if (trace_level() >= 2) {
+        std::fprintf(stderr,
+                     "[paraplan]   restart %d open: window cls %d t_goal %d thr %.9g slack %.3g; "
+                     "exact best cls %d t_goal %d cost %.9g\n",
+                     r0 + r, bd.cls, bd.t_goal, bd.thr, slack, e ? e->cls : -9,
+                     e ? e->t_goal : -9, e ? e->cost : 0.0);
+      }
       const bool same = e != nullptr && e->cls == bd.cls && (bd.cls != 2 || e->t_goal == bd.t_goal);
       const double widened = bd.thr * 1.25 + alpha;
       bound[r].thr = same ? std::max(e->cost * (1.0 + rho) + alpha, widened) : widened;

@@ -141,6 +141,11 @@ struct RoundArgs {
   // keys, and reduce_keys_kernel forms the per-restart winners from them
   // (lanes crossing restarts would otherwise flush their bests every batch)
   int32_t keys_only;
+  // keys_only: per restart also the best candidate NOT flagged marginal; the
+  // first window is built around it (flagged candidates are always in the
+  // window), so a flagged FP32 winner that the exact arithmetic demotes
+  // does not force extra widening passes
+  Rec* out_free;
   const void* field64;         // FP64 image of the field (same layout as `field`)
   int64_t* sel_list;           // [sel_cap] selected flat indices
   SelRec* sel_out;             // [sel_cap] their FP64 keys

@@ -855,16 +855,23 @@ __device__ __forceinline__ void write_sample(const RoundArgs& a, int64_t slot, i
 
 // Last CTA: per-restart reduction of `n_src` records per restart (laid out
 // restart-major), publish the work counters, re-arm the tickets.
-__device__ __forceinline__ void finish_round(const RoundArgs& a, const Rec* recs, int n_src,
-                                             Key* red) {
+// Last-block election over the whole grid (the ticket is re-armed by
+// publish_round).
+__device__ __forceinline__ bool last_block(const RoundArgs& a) {
   __shared__ int s_last;
   __threadfence();
   __syncthreads();
   const unsigned n_blocks = gridDim.x * gridDim.y;
   if (threadIdx.x == 0) s_last = atomicAdd(&a.counters[1], 1u) == n_blocks - 1;
   __syncthreads();
-  if (!s_last) return;
-  __threadfence();
+  if (s_last) __threadfence();
+  return s_last != 0;
+}
+
+// Per-restart reduction of `n_src` records per restart (restart-major) into
+// out[restart].
+__device__ __forceinline__ void reduce_recs(const RoundArgs& a, const Rec* recs, int n_src,
+                                            Key* red, Rec* out) {
   for (int r = 0; r < a.restart_count; ++r) {
     Key k = empty_key();
     for (int t = threadIdx.x; t < n_src; t += blockDim.x) {
@@ -872,8 +879,12 @@ __device__ __forceinline__ void finish_round(const RoundArgs& a, const Rec* recs
       if (o.cls >= 0 && (k.cls < 0 || prefer(o, k))) k = o;
     }
     const Key best = block_best(k, red);
-    if (threadIdx.x == 0) a.out[r] = Rec{best.cls, best.idx, best.k1, best.k2};
+    if (threadIdx.x == 0) out[r] = Rec{best.cls, best.idx, best.k1, best.k2};
   }
+}
+
+// Publish the work counters and re-arm the tickets (last block only).
+__device__ __forceinline__ void publish_round(const RoundArgs& a) {
   if (threadIdx.x == 0) {
     a.exec[2] = atomicExch(&a.exec[0], 0ull);
     a.exec[3] = atomicExch(&a.exec[1], 0ull);
@@ -881,6 +892,13 @@ __device__ __forceinline__ void finish_round(const RoundArgs& a, const Rec* recs
     a.counters[1] = 0;
     a.counters[2] = 0;  // the window selection that follows counts from zero
   }
+}
+
+__device__ __forceinline__ void finish_round(const RoundArgs& a, const Rec* recs, int n_src,
+                                             Key* red) {
+  if (!last_block(a)) return;
+  reduce_recs(a, recs, n_src, red, a.out);
+  publish_round(a);
 }
 
 // Warp-cooperative flush of the lanes' best keys (flagged by `flush`) into
@@ -1110,7 +1128,7 @@ static __global__ void __launch_bounds__(256) reduce_keys_kernel(const RoundArgs
   const int64_t chunk = (a.count + gridDim.x - 1) / gridDim.x;
   const int64_t lo = static_cast<int64_t>(blockIdx.x) * chunk;
   const int64_t hi = lo + chunk < a.count ? lo + chunk : a.count;
-  Key k = empty_key();
+  Key k = empty_key(), kf = empty_key();  // best, best not flagged marginal
   for (int64_t c = lo + threadIdx.x; c < hi; c += blockDim.x) {
     const int64_t slot = static_cast<int64_t>(r) * a.count + c;
     double cost;
@@ -1135,12 +1153,20 @@ static __global__ void __launch_bounds__(256) reduce_keys_kernel(const RoundArgs
       o.k2 = 0.0;
     }
     if (k.cls < 0 || prefer(o, k)) k = o;
+    if ((meta & 4u) == 0u && (kf.cls < 0 || prefer(o, kf))) kf = o;
   }
   k = block_best(k, red);
+  kf = block_best(kf, red);
+  const unsigned n_src = gridDim.x;
+  Rec* tiles_free = a.tile_recs + static_cast<size_t>(a.restart_count) * n_src;
   if (threadIdx.x == 0) {
-    a.tile_recs[static_cast<size_t>(r) * gridDim.x + blockIdx.x] = Rec{k.cls, k.idx, k.k1, k.k2};
+    a.tile_recs[static_cast<size_t>(r) * n_src + blockIdx.x] = Rec{k.cls, k.idx, k.k1, k.k2};
+    tiles_free[static_cast<size_t>(r) * n_src + blockIdx.x] = Rec{kf.cls, kf.idx, kf.k1, kf.k2};
   }
-  finish_round(a, a.tile_recs, static_cast<int>(gridDim.x), red);
+  if (!last_block(a)) return;
+  reduce_recs(a, a.tile_recs, static_cast<int>(n_src), red, a.out);
+  if (a.out_free != nullptr) reduce_recs(a, tiles_free, static_cast<int>(n_src), red, a.out_free);
+  publish_round(a);
 }
 
 // ---------------------------------------------------- lockstep kernel ----
@@ -1255,8 +1281,8 @@ static __global__ void __launch_bounds__(256) select_kernel(const RoundArgs a) {
     SelBound bd;
     if (a.sel_bound != nullptr) {  // widened window of a later pass
       bd = a.sel_bound[r];
-    } else {  // first pass: around the round winner
-      const Rec b = a.out[r];
+    } else {  // first pass: around the round winner (its best unflagged candidate)
+      const Rec b = (a.out_free != nullptr && a.out_free[r].cls >= 0) ? a.out_free[r] : a.out[r];
       bd.cls = b.cls;
       bd.t_goal = b.cls == 2 ? static_cast<int>(-b.k1) : 0;
       bd.thr = (b.cls == 2 ? -b.k2 : -b.k1) * (1.0 + a.sel_rho) + a.sel_alpha;
