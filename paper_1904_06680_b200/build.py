@@ -55,7 +55,8 @@ def _json_dir() -> Path:
 
 
 def _headers() -> list[Path]:
-    return sorted(INC.rglob("*.h*")) + sorted(CSRC.rglob("*.h")) + sorted(CSRC.rglob("*.cuh"))
+    return (sorted(INC.rglob("*.h*")) + sorted(CSRC.rglob("*.h")) + sorted(CSRC.rglob("*.hpp"))
+            + sorted(CSRC.rglob("*.cuh")))
 
 
 def _stale(out: Path, deps: list[Path]) -> bool:

@@ -1,0 +1,372 @@
+// capi_internal.hpp -- internals shared by the C-ABI implementation files
+// (not installed; the boundary is include/paraplan_cuda.h):
+//   capi.cpp        the extern "C" entry points, construction, the plan step
+//   upload.cpp      snapshots -> round constants + binned field images (HBM)
+//   round.cpp       one sampling round on the device + certified re-ranking
+//   host_exact.cpp  the reference's FP64 rollout and sampling on the host
+// All compiled with -ffp-contract=off -fno-math-errno.
+#pragma once
+
+#include "paraplan_cuda.h"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <condition_variable>
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <exception>
+#include <functional>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <thread>
+#include <unordered_map>
+#include <vector>
+
+#include "../cuda/device_api.h"
+#include "field.hpp"
+#include "paraplan/geometry.hpp"
+#include "paraplan/planner.hpp"
+#include "paraplan/policy.hpp"
+#include "paraplan/rng.hpp"
+
+namespace ppcapi {
+
+inline thread_local std::string g_error;  // pp_last_error()
+
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct NoDevice : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+inline void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) {
+    throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+  }
+}
+
+template <class F>
+pp_status guarded(F&& f) {
+  try {
+    f();
+    return PP_OK;
+  } catch (const std::invalid_argument& e) {
+    g_error = e.what();
+    return PP_INVALID_ARGUMENT;
+  } catch (const NoDevice& e) {
+    g_error = e.what();
+    return PP_NO_DEVICE;
+  } catch (const CudaError& e) {
+    g_error = e.what();
+    return PP_CUDA_ERROR;
+  } catch (const std::exception& e) {
+    g_error = e.what();
+    return PP_RUNTIME_ERROR;
+  }
+}
+
+// Device buffer that only grows.
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  // Returns true when the buffer was (re)allocated.
+  bool reserve(size_t bytes, const char* what) {
+    if (bytes <= cap) return false;
+    if (p != nullptr) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    ck(cudaMalloc(&p, bytes), what);
+    cap = bytes;
+    return true;
+  }
+  void release() {
+    if (p != nullptr) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+};
+
+struct HostBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  void reserve(size_t bytes, const char* what) {
+    if (bytes <= cap) return;
+    if (p != nullptr) cudaFreeHost(p);
+    p = nullptr;
+    cap = 0;
+    ck(cudaMallocHost(&p, bytes), what);
+    cap = bytes;
+  }
+  void release() {
+    if (p != nullptr) cudaFreeHost(p);
+    p = nullptr;
+    cap = 0;
+  }
+};
+
+inline paraplan::VehicleParams params_of(const pp_vehicle& v) {
+  paraplan::VehicleParams p;
+  p.l_f = v.l_f;
+  p.l_r = v.l_r;
+  p.delta_max = v.delta_max;
+  p.delta_rate_max = v.delta_rate_max;
+  p.u_v_min = v.u_v_min;
+  p.u_v_max = v.u_v_max;
+  p.overhang_front = v.overhang_front;
+  p.overhang_rear = v.overhang_rear;
+  p.half_width = v.half_width;
+  p.T_s = v.T_s;
+  return p;
+}
+
+inline paraplan::PlannerConfig config_of(const pp_config& c) {
+  paraplan::PlannerConfig cfg;
+  cfg.H = c.H;
+  cfg.n_restarts = c.n_restarts;
+  cfg.n_iter_max = c.n_iter_max;
+  cfg.n_candidates = c.n_candidates;
+  cfg.n_obst_pts = c.n_obst_pts;
+  cfg.tol = {c.eps_xi, c.eps_eta, c.eps_phi, c.eps_v};
+  cfg.sigma_log_low = c.sigma_log_low;
+  cfg.sigma_log_high = c.sigma_log_high;
+  cfg.master_seed = c.master_seed;
+  cfg.early_exit = c.early_exit != 0;
+  cfg.threads = c.threads;
+  cfg.precision = c.precision;
+  cfg.device = c.device;
+  cfg.refine = c.refine != 0;
+  return cfg;
+}
+
+struct Key {
+  int cls = 0;
+  double k1 = 0.0, k2 = 0.0;
+};
+
+// Fork-join pool for the host's exact re-evaluation of near-tie candidates.
+// prewarm() is called when a round is launched: the workers wake and spin
+// for the job (up to a few ms) while the GPU works, so the fork itself costs
+// no thread wake-up latency.
+class HostPool {
+ public:
+  explicit HostPool(int n) {
+    for (int i = 1; i < n; ++i) workers_.emplace_back([this] { loop(); });
+  }
+  ~HostPool() {
+    {
+      std::lock_guard<std::mutex> lock(mu_);
+      stop_.store(true);
+    }
+    cv_.notify_all();
+    for (auto& w : workers_) w.join();
+  }
+  int size() const { return static_cast<int>(workers_.size()) + 1; }
+  void prewarm() {
+    {
+      std::lock_guard<std::mutex> lock(mu_);
+      warm_.fetch_add(1);
+    }
+    cv_.notify_all();
+  }
+  // fn(i) for i in [0, n), spread over the workers and the caller.
+  void run(int n, const std::function<void(int)>& fn) {
+    fn_ = &fn;
+    n_ = n;
+    next_.store(0);
+    done_.store(0);
+    {
+      std::lock_guard<std::mutex> lock(mu_);
+      job_.fetch_add(1, std::memory_order_release);
+    }
+    cv_.notify_all();
+    drain();
+    const int workers = static_cast<int>(workers_.size());
+    while (done_.load(std::memory_order_acquire) < workers) std::this_thread::yield();
+  }
+
+ private:
+  void drain() {
+    for (int i; (i = next_.fetch_add(1)) < n_;) (*fn_)(i);
+  }
+  void loop() {
+    uint64_t seen_job = 0, seen_warm = 0;
+    for (;;) {
+      {
+        std::unique_lock<std::mutex> lock(mu_);
+        cv_.wait(lock, [&] {
+          return stop_.load() || job_.load() != seen_job || warm_.load() != seen_warm;
+        });
+        if (stop_.load()) return;
+        seen_warm = warm_.load();
+      }
+      const auto t0 = std::chrono::steady_clock::now();
+      while (job_.load(std::memory_order_acquire) == seen_job && !stop_.load() &&
+             std::chrono::steady_clock::now() - t0 < std::chrono::milliseconds(5)) {
+      }
+      if (job_.load(std::memory_order_acquire) != seen_job) {
+        seen_job = job_.load(std::memory_order_acquire);
+        drain();
+        done_.fetch_add(1, std::memory_order_release);
+      }
+    }
+  }
+  std::vector<std::thread> workers_;
+  std::mutex mu_;
+  std::condition_variable cv_;
+  const std::function<void(int)>* fn_ = nullptr;
+  std::atomic<int> next_{0}, done_{0};
+  int n_ = 0;
+  std::atomic<uint64_t> job_{0}, warm_{0};
+  std::atomic<bool> stop_{false};
+};
+
+inline bool key_better(const Key& a, const Key& b) {  // src/planner.cpp:40-44
+  if (a.cls != b.cls) return a.cls > b.cls;
+  if (a.k1 != b.k1) return a.k1 > b.k1;
+  return a.k2 > b.k2;
+}
+
+constexpr int kSelCap = 1 << 16;    // near-tie candidates re-ranked per launch
+constexpr int kSelFirst = 512;      // copied back with the round result
+// Round block (device, one allocation; its head is copied back in ONE D2H):
+// [counters u32 x 16][exec u64 x 4 + pad][Rec x kMaxRestartsPerLaunch]
+// [unflagged Rec x kMaxRestartsPerLaunch][selected indices int64 x kSelCap]
+constexpr size_t kExecOff = 64;
+constexpr size_t kRecOff = 128;
+// [Rec x kMaxRestartsPerLaunch] best unflagged per restart (keys_only rounds)
+constexpr size_t kFreeOff = kRecOff + sizeof(ppdev::Rec) * ppdev::kMaxRestartsPerLaunch;
+constexpr size_t kSelOff =
+    (kFreeOff + sizeof(ppdev::Rec) * ppdev::kMaxRestartsPerLaunch + 63) / 64 * 64;
+constexpr size_t kRoundBytes = kSelOff + sizeof(int64_t) * kSelCap;
+constexpr int kRefineGrid = 148 * 2;
+
+// PARAPLAN_TRACE=1: one stderr line per certification pass; 2: also the
+// host-side phase times of every plan step (diagnostics).
+inline int trace_level() {
+  static const int v = [] {
+    const char* e = std::getenv("PARAPLAN_TRACE");
+    return e != nullptr ? std::atoi(e) : 0;
+  }();
+  return v;
+}
+inline bool trace_on() { return trace_level() > 0; }
+
+struct PhaseClock {
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  char buf[256] = {};
+  int len = 0;
+  void mark(const char* what) {
+    if (trace_level() < 2 || len >= static_cast<int>(sizeof(buf)) - 1) return;
+    const double us =
+        std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
+    const int n = std::snprintf(buf + len, sizeof(buf) - len, " %s=%.1f", what, us);
+    if (n > 0) len = std::min(static_cast<int>(sizeof(buf)) - 1, len + n);
+  }
+  void flush() {
+    if (trace_level() >= 2) std::fprintf(stderr, "[paraplan] plan_step us:%s\n", buf);
+  }
+};
+// the plan step being traced on this thread (planners may run on several
+// threads at once, e.g. run_sweep)
+inline thread_local PhaseClock* g_clock = nullptr;
+inline void phase(const char* what) {
+  if (g_clock != nullptr) g_clock->mark(what);
+}
+
+}  // namespace ppcapi
+
+// The planner handle behind the opaque pp_handle of the C-ABI.
+struct pp_handle {
+  pp_model model{};
+  std::vector<int32_t> sizes;
+  paraplan::VehicleParams params;
+  paraplan::PlannerConfig cfg;
+  paraplan::NormConstants norm;
+  std::unique_ptr<paraplan::MlpPolicy> policy;
+  paraplan::ChassisPolytope chassis;
+  ppfield::Box box;  // the same rectangle as (front, rear, half width)
+  int P = 0;
+  ppdev::NetKind kind = ppdev::NetKind::kGeneric;
+  int device = 0;
+  bool fp64 = false;
+
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  // a deferred field goes up on `side` while the generator runs on `stream`;
+  // the rollout waits on ev_field (the dependent launch of the rollout after
+  // the generator stays intact)
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_field = nullptr;
+  bool field_via_side = false, field_event = false;
+  ppcapi::DevBuf d_field, d_params, d_round, d_tiles, d_samples, d_scratch, d_injected, d_theta, d_skeys,
+      d_sel, d_bound, d_movers, d_bin;
+  ppcapi::HostBuf h_field, h_params, h_round, h_bound, h_movers;
+
+  // near-tie re-ranking (PlannerConfig::refine): needs the host snapshot
+  bool rerank = true;
+  const pp_snapshot* snapshot = nullptr;  // -> snap_copy once a snapshot is resident
+  pp_snapshot snap_copy{};
+  std::vector<double> snap_warm;
+  double sel_rho = 1e-3;   // FP32 window: cost <= best * (1 + rho) + 1e-6
+  std::unique_ptr<ppcapi::HostPool> pool;  // exact re-evaluation of near ties
+  double dmarg32 = 2e-5;   // FP32 margin below which a worse-side verdict may flip
+
+  // resident snapshot
+  bool snap_valid = false;
+  std::map<int64_t, ppdev::LaunchShape> shapes;  // occupancy per (smem, grid mode, precision)
+  // plan_step: the field of the snapshot is binned and uploaded while the
+  // theta generator runs (consumed by the first round of the step)
+  std::function<void()> pending_field;
+  ppdev::RoundArgs base{};
+  int field_smem_bytes = 0;
+
+  pp_timing timing{};
+  // resident obstacle field: FP64 binned image (host) + device images
+  ppfield::Binned field;
+  bool field64_ready = false;
+  ppcapi::DevBuf d_field64;
+  ppcapi::HostBuf h_field64;
+};
+
+namespace ppcapi {
+
+// upload.cpp
+void finish_field(pp_handle* h, ppdev::RoundArgs& a);
+const void* ensure_field64(pp_handle* h);
+void keep_snapshot(pp_handle* h, const pp_snapshot& s);
+void set_round_constants(pp_handle* h, const pp_snapshot& s);
+void upload_field_rows(pp_handle* h, const pp_snapshot& s, ppdev::RoundArgs& a);
+void upload_points(pp_handle* h, const pp_snapshot_points& p, bool defer = false);
+void upload_snapshot(pp_handle* h, const pp_snapshot& s, bool defer = false);
+
+// round.cpp
+uint64_t key_prefix(uint64_t seed, uint64_t t, uint64_t r, uint64_t i);
+ppdev::LaunchShape launch_shape(pp_handle* h, bool fp64, int field_smem, int grid_mode);
+void consume_pending_field(pp_handle* h, bool side = false);
+void run_round_launch(pp_handle* h, uint64_t t, int iter, int r0, int rc, const double* center,
+                      int64_t c0, int64_t c1, const double* injected, pp_record* out,
+                      pp_rollout_stats* per_sample, bool force_fp64 = false);
+void certify_round(pp_handle* h, ppdev::RoundArgs& a, uint64_t t, int iter, int r0, int rc,
+                   const double* center, int64_t c0, int64_t c1, const double* injected,
+                   pp_record* out, bool fp64, uint32_t n_sel);
+void run_round(pp_handle* h, uint64_t t, int iter, int r0, int rc, const double* center,
+               int64_t c0, int64_t c1, const double* injected, pp_record* out,
+               pp_rollout_stats* per_sample);
+
+// host_exact.cpp
+void host_rollout(const pp_handle* h, const pp_snapshot& s, const double* theta,
+                  pp_rollout_stats* out, double* traj, int32_t cap, int32_t* traj_len);
+void host_sample(const pp_handle* h, const double* center, uint64_t t, int restart, int iter,
+                 int cand, double* out, int len = -1);
+
+}  // namespace ppcapi

@@ -1,0 +1,515 @@
+// round.cpp -- one sampling round on the device (generator -> rollout ->
+// window select, src/planner.cpp:259-336 for one restart x iteration block)
+// and the certified re-ranking of its winners in the reference's FP64
+// arithmetic (PlannerConfig::refine).
+#include "capi_internal.hpp"
+
+namespace ppcapi {
+
+// key prefix fold^4(seed, t, restart, iter) (src/rng.cpp:26-34 minus the
+// candidate fold, which the kernel applies).
+uint64_t key_prefix(uint64_t seed, uint64_t t, uint64_t r, uint64_t i) {
+  // KeyedRng's state after four folds == prefix; reuse the public class on a
+  // dummy candidate would fold a fifth time, so recompute here.
+  constexpr uint64_t G = 0x9E3779B97F4A7C15ULL;
+  auto mix = [](uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+  };
+  auto fold = [&](uint64_t hh, uint64_t f) { return mix(hh ^ (mix(f) + G + (hh << 6) + (hh >> 2))); };
+  uint64_t hh = mix(seed + G);
+  hh = fold(hh, t);
+  hh = fold(hh, r);
+  hh = fold(hh, i);
+  return hh;
+}
+
+constexpr int ppdev_warps() { return 4; }  // warps per CTA (rollout.cuh kBlock / 32)
+
+// Windows up to this size are re-evaluated on the host pool (exact FP64
+// rollouts, 16 workers); wider ones get the FP64 device kernel first.
+int host_max() {
+  static const int v = [] {
+    const char* e = std::getenv("PARAPLAN_HOST_MAX");
+    return e != nullptr ? std::atoi(e) : 1024;
+  }();
+  return v;
+}
+
+// Occupancy of the rollout kernel for (precision, staged field size, grid
+// mode), queried once per handle.
+ppdev::LaunchShape launch_shape(pp_handle* h, bool fp64, int field_smem, int grid_mode) {
+  const int64_t key = (static_cast<int64_t>(field_smem) << 8) | (grid_mode << 1) | (fp64 ? 1 : 0);
+  auto found = h->shapes.find(key);
+  if (found == h->shapes.end()) {
+    ppdev::LaunchShape sh{};
+    const int rcode = fp64 ? ppdev::shape_f64(h->kind, h->device, field_smem, grid_mode, &sh)
+                           : ppdev::shape_f32(h->kind, h->device, field_smem, grid_mode, &sh);
+    ck(static_cast<cudaError_t>(rcode), "occupancy query");
+    found = h->shapes.emplace(key, sh).first;
+  }
+  return found->second;
+}
+
+void consume_pending_field(pp_handle* h, bool side) {
+  std::function<void()> f = std::move(h->pending_field);
+  h->pending_field = nullptr;
+  h->field_via_side = side;
+  h->field_event = false;
+  try {
+    f();
+  } catch (...) {
+    h->field_via_side = false;
+    throw;
+  }
+  h->field_via_side = false;
+  if (h->field_event) {
+    ck(cudaStreamWaitEvent(h->stream, h->ev_field, 0), "field wait");
+    h->field_event = false;
+  }
+  phase("field");
+}
+
+// One sampling round on the device: restarts [r0, r0+rc), candidates
+// [c0, c1) of each, iteration `iter`, centred on `center` (or injected theta).
+// With re-ranking on, the round is followed by the near-tie window select,
+// the FP64 re-evaluation of the window and a host re-rank of FP64 near-ties
+// in the reference's own arithmetic, so the winner is the reference's.
+void run_round_launch(pp_handle* h, uint64_t t, int iter, int r0, int rc, const double* center,
+                      int64_t c0, int64_t c1, const double* injected, pp_record* out,
+                      pp_rollout_stats* per_sample, bool force_fp64) {
+  const int64_t count = c1 - c0;
+  const bool fp64 = h->fp64 || force_fp64;
+  const bool rerank = h->rerank && h->snapshot != nullptr;
+  // the schedule (refill: generator + rollout) and the theta record width do
+  // not depend on the field
+  const ppdev::LaunchShape shape0 = launch_shape(h, fp64, 0, 0);
+  // a pending field is binned while the generator runs; without a generator
+  // (lockstep) or for an FP64 redo it is needed now
+  if (h->pending_field && (!shape0.refill || force_fp64)) consume_pending_field(h);
+  ppdev::RoundArgs a = h->base;
+  if (force_fp64 && !h->fp64) {
+    a.field = ensure_field64(h);
+    a.lay = a.lay64;
+  }
+  a.restart_count = rc;
+  a.cand_begin = c0;
+  a.count = count;
+  a.queue_bytes = 0;
+
+  // params block: [prefix u64 x rc][center f64 x P]
+  const size_t pbytes = sizeof(uint64_t) * rc + sizeof(double) * h->P;
+  h->h_params.reserve(pbytes, "pinned params");
+  h->d_params.reserve(pbytes, "device params");
+  uint64_t* hp = static_cast<uint64_t*>(h->h_params.p);
+  for (int r = 0; r < rc; ++r) {
+    hp[r] = key_prefix(h->cfg.master_seed, t, static_cast<uint64_t>(r0 + r),
+                       static_cast<uint64_t>(iter));
+  }
+  double* hc = reinterpret_cast<double*>(hp + rc);
+  if (center != nullptr) {
+    std::memcpy(hc, center, sizeof(double) * h->P);
+  } else {
+    std::fill(hc, hc + h->P, 0.0);
+  }
+  ck(cudaMemcpyAsync(h->d_params.p, h->h_params.p, pbytes, cudaMemcpyHostToDevice, h->stream),
+     "params H2D");
+  h->timing.h2d_bytes += static_cast<int64_t>(pbytes);
+  a.key_prefix = static_cast<const uint64_t*>(h->d_params.p);
+  a.center = reinterpret_cast<const double*>(static_cast<uint64_t*>(h->d_params.p) + rc);
+
+  if (injected != nullptr) {
+    const size_t ib = sizeof(double) * h->P * static_cast<size_t>(count);
+    h->d_injected.reserve(ib, "device theta");
+    ck(cudaMemcpyAsync(h->d_injected.p, injected, ib, cudaMemcpyHostToDevice, h->stream),
+       "theta H2D");
+    h->timing.h2d_bytes += static_cast<int64_t>(ib);
+    a.injected = static_cast<const double*>(h->d_injected.p);
+  }
+
+  // the round block: counters, work counters, per-restart winners and the
+  // selected window, copied back together
+  char* dres = static_cast<char*>(h->d_round.p);
+  a.counters = reinterpret_cast<uint32_t*>(dres);
+  a.exec = reinterpret_cast<unsigned long long*>(dres + kExecOff);
+  a.out = reinterpret_cast<ppdev::Rec*>(dres + kRecOff);
+  const size_t rbytes = rerank ? kSelOff + sizeof(int64_t) * kSelFirst
+                               : kRecOff + sizeof(ppdev::Rec) * rc;
+  if (per_sample != nullptr) {
+    h->d_samples.reserve(sizeof(ppdev::SampleOut) * rc * static_cast<size_t>(count),
+                         "per-sample buffer");
+    a.per_sample = static_cast<ppdev::SampleOut*>(h->d_samples.p);
+  }
+  const size_t total = static_cast<size_t>(count) * rc;
+  if (shape0.refill) {
+    const size_t esz = fp64 ? sizeof(double) : sizeof(float);
+    h->d_theta.reserve(total * shape0.theta_elem * esz, "theta buffer");
+    a.theta_buf = h->d_theta.p;  // [total][theta_elem]: theta, first action, pad
+    a.first_buf = nullptr;
+  }
+  // several restarts on the refill schedule: winners from the sample keys
+  const bool keys_only = shape0.refill && rc > 1;
+  a.keys_only = keys_only ? 1 : 0;
+  a.out_free = keys_only && rerank ? reinterpret_cast<ppdev::Rec*>(dres + kFreeOff) : nullptr;
+  if (rerank || keys_only) {
+    h->d_skeys.reserve(total * (fp64 ? sizeof(ppdev::SKey) : sizeof(ppdev::SKey32)), "sample keys");
+    a.skeys = h->d_skeys.p;
+    a.skey32 = fp64 ? 0 : 1;
+  }
+  if (rerank) {
+    h->d_sel.reserve(kSelCap * sizeof(ppdev::SelRec), "selection");
+    a.sel_out = static_cast<ppdev::SelRec*>(h->d_sel.p);
+    a.sel_list = reinterpret_cast<int64_t*>(dres + kSelOff);
+    a.sel_cap = kSelCap;
+    a.refine_grid = kRefineGrid;
+    a.sel_rho = fp64 ? 1e-11 : h->sel_rho;
+    a.sel_alpha = fp64 ? 1e-13 : 1e-6;
+  }
+
+  ck(cudaEventRecord(h->ev0, h->stream), "event");
+  ck(static_cast<cudaError_t>(fp64 ? ppdev::launch_generate_f64(h->kind, a, h->stream)
+                                   : ppdev::launch_generate_f32(h->kind, a, h->stream)),
+     "theta generator launch");
+  if (h->pending_field) {  // bin + upload the field while the generator runs
+    consume_pending_field(h, true);
+    const ppdev::RoundArgs& b = h->base;
+    a.field = b.field;
+    a.field64 = b.field64;
+    a.n_points = b.n_points;
+    a.field_ns = b.field_ns;
+    a.field_nd = b.field_nd;
+    a.grid_nx = b.grid_nx;
+    a.grid_ny = b.grid_ny;
+    a.grid_mode = b.grid_mode;
+    a.grid_x0 = b.grid_x0;
+    a.grid_y0 = b.grid_y0;
+    a.grid_g = b.grid_g;
+    a.lay = b.lay;
+    a.lay64 = b.lay64;
+    a.kf = b.kf;
+    a.kd = b.kd;
+  }
+  const int field_smem = (force_fp64 && !h->fp64) ? 0 : h->field_smem_bytes;
+  const ppdev::LaunchShape shape = launch_shape(h, fp64, field_smem, a.grid_mode);
+  // refill: 32-candidate batches; lockstep: one tile of `block` candidates
+  const int unit = shape.refill ? 32 : shape.block;
+  const int64_t tpr64 = (count + unit - 1) / unit;
+  if (tpr64 * rc > (int64_t{1} << 30)) throw std::invalid_argument("sampling round too large");
+  a.tiles_per_restart = static_cast<int32_t>(tpr64);
+  a.n_tiles = static_cast<int32_t>(tpr64 * rc);
+  a.block = shape.block;
+  a.grid = std::max(1, std::min(shape.grid, shape.refill ? (a.n_tiles + ppdev_warps() - 1) /
+                                                               ppdev_warps()
+                                                         : a.n_tiles));
+  a.field_smem_bytes = field_smem;
+  // tile records (x2 for keys_only: best and best unflagged)
+  const size_t n_recs = shape.refill ? 2 * static_cast<size_t>(rc) * std::max(a.grid, 148 * 4)
+                                    : static_cast<size_t>(a.n_tiles);
+  h->d_tiles.reserve(sizeof(ppdev::Rec) * n_recs, "tile records");
+  a.tile_recs = static_cast<ppdev::Rec*>(h->d_tiles.p);
+  // theta in a global per-lane column (NetGlobal): any architecture without
+  // a register specialisation in this precision ([5,10,10,2] has one in FP32)
+  const bool generic = h->kind == ppdev::NetKind::kGeneric ||
+                       (fp64 && h->kind == ppdev::NetKind::k5_10_10_2);
+  if (generic || rerank) {
+    const size_t lanes = std::max<size_t>(generic ? static_cast<size_t>(a.grid) * a.block : 0,
+                                          rerank ? kRefineGrid * 128 : 0);
+    h->d_scratch.reserve(lanes * h->P * sizeof(double), "theta scratch");
+    a.theta_scratch = static_cast<float*>(h->d_scratch.p);
+    a.theta_scratch64 = static_cast<double*>(h->d_scratch.p);
+  }
+  ck(static_cast<cudaError_t>(fp64 ? ppdev::launch_rollout_f64(h->kind, a, h->stream)
+                                   : ppdev::launch_rollout_f32(h->kind, a, h->stream)),
+     "sampling kernel launch");
+  if (rerank) {
+    // the selection counter was re-armed by the rollout kernel's last CTA
+    ck(static_cast<cudaError_t>(ppdev::launch_select(a, h->stream)), "window select launch");
+    if (!h->pool) {
+      const unsigned hc = std::thread::hardware_concurrency();
+      h->pool = std::make_unique<HostPool>(static_cast<int>(std::min(16u, std::max(1u, hc))));
+    }
+    h->pool->prewarm();  // workers spin while the GPU samples
+  }
+  ck(cudaEventRecord(h->ev1, h->stream), "event");
+  // one D2H: counters (selection count), work counters, winners and the
+  // first kSelFirst selected indices
+  ck(cudaMemcpyAsync(h->h_round.p, h->d_round.p, rbytes, cudaMemcpyDeviceToHost, h->stream),
+     "result D2H");
+  phase("enqueued");
+  // the host's exact image of device-binned movers, while the round runs
+  if (h->field.dyn_deferred) {
+    ppfield::bin_dynamic(h->field);
+    phase("host-binned");
+  }
+  uint32_t n_sel = 0;
+  h->timing.d2h_bytes += static_cast<int64_t>(rbytes);
+  if (per_sample != nullptr) {
+    const size_t sb = sizeof(ppdev::SampleOut) * rc * static_cast<size_t>(count);
+    ck(cudaMemcpyAsync(per_sample, h->d_samples.p, sb, cudaMemcpyDeviceToHost, h->stream),
+       "per-sample D2H");
+    h->timing.d2h_bytes += static_cast<int64_t>(sb);
+  }
+  ck(cudaStreamSynchronize(h->stream), "sampling kernel");
+  phase("synced");
+  float ms = 0.f;
+  ck(cudaEventElapsedTime(&ms, h->ev0, h->ev1), "event timing");
+  h->timing.kernel_ms += ms;
+  h->timing.launches += (shape.refill ? 2 : 1) + (rerank ? 1 : 0) + (keys_only ? 1 : 0);
+  h->timing.samples += count * rc;
+  const char* hres = static_cast<const char*>(h->h_round.p);
+  const unsigned long long* ex = reinterpret_cast<const unsigned long long*>(hres + kExecOff);
+  h->timing.executed_steps += static_cast<int64_t>(ex[2]);
+  h->timing.checked_states += static_cast<int64_t>(ex[3]);
+  const ppdev::Rec* recs = reinterpret_cast<const ppdev::Rec*>(hres + kRecOff);
+  for (int r = 0; r < rc; ++r) {
+    out[r].cls = recs[r].cls;
+    out[r].candidate = recs[r].cand;
+    out[r].restart = r0 + r;
+    out[r].iter = iter;
+    out[r].k1 = recs[r].k1;
+    out[r].k2 = recs[r].k2;
+  }
+  if (!rerank) return;
+
+  n_sel = reinterpret_cast<const uint32_t*>(hres)[2];
+  const auto c_t0 = std::chrono::steady_clock::now();
+  certify_round(h, a, t, iter, r0, rc, center, c0, c1, injected, out, fp64, n_sel);
+  phase("certified");
+  h->timing.certify_ms +=
+      std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - c_t0).count();
+}
+
+// Certified re-ranking (PlannerConfig::refine). The FP32 keys are trusted
+// only up to a relative error rho/2 (+ alpha/2), and discrete verdicts that
+// rounding could flip toward a BETTER outcome are flagged by the kernel and
+// always selected; flips toward a worse outcome only hurt the candidate
+// itself. Each pass evaluates the window's new members in the reference's
+// own FP64 arithmetic on the host (the device FP64 kernel first when the
+// window is wide) and certifies a restart when its exact best beats every
+// unselected candidate's optimistic bound; otherwise the window widens.
+// Windows that overflow, or restarts still uncertified after the last pass,
+// are redone as an FP64 round.
+void certify_round(pp_handle* h, ppdev::RoundArgs& a, uint64_t t, int iter, int r0, int rc,
+                   const double* center, int64_t c0, int64_t c1, const double* injected,
+                   pp_record* out, bool fp64, uint32_t n_sel) {
+  const int64_t count = c1 - c0;
+  const pp_snapshot& snap = *h->snapshot;
+  std::vector<double> ctr(h->P, 0.0);
+  if (center != nullptr) ctr.assign(center, center + h->P);
+  struct Exact {
+    int cls;
+    int t_goal;
+    double cost;  // terminal cost (cls 0/1) or path length (cls 2)
+    double k1, k2;
+  };
+  std::unordered_map<int64_t, Exact> known;
+  auto exact_of = [&](int64_t s) {  // the reference's own FP64 arithmetic
+    const int r = static_cast<int>(s / count);
+    const int cand = static_cast<int>(c0 + (s - r * count));
+    std::vector<double> theta(h->P);
+    if (injected != nullptr) {
+      std::memcpy(theta.data(), injected + static_cast<size_t>(cand - c0) * h->P,
+                  sizeof(double) * h->P);
+    } else {
+      host_sample(h, ctr.data(), t, r0 + r, iter, cand, theta.data(), -1);
+    }
+    pp_rollout_stats st{};
+    host_rollout(h, snap, theta.data(), &st, nullptr, 0, nullptr);
+    Exact e;
+    e.cls = st.collided ? 0 : (st.reached ? 2 : 1);
+    e.t_goal = st.t_goal;
+    e.cost = e.cls == 2 ? st.path_length : st.terminal_cost;
+    e.k1 = e.cls == 2 ? -static_cast<double>(st.t_goal) : -st.terminal_cost;
+    e.k2 = e.cls == 2 ? -st.path_length : 0.0;
+    return e;
+  };
+  if (!h->pool) {
+    const unsigned hc = std::thread::hardware_concurrency();
+    h->pool = std::make_unique<HostPool>(static_cast<int>(std::min(16u, std::max(1u, hc))));
+  }
+  const double rho = a.sel_rho, alpha = a.sel_alpha;
+  std::vector<ppdev::SelBound> bound(rc);
+  // the first window is built around each restart's best unflagged
+  // candidate when the round reports it (keys_only), else its winner
+  const ppdev::Rec* free_recs =
+      a.out_free != nullptr
+          ? reinterpret_cast<const ppdev::Rec*>(static_cast<const char*>(h->h_round.p) + kFreeOff)
+          : nullptr;
+  for (int r = 0; r < rc; ++r) {
+    pp_record o = out[r];
+    if (free_recs != nullptr && free_recs[r].cls >= 0) {
+      o.cls = free_recs[r].cls;
+      o.k1 = free_recs[r].k1;
+      o.k2 = free_recs[r].k2;
+    }
+    bound[r].cls = o.cls;
+    bound[r].t_goal = o.cls == 2 ? static_cast<int>(-o.k1) : 0;
+    bound[r].thr = (o.cls == 2 ? -o.k2 : -o.k1) * (1.0 + rho) + alpha;
+  }
+  std::vector<char> certified(rc, 0);
+  std::vector<int64_t> list;
+  constexpr int kPasses = 6;
+  for (int pass = 0; pass < kPasses; ++pass) {
+    if (pass > 0) {  // widened select over the uncertified restarts
+      h->d_bound.reserve(sizeof(ppdev::SelBound) * rc, "window bounds");
+      h->h_bound.reserve(sizeof(ppdev::SelBound) * rc, "pinned bounds");
+      std::memcpy(h->h_bound.p, bound.data(), sizeof(ppdev::SelBound) * rc);
+      ck(cudaMemcpyAsync(h->d_bound.p, h->h_bound.p, sizeof(ppdev::SelBound) * rc,
+                         cudaMemcpyHostToDevice, h->stream),
+         "bounds H2D");
+      a.sel_bound = static_cast<const ppdev::SelBound*>(h->d_bound.p);
+      ck(cudaMemsetAsync(a.counters + 2, 0, sizeof(uint32_t), h->stream), "selection counter");
+      ck(static_cast<cudaError_t>(ppdev::launch_select(a, h->stream)), "window select launch");
+      ck(cudaMemcpyAsync(h->h_round.p, h->d_round.p, kSelOff + sizeof(int64_t) * kSelFirst,
+                         cudaMemcpyDeviceToHost, h->stream),
+         "selection D2H");
+      ck(cudaStreamSynchronize(h->stream), "window select");
+      h->timing.launches += 1;
+      n_sel = static_cast<const uint32_t*>(h->h_round.p)[2];
+    }
+    if (n_sel > static_cast<uint32_t>(kSelCap)) {
+      if (trace_on()) {
+        std::fprintf(stderr, "[paraplan] t=%llu iter=%d pass=%d selected=%u: window overflow\n",
+                     static_cast<unsigned long long>(t), iter, pass, n_sel);
+      }
+      break;
+    }
+    if (n_sel > static_cast<uint32_t>(kSelFirst)) {
+      ck(cudaMemcpy(reinterpret_cast<int64_t*>(static_cast<char*>(h->h_round.p) + kSelOff) + kSelFirst,
+                    a.sel_list + kSelFirst, sizeof(int64_t) * (n_sel - kSelFirst),
+                    cudaMemcpyDeviceToHost),
+         "selection D2H");
+    }
+    const int64_t* sl =
+        reinterpret_cast<const int64_t*>(static_cast<const char*>(h->h_round.p) + kSelOff);
+    list.clear();
+    for (uint32_t i = 0; i < n_sel; ++i) {
+      if (known.find(sl[i]) == known.end()) list.push_back(sl[i]);
+    }
+    std::sort(list.begin(), list.end());
+    list.erase(std::unique(list.begin(), list.end()), list.end());
+    h->timing.refined += static_cast<int32_t>(list.size());
+    std::vector<Exact> got(list.size());
+    if (list.size() <= static_cast<size_t>(host_max())) {
+      h->pool->run(static_cast<int>(list.size()), [&](int i) { got[i] = exact_of(list[i]); });
+    } else {
+      // wide window: FP64 keys from the device, exact host keys for the FP64
+      // near-ties of each restart's best
+      ck(cudaMemcpyAsync(a.sel_list, list.data(), sizeof(int64_t) * list.size(),
+                         cudaMemcpyHostToDevice, h->stream),
+         "refine list H2D");
+      const uint32_t n_list = static_cast<uint32_t>(list.size());
+      ck(cudaMemcpyAsync(a.counters + 2, &n_list, sizeof(uint32_t), cudaMemcpyHostToDevice,
+                         h->stream),
+         "refine count H2D");
+      a.field64 = ensure_field64(h);
+      ck(static_cast<cudaError_t>(ppdev::launch_refine(h->kind, a, h->stream)), "refine launch");
+      std::vector<ppdev::SelRec> dev(list.size());
+      ck(cudaMemcpyAsync(dev.data(), a.sel_out, sizeof(ppdev::SelRec) * list.size(),
+                         cudaMemcpyDeviceToHost, h->stream),
+         "refine D2H");
+      ck(cudaStreamSynchronize(h->stream), "refine kernel");
+      h->timing.launches += 1;
+      std::vector<int> best(rc, -1);
+      for (size_t i = 0; i < dev.size(); ++i) {
+        got[i] = Exact{dev[i].cls, dev[i].cls == 2 ? static_cast<int>(-dev[i].k1) : -1,
+                       dev[i].cls == 2 ? -dev[i].k2 : -dev[i].k1, dev[i].k1, dev[i].k2};
+        const int r = dev[i].restart;
+        if (best[r] < 0 || key_better({got[i].cls, got[i].k1, got[i].k2},
+                                      {got[best[r]].cls, got[best[r]].k1, got[best[r]].k2})) {
+          best[r] = static_cast<int>(i);
+        }
+      }
+      std::vector<int> ties;
+      for (size_t i = 0; i < dev.size(); ++i) {
+        const Exact& b = got[best[dev[i].restart]];
+        const double tol = 1e-12;
+        if (got[i].cls == b.cls && std::abs(got[i].k1 - b.k1) <= tol * std::max(1.0, std::abs(b.k1)) &&
+            std::abs(got[i].k2 - b.k2) <= tol * std::max(1.0, std::abs(b.k2))) {
+          ties.push_back(static_cast<int>(i));
+        }
+      }
+      h->pool->run(static_cast<int>(ties.size()),
+                   [&](int j) { got[ties[j]] = exact_of(list[ties[j]]); });
+    }
+    for (size_t i = 0; i < list.size(); ++i) known[list[i]] = got[i];
+
+    // certify or widen each uncertified restart
+    bool all = true;
+    for (int r = 0; r < rc; ++r) {
+      if (certified[r]) continue;
+      const ppdev::SelBound& bd = bound[r];
+      int64_t win = -1;
+      const Exact* e = nullptr;
+      for (const auto& kv : known) {
+        if (kv.first / count != r) continue;
+        const Exact& q = kv.second;
+        if (e == nullptr || key_better({q.cls, q.k1, q.k2}, {e->cls, e->k1, e->k2}) ||
+            (q.cls == e->cls && q.k1 == e->k1 && q.k2 == e->k2 && kv.first < win)) {
+          e = &q;
+          win = kv.first;
+        }
+      }
+      const double slack = 0.5 * (rho * bd.thr + alpha);
+      bool ok = false;
+      if (e != nullptr) {
+        if (e->cls > bd.cls) {
+          ok = true;  // only a flagged (always selected) candidate can rise a class
+        } else if (e->cls == bd.cls) {
+          ok = (bd.cls == 2 && e->t_goal < bd.t_goal) ||
+               ((bd.cls != 2 || e->t_goal == bd.t_goal) && e->cost <= bd.thr - slack);
+        }
+      }
+      if (ok) {
+        certified[r] = 1;
+        out[r].cls = e->cls;
+        out[r].candidate = static_cast<int>(c0 + (win - r * count));
+        out[r].k1 = e->k1;
+        out[r].k2 = e->k2;
+        bound[r].cls = -1;  // select nothing more for this restart
+        continue;
+      }
+      all = false;
+      if (trace_level() >= 2) {
+        std::fprintf(stderr,
+                     "[paraplan]   restart %d open: window cls %d t_goal %d thr %.9g slack %.3g; "
+                     "exact best cls %d t_goal %d cost %.9g\n",
+                     r0 + r, bd.cls, bd.t_goal, bd.thr, slack, e ? e->cls : -9,
+                     e ? e->t_goal : -9, e ? e->cost : 0.0);
+      }
+      const bool same = e != nullptr && e->cls == bd.cls && (bd.cls != 2 || e->t_goal == bd.t_goal);
+      const double widened = bd.thr * 1.25 + alpha;
+      bound[r].thr = same ? std::max(e->cost * (1.0 + rho) + alpha, widened) : widened;
+    }
+    if (trace_on()) {
+      std::fprintf(stderr, "[paraplan] t=%llu iter=%d pass=%d selected=%u new=%zu certified=%s\n",
+                   static_cast<unsigned long long>(t), iter, pass, n_sel, list.size(),
+                   all ? "all" : "no");
+    }
+    if (all) return;
+  }
+  // overflowed or not certified: redo the round in FP64
+  if (trace_on()) {
+    std::fprintf(stderr, "[paraplan] t=%llu iter=%d: FP64 fallback round\n",
+                 static_cast<unsigned long long>(t), iter);
+  }
+  if (fp64) throw std::runtime_error("near-tie re-ranking could not certify an FP64 round");
+  h->timing.refined = -1;
+  run_round_launch(h, t, iter, r0, rc, center, c0, c1, injected, out, nullptr, true);
+}
+
+void run_round(pp_handle* h, uint64_t t, int iter, int r0, int rc, const double* center,
+               int64_t c0, int64_t c1, const double* injected, pp_record* out,
+               pp_rollout_stats* per_sample) {
+  if (!h->snap_valid) throw std::invalid_argument("no snapshot uploaded");
+  if (rc < 1 || c1 < c0) throw std::invalid_argument("empty sampling round");
+  // the refill kernel keeps per-restart tables in shared memory: chunk
+  for (int done = 0; done < rc; done += ppdev::kMaxRestartsPerLaunch) {
+    const int n = std::min(ppdev::kMaxRestartsPerLaunch, rc - done);
+    run_round_launch(h, t, iter, r0 + done, n, center, c0, c1, injected, out + done,
+                     per_sample == nullptr ? nullptr : per_sample + done * (c1 - c0));
+  }
+}
+
+}  // namespace ppcapi
