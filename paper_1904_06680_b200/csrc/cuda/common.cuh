@@ -1,0 +1,161 @@
+// common.cuh -- constants, the keyed SplitMix64 stream (src/rng.cpp), FP32/FP64 math
+// helpers of the rollout (accurate sincos/tan/wrap kernels), round constants.
+// Part of the sampler kernels (rollout.cuh).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstdlib>
+#include <cstring>
+#include <type_traits>
+
+#include "device_api.h"
+
+namespace ppdev {
+
+constexpr uint64_t kGamma = 0x9E3779B97F4A7C15ull;
+constexpr double kPi = 3.141592653589793;
+constexpr double kTwoPi = 6.283185307179586;
+constexpr unsigned kFull = 0xffffffffu;
+constexpr int kBlock = 128;
+constexpr int kWarps = kBlock / 32;
+#ifndef PARAPLAN_COLL_EXIT
+#define PARAPLAN_COLL_EXIT 1
+#endif
+#ifndef PARAPLAN_REFILL_MINB
+#define PARAPLAN_REFILL_MINB 6  // <= 85 registers: 6 CTAs (24 warps) per SM, no spills
+#endif
+
+// src/rng.cpp:11-18
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+// src/rng.cpp:20-22
+__device__ __forceinline__ uint64_t fold(uint64_t h, uint64_t f) {
+  return mix64(h ^ (mix64(f) + kGamma + (h << 6) + (h >> 2)));
+}
+__device__ __forceinline__ double unit53(uint64_t x) {
+  return static_cast<double>(x >> 11) * 0x1.0p-53;
+}
+
+// Counter-based view of KeyedRng: draw k of key h is mix64(h + (k+1) gamma).
+struct Stream {
+  uint64_t s;
+  __device__ __forceinline__ uint64_t next() {
+    s += kGamma;
+    return mix64(s);
+  }
+};
+
+template <typename Real>
+struct Vec2T;
+template <>
+struct Vec2T<float> {
+  using type = float2;
+};
+template <>
+struct Vec2T<double> {
+  using type = double2;
+};
+
+// --------------------------------------------------------------- math ----
+template <typename Real>
+struct M;
+
+// FP32 sin/cos kernels on [-pi/4, pi/4] (minimax, ~1 ulp; Cephes-style
+// coefficients) and the quadrant reduction used by the FP32 rollout.
+__device__ __forceinline__ float sin_poly(float r) {
+  const float r2 = r * r;
+  float p = fmaf(r2, -1.9515295891e-4f, 8.3321608736e-3f);
+  p = fmaf(r2, p, -1.6666654611e-1f);
+  return fmaf(r * r2, p, r);
+}
+__device__ __forceinline__ float cos_poly(float r) {
+  const float r2 = r * r;
+  float p = fmaf(r2, 2.443315711809948e-5f, -1.388731625493765e-3f);
+  p = fmaf(r2, p, 4.166664568298827e-2f);
+  return fmaf(r2 * r2, p, fmaf(-0.5f, r2, 1.0f));
+}
+// sincos for the rollout's headings (|x| well below 2^7 * pi/2, where the
+// three-part pi/2 products stay exact).
+__device__ __forceinline__ void fast_sincosf(float x, float* s, float* c) {
+  const float q = rintf(x * 0.636619772367581343f);
+  float r = fmaf(-q, 1.5703125f, x);
+  r = fmaf(-q, 4.837512969970703125e-4f, r);
+  r = fmaf(-q, 7.54978995489188216e-8f, r);
+  const float sp = sin_poly(r), cp = cos_poly(r);
+  const int qi = static_cast<int>(q);
+  const bool swap = (qi & 1) != 0;
+  float sv = swap ? cp : sp;
+  float cv = swap ? sp : cp;
+  sv = (qi & 2) ? -sv : sv;
+  cv = ((qi + 1) & 2) ? -cv : cv;
+  *s = sv;
+  *c = cv;
+}
+
+template <>
+struct M<float> {
+  static __device__ __forceinline__ float th(float x) { return tanhf(x); }
+  static __device__ __forceinline__ float tn(float x) { return tanf(x); }
+  // tan for |x| <= pi/4 (the steering range when delta_max <= pi/4)
+  static __device__ __forceinline__ float tn_small(float x) {
+    return sin_poly(x) * __frcp_rn(cos_poly(x));
+  }
+  static __device__ __forceinline__ void sc(float x, float* s, float* c) {
+    fast_sincosf(x, s, c);
+  }
+  static __device__ __forceinline__ float sq(float x) { return sqrtf(x); }
+  static __device__ __forceinline__ float ab(float x) { return fabsf(x); }
+  // wrap_angle (src/geometry.cpp:9-13): remainder by 2*pi (two-part
+  // Cody-Waite), lower boundary folded onto +pi.
+  static __device__ __forceinline__ float wrap(float a) {
+    const float n = rintf(a * 0.15915494309189535f);
+    float r = fmaf(-n, 6.28318548202514648f, a);
+    r = fmaf(-n, -1.7484555314695172e-07f, r);
+    return r <= -3.14159274101257324f ? r + 6.28318548202514648f : r;
+  }
+  static __device__ __forceinline__ float ndiv(float a, double, float inv) { return a * inv; }
+};
+
+template <>
+struct M<double> {
+  static __device__ __forceinline__ double th(double x) { return tanh(x); }
+  static __device__ __forceinline__ double tn(double x) { return tan(x); }
+  static __device__ __forceinline__ double tn_small(double x) { return tan(x); }
+  static __device__ __forceinline__ void sc(double x, double* s, double* c) { sincos(x, s, c); }
+  static __device__ __forceinline__ double sq(double x) { return sqrt(x); }
+  static __device__ __forceinline__ double ab(double x) { return fabs(x); }
+  static __device__ __forceinline__ double wrap(double a) {
+    const double r = remainder(a, kTwoPi);  // exact, identical to glibc
+    return r <= -kPi ? r + kTwoPi : r;
+  }
+  // true division, as the reference (src/planner.cpp:117-120, 186-189)
+  static __device__ __forceinline__ double ndiv(double a, double d, double) { return a / d; }
+};
+
+template <typename Real>
+__device__ __forceinline__ Real clampr(Real v, Real lo, Real hi) {
+  return v < lo ? lo : (hi < v ? hi : v);  // std::clamp
+}
+
+// Round constants live in the kernel parameter bank (RoundArgs::kf / kd).
+template <typename Real>
+using Consts = ConstsT<Real>;
+
+template <typename Real>
+__device__ __forceinline__ const Consts<Real>& consts_of(const RoundArgs& a);
+template <>
+__device__ __forceinline__ const Consts<float>& consts_of<float>(const RoundArgs& a) {
+  return a.kf;
+}
+template <>
+__device__ __forceinline__ const Consts<double>& consts_of<double>(const RoundArgs& a) {
+  return a.kd;
+}
+
+}  // namespace ppdev

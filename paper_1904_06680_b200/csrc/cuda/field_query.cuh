@@ -1,0 +1,220 @@
+// field_query.cuh -- the binned obstacle field on the device and the collision query
+// (src/geometry.cpp:63-76) over the cells under the chassis bounding box.
+// Part of the sampler kernels (rollout.cuh).
+#pragma once
+
+#include "common.cuh"
+
+namespace ppdev {
+
+// Binned obstacle field (csrc/capi/field.hpp): static points stored once,
+// dynamic points once per state row, both in cell order of one uniform grid
+// (cell size g, origin bx0/by0); starts[cell] = first point of the cell.
+// With ncy == 1 the grid is a row of x-buckets.
+template <typename Real>
+struct Field {
+  const typename Vec2T<Real>::type* spts;
+  const typename Vec2T<Real>::type* dpts;
+  const int* sst;
+  const int* dst;
+  const typename Vec2T<Real>::type* sbox;  // per cell: (centre), (half extents)
+  int Ns, Nd;
+  int ncx, ncy;
+};
+
+template <typename Real>
+__device__ __forceinline__ Field<Real> field_at(const RoundArgs& a, const void* base,
+                                                const FieldLayout& l) {
+  using R2 = typename Vec2T<Real>::type;
+  const unsigned char* p = static_cast<const unsigned char*>(base);
+  return Field<Real>{reinterpret_cast<const R2*>(p), reinterpret_cast<const R2*>(p + l.dpts),
+                     reinterpret_cast<const int*>(p + l.sst),
+                     reinterpret_cast<const int*>(p + l.dst),
+                     reinterpret_cast<const R2*>(p + l.sbox), a.field_ns, a.field_nd, a.grid_nx,
+                     a.grid_ny};
+}
+
+// Inside-margin of one point against the chassis at (x, y, phi):
+// min(r2 - d2, fe - bx, re + bx, hw - by, hw + by) in the reference's own
+// expressions (src/geometry.cpp:63-76): > 0 iff the reference reports the
+// point inside (each difference has the exact sign of its comparison).
+template <typename Real>
+__device__ __forceinline__ Real point_margin(const Consts<Real>& K, Real x, Real y, Real c, Real s,
+                                             Real kx, Real ky, Real mx, Real my) {
+  const Real dx = mx - x, dy = my - y;
+  const Real bx = c * dx + s * dy;
+  const Real by = -s * dx + c * dy;
+  const Real pre = K.r2 - (dx * dx + dy * dy);
+  const Real box = fmin(fmin(K.fe - bx, K.re + bx), fmin(K.hw - by, K.hw + by));
+  return fmin(pre, box);
+}
+// FP32: the point in the vehicle frame via the pre-rotated vehicle position
+// (kx, ky include the rectangle centre offset), the rectangle tested around
+// its centre and no separate circle prefilter (the rectangle lies inside the
+// bounding circle; the prefilter can only matter at the rear corners within
+// rounding -- a narrow hit, which the marginal flag sends to the exact
+// re-ranking).
+template <>
+__device__ __forceinline__ float point_margin<float>(const Consts<float>& K, float, float,
+                                                     float c, float s, float kx, float ky,
+                                                     float mx, float my) {
+  const float bx = fmaf(c, mx, fmaf(s, my, -kx));
+  const float by = fmaf(-s, mx, fmaf(c, my, -ky));
+  return fminf(K.bhx - fabsf(bx), K.hw - fabsf(by));
+}
+
+// Collision of the chassis at (x, y, phi) with row h. Only the grid cells
+// covering [x - qpad, x + qpad] x [y - qpad, y + qpad] are visited: every
+// point outside them is farther than cull > r from the vehicle and fails the
+// reference's bounding-circle prefilter (src/geometry.cpp:71). Returns the
+// inside-margin max over visited points (the reference reports a collision
+// iff it is > 0; a small |margin| marks a verdict rounding could flip).
+// A lane stops at its first robust hit (margin >= stop). Warp-synchronous:
+// all 32 lanes call it, every loop is warp-uniform.
+// Points of one part (static, or the dynamic row of state h) in the cells
+// covering the query window; updates the inside-margin `best`.
+template <typename Real, int kGrid>
+__device__ __forceinline__ void scan_part(const typename Vec2T<Real>::type* pts, const int* st,
+                                          int ncy, int cx_lo, int cx_hi, int cy_lo, int cy_hi,
+                                          const Consts<Real>& K, Real x, Real y, Real c, Real s,
+                                          Real kx, Real ky, Real stop, Real& best) {
+  if constexpr (kGrid == 0) {  // x-buckets: the window is one contiguous range
+    const int lo = st[cx_lo];
+    const int cnt = st[cx_hi + 1] - lo;
+    const int rounds = __reduce_max_sync(kFull, cnt);
+    for (int j = 0; j < rounds; ++j) {
+      if (j < cnt) {
+        const auto m = pts[lo + j];
+        best = fmax(best, point_margin<Real>(K, x, y, c, s, kx, ky, m.x, m.y));
+      }
+    }
+  } else {  // 2-D cells, one contiguous range per cell column; early exit
+    const int ncol = cx_hi - cx_lo + 1;
+    const int cols = __reduce_max_sync(kFull, ncol);
+    for (int k = 0; k < cols; ++k) {
+      const bool has = k < ncol;
+      const int cell = (has ? cx_lo + k : cx_lo) * ncy;
+      const int lo = st[cell + cy_lo];
+      const int cnt = has ? st[cell + cy_hi + 1] - lo : 0;
+      // a lane stops at its first robust hit (margin >= stop)
+      for (int j = 0; __any_sync(kFull, j < cnt && best < stop); ++j) {
+        if (j < cnt && best < stop) {
+          const auto m = pts[lo + j];
+          best = fmax(best, point_margin<Real>(K, x, y, c, s, kx, ky, m.x, m.y));
+        }
+      }
+    }
+  }
+}
+
+// Dense static part (grid_mode 2), column by column. A column holding more
+// than kDenseCol points in the window is visited cell by cell: a cell whose
+// tight point box is separated from the rectangle along the rectangle's own
+// axes (by more than the pad) holds no point the reference could report
+// inside, and is skipped without reading its points. Sparser columns are
+// scanned as one range, as in grid_mode 1.
+constexpr int kDenseCol = 16;
+
+template <typename Real>
+__device__ __forceinline__ void scan_boxed(const typename Vec2T<Real>::type* pts, const int* st,
+                                           const typename Vec2T<Real>::type* box, int ncy,
+                                           int cx_lo, int cx_hi, int cy_lo, int cy_hi,
+                                           const Consts<Real>& K, Real x, Real y, Real c, Real s,
+                                           Real kx, Real ky, Real stop, Real& best) {
+  const Real ac = fabs(c), as = fabs(s);
+  const int nrow = cy_hi - cy_lo + 1;
+  const int ncol = cx_hi - cx_lo + 1;
+  const int cols = __reduce_max_sync(kFull, ncol);
+  for (int k = 0; k < cols; ++k) {
+    const bool has = k < ncol;
+    const int cell0 = (has ? cx_lo + k : cx_lo) * ncy + cy_lo;
+    const int lo = st[cell0];
+    const int n = has ? st[cell0 + nrow] - lo : 0;
+    const bool dense = n > kDenseCol;
+    // dense columns: cell by cell behind the box test
+    const int rows = __reduce_max_sync(kFull, dense ? nrow : 0);
+    for (int q = 0; q < rows; ++q) {
+      int clo = 0, cnt = 0;
+      if (dense && q < nrow && best < stop) {
+        const int cell = cell0 + q;
+        clo = st[cell];
+        cnt = st[cell + 1] - clo;
+        if (cnt > 0) {
+          const auto m = box[2 * cell], e = box[2 * cell + 1];
+          const Real du = fabs(c * m.x + s * m.y - kx), dv = fabs(-s * m.x + c * m.y - ky);
+          if (du > K.bhx + e.x * ac + e.y * as + K.qpad ||
+              dv > K.hw + e.x * as + e.y * ac + K.qpad) {
+            cnt = 0;
+          }
+        }
+      }
+      for (int j = 0; __any_sync(kFull, j < cnt && best < stop); ++j) {
+        if (j < cnt && best < stop) {
+          const auto m = pts[clo + j];
+          best = fmax(best, point_margin<Real>(K, x, y, c, s, kx, ky, m.x, m.y));
+        }
+      }
+    }
+    // sparse columns: one range
+    const int cnt = dense ? 0 : n;
+    for (int j = 0; __any_sync(kFull, j < cnt && best < stop); ++j) {
+      if (j < cnt && best < stop) {
+        const auto m = pts[lo + j];
+        best = fmax(best, point_margin<Real>(K, x, y, c, s, kx, ky, m.x, m.y));
+      }
+    }
+  }
+}
+
+// Collision of the chassis at (x, y, phi) with the field at state h. Only the
+// cells covering the world-frame bounding box of the chassis rectangle (+ a
+// pad of an eighth of a cell) are visited: the reference reports a point
+// inside only if it lies strictly inside the rectangle (src/geometry.cpp:
+// 63-76), so every point outside that box is a miss whatever the rounding.
+// Returns the inside-margin max over visited points (the reference reports a
+// collision iff it is > 0; a small |margin| marks a verdict rounding could
+// flip). Warp-synchronous: all 32 lanes call it, every loop is warp-uniform.
+template <typename Real, int kGrid>
+__device__ __forceinline__ Real collide_margin(const Field<Real>& f, const Consts<Real>& K, int h,
+                                               Real x, Real y, Real c, Real s, Real stop) {
+  const int ncx = f.ncx, ncy = f.ncy;
+  const Real ac = fabs(c), as = fabs(s);
+  const Real top = Real(ncx - 1);
+  // rectangle centre (x, y) + bcx (c, s); half extents bhx |c| + hw |s| (x)
+  const Real ox = x + K.bcx * c - K.bx0;
+  const Real ex = K.bhx * ac + K.hw * as + K.qpad;
+  const int cx_lo = static_cast<int>(fmin(fmax((ox - ex) * K.binv, Real(0)), top));
+  const int cx_hi = static_cast<int>(fmin(fmax((ox + ex) * K.binv, Real(0)), top));
+  int cy_lo = 0, cy_hi = 0;
+  if constexpr (kGrid) {
+    const Real ytop = Real(ncy - 1);
+    const Real oy = y + K.bcx * s - K.by0;
+    const Real ey = K.bhx * as + K.hw * ac + K.qpad;
+    cy_lo = static_cast<int>(fmin(fmax((oy - ey) * K.binv, Real(0)), ytop));
+    cy_hi = static_cast<int>(fmin(fmax((oy + ey) * K.binv, Real(0)), ytop));
+  }
+  const Real kx = c * x + s * y + K.bcx;  // FP32 rotated-frame form only
+  const Real ky = -s * x + c * y;
+  Real best = Real(-1e30);
+  // part 0: static points; part 1: the dynamic row of state h (one copy of
+  // the scan code, warp-uniform part loop)
+#pragma unroll 1
+  for (int part = 0; part < 2; ++part) {
+    const bool dyn = part == 1;
+    if ((dyn ? f.Nd : f.Ns) == 0) continue;
+    const auto* pts = dyn ? f.dpts + static_cast<size_t>(h) * f.Nd : f.spts;
+    const int* st = dyn ? f.dst + static_cast<size_t>(h) * (ncx * ncy + 1) : f.sst;
+    if constexpr (kGrid == 2) {
+      if (!dyn) {
+        scan_boxed<Real>(pts, st, f.sbox, ncy, cx_lo, cx_hi, cy_lo, cy_hi, K, x, y, c, s, kx, ky,
+                         stop, best);
+        continue;
+      }
+    }
+    scan_part<Real, kGrid>(pts, st, ncy, cx_lo, cx_hi, cy_lo, cy_hi, K, x, y, c, s, kx, ky, stop,
+                           best);
+  }
+  return best;
+}
+
+}  // namespace ppdev

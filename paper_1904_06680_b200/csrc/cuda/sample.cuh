@@ -1,0 +1,74 @@
+// sample.cuh -- candidate theta from the keyed stream (src/planner.cpp:207-226).
+// Part of the sampler kernels (rollout.cuh).
+#pragma once
+
+#include "common.cuh"
+
+namespace ppdev {
+
+// ------------------------------------------------------------- sample ----
+// theta for candidate c of a restart (src/planner.cpp:207-226): c == 0 is the
+// centre; otherwise sigma first, then Box-Muller pairs (cos value first). The
+// stream is evaluated in FP64, then rounded to Real; `put(i, v)` stores it.
+// In injected mode row `c` of the injected matrix is used instead.
+template <typename Real, int KP, class Put>
+__device__ __forceinline__ void draw_theta(const RoundArgs& a, uint64_t prefix, int64_t c,
+                                           int Pdyn, Put&& put) {
+  const int P = KP > 0 ? KP : Pdyn;
+  const double* center = a.center;
+  if (a.injected != nullptr) {
+    const double* src = a.injected + c * P;
+#pragma unroll
+    for (int i = 0; i < P; ++i) put(i, Real(src[i]));
+    return;
+  }
+  if (c == 0) {
+#pragma unroll
+    for (int i = 0; i < P; ++i) put(i, Real(__ldg(center + i)));
+    return;
+  }
+  Stream g{fold(prefix, static_cast<uint64_t>(c))};
+  if constexpr (sizeof(Real) == sizeof(float)) {
+    // FP32 path: the integer stream is exact; the Box-Muller transform runs in
+    // float (theta agrees with the FP64 draw to a few float ulps, well inside
+    // the FP32 parity tolerance; the host regenerates the winner in FP64).
+    const float sigma =
+        exp10f(static_cast<float>(a.sig_lo + unit53(g.next()) * a.sig_span));
+#pragma unroll
+    for (int i = 0; i < P; i += 2) {
+      // float(1 - unit53) and float(unit53) straight from the integers:
+      // 1 - m 2^-53 = (2^53 - m) 2^-53 exactly, and scaling by 2^-53 commutes
+      // with rounding to float
+      const uint64_t m1 = g.next() >> 11, m2 = g.next() >> 11;
+      const float u1 = __ull2float_rn((1ull << 53) - m1) * 0x1.0p-53f;
+      const float u2 = __ull2float_rn(m2) * 0x1.0p-53f;
+      const float r = sqrtf(-2.0f * logf(u1));
+      // sincos(2 pi u2): quarter-turn reduction t = 4 u2 - q is exact
+      const float q = rintf(4.0f * u2);
+      const float t = fmaf(4.0f, u2, -q) * 1.57079632679489662f;
+      const float sp = sin_poly(t), cp = cos_poly(t);
+      const int qi = static_cast<int>(q);
+      float sn = (qi & 1) ? cp : sp;
+      float cs = (qi & 1) ? sp : cp;
+      sn = (qi & 2) ? -sn : sn;
+      cs = ((qi + 1) & 2) ? -cs : cs;
+      put(i, Real(static_cast<float>(__ldg(center + i)) + sigma * (r * cs)));
+      if (i + 1 < P) put(i + 1, Real(static_cast<float>(__ldg(center + i + 1)) + sigma * (r * sn)));
+    }
+  } else {
+    const double sigma = pow(10.0, a.sig_lo + unit53(g.next()) * a.sig_span);
+#pragma unroll
+    for (int i = 0; i < P; i += 2) {
+      const double u1 = 1.0 - unit53(g.next());
+      const double u2 = unit53(g.next());
+      const double r = sqrt(-2.0 * log(u1));
+      const double t = kTwoPi * u2;
+      double sn, cs;
+      sincos(t, &sn, &cs);
+      put(i, Real(__ldg(center + i) + sigma * (r * cs)));
+      if (i + 1 < P) put(i + 1, Real(__ldg(center + i + 1) + sigma * (r * sn)));
+    }
+  }
+}
+
+}  // namespace ppdev
