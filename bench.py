@@ -286,10 +286,12 @@ def run_b200(a):
     kern_avg_ms = sum(kern_ms) / len(kern_ms)
     flops = workloads.algorithmic_flops([5, 2, 2], N, steps_exec // a.steps, states // a.steps)
     achieved = flops / (kern_avg_ms * 1e-3) / 1e12
-    traffic = None
+    traffic, pipes = None, None
     tf = ROOT / "profiles" / "traffic.json"
     if tf.exists():
-        traffic = json.loads(tf.read_text()).get("dram_bytes_per_launch")
+        tj = json.loads(tf.read_text())
+        traffic = tj.get("dram_bytes_per_launch")
+        pipes = tj.get("pipes")
 
     out = None
     if rank == 0:
@@ -326,6 +328,7 @@ def run_b200(a):
             "roofline": {"bound": "fp32", "achieved": achieved, "peak": peak_tf,
                          "unit": "TFLOP/s", "frac": achieved / peak_tf if peak_tf else None,
                          "traffic": traffic, "peak_source": "FFMA loop measured in this run",
+                         "ncu_pipes": pipes,
                          "kernel_ms": kern_avg_ms, "flops_per_launch": flops,
                          "executed_steps_per_launch": steps_exec // a.steps},
             "cpu_baseline": cpu,
