@@ -24,6 +24,9 @@ constexpr int kWarps = kBlock / 32;
 #ifndef PARAPLAN_COLL_EXIT
 #define PARAPLAN_COLL_EXIT 1
 #endif
+#ifndef PARAPLAN_ACCURATE_TANH
+#define PARAPLAN_ACCURATE_TANH 0
+#endif
 #ifndef PARAPLAN_REFILL_MINB
 #define PARAPLAN_REFILL_MINB 6  // <= 85 registers: 6 CTAs (24 warps) per SM, no spills
 #endif
@@ -100,7 +103,20 @@ __device__ __forceinline__ void fast_sincosf(float x, float* s, float* c) {
 
 template <>
 struct M<float> {
-  static __device__ __forceinline__ float th(float x) { return tanhf(x); }
+  // tanh(x) = 1 - 2 / (1 + 2^(2x log2 e)): one ex2, one rcp, three FP32 ops
+  // (absolute error below ~4e-7 over the whole range, saturating to +-1;
+  // libm's tanhf spends ~16 instructions for relative accuracy near 0 that
+  // the policy outputs do not need). PARAPLAN_ACCURATE_TANH=1 restores it.
+  static __device__ __forceinline__ float th(float x) {
+#if PARAPLAN_ACCURATE_TANH
+    return tanhf(x);
+#else
+    float e, r;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(x * 2.8853900817779268f));
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(e + 1.0f));
+    return fmaf(-2.0f, r, 1.0f);
+#endif
+  }
   static __device__ __forceinline__ float tn(float x) { return tanf(x); }
   // tan for |x| <= pi/4 (the steering range when delta_max <= pi/4)
   static __device__ __forceinline__ float tn_small(float x) {
