@@ -221,6 +221,17 @@ pp_status pp_sample_candidate(const pp_handle* h, const double* center,
 double pp_perturbation_sigma(const pp_handle* h, uint64_t t, int32_t restart,
                              int32_t iter, int32_t candidate);
 
+/* RNG parity dump: the theta the DEVICE draws for candidates [cand_begin,
+ * cand_end) of (t, restart, iter) around `center` (len doubles), as the
+ * rollout kernels use them (precision 64: the reference's FP64 draws, equal
+ * to pp_sample_candidate; precision 32: the FP32 transform of the same
+ * integer stream). out holds (cand_end - cand_begin) x len doubles.
+ * Replaces nothing in the reference: the device side of
+ * Planner::sample_candidate (planner.hpp:110-113, src/planner.cpp:207-226). */
+pp_status pp_draw_theta(pp_handle* h, const double* center, int32_t len, uint64_t t,
+                        int32_t restart, int32_t iter, int64_t cand_begin,
+                        int64_t cand_end, double* out);
+
 /* Copies the snapshot to the device (pinned staging, one H2D). A NULL
  * snapshot in pp_evaluate reuses the resident one. */
 pp_status pp_upload_snapshot(pp_handle* h, const pp_snapshot* snap);

@@ -52,6 +52,8 @@ def lib():
         L.pp_plan_step_points.argtypes = [C.c_void_p, P(abi.pp_snapshot_points), C.c_uint64,
                                           P(abi.pp_plan_output)]
         L.pp_upload_points.argtypes = [C.c_void_p, P(abi.pp_snapshot_points)]
+        L.pp_draw_theta.argtypes = [C.c_void_p, P(C.c_double), C.c_int32, C.c_uint64, C.c_int32,
+                                    C.c_int32, C.c_int64, C.c_int64, P(C.c_double)]
         L.pp_evaluate.argtypes = [C.c_void_p, P(abi.pp_snapshot), C.c_uint64, C.c_int32, C.c_int32,
                                   C.c_int32, P(C.c_double), C.c_int64, C.c_int64, C.c_void_p,
                                   C.c_void_p]
@@ -72,7 +74,7 @@ def lib():
 def exported_symbols() -> list[str]:
     """Every entry point include/paraplan_cuda.h declares."""
     return ["pp_create", "pp_destroy", "pp_last_error", "pp_param_count", "pp_abi_version",
-            "pp_plan_step", "pp_plan_step_points", "pp_upload_points", "pp_rollout", "pp_sample_candidate", "pp_perturbation_sigma",
+            "pp_plan_step", "pp_plan_step_points", "pp_upload_points", "pp_draw_theta", "pp_rollout", "pp_sample_candidate", "pp_perturbation_sigma",
             "pp_upload_snapshot", "pp_evaluate", "pp_eval_theta", "pp_merge_records",
             "pp_key_better", "pp_last_timing", "pp_stream", "pp_device_count",
             "pp_measure_fp32_peak"]
@@ -131,6 +133,15 @@ class DevicePlanner:
         o, theta, traj = abi.plan_output_buffers(self.n_params, self.model.H)
         _check(lib().pp_plan_step(self.h, C.byref(s), t, C.byref(o)))
         return o, theta, traj[: o.trajectory_len].copy()
+
+    def draw_theta(self, center, t: int, restart: int, iter_: int, c0: int, c1: int):
+        """The device's theta draws for candidates [c0, c1) (RNG parity dump)."""
+        ctr = np.ascontiguousarray(center, dtype=np.float64)
+        out = np.zeros((max(c1 - c0, 0), self.n_params))
+        _check(lib().pp_draw_theta(self.h, ctr.ctypes.data_as(C.POINTER(C.c_double)), len(ctr), t,
+                                   restart, iter_, c0, c1,
+                                   out.ctypes.data_as(C.POINTER(C.c_double))))
+        return out
 
     def plan_step_points(self, snap: abi.Snapshot, points, t: int, T_s: float = 0.1):
         """plan_step on extrapolate(points): raw anchor-frame points (N, 4)."""

@@ -238,6 +238,58 @@ double pp_perturbation_sigma(const pp_handle* h, uint64_t t, int32_t restart, in
                             rng.next_unit() * (h->cfg.sigma_log_high - h->cfg.sigma_log_low));
 }
 
+pp_status pp_draw_theta(pp_handle* h, const double* center, int32_t len, uint64_t t,
+                        int32_t restart, int32_t iter, int64_t cand_begin, int64_t cand_end,
+                        double* out) {
+  return guarded([&] {
+    if (h == nullptr || center == nullptr || out == nullptr) {
+      throw std::invalid_argument("null argument");
+    }
+    if (len != h->P) throw std::invalid_argument("candidate buffer size mismatch");
+    if (cand_begin < 0 || cand_end < cand_begin || restart < 0 || iter < 0) {
+      throw std::invalid_argument("candidate range out of bounds");
+    }
+    const int64_t n = cand_end - cand_begin;
+    if (n == 0) return;
+    ck(cudaSetDevice(h->device), "cudaSetDevice");
+    ppdev::RoundArgs a{};
+    a.sig_lo = h->cfg.sigma_log_low;
+    a.sig_span = h->cfg.sigma_log_high - h->cfg.sigma_log_low;
+    a.n_params = h->P;
+    a.count = n;
+    a.restart_count = 1;
+    a.cand_begin = cand_begin;
+    const size_t pbytes = sizeof(uint64_t) + sizeof(double) * h->P;
+    h->h_params.reserve(pbytes, "pinned params");
+    h->d_params.reserve(pbytes, "device params");
+    uint64_t* hp = static_cast<uint64_t*>(h->h_params.p);
+    hp[0] = key_prefix(h->cfg.master_seed, t, static_cast<uint64_t>(restart),
+                       static_cast<uint64_t>(iter));
+    std::memcpy(hp + 1, center, sizeof(double) * h->P);
+    ck(cudaMemcpyAsync(h->d_params.p, h->h_params.p, pbytes, cudaMemcpyHostToDevice, h->stream),
+       "params H2D");
+    a.key_prefix = static_cast<const uint64_t*>(h->d_params.p);
+    a.center = reinterpret_cast<const double*>(static_cast<uint64_t*>(h->d_params.p) + 1);
+    const size_t esz = h->fp64 ? sizeof(double) : sizeof(float);
+    const size_t bytes = esz * h->P * static_cast<size_t>(n);
+    h->d_samples.reserve(bytes, "theta draws");
+    ck(static_cast<cudaError_t>(h->fp64 ? ppdev::launch_draw_f64(a, h->d_samples.p, h->stream)
+                                        : ppdev::launch_draw_f32(a, h->d_samples.p, h->stream)),
+       "theta draw launch");
+    std::vector<unsigned char> host(bytes);
+    ck(cudaMemcpyAsync(host.data(), h->d_samples.p, bytes, cudaMemcpyDeviceToHost, h->stream),
+       "theta D2H");
+    ck(cudaStreamSynchronize(h->stream), "theta draws");
+    const size_t m = static_cast<size_t>(h->P) * n;
+    if (h->fp64) {
+      std::memcpy(out, host.data(), bytes);
+    } else {
+      const float* f = reinterpret_cast<const float*>(host.data());
+      for (size_t i = 0; i < m; ++i) out[i] = static_cast<double>(f[i]);
+    }
+  });
+}
+
 int32_t pp_key_better(int32_t cls_a, double k1_a, double k2_a, int32_t cls_b, double k1_b,
                       double k2_b) {
   return key_better({cls_a, k1_a, k2_a}, {cls_b, k1_b, k2_b}) ? 1 : 0;

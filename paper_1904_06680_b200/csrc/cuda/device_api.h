@@ -181,6 +181,11 @@ int launch_generate_f64(NetKind k, const RoundArgs& a, void* stream);
 int launch_rollout_f32(NetKind k, const RoundArgs& a, void* stream);
 int launch_rollout_f64(NetKind k, const RoundArgs& a, void* stream);
 
+// The device's theta draws of candidates [cand_begin, cand_begin + count) of
+// the restart whose key prefix is key_prefix[0] (P Reals each, into `out`).
+int launch_draw_f32(const RoundArgs& a, void* out, void* stream);
+int launch_draw_f64(const RoundArgs& a, void* out, void* stream);
+
 // Near-tie window after a round: counters[2] receives the number of selected
 // candidates, sel_list their flat indices.
 int launch_select(const RoundArgs& a, void* stream);

@@ -490,6 +490,29 @@ __global__ void __launch_bounds__(128) refine_kernel(const RoundArgs a) {
   }
 }
 
+// -------------------------------------------------------- theta draws ----
+// The device's own theta draws of candidates [cand_begin, cand_begin + count)
+// of restart 0 of the round (key prefix a.key_prefix[0]), P Reals per
+// candidate: the RNG parity dump (pp_draw_theta).
+template <typename Real>
+static __global__ void __launch_bounds__(256) draw_kernel(const RoundArgs a, Real* out) {
+  const int P = a.n_params;
+  for (int64_t c = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; c < a.count;
+       c += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    Real* o = out + c * P;
+    draw_theta<Real, 0>(a, __ldg(a.key_prefix), a.cand_begin + c, P,
+                        [&](int i, Real v) { o[i] = v; });
+  }
+}
+
+template <typename Real>
+int launch_draw_impl(const RoundArgs& a, void* out, void* stream) {
+  const int blocks = static_cast<int>(std::min<int64_t>((a.count + 255) / 256, 148 * 8));
+  draw_kernel<Real><<<std::max(blocks, 1), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      a, static_cast<Real*>(out));
+  return static_cast<int>(cudaGetLastError());
+}
+
 // ------------------------------------------------------------ launch ----
 // Register-resident nets use the refill schedule; PARAPLAN_SCHEDULE=lockstep
 // forces the lockstep schedule (A/B measurements only).

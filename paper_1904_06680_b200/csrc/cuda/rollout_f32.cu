@@ -42,4 +42,8 @@ int launch_rollout_f32(NetKind k, const RoundArgs& a, void* stream) {
   }
 }
 
+int launch_draw_f32(const RoundArgs& a, void* out, void* stream) {
+  return launch_draw_impl<float>(a, out, stream);
+}
+
 }  // namespace ppdev

@@ -36,6 +36,10 @@ int launch_rollout_f64(NetKind k, const RoundArgs& a, void* stream) {
   }
 }
 
+int launch_draw_f64(const RoundArgs& a, void* out, void* stream) {
+  return launch_draw_impl<double>(a, out, stream);
+}
+
 }  // namespace ppdev
 
 namespace ppdev {

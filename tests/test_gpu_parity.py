@@ -223,3 +223,36 @@ def test_refine_fixes_a_flipped_fp32_winner():
                                       int(ra[0]["candidate"]), int(ra[0]["candidate"]) + 1)[0]
         exact_cls = 0 if want_a["collided"] else (2 if want_a["reached"] else 1)
         assert exact_cls < rb[0]["cls"] or -want_a["terminal_cost"] <= rb[0]["k1"]
+
+
+@pytest.mark.parametrize("sizes", [[5, 2, 2], [5, 10, 2], [5, 10, 10, 2], [5, 3, 4, 2]])
+def test_device_theta_draws_match_reference_rng(sizes):
+    """pp_draw_theta: the device's own draws (src/planner.cpp:207-226 on the
+    keyed stream of src/rng.cpp:26-58) against the reference's
+    sample_candidate. The integer stream is exact; the Box-Muller transform
+    runs in CUDA's libm (FP64: within a few ulps of glibc, which is why the
+    returned plan's theta is always regenerated on the host) or in float
+    (FP32: within a few float ulps, relative to sigma). Candidate 0 is the
+    centre itself."""
+    rng = np.random.default_rng(3)
+    for precision in (64, 32):
+        m = abi.Model(layer_sizes=sizes, H=20, n_restarts=16, n_candidates=4096, n_iter_max=3,
+                      master_seed=77, precision=precision)
+        dp = capi.DevicePlanner(m)
+        ref = Ref(m)
+        P = m.param_count()
+        center = rng.normal(size=P)
+        tol = 1e-14 if precision == 64 else 1e-5
+        for t, r, it, c0, c1 in [(0, 0, 0, 0, 257), (5, 3, 1, 0, 257),
+                                 (123456789, 15, 2, 0, 257), (9, 2, 0, 1000, 1040)]:
+            dev = dp.draw_theta(center, t, r, it, c0, c1)
+            want = np.array([ref.sample_candidate(center, t, r, it, c) for c in range(c0, c1)])
+            sig = np.array([ref.perturbation_sigma(t, r, it, c) for c in range(c0, c1)])
+            err = np.abs(dev - want) / (np.abs(want) + sig[:, None])
+            assert err.max() < tol, (precision, t, r, it, err.max())
+            if c0 == 0:
+                cast = np.float64 if precision == 64 else np.float32
+                assert np.array_equal(dev[0], center.astype(cast).astype(np.float64))
+            if precision == 64:  # most draws agree to the last bit
+                assert np.mean(dev == want) > 0.5
+        dp.close()
