@@ -44,19 +44,24 @@ def test_c4_lot_per_sample_stats(precision):
     assert same.mean() >= 0.99
 
 
-@pytest.mark.parametrize("which", ["c2", "c5_mixed", "c5_static", "c5_dense"])
-def test_raw_points_path_equals_extrapolated_field(which):
+@pytest.mark.parametrize("precision", [32, 64])
+@pytest.mark.parametrize("which", ["c2", "c5_mixed", "c5_static", "c5_dense", "c4_lot"])
+def test_raw_points_path_equals_extrapolated_field(which, precision):
     """pp_plan_step_points(points) == pp_plan_step(extrapolate(points)),
-    bit for bit (the field is built by the planner)."""
+    bit for bit (the field is built by the planner; c5_dense
+    bins its movers on the device, c4_lot uses the cell-box grid mode)."""
     import math
     rng = np.random.default_rng(7)
     if which == "c2":
-        w = workloads.c2(samples=1 << 14)
+        w = workloads.c2(samples=1 << 14, precision=precision)
         from paper_1904_06680_b200 import import_paraplan
         pp = import_paraplan()
         m = workloads.c2_mission()
         pts = np.array([(q.x, q.y, q.heading, q.speed)
                         for q in pp.sense(m, m.initial_state, w.t, 20, 0.1)])
+    elif which == "c4_lot":
+        w = workloads.c4(samples=1 << 13, H=60, precision=precision)
+        pts = w.extra["points"]
     else:
         n = 10000 if which == "c5_dense" else 500  # c5_dense: movers binned on the device
         pts = np.zeros((n, 4))
@@ -66,7 +71,7 @@ def test_raw_points_path_equals_extrapolated_field(which):
             dyn = rng.random(n) < 0.25
             pts[dyn, 2] = rng.choice([0.0, math.pi], dyn.sum())
             pts[dyn, 3] = rng.uniform(0, 15, dyn.sum())
-        w = workloads.c5(1 << 14, 30, n)
+        w = workloads.c5(1 << 14, 30, n, precision=precision)
     snap = abi.Snapshot(ev=w.snapshot.ev, actuator_delta=w.snapshot.actuator_delta,
                         prev_action=w.snapshot.prev_action, goal=w.snapshot.goal,
                         field=abi.extrapolate(pts, w.model.H))
@@ -75,5 +80,6 @@ def test_raw_points_path_equals_extrapolated_field(which):
     o2, th2, tr2 = dp.plan_step_points(snap, pts, w.t)
     assert np.array_equal(th1, th2) and np.array_equal(tr1, tr2)
     assert (o1.action_a0, o1.action_a1, o1.evaluated) == (o2.action_a0, o2.action_a1, o2.evaluated)
-    o3, th3, tr3 = Port(w.model).plan_step(snap, w.t)
-    assert np.array_equal(th1, th3) and np.array_equal(tr1, tr3)
+    if which != "c4_lot":  # the lot at H=60 is too slow for the CPU oracle here
+        o3, th3, tr3 = Port(w.model).plan_step(snap, w.t)
+        assert np.array_equal(th1, th3) and np.array_equal(tr1, tr3)
