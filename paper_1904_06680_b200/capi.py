@@ -183,6 +183,9 @@ class DevicePlanner:
                                 self.model.H + 1, C.byref(n)))
         return st, traj[: n.value].copy()
 
+    def perturbation_sigma(self, t, restart, it, cand) -> float:
+        return lib().pp_perturbation_sigma(self.h, t, restart, it, cand)
+
     def sample_candidate(self, center, t, restart, it, cand):
         c = np.ascontiguousarray(center, dtype=np.float64)
         out = np.zeros_like(c)

@@ -136,13 +136,6 @@ __global__ void __launch_bounds__(kBlock, refill_min_blocks<Real, Net>())
   Key best = empty_key();
   int best_r = -1;
   int q_head = 32, q_count = 0, q_r = 0, q_c0 = 0;
-  // claimed batch range [qb, qe): with several restarts a warp claims runs of
-  // consecutive batches, so its lanes rarely cross restarts (each crossing
-  // flushes lane bests into the per-restart tables); single batches near the
-  // end of the round keep the tail balanced
-  unsigned qb = 0, qe = 0;
-  const unsigned run = a.restart_count > 1 ? 8u : 1u;
-  const unsigned tail = static_cast<unsigned>(gridDim.x) * kWarps * 2u * run;
   bool exhausted = false;
   unsigned long long n_steps = 0, n_states = 0;
   const bool track = a.keys_only == 0;  // lane bests (one restart) or keys only
@@ -152,27 +145,17 @@ __global__ void __launch_bounds__(kBlock, refill_min_blocks<Real, Net>())
     const unsigned need = __ballot_sync(kFull, !active);
     if (need != 0u) {
       if (q_head >= q_count && !exhausted) {
-        if (qb >= qe) {
-          unsigned b = 0;
-          if (lane == 0) {
-            const unsigned seen = __ldcg(&a.counters[0]);
-            const unsigned k = seen + tail < total_batches ? run : 1u;
-            b = atomicAdd(&a.counters[0], k);
-            qe = min(b + k, total_batches);
-          }
-          b = __shfl_sync(kFull, b, 0);
-          qe = __shfl_sync(kFull, qe, 0);
-          qb = b;
-        }
-        if (qb >= total_batches) {
+        unsigned b = 0;
+        if (lane == 0) b = atomicAdd(&a.counters[0], 1u);
+        b = __shfl_sync(kFull, b, 0);
+        if (b >= total_batches) {
           exhausted = true;
         } else {
-          q_r = static_cast<int>(qb) / bpr;
-          q_c0 = (static_cast<int>(qb) - q_r * bpr) * 32;
+          q_r = static_cast<int>(b) / bpr;
+          q_c0 = (static_cast<int>(b) - q_r * bpr) * 32;
           const int64_t left = a.count - q_c0;
           q_count = left < 32 ? static_cast<int>(left) : 32;
           q_head = 0;
-          ++qb;
         }
       }
       const int avail = q_count - q_head;
