@@ -164,6 +164,35 @@ void cell_boxes(Binned& b) {
     if (x1 >= x0) area += (x1 - x0) * (y1 - y0);
   }
   b.boxes = area < max_area * occupied * b.g * b.g;
+  if (!b.boxes) return;
+  // chunk boxes: consecutive points of a cell (the lot's points come in
+  // polyline order, so a chunk is a short piece of one line)
+  b.cst.assign(cells + 1, 0);
+  for (int c = 0; c < cells; ++c) {
+    const int n = b.sst[c + 1] - b.sst[c];
+    const int cs = chunk_size(n);
+    b.cst[c + 1] = b.cst[c] + (n + cs - 1) / cs;
+  }
+  b.cbox.resize(4 * static_cast<size_t>(b.cst[cells]));
+  for (int c = 0; c < cells; ++c) {
+    const int n = b.sst[c + 1] - b.sst[c];
+    const int cs = chunk_size(n);
+    for (int k = b.cst[c]; k < b.cst[c + 1]; ++k) {
+      const int j0 = b.sst[c] + (k - b.cst[c]) * cs, j1 = std::min(b.sst[c + 1], j0 + cs);
+      double x0 = b.spts[2 * j0], x1 = x0, y0 = b.spts[2 * j0 + 1], y1 = y0;
+      for (int j = j0 + 1; j < j1; ++j) {
+        x0 = std::min(x0, b.spts[2 * j]);
+        x1 = std::max(x1, b.spts[2 * j]);
+        y0 = std::min(y0, b.spts[2 * j + 1]);
+        y1 = std::max(y1, b.spts[2 * j + 1]);
+      }
+      double* o = b.cbox.data() + 4 * static_cast<size_t>(k);
+      o[0] = 0.5 * (x0 + x1);
+      o[1] = 0.5 * (y0 + y1);
+      o[2] = 0.5 * (x1 - x0);
+      o[3] = 0.5 * (y1 - y0);
+    }
+  }
 }
 
 // Grid + static bins (+ boxes).
@@ -235,7 +264,9 @@ Layout layout(const Binned& b, size_t elem) {
   l.sst = align16(l.dpts + 2 * elem * static_cast<size_t>(b.Nd) * b.rows);
   l.dst = align16(l.sst + sizeof(int32_t) * (b.cells() + 1));
   l.sbox = align16(l.dst + sizeof(int32_t) * static_cast<size_t>(b.rows) * (b.cells() + 1));
-  l.bytes = align16(l.sbox + (b.boxes ? 4 * elem * static_cast<size_t>(b.cells()) : 0));
+  l.cst = align16(l.sbox + (b.boxes ? 4 * elem * static_cast<size_t>(b.cells()) : 0));
+  l.cbox = align16(l.cst + (b.boxes ? sizeof(int32_t) * (b.cells() + 1) : 0));
+  l.bytes = align16(l.cbox + (b.boxes ? 2 * elem * b.cbox.size() : 0));
   return l;
 }
 
@@ -380,7 +411,11 @@ void pack(const Binned& b, bool fp64, void* out, bool with_dynamic) {
     put(l.dpts, b.dpts);
     std::memcpy(base + l.dst, b.dst.data(), b.dst.size() * sizeof(int32_t));
   }
-  if (b.boxes) put(l.sbox, b.sbox);
+  if (b.boxes) {
+    put(l.sbox, b.sbox);
+    std::memcpy(base + l.cst, b.cst.data(), b.cst.size() * sizeof(int32_t));
+    put(l.cbox, b.cbox);
+  }
 }
 
 namespace {

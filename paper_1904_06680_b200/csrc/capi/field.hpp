@@ -37,6 +37,11 @@ struct Binned {
   // box is separated from the chassis rectangle.
   bool boxes = false;
   std::vector<double> sbox;      // cells x 4 (when boxes)
+  // ... and per cell its points in chunks of chunk_size(count) consecutive
+  // points, each with its own tight box: chunk j of cell c is box
+  // cst[c] + j and covers points sst[c] + j * chunk_size .. (when boxes)
+  std::vector<int32_t> cst;      // cells + 1
+  std::vector<double> cbox;      // chunks x 4
   // Raw movers of a points field (x, y, step x, step y) x Nd. With
   // `dyn_deferred` the dynamic rows (dpts, dst) are not binned yet: the
   // device bins its own image from these, and bin_dynamic() fills the host
@@ -49,10 +54,14 @@ struct Binned {
   int points() const { return Ns + Nd; }
 };
 
-// Device image layout: byte offsets of [spts][dpts][sst][dst][sbox]
-// (16-aligned).
+// Points per box chunk of a cell holding `count` points: >= 16, and at most
+// 32 chunks per cell (the device keeps a 32-bit chunk mask).
+inline int chunk_size(int count) { return count <= 512 ? 16 : (count + 31) / 32; }
+
+// Device image layout: byte offsets of [spts][dpts][sst][dst][sbox][cst]
+// [cbox] (16-aligned; the box parts only with boxes).
 struct Layout {
-  size_t dpts = 0, sst = 0, dst = 0, sbox = 0, bytes = 0;
+  size_t dpts = 0, sst = 0, dst = 0, sbox = 0, cst = 0, cbox = 0, bytes = 0;
 };
 Layout layout(const Binned& b, size_t elem);
 

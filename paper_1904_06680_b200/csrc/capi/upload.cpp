@@ -72,9 +72,11 @@ void finish_field(pp_handle* h, ppdev::RoundArgs& a) {
   const size_t elem = h->fp64 ? sizeof(double) : sizeof(float);
   const ppfield::Layout l = ppfield::layout(b, elem), l64 = ppfield::layout(b, sizeof(double));
   a.lay = {static_cast<int64_t>(l.dpts), static_cast<int64_t>(l.sst), static_cast<int64_t>(l.dst),
-           static_cast<int64_t>(l.sbox), static_cast<int64_t>(l.bytes)};
+           static_cast<int64_t>(l.sbox), static_cast<int64_t>(l.cst), static_cast<int64_t>(l.cbox),
+           static_cast<int64_t>(l.bytes)};
   a.lay64 = {static_cast<int64_t>(l64.dpts), static_cast<int64_t>(l64.sst),
              static_cast<int64_t>(l64.dst), static_cast<int64_t>(l64.sbox),
+             static_cast<int64_t>(l64.cst), static_cast<int64_t>(l64.cbox),
              static_cast<int64_t>(l64.bytes)};
   a.field = nullptr;
   a.field64 = nullptr;
@@ -97,7 +99,7 @@ void finish_field(pp_handle* h, ppdev::RoundArgs& a) {
       };
       part(0, l.dpts);       // static points
       part(l.sst, l.dst);    // static starts
-      part(l.sbox, l.bytes); // static cell boxes
+      part(l.sbox, l.bytes); // static cell and chunk boxes
       const size_t mb = sizeof(double) * b.dbase.size();
       h->h_movers.reserve(mb, "pinned movers");
       h->d_movers.reserve(mb, "device movers");

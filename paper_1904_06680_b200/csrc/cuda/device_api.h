@@ -72,7 +72,7 @@ struct ConstsT {
 
 // Byte offsets of the parts of a field image.
 struct FieldLayout {
-  int64_t dpts, sst, dst, sbox, bytes;
+  int64_t dpts, sst, dst, sbox, cst, cbox, bytes;
 };
 
 // Everything one sampling round needs. Scalars are FP64 here; the FP32

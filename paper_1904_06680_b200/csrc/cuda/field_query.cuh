@@ -18,6 +18,8 @@ struct Field {
   const int* sst;
   const int* dst;
   const typename Vec2T<Real>::type* sbox;  // per cell: (centre), (half extents)
+  const int* cst;                          // per cell: first chunk box
+  const typename Vec2T<Real>::type* cbox;  // per chunk: (centre), (half extents)
   int Ns, Nd;
   int ncx, ncy;
 };
@@ -30,7 +32,8 @@ __device__ __forceinline__ Field<Real> field_at(const RoundArgs& a, const void* 
   return Field<Real>{reinterpret_cast<const R2*>(p), reinterpret_cast<const R2*>(p + l.dpts),
                      reinterpret_cast<const int*>(p + l.sst),
                      reinterpret_cast<const int*>(p + l.dst),
-                     reinterpret_cast<const R2*>(p + l.sbox), a.field_ns, a.field_nd, a.grid_nx,
+                     reinterpret_cast<const R2*>(p + l.sbox), reinterpret_cast<const int*>(p + l.cst),
+                     reinterpret_cast<const R2*>(p + l.cbox), a.field_ns, a.field_nd, a.grid_nx,
                      a.grid_ny};
 }
 
@@ -115,12 +118,35 @@ __device__ __forceinline__ void scan_part(const typename Vec2T<Real>::type* pts,
 // scanned as one range, as in grid_mode 1.
 constexpr int kDenseCol = 16;
 
+// Points per chunk box of a cell holding `count` points (field.hpp
+// chunk_size: >= 16, at most 32 chunks per cell).
+__device__ __forceinline__ int chunk_size_dev(int count) {
+  return count <= 512 ? 16 : (count + 31) / 32;
+}
+
+// A box (centre m, half extents e) against the chassis rectangle in the
+// rectangle's own frame: > 0 when the box lies inside the rectangle by that
+// much (every point of it is a robust hit), < -pad when it is separated from
+// it by more than the pad (no point of it can be inside), else in between.
 template <typename Real>
-__device__ __forceinline__ void scan_boxed(const typename Vec2T<Real>::type* pts, const int* st,
-                                           const typename Vec2T<Real>::type* box, int ncy,
-                                           int cx_lo, int cx_hi, int cy_lo, int cy_hi,
-                                           const Consts<Real>& K, Real x, Real y, Real c, Real s,
-                                           Real kx, Real ky, Real stop, Real& best) {
+__device__ __forceinline__ Real box_margin(const Consts<Real>& K, Real c, Real s, Real ac, Real as,
+                                           Real kx, Real ky, typename Vec2T<Real>::type m,
+                                           typename Vec2T<Real>::type e) {
+  const Real du = fabs(c * m.x + s * m.y - kx), dv = fabs(-s * m.x + c * m.y - ky);
+  const Real eu = e.x * ac + e.y * as, ev = e.x * as + e.y * ac;
+  // inside margin of the box's farthest extent; separation of its nearest
+  const Real inside = fmin(K.bhx - (du + eu), K.hw - (dv + ev));
+  const Real apart = fmax(du - eu - K.bhx, dv - ev - K.hw);
+  return apart > K.qpad ? -apart : (inside > Real(0) ? inside : Real(0));
+}
+
+template <typename Real>
+__device__ __forceinline__ void scan_boxed(const Field<Real>& f, int ncy, int cx_lo, int cx_hi,
+                                           int cy_lo, int cy_hi, const Consts<Real>& K, Real x,
+                                           Real y, Real c, Real s, Real kx, Real ky, Real stop,
+                                           Real& best) {
+  const auto* pts = f.spts;
+  const int* st = f.sst;
   const Real ac = fabs(c), as = fabs(s);
   const int nrow = cy_hi - cy_lo + 1;
   const int ncol = cx_hi - cx_lo + 1;
@@ -131,27 +157,47 @@ __device__ __forceinline__ void scan_boxed(const typename Vec2T<Real>::type* pts
     const int lo = st[cell0];
     const int n = has ? st[cell0 + nrow] - lo : 0;
     const bool dense = n > kDenseCol;
-    // dense columns: cell by cell behind the box test
+    // dense columns: cell by cell behind the cell box, then chunk by chunk
+    // behind the chunk boxes; a box inside the rectangle is a robust hit
     const int rows = __reduce_max_sync(kFull, dense ? nrow : 0);
     for (int q = 0; q < rows; ++q) {
-      int clo = 0, cnt = 0;
+      int clo = 0, cnt = 0, ch0 = 0, nch = 0;
       if (dense && q < nrow && best < stop) {
         const int cell = cell0 + q;
         clo = st[cell];
         cnt = st[cell + 1] - clo;
         if (cnt > 0) {
-          const auto m = box[2 * cell], e = box[2 * cell + 1];
-          const Real du = fabs(c * m.x + s * m.y - kx), dv = fabs(-s * m.x + c * m.y - ky);
-          if (du > K.bhx + e.x * ac + e.y * as + K.qpad ||
-              dv > K.hw + e.x * as + e.y * ac + K.qpad) {
-            cnt = 0;
+          const Real bm = box_margin(K, c, s, ac, as, kx, ky, f.sbox[2 * cell], f.sbox[2 * cell + 1]);
+          if (bm > Real(0)) {
+            best = fmax(best, bm);
+          } else if (bm == Real(0)) {
+            ch0 = f.cst[cell];
+            nch = f.cst[cell + 1] - ch0;
           }
         }
       }
-      for (int j = 0; __any_sync(kFull, j < cnt && best < stop); ++j) {
-        if (j < cnt && best < stop) {
-          const auto m = pts[clo + j];
-          best = fmax(best, point_margin<Real>(K, x, y, c, s, kx, ky, m.x, m.y));
+      const int csz = chunk_size_dev(cnt);
+      const int nchunks = __reduce_max_sync(kFull, nch);
+      for (int j = 0; j < nchunks; ++j) {
+        int at = 0, left = 0;
+        if (j < nch && best < stop) {
+          const Real bm = box_margin(K, c, s, ac, as, kx, ky, f.cbox[2 * (ch0 + j)],
+                                     f.cbox[2 * (ch0 + j) + 1]);
+          if (bm > Real(0)) {
+            best = fmax(best, bm);
+          } else if (bm == Real(0)) {
+            at = clo + j * csz;
+            left = min(csz, clo + cnt - at);
+          }
+        }
+        if (__any_sync(kFull, left > 0)) {
+#pragma unroll 4
+          for (int i = 0; i < csz; ++i) {
+            if (i < left) {
+              const auto m = pts[at + i];
+              best = fmax(best, point_margin<Real>(K, x, y, c, s, kx, ky, m.x, m.y));
+            }
+          }
         }
       }
     }
@@ -206,8 +252,7 @@ __device__ __forceinline__ Real collide_margin(const Field<Real>& f, const Const
     const int* st = dyn ? f.dst + static_cast<size_t>(h) * (ncx * ncy + 1) : f.sst;
     if constexpr (kGrid == 2) {
       if (!dyn) {
-        scan_boxed<Real>(pts, st, f.sbox, ncy, cx_lo, cx_hi, cy_lo, cy_hi, K, x, y, c, s, kx, ky,
-                         stop, best);
+        scan_boxed<Real>(f, ncy, cx_lo, cx_hi, cy_lo, cy_hi, K, x, y, c, s, kx, ky, stop, best);
         continue;
       }
     }
