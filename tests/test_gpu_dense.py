@@ -83,3 +83,24 @@ def test_raw_points_path_equals_extrapolated_field(which, precision):
     if which != "c4_lot":  # the lot at H=60 is too slow for the CPU oracle here
         o3, th3, tr3 = Port(w.model).plan_step(snap, w.t)
         assert np.array_equal(th1, th3) and np.array_equal(tr1, tr3)
+
+
+def test_raw_points_errors_and_edge_cases():
+    """pp_plan_step_points: non-finite points are rejected with the reference's
+    message; no points and all-static points plan like the field path."""
+    w = workloads.c5(1 << 12, 20, 100)
+    pts = w.extra["points"].copy()
+    dp = capi.DevicePlanner(w.model)
+    bad = pts.copy()
+    bad[3, 0] = np.nan
+    with pytest.raises(ValueError, match="non-finite"):
+        dp.plan_step_points(w.snapshot, bad, w.t)
+    # the planner stays usable after the error
+    for sub in (pts[:0], pts[pts[:, 3] == 0], pts):
+        snap = abi.Snapshot(ev=w.snapshot.ev, actuator_delta=w.snapshot.actuator_delta,
+                            prev_action=w.snapshot.prev_action, goal=w.snapshot.goal,
+                            field=abi.extrapolate(sub, w.model.H) if len(sub) else None)
+        o1, th1, tr1 = dp.plan_step(snap, w.t)
+        o2, th2, tr2 = dp.plan_step_points(snap, sub, w.t)
+        assert np.array_equal(th1, th2) and np.array_equal(tr1, tr2)
+        assert o1.evaluated == o2.evaluated
