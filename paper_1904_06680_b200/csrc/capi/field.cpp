@@ -163,10 +163,44 @@ void cell_boxes(Binned& b) {
     o[3] = 0.5 * (y1 - y0);
     if (x1 >= x0) area += (x1 - x0) * (y1 - y0);
   }
-  b.boxes = area < max_area * occupied * b.g * b.g;
+  const bool structured = area < max_area * occupied * b.g * b.g;
+  // very dense clouds profit from the chunk boxes even without structure
+  static const double min_dense = env_or("PARAPLAN_CHUNK_DENSE_MIN", 32);
+  b.boxes = structured || static_cast<double>(b.Ns) >= min_dense * occupied;
   if (!b.boxes) return;
-  // chunk boxes: consecutive points of a cell (the lot's points come in
-  // polyline order, so a chunk is a short piece of one line)
+  // chunk boxes over consecutive points of a cell. Structured clouds keep
+  // their order (points along a polyline: a chunk is a short piece of a
+  // line); a uniform fill is put in Morton (Z) order of the position in the
+  // cell first, so a chunk is a compact patch
+  if (!structured) {
+    std::vector<std::pair<uint32_t, int>> key;
+    std::vector<double> tmp;
+    for (int c = 0; c < cells; ++c) {
+      const int j0 = b.sst[c], n = b.sst[c + 1] - j0;
+      if (n <= 16) continue;
+      const double* bx = b.sbox.data() + 4 * static_cast<size_t>(c);
+      const double sx = bx[2] > 0 ? 32767.0 / (2 * bx[2]) : 0.0;
+      const double sy = bx[3] > 0 ? 32767.0 / (2 * bx[3]) : 0.0;
+      key.resize(n);
+      for (int k = 0; k < n; ++k) {
+        const double x = b.spts[2 * (j0 + k)], y = b.spts[2 * (j0 + k) + 1];
+        uint32_t ix = static_cast<uint32_t>((x - (bx[0] - bx[2])) * sx);
+        uint32_t iy = static_cast<uint32_t>((y - (bx[1] - bx[3])) * sy);
+        uint32_t z = 0;
+        for (int bit = 0; bit < 15; ++bit) {
+          z |= ((ix >> bit) & 1u) << (2 * bit) | ((iy >> bit) & 1u) << (2 * bit + 1);
+        }
+        key[k] = {z, k};
+      }
+      std::stable_sort(key.begin(), key.end(),
+                       [](const auto& l, const auto& r) { return l.first < r.first; });
+      tmp.assign(b.spts.begin() + 2 * j0, b.spts.begin() + 2 * (j0 + n));
+      for (int k = 0; k < n; ++k) {
+        b.spts[2 * (j0 + k)] = tmp[2 * key[k].second];
+        b.spts[2 * (j0 + k) + 1] = tmp[2 * key[k].second + 1];
+      }
+    }
+  }
   b.cst.assign(cells + 1, 0);
   for (int c = 0; c < cells; ++c) {
     const int n = b.sst[c + 1] - b.sst[c];
