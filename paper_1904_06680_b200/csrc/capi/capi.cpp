@@ -47,13 +47,12 @@ void prewarm(pp_handle* h) {
     const int rc = std::min(h->cfg.n_restarts, 64);
     std::vector<pp_record> rec(rc);
     run_round(h, 0, 0, 0, rc, nullptr, 0, h->cfg.n_candidates, nullptr, rec.data(), nullptr);
-    for (int mode = 1; mode <= 2; ++mode) {
+    // the other grid modes, and (FP32 planners) the FP64 kernels of the
+    // certification's fallback round
+    for (int mode = 0; mode <= 2; ++mode) {
       ppdev::LaunchShape sh{};
-      if (h->fp64) {
-        ppdev::shape_f64(h->kind, h->device, 0, mode, &sh);
-      } else {
-        ppdev::shape_f32(h->kind, h->device, 0, mode, &sh);
-      }
+      ppdev::shape_f64(h->kind, h->device, 0, mode, &sh);
+      if (!h->fp64) ppdev::shape_f32(h->kind, h->device, 0, mode, &sh);
     }
     ck(cudaStreamSynchronize(h->stream), "warm-up");
   } catch (...) {

@@ -63,7 +63,7 @@ def closed_loop(samples, H, ticks, name="exp4"):
     taus = [r.plan_time for r in log.records if r.evaluated > 0]
     return dict(ticks=len(taus), tau_avg_ms=1e3 * float(np.mean(taus)),
                 tau_max_ms=1e3 * float(np.max(taus)), wall_s=wall,
-                completed=bool(log.completed))
+                completed=bool(log.completed), tau_ms=[round(1e3 * x, 3) for x in taus])
 
 
 if __name__ == "__main__":
