@@ -172,10 +172,14 @@ void cell_boxes(Binned& b) {
   // their order (points along a polyline: a chunk is a short piece of a
   // line); a uniform fill is put in Morton (Z) order of the position in the
   // cell first, so a chunk is a compact patch
+  // (cells are independent: in parallel over cell blocks)
+  constexpr int kCellBlock = 64;
+  const int blocks = (cells + kCellBlock - 1) / kCellBlock;
   if (!structured) {
-    std::vector<std::pair<uint32_t, int>> key;
-    std::vector<double> tmp;
-    for (int c = 0; c < cells; ++c) {
+    par_for(blocks, static_cast<size_t>(b.Ns) * 4, [&](int blk) {
+    thread_local std::vector<std::pair<uint32_t, int>> key;
+    thread_local std::vector<double> tmp;
+    for (int c = blk * kCellBlock; c < std::min(cells, (blk + 1) * kCellBlock); ++c) {
       const int j0 = b.sst[c], n = b.sst[c + 1] - j0;
       if (n <= 16) continue;
       const double* bx = b.sbox.data() + 4 * static_cast<size_t>(c);
@@ -200,6 +204,7 @@ void cell_boxes(Binned& b) {
         b.spts[2 * (j0 + k) + 1] = tmp[2 * key[k].second + 1];
       }
     }
+    });
   }
   b.cst.assign(cells + 1, 0);
   for (int c = 0; c < cells; ++c) {
@@ -208,7 +213,8 @@ void cell_boxes(Binned& b) {
     b.cst[c + 1] = b.cst[c] + (n + cs - 1) / cs;
   }
   b.cbox.resize(4 * static_cast<size_t>(b.cst[cells]));
-  for (int c = 0; c < cells; ++c) {
+  par_for(blocks, static_cast<size_t>(b.Ns) * 4, [&](int blk) {
+  for (int c = blk * kCellBlock; c < std::min(cells, (blk + 1) * kCellBlock); ++c) {
     const int n = b.sst[c + 1] - b.sst[c];
     const int cs = chunk_size(n);
     for (int k = b.cst[c]; k < b.cst[c + 1]; ++k) {
@@ -227,6 +233,7 @@ void cell_boxes(Binned& b) {
       o[3] = 0.5 * (y1 - y0);
     }
   }
+  });
 }
 
 // Grid + static bins (+ boxes).
@@ -367,39 +374,75 @@ void from_points(Binned& b, const double* pts4, int N, int rows, double T_s, dou
   }
   // small mixed clouds stay one scan per state: every point dynamic
   const bool all_dynamic = N <= kSmall && any_moving;
-  std::vector<double> s_xy(2 * static_cast<size_t>(N));
-  b.dbase.resize(4 * static_cast<size_t>(N));
+  const auto is_static = [&](int j) {
+    return !all_dynamic && steps[2 * j] == 0.0 && steps[2 * j + 1] == 0.0;
+  };
+  // split in input order, in parallel over blocks of points: per-block
+  // counts and bounding boxes, then a scatter at the blocks' offsets
+  constexpr int kPtBlock = 4096;
+  const int nblk = (N + kPtBlock - 1) / kPtBlock;
+  struct Blk {
+    int ns = 0, nd = 0;
+    double xmin = INFINITY, xmax = -INFINITY, ymin = INFINITY, ymax = -INFINITY;
+    bool finite = true;
+  };
+  std::vector<Blk> blk(nblk);
+  par_for(nblk, static_cast<size_t>(N) * 4, [&](int k) {
+    Blk& q = blk[k];
+    const auto see = [&](double x, double y) {
+      q.finite &= std::isfinite(x) && std::isfinite(y);
+      q.xmin = std::min(q.xmin, x);
+      q.xmax = std::max(q.xmax, x);
+      q.ymin = std::min(q.ymin, y);
+      q.ymax = std::max(q.ymax, y);
+    };
+    for (int j = k * kPtBlock; j < std::min(N, (k + 1) * kPtBlock); ++j) {
+      const double* p = pts4 + 4 * j;
+      see(p[0], p[1]);
+      if (is_static(j)) {
+        ++q.ns;
+      } else {
+        ++q.nd;
+        // x + r * step is monotone in r (rounding is monotone): rows 0 and
+        // rows - 1 bound every position of the point
+        see(p[0] + (rows - 1) * steps[2 * j], p[1] + (rows - 1) * steps[2 * j + 1]);
+      }
+    }
+  });
   size_t ns = 0, nd = 0;
   double xmin = INFINITY, xmax = -INFINITY, ymin = INFINITY, ymax = -INFINITY;
   bool finite = true;
-  const auto see = [&](double x, double y) {
-    finite &= std::isfinite(x) && std::isfinite(y);
-    xmin = std::min(xmin, x);
-    xmax = std::max(xmax, x);
-    ymin = std::min(ymin, y);
-    ymax = std::max(ymax, y);
-  };
-  for (int j = 0; j < N; ++j) {
-    const double* p = pts4 + 4 * j;
-    const double sx = steps[2 * j], sy = steps[2 * j + 1];
-    see(p[0], p[1]);
-    if (!all_dynamic && sx == 0.0 && sy == 0.0) {  // x + h * (+-0) == x: identical rows
-      s_xy[2 * ns] = p[0];
-      s_xy[2 * ns + 1] = p[1];
-      ++ns;
-    } else {
-      double* q = b.dbase.data() + 4 * nd++;
-      q[0] = p[0];
-      q[1] = p[1];
-      q[2] = sx;
-      q[3] = sy;
-      // x + r * step is monotone in r (rounding is monotone): rows 0 and
-      // rows - 1 bound every position of the point
-      see(p[0] + (rows - 1) * sx, p[1] + (rows - 1) * sy);
-    }
+  std::vector<size_t> s_off(nblk), d_off(nblk);
+  for (int k = 0; k < nblk; ++k) {
+    s_off[k] = ns;
+    d_off[k] = nd;
+    ns += blk[k].ns;
+    nd += blk[k].nd;
+    finite &= blk[k].finite;
+    xmin = std::min(xmin, blk[k].xmin);
+    xmax = std::max(xmax, blk[k].xmax);
+    ymin = std::min(ymin, blk[k].ymin);
+    ymax = std::max(ymax, blk[k].ymax);
   }
-  s_xy.resize(2 * ns);
+  std::vector<double> s_xy(2 * ns);
   b.dbase.resize(4 * nd);
+  par_for(nblk, static_cast<size_t>(N) * 4, [&](int k) {
+    size_t is = s_off[k], id = d_off[k];
+    for (int j = k * kPtBlock; j < std::min(N, (k + 1) * kPtBlock); ++j) {
+      const double* p = pts4 + 4 * j;
+      if (is_static(j)) {
+        s_xy[2 * is] = p[0];
+        s_xy[2 * is + 1] = p[1];
+        ++is;
+      } else {
+        double* q = b.dbase.data() + 4 * id++;
+        q[0] = p[0];
+        q[1] = p[1];
+        q[2] = steps[2 * j];
+        q[3] = steps[2 * j + 1];
+      }
+    }
+  });
   BBox box;
   box.finite = finite;
   if (N > 0 && finite) {

@@ -229,7 +229,6 @@ void run_round_launch(pp_handle* h, uint64_t t, int iter, int r0, int rc, const 
       const unsigned hc = std::thread::hardware_concurrency();
       h->pool = std::make_unique<HostPool>(static_cast<int>(std::min(16u, std::max(1u, hc))));
     }
-    h->pool->prewarm();  // workers spin while the GPU samples
   }
   ck(cudaEventRecord(h->ev1, h->stream), "event");
   // one D2H: counters (selection count), work counters, winners and the
@@ -242,6 +241,9 @@ void run_round_launch(pp_handle* h, uint64_t t, int iter, int r0, int rc, const 
     ppfield::bin_dynamic(h->field);
     phase("host-binned");
   }
+  // then the certification's workers spin while the GPU finishes (woken
+  // after the binning, whose threads they would otherwise crowd out)
+  if (rerank) h->pool->prewarm();
   uint32_t n_sel = 0;
   h->timing.d2h_bytes += static_cast<int64_t>(rbytes);
   if (per_sample != nullptr) {
