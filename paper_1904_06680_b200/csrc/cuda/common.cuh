@@ -27,6 +27,15 @@ constexpr int kWarps = kBlock / 32;
 #ifndef PARAPLAN_ACCURATE_TANH
 #define PARAPLAN_ACCURATE_TANH 0
 #endif
+#ifndef PARAPLAN_SMEM_FIELD
+#define PARAPLAN_SMEM_FIELD 1
+#endif
+#ifndef PARAPLAN_BRANCHLESS_SCAN
+#define PARAPLAN_BRANCHLESS_SCAN 1
+#endif
+#ifndef PARAPLAN_FAST_SQRT
+#define PARAPLAN_FAST_SQRT 1
+#endif
 #ifndef PARAPLAN_REFILL_MINB
 #define PARAPLAN_REFILL_MINB 6  // <= 85 registers: 6 CTAs (24 warps) per SM, no spills
 #endif
@@ -120,12 +129,26 @@ struct M<float> {
   static __device__ __forceinline__ float tn(float x) { return tanf(x); }
   // tan for |x| <= pi/4 (the steering range when delta_max <= pi/4)
   static __device__ __forceinline__ float tn_small(float x) {
+#if PARAPLAN_FAST_SQRT
+    float r;  // cos_poly >= 0.7 here: no denormal or zero input
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(cos_poly(x)));
+    return sin_poly(x) * r;
+#else
     return sin_poly(x) * __frcp_rn(cos_poly(x));
+#endif
   }
   static __device__ __forceinline__ void sc(float x, float* s, float* c) {
     fast_sincosf(x, s, c);
   }
-  static __device__ __forceinline__ float sq(float x) { return sqrtf(x); }
+  static __device__ __forceinline__ float sq(float x) {
+#if PARAPLAN_FAST_SQRT
+    float r;  // path segments: ~1 ulp, no slow path for denormals
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+#else
+    return sqrtf(x);
+#endif
+  }
   static __device__ __forceinline__ float ab(float x) { return fabsf(x); }
   // wrap_angle (src/geometry.cpp:9-13): remainder by 2*pi (two-part
   // Cody-Waite), lower boundary folded onto +pi.

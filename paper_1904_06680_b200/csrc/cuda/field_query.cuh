@@ -81,16 +81,27 @@ __device__ __forceinline__ void scan_part(const typename Vec2T<Real>::type* pts,
                                           int ncy, int cx_lo, int cx_hi, int cy_lo, int cy_hi,
                                           const Consts<Real>& K, Real x, Real y, Real c, Real s,
                                           Real kx, Real ky, Real stop, Real& best) {
-  if constexpr (kGrid == 0) {  // x-buckets: the window is one contiguous range
+  if constexpr (kGrid == 0 || kGrid == 3) {  // x-buckets: one contiguous range
     const int lo = st[cx_lo];
     const int cnt = st[cx_hi + 1] - lo;
     const int rounds = __reduce_max_sync(kFull, cnt);
+#if PARAPLAN_BRANCHLESS_SCAN
+    // no per-point branch: a lane past its own range re-reads point 0 of
+    // the part (which exists: the part is not empty) and discards it
+    for (int j = 0; j < rounds; ++j) {
+      const bool in = j < cnt;
+      const auto m = pts[in ? lo + j : 0];
+      const Real pm = point_margin<Real>(K, x, y, c, s, kx, ky, m.x, m.y);
+      best = in ? fmax(best, pm) : best;
+    }
+#else
     for (int j = 0; j < rounds; ++j) {
       if (j < cnt) {
         const auto m = pts[lo + j];
         best = fmax(best, point_margin<Real>(K, x, y, c, s, kx, ky, m.x, m.y));
       }
     }
+#endif
   } else {  // 2-D cells, one contiguous range per cell column; early exit
     const int ncol = cx_hi - cx_lo + 1;
     const int cols = __reduce_max_sync(kFull, ncol);
@@ -232,7 +243,7 @@ __device__ __forceinline__ Real collide_margin(const Field<Real>& f, const Const
   const int cx_lo = static_cast<int>(fmin(fmax((ox - ex) * K.binv, Real(0)), top));
   const int cx_hi = static_cast<int>(fmin(fmax((ox + ex) * K.binv, Real(0)), top));
   int cy_lo = 0, cy_hi = 0;
-  if constexpr (kGrid) {
+  if constexpr (kGrid == 1 || kGrid == 2) {
     const Real ytop = Real(ncy - 1);
     const Real oy = y + K.bcx * s - K.by0;
     const Real ey = K.bhx * as + K.hw * ac + K.qpad;

@@ -133,9 +133,16 @@ __device__ __forceinline__ void bulk_stage(unsigned char* dst, const void* src, 
       : "memory");
 }
 
-template <typename Real>
+template <typename Real, int kGrid = 0>
 __device__ __forceinline__ Field<Real> stage_field(const RoundArgs& a, unsigned char* smem) {
   __shared__ __align__(8) uint64_t stage_bar;
+  if constexpr (kGrid == 3) {
+    // grid kind 3: x-buckets staged in shared memory (the host launches this
+    // instantiation only then), so every field load is an LDS on a 32-bit
+    // shared address instead of a generic 64-bit load
+    bulk_stage(smem, a.field, static_cast<uint32_t>(a.field_smem_bytes), &stage_bar);
+    return field_at<Real>(a, smem, a.lay);
+  }
   if (a.field_smem_bytes > 0 && a.n_points > 0) {
     bulk_stage(smem, a.field, static_cast<uint32_t>(a.field_smem_bytes), &stage_bar);
     return field_at<Real>(a, smem, a.lay);

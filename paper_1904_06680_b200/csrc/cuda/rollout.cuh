@@ -116,7 +116,7 @@ __global__ void __launch_bounds__(kBlock, refill_min_blocks<Real, Net>())
   for (int i = threadIdx.x; i < kWarps * kMaxRestartsPerLaunch; i += blockDim.x) {
     (&table[0][0])[i] = empty_key();
   }
-  const Field<Real> f = stage_field<Real>(a, smem_raw);
+  const Field<Real> f = stage_field<Real, kGrid>(a, smem_raw);
   wait_prior_grid();  // the generator's theta records
 
   const int bpr = a.tiles_per_restart;  // 32-candidate batches per restart
@@ -323,7 +323,7 @@ __global__ void __launch_bounds__(kBlock) lockstep_kernel(const RoundArgs a) {
   const Consts<Real>& K = consts_of<Real>(a);
   const int H = a.H;
   const int P = a.n_params;
-  const Field<Real> f = stage_field<Real>(a, smem_raw);
+  const Field<Real> f = stage_field<Real, kGrid>(a, smem_raw);
   Real s0[5];
   start_features(K, s0);
 
@@ -541,10 +541,26 @@ KernelFn kernel_of_g() {
 
 // grid mode of the field (0 x-buckets, 1 2-D, 2 2-D with cell boxes) -- a
 // separate instantiation each, so the small-field kernel stays lean.
+// Kind 3 = x-buckets staged in shared memory (typed shared loads).
+inline int grid_kind(int mode, int field_smem_bytes) {
+#if PARAPLAN_SMEM_FIELD
+  return mode == 0 && field_smem_bytes > 0 ? 3 : mode;
+#else
+  return mode;
+#endif
+}
 template <typename Real, class Net>
-KernelFn kernel_of(int mode) {
-  return mode == 2 ? kernel_of_g<Real, Net, 2>()
-                   : (mode == 1 ? kernel_of_g<Real, Net, 1>() : kernel_of_g<Real, Net, 0>());
+KernelFn kernel_of(int kind) {
+  switch (kind) {
+    case 3:
+      return kernel_of_g<Real, Net, 3>();
+    case 2:
+      return kernel_of_g<Real, Net, 2>();
+    case 1:
+      return kernel_of_g<Real, Net, 1>();
+    default:
+      return kernel_of_g<Real, Net, 0>();
+  }
 }
 
 // Stage 1 of a round: the theta generator (refill schedule only; a no-op
@@ -568,7 +584,7 @@ int launch_generate_impl(const RoundArgs& a, void* stream) {
 template <typename Real, class Net>
 int launch_rollout_impl(const RoundArgs& a, void* stream) {
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  auto k = kernel_of<Real, Net>(a.grid_mode);
+  auto k = kernel_of<Real, Net>(grid_kind(a.grid_mode, a.field_smem_bytes));
   const size_t smem = static_cast<size_t>(a.field_smem_bytes);
   if (smem > 32 * 1024) {
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
@@ -618,7 +634,7 @@ int launch_refine_impl(const RoundArgs& a, void* stream) {
 
 template <typename Real, class Net>
 int shape_impl(int device, int field_bytes, int grid, LaunchShape* out) {
-  auto k = kernel_of<Real, Net>(grid);
+  auto k = kernel_of<Real, Net>(grid_kind(grid, field_bytes));
   const bool refill = refill_schedule<Net>();
   const int smem_bytes = field_bytes;
   out->queue_bytes = 0;
