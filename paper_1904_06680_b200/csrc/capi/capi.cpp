@@ -55,8 +55,8 @@ void prewarm(pp_handle* h) {
       if (!h->fp64) ppdev::shape_f32(h->kind, h->device, 0, mode, &sh);
     }
     ppdev::LaunchShape sh{};  // x-buckets staged in shared memory
-    if (h->fp64) ppdev::shape_f64(h->kind, h->device, 16, 0, &sh);
-    else ppdev::shape_f32(h->kind, h->device, 16, 0, &sh);
+    if (h->fp64) ppdev::shape_f64(h->kind, h->device, 16, 3, &sh);
+    else ppdev::shape_f32(h->kind, h->device, 16, 3, &sh);
     ck(cudaStreamSynchronize(h->stream), "warm-up");
   } catch (...) {
     cudaGetLastError();

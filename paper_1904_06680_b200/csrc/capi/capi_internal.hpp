@@ -351,7 +351,7 @@ void upload_snapshot(pp_handle* h, const pp_snapshot& s, bool defer = false);
 
 // round.cpp
 uint64_t key_prefix(uint64_t seed, uint64_t t, uint64_t r, uint64_t i);
-ppdev::LaunchShape launch_shape(pp_handle* h, bool fp64, int field_smem, int grid_mode);
+ppdev::LaunchShape launch_shape(pp_handle* h, bool fp64, int field_smem, int kind);
 void consume_pending_field(pp_handle* h, bool side = false);
 void run_round_launch(pp_handle* h, uint64_t t, int iter, int r0, int rc, const double* center,
                       int64_t c0, int64_t c1, const double* injected, pp_record* out,

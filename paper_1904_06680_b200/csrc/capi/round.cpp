@@ -39,13 +39,13 @@ int host_max() {
 
 // Occupancy of the rollout kernel for (precision, staged field size, grid
 // mode), queried once per handle.
-ppdev::LaunchShape launch_shape(pp_handle* h, bool fp64, int field_smem, int grid_mode) {
-  const int64_t key = (static_cast<int64_t>(field_smem) << 8) | (grid_mode << 1) | (fp64 ? 1 : 0);
+ppdev::LaunchShape launch_shape(pp_handle* h, bool fp64, int field_smem, int kind) {
+  const int64_t key = (static_cast<int64_t>(field_smem) << 8) | (kind << 1) | (fp64 ? 1 : 0);
   auto found = h->shapes.find(key);
   if (found == h->shapes.end()) {
     ppdev::LaunchShape sh{};
-    const int rcode = fp64 ? ppdev::shape_f64(h->kind, h->device, field_smem, grid_mode, &sh)
-                           : ppdev::shape_f32(h->kind, h->device, field_smem, grid_mode, &sh);
+    const int rcode = fp64 ? ppdev::shape_f64(h->kind, h->device, field_smem, kind, &sh)
+                           : ppdev::shape_f32(h->kind, h->device, field_smem, kind, &sh);
     ck(static_cast<cudaError_t>(rcode), "occupancy query");
     found = h->shapes.emplace(key, sh).first;
   }
@@ -191,7 +191,8 @@ void run_round_launch(pp_handle* h, uint64_t t, int iter, int r0, int rc, const 
     a.kd = b.kd;
   }
   const int field_smem = (force_fp64 && !h->fp64) ? 0 : h->field_smem_bytes;
-  const ppdev::LaunchShape shape = launch_shape(h, fp64, field_smem, a.grid_mode);
+  const ppdev::LaunchShape shape = launch_shape(
+      h, fp64, field_smem, ppdev::grid_kind(a.grid_mode, field_smem, a.field_ns, a.field_nd));
   // refill: 32-candidate batches; lockstep: one tile of `block` candidates
   const int unit = shape.refill ? 32 : shape.block;
   const int64_t tpr64 = (count + unit - 1) / unit;

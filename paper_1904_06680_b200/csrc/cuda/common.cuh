@@ -27,9 +27,6 @@ constexpr int kWarps = kBlock / 32;
 #ifndef PARAPLAN_ACCURATE_TANH
 #define PARAPLAN_ACCURATE_TANH 0
 #endif
-#ifndef PARAPLAN_SMEM_FIELD
-#define PARAPLAN_SMEM_FIELD 1
-#endif
 #ifndef PARAPLAN_BRANCHLESS_SCAN
 #define PARAPLAN_BRANCHLESS_SCAN 1
 #endif
@@ -180,6 +177,12 @@ struct M<double> {
 template <typename Real>
 __device__ __forceinline__ Real clampr(Real v, Real lo, Real hi) {
   return v < lo ? lo : (hi < v ? hi : v);  // std::clamp
+}
+// FP32: two FMNMX (equal to std::clamp for every non-NaN v when lo <= hi;
+// the rollout's inputs are finite)
+template <>
+__device__ __forceinline__ float clampr<float>(float v, float lo, float hi) {
+  return fminf(fmaxf(v, lo), hi);
 }
 
 // Round constants live in the kernel parameter bank (RoundArgs::kf / kd).

@@ -170,6 +170,21 @@ struct LaunchShape {
 // field_bytes = shared-memory image of the field (0 = read from L2).
 // Returns 0 or a cudaError_t.
 // grid: the field uses the 2-D cell grid (separate kernel instantiation).
+// Rollout kernel kind of a field: its grid mode (0 x-buckets, 1 2-D by
+// column, 2 2-D with cell boxes), or 3 = x-buckets staged in shared memory
+// with a single part (all points static or all dynamic: small mixed clouds
+// are made all-dynamic by the binning, csrc/capi/field.cpp kSmall).
+#ifndef PARAPLAN_SMEM_FIELD
+#define PARAPLAN_SMEM_FIELD 1
+#endif
+inline int grid_kind(int mode, int field_smem_bytes, int ns, int nd) {
+#if PARAPLAN_SMEM_FIELD
+  return mode == 0 && field_smem_bytes > 0 && (ns == 0 || nd == 0) ? 3 : mode;
+#else
+  return mode;
+#endif
+}
+// `grid` is the kernel kind (grid_kind).
 int shape_f32(NetKind k, int device, int field_bytes, int grid, LaunchShape* out);
 int shape_f64(NetKind k, int device, int field_bytes, int grid, LaunchShape* out);
 

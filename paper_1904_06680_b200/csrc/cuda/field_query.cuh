@@ -253,6 +253,15 @@ __device__ __forceinline__ Real collide_margin(const Field<Real>& f, const Const
   const Real kx = c * x + s * y + K.bcx;  // FP32 rotated-frame form only
   const Real ky = -s * x + c * y;
   Real best = Real(-1e30);
+  if constexpr (kGrid == 3) {
+    // one part: all points static, or all dynamic (the row of state h)
+    const bool dyn = f.Nd > 0;
+    const auto* pts = dyn ? f.dpts + h * f.Nd : f.spts;
+    const int* st = dyn ? f.dst + h * (ncx + 1) : f.sst;
+    scan_part<Real, kGrid>(pts, st, ncy, cx_lo, cx_hi, cy_lo, cy_hi, K, x, y, c, s, kx, ky, stop,
+                           best);
+    return best;
+  }
   // part 0: static points; part 1: the dynamic row of state h (one copy of
   // the scan code, warp-uniform part loop)
 #pragma unroll 1

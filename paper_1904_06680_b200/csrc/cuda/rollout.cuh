@@ -541,14 +541,6 @@ KernelFn kernel_of_g() {
 
 // grid mode of the field (0 x-buckets, 1 2-D, 2 2-D with cell boxes) -- a
 // separate instantiation each, so the small-field kernel stays lean.
-// Kind 3 = x-buckets staged in shared memory (typed shared loads).
-inline int grid_kind(int mode, int field_smem_bytes) {
-#if PARAPLAN_SMEM_FIELD
-  return mode == 0 && field_smem_bytes > 0 ? 3 : mode;
-#else
-  return mode;
-#endif
-}
 template <typename Real, class Net>
 KernelFn kernel_of(int kind) {
   switch (kind) {
@@ -584,7 +576,7 @@ int launch_generate_impl(const RoundArgs& a, void* stream) {
 template <typename Real, class Net>
 int launch_rollout_impl(const RoundArgs& a, void* stream) {
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  auto k = kernel_of<Real, Net>(grid_kind(a.grid_mode, a.field_smem_bytes));
+  auto k = kernel_of<Real, Net>(grid_kind(a.grid_mode, a.field_smem_bytes, a.field_ns, a.field_nd));
   const size_t smem = static_cast<size_t>(a.field_smem_bytes);
   if (smem > 32 * 1024) {
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
@@ -634,7 +626,7 @@ int launch_refine_impl(const RoundArgs& a, void* stream) {
 
 template <typename Real, class Net>
 int shape_impl(int device, int field_bytes, int grid, LaunchShape* out) {
-  auto k = kernel_of<Real, Net>(grid_kind(grid, field_bytes));
+  auto k = kernel_of<Real, Net>(grid);
   const bool refill = refill_schedule<Net>();
   const int smem_bytes = field_bytes;
   out->queue_bytes = 0;
