@@ -306,7 +306,10 @@ void certify_round(pp_handle* h, ppdev::RoundArgs& a, uint64_t t, int iter, int 
     double cost;  // terminal cost (cls 0/1) or path length (cls 2)
     double k1, k2;
   };
-  std::unordered_map<int64_t, Exact> known;
+  // exact keys of every candidate evaluated so far, by increasing flat
+  // index (restart-major): a restart's entries are one contiguous range
+  std::vector<std::pair<int64_t, Exact>> known;
+  const auto by_index = [](const std::pair<int64_t, Exact>& kv, int64_t s) { return kv.first < s; };
   auto exact_of = [&](int64_t s) {  // the reference's own FP64 arithmetic
     const int r = static_cast<int>(s / count);
     const int cand = static_cast<int>(c0 + (s - r * count));
@@ -388,7 +391,8 @@ void certify_round(pp_handle* h, ppdev::RoundArgs& a, uint64_t t, int iter, int 
         reinterpret_cast<const int64_t*>(static_cast<const char*>(h->h_round.p) + kSelOff);
     list.clear();
     for (uint32_t i = 0; i < n_sel; ++i) {
-      if (known.find(sl[i]) == known.end()) list.push_back(sl[i]);
+      const auto it = std::lower_bound(known.begin(), known.end(), sl[i], by_index);
+      if (it == known.end() || it->first != sl[i]) list.push_back(sl[i]);
     }
     std::sort(list.begin(), list.end());
     list.erase(std::unique(list.begin(), list.end()), list.end());
@@ -413,6 +417,7 @@ void certify_round(pp_handle* h, ppdev::RoundArgs& a, uint64_t t, int iter, int 
                          cudaMemcpyDeviceToHost, h->stream),
          "refine D2H");
       ck(cudaStreamSynchronize(h->stream), "refine kernel");
+      phase("refine64");
       h->timing.launches += 1;
       std::vector<int> best(rc, -1);
       for (size_t i = 0; i < dev.size(); ++i) {
@@ -436,7 +441,18 @@ void certify_round(pp_handle* h, ppdev::RoundArgs& a, uint64_t t, int iter, int 
       h->pool->run(static_cast<int>(ties.size()),
                    [&](int j) { got[ties[j]] = exact_of(list[ties[j]]); });
     }
-    for (size_t i = 0; i < list.size(); ++i) known[list[i]] = got[i];
+    phase("exact");
+    {  // merge the (sorted, new) list into the known keys
+      std::vector<std::pair<int64_t, Exact>> merged;
+      merged.reserve(known.size() + list.size());
+      size_t k = 0;
+      for (size_t i = 0; i < list.size(); ++i) {
+        while (k < known.size() && known[k].first < list[i]) merged.push_back(known[k++]);
+        merged.emplace_back(list[i], got[i]);
+      }
+      while (k < known.size()) merged.push_back(known[k++]);
+      known.swap(merged);
+    }
 
     // certify or widen each uncertified restart
     bool all = true;
@@ -445,13 +461,14 @@ void certify_round(pp_handle* h, ppdev::RoundArgs& a, uint64_t t, int iter, int 
       const ppdev::SelBound& bd = bound[r];
       int64_t win = -1;
       const Exact* e = nullptr;
-      for (const auto& kv : known) {
-        if (kv.first / count != r) continue;
-        const Exact& q = kv.second;
-        if (e == nullptr || key_better({q.cls, q.k1, q.k2}, {e->cls, e->k1, e->k2}) ||
-            (q.cls == e->cls && q.k1 == e->k1 && q.k2 == e->k2 && kv.first < win)) {
+      // increasing index order: among equal keys the first (lowest) wins
+      const auto hi = std::lower_bound(known.begin(), known.end(), (r + 1) * count, by_index);
+      for (auto it = std::lower_bound(known.begin(), known.end(), r * count, by_index); it != hi;
+           ++it) {
+        const Exact& q = it->second;
+        if (e == nullptr || key_better({q.cls, q.k1, q.k2}, {e->cls, e->k1, e->k2})) {
           e = &q;
-          win = kv.first;
+          win = it->first;
         }
       }
       const double slack = 0.5 * (rho * bd.thr + alpha);

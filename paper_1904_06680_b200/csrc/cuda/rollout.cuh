@@ -445,8 +445,9 @@ __global__ void __launch_bounds__(128) refine_kernel(const RoundArgs a) {
   start_features(K, s0);
   Net64 net = RefineNet<Net64>::make(a);
   // warp-uniform bound so every lane of a live warp keeps stepping
+  // warps numbered block-fastest, so a short window spreads over every SM
   const unsigned stride = gridDim.x * blockDim.x;
-  for (unsigned base = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); base < n_sel;
+  for (unsigned base = ((threadIdx.x >> 5) * gridDim.x + blockIdx.x) * 32u; base < n_sel;
        base += stride) {
     const unsigned i = base + (threadIdx.x & 31u);
     const bool valid = i < n_sel;
