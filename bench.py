@@ -170,11 +170,20 @@ def run_b200(a):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # more ranks than GPUs (a code-path check on a small box, not a measurement):
+    # ranks share devices and exchange records over gloo (NCCL refuses two
+    # ranks on one GPU)
+    n_dev = torch.cuda.device_count()
+    shared = world > n_dev
+    local = local % max(n_dev, 1)
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     def barrier():
         if dist is not None:
@@ -223,7 +232,7 @@ def run_b200(a):
         barrier()
         total_ms = sum(dev_ms)
         if dist is not None:
-            t = torch.tensor([total_ms], device=f"cuda:{local}")
+            t = torch.tensor([total_ms], device="cpu" if shared else f"cuda:{local}")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             total_ms = float(t.item())
         value = model.n_candidates * H * a.steps / (total_ms * 1e-3)
@@ -277,7 +286,8 @@ def run_b200(a):
         barrier()
         e2e_s = time.perf_counter() - t0
     if dist is not None:
-        t = torch.tensor([e2e_s], device=f"cuda:{local}", dtype=torch.float64)
+        t = torch.tensor([e2e_s], device="cpu" if shared else f"cuda:{local}",
+                         dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
     e2e_value = model.n_candidates * H * a.steps / e2e_s
@@ -314,7 +324,10 @@ def run_b200(a):
                        "rollout_precision": "fp32" if a.precision == 32 else "fp64",
                        "winner": "certified: FP32 window re-ranked in the reference's FP64 "
                                  "arithmetic (PlannerConfig.refine)",
-                       "l2": "flushed (256 MiB write) between timed steps"},
+                       "l2": "flushed (256 MiB write) between timed steps",
+                       **({"devices_shared": f"{world} ranks on {n_dev} GPU(s): code-path "
+                                             "check only, not a scaling measurement"}
+                          if shared else {})},
             "value_timing": "CUDA events on the planner stream around each sampling round "
                             "(generate + rollout + window-select kernels and the host "
                             "certification between them), snapshot resident in HBM",
