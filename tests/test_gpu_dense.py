@@ -104,3 +104,27 @@ def test_raw_points_errors_and_edge_cases():
         o2, th2, tr2 = dp.plan_step_points(snap, sub, w.t)
         assert np.array_equal(th1, th2) and np.array_equal(tr1, tr2)
         assert o1.evaluated == o2.evaluated
+
+
+@pytest.mark.parametrize("precision", [32, 64])
+@pytest.mark.parametrize("n, movers", [(12, False), (40, True), (100, True), (100, False)])
+def test_small_fields_every_kernel_kind(n, movers, precision):
+    """Small clouds on the road ahead, one per rollout kernel kind: all-static
+    and all-dynamic x-buckets staged in shared memory with one part (kind 3;
+    <= 64 points with a mover are made all-dynamic), and a mixed cloud of 100
+    points (x-buckets with both parts, kind 0). The plan must be the oracle's."""
+    import math
+    rng = np.random.default_rng(n + (1000 if movers else 0))
+    pts = np.zeros((n, 4))
+    pts[:, 0] = rng.uniform(4.0, 30.0, n)
+    pts[:, 1] = rng.uniform(-3.5, 3.5, n)
+    if movers:
+        dyn = rng.random(n) < 0.3
+        pts[dyn, 2] = rng.choice([0.0, math.pi, 0.5 * math.pi], dyn.sum())
+        pts[dyn, 3] = rng.uniform(0.0, 8.0, dyn.sum())
+    w = workloads.c5(1 << 13, 30, n, precision=precision)
+    snap = abi.Snapshot(ev=w.snapshot.ev, actuator_delta=w.snapshot.actuator_delta,
+                        prev_action=w.snapshot.prev_action, goal=w.snapshot.goal,
+                        field=abi.extrapolate(pts, w.model.H))
+    w.snapshot = snap
+    _plan_equal(w)
