@@ -41,6 +41,42 @@ __device__ __forceinline__ Key make_key(int cls, int h, Real path, Real term, in
   return k;
 }
 
+// Lane-local best of the FP32 rollout: the same key with float components.
+// The FP64 key of an FP32 rollout holds exactly these float values (an int
+// t_goal or a float cost, widened), so the order is the same and the lane
+// compares in FP32 without conversions; widened only when flushed.
+struct KeyF {
+  int cls;
+  int idx;
+  float k1, k2;
+};
+__device__ __forceinline__ bool prefer(const KeyF& a, const KeyF& b) {
+  if (a.cls != b.cls) return a.cls > b.cls;
+  if (a.k1 != b.k1) return a.k1 > b.k1;
+  if (a.k2 != b.k2) return a.k2 > b.k2;
+  return static_cast<unsigned>(a.idx) < static_cast<unsigned>(b.idx);
+}
+__device__ __forceinline__ Key to_key(const Key& k) { return k; }
+__device__ __forceinline__ Key to_key(const KeyF& k) {
+  return Key{k.cls, k.idx, static_cast<double>(k.k1), static_cast<double>(k.k2)};
+}
+template <typename Real>
+using LaneKey = typename std::conditional<sizeof(Real) == sizeof(float), KeyF, Key>::type;
+template <typename Real>
+__device__ __forceinline__ LaneKey<Real> lane_empty() {
+  return LaneKey<Real>{-1, -1, Real(0), Real(0)};
+}
+template <typename Real>
+__device__ __forceinline__ LaneKey<Real> make_lane_key(int cls, int h, Real path, Real term,
+                                                       int idx) {
+  LaneKey<Real> k;  // src/planner.cpp:27-38
+  k.cls = cls;
+  k.idx = idx;
+  k.k1 = cls == 2 ? -static_cast<Real>(h) : -term;
+  k.k2 = cls == 2 ? -path : Real(0);
+  return k;
+}
+
 __device__ __forceinline__ Key shfl_key(const Key& k, int off) {
   Key o;
   o.cls = __shfl_down_sync(kFull, k.cls, off);
@@ -232,17 +268,18 @@ __device__ __forceinline__ void finish_round(const RoundArgs& a, const Rec* recs
 
 // Warp-cooperative flush of the lanes' best keys (flagged by `flush`) into
 // the warp's per-restart shared table, one restart at a time.
-__device__ __forceinline__ void flush_bests(bool& flush, Key& best, int best_r, Key* table_w,
+template <class LK>
+__device__ __forceinline__ void flush_bests(bool& flush, LK& best, int best_r, Key* table_w,
                                             int lane) {
   unsigned pend = __ballot_sync(kFull, flush);
   while (pend != 0u) {
     const int r0 = __shfl_sync(kFull, best_r, __ffs(pend) - 1);
     const bool mine = flush && best_r == r0;
-    const Key k = warp_best(mine ? best : empty_key());
+    const Key k = warp_best(mine ? to_key(best) : empty_key());
     if (lane == 0 && (table_w[r0].cls < 0 || prefer(k, table_w[r0]))) table_w[r0] = k;
     if (mine) {
       flush = false;
-      best = empty_key();
+      best.cls = -1;
     }
     pend = __ballot_sync(kFull, flush);
   }

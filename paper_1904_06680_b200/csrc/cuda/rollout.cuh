@@ -133,12 +133,14 @@ __global__ void __launch_bounds__(kBlock, refill_min_blocks<Real, Net>())
   bool active = false;
   int my_r = 0;
   int my_c = 0;  // local candidate index within [0, count)
-  Key best = empty_key();
+  LaneKey<Real> best = lane_empty<Real>();
   int best_r = -1;
   int q_head = 32, q_count = 0, q_r = 0, q_c0 = 0;
   bool exhausted = false;
-  unsigned long long n_steps = 0, n_states = 0;
+  unsigned n_steps = 0, n_states = 0;  // per lane: a few candidates x H
   const bool track = a.keys_only == 0;  // lane bests (one restart) or keys only
+  // lane bests can cross restarts only when a launch holds several
+  const bool cross = track && a.restart_count > 1;
 
   for (;;) {
     // -------- hand the warp's current batch to idle lanes --------
@@ -165,11 +167,16 @@ __global__ void __launch_bounds__(kBlock, refill_min_blocks<Real, Net>())
           my_r = q_r;
           my_c = q_c0 + q_head + rank;
           const int64_t sidx = static_cast<int64_t>(my_r) * a.count + my_c;
-          // contiguous record: one address, immediate offsets, no extra registers
-          const Real* rp = reinterpret_cast<const Real*>(recs + sidx * V);
+          // contiguous 16-byte aligned record: V vector loads
+          union {
+            Real v[W];
+            Vec16<Real> q[V];
+          } rec;
 #pragma unroll
-          for (int i = 0; i < P; ++i) net.w[i] = __ldg(rp + i);
-          L.start(K, __ldg(rp + P), __ldg(rp + P + 1));
+          for (int j = 0; j < V; ++j) rec.q[j] = __ldg(recs + sidx * V + j);
+#pragma unroll
+          for (int i = 0; i < P; ++i) net.w[i] = rec.v[i];
+          L.start(K, rec.v[P], rec.v[P + 1]);
           active = true;
         }
         q_head += __popc(need) < avail ? __popc(need) : avail;
@@ -182,20 +189,22 @@ __global__ void __launch_bounds__(kBlock, refill_min_blocks<Real, Net>())
     const int cls = advance<Real, kGrid>(L, net, K, f, H);
     const bool done = active && cls >= 0;
     // lane bests are per restart: flush the old one before crossing over
-    bool flush = track && done && best.cls >= 0 && best_r != my_r;
-    if (__any_sync(kFull, flush)) flush_bests(flush, best, best_r, table[warp], lane);
+    if (cross) {
+      bool flush = done && best.cls >= 0 && best_r != my_r;
+      if (__any_sync(kFull, flush)) flush_bests(flush, best, best_r, table[warp], lane);
+    }
     if (done) {
       const Real term = terminal_cost(L, K);
       if (track) {
-        const Key k =
-            make_key<Real>(cls, L.h, L.path, term, static_cast<int>(a.cand_begin + my_c));
+        const LaneKey<Real> k =
+            make_lane_key<Real>(cls, L.h, L.path, term, static_cast<int>(a.cand_begin + my_c));
         if (best.cls < 0 || prefer(k, best)) {
           best = k;
           best_r = my_r;
         }
       }
-      n_steps += static_cast<unsigned long long>(L.h);
-      n_states += static_cast<unsigned long long>(L.h + 1);
+      n_steps += static_cast<unsigned>(L.h);
+      n_states += static_cast<unsigned>(L.h + 1);
       if (a.per_sample != nullptr) {
         write_sample(a, static_cast<int64_t>(my_r) * a.count + my_c, cls, L, term);
       }
@@ -205,8 +214,8 @@ __global__ void __launch_bounds__(kBlock, refill_min_blocks<Real, Net>())
   }
 
   // -------- flush lane bests, combine warps, publish CTA records --------
-  const unsigned long long steps = block_sum(n_steps, red_sum);
-  const unsigned long long states = block_sum(n_states, red_sum);
+  const unsigned long long steps = block_sum(static_cast<unsigned long long>(n_steps), red_sum);
+  const unsigned long long states = block_sum(static_cast<unsigned long long>(n_states), red_sum);
   if (threadIdx.x == 0) {
     atomicAdd(&a.exec[0], steps);
     atomicAdd(&a.exec[1], states);
@@ -367,8 +376,8 @@ __global__ void __launch_bounds__(kBlock) lockstep_kernel(const RoundArgs a) {
     // tile records are restart-major: [r][tile within restart]
     if (threadIdx.x == 0) a.tile_recs[tile] = Rec{best.cls, best.idx, best.k1, best.k2};
   }
-  const unsigned long long steps = block_sum(n_steps, red_sum);
-  const unsigned long long states = block_sum(n_states, red_sum);
+  const unsigned long long steps = block_sum(static_cast<unsigned long long>(n_steps), red_sum);
+  const unsigned long long states = block_sum(static_cast<unsigned long long>(n_states), red_sum);
   if (threadIdx.x == 0) {
     atomicAdd(&a.exec[0], steps);
     atomicAdd(&a.exec[1], states);
