@@ -256,3 +256,39 @@ def test_device_theta_draws_match_reference_rng(sizes):
             if precision == 64:  # most draws agree to the last bit
                 assert np.mean(dev == want) > 0.5
         dp.close()
+
+
+@pytest.mark.parametrize("log2n, H", [(24, 10), (26, 10)])
+def test_maximum_size_round(log2n, H):
+    """The largest BASELINE sweep size (2^26 samples, C5): flat indices,
+    batch tickets and counters past 2^24, and the certified winner still
+    the reference's. The oracle cannot evaluate the whole round, so: the
+    returned plan equals the host FP64 re-simulation of the winner's theta;
+    the winner is at least as good (exact keys) as every candidate of a
+    random sample and of the last 1024 indices, all evaluated by the oracle;
+    and all 2^k candidates were evaluated."""
+    w = workloads.c2(samples=1 << 10)
+    n = 1 << log2n
+    m = abi.Model(H=H, n_restarts=1, n_candidates=n, precision=32)
+    dp = capi.DevicePlanner(m)
+    o, theta, traj = dp.plan_step(w.snapshot, w.t)
+    assert o.evaluated == n
+    win = int(o.winner.candidate)
+    assert 0 <= win < n
+    port = Port(m)
+    th_ref = port.sample_candidate(np.zeros(18), w.t, 0, 0, win)
+    assert np.array_equal(theta, th_ref)
+    st, tr = port.rollout(w.snapshot, th_ref)
+    assert np.array_equal(traj, tr)
+    cls = 0 if st.collided else (2 if st.reached else 1)
+    k1 = -float(st.t_goal) if cls == 2 else -st.terminal_cost
+    k2 = -st.path_length if cls == 2 else 0.0
+    assert (cls, k1, k2) == (o.winner.cls, o.winner.k1, o.winner.k2)
+    rng = np.random.default_rng(log2n)
+    picks = np.unique(np.concatenate([rng.integers(0, n, 3072), np.arange(n - 1024, n)]))
+    for c in picks:
+        s = port.eval_candidates(w.snapshot, w.t, 0, 0, np.zeros(18), int(c), int(c) + 1)[0]
+        c_cls = 0 if s["collided"] else (2 if s["reached"] else 1)
+        c_k1 = -float(s["t_goal"]) if c_cls == 2 else -s["terminal_cost"]
+        c_k2 = -s["path_length"] if c_cls == 2 else 0.0
+        assert (c_cls, c_k1, c_k2) <= (cls, k1, k2) or (c_cls, c_k1, c_k2) == (cls, k1, k2), c
