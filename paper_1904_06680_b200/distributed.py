@@ -89,8 +89,9 @@ class ShardedPlanner:
         last = {"snap": None}
 
         def evaluate(snap, t, it, r0, rc, center, c0, c1):
-            # upload the snapshot once per tick; later rounds reuse it in HBM
-            fresh = snap is not last["snap"]
+            # upload the snapshot once per plan step (its first round is
+            # iteration 0 of every restart); later rounds reuse it in HBM
+            fresh = (it == 0 and r0 == 0) or snap is not last["snap"]
             last["snap"] = snap
             return dp.evaluate(snap if fresh else None, t, it, r0, rc, center, c0, c1)[0]
 
