@@ -296,11 +296,12 @@ def run_b200(a):
     kern_avg_ms = sum(kern_ms) / len(kern_ms)
     flops = workloads.algorithmic_flops([5, 2, 2], N, steps_exec // a.steps, states // a.steps)
     achieved = flops / (kern_avg_ms * 1e-3) / 1e12
-    traffic, pipes = None, None
+    traffic, traffic_live, pipes = None, None, None
     tf = ROOT / "profiles" / "traffic.json"
     if tf.exists():
         tj = json.loads(tf.read_text())
         traffic = tj.get("dram_bytes_per_launch")
+        traffic_live = tj.get("live_dram_bytes_per_launch")
         pipes = tj.get("pipes")
 
     out = None
@@ -340,7 +341,8 @@ def run_b200(a):
             "gpu_launches": launches,
             "roofline": {"bound": "fp32", "achieved": achieved, "peak": peak_tf,
                          "unit": "TFLOP/s", "frac": achieved / peak_tf if peak_tf else None,
-                         "traffic": traffic, "peak_source": "FFMA loop measured in this run",
+                         "traffic": traffic, "traffic_live": traffic_live,
+                         "peak_source": "FFMA loop measured in this run",
                          "ncu_pipes": pipes,
                          "kernel_ms": kern_avg_ms, "flops_per_launch": flops,
                          "executed_steps_per_launch": steps_exec // a.steps},
