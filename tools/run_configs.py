@@ -74,6 +74,10 @@ if __name__ == "__main__":
     ap.add_argument("--fp64", type=int, default=1)
     ap.add_argument("--c5-n", default="100,1000,10000,100000")
     ap.add_argument("--c5-H", default="10,30,100")
+    ap.add_argument("--c5-samples", default="12,16,20,24,26",
+                    help="log2 sample counts of the C5 samples sweep (N=1000, H=30)")
+    ap.add_argument("--c4-shard", type=int, default=1 << 19,
+                    help="C4 per-GPU shard (2^22 samples over 8 GPUs)")
     a = ap.parse_args()
     res = {}
     which = a.which.split(",")
@@ -87,8 +91,25 @@ if __name__ == "__main__":
         res["C3"] = closed_loop(1 << 20, 200, a.c3_ticks)
     if "C4" in which:
         res["C4"] = time_round(workloads.c4(samples=a.c4_samples), reps=1)
+        # one GPU's shard of the BASELINE C4 run (2^22 samples over 8 GPUs):
+        # the candidates [0, 2^19) of the 2^22-sample round
+        w = workloads.c4(samples=1 << 22)
+        dp = capi.DevicePlanner(w.model)
+        dp.upload(w.snapshot)
+        ts = []
+        for _ in range(3):
+            t0 = time.perf_counter()
+            dp.evaluate(None, w.t, 0, 0, 1, None, 0, a.c4_shard)
+            ts.append((time.perf_counter() - t0) * 1e3)
+        tm = dp.timing()
+        res["C4_shard_of_2^22_over_8"] = dict(samples=a.c4_shard, wall_ms=min(ts[1:]),
+                                              device_ms=tm.kernel_ms, steps=tm.executed_steps)
+        dp.close()
     if "C5" in which:
         for n_pts in map(int, a.c5_n.split(",")):
             for H in map(int, a.c5_H.split(",")):
                 res[f"C5_n{n_pts}_H{H}"] = time_round(workloads.c5(1 << 20, H, n_pts), reps=1)
+        for k in map(int, a.c5_samples.split(",")):
+            r = time_round(workloads.c5(1 << k, 30, 1000), reps=1)
+            res[f"C5_samples2^{k}_n1000_H30"] = r
     print(json.dumps(res, indent=1))
