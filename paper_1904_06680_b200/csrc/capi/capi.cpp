@@ -58,6 +58,16 @@ void prewarm(pp_handle* h) {
     if (h->fp64) ppdev::shape_f64(h->kind, h->device, 16, 3, &sh);
     else ppdev::shape_f32(h->kind, h->device, 16, 3, &sh);
     ck(cudaStreamSynchronize(h->stream), "warm-up");
+    // An FP32 planner whose certification overflows redoes the round in
+    // FP64, with twice the theta record and key sizes. Growing those buffers
+    // at that tick cost 0.25-0.8 s on B200 (C3 tick 38), so rounds of up to
+    // 2^23 candidates reserve the FP64 sizes here.
+    const size_t total = static_cast<size_t>(h->cfg.n_candidates) * std::max(1, rc);
+    if (!h->fp64 && h->rerank && total <= (size_t{1} << 23)) {
+      const ppdev::LaunchShape s64 = launch_shape(h, true, 0, 0);
+      if (s64.refill) h->d_theta.reserve(total * s64.theta_elem * sizeof(double), "theta buffer");
+      h->d_skeys.reserve(total * sizeof(ppdev::SKey), "sample keys");
+    }
   } catch (...) {
     cudaGetLastError();
   }

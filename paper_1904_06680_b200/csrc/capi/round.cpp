@@ -167,10 +167,12 @@ void run_round_launch(pp_handle* h, uint64_t t, int iter, int r0, int rc, const 
     a.sel_alpha = fp64 ? 1e-13 : 1e-6;
   }
 
+  phase("buffers");
   ck(cudaEventRecord(h->ev0, h->stream), "event");
   ck(static_cast<cudaError_t>(fp64 ? ppdev::launch_generate_f64(h->kind, a, h->stream)
                                    : ppdev::launch_generate_f32(h->kind, a, h->stream)),
      "theta generator launch");
+  phase("generator");
   if (h->pending_field) {  // bin + upload the field while the generator runs
     consume_pending_field(h, true);
     const ppdev::RoundArgs& b = h->base;
