@@ -223,6 +223,74 @@ __device__ __forceinline__ void scan_boxed(const Field<Real>& f, int ncy, int cx
   }
 }
 
+// Dense static part for ONE query, scanned by the whole warp: lane k takes
+// the window cells k, k + 32, ... and applies scan_boxed's per-cell rule
+// (a column holding <= kDenseCol points in the window: all its points; else
+// the cell box, then the chunk boxes, then the points of straddling chunks).
+// The contributions are scan_boxed's without its early exit, so the
+// max margin decides the same verdict and the same marginal flag. Returns
+// the warp-wide max (every lane). Used when few lanes of a warp still need
+// a dense scan (the end of a round), where the lane-serial scan would run
+// one long latency chain per lane.
+template <typename Real>
+__device__ __forceinline__ Real coop_scan_boxed(const Field<Real>& f, int ncy, int cx_lo, int cx_hi,
+                                                int cy_lo, int cy_hi, const Consts<Real>& K,
+                                                Real x, Real y, Real c, Real s, Real kx, Real ky,
+                                                int lane) {
+  const auto* pts = f.spts;
+  const int* st = f.sst;
+  const Real ac = fabs(c), as = fabs(s);
+  const int nrow = cy_hi - cy_lo + 1;
+  const int ncell = (cx_hi - cx_lo + 1) * nrow;
+  Real best = Real(-1e30);
+  for (int idx = lane; idx < ncell; idx += 32) {
+    const int col = idx / nrow;
+    const int cell0 = (cx_lo + col) * ncy + cy_lo;
+    const int cell = cell0 + (idx - col * nrow);
+    const int clo = st[cell];
+    const int cnt = st[cell + 1] - clo;
+    if (cnt == 0) continue;
+    if (st[cell0 + nrow] - st[cell0] <= kDenseCol) {  // sparse column: its points
+      for (int i = 0; i < cnt; ++i) {
+        const auto m = pts[clo + i];
+        best = fmax(best, point_margin<Real>(K, x, y, c, s, kx, ky, m.x, m.y));
+      }
+      continue;
+    }
+    const Real bm = box_margin(K, c, s, ac, as, kx, ky, f.sbox[2 * cell], f.sbox[2 * cell + 1]);
+    if (bm > Real(0)) {
+      best = fmax(best, bm);
+      continue;
+    }
+    if (bm < Real(0)) continue;
+    const int ch0 = f.cst[cell], nch = f.cst[cell + 1] - ch0;
+    const int csz = chunk_size_dev(cnt);
+    for (int j = 0; j < nch; ++j) {
+      const Real cm = box_margin(K, c, s, ac, as, kx, ky, f.cbox[2 * (ch0 + j)],
+                                 f.cbox[2 * (ch0 + j) + 1]);
+      if (cm > Real(0)) {
+        best = fmax(best, cm);
+      } else if (cm == Real(0)) {
+        const int at = clo + j * csz;
+        const int left = min(csz, clo + cnt - at);
+        for (int i = 0; i < left; ++i) {
+          const auto m = pts[at + i];
+          best = fmax(best, point_margin<Real>(K, x, y, c, s, kx, ky, m.x, m.y));
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) best = fmax(best, __shfl_xor_sync(kFull, best, off));
+  return best;
+}
+
+// At most this many lanes needing a dense static scan: the warp scans each
+// of their windows together (coop_scan_boxed) instead of lane by lane.
+#ifndef PARAPLAN_COOP_LANES
+#define PARAPLAN_COOP_LANES 4
+#endif
+
 // Collision of the chassis at (x, y, phi) with the field at state h. Only the
 // cells covering the world-frame bounding box of the chassis rectangle (+ a
 // pad of an eighth of a cell) are visited: the reference reports a point
@@ -233,7 +301,8 @@ __device__ __forceinline__ void scan_boxed(const Field<Real>& f, int ncy, int cx
 // flip). Warp-synchronous: all 32 lanes call it, every loop is warp-uniform.
 template <typename Real, int kGrid>
 __device__ __forceinline__ Real collide_margin(const Field<Real>& f, const Consts<Real>& K, int h,
-                                               Real x, Real y, Real c, Real s, Real stop) {
+                                               Real x, Real y, Real c, Real s, Real stop,
+                                               bool live = true) {
   const int ncx = f.ncx, ncy = f.ncy;
   const Real ac = fabs(c), as = fabs(s);
   const Real top = Real(ncx - 1);
@@ -272,7 +341,27 @@ __device__ __forceinline__ Real collide_margin(const Field<Real>& f, const Const
     const int* st = dyn ? f.dst + static_cast<size_t>(h) * (ncx * ncy + 1) : f.sst;
     if constexpr (kGrid == 2) {
       if (!dyn) {
-        scan_boxed<Real>(f, ncy, cx_lo, cx_hi, cy_lo, cy_hi, K, x, y, c, s, kx, ky, stop, best);
+        // lanes whose rollout is over (idle at the end of a round) skip the
+        // dense scan; a warp with few live lanes scans each of their
+        // windows together
+        const unsigned want = __ballot_sync(kFull, live);
+        if (__popc(want) <= PARAPLAN_COOP_LANES) {
+          const int lane = static_cast<int>(threadIdx.x & 31u);
+          for (unsigned pend = want; pend != 0u; pend &= pend - 1u) {
+            const int src = __ffs(pend) - 1;
+            const Real qx = __shfl_sync(kFull, x, src), qy = __shfl_sync(kFull, y, src);
+            const Real qc = __shfl_sync(kFull, c, src), qs = __shfl_sync(kFull, s, src);
+            const Real qkx = __shfl_sync(kFull, kx, src), qky = __shfl_sync(kFull, ky, src);
+            const int q0 = __shfl_sync(kFull, cx_lo, src), q1 = __shfl_sync(kFull, cx_hi, src);
+            const int r0 = __shfl_sync(kFull, cy_lo, src), r1 = __shfl_sync(kFull, cy_hi, src);
+            const Real m =
+                coop_scan_boxed<Real>(f, ncy, q0, q1, r0, r1, K, qx, qy, qc, qs, qkx, qky, lane);
+            if (lane == src) best = fmax(best, m);
+          }
+        } else {
+          scan_boxed<Real>(f, ncy, cx_lo, live ? cx_hi : cx_lo - 1, cy_lo, cy_hi, K, x, y, c, s,
+                           kx, ky, stop, best);
+        }
         continue;
       }
     }

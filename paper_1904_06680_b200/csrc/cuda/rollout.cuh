@@ -186,7 +186,7 @@ __global__ void __launch_bounds__(kBlock, refill_min_blocks<Real, Net>())
 
     // -------- one rollout state per lane --------
     // every lane steps (idle lanes only at the stream tail, results unused)
-    const int cls = advance<Real, kGrid>(L, net, K, f, H);
+    const int cls = advance<Real, kGrid>(L, net, K, f, H, active);
     const bool done = active && cls >= 0;
     // lane bests are per restart: flush the old one before crossing over
     if (cross) {

@@ -43,14 +43,14 @@ __device__ __forceinline__ void start_features(const Consts<Real>& K, Real s[5])
 // so the warp never splits into per-outcome paths.
 template <typename Real, int kGrid, class Net>
 __device__ __forceinline__ int advance(Lane<Real>& L, const Net& net, const Consts<Real>& K,
-                                       const Field<Real>& f, int H) {
+                                       const Field<Real>& f, int H, bool live = true) {
   Real sphi, cphi;
   M<Real>::sc(L.phi, &sphi, &cphi);
   L.ephi = M<Real>::wrap(K.gphi - L.phi);
   bool hit = false;
   if (f.Ns + f.Nd > 0) {
     // a lane may stop at a hit whose margin is too large to flip
-    const Real cm = collide_margin<Real, kGrid>(f, K, L.h, L.x, L.y, cphi, sphi, K.dmarg);
+    const Real cm = collide_margin<Real, kGrid>(f, K, L.h, L.x, L.y, cphi, sphi, K.dmarg, live);
     hit = cm > Real(0);
     // a narrow hit might be free in exact arithmetic (a better outcome)
     L.marg |= hit & (cm < K.dmarg);
