@@ -184,6 +184,7 @@ void run_round_launch(pp_handle* h, uint64_t t, int iter, int r0, int rc, const 
     a.grid_nx = b.grid_nx;
     a.grid_ny = b.grid_ny;
     a.grid_mode = b.grid_mode;
+    a.coop = b.coop;
     a.grid_x0 = b.grid_x0;
     a.grid_y0 = b.grid_y0;
     a.grid_g = b.grid_g;

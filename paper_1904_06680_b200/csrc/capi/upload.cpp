@@ -69,6 +69,10 @@ void finish_field(pp_handle* h, ppdev::RoundArgs& a) {
   a.grid_y0 = b.y0;
   a.grid_g = b.g;
   a.grid_mode = b.mode();
+  // cooperative window scans pay where a window holds many points: dense
+  // static clouds (cell boxes), or 2-D grids averaging >= 1 point per cell
+  a.coop = b.mode() == 2 ||
+           (b.mode() == 1 && b.Ns + static_cast<double>(b.Nd) >= static_cast<double>(b.cells()));
   const size_t elem = h->fp64 ? sizeof(double) : sizeof(float);
   const ppfield::Layout l = ppfield::layout(b, elem), l64 = ppfield::layout(b, sizeof(double));
   a.lay = {static_cast<int64_t>(l.dpts), static_cast<int64_t>(l.sst), static_cast<int64_t>(l.dst),

@@ -114,7 +114,7 @@ struct RoundArgs {
   int32_t field_ns, field_nd;  // static points, dynamic points per row
   int32_t grid_nx, grid_ny;    // cells (grid_ny == 1: x-buckets)
   int32_t grid_mode;           // 0 x-buckets, 1 2-D by column, 2 2-D with static cell boxes
-  int32_t _pad_mode;
+  int32_t coop;                // 2-D grids: warps with few live lanes scan windows together
   double grid_x0, grid_y0, grid_g;  // grid origin and cell size (host side)
   FieldLayout lay;             // byte offsets of the compute-precision image
   FieldLayout lay64;           // byte offsets of the FP64 image (field64)

@@ -22,6 +22,7 @@ struct Field {
   const typename Vec2T<Real>::type* cbox;  // per chunk: (centre), (half extents)
   int Ns, Nd;
   int ncx, ncy;
+  int coop;  // RoundArgs::coop
 };
 
 template <typename Real>
@@ -34,7 +35,7 @@ __device__ __forceinline__ Field<Real> field_at(const RoundArgs& a, const void* 
                      reinterpret_cast<const int*>(p + l.dst),
                      reinterpret_cast<const R2*>(p + l.sbox), reinterpret_cast<const int*>(p + l.cst),
                      reinterpret_cast<const R2*>(p + l.cbox), a.field_ns, a.field_nd, a.grid_nx,
-                     a.grid_ny};
+                     a.grid_ny, a.coop};
 }
 
 // Inside-margin of one point against the chassis at (x, y, phi):
@@ -285,8 +286,33 @@ __device__ __forceinline__ Real coop_scan_boxed(const Field<Real>& f, int ncy, i
   return best;
 }
 
-// At most this many lanes needing a dense static scan: the warp scans each
-// of their windows together (coop_scan_boxed) instead of lane by lane.
+// The points of the window cells (one contiguous range per cell column) for
+// ONE query, scanned by the whole warp: column by column, lane k takes the
+// points k, k + 32, ... Returns the warp-wide max margin (every lane).
+template <typename Real>
+__device__ __forceinline__ Real coop_scan_cells(const typename Vec2T<Real>::type* pts,
+                                                const int* st, int ncy, int cx_lo, int cx_hi,
+                                                int cy_lo, int cy_hi, const Consts<Real>& K,
+                                                Real x, Real y, Real c, Real s, Real kx, Real ky,
+                                                int lane) {
+  Real best = Real(-1e30);
+  for (int k = cx_lo; k <= cx_hi; ++k) {
+    const int cell = k * ncy;
+    const int hi = st[cell + cy_hi + 1];
+    for (int j = st[cell + cy_lo] + lane; j < hi; j += 32) {
+      const auto m = pts[j];
+      best = fmax(best, point_margin<Real>(K, x, y, c, s, kx, ky, m.x, m.y));
+    }
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) best = fmax(best, __shfl_xor_sync(kFull, best, off));
+  return best;
+}
+
+// At most this many live lanes in a warp: the warp scans each of their
+// collision windows together (coop_scan_boxed / coop_scan_cells) instead of
+// lane by lane. At the end of a round most lanes are idle and the few
+// remaining rollouts would otherwise run as long single-lane latency chains.
 #ifndef PARAPLAN_COOP_LANES
 #define PARAPLAN_COOP_LANES 4
 #endif
@@ -331,41 +357,54 @@ __device__ __forceinline__ Real collide_margin(const Field<Real>& f, const Const
                            best);
     return best;
   }
-  // part 0: static points; part 1: the dynamic row of state h (one copy of
-  // the scan code, warp-uniform part loop)
+  const size_t row_cells = static_cast<size_t>(ncx) * ncy + 1;
+  if constexpr (kGrid == 1 || kGrid == 2) {
+    // few live lanes (the end of a round): the warp scans each live lane's
+    // window together, both parts; lanes whose rollout is over scan nothing
+    const unsigned want = __ballot_sync(kFull, live);
+    if (f.coop && __popc(want) <= PARAPLAN_COOP_LANES) {
+      const int lane = static_cast<int>(threadIdx.x & 31u);
+      for (unsigned pend = want; pend != 0u; pend &= pend - 1u) {
+        const int src = __ffs(pend) - 1;
+        const Real qx = __shfl_sync(kFull, x, src), qy = __shfl_sync(kFull, y, src);
+        const Real qc = __shfl_sync(kFull, c, src), qs = __shfl_sync(kFull, s, src);
+        const Real qkx = __shfl_sync(kFull, kx, src), qky = __shfl_sync(kFull, ky, src);
+        const int q0 = __shfl_sync(kFull, cx_lo, src), q1 = __shfl_sync(kFull, cx_hi, src);
+        const int r0 = __shfl_sync(kFull, cy_lo, src), r1 = __shfl_sync(kFull, cy_hi, src);
+        const int qh = __shfl_sync(kFull, h, src);
+        Real m = Real(-1e30);
+        if (f.Ns > 0) {
+          m = kGrid == 2 ? coop_scan_boxed<Real>(f, ncy, q0, q1, r0, r1, K, qx, qy, qc, qs, qkx,
+                                                 qky, lane)
+                         : coop_scan_cells<Real>(f.spts, f.sst, ncy, q0, q1, r0, r1, K, qx, qy,
+                                                 qc, qs, qkx, qky, lane);
+        }
+        if (f.Nd > 0) {
+          m = fmax(m, coop_scan_cells<Real>(f.dpts + static_cast<size_t>(qh) * f.Nd,
+                                            f.dst + static_cast<size_t>(qh) * row_cells, ncy, q0,
+                                            q1, r0, r1, K, qx, qy, qc, qs, qkx, qky, lane));
+        }
+        if (lane == src) best = m;
+      }
+      return best;
+    }
+  }
+  // lane by lane. part 0: static points; part 1: the dynamic row of state h
+  // (one copy of the scan code, warp-uniform part loop)
+  const int cl_hi = live ? cx_hi : cx_lo - 1;  // a lane whose rollout is over scans nothing
 #pragma unroll 1
   for (int part = 0; part < 2; ++part) {
     const bool dyn = part == 1;
     if ((dyn ? f.Nd : f.Ns) == 0) continue;
     const auto* pts = dyn ? f.dpts + static_cast<size_t>(h) * f.Nd : f.spts;
-    const int* st = dyn ? f.dst + static_cast<size_t>(h) * (ncx * ncy + 1) : f.sst;
+    const int* st = dyn ? f.dst + static_cast<size_t>(h) * row_cells : f.sst;
     if constexpr (kGrid == 2) {
       if (!dyn) {
-        // lanes whose rollout is over (idle at the end of a round) skip the
-        // dense scan; a warp with few live lanes scans each of their
-        // windows together
-        const unsigned want = __ballot_sync(kFull, live);
-        if (__popc(want) <= PARAPLAN_COOP_LANES) {
-          const int lane = static_cast<int>(threadIdx.x & 31u);
-          for (unsigned pend = want; pend != 0u; pend &= pend - 1u) {
-            const int src = __ffs(pend) - 1;
-            const Real qx = __shfl_sync(kFull, x, src), qy = __shfl_sync(kFull, y, src);
-            const Real qc = __shfl_sync(kFull, c, src), qs = __shfl_sync(kFull, s, src);
-            const Real qkx = __shfl_sync(kFull, kx, src), qky = __shfl_sync(kFull, ky, src);
-            const int q0 = __shfl_sync(kFull, cx_lo, src), q1 = __shfl_sync(kFull, cx_hi, src);
-            const int r0 = __shfl_sync(kFull, cy_lo, src), r1 = __shfl_sync(kFull, cy_hi, src);
-            const Real m =
-                coop_scan_boxed<Real>(f, ncy, q0, q1, r0, r1, K, qx, qy, qc, qs, qkx, qky, lane);
-            if (lane == src) best = fmax(best, m);
-          }
-        } else {
-          scan_boxed<Real>(f, ncy, cx_lo, live ? cx_hi : cx_lo - 1, cy_lo, cy_hi, K, x, y, c, s,
-                           kx, ky, stop, best);
-        }
+        scan_boxed<Real>(f, ncy, cx_lo, cl_hi, cy_lo, cy_hi, K, x, y, c, s, kx, ky, stop, best);
         continue;
       }
     }
-    scan_part<Real, kGrid>(pts, st, ncy, cx_lo, cx_hi, cy_lo, cy_hi, K, x, y, c, s, kx, ky, stop,
+    scan_part<Real, kGrid>(pts, st, ncy, cx_lo, cl_hi, cy_lo, cy_hi, K, x, y, c, s, kx, ky, stop,
                            best);
   }
   return best;
