@@ -353,8 +353,10 @@ __device__ __forceinline__ Real collide_margin(const Field<Real>& f, const Const
     const bool dyn = f.Nd > 0;
     const auto* pts = dyn ? f.dpts + h * f.Nd : f.spts;
     const int* st = dyn ? f.dst + h * (ncx + 1) : f.sst;
-    scan_part<Real, kGrid>(pts, st, ncy, cx_lo, cx_hi, cy_lo, cy_hi, K, x, y, c, s, kx, ky, stop,
-                           best);
+    // a lane whose rollout is over scans nothing (its window would only
+    // lengthen the warp's point loop)
+    scan_part<Real, kGrid>(pts, st, ncy, cx_lo, live ? cx_hi : cx_lo - 1, cy_lo, cy_hi, K, x, y, c,
+                           s, kx, ky, stop, best);
     return best;
   }
   const size_t row_cells = static_cast<size_t>(ncx) * ncy + 1;
