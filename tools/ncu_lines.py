@@ -22,8 +22,11 @@ for r in rows:
         st = hdr.index("Warp Stall Sampling (All Samples)")
         continue
     if hdr and r and r[0].isdigit():
-        w = int(r[ie] or 0)
-        t = int(r[ti] or 0)
+        try:  # source lines with unescaped quotes (inline asm) break the CSV
+            w = int(r[ie] or 0)
+            t = int(r[ti] or 0)
+        except (ValueError, IndexError):
+            continue
         s = int(r[st] or 0) if r[st].isdigit() else 0
         tw += w
         tt += t
