@@ -392,27 +392,21 @@ __global__ void __launch_bounds__(kBlock) lockstep_kernel(const RoundArgs a) {
 static __global__ void __launch_bounds__(256) select_kernel(const RoundArgs a) {
   wait_prior_grid();  // the rollout's keys and winners
   const int64_t total = a.count * a.restart_count;
-  const bool small = total <= 0x7fffffff;
-  int cur = -1;  // the bound of restart `cur`, loaded when the restart changes
-  SelBound bd{};
   for (int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; s < total;
        s += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int r = a.restart_count == 1
                       ? 0
-                      : (small ? static_cast<int>(static_cast<uint32_t>(s) /
-                                                  static_cast<uint32_t>(a.count))
-                               : static_cast<int>(s / a.count));
-    if (r != cur) {
-      cur = r;
-      if (a.sel_bound != nullptr) {  // widened window of a later pass
-        bd = a.sel_bound[r];
-      } else {  // first pass: around the round winner (its best unflagged candidate)
-        const Rec b =
-            (a.out_free != nullptr && a.out_free[r].cls >= 0) ? a.out_free[r] : a.out[r];
-        bd.cls = b.cls;
-        bd.t_goal = b.cls == 2 ? static_cast<int>(-b.k1) : 0;
-        bd.thr = (b.cls == 2 ? -b.k2 : -b.k1) * (1.0 + a.sel_rho) + a.sel_alpha;
-      }
+                      : (total <= 0x7fffffff ? static_cast<int>(static_cast<uint32_t>(s) /
+                                                                 static_cast<uint32_t>(a.count))
+                                             : static_cast<int>(s / a.count));
+    SelBound bd;
+    if (a.sel_bound != nullptr) {  // widened window of a later pass
+      bd = a.sel_bound[r];
+    } else {  // first pass: around the round winner (its best unflagged candidate)
+      const Rec b = (a.out_free != nullptr && a.out_free[r].cls >= 0) ? a.out_free[r] : a.out[r];
+      bd.cls = b.cls;
+      bd.t_goal = b.cls == 2 ? static_cast<int>(-b.k1) : 0;
+      bd.thr = (b.cls == 2 ? -b.k2 : -b.k1) * (1.0 + a.sel_rho) + a.sel_alpha;
     }
     SKey k;
     if (a.skey32) {
