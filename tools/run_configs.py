@@ -87,6 +87,14 @@ if __name__ == "__main__":
         res["C2"] = time_round(workloads.c2())
         if a.fp64:
             res["C2_fp64"] = time_round(workloads.c2(precision=64))
+    if "defaults" in which or a.which == "C1,C2,C3,C4,C5":
+        # the reference's default PlannerConfig (planner.hpp:21-35: H=200,
+        # 15 restarts x 20480 candidates) on the C2 scene
+        m = workloads.c2_mission()
+        snap = workloads.snapshot_from_mission(m, m.initial_state, 5, 200, 20)
+        w = workloads.Workload("defaults", abi.Model(H=200, n_restarts=15, n_candidates=20480),
+                               snap, 5, "reference PlannerConfig defaults on the C2 scene")
+        res["reference_defaults_R15x20480_H200"] = time_round(w)
     if "C3" in which:
         res["C3"] = closed_loop(1 << 20, 200, a.c3_ticks)
     if "C4" in which:
