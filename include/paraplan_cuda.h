@@ -39,7 +39,8 @@
 extern "C" {
 #endif
 
-#define PP_ABI_VERSION 1
+#define PP_ABI_VERSION 2
+#define PP_MAX_DEVICES 8
 
 typedef enum pp_status {
   PP_OK = 0,
@@ -88,6 +89,13 @@ typedef struct pp_config {
   int32_t precision; /* pp_precision */
   int32_t device;    /* CUDA ordinal */
   int32_t refine;    /* FP32 only: re-rank the near-tie window in FP64 (1 = on) */
+  /* Several GPUs in one process (n_devices > 1; else `device` alone): the
+   * candidates of every sampling round are split into contiguous shards,
+   * shard k on devices[k]; the shard winners (each certified) are merged in
+   * shard order, as the reference merges its worker ranges
+   * (src/planner.cpp:280-281, 310-321), so the plan is the single-GPU one. */
+  int32_t n_devices;
+  int32_t devices[PP_MAX_DEVICES];
 } pp_config;
 
 /* Planner constructor arguments. layer_sizes is MlpArchitecture::layer_sizes

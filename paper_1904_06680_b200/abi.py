@@ -34,7 +34,8 @@ class pp_config(C.Structure):
         ("eps_xi", C.c_double), ("eps_eta", C.c_double), ("eps_phi", C.c_double),
         ("eps_v", C.c_double), ("sigma_log_low", C.c_double), ("sigma_log_high", C.c_double),
         ("master_seed", C.c_uint64), ("threads", C.c_int32), ("precision", C.c_int32),
-        ("device", C.c_int32), ("refine", C.c_int32),
+        ("device", C.c_int32), ("refine", C.c_int32), ("n_devices", C.c_int32),
+        ("devices", C.c_int32 * 8),
     ]
 
 
@@ -127,6 +128,7 @@ class Model:
     precision: int = PP_FP32
     device: int = 0
     refine: int = 1
+    devices: Sequence[int] = ()  # several GPUs in one process (empty: `device`)
     vehicle: dict = field(default_factory=dict)
     norm: dict = field(default_factory=dict)
 
@@ -153,6 +155,11 @@ class Model:
                   "master_seed", "threads", "precision", "device", "refine"):
             setattr(c, k, getattr(self, k))
         c.early_exit = int(bool(self.early_exit))
+        if len(self.devices) > 8:
+            raise ValueError("at most 8 devices per planner")
+        c.n_devices = len(self.devices)
+        for k, d in enumerate(self.devices):
+            c.devices[k] = d
         arr = (C.c_int32 * len(self.layer_sizes))(*self.layer_sizes)
         m.layer_sizes = arr
         m.n_layers = len(self.layer_sizes)

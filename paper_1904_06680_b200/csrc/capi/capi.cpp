@@ -106,6 +106,12 @@ pp_status pp_create(const pp_model* m, pp_handle** out) {
     if (const char* e = std::getenv("PARAPLAN_SEL_RHO")) hp->sel_rho = std::atof(e);
     if (const char* e = std::getenv("PARAPLAN_DMARG")) hp->dmarg32 = std::atof(e);
     hp->device = hp->cfg.device;
+    const int n_dev = m->config.n_devices;
+    if (n_dev > PP_MAX_DEVICES) throw std::invalid_argument("at most 8 devices per planner");
+    if (n_dev > 1) {
+      hp->device = m->config.devices[0];
+      hp->pool_threads = std::max(2, 16 / n_dev);
+    }
 
     int n = 0;
     if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
@@ -133,6 +139,27 @@ pp_status pp_create(const pp_model* m, pp_handle** out) {
   });
   if (st == PP_OK) {
     prewarm(h);
+    // the other shards: the same model on devices[1..n)
+    const pp_status sst = guarded([&] {
+      for (int k = 1; k < m->config.n_devices; ++k) {
+        pp_model mk = *m;
+        mk.config.n_devices = 0;
+        mk.config.device = m->config.devices[k];
+        pp_handle* g = nullptr;
+        if (pp_create(&mk, &g) != PP_OK) throw std::runtime_error(pp_last_error());
+        g->pool_threads = h->pool_threads;
+        h->shards.push_back(g);
+      }
+      if (!h->shards.empty()) {
+        h->shard_pool = std::make_unique<HostPool>(static_cast<int>(h->shards.size()) + 1);
+      }
+    });
+    if (sst != PP_OK) {
+      const std::string msg = pp_last_error();
+      pp_destroy(h);
+      g_error = msg;
+      return sst;
+    }
     *out = h;
   }
   return st;
@@ -140,6 +167,9 @@ pp_status pp_create(const pp_model* m, pp_handle** out) {
 
 void pp_destroy(pp_handle* h) {
   if (h == nullptr) return;
+  h->shard_pool.reset();
+  for (pp_handle* g : h->shards) pp_destroy(g);
+  h->shards.clear();
   cudaSetDevice(h->device);
   if (h->stream != nullptr) cudaStreamSynchronize(h->stream);
   for (DevBuf* b : {&h->d_field, &h->d_params, &h->d_round, &h->d_tiles, &h->d_movers, &h->d_bin,
@@ -328,6 +358,69 @@ pp_status pp_merge_records(const pp_record* recs, int32_t n, pp_record* out) {
 namespace {
 
 // Planner::plan_step after the snapshot is resident (src/planner.cpp:238-351).
+// One sampling round over every shard of the planner (PlannerConfig
+// devices): shard k evaluates candidates [n k / S, n (k + 1) / S) of each
+// restart on its own device and thread, certifying its own winners; the
+// records are merged in shard order with the strict-better rule, i.e. in
+// increasing candidate index as the reference's ordered merge of worker
+// ranges (src/planner.cpp:280-281, 310-321). One shard: run_round.
+void run_round_shards(pp_handle* h, uint64_t t, int iter, int r0, int rc, const double* center,
+                      int64_t n, pp_record* out) {
+  if (h->shards.empty()) {
+    run_round(h, t, iter, r0, rc, center, 0, n, nullptr, out, nullptr);
+    return;
+  }
+  const int S = static_cast<int>(h->shards.size()) + 1;
+  std::vector<std::vector<pp_record>> recs(S, std::vector<pp_record>(rc));
+  std::vector<std::exception_ptr> errs(S);
+  std::vector<std::string> msgs(S);
+  h->shard_pool->run(S, [&](int k) {
+    pp_handle* g = k == 0 ? h : h->shards[k - 1];
+    try {
+      ck(cudaSetDevice(g->device), "cudaSetDevice");
+      if (g->pending_upload) {  // this plan step's snapshot, on the shard's own thread
+        std::function<void()> up = std::move(g->pending_upload);
+        g->pending_upload = nullptr;
+        up();
+      }
+      run_round(g, t, iter, r0, rc, center, n * k / S, n * (k + 1) / S, nullptr, recs[k].data(),
+                nullptr);
+    } catch (...) {
+      errs[k] = std::current_exception();
+    }
+  });
+  ck(cudaSetDevice(h->device), "cudaSetDevice");
+  for (auto& e : errs) {
+    if (e) std::rethrow_exception(e);
+  }
+  for (int r = 0; r < rc; ++r) {
+    pp_record m = recs[0][r];
+    for (int k = 1; k < S; ++k) {
+      const pp_record& q = recs[k][r];
+      if (q.cls < 0) continue;
+      if (m.cls < 0 || key_better({q.cls, q.k1, q.k2}, {m.cls, m.k1, m.k2})) m = q;
+    }
+    out[r] = m;
+  }
+}
+
+// The shards' timings folded into the planner's (kernel time: the slowest
+// shard, the shards run concurrently).
+void gather_shard_timing(pp_handle* h) {
+  for (pp_handle* g : h->shards) {
+    const pp_timing& q = g->timing;
+    h->timing.kernel_ms = std::max(h->timing.kernel_ms, q.kernel_ms);
+    h->timing.executed_steps += q.executed_steps;
+    h->timing.checked_states += q.checked_states;
+    h->timing.samples += q.samples;
+    h->timing.launches += q.launches;
+    h->timing.refined += std::max(q.refined, 0);
+    h->timing.h2d_bytes += q.h2d_bytes;
+    h->timing.d2h_bytes += q.d2h_bytes;
+    g->timing = pp_timing{};
+  }
+}
+
 void plan_step_resident(pp_handle* h, uint64_t t, pp_plan_output* out) {
   const int P = h->P;
   const auto& cfg = h->cfg;
@@ -338,7 +431,7 @@ void plan_step_resident(pp_handle* h, uint64_t t, pp_plan_output* out) {
   const int R = cfg.n_restarts, I = cfg.n_iter_max, n = cfg.n_candidates;
   // Iteration 0 of every restart centres on the warm start: one launch.
   std::vector<pp_record> first(R);
-  run_round(h, t, 0, 0, R, init_center.data(), 0, n, nullptr, first.data(), nullptr);
+  run_round_shards(h, t, 0, 0, R, init_center.data(), n, first.data());
 
   Key best;
   bool best_valid = false, any_free = false;
@@ -354,7 +447,7 @@ void plan_step_resident(pp_handle* h, uint64_t t, pp_plan_output* out) {
         rec = first[r];
       } else {
         if (best_valid) center = best_theta;  // :275-276
-        run_round(h, t, it, r, 1, center.data(), 0, n, nullptr, &rec, nullptr);
+        run_round_shards(h, t, it, r, 1, center.data(), n, &rec);
       }
       evaluated += n;
       any_free = any_free || rec.cls >= 1;
@@ -374,6 +467,7 @@ void plan_step_resident(pp_handle* h, uint64_t t, pp_plan_output* out) {
   }
 
   // FP64 epilogue (:339-350).
+  gather_shard_timing(h);
   phase("merged");
   out->evaluated = evaluated;
   if (out->best_theta != nullptr) std::memcpy(out->best_theta, best_theta.data(), sizeof(double) * P);
@@ -398,6 +492,10 @@ struct PendingGuard {
   explicit PendingGuard(pp_handle* hh) : h(hh) {}
   ~PendingGuard() {
     h->pending_field = nullptr;
+    for (pp_handle* g : h->shards) {
+      g->pending_upload = nullptr;
+      g->pending_field = nullptr;
+    }
     g_clock = nullptr;
   }
 };
@@ -424,6 +522,10 @@ pp_status pp_plan_step(pp_handle* h, const pp_snapshot* snap, uint64_t t, pp_pla
     g_clock = &clock;
     PendingGuard pending(h);
     upload_snapshot(h, *snap, true);  // field binned while the generator runs
+    for (pp_handle* g : h->shards) {
+      g->timing = pp_timing{};
+      g->pending_upload = [g, snap] { upload_snapshot(g, *snap, true); };
+    }
     phase("upload");
     plan_step_resident(h, t, out);
     phase("done");
@@ -454,6 +556,10 @@ pp_status pp_plan_step_points(pp_handle* h, const pp_snapshot_points* snap, uint
     g_clock = &clock;
     PendingGuard pending(h);
     upload_points(h, *snap, true);  // field binned while the generator runs
+    for (pp_handle* g : h->shards) {
+      g->timing = pp_timing{};
+      g->pending_upload = [g, snap] { upload_points(g, *snap, true); };
+    }
     phase("upload");
     plan_step_resident(h, t, out);
     phase("done");

@@ -327,6 +327,13 @@ struct pp_handle {
   // plan_step: the field of the snapshot is binned and uploaded while the
   // theta generator runs (consumed by the first round of the step)
   std::function<void()> pending_field;
+  // several GPUs in one process: the other shards' handles (this handle is
+  // shard 0), a pool running one shard per thread, and each shard's
+  // snapshot upload of the current plan step (done on its own thread)
+  std::vector<pp_handle*> shards;
+  std::unique_ptr<ppcapi::HostPool> shard_pool;
+  std::function<void()> pending_upload;
+  int pool_threads = 16;  // certification pool size (split between shards)
   ppdev::RoundArgs base{};
   int field_smem_bytes = 0;
 

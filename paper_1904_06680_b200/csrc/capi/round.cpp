@@ -231,7 +231,8 @@ void run_round_launch(pp_handle* h, uint64_t t, int iter, int r0, int rc, const 
     ck(static_cast<cudaError_t>(ppdev::launch_select(a, h->stream)), "window select launch");
     if (!h->pool) {
       const unsigned hc = std::thread::hardware_concurrency();
-      h->pool = std::make_unique<HostPool>(static_cast<int>(std::min(16u, std::max(1u, hc))));
+      h->pool = std::make_unique<HostPool>(
+        static_cast<int>(std::min(static_cast<unsigned>(h->pool_threads), std::max(1u, hc))));
     }
   }
   ck(cudaEventRecord(h->ev1, h->stream), "event");
@@ -335,7 +336,8 @@ void certify_round(pp_handle* h, ppdev::RoundArgs& a, uint64_t t, int iter, int 
   };
   if (!h->pool) {
     const unsigned hc = std::thread::hardware_concurrency();
-    h->pool = std::make_unique<HostPool>(static_cast<int>(std::min(16u, std::max(1u, hc))));
+    h->pool = std::make_unique<HostPool>(
+        static_cast<int>(std::min(static_cast<unsigned>(h->pool_threads), std::max(1u, hc))));
   }
   const double rho = a.sel_rho, alpha = a.sel_alpha;
   std::vector<ppdev::SelBound> bound(rc);

@@ -78,6 +78,9 @@ pp_model model_of(const VehicleParams& p, const MlpArchitecture& arch, const Pla
   c.precision = cfg.precision;
   c.device = cfg.device;
   c.refine = cfg.refine ? 1 : 0;
+  if (cfg.devices.size() > PP_MAX_DEVICES) throw std::invalid_argument("at most 8 devices per planner");
+  c.n_devices = static_cast<int32_t>(cfg.devices.size());
+  for (size_t k = 0; k < cfg.devices.size(); ++k) c.devices[k] = cfg.devices[k];
   sizes.assign(arch.layer_sizes.begin(), arch.layer_sizes.end());
   m.layer_sizes = sizes.data();
   m.n_layers = static_cast<int32_t>(sizes.size());

@@ -55,3 +55,43 @@ def test_two_ranks_equal_one_gpu_plan():
             bt, tr, action, evaluated, win = out[(rank, k)]
             assert bt == theta.tobytes() and tr == traj.tobytes(), (k, rank)
             assert action == (o.action_a0, o.action_a1) and evaluated == o.evaluated
+
+
+@pytest.mark.parametrize("cfg", CFGS + [dict(H=30, n_restarts=15, n_candidates=20480)])
+@pytest.mark.parametrize("shards", [2, 3])
+def test_in_process_shards_equal_one_gpu_plan(cfg, shards):
+    """PlannerConfig.devices: one process drives several shards (here all on
+    cuda:0, each with its own stream and certification pool); the plan is
+    the single-shard plan bit for bit, for the field and the raw-points path."""
+    w = workloads.c2(samples=1 << 10)
+    one = capi.DevicePlanner(abi.Model(**cfg))
+    many = capi.DevicePlanner(abi.Model(**cfg, devices=[0] * shards))
+    o1, th1, tr1 = one.plan_step(w.snapshot, w.t)
+    o2, th2, tr2 = many.plan_step(w.snapshot, w.t)
+    assert np.array_equal(th1, th2) and np.array_equal(tr1, tr2)
+    assert (o1.action_a0, o1.action_a1, o1.evaluated, o1.success) == \
+        (o2.action_a0, o2.action_a1, o2.evaluated, o2.success)
+    assert (o1.winner.restart, o1.winner.candidate) == (o2.winner.restart, o2.winner.candidate)
+    t = many.timing()
+    assert t.launches >= 3 * shards and t.samples >= o1.evaluated
+    many.close()
+    one.close()
+
+
+def test_in_process_shards_closed_loop_matches_one_gpu():
+    """run_mission through the drop-in module with PlannerConfig.devices."""
+    from paper_1904_06680_b200 import import_paraplan
+    pp = import_paraplan()
+    logs = []
+    for devices in ([], [0, 0]):
+        spec = pp.builtin_scenario("exp3_explicit")
+        c = spec.planner
+        c.H, c.n_restarts, c.n_candidates = 30, 2, 4096
+        c.devices = devices
+        spec.mission.time_limit = 1.0
+        logs.append(pp.run_mission(spec.mission, c, spec.arch, 0))
+    a, b = logs
+    assert len(a.records) == len(b.records) > 0
+    for ra, rb in zip(a.records, b.records):
+        assert (ra.state.x, ra.state.y, ra.state.phi, ra.state.v) == \
+            (rb.state.x, rb.state.y, rb.state.phi, rb.state.v)

@@ -35,7 +35,7 @@ def test_library_exports_every_declared_symbol():
     for s in sorted(syms):
         assert hasattr(lib, s), f"{s} declared in paraplan_cuda.h but not exported"
     assert set(capi.exported_symbols()) == syms
-    assert lib.pp_abi_version() == 1
+    assert lib.pp_abi_version() == 2
 
 
 def test_struct_layout_matches_c(tmp_path: Path):
