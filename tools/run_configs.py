@@ -68,7 +68,8 @@ def closed_loop(samples, H, ticks, name="exp4"):
 
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
-    ap.add_argument("--which", default="C1,C2,C3,C4,C5")
+    ap.add_argument("--which", default="C1,C2,C3,C4,C5",
+                    help="comma list of C1..C5, defaults (reference PlannerConfig), archs")
     ap.add_argument("--c4-samples", type=int, default=1 << 20)
     ap.add_argument("--c3-ticks", type=int, default=20)
     ap.add_argument("--fp64", type=int, default=1)
@@ -95,6 +96,13 @@ if __name__ == "__main__":
         w = workloads.Workload("defaults", abi.Model(H=200, n_restarts=15, n_candidates=20480),
                                snap, 5, "reference PlannerConfig defaults on the C2 scene")
         res["reference_defaults_R15x20480_H200"] = time_round(w)
+    if "archs" in which:
+        # C2 per network architecture (profiles/r1_archs_c2.json)
+        for sizes in ((5, 2, 2), (5, 10, 2), (5, 10, 10, 2), (5, 3, 4, 2)):
+            w = workloads.c2()
+            w.model.layer_sizes = sizes
+            r = time_round(w)
+            res[str(sizes)] = {k: r[k] for k in ("wall_ms", "device_ms", "steps", "refined")}
     if "C3" in which:
         res["C3"] = closed_loop(1 << 20, 200, a.c3_ticks)
     if "C4" in which:
