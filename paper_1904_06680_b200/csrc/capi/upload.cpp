@@ -38,6 +38,8 @@ void fill_consts(const ppdev::RoundArgs& a, ppdev::ConstsT<Real>* k) {
   k->Ts = Real(a.T_s);
   k->umin = Real(a.u_v_min);
   k->umax = Real(a.u_v_max);
+  k->ts_umid = Real(a.T_s * 0.5 * (a.u_v_min + a.u_v_max));
+  k->ts_uhalf = Real(a.T_s * 0.5 * (a.u_v_max - a.u_v_min));
   k->fe = Real(a.fe);
   k->re = Real(a.re);
   k->hw = Real(a.hw);

@@ -59,6 +59,7 @@ struct ConstsT {
   double d_xi, d_eta, d_phi, d_v;     // NormConstants (FP64 path divides)
   Real eps_xi, eps_eta, eps_phi, eps_v;
   Real dmax, window, l_r, wb, Ts, umin, umax;
+  Real ts_umid, ts_uhalf;  // T_s (umin + umax) / 2, T_s (umax - umin) / 2 (FP32 speed update)
   Real fe, re, hw, r2;  // chassis half-planes, squared bounding radius
   Real cull;            // collision x-window half width: bounding radius + 1e-3
   Real bx0, by0, binv;  // cell grid of the field: origin, 1 / cell size

@@ -82,8 +82,13 @@ __device__ __forceinline__ int advance(Lane<Real>& L, const Net& net, const Cons
   const Real c1 = clampr(a1, Real(-1), Real(1));
   Real delta = clampr(K.dmax * c0, L.act - K.window, L.act + K.window);
   delta = clampr(delta, -K.dmax, K.dmax);
-  const Real w = Real(0.5) * (c1 + Real(1));
-  const Real u_v = (Real(1) - w) * K.umin + w * K.umax;
+  // u_v = lerp(umin, umax, (c1 + 1) / 2) (src/dynamics.cpp:40-42); FP32 folds
+  // it with T_s into one FMA of the speed update below
+  Real u_v = Real(0);
+  if constexpr (sizeof(Real) == sizeof(double)) {
+    const Real w = Real(0.5) * (c1 + Real(1));
+    u_v = (Real(1) - w) * K.umin + w * K.umax;
+  }
   // explicit Euler (src/dynamics.cpp:45-62)
   const Real tan_d = K.tan_small ? M<Real>::tn_small(delta) : M<Real>::tn(delta);
   const Real tb = M<Real>::ndiv(K.l_r * tan_d, K.wb_d, K.inv_wb);
@@ -91,7 +96,12 @@ __device__ __forceinline__ int advance(Lane<Real>& L, const Net& net, const Cons
   const Real nx = L.x + tv * (cphi - tb * sphi);
   const Real ny = L.y + tv * (sphi + tb * cphi);
   const Real nphi = L.phi + M<Real>::ndiv(tv * tan_d, K.wb_d, K.inv_wb);
-  const Real nv = L.v + K.Ts * u_v;
+  Real nv;
+  if constexpr (sizeof(Real) == sizeof(double)) {
+    nv = L.v + K.Ts * u_v;
+  } else {
+    nv = fmaf(c1, K.ts_uhalf, L.v + K.ts_umid);
+  }
   const Real dx = nx - L.x, dy = ny - L.y;
   const Real seg = M<Real>::sq(dx * dx + dy * dy);
   if (cls < 0) {
