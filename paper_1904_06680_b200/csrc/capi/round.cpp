@@ -232,7 +232,7 @@ void run_round_launch(pp_handle* h, uint64_t t, int iter, int r0, int rc, const 
     if (!h->pool) {
       const unsigned hc = std::thread::hardware_concurrency();
       h->pool = std::make_unique<HostPool>(
-        static_cast<int>(std::min(static_cast<unsigned>(h->pool_threads), std::max(1u, hc))));
+        static_cast<int>(std::min(static_cast<unsigned>(h->pool_threads), std::max(1u, hc - 1))));
     }
   }
   ck(cudaEventRecord(h->ev1, h->stream), "event");
@@ -337,7 +337,7 @@ void certify_round(pp_handle* h, ppdev::RoundArgs& a, uint64_t t, int iter, int 
   if (!h->pool) {
     const unsigned hc = std::thread::hardware_concurrency();
     h->pool = std::make_unique<HostPool>(
-        static_cast<int>(std::min(static_cast<unsigned>(h->pool_threads), std::max(1u, hc))));
+        static_cast<int>(std::min(static_cast<unsigned>(h->pool_threads), std::max(1u, hc - 1))));
   }
   const double rho = a.sel_rho, alpha = a.sel_alpha;
   std::vector<ppdev::SelBound> bound(rc);
