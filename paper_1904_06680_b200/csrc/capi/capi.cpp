@@ -139,21 +139,25 @@ pp_status pp_create(const pp_model* m, pp_handle** out) {
   });
   if (st == PP_OK) {
     prewarm(h);
-    // the other shards: the same model on devices[1..n)
-    const pp_status sst = guarded([&] {
-      for (int k = 1; k < m->config.n_devices; ++k) {
-        pp_model mk = *m;
-        mk.config.n_devices = 0;
-        mk.config.device = m->config.devices[k];
-        pp_handle* g = nullptr;
-        if (pp_create(&mk, &g) != PP_OK) throw std::runtime_error(pp_last_error());
+    // the other shards: the same model on devices[1..n) (a shard's error,
+    // e.g. a missing device, is the planner's)
+    pp_status sst = PP_OK;
+    for (int k = 1; k < m->config.n_devices && sst == PP_OK; ++k) {
+      pp_model mk = *m;
+      mk.config.n_devices = 0;
+      mk.config.device = m->config.devices[k];
+      pp_handle* g = nullptr;
+      sst = pp_create(&mk, &g);
+      if (sst == PP_OK) {
         g->pool_threads = h->pool_threads;
         h->shards.push_back(g);
       }
-      if (!h->shards.empty()) {
+    }
+    if (sst == PP_OK && !h->shards.empty()) {
+      sst = guarded([&] {
         h->shard_pool = std::make_unique<HostPool>(static_cast<int>(h->shards.size()) + 1);
-      }
-    });
+      });
+    }
     if (sst != PP_OK) {
       const std::string msg = pp_last_error();
       pp_destroy(h);

@@ -95,3 +95,15 @@ def test_in_process_shards_closed_loop_matches_one_gpu():
     for ra, rb in zip(a.records, b.records):
         assert (ra.state.x, ra.state.y, ra.state.phi, ra.state.v) == \
             (rb.state.x, rb.state.y, rb.state.phi, rb.state.v)
+
+
+def test_in_process_shards_reject_a_missing_device():
+    import torch
+    bad = torch.cuda.device_count()  # one past the last ordinal
+    with pytest.raises(ValueError, match="out of range"):
+        capi.DevicePlanner(abi.Model(H=30, n_restarts=1, n_candidates=1024, devices=[0, bad]))
+    # the failed construction left no shard behind: a good planner still works
+    w = workloads.c2(samples=1 << 10)
+    dp = capi.DevicePlanner(abi.Model(H=30, n_restarts=1, n_candidates=1024, devices=[0, 0]))
+    o, _, _ = dp.plan_step(w.snapshot, w.t)
+    assert o.evaluated == 1024

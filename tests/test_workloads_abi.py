@@ -121,3 +121,13 @@ def test_c1_and_c4_inputs():
 def test_algorithmic_flops_formula():
     # 48 + 2*MAC per step, 19 + 6N per checked state; MAC([5,2,2]) = 14
     assert workloads.algorithmic_flops([5, 2, 2], 20, 10, 11) == 10 * 76 + 11 * 139
+
+
+def test_model_devices_field():
+    """pp_config.devices (C-ABI v2): the list is copied with its length; more
+    than PP_MAX_DEVICES is refused before it reaches the library."""
+    c = abi.Model(devices=[3, 1]).to_c().config
+    assert c.n_devices == 2 and list(c.devices)[:2] == [3, 1]
+    assert abi.Model().to_c().config.n_devices == 0
+    with pytest.raises(ValueError):
+        abi.Model(devices=list(range(9))).to_c()
