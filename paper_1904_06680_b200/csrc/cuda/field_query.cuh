@@ -325,6 +325,9 @@ __device__ __forceinline__ Real coop_scan_cells(const typename Vec2T<Real>::type
 // Returns the inside-margin max over visited points (the reference reports a
 // collision iff it is > 0; a small |margin| marks a verdict rounding could
 // flip). Warp-synchronous: all 32 lanes call it, every loop is warp-uniform.
+// `live` is false for a lane whose rollout is over (idle at the end of a
+// round): it scans nothing, and on 2-D grids a warp with few live lanes
+// scans their windows with all 32 lanes (coop_scan_boxed / coop_scan_cells).
 template <typename Real, int kGrid>
 __device__ __forceinline__ Real collide_margin(const Field<Real>& f, const Consts<Real>& K, int h,
                                                Real x, Real y, Real c, Real s, Real stop,
