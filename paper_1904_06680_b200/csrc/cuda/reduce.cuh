@@ -235,17 +235,34 @@ __device__ __forceinline__ bool last_block(const RoundArgs& a) {
 
 // Per-restart reduction of `n_src` records per restart (restart-major) into
 // out[restart].
+// One restart: the whole block reduces its records. Several: one warp per
+// restart (restarts spread over the block's warps), with no block barrier
+// per restart, so 64 restarts cost a few L2 round trips rather than 64
+// block reductions.
 __device__ __forceinline__ void reduce_recs(const RoundArgs& a, const Rec* recs, int n_src,
                                             Key* red, Rec* out) {
-  for (int r = 0; r < a.restart_count; ++r) {
+  if (a.restart_count == 1) {
     Key k = empty_key();
     for (int t = threadIdx.x; t < n_src; t += blockDim.x) {
-      const Key o = load_rec_cg(recs + static_cast<size_t>(r) * n_src + t);
+      const Key o = load_rec_cg(recs + t);
       if (o.cls >= 0 && (k.cls < 0 || prefer(o, k))) k = o;
     }
     const Key best = block_best(k, red);
-    if (threadIdx.x == 0) out[r] = Rec{best.cls, best.idx, best.k1, best.k2};
+    if (threadIdx.x == 0) out[0] = Rec{best.cls, best.idx, best.k1, best.k2};
+    return;
   }
+  const int lane = static_cast<int>(threadIdx.x & 31u), warp = static_cast<int>(threadIdx.x >> 5);
+  const int n_warps = static_cast<int>(blockDim.x >> 5);
+  for (int r = warp; r < a.restart_count; r += n_warps) {
+    Key k = empty_key();
+    for (int t = lane; t < n_src; t += 32) {
+      const Key o = load_rec_cg(recs + static_cast<size_t>(r) * n_src + t);
+      if (o.cls >= 0 && (k.cls < 0 || prefer(o, k))) k = o;
+    }
+    const Key best = warp_best(k);
+    if (lane == 0) out[r] = Rec{best.cls, best.idx, best.k1, best.k2};
+  }
+  __syncthreads();  // every restart's record is written before publish_round
 }
 
 // Publish the work counters and re-arm the tickets (last block only).
