@@ -69,6 +69,7 @@ struct ConstsT {
   Real inv_wb;          // 1 / wheelbase (FP32 path multiplies)
   double wb_d;          // wheelbase (FP64 path divides, src/dynamics.cpp:52-55)
   int32_t tan_small;    // delta_max <= pi/4: tan by polynomial ratio (FP32)
+  int32_t flag_near_miss;  // several restarts: narrow collision misses are marginal too
 };
 
 // Byte offsets of the parts of a field image.

@@ -52,8 +52,12 @@ __device__ __forceinline__ int advance(Lane<Real>& L, const Net& net, const Cons
     // a lane may stop at a hit whose margin is too large to flip
     const Real cm = collide_margin<Real, kGrid>(f, K, L.h, L.x, L.y, cphi, sphi, K.dmarg, live);
     hit = cm > Real(0);
-    // a narrow hit might be free in exact arithmetic (a better outcome)
-    L.marg |= hit & (cm < K.dmarg);
+    // a narrow hit might be free in exact arithmetic (a better outcome).
+    // With several restarts a narrow miss is flagged too: it might be a hit
+    // (a worse outcome), so it must not anchor a restart's window, which is
+    // built around the restart's best unflagged candidate (flagged ones are
+    // always in the window)
+    L.marg |= cm < K.dmarg && (hit || (K.flag_near_miss && cm > -K.dmarg));
   }
   const Real gdx = K.gx - L.x, gdy = K.gy - L.y;
   // inclusive goal box: eps - |err| >= 0 <=> |err| <= eps, exactly
