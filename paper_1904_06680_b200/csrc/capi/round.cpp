@@ -224,7 +224,8 @@ void run_round_launch(pp_handle* h, uint64_t t, int iter, int r0, int rc, const 
     a.theta_scratch64 = static_cast<double*>(h->d_scratch.p);
   }
   // several restarts: narrow collision misses are marginal too (step.cuh)
-  a.kf.flag_near_miss = a.kd.flag_near_miss = rc > 1 ? 1 : 0;
+  a.kf.marg_lo = rc > 1 ? -a.kf.dmarg : 0.0f;
+  a.kd.marg_lo = rc > 1 ? -a.kd.dmarg : 0.0;
   ck(static_cast<cudaError_t>(fp64 ? ppdev::launch_rollout_f64(h->kind, a, h->stream)
                                    : ppdev::launch_rollout_f32(h->kind, a, h->stream)),
      "sampling kernel launch");

@@ -57,6 +57,7 @@ void fill_consts(const ppdev::RoundArgs& a, ppdev::ConstsT<Real>* k) {
   k->inv_wb = Real(1.0 / a.wheelbase);
   k->wb_d = a.wheelbase;
   k->tan_small = a.delta_max <= 0.785 ? 1 : 0;
+  k->marg_lo = Real(0);  // per round (round.cpp)
 }
 
 // Device image of h->field in the compute precision (one H2D); the FP64 image

@@ -69,7 +69,8 @@ struct ConstsT {
   Real inv_wb;          // 1 / wheelbase (FP32 path multiplies)
   double wb_d;          // wheelbase (FP64 path divides, src/dynamics.cpp:52-55)
   int32_t tan_small;    // delta_max <= pi/4: tan by polynomial ratio (FP32)
-  int32_t flag_near_miss;  // several restarts: narrow collision misses are marginal too
+  Real marg_lo;         // collision margins in (marg_lo, dmarg) are marginal: 0 (narrow hits),
+                        // -dmarg with several restarts (narrow misses too)
 };
 
 // Byte offsets of the parts of a field image.

@@ -235,22 +235,27 @@ __device__ __forceinline__ bool last_block(const RoundArgs& a) {
 
 // Per-restart reduction of `n_src` records per restart (restart-major) into
 // out[restart].
-// One restart: the whole block reduces its records. Several: one warp per
-// restart (restarts spread over the block's warps), with no block barrier
-// per restart, so 64 restarts cost a few L2 round trips rather than 64
-// block reductions.
+// Block-wide, one restart after the other (the rollout kernels' last CTA:
+// one restart on the refill schedule).
 __device__ __forceinline__ void reduce_recs(const RoundArgs& a, const Rec* recs, int n_src,
                                             Key* red, Rec* out) {
-  if (a.restart_count == 1) {
+  for (int r = 0; r < a.restart_count; ++r) {
     Key k = empty_key();
     for (int t = threadIdx.x; t < n_src; t += blockDim.x) {
-      const Key o = load_rec_cg(recs + t);
+      const Key o = load_rec_cg(recs + static_cast<size_t>(r) * n_src + t);
       if (o.cls >= 0 && (k.cls < 0 || prefer(o, k))) k = o;
     }
     const Key best = block_best(k, red);
-    if (threadIdx.x == 0) out[0] = Rec{best.cls, best.idx, best.k1, best.k2};
-    return;
+    if (threadIdx.x == 0) out[r] = Rec{best.cls, best.idx, best.k1, best.k2};
   }
+}
+
+// One warp per restart (restarts spread over the block's warps), with no
+// block barrier per restart: 64 restarts cost a few L2 round trips rather
+// than 64 block reductions (reduce_keys_kernel's last block). A separate
+// function so the rollout kernels do not carry it.
+__device__ __forceinline__ void reduce_recs_warps(const RoundArgs& a, const Rec* recs, int n_src,
+                                                  Rec* out) {
   const int lane = static_cast<int>(threadIdx.x & 31u), warp = static_cast<int>(threadIdx.x >> 5);
   const int n_warps = static_cast<int>(blockDim.x >> 5);
   for (int r = warp; r < a.restart_count; r += n_warps) {

@@ -281,8 +281,8 @@ static __global__ void __launch_bounds__(256) reduce_keys_kernel(const RoundArgs
     tiles_free[static_cast<size_t>(r) * n_src + blockIdx.x] = Rec{kf.cls, kf.idx, kf.k1, kf.k2};
   }
   if (!last_block(a)) return;
-  reduce_recs(a, a.tile_recs, static_cast<int>(n_src), red, a.out);
-  if (a.out_free != nullptr) reduce_recs(a, tiles_free, static_cast<int>(n_src), red, a.out_free);
+  reduce_recs_warps(a, a.tile_recs, static_cast<int>(n_src), a.out);
+  if (a.out_free != nullptr) reduce_recs_warps(a, tiles_free, static_cast<int>(n_src), a.out_free);
   publish_round(a);
 }
 

@@ -57,7 +57,7 @@ __device__ __forceinline__ int advance(Lane<Real>& L, const Net& net, const Cons
     // (a worse outcome), so it must not anchor a restart's window, which is
     // built around the restart's best unflagged candidate (flagged ones are
     // always in the window)
-    L.marg |= cm < K.dmarg && (hit || (K.flag_near_miss && cm > -K.dmarg));
+    L.marg |= (cm > K.marg_lo) & (cm < K.dmarg);
   }
   const Real gdx = K.gx - L.x, gdy = K.gy - L.y;
   // inclusive goal box: eps - |err| >= 0 <=> |err| <= eps, exactly
