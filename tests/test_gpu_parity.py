@@ -292,3 +292,21 @@ def test_maximum_size_round(log2n, H):
         c_k1 = -float(s["t_goal"]) if c_cls == 2 else -s["terminal_cost"]
         c_k2 = -s["path_length"] if c_cls == 2 else 0.0
         assert (c_cls, c_k1, c_k2) <= (cls, k1, k2) or (c_cls, c_k1, c_k2) == (cls, k1, k2), c
+
+
+@pytest.mark.parametrize("R", [16, 64])
+def test_several_restarts_plan_and_single_certification_pass(R):
+    """Several restarts (keys-only rounds, per-restart windows): the plan is
+    the oracle's, and the C2 scene certifies in one pass although every
+    restart's FP32 winner (the unperturbed centre) is a narrow miss that the
+    reference calls a collision: narrow misses are marginal with several
+    restarts, so they never anchor a window (round.cpp, step.cuh)."""
+    w = workloads.c2(samples=1 << 10)
+    m = abi.Model(H=30, n_restarts=R, n_candidates=(1 << 16) // R)
+    o1, th1, tr1 = Port(m).plan_step(w.snapshot, w.t)
+    dp = capi.DevicePlanner(m)
+    o2, th2, tr2 = dp.plan_step(w.snapshot, w.t)
+    assert (o1.winner.restart, o1.winner.candidate) == (o2.winner.restart, o2.winner.candidate)
+    assert np.array_equal(th1, th2) and np.array_equal(tr1, tr2)
+    # generator, rollout, per-restart reduction, one window select
+    assert dp.timing().launches == 4, dp.timing().launches
