@@ -46,6 +46,7 @@ void prewarm(pp_handle* h) {
     upload_snapshot(h, s);
     const int rc = std::min(h->cfg.n_restarts, 64);
     std::vector<pp_record> rec(rc);
+    h->winner_rollouts.clear();  // kept by plan steps only
     run_round(h, 0, 0, 0, rc, nullptr, 0, h->cfg.n_candidates, nullptr, rec.data(), nullptr);
     // the other grid modes, and (FP32 planners) the FP64 kernels of the
     // certification's fallback round
@@ -233,6 +234,7 @@ pp_status pp_evaluate(pp_handle* h, const pp_snapshot* snap, uint64_t t, int32_t
       }
       return;
     }
+    h->winner_rollouts.clear();  // kept by plan steps only
     run_round(h, t, iter, restart_begin, restart_count, center, cand_begin, cand_end, nullptr,
               out, per_sample);
   });
@@ -249,6 +251,7 @@ pp_status pp_eval_theta(pp_handle* h, const pp_snapshot* snap, const double* the
     if (snap != nullptr) upload_snapshot(h, *snap);
     if (n <= 0) return;
     pp_record rec{};
+    h->winner_rollouts.clear();  // kept by plan steps only
     run_round(h, 0, 0, 0, 1, nullptr, 0, n, theta, &rec, out);
   });
 }
@@ -433,6 +436,8 @@ void plan_step_resident(pp_handle* h, uint64_t t, pp_plan_output* out) {
   if (snap.warm_theta_len == P) init_center.assign(snap.warm_theta, snap.warm_theta + P);
 
   const int R = cfg.n_restarts, I = cfg.n_iter_max, n = cfg.n_candidates;
+  h->winner_rollouts.clear();
+  for (pp_handle* g : h->shards) g->winner_rollouts.clear();
   // Iteration 0 of every restart centres on the warm start: one launch.
   std::vector<pp_record> first(R);
   run_round_shards(h, t, 0, 0, R, init_center.data(), n, first.data());
@@ -476,7 +481,27 @@ void plan_step_resident(pp_handle* h, uint64_t t, pp_plan_output* out) {
   out->evaluated = evaluated;
   if (out->best_theta != nullptr) std::memcpy(out->best_theta, best_theta.data(), sizeof(double) * P);
   int32_t len = 0;
-  host_rollout(h, snap, best_theta.data(), &out->predicted, out->trajectory, cfg.H + 1, &len);
+  // the certification already ran this rollout when the winner was one of
+  // its window members (any shard): copy it
+  const pp_handle::WinnerRollout* done_w = nullptr;
+  for (size_t k = 0; k <= h->shards.size() && done_w == nullptr && win.candidate >= 0; ++k) {
+    const pp_handle* g = k == 0 ? h : h->shards[k - 1];
+    for (const auto& w : g->winner_rollouts) {
+      if (w.restart == win.restart && w.iter == win.iter && w.candidate == win.candidate) {
+        done_w = &w;
+        break;
+      }
+    }
+  }
+  if (done_w != nullptr) {
+    out->predicted = done_w->stats;
+    len = done_w->len;
+    if (out->trajectory != nullptr) {
+      std::memcpy(out->trajectory, done_w->traj.data(), sizeof(double) * done_w->traj.size());
+    }
+  } else {
+    host_rollout(h, snap, best_theta.data(), &out->predicted, out->trajectory, cfg.H + 1, &len);
+  }
   out->trajectory_len = len;
   out->success = out->predicted.reached && !out->predicted.collided;
   if (any_free) {

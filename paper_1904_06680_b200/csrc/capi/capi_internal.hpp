@@ -320,6 +320,20 @@ struct pp_handle {
   double sel_rho = 1e-3;   // FP32 window: cost <= best * (1 + rho) + 1e-6
   std::unique_ptr<ppcapi::HostPool> pool;  // exact re-evaluation of near ties
   double dmarg32 = 2e-5;   // FP32 margin below which a worse-side verdict may flip
+  // The certification's FP64 rollouts of each certified restart winner in
+  // the current plan step (stats + trajectory, recorded while the window is
+  // re-evaluated). The FP64 epilogue copies the final winner's instead of
+  // re-simulating it: same function, same theta, same snapshot.
+  struct WinnerRollout {
+    int restart = -1, iter = -1, candidate = -1;
+    pp_rollout_stats stats{};
+    std::vector<double> traj;
+    int32_t len = 0;
+  };
+  std::vector<WinnerRollout> winner_rollouts;
+  std::vector<double> cert_traj;  // per window member, (H + 1) x 4 doubles
+  std::vector<pp_rollout_stats> cert_stats;
+  std::vector<int32_t> cert_len;
 
   // resident snapshot
   bool snap_valid = false;

@@ -312,12 +312,30 @@ void certify_round(pp_handle* h, ppdev::RoundArgs& a, uint64_t t, int iter, int 
     int t_goal;
     double cost;  // terminal cost (cls 0/1) or path length (cls 2)
     double k1, k2;
+    int slot;  // its recorded trajectory in h->cert_traj, or -1
+  };
+  // Trajectories of the window members are recorded for the epilogue while
+  // they fit a small arena (C2: 43 members x 31 states); wider windows keep
+  // only their keys and the epilogue re-simulates its winner.
+  const size_t stride = static_cast<size_t>(h->cfg.H + 1) * 4;
+  constexpr size_t kTrajArena = size_t{1} << 16;  // doubles
+  int slots = 0;
+  auto take_slots = [&](size_t n) {
+    if (injected != nullptr || (slots + n) * stride > kTrajArena) return -1;
+    const int base = slots;
+    slots += static_cast<int>(n);
+    if (h->cert_stats.size() < static_cast<size_t>(slots)) {
+      h->cert_traj.resize(std::max(h->cert_traj.size(), slots * stride));
+      h->cert_stats.resize(slots);
+      h->cert_len.resize(slots);
+    }
+    return base;
   };
   // exact keys of every candidate evaluated so far, by increasing flat
   // index (restart-major): a restart's entries are one contiguous range
   std::vector<std::pair<int64_t, Exact>> known;
   const auto by_index = [](const std::pair<int64_t, Exact>& kv, int64_t s) { return kv.first < s; };
-  auto exact_of = [&](int64_t s) {  // the reference's own FP64 arithmetic
+  auto exact_of = [&](int64_t s, int slot) {  // the reference's own FP64 arithmetic
     const int r = static_cast<int>(s / count);
     const int cand = static_cast<int>(c0 + (s - r * count));
     std::vector<double> theta(h->P);
@@ -328,8 +346,15 @@ void certify_round(pp_handle* h, ppdev::RoundArgs& a, uint64_t t, int iter, int 
       host_sample(h, ctr.data(), t, r0 + r, iter, cand, theta.data(), -1);
     }
     pp_rollout_stats st{};
-    host_rollout(h, snap, theta.data(), &st, nullptr, 0, nullptr);
+    if (slot >= 0) {
+      host_rollout(h, snap, theta.data(), &st, h->cert_traj.data() + slot * stride, h->cfg.H + 1,
+                   &h->cert_len[slot]);
+      h->cert_stats[slot] = st;
+    } else {
+      host_rollout(h, snap, theta.data(), &st, nullptr, 0, nullptr);
+    }
     Exact e;
+    e.slot = slot;
     e.cls = st.collided ? 0 : (st.reached ? 2 : 1);
     e.t_goal = st.t_goal;
     e.cost = e.cls == 2 ? st.path_length : st.terminal_cost;
@@ -407,7 +432,10 @@ void certify_round(pp_handle* h, ppdev::RoundArgs& a, uint64_t t, int iter, int 
     h->timing.refined += static_cast<int32_t>(list.size());
     std::vector<Exact> got(list.size());
     if (list.size() <= static_cast<size_t>(host_max())) {
-      h->pool->run(static_cast<int>(list.size()), [&](int i) { got[i] = exact_of(list[i]); });
+      const int base = take_slots(list.size());
+      h->pool->run(static_cast<int>(list.size()), [&](int i) {
+        got[i] = exact_of(list[i], base < 0 ? -1 : base + i);
+      });
     } else {
       // wide window: FP64 keys from the device, exact host keys for the FP64
       // near-ties of each restart's best
@@ -430,7 +458,7 @@ void certify_round(pp_handle* h, ppdev::RoundArgs& a, uint64_t t, int iter, int 
       std::vector<int> best(rc, -1);
       for (size_t i = 0; i < dev.size(); ++i) {
         got[i] = Exact{dev[i].cls, dev[i].cls == 2 ? static_cast<int>(-dev[i].k1) : -1,
-                       dev[i].cls == 2 ? -dev[i].k2 : -dev[i].k1, dev[i].k1, dev[i].k2};
+                       dev[i].cls == 2 ? -dev[i].k2 : -dev[i].k1, dev[i].k1, dev[i].k2, -1};
         const int r = dev[i].restart;
         if (best[r] < 0 || key_better({got[i].cls, got[i].k1, got[i].k2},
                                       {got[best[r]].cls, got[best[r]].k1, got[best[r]].k2})) {
@@ -446,8 +474,10 @@ void certify_round(pp_handle* h, ppdev::RoundArgs& a, uint64_t t, int iter, int 
           ties.push_back(static_cast<int>(i));
         }
       }
-      h->pool->run(static_cast<int>(ties.size()),
-                   [&](int j) { got[ties[j]] = exact_of(list[ties[j]]); });
+      const int base = take_slots(ties.size());
+      h->pool->run(static_cast<int>(ties.size()), [&](int j) {
+        got[ties[j]] = exact_of(list[ties[j]], base < 0 ? -1 : base + j);
+      });
     }
     phase("exact");
     {  // merge the (sorted, new) list into the known keys
@@ -495,6 +525,17 @@ void certify_round(pp_handle* h, ppdev::RoundArgs& a, uint64_t t, int iter, int 
         out[r].candidate = static_cast<int>(c0 + (win - r * count));
         out[r].k1 = e->k1;
         out[r].k2 = e->k2;
+        if (e->slot >= 0) {
+          pp_handle::WinnerRollout w;
+          w.restart = out[r].restart;
+          w.iter = out[r].iter;
+          w.candidate = out[r].candidate;
+          w.stats = h->cert_stats[e->slot];
+          w.len = h->cert_len[e->slot];
+          const double* tr = h->cert_traj.data() + e->slot * stride;
+          w.traj.assign(tr, tr + static_cast<size_t>(std::min<int32_t>(w.len, h->cfg.H + 1)) * 4);
+          h->winner_rollouts.push_back(std::move(w));
+        }
         bound[r].cls = -1;  // select nothing more for this restart
         continue;
       }

@@ -263,3 +263,32 @@ def test_run_sweep_outputs_match_reference(pp, tmp_path, precision):
             assert strip_tau(json.loads(a)) == strip_tau(json.loads(b)), name
         else:  # scenario file (JSON with the reference's comments), xy files
             assert a == b, name
+
+
+@pytest.mark.parametrize("precision", [32, 64])
+def test_epilogue_reuses_certified_rollout_exactly(pp, precision):
+    """The FP64 epilogue copies the certification's rollout of the final
+    winner (capi.cpp, plan_step_resident) instead of re-simulating it: the
+    copy must equal an independent re-simulation bit for bit, with obstacles,
+    several restarts and hill-climb iterations (iter > 0 centres on the
+    incumbent)."""
+    H = 40
+    p = planner(pp, H=H, n_candidates=4096, n_restarts=2, n_iter_max=3, precision=precision,
+                master_seed=21)
+    rnd = np.random.default_rng(77)
+    for i in range(6):
+        s = snapshot_towards(pp, (12 + 4 * rnd.uniform(), 3 * rnd.uniform(-1, 1), 0.3 * rnd.uniform(-1, 1),
+                                  4.0), 5.0, H)
+        obst = [pp.ObstaclePoint(6 + 2 * rnd.uniform(), rnd.uniform(-1.5, 1.5), rnd.uniform(-1, 1), 0.0)
+                for _ in range(12)]
+        s.obstacle_field = pp.extrapolate(obst, H, 0.1, pp.Pose2(0, 0, 0))
+        out = p.plan_step(s, i)
+        resim = pp.resimulate_rollout(list(out.best_theta), s, p)
+        assert (out.predicted.reached, out.predicted.collided, out.predicted.t_goal) == \
+            (resim.reached, resim.collided, resim.t_goal)
+        assert out.predicted.path_length == resim.path_length
+        assert out.predicted.terminal_cost == resim.terminal_cost
+        assert (out.predicted.first_action.a0, out.predicted.first_action.a1) == \
+            (resim.first_action.a0, resim.first_action.a1)
+        assert [(z.x, z.y, z.phi, z.v) for z in out.predicted.trajectory] == \
+            [(z.x, z.y, z.phi, z.v) for z in resim.trajectory]
