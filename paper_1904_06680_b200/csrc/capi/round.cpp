@@ -315,10 +315,11 @@ void certify_round(pp_handle* h, ppdev::RoundArgs& a, uint64_t t, int iter, int 
     int slot;  // its recorded trajectory in h->cert_traj, or -1
   };
   // Trajectories of the window members are recorded for the epilogue while
-  // they fit a small arena (C2: 43 members x 31 states); wider windows keep
-  // only their keys and the epilogue re-simulates its winner.
+  // they fit a small arena (2 MB: C2's 43 members x 31 states; up to 326
+  // members at H=200); wider windows keep only their keys and the epilogue
+  // re-simulates its winner.
   const size_t stride = static_cast<size_t>(h->cfg.H + 1) * 4;
-  constexpr size_t kTrajArena = size_t{1} << 16;  // doubles
+  constexpr size_t kTrajArena = size_t{1} << 18;  // doubles (2 MB)
   int slots = 0;
   auto take_slots = [&](size_t n) {
     if (injected != nullptr || (slots + n) * stride > kTrajArena) return -1;
