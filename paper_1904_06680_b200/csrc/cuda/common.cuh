@@ -33,6 +33,9 @@ constexpr int kWarps = kBlock / 32;
 #ifndef PARAPLAN_FAST_SQRT
 #define PARAPLAN_FAST_SQRT 1
 #endif
+#ifndef PARAPLAN_GEN_MINB
+#define PARAPLAN_GEN_MINB 1  // theta generator: resident CTAs the register cap must allow
+#endif
 #ifndef PARAPLAN_REFILL_MINB
 #define PARAPLAN_REFILL_MINB 6  // <= 85 registers: 6 CTAs (24 warps) per SM, no spills
 #endif

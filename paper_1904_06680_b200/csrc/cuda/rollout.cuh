@@ -59,7 +59,7 @@ template <typename Real>
 using Vec16 = typename std::conditional<sizeof(Real) == 4, float4, double2>::type;
 
 template <typename Real, class Net>
-__global__ void __launch_bounds__(256) generate_kernel(const RoundArgs a) {
+__global__ void __launch_bounds__(256, PARAPLAN_GEN_MINB) generate_kernel(const RoundArgs a) {
   constexpr int P = Net::P;
   constexpr int W = rec_width<Real>(P);
   constexpr int V = W * static_cast<int>(sizeof(Real)) / 16;
