@@ -238,11 +238,14 @@ void run_round_launch(pp_handle* h, uint64_t t, int iter, int r0, int rc, const 
         static_cast<int>(std::min(static_cast<unsigned>(h->pool_threads), std::max(1u, hc - 1))));
     }
   }
-  ck(cudaEventRecord(h->ev1, h->stream), "event");
   // one D2H: counters (selection count), work counters, winners and the
-  // first kSelFirst selected indices
-  ck(cudaMemcpyAsync(h->h_round.p, h->d_round.p, rbytes, cudaMemcpyDeviceToHost, h->stream),
+  // first kSelFirst selected indices, stored into pinned host memory by a
+  // dependent kernel right behind the last round kernel (no event between
+  // them, which would break the programmatic dependency)
+  ck(static_cast<cudaError_t>(
+         ppdev::launch_copy_out(h->d_round.p, h->h_round.p, (rbytes + 15) / 16 * 16, h->stream)),
      "result D2H");
+  ck(cudaEventRecord(h->ev1, h->stream), "event");
   phase("enqueued");
   // the host's exact image of device-binned movers, while the round runs
   if (h->field.dyn_deferred) {
@@ -264,8 +267,9 @@ void run_round_launch(pp_handle* h, uint64_t t, int iter, int r0, int rc, const 
   phase("synced");
   float ms = 0.f;
   ck(cudaEventElapsedTime(&ms, h->ev0, h->ev1), "event timing");
+  if (trace_level() >= 2) std::fprintf(stderr, "[paraplan] round gpu us: %.1f\n", 1e3 * ms);
   h->timing.kernel_ms += ms;
-  h->timing.launches += (shape.refill ? 2 : 1) + (rerank ? 1 : 0) + (keys_only ? 1 : 0);
+  h->timing.launches += (shape.refill ? 2 : 1) + (rerank ? 1 : 0) + (keys_only ? 1 : 0) + 1;
   h->timing.samples += count * rc;
   const char* hres = static_cast<const char*>(h->h_round.p);
   const unsigned long long* ex = reinterpret_cast<const unsigned long long*>(hres + kExecOff);

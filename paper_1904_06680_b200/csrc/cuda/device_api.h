@@ -207,6 +207,9 @@ int launch_draw_f64(const RoundArgs& a, void* out, void* stream);
 // Near-tie window after a round: counters[2] receives the number of selected
 // candidates, sel_list their flat indices.
 int launch_select(const RoundArgs& a, void* stream);
+// Copy `bytes` (a multiple of 16) of device memory into pinned host memory
+// with SM stores, after the previous kernel on `stream` (dependent launch).
+int launch_copy_out(const void* src, void* host_dst, size_t bytes, void* stream);
 // FP64 re-evaluation of the selected candidates into sel_out.
 int launch_refine(NetKind k, const RoundArgs& a, void* stream);
 
