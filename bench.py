@@ -52,6 +52,8 @@ def parse():
     ap.add_argument("--samples", type=int, default=1 << 20, help="candidates per GPU")
     ap.add_argument("--cpu-seconds", type=float, default=12.0,
                     help="budget of the CPU-baseline sample")
+    ap.add_argument("--allow-shared", action="store_true",
+                    help="allow more ranks than GPUs (code-path check, not a measurement)")
     return ap.parse_args()
 
 
@@ -104,77 +106,180 @@ class ClockSampler:
                 "samples": len(self.rows)}
 
 
-def cpu_reference_timing(workload, cores: int, budget_s: float, steps: int | None = None,
-                         warmup: int = 1):
-    """The reference planner (oracle/_ref, compiled from its own sources) on a
-    bounded sample of the workload: same snapshot, H and arch, fewer
-    candidates. Returns (samples*H/s, sample description, per-step seconds)."""
+def bench_config(a, world: int) -> dict:
+    """The workload identity, shared by both arms (the driver compares them)."""
+    return {"workload": "C2 dynamic obstacle avoidance (BASELINE.json configs[1])",
+            "samples_per_gpu": a.samples, "samples_total": a.samples * world, "H": 30,
+            "n_points": 20, "moving_points": 4, "arch": [5, 2, 2], "restarts": 1,
+            "parallelism": f"candidate shards x{world}"}
+
+
+def c2_reference_snapshot():
+    """The C2 snapshot built by the REFERENCE's own select_goal -> sense ->
+    extrapolate (oracle/_ref), so the reference arm never loads this repo's
+    native code (workloads.c2_mission_arrays is plain data)."""
+    from oracle.oracle import Ref
+    from paper_1904_06680_b200 import workloads as W
+    wp, st, dy, ev = W.c2_mission_arrays()
+    return Ref.mission_snapshot(wp, st, dy, ev, W.C2_T, W.C2_H, W.C2_N_OBST), W.C2_T, W.C2_H
+
+
+def cpu_model() -> str:
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                return line.split(":", 1)[1].strip()
+    except (OSError, subprocess.SubprocessError):
+        pass
+    return "unknown"
+
+
+def thread_counts(nproc: int) -> list[int]:
+    out, k = [], 1
+    while k < nproc:
+        out.append(k)
+        k *= 2
+    return out + [nproc]
+
+
+def spin_calibration(nproc: int) -> dict:
+    """W threads x 2.5 ms of independent spin work, wall
+    time (raw std::thread and the reference's own ThreadPool)."""
+    from oracle.oracle import Ref
+    L = Ref.lib()
+    rows = []
+    for w in thread_counts(nproc):
+        raw = min(L.ref_spin_calibration(w, 2.5, 0) for _ in range(3))
+        pool = min(L.ref_spin_calibration(w, 2.5, 1) for _ in range(3))
+        rows.append({"threads": w, "raw_ms": round(raw, 3), "pool_ms": round(pool, 3),
+                     "efficiency": round(2.5 / pool, 3)})
+    return {"work_per_thread_ms": 2.5, "rows": rows}
+
+
+def cpu_protocol(snap, t: int, H: int, total: int, budget_s: float) -> dict:
+    """The reference planner (oracle/_ref, compiled from its own sources) on
+    the box's host cores: spin calibration, then a thread
+    sweep {1, 2, 4, ..., nproc} of Planner::plan_step on a bounded sample of
+    the workload (same snapshot, H and arch, fewer candidates), 1 warm-up +
+    best / median of the timed calls."""
     from oracle.oracle import Ref
     from paper_1904_06680_b200 import abi
-
-    m0 = workload.model
-    n = 1 << 14
-    probe = abi.Model(H=m0.H, n_restarts=1, n_candidates=n, threads=cores)
-    ref = Ref(probe)
+    nproc = os.cpu_count() or 1
+    counts = thread_counts(nproc)
+    # size the sample: one single-thread call ~ budget / (3 * len(counts))
+    probe = Ref(abi.Model(H=H, n_restarts=1, n_candidates=2048, threads=1))
     t0 = time.perf_counter()
-    ref.plan_step(workload.snapshot, workload.t)
-    dt = time.perf_counter() - t0
-    # scale the sample so one step costs ~budget/4 (bounded by the workload)
-    target = budget_s / (steps + warmup if steps else 4)
-    n = int(min(m0.n_candidates, max(1 << 12, n * target / max(dt, 1e-6))))
-    n = 1 << max(12, n.bit_length() - 1)
-    model = abi.Model(H=m0.H, n_restarts=1, n_candidates=n, threads=cores)
-    ref = Ref(model)
-    for _ in range(warmup):
-        ref.plan_step(workload.snapshot, workload.t)
-    times = []
-    reps = steps if steps else 3
-    for _ in range(reps):
-        t0 = time.perf_counter()
-        ref.plan_step(workload.snapshot, workload.t)
-        times.append(time.perf_counter() - t0)
-    per = statistics.median(times)
-    return n * m0.H / per, n, times
+    probe.plan_step(snap, t)
+    per_cand = (time.perf_counter() - t0) / 2048
+    n = int(min(total, max(4096, budget_s / (3 * len(counts)) / max(per_cand, 1e-9))))
+    n = 1 << (n.bit_length() - 1)
+    sweep = []
+    for th in counts:
+        ref = Ref(abi.Model(H=H, n_restarts=1, n_candidates=n, threads=th))
+        ref.plan_step(snap, t)  # warm-up (pool threads spawned)
+        reps = 5 if th == nproc else 2
+        times = []
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            ref.plan_step(snap, t)
+            times.append(time.perf_counter() - t0)
+        sweep.append({"threads": th, "best_ms": round(min(times) * 1e3, 3),
+                      "median_ms": round(statistics.median(times) * 1e3, 3),
+                      "steps_per_s": n * H / min(times)})
+    best = max(sweep, key=lambda r: r["steps_per_s"])
+    at_nproc = sweep[-1]
+    return {"value": best["steps_per_s"], "unit": UNIT, "cores": best["threads"],
+            "kind": "reference", "nproc": nproc, "cpu_model": cpu_model(),
+            "value_at_nproc": at_nproc["steps_per_s"],
+            "sample": f"{n} of {total} C2 candidates (same snapshot, H, arch) per "
+                      f"reference Planner::plan_step; 1 warm-up, best of 2-5 calls per "
+                      f"thread count; value = best thread count ({best['threads']})",
+            "thread_sweep": sweep, "spin_calibration": spin_calibration(nproc)}
 
 
 def run_reference(a):
+    """--impl reference: the unmodified reference planner (oracle/_ref) on
+    the host cores, all threads, on the same C2 workload; only rank 0 runs."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    from paper_1904_06680_b200 import workloads
-    w = workloads.c2(samples=a.samples)
-    cores = os.cpu_count() or 1
-    value, n, times = cpu_reference_timing(w, cores, a.cpu_seconds * 4, steps=a.steps,
-                                           warmup=max(1, min(a.warmup, 2)))
-    ms = statistics.median(times) * 1e3
+    from oracle.oracle import Ref
+    from paper_1904_06680_b200 import abi
+    world = int(os.environ.get("WORLD_SIZE", str(a.gpus)))
+    snap, t, H = c2_reference_snapshot()
+    total = a.samples * world
+    proto = cpu_protocol(snap, t, H, total, budget_s=a.cpu_seconds)
+    nproc = proto["nproc"]
+    # timed steps: all host threads, a sample sized so the K + W calls take
+    # about 4 x cpu_seconds
+    at = proto["thread_sweep"][-1]
+    n_s = int(proto["sample"].split(" of ")[0])
+    per_call = at["best_ms"] * 1e-3 / n_s
+    n = int(min(total, max(4096, 4 * a.cpu_seconds / (a.steps + a.warmup) / max(per_call, 1e-9))))
+    n = 1 << (n.bit_length() - 1)
+    ref = Ref(abi.Model(H=H, n_restarts=1, n_candidates=n, threads=nproc))
+    for _ in range(max(1, a.warmup)):
+        ref.plan_step(snap, t)
+    times = []
+    for _ in range(a.steps):
+        t0 = time.perf_counter()
+        ref.plan_step(snap, t)
+        times.append(time.perf_counter() - t0)
+    per = statistics.median(times)
+    value = n * H / per
+    cpu = dict(proto)
+    cpu.update({"value": value, "cores": nproc,
+                "sample": f"{n} of {total} C2 candidates per reference Planner::plan_step "
+                          f"(same snapshot, H, arch), threads={nproc}, median of {a.steps}"})
     print(json.dumps({
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": a.gpus,
-        "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "C2 dynamic obstacle avoidance (bounded CPU sample)",
-                   "samples": n, "H": w.model.H, "n_points": int(w.snapshot.field.shape[1]),
-                   "arch": [5, 2, 2]},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference",
-                         "sample": f"{n} of {w.samples} candidates of C2 per step, "
-                                   f"reference Planner::plan_step threads={cores}"},
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": a.steps, "warmup": a.warmup, "ms_per_step": per * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": bench_config(a, world),
+        "cpu_baseline": cpu,
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
+
+
+def spawn_ranks(a) -> int:
+    """`bench.py --gpus N` without torchrun: launch N ranks (one per GPU) the
+    way the driver does, after checking that N GPUs exist."""
+    import torch
+    n_dev = torch.cuda.device_count()
+    if n_dev < a.gpus:
+        print(json.dumps({"error": f"--gpus {a.gpus} but only {n_dev} CUDA device(s) visible"}),
+              flush=True)
+        return 2
+    import socket
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={a.gpus}", "--master-addr", "127.0.0.1", "--master-port",
+           str(port), str(ROOT / "bench.py")] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def run_b200(a):
     import torch
 
     from paper_1904_06680_b200 import abi, capi, import_paraplan, workloads
-    from paper_1904_06680_b200.distributed import ShardedPlanner
+    from paper_1904_06680_b200.distributed import ShardedPlanner, shard_range
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    # more ranks than GPUs (a code-path check on a small box, not a measurement):
-    # ranks share devices and exchange records over gloo (NCCL refuses two
-    # ranks on one GPU)
     n_dev = torch.cuda.device_count()
+    if world != a.gpus:
+        raise SystemExit(f"--gpus {a.gpus} but WORLD_SIZE={world}")
+    # more ranks than GPUs only on request (a code-path check on a small box,
+    # never a measurement): ranks share devices and exchange over gloo
     shared = world > n_dev
+    if shared and not a.allow_shared:
+        raise SystemExit(f"{world} ranks but only {n_dev} CUDA device(s); "
+                         "--allow-shared runs a code-path check, not a measurement")
     local = local % max(n_dev, 1)
     torch.cuda.set_device(local)
     dist = None
@@ -190,6 +295,13 @@ def run_b200(a):
             dist.barrier()
         torch.cuda.synchronize()
 
+    def max_over_ranks(v: float) -> float:
+        if dist is None:
+            return v
+        t = torch.tensor([v], device="cpu" if shared else f"cuda:{local}", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
     per_gpu = a.samples
     w = workloads.c2(samples=per_gpu * world, precision=a.precision)
     model = w.model
@@ -201,41 +313,51 @@ def run_b200(a):
         peak_tf, _ = capi.measure_fp32_peak(local)
 
     # ---------------- value: device-resident sampling rounds -----------------
-    from paper_1904_06680_b200.distributed import shard_range
     dp = capi.DevicePlanner(model)
-    c0, c1 = shard_range(model.n_candidates, rank, world)
     dp.upload(w.snapshot)
     stream = torch.cuda.ExternalStream(dp.stream(), device=torch.device("cuda", local))
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local}")  # > 126 MB L2
-    center = np.zeros(model.param_count())
-    for _ in range(a.warmup):
-        dp.evaluate(None, w.t, 0, 0, 1, center, c0, c1)
-    dev_ms, kern_ms, steps_exec, states, launches, refined = [], [], 0, 0, 0, 0
-    barrier()
-    with ClockSampler(local) as clocks:
-        for _ in range(a.steps):
+
+    def device_rounds(c0, c1, steps, stats=None):
+        """`steps` sampling rounds over [c0, c1); returns the device ms of each."""
+        out = []
+        for _ in range(steps):
             with torch.cuda.stream(stream):
                 flush.zero_()
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            dp.evaluate(None, w.t, 0, 0, 1, center, c0, c1)
+            dp.evaluate(None, w.t, 0, 0, 1, None, c0, c1)
             e1.record(stream)
             e1.synchronize()
-            dev_ms.append(e0.elapsed_time(e1))
-            tm = dp.timing()
-            kern_ms.append(tm.kernel_ms)
-            steps_exec += tm.executed_steps
-            states += tm.checked_states
-            launches += tm.launches
-            refined += max(tm.refined, 0)
+            out.append(e0.elapsed_time(e1))
+            if stats is not None:
+                tm = dp.timing()
+                stats["kern_ms"].append(tm.kernel_ms)
+                stats["roll_ms"].append(tm.rollout_ms)
+                stats["steps"] += tm.executed_steps
+                stats["states"] += tm.checked_states
+                stats["launches"] += tm.launches
+                stats["refined"] += max(tm.refined, 0)
+        return out
+
+    c0, c1 = shard_range(model.n_candidates, rank, world)
+    device_rounds(c0, c1, a.warmup)
+    st = {"kern_ms": [], "roll_ms": [], "steps": 0, "states": 0, "launches": 0, "refined": 0}
+    barrier()
+    with ClockSampler(local) as clocks:
+        dev_ms = device_rounds(c0, c1, a.steps, st)
         barrier()
-        total_ms = sum(dev_ms)
-        if dist is not None:
-            t = torch.tensor([total_ms], device="cpu" if shared else f"cuda:{local}")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            total_ms = float(t.item())
+        total_ms = max_over_ranks(sum(dev_ms))
         value = model.n_candidates * H * a.steps / (total_ms * 1e-3)
+
+        # strong scaling: the BASELINE latency workload (2^20 candidates in
+        # total) split over the ranks
+        s0, s1 = shard_range(per_gpu, rank, world)
+        device_rounds(s0, s1, a.warmup)
+        barrier()
+        strong_ms = max_over_ranks(sum(device_rounds(s0, s1, a.steps))) / a.steps
+        barrier()
 
         # ---------------- e2e: public API, host buffers ----------------------
         if world == 1:
@@ -285,16 +407,16 @@ def run_b200(a):
             d2h += tm.d2h_bytes
         barrier()
         e2e_s = time.perf_counter() - t0
-    if dist is not None:
-        t = torch.tensor([e2e_s], device="cpu" if shared else f"cuda:{local}",
-                         dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
+    e2e_s = max_over_ranks(e2e_s)
     e2e_value = model.n_candidates * H * a.steps / e2e_s
 
     # ---------------- roofline ------------------------------------------------
-    kern_avg_ms = sum(kern_ms) / len(kern_ms)
-    flops = workloads.algorithmic_flops([5, 2, 2], N, steps_exec // a.steps, states // a.steps)
+    round_avg_ms = sum(st["kern_ms"]) / len(st["kern_ms"])
+    # the dominant kernel alone (the rollout, refill_kernel): its device span
+    # from %globaltimer, first CTA start to last CTA end
+    kern_avg_ms = sum(st["roll_ms"]) / len(st["roll_ms"])
+    flops = workloads.algorithmic_flops([5, 2, 2], N, st["steps"] // a.steps,
+                                        st["states"] // a.steps)
     achieved = flops / (kern_avg_ms * 1e-3) / 1e12
     traffic, traffic_live, pipes = None, None, None
     tf = ROOT / "profiles" / "traffic.json"
@@ -304,25 +426,17 @@ def run_b200(a):
         traffic_live = tj.get("live_dram_bytes_per_launch")
         pipes = tj.get("pipes")
 
-    out = None
     if rank == 0:
         cpu = None
         if world == 1:
-            cores = os.cpu_count() or 1
-            cv, n_cpu, times = cpu_reference_timing(w, cores, a.cpu_seconds)
-            cpu = {"value": cv, "unit": UNIT, "cores": cores, "kind": "reference",
-                   "sample": f"{n_cpu} of {w.samples} C2 candidates per plan_step, median of "
-                             f"{len(times)}, reference Planner::plan_step threads={cores}"}
+            cpu = cpu_protocol(w.snapshot, w.t, H, model.n_candidates, a.cpu_seconds)
         out = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": total_ms / a.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None,
             "dtype": "f32" if a.precision == 32 else "f64", "data": "synthetic",
-            "config": {"workload": "C2 dynamic obstacle avoidance (BASELINE.json configs[1])",
-                       "samples_per_gpu": per_gpu, "samples_total": model.n_candidates,
-                       "H": H, "n_points": N, "moving_points": 4, "arch": [5, 2, 2],
-                       "restarts": 1, "parallelism": f"candidate shards x{world}",
-                       "rollout_precision": "fp32" if a.precision == 32 else "fp64",
+            "config": bench_config(a, world),
+            "method": {"rollout_precision": "fp32" if a.precision == 32 else "fp64",
                        "winner": "certified: FP32 window re-ranked in the reference's FP64 "
                                  "arithmetic (PlannerConfig.refine)",
                        "l2": "flushed (256 MiB write) between timed steps",
@@ -331,21 +445,29 @@ def run_b200(a):
                           if shared else {})},
             "value_timing": "CUDA events on the planner stream around each sampling round "
                             "(generate + rollout + window-select kernels and the host "
-                            "certification between them), snapshot resident in HBM",
-            "near_tie_candidates_per_step": refined // a.steps,
+                            "certification between them), snapshot resident in HBM, max over "
+                            "ranks",
+            "strong": {"samples_total": per_gpu, "ms_per_step": strong_ms,
+                       "value": per_gpu * H / (strong_ms * 1e-3), "unit": UNIT},
+            "near_tie_candidates_per_step": st["refined"] // a.steps,
             "e2e": {"value": e2e_value, "unit": UNIT, "ms_per_step": e2e_s / a.steps * 1e3,
                     "h2d_bytes_per_step": h2d // a.steps, "d2h_bytes_per_step": d2h // a.steps,
                     "api": "paraplan.Planner.plan_step" if world == 1 else
                            "ShardedPlanner.plan_step (NCCL all-gather of winner records)"},
             "latency_ms": e2e_s / a.steps * 1e3,
-            "gpu_launches": launches,
+            "gpu_launches": st["launches"],
+            "nccl": ({"ranks": world, "version": ".".join(map(str, torch.cuda.nccl.version()))}
+                     if world > 1 and not shared else None),
             "roofline": {"bound": "fp32", "achieved": achieved, "peak": peak_tf,
                          "unit": "TFLOP/s", "frac": achieved / peak_tf if peak_tf else None,
                          "traffic": traffic, "traffic_live": traffic_live,
                          "peak_source": "FFMA loop measured in this run",
                          "ncu_pipes": pipes,
-                         "kernel_ms": kern_avg_ms, "flops_per_launch": flops,
-                         "executed_steps_per_launch": steps_exec // a.steps},
+                         "kernel": "refill_kernel (rollout)", "kernel_ms": kern_avg_ms,
+                         "kernel_timing": "%globaltimer span inside the kernel, averaged over "
+                                          "the timed rounds",
+                         "round_ms": round_avg_ms, "flops_per_launch": flops,
+                         "executed_steps_per_launch": st["steps"] // a.steps},
             "cpu_baseline": cpu,
             "clocks": clocks.summary(),
         }
@@ -358,6 +480,8 @@ def main():
     a = parse()
     if a.impl == "reference":
         run_reference(a)
+    elif a.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(a))
     else:
         run_b200(a)
 

@@ -191,6 +191,8 @@ typedef struct pp_timing {
   int32_t refined;         /* FP32 candidates re-ranked in FP64 */
   int64_t h2d_bytes, d2h_bytes;
   double certify_ms;       /* host time of the certified re-ranking (wall) */
+  double rollout_ms;       /* device span of the rollout kernel alone (%globaltimer,
+                              first CTA start to last CTA end) */
 } pp_timing;
 
 typedef struct pp_handle pp_handle;
@@ -226,6 +228,7 @@ pp_status pp_rollout(const pp_handle* h, const pp_snapshot* snap,
 pp_status pp_sample_candidate(const pp_handle* h, const double* center,
                               int32_t len, uint64_t t, int32_t restart,
                               int32_t iter, int32_t candidate, double* out);
+/* NaN for a null handle (pp_last_error() says so). */
 double pp_perturbation_sigma(const pp_handle* h, uint64_t t, int32_t restart,
                              int32_t iter, int32_t candidate);
 

@@ -80,6 +80,19 @@ class Ref(_Base):
             L.ref_builtin_snapshot.argtypes = [C.c_char_p, C.c_int32, C.c_int32, C.c_int32,
                                                C.c_int32, C.POINTER(abi.pp_snapshot),
                                                C.POINTER(C.c_double), C.c_int64]
+            L.ref_mission_snapshot.argtypes = [C.POINTER(C.c_double), C.c_int32,
+                                               C.POINTER(C.c_double), C.c_int32,
+                                               C.POINTER(C.c_double), C.c_int32,
+                                               C.POINTER(C.c_double), C.c_int32, C.c_int32,
+                                               C.c_int32, C.POINTER(abi.pp_snapshot),
+                                               C.POINTER(C.c_double), C.c_int64]
+            L.ref_spin_calibration.restype = C.c_double
+            L.ref_spin_calibration.argtypes = [C.c_int32, C.c_double, C.c_int32]
+            L.ref_acceptance9_snapshot.argtypes = [C.c_int32, C.c_int32,
+                                                   C.POINTER(abi.pp_snapshot),
+                                                   C.POINTER(C.c_double), C.c_int64,
+                                                   C.POINTER(C.c_double),
+                                                   C.POINTER(C.c_int32)]
             L.ref_run_mission_builtin.argtypes = [C.c_char_p, C.c_int32, C.c_int32,
                                                   C.c_int32, C.c_double, C.c_uint64,
                                                   C.c_int32, C.POINTER(C.c_double), C.c_int32,
@@ -178,6 +191,48 @@ class Ref(_Base):
                             field=field[: 2 * (H + 1) * n].reshape(H + 1, n, 2).copy())
 
 
+    @classmethod
+    def mission_snapshot(cls, waypoints, static_pts, dyn_pts, ev, t, H, n_obst_pts):
+        """Tick-t snapshot of a mission through the reference's own
+        select_goal -> sense -> extrapolate (src/mission.cpp:124-144)."""
+        wp = np.ascontiguousarray(waypoints, dtype=np.float64).reshape(-1, 4)
+        st = np.ascontiguousarray(static_pts, dtype=np.float64).reshape(-1, 4)
+        dy = np.ascontiguousarray(dyn_pts, dtype=np.float64).reshape(-1, 4)
+        e = np.ascontiguousarray(ev, dtype=np.float64)
+        cap = 2 * (H + 1) * max(n_obst_pts, 1)
+        field = np.zeros(cap)
+        s = abi.pp_snapshot()
+        n = cls.lib().ref_mission_snapshot(_ptr(wp), len(wp), _ptr(st), len(st), _ptr(dy),
+                                           len(dy), _ptr(e), t, H, n_obst_pts, C.byref(s),
+                                           _ptr(field), cap)
+        if n < 0:
+            raise RuntimeError(cls.lib().ref_last_error().decode())
+        return abi.Snapshot(ev=(s.ev_x, s.ev_y, s.ev_phi, s.ev_v),
+                            actuator_delta=s.actuator_delta, prev_action=(s.prev_a0, s.prev_a1),
+                            goal=(s.goal_x, s.goal_y, s.goal_phi, s.goal_v),
+                            field=field[: 2 * (H + 1) * n].reshape(H + 1, n, 2).copy())
+
+
+    @classmethod
+    def acceptance9_snapshot(cls, index, H=60):
+        """Snapshot `index` of acceptance criterion 9's random sequence
+        (tests/acceptance_test.cpp:271-334: mt19937_64(4242))."""
+        cap = 2 * (H + 1) * 16
+        field = np.zeros(cap)
+        warm = np.zeros(18)
+        wl = C.c_int32()
+        s = abi.pp_snapshot()
+        n = cls.lib().ref_acceptance9_snapshot(index, H, C.byref(s), _ptr(field), cap,
+                                               _ptr(warm), C.byref(wl))
+        if n < 0:
+            raise RuntimeError(cls.lib().ref_last_error().decode())
+        return abi.Snapshot(ev=(s.ev_x, s.ev_y, s.ev_phi, s.ev_v),
+                            actuator_delta=s.actuator_delta, prev_action=(s.prev_a0, s.prev_a1),
+                            goal=(s.goal_x, s.goal_y, s.goal_phi, s.goal_v),
+                            field=field[: 2 * (H + 1) * n].reshape(H + 1, n, 2).copy(),
+                            warm_theta=warm.copy() if wl.value else None)
+
+
 class Port(_Base):
     """The plain-C restatement (paraplan_oracle.c)."""
 
@@ -201,6 +256,10 @@ class Port(_Base):
                                              C.c_uint64, C.c_int32, C.c_int32,
                                              C.POINTER(C.c_double), C.c_int64, C.c_int64,
                                              C.c_void_p]
+            L.po_eval_candidates_mt.argtypes = [C.POINTER(abi.pp_model),
+                                                C.POINTER(abi.pp_snapshot), C.c_uint64,
+                                                C.c_int32, C.c_int32, C.POINTER(C.c_double),
+                                                C.c_int64, C.c_int64, C.c_int32, C.c_void_p]
             L.po_plan_step.argtypes = [C.POINTER(abi.pp_model), C.POINTER(abi.pp_snapshot),
                                        C.c_uint64, C.c_int32, C.POINTER(abi.pp_plan_output)]
             L.po_rng_stream.argtypes = [C.c_uint64] * 5 + [C.c_int32, C.c_int32, C.c_void_p]
@@ -240,12 +299,17 @@ class Port(_Base):
         self.lib().po_sample_candidate(C.byref(self._m), _ptr(c), t, restart, it, cand, _ptr(out))
         return out
 
-    def eval_candidates(self, snap, t, it, restart, center, c_begin, c_end):
+    def eval_candidates(self, snap, t, it, restart, center, c_begin, c_end, threads=None):
+        """Per-candidate stats; threads=None uses every host core (the bits do
+        not depend on the thread count)."""
         s = snap.to_c(self.model.H)
         c = np.ascontiguousarray(center, dtype=np.float64)
         out = self._stats_array(c_end - c_begin)
-        self.lib().po_eval_candidates(C.byref(self._m), C.byref(s), t, it, restart, _ptr(c),
-                                      c_begin, c_end, out.ctypes.data)
+        n = (os.cpu_count() or 1) if threads is None else threads
+        if c_end - c_begin < 256:
+            n = 1
+        self.lib().po_eval_candidates_mt(C.byref(self._m), C.byref(s), t, it, restart, _ptr(c),
+                                         c_begin, c_end, n, out.ctypes.data)
         return out
 
     @classmethod

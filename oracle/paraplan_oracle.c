@@ -401,14 +401,28 @@ int32_t po_better(int32_t cls_a, double k1_a, double k2_a, int32_t cls_b, double
 void po_eval_candidates(const pp_model* m, const pp_snapshot* s, uint64_t t, int32_t iter,
                         int32_t restart, const double* center, int64_t c_begin,
                         int64_t c_end, pp_rollout_stats* out) {
+  po_eval_candidates_mt(m, s, t, iter, restart, center, c_begin, c_end, 1, out);
+}
+
+/* Per-candidate stats are independent of the worker split (each candidate
+ * is its own sample_candidate + rollout), so any thread count gives the same
+ * bits. */
+void po_eval_candidates_mt(const pp_model* m, const pp_snapshot* s, uint64_t t, int32_t iter,
+                           int32_t restart, const double* center, int64_t c_begin,
+                           int64_t c_end, int32_t threads, pp_rollout_stats* out) {
   const int32_t np = po_param_count(m);
-  double* theta = (double*)malloc(sizeof(double) * (size_t)np);
+  const int32_t workers = threads < 1 ? 1 : threads;
   int64_t c;
-  for (c = c_begin; c < c_end; ++c) {
-    po_sample_candidate(m, center, t, restart, iter, (int32_t)c, theta);
-    po_rollout(m, s, theta, &out[c - c_begin], NULL, NULL);
+#pragma omp parallel num_threads(workers) if (workers > 1)
+  {
+    double* theta = (double*)malloc(sizeof(double) * (size_t)np);
+#pragma omp for schedule(dynamic, 64)
+    for (c = c_begin; c < c_end; ++c) {
+      po_sample_candidate(m, center, t, restart, iter, (int32_t)c, theta);
+      po_rollout(m, s, theta, &out[c - c_begin], NULL, NULL);
+    }
+    free(theta);
   }
-  free(theta);
 }
 
 typedef struct {

@@ -37,6 +37,10 @@ void po_rollout(const pp_model* m, const pp_snapshot* s, const double* theta,
 void po_eval_candidates(const pp_model* m, const pp_snapshot* s, uint64_t t,
                         int32_t iter, int32_t restart, const double* center,
                         int64_t c_begin, int64_t c_end, pp_rollout_stats* out);
+void po_eval_candidates_mt(const pp_model* m, const pp_snapshot* s, uint64_t t,
+                           int32_t iter, int32_t restart, const double* center,
+                           int64_t c_begin, int64_t c_end, int32_t threads,
+                           pp_rollout_stats* out);
 
 /* threads > 1 uses OpenMP over contiguous candidate blocks with the
  * reference's ordered merge (bit-identical to threads == 1). */

@@ -27,6 +27,11 @@
 #include "paraplan/scenario.hpp"
 #include "paraplan/selfcheck.hpp"
 #include "paraplan_cuda.h"
+#include "thread_pool.hpp"  // the reference pool (src/thread_pool.hpp)
+
+#include <chrono>
+#include <random>
+#include <thread>
 
 using namespace paraplan;
 
@@ -297,6 +302,178 @@ int ref_builtin_snapshot(const char* name, int32_t t, int32_t H, int32_t n_obst_
     }
     out->field_xy = field_xy;
     n = f.n_points;
+  });
+  return n;
+}
+
+// Snapshot of tick t of a caller-described mission, built by the reference's
+// own select_goal -> sense -> extrapolate (src/mission.cpp:124-144). The
+// mission: waypoints (x, y, phi, v) x n_wp, static and dynamic points
+// (x, y, heading, speed) in the world frame, EV state (x, y, phi, v). Used by
+// bench.py's reference arm so that process loads only oracle/_ref.
+int ref_mission_snapshot(const double* waypoints, int32_t n_wp, const double* static_pts,
+                         int32_t n_static, const double* dyn_pts, int32_t n_dyn,
+                         const double* ev_state, int32_t t, int32_t H, int32_t n_obst_pts,
+                         pp_snapshot* out, double* field_xy, int64_t cap) {
+  int n = -1;
+  guarded([&] {
+    Mission m;
+    for (int32_t i = 0; i < n_wp; ++i) {
+      const double* w = waypoints + 4 * i;
+      m.waypoints.push_back(GoalSetpoint{w[0], w[1], w[2], w[3]});
+    }
+    for (int32_t i = 0; i < n_static; ++i) {
+      const double* q = static_pts + 4 * i;
+      m.static_points.push_back(ObstaclePoint{q[0], q[1], q[2], q[3]});
+    }
+    for (int32_t i = 0; i < n_dyn; ++i) {
+      const double* q = dyn_pts + 4 * i;
+      m.dynamic_points.push_back(ObstaclePoint{q[0], q[1], q[2], q[3]});
+    }
+    m.initial_state = VehicleState{ev_state[0], ev_state[1], ev_state[2], ev_state[3]};
+    const VehicleParams params;
+    const VehicleState ev = m.initial_state;
+    const GoalSelection sel = select_goal(m, ev, 0, GoalTolerance{});
+    const std::vector<ObstaclePoint> pts = sense(m, ev, t, n_obst_pts, params.T_s);
+    const ExtrapolatedField f = extrapolate(pts, H, params.T_s, {ev.x, ev.y, ev.phi});
+    out->ev_x = ev.x;
+    out->ev_y = ev.y;
+    out->ev_phi = ev.phi;
+    out->ev_v = ev.v;
+    out->actuator_delta = 0.0;
+    out->prev_a0 = 0.0;
+    out->prev_a1 = idle_longitudinal(params);
+    out->goal_x = sel.goal.x;
+    out->goal_y = sel.goal.y;
+    out->goal_phi = sel.goal.phi;
+    out->goal_v = sel.goal.v;
+    out->field_H = f.H;
+    out->n_points = f.n_points;
+    out->warm_theta = nullptr;
+    out->warm_theta_len = 0;
+    if (static_cast<int64_t>(2 * f.positions.size()) > cap) throw std::runtime_error("cap");
+    for (std::size_t k = 0; k < f.positions.size(); ++k) {
+      field_xy[2 * k] = f.positions[k].x;
+      field_xy[2 * k + 1] = f.positions[k].y;
+    }
+    out->field_xy = field_xy;
+    n = f.n_points;
+  });
+  return n;
+}
+
+// Parallel-efficiency calibration of the host: each of
+// `threads` workers runs `ms` milliseconds' worth (single-thread calibrated)
+// of independent spin work; returns the wall-clock milliseconds of the whole
+// fork-join. pool = 0: raw std::thread per worker; pool = 1: the reference's
+// own detail::ThreadPool (src/thread_pool.hpp:33-49), worker 0 on the caller.
+double ref_spin_calibration(int32_t threads, double ms, int32_t pool) {
+  using clk = std::chrono::steady_clock;
+  auto spin = [](uint64_t n) {
+    volatile uint64_t x = 0x9E3779B97F4A7C15ull;
+    for (uint64_t i = 0; i < n; ++i) x = x * 6364136223846793005ull + 1442695040888963407ull;
+    return x;
+  };
+  // iterations per millisecond on one thread
+  uint64_t n = 1 << 16;
+  for (;;) {
+    const auto t0 = clk::now();
+    spin(n);
+    const double dt = std::chrono::duration<double, std::milli>(clk::now() - t0).count();
+    if (dt > 5.0) {
+      n = static_cast<uint64_t>(static_cast<double>(n) * ms / dt);
+      break;
+    }
+    n *= 2;
+  }
+  const int w = threads < 1 ? 1 : threads;
+  const auto t0 = clk::now();
+  if (pool != 0) {
+    static thread_local std::unique_ptr<paraplan::detail::ThreadPool> tp;
+    if (!tp || tp->workers() != w) tp = std::make_unique<paraplan::detail::ThreadPool>(w);
+    const auto t1 = clk::now();
+    tp->run([&](int) { spin(n); });
+    return std::chrono::duration<double, std::milli>(clk::now() - t1).count();
+  }
+  std::vector<std::thread> ts;
+  for (int i = 1; i < w; ++i) ts.emplace_back([&] { spin(n); });
+  spin(n);
+  for (auto& t : ts) t.join();
+  return std::chrono::duration<double, std::milli>(clk::now() - t0).count();
+}
+
+// Snapshot i (0-based) of the reference's acceptance criterion 9 sequence
+// (tests/acceptance_test.cpp:271-334): mt19937_64(4242), the same
+// distributions drawn in the same order, points extrapolated over H = 60 by
+// the reference's extrapolate. warm (capacity 18) receives the warm start
+// when the sequence draws one (*warm_len = 18, else 0). Returns n_points.
+int ref_acceptance9_snapshot(int32_t index, int32_t H, pp_snapshot* out, double* field_xy,
+                             int64_t cap, double* warm, int32_t* warm_len) {
+  int n = -1;
+  guarded([&] {
+    constexpr double pi = 3.141592653589793;
+    std::mt19937_64 rng(4242);
+    std::uniform_real_distribution<double> pos(-20.0, 20.0);
+    std::uniform_real_distribution<double> ang(-2.0 * pi, 2.0 * pi);
+    std::uniform_real_distribution<double> vel(-8.0, 12.0);
+    std::uniform_real_distribution<double> unit(-1.0, 1.0);
+    std::uniform_int_distribution<int> n_pts(0, 12);
+    for (int i = 0; i <= index; ++i) {
+      PlanningSnapshot snap;
+      snap.ev_state.x = pos(rng);
+      snap.ev_state.y = pos(rng);
+      snap.ev_state.phi = ang(rng);
+      snap.ev_state.v = vel(rng);
+      snap.actuator.delta = 0.6 * unit(rng);
+      snap.prev_action.a0 = 0.9 * unit(rng);
+      snap.prev_action.a1 = 0.9 * unit(rng);
+      snap.goal.x = snap.ev_state.x + pos(rng);
+      snap.goal.y = snap.ev_state.y + pos(rng);
+      snap.goal.phi = ang(rng);
+      snap.goal.v = vel(rng);
+      std::vector<ObstaclePoint> pts;
+      const int count = n_pts(rng);
+      for (int j = 0; j < count; ++j) {
+        ObstaclePoint q;
+        q.x = snap.ev_state.x + pos(rng);
+        q.y = snap.ev_state.y + pos(rng);
+        q.heading = ang(rng);
+        q.speed = std::abs(vel(rng));
+        pts.push_back(q);
+      }
+      const ExtrapolatedField f =
+          extrapolate(pts, H, 0.1, {snap.ev_state.x, snap.ev_state.y, snap.ev_state.phi});
+      std::vector<double> wt;
+      if (unit(rng) > 0.0) {
+        wt.resize(18);
+        for (double& w : wt) w = unit(rng);
+      }
+      if (i < index) continue;
+      out->ev_x = snap.ev_state.x;
+      out->ev_y = snap.ev_state.y;
+      out->ev_phi = snap.ev_state.phi;
+      out->ev_v = snap.ev_state.v;
+      out->actuator_delta = snap.actuator.delta;
+      out->prev_a0 = snap.prev_action.a0;
+      out->prev_a1 = snap.prev_action.a1;
+      out->goal_x = snap.goal.x;
+      out->goal_y = snap.goal.y;
+      out->goal_phi = snap.goal.phi;
+      out->goal_v = snap.goal.v;
+      out->field_H = f.H;
+      out->n_points = f.n_points;
+      if (static_cast<int64_t>(2 * f.positions.size()) > cap) throw std::runtime_error("cap");
+      for (std::size_t k = 0; k < f.positions.size(); ++k) {
+        field_xy[2 * k] = f.positions[k].x;
+        field_xy[2 * k + 1] = f.positions[k].y;
+      }
+      out->field_xy = field_xy;
+      *warm_len = static_cast<int32_t>(wt.size());
+      for (std::size_t k = 0; k < wt.size(); ++k) warm[k] = wt[k];
+      out->warm_theta = wt.empty() ? nullptr : warm;
+      out->warm_theta_len = static_cast<int32_t>(wt.size());
+      n = f.n_points;
+    }
   });
   return n;
 }

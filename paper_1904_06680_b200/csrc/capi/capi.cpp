@@ -109,10 +109,7 @@ pp_status pp_create(const pp_model* m, pp_handle** out) {
     hp->device = hp->cfg.device;
     const int n_dev = m->config.n_devices;
     if (n_dev > PP_MAX_DEVICES) throw std::invalid_argument("at most 8 devices per planner");
-    if (n_dev > 1) {
-      hp->device = m->config.devices[0];
-      hp->pool_threads = std::max(2, 16 / n_dev);
-    }
+    if (n_dev > 1) hp->device = m->config.devices[0];
 
     int n = 0;
     if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
@@ -127,6 +124,8 @@ pp_status pp_create(const pp_model* m, pp_handle** out) {
                      " is not sm_100 (B200); kernels are built for sm_100a only");
     }
     ck(cudaSetDevice(hp->device), "cudaSetDevice");
+    ck(cudaDeviceGetAttribute(&hp->sms, cudaDevAttrMultiProcessorCount, hp->device), "SM count");
+    hp->base.sms = hp->sms;
     ck(cudaStreamCreateWithFlags(&hp->stream, cudaStreamNonBlocking), "stream");
     ck(cudaEventCreate(&hp->ev0), "event");
     ck(cudaEventCreate(&hp->ev1), "event");
@@ -149,10 +148,7 @@ pp_status pp_create(const pp_model* m, pp_handle** out) {
       mk.config.device = m->config.devices[k];
       pp_handle* g = nullptr;
       sst = pp_create(&mk, &g);
-      if (sst == PP_OK) {
-        g->pool_threads = h->pool_threads;
-        h->shards.push_back(g);
-      }
+      if (sst == PP_OK) h->shards.push_back(g);
     }
     if (sst == PP_OK && !h->shards.empty()) {
       sst = guarded([&] {
@@ -281,6 +277,10 @@ pp_status pp_sample_candidate(const pp_handle* h, const double* center, int32_t 
 
 double pp_perturbation_sigma(const pp_handle* h, uint64_t t, int32_t restart, int32_t iter,
                              int32_t candidate) {
+  if (h == nullptr) {  // no status out-parameter: NaN marks the invalid handle
+    g_error = "null argument";
+    return std::nan("");
+  }
   paraplan::KeyedRng rng(h->cfg.master_seed, t, static_cast<uint64_t>(restart),
                          static_cast<uint64_t>(iter), static_cast<uint64_t>(candidate));
   return std::pow(10.0, h->cfg.sigma_log_low +
@@ -302,6 +302,7 @@ pp_status pp_draw_theta(pp_handle* h, const double* center, int32_t len, uint64_
     if (n == 0) return;
     ck(cudaSetDevice(h->device), "cudaSetDevice");
     ppdev::RoundArgs a{};
+    a.sms = h->sms;
     a.sig_lo = h->cfg.sigma_log_low;
     a.sig_span = h->cfg.sigma_log_high - h->cfg.sigma_log_low;
     a.n_params = h->P;
@@ -417,6 +418,7 @@ void gather_shard_timing(pp_handle* h) {
   for (pp_handle* g : h->shards) {
     const pp_timing& q = g->timing;
     h->timing.kernel_ms = std::max(h->timing.kernel_ms, q.kernel_ms);
+    h->timing.rollout_ms = std::max(h->timing.rollout_ms, q.rollout_ms);
     h->timing.executed_steps += q.executed_steps;
     h->timing.checked_states += q.checked_states;
     h->timing.samples += q.samples;

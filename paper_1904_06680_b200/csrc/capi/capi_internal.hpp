@@ -230,6 +230,24 @@ class HostPool {
   std::atomic<bool> stop_{false};
 };
 
+// One certification pool per process, shared by every planner handle (a
+// run_sweep drives several planners at once; one pool per planner would
+// oversubscribe the host with spinning workers). One thread per host core
+// but one; callers take turns (lock()), a certification is tens of us.
+struct SharedPool {
+  std::mutex mu;
+  std::unique_ptr<HostPool> pool;
+};
+inline SharedPool& shared_pool() {
+  static SharedPool* sp = [] {
+    auto* p = new SharedPool;  // never destroyed: planners may outlive statics
+    const unsigned hc = std::thread::hardware_concurrency();
+    p->pool = std::make_unique<HostPool>(static_cast<int>(std::max(1u, hc > 1 ? hc - 1 : 1u)));
+    return p;
+  }();
+  return *sp;
+}
+
 inline bool key_better(const Key& a, const Key& b) {  // src/planner.cpp:40-44
   if (a.cls != b.cls) return a.cls > b.cls;
   if (a.k1 != b.k1) return a.k1 > b.k1;
@@ -248,7 +266,8 @@ constexpr size_t kFreeOff = kRecOff + sizeof(ppdev::Rec) * ppdev::kMaxRestartsPe
 constexpr size_t kSelOff =
     (kFreeOff + sizeof(ppdev::Rec) * ppdev::kMaxRestartsPerLaunch + 63) / 64 * 64;
 constexpr size_t kRoundBytes = kSelOff + sizeof(int64_t) * kSelCap;
-constexpr int kRefineGrid = 148 * 2;
+// refine_kernel: two CTAs of 128 threads per SM
+inline int refine_grid(int sms) { return sms * 2; }
 
 // PARAPLAN_TRACE=1: one stderr line per certification pass; 2: also the
 // host-side phase times of every plan step (diagnostics).
@@ -298,6 +317,7 @@ struct pp_handle {
   int P = 0;
   ppdev::NetKind kind = ppdev::NetKind::kGeneric;
   int device = 0;
+  int sms = 148;  // multiprocessors of `device` (queried at construction)
   bool fp64 = false;
 
   cudaStream_t stream = nullptr;
@@ -318,7 +338,7 @@ struct pp_handle {
   pp_snapshot snap_copy{};
   std::vector<double> snap_warm;
   double sel_rho = 1e-3;   // FP32 window: cost <= best * (1 + rho) + 1e-6
-  std::unique_ptr<ppcapi::HostPool> pool;  // exact re-evaluation of near ties
+  ppcapi::HostPool* pool = nullptr;  // exact re-evaluation of near ties (shared_pool())
   double dmarg32 = 2e-5;   // FP32 margin below which a worse-side verdict may flip
   // The certification's FP64 rollouts of each certified restart winner in
   // the current plan step (stats + trajectory, recorded while the window is
@@ -347,7 +367,6 @@ struct pp_handle {
   std::vector<pp_handle*> shards;
   std::unique_ptr<ppcapi::HostPool> shard_pool;
   std::function<void()> pending_upload;
-  int pool_threads = 16;  // certification pool size (split between shards)
   ppdev::RoundArgs base{};
   int field_smem_bytes = 0;
 

@@ -162,7 +162,7 @@ void run_round_launch(pp_handle* h, uint64_t t, int iter, int r0, int rc, const 
     a.sel_out = static_cast<ppdev::SelRec*>(h->d_sel.p);
     a.sel_list = reinterpret_cast<int64_t*>(dres + kSelOff);
     a.sel_cap = kSelCap;
-    a.refine_grid = kRefineGrid;
+    a.refine_grid = refine_grid(h->sms);
     a.sel_rho = fp64 ? 1e-11 : h->sel_rho;
     a.sel_alpha = fp64 ? 1e-13 : 1e-6;
   }
@@ -208,7 +208,7 @@ void run_round_launch(pp_handle* h, uint64_t t, int iter, int r0, int rc, const 
                                                          : a.n_tiles));
   a.field_smem_bytes = field_smem;
   // tile records (x2 for keys_only: best and best unflagged)
-  const size_t n_recs = shape.refill ? 2 * static_cast<size_t>(rc) * std::max(a.grid, 148 * 4)
+  const size_t n_recs = shape.refill ? 2 * static_cast<size_t>(rc) * std::max(a.grid, h->sms * 4)
                                     : static_cast<size_t>(a.n_tiles);
   h->d_tiles.reserve(sizeof(ppdev::Rec) * n_recs, "tile records");
   a.tile_recs = static_cast<ppdev::Rec*>(h->d_tiles.p);
@@ -218,7 +218,7 @@ void run_round_launch(pp_handle* h, uint64_t t, int iter, int r0, int rc, const 
                        (fp64 && h->kind == ppdev::NetKind::k5_10_10_2);
   if (generic || rerank) {
     const size_t lanes = std::max<size_t>(generic ? static_cast<size_t>(a.grid) * a.block : 0,
-                                          rerank ? kRefineGrid * 128 : 0);
+                                          rerank ? refine_grid(h->sms) * 128 : 0);
     h->d_scratch.reserve(lanes * h->P * sizeof(double), "theta scratch");
     a.theta_scratch = static_cast<float*>(h->d_scratch.p);
     a.theta_scratch64 = static_cast<double*>(h->d_scratch.p);
@@ -232,11 +232,7 @@ void run_round_launch(pp_handle* h, uint64_t t, int iter, int r0, int rc, const 
   if (rerank) {
     // the selection counter was re-armed by the rollout kernel's last CTA
     ck(static_cast<cudaError_t>(ppdev::launch_select(a, h->stream)), "window select launch");
-    if (!h->pool) {
-      const unsigned hc = std::thread::hardware_concurrency();
-      h->pool = std::make_unique<HostPool>(
-        static_cast<int>(std::min(static_cast<unsigned>(h->pool_threads), std::max(1u, hc - 1))));
-    }
+    if (h->pool == nullptr) h->pool = shared_pool().pool.get();
   }
   // one D2H: counters (selection count), work counters, winners and the
   // first kSelFirst selected indices, stored into pinned host memory by a
@@ -275,6 +271,7 @@ void run_round_launch(pp_handle* h, uint64_t t, int iter, int r0, int rc, const 
   const unsigned long long* ex = reinterpret_cast<const unsigned long long*>(hres + kExecOff);
   h->timing.executed_steps += static_cast<int64_t>(ex[2]);
   h->timing.checked_states += static_cast<int64_t>(ex[3]);
+  h->timing.rollout_ms += 1e-6 * static_cast<double>(ex[6]);
   const ppdev::Rec* recs = reinterpret_cast<const ppdev::Rec*>(hres + kRecOff);
   for (int r = 0; r < rc; ++r) {
     out[r].cls = recs[r].cls;
@@ -367,10 +364,34 @@ void certify_round(pp_handle* h, ppdev::RoundArgs& a, uint64_t t, int iter, int 
     e.k2 = e.cls == 2 ? -st.path_length : 0.0;
     return e;
   };
-  if (!h->pool) {
-    const unsigned hc = std::thread::hardware_concurrency();
-    h->pool = std::make_unique<HostPool>(
-        static_cast<int>(std::min(static_cast<unsigned>(h->pool_threads), std::max(1u, hc - 1))));
+  if (h->pool == nullptr) h->pool = shared_pool().pool.get();
+  // Every rollout starts from the same state 0, so the checks at state 0
+  // (collision with field row 0, then the goal box; src/planner.cpp:137-152)
+  // do not depend on theta. If they stop the rollout there, every candidate
+  // of the round has the same exact key, and each restart's winner is its
+  // lowest index (strict-better scans, :295, :316). The window would hold
+  // the whole round (equal keys), so the round is certified directly.
+  {
+    std::vector<double> th0(ctr);
+    if (injected != nullptr) th0.assign(injected, injected + h->P);
+    pp_rollout_stats st{};
+    host_rollout(h, snap, th0.data(), &st, nullptr, 0, nullptr);
+    if (st.steps == 0) {
+      const int cls = st.collided ? 0 : (st.reached ? 2 : 1);
+      const double k1 = cls == 2 ? -static_cast<double>(st.t_goal) : -st.terminal_cost;
+      const double k2 = cls == 2 ? -st.path_length : 0.0;
+      for (int r = 0; r < rc; ++r) {
+        out[r].cls = cls;
+        out[r].candidate = static_cast<int>(c0);
+        out[r].k1 = k1;
+        out[r].k2 = k2;
+      }
+      if (trace_on()) {
+        std::fprintf(stderr, "[paraplan] t=%llu iter=%d: every rollout stops at state 0\n",
+                     static_cast<unsigned long long>(t), iter);
+      }
+      return;
+    }
   }
   const double rho = a.sel_rho, alpha = a.sel_alpha;
   std::vector<ppdev::SelBound> bound(rc);
@@ -438,6 +459,7 @@ void certify_round(pp_handle* h, ppdev::RoundArgs& a, uint64_t t, int iter, int 
     std::vector<Exact> got(list.size());
     if (list.size() <= static_cast<size_t>(host_max())) {
       const int base = take_slots(list.size());
+      std::lock_guard<std::mutex> turn(shared_pool().mu);
       h->pool->run(static_cast<int>(list.size()), [&](int i) {
         got[i] = exact_of(list[i], base < 0 ? -1 : base + i);
       });
@@ -480,6 +502,7 @@ void certify_round(pp_handle* h, ppdev::RoundArgs& a, uint64_t t, int iter, int 
         }
       }
       const int base = take_slots(ties.size());
+      std::lock_guard<std::mutex> turn(shared_pool().mu);
       h->pool->run(static_cast<int>(ties.size()), [&](int j) {
         got[ties[j]] = exact_of(list[ties[j]], base < 0 ? -1 : base + j);
       });

@@ -128,6 +128,7 @@ void finish_field(pp_handle* h, ppdev::RoundArgs& a) {
       ba.dst = reinterpret_cast<int32_t*>(df + l.dst);
       ba.cursor = static_cast<int32_t*>(h->d_bin.p);
       ba.fp64 = h->fp64 ? 1 : 0;
+      ba.sms = h->sms;
       ck(static_cast<cudaError_t>(ppdev::bin_movers(ba, st)), "mover binning");
       h->timing.launches += 3;
     } else {

@@ -113,7 +113,7 @@ int bin_movers(const BinArgs& a, void* stream) {
   cudaError_t e = cudaMemsetAsync(a.dst, 0, sizeof(int32_t) * a.rows * static_cast<size_t>(cells + 1), st);
   if (e != cudaSuccess) return static_cast<int>(e);
   const int64_t total = static_cast<int64_t>(a.rows) * a.Nd;
-  const int blocks = static_cast<int>(std::min<int64_t>((total + 255) / 256, 148 * 32));
+  const int blocks = static_cast<int>(std::min<int64_t>((total + 255) / 256, std::max(a.sms, 1) * 32));
   count_kernel<<<blocks, 256, 0, st>>>(a);
   scan_kernel<<<a.rows, 1024, 0, st>>>(a);
   scatter_kernel<<<blocks, 256, 0, st>>>(a);

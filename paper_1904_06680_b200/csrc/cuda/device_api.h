@@ -157,6 +157,8 @@ struct RoundArgs {
   double sel_rho, sel_alpha;   // window: cost <= best * (1 + rho) + alpha
   const SelBound* sel_bound;   // null: first pass (window around a.out)
   double dmarg32;              // FP32 marginal threshold (host side, copied into kf)
+  int32_t sms;                 // multiprocessors of the device (launch sizing)
+  int32_t _pad_sms;
 };
 
 // Architecture dispatch of the specialised kernels.
@@ -225,7 +227,7 @@ struct BinArgs {
   int32_t* dst;          // rows x (cells + 1) starts
   int32_t* cursor;       // rows x cells scratch
   int32_t fp64;
-  int32_t _pad;
+  int32_t sms;  // multiprocessors of the device (launch sizing)
 };
 int bin_movers(const BinArgs& a, void* stream);
 

@@ -270,11 +270,30 @@ __device__ __forceinline__ void reduce_recs_warps(const RoundArgs& a, const Rec*
   __syncthreads();  // every restart's record is written before publish_round
 }
 
+// %globaltimer (ns): the rollout kernel's own span, first CTA start to last
+// CTA end (exec[4] holds ~min start, exec[5] max end; published in exec[6]),
+// so the roofline divides by the kernel alone without an event between the
+// dependent launches.
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void mark_start(const RoundArgs& a) {
+  if (threadIdx.x == 0) atomicMax(&a.exec[4], ~global_ns());
+}
+__device__ __forceinline__ void mark_end(const RoundArgs& a) {
+  if (threadIdx.x == 0) atomicMax(&a.exec[5], global_ns());
+}
+
 // Publish the work counters and re-arm the tickets (last block only).
 __device__ __forceinline__ void publish_round(const RoundArgs& a) {
   if (threadIdx.x == 0) {
     a.exec[2] = atomicExch(&a.exec[0], 0ull);
     a.exec[3] = atomicExch(&a.exec[1], 0ull);
+    const unsigned long long t0 = ~atomicExch(&a.exec[4], 0ull);
+    const unsigned long long t1 = atomicExch(&a.exec[5], 0ull);
+    a.exec[6] = t1 > t0 ? t1 - t0 : 0ull;
     a.counters[0] = 0;
     a.counters[1] = 0;
     a.counters[2] = 0;  // the window selection that follows counts from zero

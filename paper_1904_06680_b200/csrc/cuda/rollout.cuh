@@ -110,6 +110,7 @@ __global__ void __launch_bounds__(kBlock, refill_min_blocks<Real, Net>())
   __shared__ Key red[32];
   __shared__ unsigned long long red_sum[32];
 
+  mark_start(a);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const Consts<Real>& K = consts_of<Real>(a);
   const int H = a.H;
@@ -214,6 +215,7 @@ __global__ void __launch_bounds__(kBlock, refill_min_blocks<Real, Net>())
   }
 
   // -------- flush lane bests, combine warps, publish CTA records --------
+  mark_end(a);
   const unsigned long long steps = block_sum(static_cast<unsigned long long>(n_steps), red_sum);
   const unsigned long long states = block_sum(static_cast<unsigned long long>(n_states), red_sum);
   if (threadIdx.x == 0) {
@@ -329,6 +331,7 @@ __global__ void __launch_bounds__(kBlock) lockstep_kernel(const RoundArgs a) {
   __shared__ unsigned long long red_sum[32];
   __shared__ int s_tile;
 
+  mark_start(a);
   const Consts<Real>& K = consts_of<Real>(a);
   const int H = a.H;
   const int P = a.n_params;
@@ -376,6 +379,7 @@ __global__ void __launch_bounds__(kBlock) lockstep_kernel(const RoundArgs a) {
     // tile records are restart-major: [r][tile within restart]
     if (threadIdx.x == 0) a.tile_recs[tile] = Rec{best.cls, best.idx, best.k1, best.k2};
   }
+  mark_end(a);
   const unsigned long long steps = block_sum(static_cast<unsigned long long>(n_steps), red_sum);
   const unsigned long long states = block_sum(static_cast<unsigned long long>(n_states), red_sum);
   if (threadIdx.x == 0) {
@@ -504,7 +508,7 @@ static __global__ void __launch_bounds__(256) draw_kernel(const RoundArgs a, Rea
 
 template <typename Real>
 int launch_draw_impl(const RoundArgs& a, void* out, void* stream) {
-  const int blocks = static_cast<int>(std::min<int64_t>((a.count + 255) / 256, 148 * 8));
+  const int blocks = static_cast<int>(std::min<int64_t>((a.count + 255) / 256, std::max(a.sms, 1) * 8));
   draw_kernel<Real><<<std::max(blocks, 1), 256, 0, static_cast<cudaStream_t>(stream)>>>(
       a, static_cast<Real*>(out));
   return static_cast<int>(cudaGetLastError());
@@ -601,7 +605,7 @@ int launch_rollout_impl(const RoundArgs& a, void* stream) {
   if (e == cudaSuccess && a.keys_only) {
     // about four blocks per SM over all restarts
     const int64_t per = std::max<int64_t>(1, std::min<int64_t>((a.count + 2047) / 2048,
-                                                              148 * 4 / a.restart_count));
+                                                              std::max(a.sms, 1) * 4 / a.restart_count));
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(static_cast<unsigned>(per), static_cast<unsigned>(a.restart_count));
     cfg.blockDim = dim3(256);
@@ -619,7 +623,7 @@ int launch_rollout_impl(const RoundArgs& a, void* stream) {
 // Near-tie window of a finished round (a dependent launch after the rollout).
 inline int launch_select_impl(const RoundArgs& a, void* stream) {
   const int64_t total = a.count * a.restart_count;
-  const int blocks = static_cast<int>(std::min<int64_t>((total + 255) / 256, 148 * 16));
+  const int blocks = static_cast<int>(std::min<int64_t>((total + 255) / 256, std::max(a.sms, 1) * 16));
   return static_cast<int>(
       launch_dependent(select_kernel, blocks, 256, 0, static_cast<cudaStream_t>(stream), true, a));
 }

@@ -72,21 +72,36 @@ def builtin_snapshot(name: str, t: int, H: int, n_obst_pts: int = 20,
     return snapshot_from_mission(m, m.initial_state, t, H, n_obst_pts)
 
 
+C2_T = 5
+C2_H = 30
+C2_N_OBST = 20
+
+
+def c2_mission_arrays():
+    """C2 mission as plain arrays (no native code): waypoints (x, y, phi, v),
+    static and dynamic points (x, y, heading, speed) in the world frame, EV
+    state (x, y, phi, v). The reference's sensing fixture
+    (mission_test.cpp:54-74)."""
+    wp = np.array([[50.0, 0.0, 0.0, 50.0 / 3.6]])
+    st = []
+    for i in range(8):
+        st.append((2.0 + 3.0 * i, -1.75, 0.0, 0.0))
+        st.append((2.0 + 3.0 * i, 5.25, 0.0, 0.0))
+    sp = 20.0 / 3.6
+    dy = [(28.2, -1.0, math.pi, sp), (28.2, 1.0, math.pi, sp),
+          (32.0, -1.0, math.pi, sp), (32.0, 1.0, math.pi, sp)]
+    ev = np.array([0.0, 0.0, 0.0, 50.0 / 3.6])
+    return wp, np.array(st), np.array(dy), ev
+
+
 def c2_mission():
     pp = _pp()
+    wp, st, dy, ev = c2_mission_arrays()
     m = pp.Mission()
-    m.waypoints = [pp.GoalSetpoint(50.0, 0.0, 0.0, 50.0 / 3.6)]
-    pts = []
-    for i in range(8):
-        pts.append(pp.ObstaclePoint(2.0 + 3.0 * i, -1.75, 0.0, 0.0))
-        pts.append(pp.ObstaclePoint(2.0 + 3.0 * i, 5.25, 0.0, 0.0))
-    m.static_points = pts
-    sp = 20.0 / 3.6
-    m.dynamic_points = [pp.ObstaclePoint(28.2, -1.0, math.pi, sp),
-                        pp.ObstaclePoint(28.2, 1.0, math.pi, sp),
-                        pp.ObstaclePoint(32.0, -1.0, math.pi, sp),
-                        pp.ObstaclePoint(32.0, 1.0, math.pi, sp)]
-    m.initial_state = pp.VehicleState(0.0, 0.0, 0.0, 50.0 / 3.6)
+    m.waypoints = [pp.GoalSetpoint(*w) for w in wp]
+    m.static_points = [pp.ObstaclePoint(*q) for q in st]
+    m.dynamic_points = [pp.ObstaclePoint(*q) for q in dy]
+    m.initial_state = pp.VehicleState(*ev)
     return m
 
 
@@ -100,9 +115,9 @@ def c1(precision: int = abi.PP_FP32, samples: int = 4096) -> Workload:
 
 
 def c2(precision: int = abi.PP_FP32, samples: int = 1 << 20) -> Workload:
-    H = 30
+    H = C2_H
     m = c2_mission()
-    snap = snapshot_from_mission(m, m.initial_state, 5, H, 20)
+    snap = snapshot_from_mission(m, m.initial_state, C2_T, H, C2_N_OBST)
     model = abi.Model(H=H, n_restarts=1, n_candidates=samples, precision=precision)
     return Workload("C2", model, snap, 5,
                     f"dynamic obstacle avoidance: 16 static + 4 oncoming points at 20 km/h "

@@ -1,0 +1,146 @@
+"""Measurement (GPU box, test infrastructure): the device rollout's error
+against the reference arithmetic, per configuration.
+
+For every candidate of one sampling round it compares the device FP32 and
+FP64 rollouts (per-sample stats, no re-ranking) with the oracle port's exact
+FP64 stats (pinned bitwise to the reference), and reports
+  * discrete flips (class, t_goal) FP32 / FP64 vs exact,
+  * relative error quantiles of the cost on same-outcome samples,
+  * the same restricted to the candidates that matter for the argmin (exact
+    cost within 10% / 2x of the exact best of the winning class),
+  * where the exact winner sits in the FP32 order: the relative FP32 cost
+    gap a window must span to contain it ("rho needed"),
+  * whether the certified plan (refine=1) returns the exact winner.
+
+Usage: python tests/measure_fp_error.py [out.json] [--quick]
+"""
+from __future__ import annotations
+
+import json
+import os
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+
+from oracle.oracle import Port, Ref  # noqa: E402
+from paper_1904_06680_b200 import abi, capi, workloads  # noqa: E402
+
+NPROC = os.cpu_count() or 1
+
+
+def keys(st):
+    cls = np.where(st["collided"] != 0, 0, np.where(st["reached"] != 0, 2, 1))
+    cost = np.where(cls == 2, st["path_length"], st["terminal_cost"])
+    tg = np.where(cls == 2, st["t_goal"], 0)
+    return cls, tg, cost
+
+
+def order(cls, tg, cost):
+    """Indices best-first by (cls desc, t_goal asc, cost asc, index asc)."""
+    n = len(cls)
+    return np.lexsort((np.arange(n), cost, tg, -cls))
+
+
+def quant(r):
+    if r.size == 0:
+        return None
+    return {"n": int(r.size), "p50": float(np.quantile(r, 0.5)), "p99": float(np.quantile(r, 0.99)),
+            "p999": float(np.quantile(r, 0.999)), "max": float(r.max()),
+            "frac_gt_1e-5": float(np.mean(r > 1e-5)), "frac_gt_5e-4": float(np.mean(r > 5e-4))}
+
+
+def measure(name, model, snap, t):
+    n = model.n_candidates
+    out = {"config": name, "samples": n, "H": model.H,
+           "n_points": int(snap.field.shape[1]) if snap.field is not None else 0}
+    t0 = time.time()
+    ex = Port(model).eval_candidates(snap, t, 0, 0, np.zeros(model.param_count()), 0, n,
+                                     threads=NPROC)
+    out["oracle_s"] = time.time() - t0
+    ce, te, ke = keys(ex)
+    oe = order(ce, te, ke)
+    w = oe[0]
+    out["exact_winner"] = {"candidate": int(w), "cls": int(ce[w]), "t_goal": int(te[w]),
+                           "cost": float(ke[w])}
+    same_best = (ce == ce[w]) & (te == te[w])
+    for prec in (32, 64):
+        m = abi.Model(**{**model.__dict__, "precision": prec, "refine": 0, "n_restarts": 1})
+        dp = capi.DevicePlanner(m)
+        _, got = dp.evaluate(snap, t, 0, 0, 1, None, 0, n, per_sample=True)
+        dp.close()
+        cg, tgg, kg = keys(got)
+        flips_cls = int(np.count_nonzero(cg != ce))
+        flips_t = int(np.count_nonzero((cg == ce) & (tgg != te)))
+        same = (cg == ce) & (tgg == te)
+        rel = np.abs(kg - ke) / np.maximum(np.abs(ke), 1e-12)
+        near10 = same & same_best & (ke <= ke[w] * 1.1 + 1e-9)
+        near2x = same & same_best & (ke <= ke[w] * 2.0 + 1e-9)
+        og = order(cg, tgg, kg)
+        d = {"flips_cls": flips_cls, "flips_t_goal": flips_t,
+             "rel_err_same_outcome": quant(rel[same]),
+             "rel_err_within_10pct_of_best": quant(rel[near10]),
+             "rel_err_within_2x_of_best": quant(rel[near2x]),
+             "device_winner": int(og[0]), "device_winner_is_exact": bool(og[0] == w)}
+        # the FP32 gap a window around the device best must span to hold w
+        if cg[w] == cg[og[0]] and tgg[w] == tgg[og[0]]:
+            d["rho_needed"] = float(kg[w] / max(kg[og[0]], 1e-300) - 1.0)
+        else:
+            d["rho_needed"] = None
+            d["exact_winner_device_outcome"] = {"cls": int(cg[w]), "t_goal": int(tgg[w]),
+                                                "cost": float(kg[w])}
+        # candidates whose device verdict is worse than the exact winner's
+        # class/t_goal but exactly at least as good (a flag must catch them)
+        better_exact = (ce > ce[w]) | ((ce == ce[w]) & (te < te[w])) | \
+            ((ce == ce[w]) & (te == te[w]) & (ke <= ke[w]))
+        d["exactly_tied_or_better_count"] = int(np.count_nonzero(better_exact))
+        out[f"fp{prec}"] = d
+    # the certified plan (default path)
+    m = abi.Model(**{**model.__dict__, "precision": 32, "refine": 1, "n_restarts": 1})
+    dp = capi.DevicePlanner(m)
+    rec, _ = dp.evaluate(snap, t, 0, 0, 1, None, 0, n)
+    tm = dp.timing()
+    dp.close()
+    out["certified"] = {"candidate": int(rec[0]["candidate"]),
+                        "equals_exact": bool(rec[0]["candidate"] == w),
+                        "refined": int(tm.refined), "kernel_ms": tm.kernel_ms,
+                        "certify_ms": tm.certify_ms}
+    return out
+
+
+def configs(quick: bool):
+    c2 = workloads.c2(samples=1 << (16 if quick else 20))
+    yield "C2", c2.model, c2.snapshot, c2.t
+    m = workloads.c2_mission()
+    snap = workloads.snapshot_from_mission(m, m.initial_state, workloads.C2_T, 200, 20)
+    yield "C2 scene H=200", abi.Model(H=200, n_restarts=1, n_candidates=1 << (14 if quick else 18)), \
+        snap, workloads.C2_T
+    c4 = workloads.c4(samples=1 << (12 if quick else 16))
+    yield "C4 lot H=200", c4.model, c4.snapshot, c4.t
+    c5 = workloads.c5(1 << (12 if quick else 16), 100, 10000)
+    yield "C5 10k H=100", c5.model, c5.snapshot, c5.t
+    for scene in ("exp1", "exp2", "exp4", "exp5_3wp", "exp3_explicit"):
+        s = Ref.builtin_snapshot(scene, 0, 200)
+        yield f"{scene} H=200", abi.Model(H=200, n_restarts=1,
+                                          n_candidates=1 << (14 if quick else 17)), s, 0
+
+
+def main():
+    out_path = Path(sys.argv[1]) if len(sys.argv) > 1 and not sys.argv[1].startswith("-") \
+        else ROOT / "gpurun_out" / "r2_error_model.json"
+    quick = "--quick" in sys.argv
+    res = []
+    for name, model, snap, t in configs(quick):
+        r = measure(name, model, snap, t)
+        print(json.dumps(r), flush=True)
+        res.append(r)
+        out_path.parent.mkdir(parents=True, exist_ok=True)
+        out_path.write_text(json.dumps(res, indent=1))
+
+
+if __name__ == "__main__":
+    main()

@@ -12,6 +12,9 @@ accepted only as a near tie (same class, key within 1e-5 relative).
 """
 from __future__ import annotations
 
+import json
+import os
+
 import numpy as np
 import pytest
 
@@ -29,7 +32,25 @@ def _rel(a, b):
     return np.abs(a - b) / np.maximum(np.abs(b), 1e-12)
 
 
+RECORD = os.environ.get("PARAPLAN_PARITY_LOG")  # JSON lines of the measured parity
+
+
+def _record(**kw):
+    if RECORD:
+        with open(RECORD, "a") as f:
+            f.write(json.dumps(kw) + "\n")
+
+
 def check_stats(got, want, precision, min_frac=0.99):
+    same0 = (got["collided"] == want["collided"]) & (got["t_goal"] == want["t_goal"]) & \
+            (got["steps"] == want["steps"])
+    _record(test=os.environ.get("PYTEST_CURRENT_TEST", "").split(" ")[0], precision=precision,
+            n=int(len(want)), **{f"flips_{k}": int(np.count_nonzero(got[k] != want[k]))
+                                 for k in ("reached", "collided", "t_goal", "steps")},
+            **{f"within_1e-5_{k}": float(np.mean(_rel(got[k][same0], want[k][same0]) <= 1e-5))
+               for k in ("path_length", "terminal_cost")},
+            **{f"max_rel_{k}": float(_rel(got[k][same0], want[k][same0]).max(initial=0.0))
+               for k in ("path_length", "terminal_cost")})
     for k in ("reached", "collided", "t_goal", "steps"):
         flips = np.count_nonzero(got[k] != want[k])
         assert flips <= (0 if precision == 64 else max(1, len(want) // 200)), (k, flips)
