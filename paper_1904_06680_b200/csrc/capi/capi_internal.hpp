@@ -408,5 +408,6 @@ void host_rollout(const pp_handle* h, const pp_snapshot& s, const double* theta,
                   pp_rollout_stats* out, double* traj, int32_t cap, int32_t* traj_len);
 void host_sample(const pp_handle* h, const double* center, uint64_t t, int restart, int iter,
                  int cand, double* out, int len = -1);
+bool host_stops_at_state0(const pp_handle* h, const pp_snapshot& s, pp_rollout_stats* out);
 
 }  // namespace ppcapi

@@ -93,6 +93,52 @@ void host_rollout(const pp_handle* h, const pp_snapshot& s, const double* theta,
   if (traj_len != nullptr) *traj_len = n;
 }
 
+// The checks of state 0 alone (src/planner.cpp:137-153 at h = 0), which no
+// candidate's theta can influence: returns true when every rollout stops
+// there, with the (common) exact key's stats in *out.
+bool host_stops_at_state0(const pp_handle* h, const pp_snapshot& s, pp_rollout_stats* out) {
+  using namespace paraplan;
+  const auto& cfg = h->cfg;
+  const Pose2 anchor{s.ev_x, s.ev_y, s.ev_phi};
+  const Vec2 gp = to_ev_frame(anchor, {s.goal_x, s.goal_y});
+  const GoalSetpoint goal{gp.x, gp.y, s.goal_phi - anchor.phi, s.goal_v};
+  const double gc = std::cos(goal.phi), gs = std::sin(goal.phi);
+  const VehicleState z{0.0, 0.0, 0.0, s.ev_v};
+  std::memset(out, 0, sizeof(*out));
+  out->t_goal = -1;
+  bool stop = false;
+  if (s.n_points > 0) {
+    bool hit;
+    if (s.field_xy == nullptr) {
+      hit = ppfield::collides(h->field, h->chassis, h->box, 0, z.x, z.y, z.phi);
+    } else {
+      const std::span<const Vec2> row(reinterpret_cast<const Vec2*>(s.field_xy), s.n_points);
+      hit = collision({z.x, z.y, z.phi}, row, h->chassis);
+    }
+    if (hit) {
+      out->collided = 1;
+      stop = true;
+    }
+  }
+  if (!stop) {
+    const double gdx = goal.x - z.x, gdy = goal.y - z.y;
+    if (std::abs(gc * gdx + gs * gdy) <= cfg.tol.eps_xi &&
+        std::abs(-gs * gdx + gc * gdy) <= cfg.tol.eps_eta &&
+        std::abs(wrap_angle(goal.phi - z.phi)) <= cfg.tol.eps_phi &&
+        std::abs(goal.v - z.v) <= cfg.tol.eps_v) {
+      out->reached = 1;
+      out->t_goal = 0;
+      stop = true;
+    }
+  }
+  if (!stop && cfg.H != 0) return false;
+  out->terminal_cost = std::abs(goal.x - z.x) / h->norm.d_xi +
+                       std::abs(goal.y - z.y) / h->norm.d_eta +
+                       std::abs(wrap_angle(goal.phi - z.phi)) / h->norm.d_phi +
+                       std::abs(goal.v - z.v) / h->norm.d_v;
+  return true;
+}
+
 void host_sample(const pp_handle* h, const double* center, uint64_t t, int restart, int iter,
                  int cand, double* out, int len) {
   if (len < 0) len = h->P;

@@ -89,6 +89,7 @@ void run_round_launch(pp_handle* h, uint64_t t, int iter, int r0, int rc, const 
   // (lockstep) or for an FP64 redo it is needed now
   if (h->pending_field && (!shape0.refill || force_fp64)) consume_pending_field(h);
   ppdev::RoundArgs a = h->base;
+  if (a.sms <= 0) throw std::logic_error("round constants without a device SM count");
   if (force_fp64 && !h->fp64) {
     a.field = ensure_field64(h);
     a.lay = a.lay64;
@@ -372,11 +373,8 @@ void certify_round(pp_handle* h, ppdev::RoundArgs& a, uint64_t t, int iter, int 
   // lowest index (strict-better scans, :295, :316). The window would hold
   // the whole round (equal keys), so the round is certified directly.
   {
-    std::vector<double> th0(ctr);
-    if (injected != nullptr) th0.assign(injected, injected + h->P);
     pp_rollout_stats st{};
-    host_rollout(h, snap, th0.data(), &st, nullptr, 0, nullptr);
-    if (st.steps == 0) {
+    if (host_stops_at_state0(h, snap, &st)) {
       const int cls = st.collided ? 0 : (st.reached ? 2 : 1);
       const double k1 = cls == 2 ? -static_cast<double>(st.t_goal) : -st.terminal_cost;
       const double k2 = cls == 2 ? -st.path_length : 0.0;

@@ -265,6 +265,7 @@ void set_round_constants(pp_handle* h, const pp_snapshot& s) {
   const auto& cfg = h->cfg;
   ppdev::RoundArgs& a = h->base;
   a = ppdev::RoundArgs{};
+  a.sms = h->sms;
   const paraplan::Pose2 anchor{s.ev_x, s.ev_y, s.ev_phi};
   const paraplan::Vec2 g = paraplan::to_ev_frame(anchor, {s.goal_x, s.goal_y});
   a.gx = g.x;
