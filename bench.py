@@ -389,6 +389,8 @@ def run_b200(a):
         else:
             sp = ShardedPlanner.on_device(model, rank, world)
 
+            assert sp.exchange() == "nccl", sp.exchange()
+
             def e2e_step():
                 return sp.plan_step(w.snapshot, w.t).action[0]
 
@@ -453,7 +455,9 @@ def run_b200(a):
             "e2e": {"value": e2e_value, "unit": UNIT, "ms_per_step": e2e_s / a.steps * 1e3,
                     "h2d_bytes_per_step": h2d // a.steps, "d2h_bytes_per_step": d2h // a.steps,
                     "api": "paraplan.Planner.plan_step" if world == 1 else
-                           "ShardedPlanner.plan_step (NCCL all-gather of winner records)"},
+                           "pp_plan_step on a pp_comm_init rank (C++ sharded planner: "
+                           "ncclAllReduce(min) of packed winner keys + ncclAllGather of "
+                           "exact bests)"},
             "latency_ms": e2e_s / a.steps * 1e3,
             "gpu_launches": st["launches"],
             "nccl": ({"ranks": world, "version": ".".join(map(str, torch.cuda.nccl.version()))}

@@ -279,6 +279,31 @@ void* pp_stream(const pp_handle* h);
 /* Number of visible CUDA devices (0 without a GPU; never fails). */
 int32_t pp_device_count(void);
 
+/* ---- One process per GPU (torch.distributed / MPI style launch) ----------
+ * The candidates of every sampling round are split into contiguous shards,
+ * rank r of W owning [n r / W, n (r + 1) / W) of each restart. Each rank
+ * evaluates its shard on its own GPU; the per-restart winners are combined by
+ * ONE ncclAllReduce(ncclMin, uint64) on a packed (class, t_goal, FP32 cost,
+ * index) key (n_candidates <= 2^22, H <= 255; else an all-gather of the
+ * records), and the certification's exact keys by an ncclAllGather, so every
+ * rank returns the same plan -- the reference's ordered merge of contiguous
+ * worker ranges (src/planner.cpp:280-281, 310-321). Every rank calls
+ * pp_plan_step / pp_plan_step_points with the same snapshot and t. */
+/* Rank 0 makes the NCCL unique id (128 bytes); the caller shares it. */
+pp_status pp_comm_unique_id(uint8_t* out128);
+/* Joins rank `rank` of a `world`-rank communicator (a one-rank communicator
+ * runs the same exchange path on one GPU). */
+pp_status pp_comm_init(pp_handle* h, const uint8_t* id128, int32_t world, int32_t rank);
+/* The packed key of the winner allreduce (no device needed): smaller is
+ * better in the reference's order (better(), src/planner.cpp:40-44), ties to
+ * the lower candidate index. cls -1 packs to UINT64_MAX. */
+uint64_t pp_pack_key(int32_t cls, int32_t t_goal, float cost, uint32_t candidate);
+void pp_unpack_key(uint64_t key, int32_t* cls, int32_t* t_goal, float* cost,
+                   uint32_t* candidate);
+/* The exchange between the planner's shards: "nccl", "host" (shards of one
+ * process sharing a GPU) or "none" (one shard). */
+const char* pp_exchange_kind(const pp_handle* h);
+
 /* Measured FP32 FMA throughput of `device` in TFLOP/s (FFMA loop, 2 flop per
  * FMA) -- the roofline denominator of the rollout kernel. */
 pp_status pp_measure_fp32_peak(int32_t device, double* tflops, double* sm_mhz);

@@ -67,6 +67,14 @@ def lib():
         L.pp_stream.argtypes = [C.c_void_p]
         L.pp_stream.restype = C.c_void_p
         L.pp_measure_fp32_peak.argtypes = [C.c_int32, P(C.c_double), P(C.c_double)]
+        L.pp_comm_unique_id.argtypes = [C.c_char_p]
+        L.pp_comm_init.argtypes = [C.c_void_p, C.c_char_p, C.c_int32, C.c_int32]
+        L.pp_exchange_kind.argtypes = [C.c_void_p]
+        L.pp_exchange_kind.restype = C.c_char_p
+        L.pp_pack_key.argtypes = [C.c_int32, C.c_int32, C.c_float, C.c_uint32]
+        L.pp_pack_key.restype = C.c_uint64
+        L.pp_unpack_key.argtypes = [C.c_uint64, P(C.c_int32), P(C.c_int32), P(C.c_float),
+                                    P(C.c_uint32)]
         _lib = L
     return _lib
 
@@ -77,7 +85,8 @@ def exported_symbols() -> list[str]:
             "pp_plan_step", "pp_plan_step_points", "pp_upload_points", "pp_draw_theta", "pp_rollout", "pp_sample_candidate", "pp_perturbation_sigma",
             "pp_upload_snapshot", "pp_evaluate", "pp_eval_theta", "pp_merge_records",
             "pp_key_better", "pp_last_timing", "pp_stream", "pp_device_count",
-            "pp_measure_fp32_peak"]
+            "pp_measure_fp32_peak", "pp_comm_unique_id", "pp_comm_init", "pp_exchange_kind",
+            "pp_pack_key", "pp_unpack_key"]
 
 
 def _check(rc: int):
@@ -104,6 +113,24 @@ def measure_fp32_peak(device: int = 0) -> tuple[float, float]:
     tf, mhz = C.c_double(), C.c_double()
     _check(lib().pp_measure_fp32_peak(device, C.byref(tf), C.byref(mhz)))
     return tf.value, mhz.value
+
+
+def comm_unique_id() -> bytes:
+    """NCCL unique id for pp_comm_init (rank 0 makes it, the caller shares it)."""
+    buf = C.create_string_buffer(128)
+    _check(lib().pp_comm_unique_id(buf))
+    return buf.raw
+
+
+def pack_key(cls: int, t_goal: int, cost: float, candidate: int) -> int:
+    """The packed winner key of the cross-GPU allreduce (keypack.h)."""
+    return lib().pp_pack_key(cls, t_goal, cost, candidate)
+
+
+def unpack_key(key: int) -> tuple[int, int, float, int]:
+    c, tg, cost, idx = C.c_int32(), C.c_int32(), C.c_float(), C.c_uint32()
+    lib().pp_unpack_key(key, C.byref(c), C.byref(tg), C.byref(cost), C.byref(idx))
+    return c.value, tg.value, cost.value, idx.value
 
 
 def _dptr(a: np.ndarray):
@@ -192,6 +219,16 @@ class DevicePlanner:
         _check(lib().pp_sample_candidate(self.h, _dptr(c), len(c), t, restart, it, cand,
                                          _dptr(out)))
         return out
+
+    def join_communicator(self, unique_id: bytes, world: int, rank: int):
+        """This planner becomes rank `rank` of `world` (one process per GPU):
+        plan_step evaluates its shard and exchanges over NCCL."""
+        if len(unique_id) != 128:
+            raise ValueError("NCCL unique id must be 128 bytes")
+        _check(lib().pp_comm_init(self.h, unique_id, world, rank))
+
+    def exchange(self) -> str:
+        return lib().pp_exchange_kind(self.h).decode()
 
     def timing(self) -> abi.pp_timing:
         t = abi.pp_timing()

@@ -77,6 +77,36 @@ void prewarm(pp_handle* h) {
   h->timing = pp_timing{};
 }
 
+// The exchange of an in-process sharded planner (PlannerConfig::devices):
+// NCCL over the listed GPUs when they are distinct and NCCL loads, else host
+// memory (shards sharing a GPU: NCCL refuses duplicate devices).
+// PARAPLAN_EXCHANGE=host|nccl forces one (A/B and tests).
+void attach_shard_exchanges(pp_handle* h, const pp_model& m) {
+  const int S = static_cast<int>(h->shards.size()) + 1;
+  std::vector<pp_handle*> all{h};
+  all.insert(all.end(), h->shards.begin(), h->shards.end());
+  std::vector<int> devs;
+  for (pp_handle* g : all) devs.push_back(g->device);
+  std::vector<int> sorted(devs);
+  std::sort(sorted.begin(), sorted.end());
+  const bool distinct = std::adjacent_find(sorted.begin(), sorted.end()) == sorted.end();
+  const char* env = std::getenv("PARAPLAN_EXCHANGE");
+  const std::string want = env != nullptr ? env : "";
+  bool use_nccl = distinct && want != "host" && nccl_available();
+  if (want == "nccl" && !use_nccl) {
+    std::string why = distinct ? "" : "shards share a device";
+    nccl_available(&why);
+    throw std::invalid_argument("PARAPLAN_EXCHANGE=nccl: " + why);
+  }
+  if (use_nccl) {
+    auto ex = make_nccl_exchanges(devs.data(), S);
+    for (int k = 0; k < S; ++k) all[k]->xchg = std::move(ex[k]);
+  } else {
+    h->thread_group = std::make_shared<ThreadGroup>(S);
+    for (int k = 0; k < S; ++k) all[k]->xchg = make_thread_exchange(h->thread_group, k);
+  }
+}
+
 pp_status pp_create(const pp_model* m, pp_handle** out) {
   if (out != nullptr) *out = nullptr;
   pp_handle* h = nullptr;
@@ -153,6 +183,7 @@ pp_status pp_create(const pp_model* m, pp_handle** out) {
     if (sst == PP_OK && !h->shards.empty()) {
       sst = guarded([&] {
         h->shard_pool = std::make_unique<HostPool>(static_cast<int>(h->shards.size()) + 1);
+        attach_shard_exchanges(h, *m);
       });
     }
     if (sst != PP_OK) {
@@ -365,15 +396,29 @@ pp_status pp_merge_records(const pp_record* recs, int32_t n, pp_record* out) {
 
 namespace {
 
-// Planner::plan_step after the snapshot is resident (src/planner.cpp:238-351).
-// One sampling round over every shard of the planner (PlannerConfig
-// devices): shard k evaluates candidates [n k / S, n (k + 1) / S) of each
-// restart on its own device and thread, certifying its own winners; the
-// records are merged in shard order with the strict-better rule, i.e. in
-// increasing candidate index as the reference's ordered merge of worker
-// ranges (src/planner.cpp:280-281, 310-321). One shard: run_round.
+// One sampling round over every shard of the planner. Shard k of S
+// evaluates candidates [n k / S, n (k + 1) / S) of each restart, and the
+// shards exchange their winners and exact keys (round.cpp certify_round,
+// exchange.hpp) so that every shard returns the same, global winner: the
+// reference's ordered merge of its worker ranges (src/planner.cpp:280-281,
+// 310-321). Shards are either the threads of this process (PlannerConfig
+// devices, one handle per device) or the processes of a communicator
+// (pp_comm_init, one process per GPU). One shard: run_round.
+struct ExchangeScope {  // the exchange serves plan steps only
+  pp_handle* g;
+  explicit ExchangeScope(pp_handle* gg) : g(gg) { g->xchg_active = g->xchg != nullptr; }
+  ~ExchangeScope() { g->xchg_active = false; }
+};
+
 void run_round_shards(pp_handle* h, uint64_t t, int iter, int r0, int rc, const double* center,
                       int64_t n, pp_record* out) {
+  if (h->xchg != nullptr && h->shards.empty()) {  // one rank of a communicator
+    ExchangeScope scope(h);
+    const int64_t c0 = n * h->shard_rank / h->shard_world;
+    const int64_t c1 = n * (h->shard_rank + 1) / h->shard_world;
+    run_round(h, t, iter, r0, rc, center, c0, c1, nullptr, out, nullptr);
+    return;
+  }
   if (h->shards.empty()) {
     run_round(h, t, iter, r0, rc, center, 0, n, nullptr, out, nullptr);
     return;
@@ -381,7 +426,7 @@ void run_round_shards(pp_handle* h, uint64_t t, int iter, int r0, int rc, const 
   const int S = static_cast<int>(h->shards.size()) + 1;
   std::vector<std::vector<pp_record>> recs(S, std::vector<pp_record>(rc));
   std::vector<std::exception_ptr> errs(S);
-  std::vector<std::string> msgs(S);
+  if (h->thread_group) h->thread_group->reset();
   h->shard_pool->run(S, [&](int k) {
     pp_handle* g = k == 0 ? h : h->shards[k - 1];
     try {
@@ -391,24 +436,26 @@ void run_round_shards(pp_handle* h, uint64_t t, int iter, int r0, int rc, const 
         g->pending_upload = nullptr;
         up();
       }
+      ExchangeScope scope(g);
       run_round(g, t, iter, r0, rc, center, n * k / S, n * (k + 1) / S, nullptr, recs[k].data(),
                 nullptr);
     } catch (...) {
       errs[k] = std::current_exception();
+      if (h->thread_group) h->thread_group->abort();  // release the other shards
     }
   });
   ck(cudaSetDevice(h->device), "cudaSetDevice");
   for (auto& e : errs) {
     if (e) std::rethrow_exception(e);
   }
+  // every shard certified the same global winners
   for (int r = 0; r < rc; ++r) {
-    pp_record m = recs[0][r];
     for (int k = 1; k < S; ++k) {
-      const pp_record& q = recs[k][r];
-      if (q.cls < 0) continue;
-      if (m.cls < 0 || key_better({q.cls, q.k1, q.k2}, {m.cls, m.k1, m.k2})) m = q;
+      if (recs[k][r].candidate != recs[0][r].candidate || recs[k][r].cls != recs[0][r].cls) {
+        throw std::logic_error("sharded round: shards disagree on the winner");
+      }
     }
-    out[r] = m;
+    out[r] = recs[0][r];
   }
 }
 
@@ -597,6 +644,51 @@ pp_status pp_plan_step_points(pp_handle* h, const pp_snapshot_points* snap, uint
     g_clock = nullptr;
     clock.flush();
   });
+}
+
+pp_status pp_comm_unique_id(uint8_t* out) {
+  return guarded([&] {
+    if (out == nullptr) throw std::invalid_argument("null argument");
+    std::string why;
+    if (!nccl_available(&why)) throw std::runtime_error("NCCL unavailable: " + why);
+    nccl_unique_id(out);
+  });
+}
+
+pp_status pp_comm_init(pp_handle* h, const uint8_t* id, int32_t world, int32_t rank) {
+  return guarded([&] {
+    if (h == nullptr || id == nullptr) throw std::invalid_argument("null argument");
+    if (world < 1 || rank < 0 || rank >= world) throw std::invalid_argument("bad rank / world");
+    if (!h->shards.empty()) {
+      throw std::invalid_argument("a planner over several devices cannot join a communicator");
+    }
+    if (h->cfg.n_candidates < world) {
+      throw std::invalid_argument("fewer candidates than ranks");
+    }
+    ck(cudaSetDevice(h->device), "cudaSetDevice");
+    h->xchg.reset();
+    h->xchg = make_nccl_exchange(id, world, rank);
+    h->shard_rank = rank;
+    h->shard_world = world;
+  });
+}
+
+uint64_t pp_pack_key(int32_t cls, int32_t t_goal, float cost, uint32_t candidate) {
+  return ppdev::pack_key(cls, t_goal, cost, candidate);
+}
+
+void pp_unpack_key(uint64_t key, int32_t* cls, int32_t* t_goal, float* cost,
+                   uint32_t* candidate) {
+  const ppdev::Unpacked u = ppdev::unpack_key(key);
+  if (cls != nullptr) *cls = u.cls;
+  if (t_goal != nullptr) *t_goal = u.t_goal;
+  if (cost != nullptr) *cost = u.cost;
+  if (candidate != nullptr) *candidate = u.idx;
+}
+
+const char* pp_exchange_kind(const pp_handle* h) {
+  if (h == nullptr || h->xchg == nullptr) return "none";
+  return h->xchg->kind();
 }
 
 pp_status pp_measure_fp32_peak(int32_t device, double* tflops, double* sm_mhz) {

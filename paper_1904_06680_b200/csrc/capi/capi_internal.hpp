@@ -32,6 +32,7 @@
 #include <vector>
 
 #include "../cuda/device_api.h"
+#include "exchange.hpp"
 #include "field.hpp"
 #include "paraplan/geometry.hpp"
 #include "paraplan/planner.hpp"
@@ -263,8 +264,12 @@ constexpr size_t kExecOff = 64;
 constexpr size_t kRecOff = 128;
 // [Rec x kMaxRestartsPerLaunch] best unflagged per restart (keys_only rounds)
 constexpr size_t kFreeOff = kRecOff + sizeof(ppdev::Rec) * ppdev::kMaxRestartsPerLaunch;
-constexpr size_t kSelOff =
+// [uint64 x 2 x kMaxRestartsPerLaunch] packed winners of a sharded round
+// (keypack.h), reduced across the shards in place
+constexpr size_t kPackOff =
     (kFreeOff + sizeof(ppdev::Rec) * ppdev::kMaxRestartsPerLaunch + 63) / 64 * 64;
+constexpr size_t kSelOff =
+    (kPackOff + sizeof(uint64_t) * 2 * ppdev::kMaxRestartsPerLaunch + 63) / 64 * 64;
 constexpr size_t kRoundBytes = kSelOff + sizeof(int64_t) * kSelCap;
 // refine_kernel: two CTAs of 128 threads per SM
 inline int refine_grid(int sms) { return sms * 2; }
@@ -366,6 +371,16 @@ struct pp_handle {
   // snapshot upload of the current plan step (done on its own thread)
   std::vector<pp_handle*> shards;
   std::unique_ptr<ppcapi::HostPool> shard_pool;
+  // Sharded plan step: this handle evaluates shard `shard_rank` of
+  // `shard_world` of every round's candidates and exchanges with the other
+  // shards through `xchg` (NCCL, or host memory for shards sharing a
+  // device); set by pp_comm_init (one process per GPU) or at construction
+  // for PlannerConfig::devices (one thread per shard). The exchange is used
+  // by plan steps only (xchg_active), never by pp_evaluate's explicit ranges.
+  std::unique_ptr<ppcapi::Exchange> xchg;
+  std::shared_ptr<ppcapi::ThreadGroup> thread_group;  // primary: host exchange of its shards
+  int shard_rank = 0, shard_world = 1;
+  bool xchg_active = false;
   std::function<void()> pending_upload;
   ppdev::RoundArgs base{};
   int field_smem_bytes = 0;
@@ -396,9 +411,12 @@ void consume_pending_field(pp_handle* h, bool side = false);
 void run_round_launch(pp_handle* h, uint64_t t, int iter, int r0, int rc, const double* center,
                       int64_t c0, int64_t c1, const double* injected, pp_record* out,
                       pp_rollout_stats* per_sample, bool force_fp64 = false);
+// shard_mode: 0 unsharded; 1 sharded, the first window anchored on the
+// packed global winners (in-stream allreduce); 2 sharded, anchors exchanged
+// on the host first (no packed keys: n_candidates > 2^22 or H > 255)
 void certify_round(pp_handle* h, ppdev::RoundArgs& a, uint64_t t, int iter, int r0, int rc,
                    const double* center, int64_t c0, int64_t c1, const double* injected,
-                   pp_record* out, bool fp64, uint32_t n_sel);
+                   pp_record* out, bool fp64, uint32_t n_sel, int shard_mode = 0);
 void run_round(pp_handle* h, uint64_t t, int iter, int r0, int rc, const double* center,
                int64_t c0, int64_t c1, const double* injected, pp_record* out,
                pp_rollout_stats* per_sample);

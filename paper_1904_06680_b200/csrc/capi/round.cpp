@@ -230,9 +230,27 @@ void run_round_launch(pp_handle* h, uint64_t t, int iter, int r0, int rc, const 
   ck(static_cast<cudaError_t>(fp64 ? ppdev::launch_rollout_f64(h->kind, a, h->stream)
                                    : ppdev::launch_rollout_f32(h->kind, a, h->stream)),
      "sampling kernel launch");
+  // sharded plan step: the shards exchange their per-restart winners
+  const bool sharded = h->xchg_active && h->xchg != nullptr;
+  const bool packed = sharded && rerank && injected == nullptr &&
+                      h->cfg.n_candidates <= ppdev::kPackMaxCandidates &&
+                      h->cfg.H <= ppdev::kPackMaxTGoal;
   if (rerank) {
-    // the selection counter was re-armed by the rollout kernel's last CTA
-    ck(static_cast<cudaError_t>(ppdev::launch_select(a, h->stream)), "window select launch");
+    if (packed) {
+      // one min-allreduce of the packed winners in the stream, then every
+      // shard's window is anchored on the global best (keypack.h)
+      a.pkeys = reinterpret_cast<uint64_t*>(dres + kPackOff);
+      ck(static_cast<cudaError_t>(ppdev::launch_pack_keys(a, h->stream)), "pack keys launch");
+      h->xchg->allreduce_min_u64(a.pkeys, 2 * rc, h->stream);
+      a.sel_packed = 1;
+      h->timing.launches += 2;
+    }
+    // the selection counter was re-armed by the rollout kernel's last CTA;
+    // sharded rounds without packed keys select after a host exchange
+    // (certify_round)
+    if (!sharded || packed) {
+      ck(static_cast<cudaError_t>(ppdev::launch_select(a, h->stream)), "window select launch");
+    }
     if (h->pool == nullptr) h->pool = shared_pool().pool.get();
   }
   // one D2H: counters (selection count), work counters, winners and the
@@ -266,7 +284,8 @@ void run_round_launch(pp_handle* h, uint64_t t, int iter, int r0, int rc, const 
   ck(cudaEventElapsedTime(&ms, h->ev0, h->ev1), "event timing");
   if (trace_level() >= 2) std::fprintf(stderr, "[paraplan] round gpu us: %.1f\n", 1e3 * ms);
   h->timing.kernel_ms += ms;
-  h->timing.launches += (shape.refill ? 2 : 1) + (rerank ? 1 : 0) + (keys_only ? 1 : 0) + 1;
+  h->timing.launches += (shape.refill ? 2 : 1) + (rerank && (!sharded || packed) ? 1 : 0) +
+                        (keys_only ? 1 : 0) + 1;
   h->timing.samples += count * rc;
   const char* hres = static_cast<const char*>(h->h_round.p);
   const unsigned long long* ex = reinterpret_cast<const unsigned long long*>(hres + kExecOff);
@@ -286,7 +305,8 @@ void run_round_launch(pp_handle* h, uint64_t t, int iter, int r0, int rc, const 
 
   n_sel = reinterpret_cast<const uint32_t*>(hres)[2];
   const auto c_t0 = std::chrono::steady_clock::now();
-  certify_round(h, a, t, iter, r0, rc, center, c0, c1, injected, out, fp64, n_sel);
+  certify_round(h, a, t, iter, r0, rc, center, c0, c1, injected, out, fp64, n_sel,
+                sharded ? (packed ? 1 : 2) : 0);
   phase("certified");
   h->timing.certify_ms +=
       std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - c_t0).count();
@@ -302,11 +322,32 @@ void run_round_launch(pp_handle* h, uint64_t t, int iter, int r0, int rc, const 
 // unselected candidate's optimistic bound; otherwise the window widens.
 // Windows that overflow, or restarts still uncertified after the last pass,
 // are redone as an FP64 round.
+//
+// Sharded (shard_mode != 0): every shard selects its own candidates against
+// the same bounds, evaluates them, and the shards all-gather their exact
+// per-restart bests after each pass (XBest), so every shard takes the same
+// decision and returns the same winner -- the global exact best, ties to the
+// lowest index as the reference's ordered merge (src/planner.cpp:310-321).
+
+namespace {
+
+// One shard's exact best of a restart in a certification pass.
+struct XBest {
+  int32_t cls, t_goal;  // cls -1: no window member
+  double cost, k1, k2;
+  int64_t cand;       // candidate index within the restart
+  int32_t overflow;   // the shard's window overflowed this pass
+  int32_t _pad;
+};
+
+}  // namespace
+
 void certify_round(pp_handle* h, ppdev::RoundArgs& a, uint64_t t, int iter, int r0, int rc,
                    const double* center, int64_t c0, int64_t c1, const double* injected,
-                   pp_record* out, bool fp64, uint32_t n_sel) {
+                   pp_record* out, bool fp64, uint32_t n_sel, int shard_mode) {
   const int64_t count = c1 - c0;
   const pp_snapshot& snap = *h->snapshot;
+  Exchange* xg = shard_mode != 0 ? h->xchg.get() : nullptr;
   std::vector<double> ctr(h->P, 0.0);
   if (center != nullptr) ctr.assign(center, center + h->P);
   struct Exact {
@@ -370,8 +411,10 @@ void certify_round(pp_handle* h, ppdev::RoundArgs& a, uint64_t t, int iter, int 
   // (collision with field row 0, then the goal box; src/planner.cpp:137-152)
   // do not depend on theta. If they stop the rollout there, every candidate
   // of the round has the same exact key, and each restart's winner is its
-  // lowest index (strict-better scans, :295, :316). The window would hold
-  // the whole round (equal keys), so the round is certified directly.
+  // lowest index (strict-better scans, :295, :316) -- candidate 0 of a
+  // sharded round, whose shard 0 starts there. The window would hold the
+  // whole round (equal keys), so the round is certified directly (the same
+  // decision on every shard, no exchange).
   {
     pp_rollout_stats st{};
     if (host_stops_at_state0(h, snap, &st)) {
@@ -380,7 +423,7 @@ void certify_round(pp_handle* h, ppdev::RoundArgs& a, uint64_t t, int iter, int 
       const double k2 = cls == 2 ? -st.path_length : 0.0;
       for (int r = 0; r < rc; ++r) {
         out[r].cls = cls;
-        out[r].candidate = static_cast<int>(c0);
+        out[r].candidate = xg != nullptr ? 0 : static_cast<int>(c0);
         out[r].k1 = k1;
         out[r].k2 = k2;
       }
@@ -392,29 +435,60 @@ void certify_round(pp_handle* h, ppdev::RoundArgs& a, uint64_t t, int iter, int 
     }
   }
   const double rho = a.sel_rho, alpha = a.sel_alpha;
+  const char* hres = static_cast<const char*>(h->h_round.p);
   std::vector<ppdev::SelBound> bound(rc);
-  // the first window is built around each restart's best unflagged
-  // candidate when the round reports it (keys_only), else its winner
-  const ppdev::Rec* free_recs =
-      a.out_free != nullptr
-          ? reinterpret_cast<const ppdev::Rec*>(static_cast<const char*>(h->h_round.p) + kFreeOff)
-          : nullptr;
-  for (int r = 0; r < rc; ++r) {
-    pp_record o = out[r];
-    if (free_recs != nullptr && free_recs[r].cls >= 0) {
-      o.cls = free_recs[r].cls;
-      o.k1 = free_recs[r].k1;
-      o.k2 = free_recs[r].k2;
+  auto set_bound = [&](int r, int cls, int t_goal, double cost) {
+    bound[r].cls = cls;
+    bound[r].t_goal = cls == 2 ? t_goal : 0;
+    bound[r].thr = cost * (1.0 + rho) + alpha;  // as select_kernel (no contraction)
+  };
+  if (shard_mode == 1) {
+    // the packed global winners the select kernel anchored on (keypack.h)
+    const uint64_t* pk = reinterpret_cast<const uint64_t*>(hres + kPackOff);
+    for (int r = 0; r < rc; ++r) {
+      const uint64_t pf = pk[rc + r];
+      const ppdev::Unpacked u = ppdev::unpack_key(pf != ppdev::kPackEmpty ? pf : pk[r]);
+      set_bound(r, u.cls, u.t_goal, static_cast<double>(u.cost));
     }
-    bound[r].cls = o.cls;
-    bound[r].t_goal = o.cls == 2 ? static_cast<int>(-o.k1) : 0;
-    bound[r].thr = (o.cls == 2 ? -o.k2 : -o.k1) * (1.0 + rho) + alpha;
+  } else {
+    // the first window is built around each restart's best unflagged
+    // candidate when the round reports it (keys_only), else its winner
+    const ppdev::Rec* free_recs =
+        a.out_free != nullptr ? reinterpret_cast<const ppdev::Rec*>(hres + kFreeOff) : nullptr;
+    std::vector<XBest> mine(rc), all;
+    for (int r = 0; r < rc; ++r) {
+      pp_record o = out[r];
+      if (free_recs != nullptr && free_recs[r].cls >= 0) {
+        o.cls = free_recs[r].cls;
+        o.k1 = free_recs[r].k1;
+        o.k2 = free_recs[r].k2;
+        o.candidate = free_recs[r].cand;
+      }
+      mine[r] = XBest{o.cls, o.cls == 2 ? static_cast<int>(-o.k1) : 0,
+                      o.cls == 2 ? -o.k2 : -o.k1, o.k1, o.k2, o.candidate, 0, 0};
+    }
+    if (shard_mode == 2) {  // the global anchors through a host exchange
+      all.resize(static_cast<size_t>(rc) * xg->world);
+      xg->allgather(mine.data(), all.data(), sizeof(XBest) * rc, h->stream);
+      for (int r = 0; r < rc; ++r) {
+        XBest g = all[r];
+        for (int w = 1; w < xg->world; ++w) {
+          const XBest& q = all[static_cast<size_t>(w) * rc + r];
+          if (q.cls < 0) continue;
+          if (g.cls < 0 || key_better({q.cls, q.k1, q.k2}, {g.cls, g.k1, g.k2})) g = q;
+        }
+        mine[r] = g;
+      }
+    }
+    for (int r = 0; r < rc; ++r) set_bound(r, mine[r].cls, mine[r].t_goal, mine[r].cost);
   }
   std::vector<char> certified(rc, 0);
   std::vector<int64_t> list;
+  std::vector<XBest> xmine(rc), xall;
+  bool widened = shard_mode == 2;  // no select ran yet
   constexpr int kPasses = 6;
   for (int pass = 0; pass < kPasses; ++pass) {
-    if (pass > 0) {  // widened select over the uncertified restarts
+    if (pass > 0 || widened) {  // (widened) select over the uncertified restarts
       h->d_bound.reserve(sizeof(ppdev::SelBound) * rc, "window bounds");
       h->h_bound.reserve(sizeof(ppdev::SelBound) * rc, "pinned bounds");
       std::memcpy(h->h_bound.p, bound.data(), sizeof(ppdev::SelBound) * rc);
@@ -430,29 +504,31 @@ void certify_round(pp_handle* h, ppdev::RoundArgs& a, uint64_t t, int iter, int 
       ck(cudaStreamSynchronize(h->stream), "window select");
       h->timing.launches += 1;
       n_sel = static_cast<const uint32_t*>(h->h_round.p)[2];
+      widened = false;
     }
-    if (n_sel > static_cast<uint32_t>(kSelCap)) {
-      if (trace_on()) {
-        std::fprintf(stderr, "[paraplan] t=%llu iter=%d pass=%d selected=%u: window overflow\n",
-                     static_cast<unsigned long long>(t), iter, pass, n_sel);
-      }
-      break;
+    const bool overflow = n_sel > static_cast<uint32_t>(kSelCap);
+    if (overflow && trace_on()) {
+      std::fprintf(stderr, "[paraplan] t=%llu iter=%d pass=%d selected=%u: window overflow\n",
+                   static_cast<unsigned long long>(t), iter, pass, n_sel);
     }
-    if (n_sel > static_cast<uint32_t>(kSelFirst)) {
-      ck(cudaMemcpy(reinterpret_cast<int64_t*>(static_cast<char*>(h->h_round.p) + kSelOff) + kSelFirst,
-                    a.sel_list + kSelFirst, sizeof(int64_t) * (n_sel - kSelFirst),
-                    cudaMemcpyDeviceToHost),
-         "selection D2H");
-    }
-    const int64_t* sl =
-        reinterpret_cast<const int64_t*>(static_cast<const char*>(h->h_round.p) + kSelOff);
     list.clear();
-    for (uint32_t i = 0; i < n_sel; ++i) {
-      const auto it = std::lower_bound(known.begin(), known.end(), sl[i], by_index);
-      if (it == known.end() || it->first != sl[i]) list.push_back(sl[i]);
+    if (!overflow) {
+      if (n_sel > static_cast<uint32_t>(kSelFirst)) {
+        ck(cudaMemcpy(reinterpret_cast<int64_t*>(static_cast<char*>(h->h_round.p) + kSelOff) +
+                          kSelFirst,
+                      a.sel_list + kSelFirst, sizeof(int64_t) * (n_sel - kSelFirst),
+                      cudaMemcpyDeviceToHost),
+           "selection D2H");
+      }
+      const int64_t* sl =
+          reinterpret_cast<const int64_t*>(static_cast<const char*>(h->h_round.p) + kSelOff);
+      for (uint32_t i = 0; i < n_sel; ++i) {
+        const auto it = std::lower_bound(known.begin(), known.end(), sl[i], by_index);
+        if (it == known.end() || it->first != sl[i]) list.push_back(sl[i]);
+      }
+      std::sort(list.begin(), list.end());
+      list.erase(std::unique(list.begin(), list.end()), list.end());
     }
-    std::sort(list.begin(), list.end());
-    list.erase(std::unique(list.begin(), list.end()), list.end());
     h->timing.refined += static_cast<int32_t>(list.size());
     std::vector<Exact> got(list.size());
     if (list.size() <= static_cast<size_t>(host_max())) {
@@ -518,47 +594,79 @@ void certify_round(pp_handle* h, ppdev::RoundArgs& a, uint64_t t, int iter, int 
       known.swap(merged);
     }
 
-    // certify or widen each uncertified restart
-    bool all = true;
+    // each uncertified restart's exact best (this shard's, then the global)
+    std::vector<const Exact*> local(rc, nullptr);
+    std::vector<int64_t> local_win(rc, -1);
     for (int r = 0; r < rc; ++r) {
       if (certified[r]) continue;
-      const ppdev::SelBound& bd = bound[r];
-      int64_t win = -1;
-      const Exact* e = nullptr;
       // increasing index order: among equal keys the first (lowest) wins
       const auto hi = std::lower_bound(known.begin(), known.end(), (r + 1) * count, by_index);
       for (auto it = std::lower_bound(known.begin(), known.end(), r * count, by_index); it != hi;
            ++it) {
         const Exact& q = it->second;
-        if (e == nullptr || key_better({q.cls, q.k1, q.k2}, {e->cls, e->k1, e->k2})) {
-          e = &q;
-          win = it->first;
+        if (local[r] == nullptr ||
+            key_better({q.cls, q.k1, q.k2}, {local[r]->cls, local[r]->k1, local[r]->k2})) {
+          local[r] = &q;
+          local_win[r] = it->first;
         }
       }
+    }
+    for (int r = 0; r < rc; ++r) {
+      const Exact* e = local[r];
+      xmine[r] = e == nullptr
+                     ? XBest{-1, 0, 0.0, 0.0, 0.0, -1, overflow ? 1 : 0, 0}
+                     : XBest{e->cls, e->t_goal, e->cost, e->k1, e->k2,
+                             c0 + (local_win[r] - r * count), overflow ? 1 : 0, 0};
+    }
+    bool any_overflow = overflow;
+    std::vector<XBest> gbest(xmine);
+    if (xg != nullptr) {  // the same decision on every shard
+      xall.resize(static_cast<size_t>(rc) * xg->world);
+      xg->allgather(xmine.data(), xall.data(), sizeof(XBest) * rc, h->stream);
+      for (int r = 0; r < rc; ++r) {
+        XBest g{-1, 0, 0.0, 0.0, 0.0, -1, 0, 0};
+        for (int w = 0; w < xg->world; ++w) {  // shard order = index order
+          const XBest& q = xall[static_cast<size_t>(w) * rc + r];
+          any_overflow = any_overflow || q.overflow != 0;
+          if (q.cls < 0) continue;
+          if (g.cls < 0 || key_better({q.cls, q.k1, q.k2}, {g.cls, g.k1, g.k2})) g = q;
+        }
+        gbest[r] = g;
+      }
+    }
+    if (any_overflow) break;
+
+    // certify or widen each uncertified restart
+    bool all = true;
+    for (int r = 0; r < rc; ++r) {
+      if (certified[r]) continue;
+      const ppdev::SelBound& bd = bound[r];
+      const XBest& e = gbest[r];
       const double slack = 0.5 * (rho * bd.thr + alpha);
       bool ok = false;
-      if (e != nullptr) {
-        if (e->cls > bd.cls) {
+      if (e.cls >= 0) {
+        if (e.cls > bd.cls) {
           ok = true;  // only a flagged (always selected) candidate can rise a class
-        } else if (e->cls == bd.cls) {
-          ok = (bd.cls == 2 && e->t_goal < bd.t_goal) ||
-               ((bd.cls != 2 || e->t_goal == bd.t_goal) && e->cost <= bd.thr - slack);
+        } else if (e.cls == bd.cls) {
+          ok = (bd.cls == 2 && e.t_goal < bd.t_goal) ||
+               ((bd.cls != 2 || e.t_goal == bd.t_goal) && e.cost <= bd.thr - slack);
         }
       }
       if (ok) {
         certified[r] = 1;
-        out[r].cls = e->cls;
-        out[r].candidate = static_cast<int>(c0 + (win - r * count));
-        out[r].k1 = e->k1;
-        out[r].k2 = e->k2;
-        if (e->slot >= 0) {
-          pp_handle::WinnerRollout w;
+        out[r].cls = e.cls;
+        out[r].candidate = static_cast<int>(e.cand);
+        out[r].k1 = e.k1;
+        out[r].k2 = e.k2;
+        const Exact* le = local[r];
+        if (le != nullptr && le->slot >= 0 && c0 + (local_win[r] - r * count) == e.cand) {
+          pp_handle::WinnerRollout w;  // the winner is this shard's: keep its rollout
           w.restart = out[r].restart;
           w.iter = out[r].iter;
           w.candidate = out[r].candidate;
-          w.stats = h->cert_stats[e->slot];
-          w.len = h->cert_len[e->slot];
-          const double* tr = h->cert_traj.data() + e->slot * stride;
+          w.stats = h->cert_stats[le->slot];
+          w.len = h->cert_len[le->slot];
+          const double* tr = h->cert_traj.data() + le->slot * stride;
           w.traj.assign(tr, tr + static_cast<size_t>(std::min<int32_t>(w.len, h->cfg.H + 1)) * 4);
           h->winner_rollouts.push_back(std::move(w));
         }
@@ -570,12 +678,11 @@ void certify_round(pp_handle* h, ppdev::RoundArgs& a, uint64_t t, int iter, int 
         std::fprintf(stderr,
                      "[paraplan]   restart %d open: window cls %d t_goal %d thr %.9g slack %.3g; "
                      "exact best cls %d t_goal %d cost %.9g\n",
-                     r0 + r, bd.cls, bd.t_goal, bd.thr, slack, e ? e->cls : -9,
-                     e ? e->t_goal : -9, e ? e->cost : 0.0);
+                     r0 + r, bd.cls, bd.t_goal, bd.thr, slack, e.cls, e.t_goal, e.cost);
       }
-      const bool same = e != nullptr && e->cls == bd.cls && (bd.cls != 2 || e->t_goal == bd.t_goal);
-      const double widened = bd.thr * 1.25 + alpha;
-      bound[r].thr = same ? std::max(e->cost * (1.0 + rho) + alpha, widened) : widened;
+      const bool same = e.cls >= 0 && e.cls == bd.cls && (bd.cls != 2 || e.t_goal == bd.t_goal);
+      const double wider = bd.thr * 1.25 + alpha;
+      bound[r].thr = same ? std::max(e.cost * (1.0 + rho) + alpha, wider) : wider;
     }
     if (trace_on()) {
       std::fprintf(stderr, "[paraplan] t=%llu iter=%d pass=%d selected=%u new=%zu certified=%s\n",
@@ -584,7 +691,7 @@ void certify_round(pp_handle* h, ppdev::RoundArgs& a, uint64_t t, int iter, int 
     }
     if (all) return;
   }
-  // overflowed or not certified: redo the round in FP64
+  // overflowed or not certified (on any shard): redo the round in FP64
   if (trace_on()) {
     std::fprintf(stderr, "[paraplan] t=%llu iter=%d: FP64 fallback round\n",
                  static_cast<unsigned long long>(t), iter);

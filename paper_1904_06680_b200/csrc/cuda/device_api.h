@@ -5,6 +5,8 @@
 
 #include <cstdint>
 
+#include "keypack.h"
+
 namespace ppdev {
 
 constexpr int kMaxLayers = 16;
@@ -158,7 +160,13 @@ struct RoundArgs {
   const SelBound* sel_bound;   // null: first pass (window around a.out)
   double dmarg32;              // FP32 marginal threshold (host side, copied into kf)
   int32_t sms;                 // multiprocessors of the device (launch sizing)
-  int32_t _pad_sms;
+  // sharded plan step (one shard of the candidates per GPU): the packed
+  // per-restart winners [best x restart_count][best unflagged x
+  // restart_count] (keypack.h), reduced across the shards in place by the
+  // exchange; select_kernel then anchors each restart's first window on the
+  // GLOBAL best unflagged candidate (sel_packed != 0)
+  int32_t sel_packed;
+  uint64_t* pkeys;
 };
 
 // Architecture dispatch of the specialised kernels.
@@ -209,6 +217,9 @@ int launch_draw_f64(const RoundArgs& a, void* out, void* stream);
 // Near-tie window after a round: counters[2] receives the number of selected
 // candidates, sel_list their flat indices.
 int launch_select(const RoundArgs& a, void* stream);
+// Packed keys of the round's per-restart winners into a.pkeys (a dependent
+// launch after the rollout / per-restart reduction).
+int launch_pack_keys(const RoundArgs& a, void* stream);
 // Copy `bytes` (a multiple of 16) of device memory into pinned host memory
 // with SM stores, after the previous kernel on `stream` (dependent launch).
 int launch_copy_out(const void* src, void* host_dst, size_t bytes, void* stream);

@@ -406,6 +406,12 @@ static __global__ void __launch_bounds__(256) select_kernel(const RoundArgs a) {
     SelBound bd;
     if (a.sel_bound != nullptr) {  // widened window of a later pass
       bd = a.sel_bound[r];
+    } else if (a.sel_packed) {  // sharded: around the GLOBAL best unflagged candidate
+      const uint64_t pf = a.pkeys[a.restart_count + r];
+      const Unpacked u = unpack_key(pf != kPackEmpty ? pf : a.pkeys[r]);
+      bd.cls = u.cls;
+      bd.t_goal = u.cls == 2 ? u.t_goal : 0;
+      bd.thr = static_cast<double>(u.cost) * (1.0 + a.sel_rho) + a.sel_alpha;
     } else {  // first pass: around the round winner (its best unflagged candidate)
       const Rec b = (a.out_free != nullptr && a.out_free[r].cls >= 0) ? a.out_free[r] : a.out[r];
       bd.cls = b.cls;
@@ -428,6 +434,21 @@ static __global__ void __launch_bounds__(256) select_kernel(const RoundArgs a) {
     if (take) {
       const unsigned i = atomicAdd(&a.counters[2], 1u);
       if (i < static_cast<unsigned>(a.sel_cap)) a.sel_list[i] = s;
+    }
+  }
+}
+
+// Packed keys of the per-restart winners (keypack.h): [best][best unflagged]
+// per restart, for the cross-shard min-reduction. FP64 costs round up.
+static __global__ void __launch_bounds__(128) pack_keys_kernel(const RoundArgs a) {
+  wait_prior_grid();  // the round's winners
+  for (int r = threadIdx.x; r < a.restart_count; r += blockDim.x) {
+    for (int which = 0; which < 2; ++which) {
+      const Rec b = which == 0 ? a.out[r] : (a.out_free != nullptr ? a.out_free[r] : a.out[r]);
+      const double cost = b.cls == 2 ? -b.k2 : -b.k1;
+      a.pkeys[which * a.restart_count + r] =
+          pack_key(b.cls, b.cls == 2 ? static_cast<int>(-b.k1) : 0, __double2float_ru(cost),
+                   static_cast<uint32_t>(b.cand));
     }
   }
 }

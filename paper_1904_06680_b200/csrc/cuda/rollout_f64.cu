@@ -47,6 +47,11 @@ namespace ppdev {
 // The re-ranking kernels live in the --fmad=false translation unit.
 int launch_select(const RoundArgs& a, void* stream) { return launch_select_impl(a, stream); }
 
+int launch_pack_keys(const RoundArgs& a, void* stream) {
+  return static_cast<int>(
+      launch_dependent(pack_keys_kernel, 1, 128, 0, static_cast<cudaStream_t>(stream), true, a));
+}
+
 // The round's result block, stored straight into pinned host memory by the
 // SMs (a dependent launch after the last round kernel). A cudaMemcpyAsync of
 // the same ~7 KB spent 7-15 us of GPU time in the copy engine (measured on

@@ -1,16 +1,23 @@
-"""Multi-GPU plan_step: one process per GPU, candidates sharded, one exchange.
+"""Multi-GPU plan_step: one process per GPU, candidates sharded.
 
 The flat candidate index space of every restart is split into contiguous,
-increasing ranges, rank r owning [n*r/W, n*(r+1)/W). Each rank runs the fused
-kernel on its range (pp_evaluate) and produces one winner record per restart.
-The only exchange is an all-gather of those records (6 doubles each,
-torch.distributed over NCCL on GPUs, gloo in the CPU tests); every rank then
-merges them in rank order with the strict-better rule, which reproduces the
-reference's ordered merge of contiguous worker ranges
-(/root/reference/proj/src/planner.cpp:280-281, 310-321) -- so the result is
-bit-identical for any world size. The incumbent schedule, the theta
-regeneration of the winner and the FP64 epilogue then run identically on all
-ranks (src/planner.cpp:269-350), so no broadcast is needed.
+increasing ranges, rank r owning [n*r/W, n*(r+1)/W)
+(/root/reference/proj/src/planner.cpp:280-281 splits worker ranges the same
+way).
+
+GPU ranks (`CommPlanner`): the planner itself is sharded in C++
+(pp_comm_init, csrc/capi/round.cpp + exchange.cpp). Each rank's round runs on
+its own GPU; one ncclAllReduce(ncclMin, uint64) of packed (class, t_goal,
+FP32 cost, index) keys in the stream anchors every rank's near-tie window on
+the global winner, the ranks certify their own window members in the
+reference's FP64 arithmetic and all-gather the exact per-restart bests, so
+every rank returns the same plan: the reference's ordered merge
+(src/planner.cpp:310-321). Python only shares the NCCL unique id.
+
+`ShardedPlanner` is the same partition and merge written in Python over any
+per-shard evaluator and any all-gather: the CPU tests run it over gloo with
+the C oracle as the shard evaluator (tests/test_distributed.py), and it
+checks the packed-key reduction against the ordered merge.
 """
 from __future__ import annotations
 
@@ -78,14 +85,20 @@ class ShardedPlanner:
 
     @classmethod
     def on_device(cls, model: abi.Model, rank: int, world: int, group=None):
-        """GPU ranks: DevicePlanner on this rank's device, NCCL all-gather."""
+        """GPU ranks, one GPU each: the C++ sharded planner over NCCL."""
+        return CommPlanner(model, rank, world, group)
+
+    @classmethod
+    def on_shared_device(cls, model: abi.Model, rank: int, world: int, group=None):
+        """Ranks that share a GPU (NCCL refuses duplicate devices; a 1-GPU
+        box): each rank's shard runs on the device through pp_evaluate and
+        the winner records are all-gathered over the group's backend."""
         import torch
         import torch.distributed as dist
 
         from .capi import DevicePlanner
 
         dp = DevicePlanner(model)
-
         last = {"snap": None}
 
         def evaluate(snap, t, it, r0, rc, center, c0, c1):
@@ -165,3 +178,31 @@ class ShardedPlanner:
         else:
             action = (snap.actuator_delta / m.to_c().vehicle.delta_max, -1.0)
         return PlanResult(best_theta, action, st, traj, success, evaluated, best)
+
+
+class CommPlanner:
+    """One rank of a sharded planner: a DevicePlanner joined to a `world`-rank
+    NCCL communicator (the unique id travels over torch.distributed). Every
+    rank calls plan_step with the same snapshot and gets the same plan."""
+
+    def __init__(self, model: abi.Model, rank: int, world: int, group=None):
+        import torch.distributed as dist
+
+        from .capi import DevicePlanner, comm_unique_id
+
+        self.model = model
+        self.rank, self.world = rank, world
+        self.device_planner = DevicePlanner(model)
+        uid = [comm_unique_id() if rank == 0 else None]
+        if world > 1:
+            dist.broadcast_object_list(uid, src=0, group=group)
+        self.device_planner.join_communicator(uid[0], world, rank)
+
+    def plan_step(self, snap: abi.Snapshot, t: int) -> PlanResult:
+        o, theta, traj = self.device_planner.plan_step(snap, t)
+        w = o.winner
+        return PlanResult(theta, (o.action_a0, o.action_a1), o.predicted, traj, bool(o.success),
+                          o.evaluated, (w.cls, w.candidate, w.restart, w.iter, w.k1, w.k2))
+
+    def exchange(self) -> str:
+        return self.device_planner.exchange()

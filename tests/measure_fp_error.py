@@ -129,12 +129,29 @@ def configs(quick: bool):
                                           n_candidates=1 << (14 if quick else 17)), s, 0
 
 
+def sweep_configs():
+    """Error envelope against the horizon: scenes whose winner is of class 0/1
+    (terminal cost) and class 2, H in {30, 60, 100, 150, 200}."""
+    m = workloads.c2_mission()
+    for H in (30, 60, 100, 150, 200):
+        snap = workloads.snapshot_from_mission(m, m.initial_state, workloads.C2_T, H, 20)
+        yield f"C2 scene H={H}", abi.Model(H=H, n_restarts=1, n_candidates=1 << 16), snap, 5
+        for scene in ("exp3_explicit", "exp2"):
+            s = Ref.builtin_snapshot(scene, 0, H)
+            yield f"{scene} H={H}", abi.Model(H=H, n_restarts=1, n_candidates=1 << 15), s, 0
+        for i in range(6):
+            s = Ref.acceptance9_snapshot(i, H)
+            yield f"acc9[{i}] H={H}", abi.Model(H=H, n_restarts=1, n_candidates=1 << 15,
+                                                master_seed=77), s, i
+
+
 def main():
     out_path = Path(sys.argv[1]) if len(sys.argv) > 1 and not sys.argv[1].startswith("-") \
         else ROOT / "gpurun_out" / "r2_error_model.json"
     quick = "--quick" in sys.argv
     res = []
-    for name, model, snap, t in configs(quick):
+    gen = sweep_configs() if "--sweep" in sys.argv else configs(quick)
+    for name, model, snap, t in gen:
         r = measure(name, model, snap, t)
         print(json.dumps(r), flush=True)
         res.append(r)

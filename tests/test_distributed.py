@@ -98,3 +98,82 @@ def test_shard_ranges_partition_in_order():
             rs = [shard_range(n, r, w) for r in range(w)]
             assert rs[0][0] == 0 and rs[-1][1] == n
             assert all(a[1] == b[0] for a, b in zip(rs, rs[1:]))
+
+
+# ---- the packed-key winner collective (csrc/cuda/keypack.h) -------------
+
+def _ref_order_key(cls, t_goal, cost, idx):
+    """The reference's order (better(), src/planner.cpp:40-44; ties to the
+    lowest index) as a Python sort key: smaller is better."""
+    return (-cls, t_goal if cls == 2 else 0, cost, idx)
+
+
+def test_packed_key_order_is_the_reference_order():
+    from paper_1904_06680_b200 import capi
+    rng = np.random.default_rng(5)
+    keys = []
+    for _ in range(4000):
+        cls = int(rng.integers(0, 3))
+        tg = int(rng.integers(0, 256)) if cls == 2 else 0
+        # float costs, with deliberate exact ties
+        cost = float(np.float32(rng.choice([0.5, 1.25, rng.uniform(0, 50)])))
+        idx = int(rng.integers(0, 1 << 22))
+        keys.append((cls, tg, cost, idx))
+    packed = [capi.pack_key(*k) for k in keys]
+    by_pack = [keys[i] for i in np.argsort(np.array(packed, dtype=np.uint64), kind="stable")]
+    by_ref = sorted(keys, key=lambda k: _ref_order_key(*k))
+    assert by_pack == by_ref
+    for k, p in zip(keys, packed):
+        assert capi.unpack_key(p) == k
+    assert capi.pack_key(-1, 0, 0.0, 0) == (1 << 64) - 1
+
+
+def _key_worker(rank, world, port_no, results):
+    """Each rank evaluates its contiguous shard with the oracle, packs its
+    best, and the ranks min-reduce over gloo: the reduced key must be the
+    single-process winner (the C++ planner does the same with ncclMin)."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port_no)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import torch
+
+    from paper_1904_06680_b200 import capi
+    for name, t_snap, cfg, t in CASES:
+        model = abi.Model(**cfg)
+        snap = Ref.builtin_snapshot(name, t_snap, model.H)
+        port = Port(model)
+        n = model.n_candidates
+        c0, c1 = shard_range(n, rank, world)
+        st = port.eval_candidates(snap, t, 0, 0, np.zeros(model.param_count()), c0, c1)
+        best = (1 << 64) - 1
+        for i, s in enumerate(st):
+            cls = 0 if s["collided"] else (2 if s["reached"] else 1)
+            cost = s["path_length"] if cls == 2 else s["terminal_cost"]
+            best = min(best, capi.pack_key(cls, int(s["t_goal"]), float(np.float32(cost)), c0 + i))
+        # gloo reduces int64: flip the sign bit so the signed order is the
+        # unsigned one
+        x = torch.tensor([best ^ (1 << 63)], dtype=torch.uint64).view(torch.int64)
+        dist.all_reduce(x, op=dist.ReduceOp.MIN)
+        results[(rank, name)] = int(x.view(torch.uint64).item()) ^ (1 << 63)
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_packed_winner_allreduce_over_ranks(world):
+    from paper_1904_06680_b200 import capi
+    mgr = mp.get_context("spawn").Manager()
+    results = mgr.dict()
+    mp.spawn(_key_worker, args=(world, _free_port(), results), nprocs=world, join=True)
+    for name, t_snap, cfg, t in CASES:
+        model = abi.Model(**cfg)
+        snap = Ref.builtin_snapshot(name, t_snap, model.H)
+        st = Port(model).eval_candidates(snap, t, 0, 0, np.zeros(model.param_count()), 0,
+                                         model.n_candidates)
+        keys = []
+        for i, s in enumerate(st):
+            cls = 0 if s["collided"] else (2 if s["reached"] else 1)
+            cost = s["path_length"] if cls == 2 else s["terminal_cost"]
+            keys.append(capi.pack_key(cls, int(s["t_goal"]), float(np.float32(cost)), i))
+        want = min(keys)
+        for rank in range(world):
+            assert results[(rank, name)] == want, (name, rank)

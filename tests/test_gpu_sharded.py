@@ -28,7 +28,7 @@ def _worker(rank, world, port, out):
     from paper_1904_06680_b200.distributed import ShardedPlanner
     w = workloads.c2(samples=1 << 10)
     for k, cfg in enumerate(CFGS):
-        sp = ShardedPlanner.on_device(abi.Model(**cfg), rank, world)
+        sp = ShardedPlanner.on_shared_device(abi.Model(**cfg), rank, world)
         r = sp.plan_step(w.snapshot, w.t)
         out[(rank, k)] = (r.best_theta.tobytes(), r.trajectory.tobytes(), r.action, r.evaluated,
                           r.winner[:2])
@@ -107,3 +107,51 @@ def test_in_process_shards_reject_a_missing_device():
     dp = capi.DevicePlanner(abi.Model(H=30, n_restarts=1, n_candidates=1024, devices=[0, 0]))
     o, _, _ = dp.plan_step(w.snapshot, w.t)
     assert o.evaluated == 1024
+
+
+@pytest.mark.parametrize("cfg", CFGS + [dict(H=30, n_restarts=15, n_candidates=20480),
+                                        dict(H=200, n_restarts=1, n_candidates=1 << 15)])
+def test_one_rank_nccl_communicator_equals_unsharded(cfg):
+    """pp_comm_init on a one-rank NCCL communicator runs the whole sharded
+    path on one GPU: packed winner keys, the in-stream
+    ncclAllReduce(ncclMin, uint64), the globally anchored window, the
+    ncclAllGather of exact bests -- and returns the unsharded plan."""
+    w = workloads.c2(samples=1 << 10)
+    m = workloads.c2_mission()
+    snap = w.snapshot if cfg["H"] == 30 else workloads.snapshot_from_mission(
+        m, m.initial_state, workloads.C2_T, cfg["H"], 20)
+    one = capi.DevicePlanner(abi.Model(**cfg))
+    comm = capi.DevicePlanner(abi.Model(**cfg))
+    comm.join_communicator(capi.comm_unique_id(), 1, 0)
+    assert comm.exchange() == "nccl" and one.exchange() == "none"
+    o1, th1, tr1 = one.plan_step(snap, w.t)
+    o2, th2, tr2 = comm.plan_step(snap, w.t)
+    assert np.array_equal(th1, th2) and np.array_equal(tr1, tr2)
+    assert (o1.winner.restart, o1.winner.candidate, o1.evaluated) == \
+        (o2.winner.restart, o2.winner.candidate, o2.evaluated)
+    # + the pack kernel and the NCCL kernel per round
+    assert comm.timing().launches > one.timing().launches
+    comm.close()
+    one.close()
+
+
+def test_in_process_shards_use_host_exchange_on_one_gpu():
+    many = capi.DevicePlanner(abi.Model(H=30, n_restarts=1, n_candidates=4096, devices=[0, 0]))
+    assert many.exchange() == "host"
+    many.close()
+
+
+def test_sharded_state0_stop_returns_candidate_zero():
+    """Every rollout stops at state 0 (obstacle in the chassis): each shard
+    certifies directly, and the winner is global candidate 0 (shard 0)."""
+    field = np.zeros((31, 1, 2))
+    snap = abi.Snapshot(ev=(0.0, 0.0, 0.0, 5.0), actuator_delta=0.2,
+                        prev_action=(0.0, 0.32142857142857145), goal=(20.0, 0.0, 0.0, 5.0),
+                        field=field)
+    cfg = dict(H=30, n_restarts=2, n_candidates=6000)
+    one = capi.DevicePlanner(abi.Model(**cfg))
+    many = capi.DevicePlanner(abi.Model(**cfg, devices=[0, 0, 0]))
+    o1, th1, _ = one.plan_step(snap, 0)
+    o2, th2, _ = many.plan_step(snap, 0)
+    assert o1.winner.candidate == o2.winner.candidate == 0
+    assert np.array_equal(th1, th2) and o2.action_a1 == -1.0
