@@ -193,6 +193,9 @@ typedef struct pp_timing {
   double certify_ms;       /* host time of the certified re-ranking (wall) */
   double rollout_ms;       /* device span of the rollout kernel alone (%globaltimer,
                               first CTA start to last CTA end) */
+  int32_t fp64_rounds;     /* FP32 rounds redone in FP64 (outside the FP32 error
+                              envelope, or not certified) */
+  int32_t _pad;
 } pp_timing;
 
 typedef struct pp_handle pp_handle;

@@ -91,7 +91,8 @@ class pp_timing(C.Structure):
                 ("checked_states", C.c_int64), ("samples", C.c_int64),
                 ("launches", C.c_int32), ("refined", C.c_int32),
                 ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64),
-                ("certify_ms", C.c_double), ("rollout_ms", C.c_double)]
+                ("certify_ms", C.c_double), ("rollout_ms", C.c_double),
+                ("fp64_rounds", C.c_int32), ("_pad", C.c_int32)]
 
 
 # numpy view of pp_rollout_stats arrays (same layout, 48 bytes)

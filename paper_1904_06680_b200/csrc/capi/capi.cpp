@@ -471,6 +471,7 @@ void gather_shard_timing(pp_handle* h) {
     h->timing.samples += q.samples;
     h->timing.launches += q.launches;
     h->timing.refined += std::max(q.refined, 0);
+    h->timing.fp64_rounds = std::max(h->timing.fp64_rounds, q.fp64_rounds);
     h->timing.h2d_bytes += q.h2d_bytes;
     h->timing.d2h_bytes += q.d2h_bytes;
     g->timing = pp_timing{};

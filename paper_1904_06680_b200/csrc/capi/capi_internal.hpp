@@ -255,11 +255,12 @@ inline bool key_better(const Key& a, const Key& b) {  // src/planner.cpp:40-44
   return a.k2 > b.k2;
 }
 
-constexpr int kSelCap = 1 << 16;    // near-tie candidates re-ranked per launch
-constexpr int kSelFirst = 512;      // copied back with the round result
+constexpr int kSelCap = 1 << 16;    // initial selection capacity per launch (grows)
+constexpr int kSelMax = 1 << 24;    // largest selection (beyond it: the FP64 round)
+using ppdev::kSelFirst;             // copied back with the round result
 // Round block (device, one allocation; its head is copied back in ONE D2H):
 // [counters u32 x 16][exec u64 x 4 + pad][Rec x kMaxRestartsPerLaunch]
-// [unflagged Rec x kMaxRestartsPerLaunch][selected indices int64 x kSelCap]
+// [unflagged Rec x kMaxRestartsPerLaunch][packed keys][selected indices int64 x kSelFirst]
 constexpr size_t kExecOff = 64;
 constexpr size_t kRecOff = 128;
 // [Rec x kMaxRestartsPerLaunch] best unflagged per restart (keys_only rounds)
@@ -270,7 +271,7 @@ constexpr size_t kPackOff =
     (kFreeOff + sizeof(ppdev::Rec) * ppdev::kMaxRestartsPerLaunch + 63) / 64 * 64;
 constexpr size_t kSelOff =
     (kPackOff + sizeof(uint64_t) * 2 * ppdev::kMaxRestartsPerLaunch + 63) / 64 * 64;
-constexpr size_t kRoundBytes = kSelOff + sizeof(int64_t) * kSelCap;
+constexpr size_t kRoundBytes = kSelOff + sizeof(int64_t) * kSelFirst;
 // refine_kernel: two CTAs of 128 threads per SM
 inline int refine_grid(int sms) { return sms * 2; }
 
@@ -334,7 +335,8 @@ struct pp_handle {
   cudaEvent_t ev_field = nullptr;
   bool field_via_side = false, field_event = false;
   ppcapi::DevBuf d_field, d_params, d_round, d_tiles, d_samples, d_scratch, d_injected, d_theta, d_skeys,
-      d_sel, d_bound, d_movers, d_bin;
+      d_sel, d_bound, d_movers, d_bin, d_selmore, d_reflist;
+  int sel_cap = 1 << 16;  // selection capacity of this handle (kSelCap, grown on overflow)
   ppcapi::HostBuf h_field, h_params, h_round, h_bound, h_movers;
 
   // near-tie re-ranking (PlannerConfig::refine): needs the host snapshot

@@ -25,7 +25,20 @@ uint64_t key_prefix(uint64_t seed, uint64_t t, uint64_t r, uint64_t i) {
   return hh;
 }
 
-constexpr int ppdev_warps() { return 4; }  // warps per CTA (rollout.cuh kBlock / 32)
+constexpr int ppdev_warps() { return 4; }
+
+// Selection buffers of capacity `cap`: the indices beyond the round block's
+// first kSelFirst, the refine kernel's input list and its FP64 keys.
+void grow_selection(pp_handle* h, ppdev::RoundArgs& a, int cap) {
+  h->sel_cap = std::max(h->sel_cap, cap);
+  h->d_selmore.reserve(sizeof(int64_t) * (h->sel_cap - kSelFirst), "selection");
+  h->d_reflist.reserve(sizeof(int64_t) * h->sel_cap, "refine list");
+  h->d_sel.reserve(sizeof(ppdev::SelRec) * h->sel_cap, "refine keys");
+  a.sel_more = static_cast<int64_t*>(h->d_selmore.p);
+  a.ref_list = static_cast<const int64_t*>(h->d_reflist.p);
+  a.sel_out = static_cast<ppdev::SelRec*>(h->d_sel.p);
+  a.sel_cap = h->sel_cap;
+}  // warps per CTA (rollout.cuh kBlock / 32)
 
 // Windows up to this size are re-evaluated on the host pool (exact FP64
 // rollouts, 16 workers); wider ones get the FP64 device kernel first.
@@ -36,6 +49,27 @@ int host_max() {
   }();
   return v;
 }
+
+// The certification's error model (measured: profiles/r2_error_model*.json,
+// tests/measure_fp_error.py). The device rollout's relative cost
+// error against the reference's own FP64 arithmetic, at the exact winner:
+//   FP32, class 2 (reached; cost = path length), any H:   <= 2.1e-5
+//   FP32, class 0/1 (cost = terminal cost), H <= 30:      <= 1.4e-6
+//   FP32, class 0/1, H >= 60:  up to 2.2e-2 (H 60) ... 0.5 (H 200): chaotic
+//                              amplification through saturated steering
+//   FP64 (device libm, no contraction), any H, class:     <= 5.1e-10
+// So an FP32 round is certified with rho = 1e-3 only where that envelope
+// holds with a wide margin: every class up to H = fp32_max_h() (40), class 2
+// beyond. A longer round whose anchor is of class 0/1 is redone in FP64, and
+// FP64 rounds use rho64(H).
+int fp32_max_h() {
+  static const int v = [] {
+    const char* e = std::getenv("PARAPLAN_FP32_MAX_H");
+    return e != nullptr ? std::atoi(e) : 40;
+  }();
+  return v;
+}
+double rho64(int H) { return H <= 60 ? 1e-9 : 1e-6; }
 
 // Occupancy of the rollout kernel for (precision, staged field size, grid
 // mode), queried once per handle.
@@ -159,12 +193,10 @@ void run_round_launch(pp_handle* h, uint64_t t, int iter, int r0, int rc, const 
     a.skey32 = fp64 ? 0 : 1;
   }
   if (rerank) {
-    h->d_sel.reserve(kSelCap * sizeof(ppdev::SelRec), "selection");
-    a.sel_out = static_cast<ppdev::SelRec*>(h->d_sel.p);
+    grow_selection(h, a, h->sel_cap);
     a.sel_list = reinterpret_cast<int64_t*>(dres + kSelOff);
-    a.sel_cap = kSelCap;
     a.refine_grid = refine_grid(h->sms);
-    a.sel_rho = fp64 ? 1e-11 : h->sel_rho;
+    a.sel_rho = fp64 ? rho64(h->cfg.H) : h->sel_rho;
     a.sel_alpha = fp64 ? 1e-13 : 1e-6;
   }
 
@@ -482,20 +514,37 @@ void certify_round(pp_handle* h, ppdev::RoundArgs& a, uint64_t t, int iter, int 
     }
     for (int r = 0; r < rc; ++r) set_bound(r, mine[r].cls, mine[r].t_goal, mine[r].cost);
   }
+  // outside the FP32 envelope (class 0/1 anchors beyond fp32_max_h): the
+  // round is redone in FP64 (every shard decides alike: global anchors)
+  if (!fp64 && h->cfg.H > fp32_max_h()) {
+    bool terminal = false;
+    for (int r = 0; r < rc; ++r) terminal = terminal || (bound[r].cls >= 0 && bound[r].cls < 2);
+    if (terminal) {
+      if (trace_on()) {
+        std::fprintf(stderr, "[paraplan] t=%llu iter=%d: class 0/1 at H=%d: FP64 round\n",
+                     static_cast<unsigned long long>(t), iter, h->cfg.H);
+      }
+      h->timing.fp64_rounds += 1;
+      run_round_launch(h, t, iter, r0, rc, center, c0, c1, injected, out, nullptr, true);
+      return;
+    }
+  }
   std::vector<char> certified(rc, 0);
   std::vector<int64_t> list;
   std::vector<XBest> xmine(rc), xall;
   bool widened = shard_mode == 2;  // no select ran yet
   constexpr int kPasses = 6;
   for (int pass = 0; pass < kPasses; ++pass) {
-    if (pass > 0 || widened) {  // (widened) select over the uncertified restarts
-      h->d_bound.reserve(sizeof(ppdev::SelBound) * rc, "window bounds");
-      h->h_bound.reserve(sizeof(ppdev::SelBound) * rc, "pinned bounds");
-      std::memcpy(h->h_bound.p, bound.data(), sizeof(ppdev::SelBound) * rc);
-      ck(cudaMemcpyAsync(h->d_bound.p, h->h_bound.p, sizeof(ppdev::SelBound) * rc,
-                         cudaMemcpyHostToDevice, h->stream),
-         "bounds H2D");
-      a.sel_bound = static_cast<const ppdev::SelBound*>(h->d_bound.p);
+    auto reselect = [&] {  // the select kernel with the current bounds
+      if (a.sel_bound != nullptr || pass > 0 || widened) {
+        h->d_bound.reserve(sizeof(ppdev::SelBound) * rc, "window bounds");
+        h->h_bound.reserve(sizeof(ppdev::SelBound) * rc, "pinned bounds");
+        std::memcpy(h->h_bound.p, bound.data(), sizeof(ppdev::SelBound) * rc);
+        ck(cudaMemcpyAsync(h->d_bound.p, h->h_bound.p, sizeof(ppdev::SelBound) * rc,
+                           cudaMemcpyHostToDevice, h->stream),
+           "bounds H2D");
+        a.sel_bound = static_cast<const ppdev::SelBound*>(h->d_bound.p);
+      }
       ck(cudaMemsetAsync(a.counters + 2, 0, sizeof(uint32_t), h->stream), "selection counter");
       ck(static_cast<cudaError_t>(ppdev::launch_select(a, h->stream)), "window select launch");
       ck(cudaMemcpyAsync(h->h_round.p, h->d_round.p, kSelOff + sizeof(int64_t) * kSelFirst,
@@ -505,23 +554,33 @@ void certify_round(pp_handle* h, ppdev::RoundArgs& a, uint64_t t, int iter, int 
       h->timing.launches += 1;
       n_sel = static_cast<const uint32_t*>(h->h_round.p)[2];
       widened = false;
+    };
+    if (pass > 0 || widened) reselect();  // (widened) window of the uncertified restarts
+    // a window wider than the selection buffers: grow them, select again
+    while (n_sel > static_cast<uint32_t>(h->sel_cap) && n_sel <= static_cast<uint32_t>(kSelMax)) {
+      if (trace_on()) {
+        std::fprintf(stderr, "[paraplan] t=%llu iter=%d pass=%d selected=%u: selection grows\n",
+                     static_cast<unsigned long long>(t), iter, pass, n_sel);
+      }
+      grow_selection(h, a, static_cast<int>(std::min<uint32_t>(
+                               static_cast<uint32_t>(kSelMax), n_sel + n_sel / 4)));
+      reselect();
     }
-    const bool overflow = n_sel > static_cast<uint32_t>(kSelCap);
+    const bool overflow = n_sel > static_cast<uint32_t>(h->sel_cap);
     if (overflow && trace_on()) {
       std::fprintf(stderr, "[paraplan] t=%llu iter=%d pass=%d selected=%u: window overflow\n",
                    static_cast<unsigned long long>(t), iter, pass, n_sel);
     }
     list.clear();
     if (!overflow) {
+      std::vector<int64_t> sl(n_sel);
+      std::memcpy(sl.data(), static_cast<const char*>(h->h_round.p) + kSelOff,
+                  sizeof(int64_t) * std::min<uint32_t>(n_sel, kSelFirst));
       if (n_sel > static_cast<uint32_t>(kSelFirst)) {
-        ck(cudaMemcpy(reinterpret_cast<int64_t*>(static_cast<char*>(h->h_round.p) + kSelOff) +
-                          kSelFirst,
-                      a.sel_list + kSelFirst, sizeof(int64_t) * (n_sel - kSelFirst),
+        ck(cudaMemcpy(sl.data() + kSelFirst, a.sel_more, sizeof(int64_t) * (n_sel - kSelFirst),
                       cudaMemcpyDeviceToHost),
            "selection D2H");
       }
-      const int64_t* sl =
-          reinterpret_cast<const int64_t*>(static_cast<const char*>(h->h_round.p) + kSelOff);
       for (uint32_t i = 0; i < n_sel; ++i) {
         const auto it = std::lower_bound(known.begin(), known.end(), sl[i], by_index);
         if (it == known.end() || it->first != sl[i]) list.push_back(sl[i]);
@@ -540,7 +599,7 @@ void certify_round(pp_handle* h, ppdev::RoundArgs& a, uint64_t t, int iter, int 
     } else {
       // wide window: FP64 keys from the device, exact host keys for the FP64
       // near-ties of each restart's best
-      ck(cudaMemcpyAsync(a.sel_list, list.data(), sizeof(int64_t) * list.size(),
+      ck(cudaMemcpyAsync(h->d_reflist.p, list.data(), sizeof(int64_t) * list.size(),
                          cudaMemcpyHostToDevice, h->stream),
          "refine list H2D");
       const uint32_t n_list = static_cast<uint32_t>(list.size());
@@ -569,7 +628,7 @@ void certify_round(pp_handle* h, ppdev::RoundArgs& a, uint64_t t, int iter, int 
       std::vector<int> ties;
       for (size_t i = 0; i < dev.size(); ++i) {
         const Exact& b = got[best[dev[i].restart]];
-        const double tol = 1e-12;
+        const double tol = rho64(h->cfg.H);  // two FP64 keys' error bounds
         if (got[i].cls == b.cls && std::abs(got[i].k1 - b.k1) <= tol * std::max(1.0, std::abs(b.k1)) &&
             std::abs(got[i].k2 - b.k2) <= tol * std::max(1.0, std::abs(b.k2))) {
           ties.push_back(static_cast<int>(i));
@@ -698,6 +757,7 @@ void certify_round(pp_handle* h, ppdev::RoundArgs& a, uint64_t t, int iter, int 
   }
   if (fp64) throw std::runtime_error("near-tie re-ranking could not certify an FP64 round");
   h->timing.refined = -1;
+  h->timing.fp64_rounds += 1;
   run_round_launch(h, t, iter, r0, rc, center, c0, c1, injected, out, nullptr, true);
 }
 

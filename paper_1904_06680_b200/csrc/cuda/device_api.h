@@ -11,6 +11,7 @@ namespace ppdev {
 
 constexpr int kMaxLayers = 16;
 constexpr int kMaxRestartsPerLaunch = 64;  // per-warp restart tables of the refill kernel
+constexpr int kSelFirst = 512;  // selected indices stored in the round block (copied back with it)
 
 // Per-sample output of the parity/debug path (same layout as pp_rollout_stats).
 struct SampleOut {
@@ -152,9 +153,11 @@ struct RoundArgs {
   // does not force extra widening passes
   Rec* out_free;
   const void* field64;         // FP64 image of the field (same layout as `field`)
-  int64_t* sel_list;           // [sel_cap] selected flat indices
+  int64_t* sel_list;           // [kSelFirst] the first selected flat indices (round block)
+  int64_t* sel_more;           // [sel_cap - kSelFirst] the rest of them
+  const int64_t* ref_list;     // [counters[2]] the members refine_kernel evaluates
   SelRec* sel_out;             // [sel_cap] their FP64 keys
-  int32_t sel_cap;
+  int32_t sel_cap;             // selection capacity (grown by the host on overflow)
   int32_t refine_grid;
   double sel_rho, sel_alpha;   // window: cost <= best * (1 + rho) + alpha
   const SelBound* sel_bound;   // null: first pass (window around a.out)

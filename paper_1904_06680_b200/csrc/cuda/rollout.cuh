@@ -433,7 +433,13 @@ static __global__ void __launch_bounds__(256) select_kernel(const RoundArgs a) {
     }
     if (take) {
       const unsigned i = atomicAdd(&a.counters[2], 1u);
-      if (i < static_cast<unsigned>(a.sel_cap)) a.sel_list[i] = s;
+      if (i < static_cast<unsigned>(a.sel_cap)) {
+        if (i < static_cast<unsigned>(kSelFirst)) {
+          a.sel_list[i] = s;
+        } else {
+          a.sel_more[i - kSelFirst] = s;
+        }
+      }
     }
   }
 }
@@ -489,7 +495,7 @@ __global__ void __launch_bounds__(128) refine_kernel(const RoundArgs a) {
        base += stride) {
     const unsigned i = base + (threadIdx.x & 31u);
     const bool valid = i < n_sel;
-    const int64_t s = a.sel_list[valid ? i : base];
+    const int64_t s = a.ref_list[valid ? i : base];
     const int r = static_cast<int>(s / a.count);
     const int64_t local = s - static_cast<int64_t>(r) * a.count;
     draw_theta<double, Net64::kP>(a, __ldg(a.key_prefix + r),

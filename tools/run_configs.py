@@ -30,6 +30,7 @@ def time_round(w, reps=3, refine=1):
         t = dp.timing()
         out.append(dict(wall_ms=wall, device_ms=t.kernel_ms, certify_ms=t.certify_ms,
                         refined=t.refined, steps=t.executed_steps, cls=int(rec[0]["cls"]),
+                        fp64_rounds=t.fp64_rounds, rollout_ms=t.rollout_ms,
                         cand=int(rec[0]["candidate"])))
     best = min(out[1:], key=lambda d: d["wall_ms"])
     best["nominal_steps_per_s"] = w.samples * w.model.H / (best["wall_ms"] * 1e-3)
