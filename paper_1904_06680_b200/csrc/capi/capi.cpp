@@ -75,6 +75,7 @@ void prewarm(pp_handle* h) {
   h->snap_valid = false;
   h->snapshot = nullptr;
   h->timing = pp_timing{};
+  h->prefer_fp64 = false;  // the warm-up's fake snapshot says nothing about real ticks
 }
 
 // The exchange of an in-process sharded planner (PlannerConfig::devices):
@@ -206,7 +207,8 @@ void pp_destroy(pp_handle* h) {
   if (h->stream != nullptr) cudaStreamSynchronize(h->stream);
   for (DevBuf* b : {&h->d_field, &h->d_params, &h->d_round, &h->d_tiles, &h->d_movers, &h->d_bin,
                     &h->d_samples, &h->d_scratch, &h->d_injected, &h->d_theta, &h->d_skeys,
-                    &h->d_sel, &h->d_bound, &h->d_field64}) {
+                    &h->d_sel, &h->d_bound, &h->d_field64, &h->d_selmore, &h->d_reflist,
+                    &h->d_listkeys, &h->d_listout}) {
     b->release();
   }
   for (HostBuf* b : {&h->h_field, &h->h_params, &h->h_round, &h->h_bound, &h->h_movers,

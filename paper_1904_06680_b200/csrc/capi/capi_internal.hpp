@@ -272,8 +272,6 @@ constexpr size_t kPackOff =
 constexpr size_t kSelOff =
     (kPackOff + sizeof(uint64_t) * 2 * ppdev::kMaxRestartsPerLaunch + 63) / 64 * 64;
 constexpr size_t kRoundBytes = kSelOff + sizeof(int64_t) * kSelFirst;
-// refine_kernel: two CTAs of 128 threads per SM
-inline int refine_grid(int sms) { return sms * 2; }
 
 // PARAPLAN_TRACE=1: one stderr line per certification pass; 2: also the
 // host-side phase times of every plan step (diagnostics).
@@ -324,7 +322,11 @@ struct pp_handle {
   ppdev::NetKind kind = ppdev::NetKind::kGeneric;
   int device = 0;
   int sms = 148;  // multiprocessors of `device` (queried at construction)
+  int refine_blocks = 0;  // resident refine_kernel CTAs per SM (0: not queried yet)
   bool fp64 = false;
+  // FP32 planner: the last certified round needed FP64 (class 0/1 anchors
+  // beyond the FP32 error envelope); the next round starts in FP64
+  bool prefer_fp64 = false;
 
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -335,7 +337,7 @@ struct pp_handle {
   cudaEvent_t ev_field = nullptr;
   bool field_via_side = false, field_event = false;
   ppcapi::DevBuf d_field, d_params, d_round, d_tiles, d_samples, d_scratch, d_injected, d_theta, d_skeys,
-      d_sel, d_bound, d_movers, d_bin, d_selmore, d_reflist;
+      d_sel, d_bound, d_movers, d_bin, d_selmore, d_reflist, d_listkeys, d_listout;
   int sel_cap = 1 << 16;  // selection capacity of this handle (kSelCap, grown on overflow)
   ppcapi::HostBuf h_field, h_params, h_round, h_bound, h_movers;
 
@@ -396,6 +398,12 @@ struct pp_handle {
 };
 
 namespace ppcapi {
+
+// refine_kernel: every resident CTA of 128 threads (queried once per handle)
+inline int refine_grid(pp_handle* h) {
+  if (h->refine_blocks == 0) h->refine_blocks = ppdev::refine_occupancy(h->kind);
+  return h->sms * h->refine_blocks;
+}
 
 // upload.cpp
 void finish_field(pp_handle* h, ppdev::RoundArgs& a);

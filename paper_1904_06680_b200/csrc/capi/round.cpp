@@ -69,7 +69,10 @@ int fp32_max_h() {
   }();
   return v;
 }
+// FP64 windows: class 0/1 anchors (terminal cost) by the horizon; class 2
+// (path length of a reaching rollout, measured FP64 error <= 1.1e-13)
 double rho64(int H) { return H <= 60 ? 1e-9 : 1e-6; }
+constexpr double kRho64Reached = 1e-11;
 
 // Occupancy of the rollout kernel for (precision, staged field size, grid
 // mode), queried once per handle.
@@ -114,6 +117,12 @@ void run_round_launch(pp_handle* h, uint64_t t, int iter, int r0, int rc, const 
                       int64_t c0, int64_t c1, const double* injected, pp_record* out,
                       pp_rollout_stats* per_sample, bool force_fp64) {
   const int64_t count = c1 - c0;
+  // the last round of this planner needed FP64 (class 0/1 beyond the FP32
+  // envelope): start in FP64 (a closed loop's ticks look alike)
+  if (!h->fp64 && h->prefer_fp64 && h->rerank && h->snapshot != nullptr &&
+      per_sample == nullptr && h->cfg.H > fp32_max_h()) {
+    force_fp64 = true;
+  }
   const bool fp64 = h->fp64 || force_fp64;
   const bool rerank = h->rerank && h->snapshot != nullptr;
   // the schedule (refill: generator + rollout) and the theta record width do
@@ -195,8 +204,9 @@ void run_round_launch(pp_handle* h, uint64_t t, int iter, int r0, int rc, const 
   if (rerank) {
     grow_selection(h, a, h->sel_cap);
     a.sel_list = reinterpret_cast<int64_t*>(dres + kSelOff);
-    a.refine_grid = refine_grid(h->sms);
+    a.refine_grid = refine_grid(h);
     a.sel_rho = fp64 ? rho64(h->cfg.H) : h->sel_rho;
+    a.sel_rho2 = fp64 ? kRho64Reached : h->sel_rho;
     a.sel_alpha = fp64 ? 1e-13 : 1e-6;
   }
 
@@ -251,7 +261,7 @@ void run_round_launch(pp_handle* h, uint64_t t, int iter, int r0, int rc, const 
                        (fp64 && h->kind == ppdev::NetKind::k5_10_10_2);
   if (generic || rerank) {
     const size_t lanes = std::max<size_t>(generic ? static_cast<size_t>(a.grid) * a.block : 0,
-                                          rerank ? refine_grid(h->sms) * 128 : 0);
+                                          rerank ? refine_grid(h) * 128 : 0);
     h->d_scratch.reserve(lanes * h->P * sizeof(double), "theta scratch");
     a.theta_scratch = static_cast<float*>(h->d_scratch.p);
     a.theta_scratch64 = static_cast<double*>(h->d_scratch.p);
@@ -342,6 +352,69 @@ void run_round_launch(pp_handle* h, uint64_t t, int iter, int r0, int rc, const 
   phase("certified");
   h->timing.certify_ms +=
       std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - c_t0).count();
+}
+
+// FP64 re-evaluation of the n window members listed in h->d_reflist (flat
+// indices of the round `a`, restart-major over `count` candidates per
+// restart, candidates starting at c0): a list round of the FP64 generator +
+// refill rollout (the FP64 round's own kernels and per-candidate cost, at
+// full occupancy), keys only. dev[i] receives member i's FP64 key, flagged[i]
+// whether a discrete FP64 verdict came within the FP64 margin of flipping.
+void eval_list_fp64(pp_handle* h, const ppdev::RoundArgs& a, int64_t n, int64_t count, int64_t c0,
+                    std::vector<ppdev::SelRec>& dev, std::vector<char>& flagged) {
+  ppdev::RoundArgs L = a;
+  L.list = static_cast<const int64_t*>(h->d_reflist.p);
+  L.list_count = count;
+  L.count = n;
+  L.restart_count = 1;
+  L.cand_begin = c0;
+  L.field = ensure_field64(h);
+  L.field64 = L.field;
+  L.lay = L.lay64;
+  L.field_smem_bytes = 0;
+  L.per_sample = nullptr;
+  L.keys_only = 1;
+  L.out_free = nullptr;
+  L.sel_packed = 0;
+  L.pkeys = nullptr;
+  L.skey32 = 0;
+  h->d_listkeys.reserve(sizeof(ppdev::SKey) * static_cast<size_t>(n), "list keys");
+  h->d_listout.reserve(sizeof(ppdev::Rec) * 2, "list winner");
+  L.skeys = h->d_listkeys.p;
+  L.out = static_cast<ppdev::Rec*>(h->d_listout.p);
+  const ppdev::LaunchShape s0 = launch_shape(h, true, 0, 0);
+  h->d_theta.reserve(static_cast<size_t>(n) * s0.theta_elem * sizeof(double), "theta buffer");
+  L.theta_buf = h->d_theta.p;
+  const ppdev::LaunchShape shape =
+      launch_shape(h, true, 0, ppdev::grid_kind(L.grid_mode, 0, L.field_ns, L.field_nd));
+  const int64_t tiles = (n + 31) / 32;
+  L.tiles_per_restart = static_cast<int32_t>(tiles);
+  L.n_tiles = static_cast<int32_t>(tiles);
+  L.block = shape.block;
+  L.grid = std::max(1, std::min(shape.grid, static_cast<int>((tiles + ppdev_warps() - 1) /
+                                                             ppdev_warps())));
+  // the FP64 margin flags as an FP64 round's (narrow misses too: a member
+  // must never look robust when its exact class could differ)
+  L.kd.marg_lo = -L.kd.dmarg;
+  ck(static_cast<cudaError_t>(ppdev::launch_generate_f64(h->kind, L, h->stream)),
+     "list generator launch");
+  ck(static_cast<cudaError_t>(ppdev::launch_rollout_f64(h->kind, L, h->stream)),
+     "list rollout launch");
+  std::vector<ppdev::SKey> keys(static_cast<size_t>(n));
+  ck(cudaMemcpyAsync(keys.data(), h->d_listkeys.p, sizeof(ppdev::SKey) * keys.size(),
+                     cudaMemcpyDeviceToHost, h->stream),
+     "list keys D2H");
+  ck(cudaStreamSynchronize(h->stream), "list round");
+  h->timing.launches += 3;
+  for (int64_t i = 0; i < n; ++i) {
+    const ppdev::SKey& k = keys[static_cast<size_t>(i)];
+    ppdev::SelRec& d = dev[static_cast<size_t>(i)];
+    d.cls = static_cast<int32_t>(k.meta & 3u);
+    const int tg = static_cast<int>(k.meta >> 8);
+    d.k1 = d.cls == 2 ? -static_cast<double>(tg) : -k.cost;
+    d.k2 = d.cls == 2 ? -k.cost : 0.0;
+    flagged[static_cast<size_t>(i)] = (k.meta & 4u) != 0u;
+  }
 }
 
 // Certified re-ranking (PlannerConfig::refine). The FP32 keys are trusted
@@ -466,13 +539,14 @@ void certify_round(pp_handle* h, ppdev::RoundArgs& a, uint64_t t, int iter, int 
       return;
     }
   }
-  const double rho = a.sel_rho, alpha = a.sel_alpha;
+  const double alpha = a.sel_alpha;
+  const auto rho_of = [&](int cls) { return cls == 2 ? a.sel_rho2 : a.sel_rho; };
   const char* hres = static_cast<const char*>(h->h_round.p);
   std::vector<ppdev::SelBound> bound(rc);
   auto set_bound = [&](int r, int cls, int t_goal, double cost) {
     bound[r].cls = cls;
     bound[r].t_goal = cls == 2 ? t_goal : 0;
-    bound[r].thr = cost * (1.0 + rho) + alpha;  // as select_kernel (no contraction)
+    bound[r].thr = cost * (1.0 + rho_of(cls)) + alpha;  // as select_kernel (no contraction)
   };
   if (shard_mode == 1) {
     // the packed global winners the select kernel anchored on (keypack.h)
@@ -514,6 +588,12 @@ void certify_round(pp_handle* h, ppdev::RoundArgs& a, uint64_t t, int iter, int 
     }
     for (int r = 0; r < rc; ++r) set_bound(r, mine[r].cls, mine[r].t_goal, mine[r].cost);
   }
+  // an FP32 planner's FP64 round: would FP32 have done (class 2 anchors)?
+  if (fp64 && !h->fp64) {
+    bool terminal = false;
+    for (int r = 0; r < rc; ++r) terminal = terminal || (bound[r].cls >= 0 && bound[r].cls < 2);
+    h->prefer_fp64 = terminal;
+  }
   // outside the FP32 envelope (class 0/1 anchors beyond fp32_max_h): the
   // round is redone in FP64 (every shard decides alike: global anchors)
   if (!fp64 && h->cfg.H > fp32_max_h()) {
@@ -525,6 +605,7 @@ void certify_round(pp_handle* h, ppdev::RoundArgs& a, uint64_t t, int iter, int 
                      static_cast<unsigned long long>(t), iter, h->cfg.H);
       }
       h->timing.fp64_rounds += 1;
+      h->prefer_fp64 = true;
       run_round_launch(h, t, iter, r0, rc, center, c0, c1, injected, out, nullptr, true);
       return;
     }
@@ -602,19 +683,29 @@ void certify_round(pp_handle* h, ppdev::RoundArgs& a, uint64_t t, int iter, int 
       ck(cudaMemcpyAsync(h->d_reflist.p, list.data(), sizeof(int64_t) * list.size(),
                          cudaMemcpyHostToDevice, h->stream),
          "refine list H2D");
-      const uint32_t n_list = static_cast<uint32_t>(list.size());
-      ck(cudaMemcpyAsync(a.counters + 2, &n_list, sizeof(uint32_t), cudaMemcpyHostToDevice,
-                         h->stream),
-         "refine count H2D");
-      a.field64 = ensure_field64(h);
-      ck(static_cast<cudaError_t>(ppdev::launch_refine(h->kind, a, h->stream)), "refine launch");
       std::vector<ppdev::SelRec> dev(list.size());
-      ck(cudaMemcpyAsync(dev.data(), a.sel_out, sizeof(ppdev::SelRec) * list.size(),
-                         cudaMemcpyDeviceToHost, h->stream),
-         "refine D2H");
-      ck(cudaStreamSynchronize(h->stream), "refine kernel");
+      std::vector<char> flagged(list.size(), 0);
+      if (launch_shape(h, true, 0, 0).refill) {
+        eval_list_fp64(h, a, static_cast<int64_t>(list.size()), count, c0, dev, flagged);
+        for (size_t i = 0; i < list.size(); ++i) {
+          dev[i].restart = static_cast<int32_t>(list[i] / count);
+          dev[i].cand = static_cast<int32_t>(c0 + (list[i] - dev[i].restart * count));
+        }
+      } else {  // generic architectures: one lockstep FP64 rollout per lane
+        const uint32_t n_list = static_cast<uint32_t>(list.size());
+        ck(cudaMemcpyAsync(a.counters + 2, &n_list, sizeof(uint32_t), cudaMemcpyHostToDevice,
+                           h->stream),
+           "refine count H2D");
+        a.field64 = ensure_field64(h);
+        ck(static_cast<cudaError_t>(ppdev::launch_refine(h->kind, a, h->stream)),
+           "refine launch");
+        ck(cudaMemcpyAsync(dev.data(), a.sel_out, sizeof(ppdev::SelRec) * list.size(),
+                           cudaMemcpyDeviceToHost, h->stream),
+           "refine D2H");
+        ck(cudaStreamSynchronize(h->stream), "refine kernel");
+        h->timing.launches += 1;
+      }
       phase("refine64");
-      h->timing.launches += 1;
       std::vector<int> best(rc, -1);
       for (size_t i = 0; i < dev.size(); ++i) {
         got[i] = Exact{dev[i].cls, dev[i].cls == 2 ? static_cast<int>(-dev[i].k1) : -1,
@@ -628,9 +719,13 @@ void certify_round(pp_handle* h, ppdev::RoundArgs& a, uint64_t t, int iter, int 
       std::vector<int> ties;
       for (size_t i = 0; i < dev.size(); ++i) {
         const Exact& b = got[best[dev[i].restart]];
-        const double tol = rho64(h->cfg.H);  // two FP64 keys' error bounds
-        if (got[i].cls == b.cls && std::abs(got[i].k1 - b.k1) <= tol * std::max(1.0, std::abs(b.k1)) &&
-            std::abs(got[i].k2 - b.k2) <= tol * std::max(1.0, std::abs(b.k2))) {
+        // two FP64 keys' error bounds
+        const double tol = b.cls == 2 ? kRho64Reached : rho64(h->cfg.H);
+        // FP64 near-ties of the best, and every member whose FP64 verdict
+        // came within the FP64 margin of flipping (it may rise a class)
+        if (flagged[i] ||
+            (got[i].cls == b.cls && std::abs(got[i].k1 - b.k1) <= tol * std::max(1.0, std::abs(b.k1)) &&
+             std::abs(got[i].k2 - b.k2) <= tol * std::max(1.0, std::abs(b.k2)))) {
           ties.push_back(static_cast<int>(i));
         }
       }
@@ -701,6 +796,7 @@ void certify_round(pp_handle* h, ppdev::RoundArgs& a, uint64_t t, int iter, int 
       if (certified[r]) continue;
       const ppdev::SelBound& bd = bound[r];
       const XBest& e = gbest[r];
+      const double rho = rho_of(bd.cls);
       const double slack = 0.5 * (rho * bd.thr + alpha);
       bool ok = false;
       if (e.cls >= 0) {

@@ -160,6 +160,13 @@ struct RoundArgs {
   int32_t sel_cap;             // selection capacity (grown by the host on overflow)
   int32_t refine_grid;
   double sel_rho, sel_alpha;   // window: cost <= best * (1 + rho) + alpha
+  double sel_rho2;             // rho of windows anchored on a class-2 (reached) candidate
+  // list rounds (the certification's FP64 re-evaluation of a wide window):
+  // item i of the round is the flat candidate list[i] (restart-major over
+  // list_count candidates per restart) of the round the list came from; the
+  // round itself is one "restart" of count = n items, keys_only
+  const int64_t* list;
+  int64_t list_count;
   const SelBound* sel_bound;   // null: first pass (window around a.out)
   double dmarg32;              // FP32 marginal threshold (host side, copied into kf)
   int32_t sms;                 // multiprocessors of the device (launch sizing)
@@ -228,6 +235,8 @@ int launch_pack_keys(const RoundArgs& a, void* stream);
 int launch_copy_out(const void* src, void* host_dst, size_t bytes, void* stream);
 // FP64 re-evaluation of the selected candidates into sel_out.
 int launch_refine(NetKind k, const RoundArgs& a, void* stream);
+// Resident refine_kernel CTAs of 128 threads per SM.
+int refine_occupancy(NetKind k);
 
 // Device binning of the dynamic rows of a raw-points field (field.hpp's
 // layout): row r of mover k sits at x + r * step (FP64, no contraction: the

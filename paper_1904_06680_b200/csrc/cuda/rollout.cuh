@@ -70,11 +70,14 @@ __global__ void __launch_bounds__(256, PARAPLAN_GEN_MINB) generate_kernel(const 
   const int64_t total = a.count * a.restart_count;
   for (int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; s < total;
        s += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    // restart of flat index s (32-bit division when the round is small)
-    const int r = total <= 0x7fffffff
-                      ? static_cast<int>(static_cast<uint32_t>(s) / static_cast<uint32_t>(a.count))
-                      : static_cast<int>(s / a.count);
-    const int64_t local = s - static_cast<int64_t>(r) * a.count;
+    // restart of flat index s (32-bit division when the round is small); a
+    // list round draws item s = candidate list[s] of the listed round
+    const int64_t flat = a.list != nullptr ? a.list[s] : s;
+    const int64_t cnt = a.list != nullptr ? a.list_count : a.count;
+    const int r = flat <= 0x7fffffff && cnt <= 0x7fffffff
+                      ? static_cast<int>(static_cast<uint32_t>(flat) / static_cast<uint32_t>(cnt))
+                      : static_cast<int>(flat / cnt);
+    const int64_t local = flat - static_cast<int64_t>(r) * cnt;
     union {
       Real v[W];
       Vec16<Real> q[V];
@@ -411,12 +414,14 @@ static __global__ void __launch_bounds__(256) select_kernel(const RoundArgs a) {
       const Unpacked u = unpack_key(pf != kPackEmpty ? pf : a.pkeys[r]);
       bd.cls = u.cls;
       bd.t_goal = u.cls == 2 ? u.t_goal : 0;
-      bd.thr = static_cast<double>(u.cost) * (1.0 + a.sel_rho) + a.sel_alpha;
+      bd.thr = static_cast<double>(u.cost) * (1.0 + (u.cls == 2 ? a.sel_rho2 : a.sel_rho)) +
+               a.sel_alpha;
     } else {  // first pass: around the round winner (its best unflagged candidate)
       const Rec b = (a.out_free != nullptr && a.out_free[r].cls >= 0) ? a.out_free[r] : a.out[r];
       bd.cls = b.cls;
       bd.t_goal = b.cls == 2 ? static_cast<int>(-b.k1) : 0;
-      bd.thr = (b.cls == 2 ? -b.k2 : -b.k1) * (1.0 + a.sel_rho) + a.sel_alpha;
+      bd.thr = (b.cls == 2 ? -b.k2 : -b.k1) * (1.0 + (b.cls == 2 ? a.sel_rho2 : a.sel_rho)) +
+               a.sel_alpha;
     }
     SKey k;
     if (a.skey32) {
@@ -667,6 +672,19 @@ int launch_refine_impl(const RoundArgs& a, void* stream) {
     refine_kernel<Net64, 0><<<a.refine_grid, 128, 0, st>>>(a);
   }
   return static_cast<int>(cudaGetLastError());
+}
+
+// Resident refine_kernel CTAs per SM (the smallest over the grid modes), so
+// a wide window fills the GPU.
+template <class Net64>
+int refine_occupancy_impl() {
+  int occ = 1 << 30;
+  for (KernelFn k : {refine_kernel<Net64, 0>, refine_kernel<Net64, 1>, refine_kernel<Net64, 2>}) {
+    int b = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k, 128, 0) != cudaSuccess) return 2;
+    occ = std::min(occ, b);
+  }
+  return std::max(1, occ);
 }
 
 template <typename Real, class Net>

@@ -83,6 +83,17 @@ int launch_copy_out(const void* src, void* host_dst, size_t bytes, void* stream)
                                              static_cast<uint4*>(dst), n16));
 }
 
+int refine_occupancy(NetKind k) {
+  switch (k) {
+    case NetKind::k5_2_2:
+      return refine_occupancy_impl<NetReg<double, 2>>();
+    case NetKind::k5_10_2:
+      return refine_occupancy_impl<NetReg<double, 10>>();
+    default:
+      return refine_occupancy_impl<NetGlobal<double>>();
+  }
+}
+
 int launch_refine(NetKind k, const RoundArgs& a, void* stream) {
   switch (k) {
     case NetKind::k5_2_2:

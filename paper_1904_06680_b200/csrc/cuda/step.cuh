@@ -97,8 +97,10 @@ __device__ __forceinline__ int advance(Lane<Real>& L, const Net& net, const Cons
   const Real tan_d = K.tan_small ? M<Real>::tn_small(delta) : M<Real>::tn(delta);
   const Real tb = M<Real>::ndiv(K.l_r * tan_d, K.wb_d, K.inv_wb);
   const Real tv = K.Ts * L.v;
-  const Real nx = L.x + tv * (cphi - tb * sphi);
-  const Real ny = L.y + tv * (sphi + tb * cphi);
+  const Real ix = tv * (cphi - tb * sphi);
+  const Real iy = tv * (sphi + tb * cphi);
+  const Real nx = L.x + ix;
+  const Real ny = L.y + iy;
   const Real nphi = L.phi + M<Real>::ndiv(tv * tan_d, K.wb_d, K.inv_wb);
   Real nv;
   if constexpr (sizeof(Real) == sizeof(double)) {
@@ -106,8 +108,17 @@ __device__ __forceinline__ int advance(Lane<Real>& L, const Net& net, const Cons
   } else {
     nv = fmaf(c1, K.ts_uhalf, L.v + K.ts_umid);
   }
-  const Real dx = nx - L.x, dy = ny - L.y;
-  const Real seg = M<Real>::sq(dx * dx + dy * dy);
+  // path segment (src/planner.cpp:177-179): FP64 takes the reference's
+  // difference of the rounded positions; FP32 takes the increment itself,
+  // since nx - x cancels ~|x| / |dx| float ulps (1e-6 relative per segment at
+  // 30 m), which the FP64 difference does not
+  Real seg;
+  if constexpr (sizeof(Real) == sizeof(double)) {
+    const Real dx = nx - L.x, dy = ny - L.y;
+    seg = M<Real>::sq(dx * dx + dy * dy);
+  } else {
+    seg = M<Real>::sq(ix * ix + iy * iy);
+  }
   if (cls < 0) {
     L.path += seg;
     L.x = nx;
