@@ -129,6 +129,9 @@ pp_status pp_create(const pp_model* m, pp_handle** out) {
     hp->policy = std::make_unique<paraplan::MlpPolicy>(arch);
     hp->params.validate();
     hp->cfg.validate();
+    if (hp->cfg.H > ppdev::kMaxKeyHorizon) {  // the 15-bit state fields of the sample keys
+      throw std::invalid_argument("the device planner supports horizons H <= 32766");
+    }
     hp->chassis = paraplan::ChassisPolytope::rectangle(hp->params);
     hp->box = {hp->params.front_extent(), hp->params.rear_extent(), hp->params.half_width};
     hp->P = hp->policy->param_count();

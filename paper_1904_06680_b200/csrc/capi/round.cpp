@@ -267,8 +267,8 @@ void run_round_launch(pp_handle* h, uint64_t t, int iter, int r0, int rc, const 
     a.theta_scratch64 = static_cast<double*>(h->d_scratch.p);
   }
   // several restarts: narrow collision misses are marginal too (step.cuh)
-  a.kf.marg_lo = rc > 1 ? -a.kf.dmarg : 0.0f;
-  a.kd.marg_lo = rc > 1 ? -a.kd.dmarg : 0.0;
+  a.kf.flag_miss = rc > 1 ? 1 : 0;
+  a.kd.flag_miss = rc > 1 ? 1 : 0;
   ck(static_cast<cudaError_t>(fp64 ? ppdev::launch_rollout_f64(h->kind, a, h->stream)
                                    : ppdev::launch_rollout_f32(h->kind, a, h->stream)),
      "sampling kernel launch");
@@ -378,7 +378,8 @@ void eval_list_fp64(pp_handle* h, const ppdev::RoundArgs& a, int64_t n, int64_t 
   L.sel_packed = 0;
   L.pkeys = nullptr;
   L.skey32 = 0;
-  h->d_listkeys.reserve(sizeof(ppdev::SKey) * static_cast<size_t>(n), "list keys");
+  // sized to the selection capacity: a closed loop's windows grow tick by tick
+  h->d_listkeys.reserve(sizeof(ppdev::SKey) * std::max<size_t>(n, h->sel_cap), "list keys");
   h->d_listout.reserve(sizeof(ppdev::Rec) * 2, "list winner");
   L.skeys = h->d_listkeys.p;
   L.out = static_cast<ppdev::Rec*>(h->d_listout.p);
@@ -395,7 +396,7 @@ void eval_list_fp64(pp_handle* h, const ppdev::RoundArgs& a, int64_t n, int64_t 
                                                              ppdev_warps())));
   // the FP64 margin flags as an FP64 round's (narrow misses too: a member
   // must never look robust when its exact class could differ)
-  L.kd.marg_lo = -L.kd.dmarg;
+  L.kd.flag_miss = 1;
   ck(static_cast<cudaError_t>(ppdev::launch_generate_f64(h->kind, L, h->stream)),
      "list generator launch");
   ck(static_cast<cudaError_t>(ppdev::launch_rollout_f64(h->kind, L, h->stream)),
@@ -409,11 +410,11 @@ void eval_list_fp64(pp_handle* h, const ppdev::RoundArgs& a, int64_t n, int64_t 
   for (int64_t i = 0; i < n; ++i) {
     const ppdev::SKey& k = keys[static_cast<size_t>(i)];
     ppdev::SelRec& d = dev[static_cast<size_t>(i)];
-    d.cls = static_cast<int32_t>(k.meta & 3u);
-    const int tg = static_cast<int>(k.meta >> 8);
+    d.cls = ppdev::meta_cls(k.meta);
+    const int tg = ppdev::meta_tgoal(k.meta);
     d.k1 = d.cls == 2 ? -static_cast<double>(tg) : -k.cost;
     d.k2 = d.cls == 2 ? -k.cost : 0.0;
-    flagged[static_cast<size_t>(i)] = (k.meta & 4u) != 0u;
+    flagged[static_cast<size_t>(i)] = ppdev::meta_flagged(k.meta);
   }
 }
 

@@ -52,12 +52,15 @@ void fill_consts(const ppdev::RoundArgs& a, ppdev::ConstsT<Real>* k) {
   k->qpad = Real(a.grid_g / 8.0);
   // a discrete verdict whose margin is below this may flip under rounding
   k->dmarg = sizeof(Real) == sizeof(float) ? Real(a.dmarg32) : Real(1e-9);
+  // twice the largest relative drift measured over a rollout (FP32 2.1e-5 at
+  // H=200, FP64 1.1e-13; profiles/r2_error_model*.json)
+  k->dmarg_rel = sizeof(Real) == sizeof(float) ? Real(4e-5) : Real(1e-12);
   k->bcx = Real(0.5 * (a.fe - a.re));
   k->bhx = Real(0.5 * (a.fe + a.re));
   k->inv_wb = Real(1.0 / a.wheelbase);
   k->wb_d = a.wheelbase;
   k->tan_small = a.delta_max <= 0.785 ? 1 : 0;
-  k->marg_lo = Real(0);  // per round (round.cpp)
+  k->flag_miss = 0;  // per round (round.cpp)
 }
 
 // Device image of h->field in the compute precision (one H2D); the FP64 image

@@ -23,9 +23,25 @@ struct SampleOut {
 // 8 bytes (SKey32) for FP32 rounds, whose costs are floats anyway.
 struct SKey {
   double cost;    // terminal cost (cls 0/1) or path length (cls 2)
-  uint32_t meta;  // cls | marginal << 2 | t_goal << 8
+  uint32_t meta;  // make_meta below
   uint32_t pad;
 };
+
+// meta of a sample key: cls (2 bits) | t_goal (15 bits, class 2) | the
+// earliest state index at which a discrete verdict that could IMPROVE the
+// candidate came within the flag band of flipping (a narrow goal miss, a
+// narrow collision hit; 15 bits, kNoStep = none). A class-2 window anchored
+// at t_goal T needs only the flags at states <= T: a later flip reaches later.
+constexpr uint32_t kNoStep = 0x7fff;
+constexpr int kMaxKeyHorizon = 0x7ffe;  // H the 15-bit fields hold
+PP_HD uint32_t make_meta(int cls, int t_goal, uint32_t mstep) {
+  return static_cast<uint32_t>(cls) | (static_cast<uint32_t>(cls == 2 ? t_goal : 0) << 2) |
+         (mstep << 17);
+}
+PP_HD int meta_cls(uint32_t m) { return static_cast<int>(m & 3u); }
+PP_HD int meta_tgoal(uint32_t m) { return static_cast<int>((m >> 2) & 0x7fffu); }
+PP_HD uint32_t meta_mstep(uint32_t m) { return m >> 17; }
+PP_HD bool meta_flagged(uint32_t m) { return (m >> 17) != kNoStep; }
 struct SKey32 {
   float cost;
   uint32_t meta;
@@ -72,8 +88,9 @@ struct ConstsT {
   Real inv_wb;          // 1 / wheelbase (FP32 path multiplies)
   double wb_d;          // wheelbase (FP64 path divides, src/dynamics.cpp:52-55)
   int32_t tan_small;    // delta_max <= pi/4: tan by polynomial ratio (FP32)
-  Real marg_lo;         // collision margins in (marg_lo, dmarg) are marginal: 0 (narrow hits),
-                        // -dmarg with several restarts (narrow misses too)
+  Real dmarg_rel;       // + this x the path so far: the flag band widens with the distance
+                        // travelled (the measured relative drift of a rollout's state)
+  int32_t flag_miss;    // several restarts: narrow collision MISSES are marginal too
 };
 
 // Byte offsets of the parts of a field image.

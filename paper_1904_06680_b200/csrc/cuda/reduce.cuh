@@ -194,8 +194,7 @@ template <typename Real>
 __device__ __forceinline__ void write_skey(const RoundArgs& a, int64_t slot, int cls,
                                            const Lane<Real>& L, Real term) {
   if (a.skeys == nullptr) return;
-  const uint32_t meta = static_cast<uint32_t>(cls) | (L.marg ? 4u : 0u) |
-                        (static_cast<uint32_t>(cls == 2 ? L.h : 0) << 8);
+  const uint32_t meta = make_meta(cls, L.h, L.mstep);
   if constexpr (sizeof(Real) == sizeof(float)) {
     static_cast<SKey32*>(a.skeys)[slot] = SKey32{cls == 2 ? L.path : term, meta};
   } else {

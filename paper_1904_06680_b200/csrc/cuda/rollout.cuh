@@ -265,17 +265,17 @@ static __global__ void __launch_bounds__(256) reduce_keys_kernel(const RoundArgs
       meta = q.meta;
     }
     Key o;
-    o.cls = static_cast<int>(meta & 3u);
+    o.cls = meta_cls(meta);
     o.idx = static_cast<int>(a.cand_begin + c);
     if (o.cls == 2) {
-      o.k1 = -static_cast<double>(meta >> 8);
+      o.k1 = -static_cast<double>(meta_tgoal(meta));
       o.k2 = -cost;
     } else {
       o.k1 = -cost;
       o.k2 = 0.0;
     }
     if (k.cls < 0 || prefer(o, k)) k = o;
-    if ((meta & 4u) == 0u && (kf.cls < 0 || prefer(o, kf))) kf = o;
+    if (!meta_flagged(meta) && (kf.cls < 0 || prefer(o, kf))) kf = o;
   }
   k = block_best(k, red);
   kf = block_best(kf, red);
@@ -431,10 +431,13 @@ static __global__ void __launch_bounds__(256) select_kernel(const RoundArgs a) {
     } else {
       k = static_cast<const SKey*>(a.skeys)[s];
     }
-    const int cls = static_cast<int>(k.meta & 3u);
-    bool take = (k.meta & 4u) != 0u && bd.cls >= 0;
+    const int cls = meta_cls(k.meta);
+    // flagged: a flip could improve it -- before a class-2 anchor's t_goal
+    const uint32_t ms = meta_mstep(k.meta);
+    bool take = bd.cls >= 0 && ms != kNoStep &&
+                (bd.cls != 2 || ms <= static_cast<uint32_t>(bd.t_goal));
     if (cls == bd.cls && k.cost <= bd.thr) {
-      take |= cls != 2 || static_cast<int>(k.meta >> 8) == bd.t_goal;
+      take |= cls != 2 || meta_tgoal(k.meta) == bd.t_goal;
     }
     if (take) {
       const unsigned i = atomicAdd(&a.counters[2], 1u);

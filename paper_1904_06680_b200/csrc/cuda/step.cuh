@@ -12,7 +12,7 @@ template <typename Real>
 struct Lane {
   Real x, y, phi, v, act, pa0, path, f0, f1, ephi;
   int h;
-  bool marg;  // a worse-side collision / goal verdict came within K.dmarg of flipping
+  uint32_t mstep;  // earliest state of a verdict within the flag band (meta, kNoStep = none)
   __device__ __forceinline__ void start(const Consts<Real>& K, Real first0, Real first1) {
     x = y = phi = Real(0);
     v = K.v0;
@@ -22,7 +22,7 @@ struct Lane {
     f0 = first0;
     f1 = first1;
     h = 0;
-    marg = false;
+    mstep = kNoStep;
   }
 };
 
@@ -48,16 +48,20 @@ __device__ __forceinline__ int advance(Lane<Real>& L, const Net& net, const Cons
   M<Real>::sc(L.phi, &sphi, &cphi);
   L.ephi = M<Real>::wrap(K.gphi - L.phi);
   bool hit = false;
+  // the flag band: the base margin plus the drift the state may have
+  // accumulated over the path so far
+  const Real band = K.dmarg + K.dmarg_rel * L.path;
+  bool narrow = false;
   if (f.Ns + f.Nd > 0) {
     // a lane may stop at a hit whose margin is too large to flip
-    const Real cm = collide_margin<Real, kGrid>(f, K, L.h, L.x, L.y, cphi, sphi, K.dmarg, live);
+    const Real cm = collide_margin<Real, kGrid>(f, K, L.h, L.x, L.y, cphi, sphi, band, live);
     hit = cm > Real(0);
     // a narrow hit might be free in exact arithmetic (a better outcome).
     // With several restarts a narrow miss is flagged too: it might be a hit
     // (a worse outcome), so it must not anchor a restart's window, which is
     // built around the restart's best unflagged candidate (flagged ones are
     // always in the window)
-    L.marg |= (cm > K.marg_lo) & (cm < K.dmarg);
+    narrow = (cm > (K.flag_miss ? -band : Real(0))) & (cm < band);
   }
   const Real gdx = K.gx - L.x, gdy = K.gy - L.y;
   // inclusive goal box: eps - |err| >= 0 <=> |err| <= eps, exactly
@@ -66,7 +70,8 @@ __device__ __forceinline__ int advance(Lane<Real>& L, const Net& net, const Cons
                        fmin(K.eps_phi - M<Real>::ab(L.ephi), K.eps_v - M<Real>::ab(K.gv - L.v)));
   const bool reached = gm >= Real(0);
   // a narrow miss might reach in exact arithmetic (a better outcome)
-  L.marg |= !reached & (gm > -K.dmarg);
+  narrow |= !reached & (gm > -band);
+  L.mstep = narrow ? min(L.mstep, static_cast<uint32_t>(L.h)) : L.mstep;
   const int cls = hit ? 0 : (reached ? 2 : (L.h == H ? 1 : -1));
 
   Real s[5];
