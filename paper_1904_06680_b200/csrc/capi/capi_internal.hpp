@@ -273,6 +273,16 @@ constexpr size_t kSelOff =
     (kPackOff + sizeof(uint64_t) * 2 * ppdev::kMaxRestartsPerLaunch + 63) / 64 * 64;
 constexpr size_t kRoundBytes = kSelOff + sizeof(int64_t) * kSelFirst;
 
+// FP32 rounds are certified for every class up to this horizon, beyond it for
+// class-2 (reaching) windows only (round.cpp: the error model).
+inline int fp32_max_h() {
+  static const int v = [] {
+    const char* e = std::getenv("PARAPLAN_FP32_MAX_H");
+    return e != nullptr ? std::atoi(e) : 40;
+  }();
+  return v;
+}
+
 // PARAPLAN_TRACE=1: one stderr line per certification pass; 2: also the
 // host-side phase times of every plan step (diagnostics).
 inline int trace_level() {

@@ -62,13 +62,6 @@ int host_max() {
 // holds with a wide margin: every class up to H = fp32_max_h() (40), class 2
 // beyond. A longer round whose anchor is of class 0/1 is redone in FP64, and
 // FP64 rounds use rho64(H).
-int fp32_max_h() {
-  static const int v = [] {
-    const char* e = std::getenv("PARAPLAN_FP32_MAX_H");
-    return e != nullptr ? std::atoi(e) : 40;
-  }();
-  return v;
-}
 // FP64 windows: class 0/1 anchors (terminal cost) by the horizon; class 2
 // (path length of a reaching rollout, measured FP64 error <= 1.1e-13)
 double rho64(int H) { return H <= 60 ? 1e-9 : 1e-6; }
@@ -207,6 +200,7 @@ void run_round_launch(pp_handle* h, uint64_t t, int iter, int r0, int rc, const 
     a.refine_grid = refine_grid(h);
     a.sel_rho = fp64 ? rho64(h->cfg.H) : h->sel_rho;
     a.sel_rho2 = fp64 ? kRho64Reached : h->sel_rho;
+    a.rho2_by_tgoal = fp64 ? 0 : 1;
     a.sel_alpha = fp64 ? 1e-13 : 1e-6;
   }
 
@@ -541,13 +535,15 @@ void certify_round(pp_handle* h, ppdev::RoundArgs& a, uint64_t t, int iter, int 
     }
   }
   const double alpha = a.sel_alpha;
-  const auto rho_of = [&](int cls) { return cls == 2 ? a.sel_rho2 : a.sel_rho; };
+  const auto rho_of = [&](int cls, int t_goal) {
+    return cls != 2 ? a.sel_rho : (a.rho2_by_tgoal ? ppdev::rho2_fp32(a.sel_rho2, t_goal) : a.sel_rho2);
+  };
   const char* hres = static_cast<const char*>(h->h_round.p);
   std::vector<ppdev::SelBound> bound(rc);
   auto set_bound = [&](int r, int cls, int t_goal, double cost) {
     bound[r].cls = cls;
     bound[r].t_goal = cls == 2 ? t_goal : 0;
-    bound[r].thr = cost * (1.0 + rho_of(cls)) + alpha;  // as select_kernel (no contraction)
+    bound[r].thr = cost * (1.0 + rho_of(cls, t_goal)) + alpha;  // as select_kernel
   };
   if (shard_mode == 1) {
     // the packed global winners the select kernel anchored on (keypack.h)
@@ -797,7 +793,7 @@ void certify_round(pp_handle* h, ppdev::RoundArgs& a, uint64_t t, int iter, int 
       if (certified[r]) continue;
       const ppdev::SelBound& bd = bound[r];
       const XBest& e = gbest[r];
-      const double rho = rho_of(bd.cls);
+      const double rho = rho_of(bd.cls, bd.t_goal);
       const double slack = 0.5 * (rho * bd.thr + alpha);
       bool ok = false;
       if (e.cls >= 0) {
