@@ -71,6 +71,10 @@ __device__ __forceinline__ int advance(Lane<Real>& L, const Net& net, const Cons
   const bool reached = gm >= Real(0);
   // a narrow miss might reach in exact arithmetic (a better outcome)
   narrow |= !reached & (gm > -band);
+  // state 0 is every candidate's (theta plays no part before the first
+  // step): its verdicts cannot order candidates, and the host decides them
+  // exactly (host_stops_at_state0), so they are never flags
+  narrow &= L.h > 0;
   L.mstep = narrow ? min(L.mstep, static_cast<uint32_t>(L.h)) : L.mstep;
   const int cls = hit ? 0 : (reached ? 2 : (L.h == H ? 1 : -1));
 
