@@ -215,6 +215,7 @@ void pp_destroy(pp_handle* h) {
     b->release();
   }
   for (HostBuf* b : {&h->h_field, &h->h_params, &h->h_round, &h->h_bound, &h->h_movers,
+                     &h->h_listkeys,
                      &h->h_field64}) {
     b->release();
   }

@@ -349,7 +349,7 @@ struct pp_handle {
   ppcapi::DevBuf d_field, d_params, d_round, d_tiles, d_samples, d_scratch, d_injected, d_theta, d_skeys,
       d_sel, d_bound, d_movers, d_bin, d_selmore, d_reflist, d_listkeys, d_listout;
   int sel_cap = 1 << 16;  // selection capacity of this handle (kSelCap, grown on overflow)
-  ppcapi::HostBuf h_field, h_params, h_round, h_bound, h_movers;
+  ppcapi::HostBuf h_field, h_params, h_round, h_bound, h_movers, h_listkeys;
 
   // near-tie re-ranking (PlannerConfig::refine): needs the host snapshot
   bool rerank = true;

@@ -395,8 +395,9 @@ void eval_list_fp64(pp_handle* h, const ppdev::RoundArgs& a, int64_t n, int64_t 
      "list generator launch");
   ck(static_cast<cudaError_t>(ppdev::launch_rollout_f64(h->kind, L, h->stream)),
      "list rollout launch");
-  std::vector<ppdev::SKey> keys(static_cast<size_t>(n));
-  ck(cudaMemcpyAsync(keys.data(), h->d_listkeys.p, sizeof(ppdev::SKey) * keys.size(),
+  h->h_listkeys.reserve(sizeof(ppdev::SKey) * std::max<size_t>(n, h->sel_cap), "pinned list keys");
+  const ppdev::SKey* keys = static_cast<const ppdev::SKey*>(h->h_listkeys.p);
+  ck(cudaMemcpyAsync(h->h_listkeys.p, h->d_listkeys.p, sizeof(ppdev::SKey) * n,
                      cudaMemcpyDeviceToHost, h->stream),
      "list keys D2H");
   ck(cudaStreamSynchronize(h->stream), "list round");
@@ -659,14 +660,45 @@ void certify_round(pp_handle* h, ppdev::RoundArgs& a, uint64_t t, int iter, int 
                       cudaMemcpyDeviceToHost),
            "selection D2H");
       }
+      list.reserve(n_sel);
       for (uint32_t i = 0; i < n_sel; ++i) {
+        if (known.empty()) {
+          list.push_back(sl[i]);
+          continue;
+        }
         const auto it = std::lower_bound(known.begin(), known.end(), sl[i], by_index);
         if (it == known.end() || it->first != sl[i]) list.push_back(sl[i]);
       }
-      std::sort(list.begin(), list.end());
-      list.erase(std::unique(list.begin(), list.end()), list.end());
+      // the device appends in no particular order; a wide window is ordered
+      // after its FP64 pass, on the members it keeps
+      if (list.size() <= static_cast<size_t>(host_max())) std::sort(list.begin(), list.end());
     }
     h->timing.refined += static_cast<int32_t>(list.size());
+    if (trace_level() >= 3 && !list.empty() && !fp64) {  // window composition
+      std::vector<ppdev::SKey32> ks(list.size());
+      for (size_t i = 0; i < list.size(); ++i) {
+        ck(cudaMemcpy(&ks[i], static_cast<const ppdev::SKey32*>(a.skeys) + list[i],
+                      sizeof(ppdev::SKey32), cudaMemcpyDeviceToHost),
+           "trace D2H");
+        if (i >= 20000) break;
+      }
+      const size_t m = std::min<size_t>(list.size(), 20001);
+      size_t flagged = 0, incost = 0, ms_hist[4] = {0, 0, 0, 0};
+      for (size_t i = 0; i < m; ++i) {
+        const int r = static_cast<int>(list[i] / count);
+        const uint32_t ms = ppdev::meta_mstep(ks[i].meta);
+        if (ms != ppdev::kNoStep) {
+          ++flagged;
+          ms_hist[std::min<uint32_t>(ms, 3)]++;
+        }
+        if (ppdev::meta_cls(ks[i].meta) == bound[r].cls && ks[i].cost <= bound[r].thr) ++incost;
+      }
+      std::fprintf(stderr,
+                   "[paraplan]   window %zu (sampled %zu): anchor cls %d t_goal %d thr %.9g; "
+                   "flagged %zu (mstep 0/1/2/3+: %zu %zu %zu %zu), within thr %zu\n",
+                   list.size(), m, bound[0].cls, bound[0].t_goal, bound[0].thr, flagged, ms_hist[0],
+                   ms_hist[1], ms_hist[2], ms_hist[3], incost);
+    }
     std::vector<Exact> got(list.size());
     if (list.size() <= static_cast<size_t>(host_max())) {
       const int base = take_slots(list.size());
@@ -709,28 +741,73 @@ void certify_round(pp_handle* h, ppdev::RoundArgs& a, uint64_t t, int iter, int 
                        dev[i].cls == 2 ? -dev[i].k2 : -dev[i].k1, dev[i].k1, dev[i].k2, -1};
         const int r = dev[i].restart;
         if (best[r] < 0 || key_better({got[i].cls, got[i].k1, got[i].k2},
-                                      {got[best[r]].cls, got[best[r]].k1, got[best[r]].k2})) {
+                                      {got[best[r]].cls, got[best[r]].k1, got[best[r]].k2}) ||
+            (!key_better({got[best[r]].cls, got[best[r]].k1, got[best[r]].k2},
+                         {got[i].cls, got[i].k1, got[i].k2}) &&
+             list[i] < list[best[r]])) {
           best[r] = static_cast<int>(i);
         }
       }
-      std::vector<int> ties;
-      for (size_t i = 0; i < dev.size(); ++i) {
-        const Exact& b = got[best[dev[i].restart]];
-        // two FP64 keys' error bounds
-        const double tol = b.cls == 2 ? kRho64Reached : rho64(h->cfg.H);
-        // FP64 near-ties of the best, and every member whose FP64 verdict
-        // came within the FP64 margin of flipping (it may rise a class)
-        if (flagged[i] ||
-            (got[i].cls == b.cls && std::abs(got[i].k1 - b.k1) <= tol * std::max(1.0, std::abs(b.k1)) &&
-             std::abs(got[i].k2 - b.k2) <= tol * std::max(1.0, std::abs(b.k2)))) {
-          ties.push_back(static_cast<int>(i));
+      // The members to evaluate exactly: the FP64 near-ties of each
+      // restart's best, and every member whose FP64 verdict came within the
+      // FP64 margin of flipping (it may rise a class). The rest are worse
+      // than the best by more than two FP64 error bounds, so exactly worse
+      // too, and are dropped. Near-ties whose FP64 keys are bitwise equal
+      // (e.g. rollouts whose steering saturates identically: the same
+      // trajectory) are one group: its lowest index is evaluated and the
+      // others, identical rollouts that lose the index tie-break, dropped.
+      std::vector<int> keep;
+      {
+        struct GroupKey {
+          int r, cls;
+          double k1, k2;
+          bool operator<(const GroupKey& o) const {
+            if (r != o.r) return r < o.r;
+            if (cls != o.cls) return cls < o.cls;
+            if (k1 != o.k1) return k1 < o.k1;
+            return k2 < o.k2;
+          }
+        };
+        std::map<GroupKey, int> groups;  // -> member of the lowest index
+        for (size_t i = 0; i < dev.size(); ++i) {
+          const Exact& b = got[best[dev[i].restart]];
+          const double tol = b.cls == 2 ? kRho64Reached : rho64(h->cfg.H);
+          if (flagged[i]) {
+            keep.push_back(static_cast<int>(i));
+            continue;
+          }
+          if (got[i].cls == b.cls &&
+              std::abs(got[i].k1 - b.k1) <= tol * std::max(1.0, std::abs(b.k1)) &&
+              std::abs(got[i].k2 - b.k2) <= tol * std::max(1.0, std::abs(b.k2))) {
+            const GroupKey g{dev[i].restart, got[i].cls, got[i].k1, got[i].k2};
+            auto it = groups.find(g);
+            if (it == groups.end()) {
+              groups.emplace(g, static_cast<int>(i));
+            } else if (list[i] < list[it->second]) {
+              it->second = static_cast<int>(i);
+            }
+          }
         }
+        for (const auto& kv : groups) keep.push_back(kv.second);
+        std::sort(keep.begin(), keep.end(), [&](int x, int y) { return list[x] < list[y]; });
+        keep.erase(std::unique(keep.begin(), keep.end()), keep.end());
       }
-      const int base = take_slots(ties.size());
-      std::lock_guard<std::mutex> turn(shared_pool().mu);
-      h->pool->run(static_cast<int>(ties.size()), [&](int j) {
-        got[ties[j]] = exact_of(list[ties[j]], base < 0 ? -1 : base + j);
-      });
+      std::vector<int64_t> kept_list(keep.size());
+      for (size_t j = 0; j < keep.size(); ++j) kept_list[j] = list[keep[j]];
+      std::vector<Exact> kept_got(keep.size());
+      const int base = take_slots(keep.size());
+      {
+        std::lock_guard<std::mutex> turn(shared_pool().mu);
+        h->pool->run(static_cast<int>(keep.size()), [&](int j) {
+          kept_got[j] = exact_of(kept_list[j], base < 0 ? -1 : base + j);
+        });
+      }
+      if (trace_on()) {
+        std::fprintf(stderr, "[paraplan]   wide window %zu: %zu FP64 near-tie groups / flags to "
+                             "the host\n", list.size(), keep.size());
+      }
+      list.swap(kept_list);
+      got.swap(kept_got);
     }
     phase("exact");
     {  // merge the (sorted, new) list into the known keys

@@ -52,11 +52,13 @@ void fill_consts(const ppdev::RoundArgs& a, ppdev::ConstsT<Real>* k) {
   k->qpad = Real(a.grid_g / 8.0);
   // a discrete verdict whose margin is below this may flip under rounding
   k->dmarg = sizeof(Real) == sizeof(float) ? Real(a.dmarg32) : Real(1e-9);
-  // twice the largest relative drift measured over a rollout (FP32 2.1e-5 at
-  // H=200, FP64 1.1e-13; profiles/r2_error_model*.json); short FP32
+  // the relative drift of the state after h steps, bounded like a class-2
+  // window's rho (rho2_fp32: 1e-3 (h / 150)^2, at least 2e-6; >= 8x the
+  // measured path error at every h; FP64: 1.1e-13 measured); short FP32
   // horizons keep the fixed band (their drift stays below it)
-  k->dmarg_rel = sizeof(Real) == sizeof(float) ? Real(a.H > fp32_max_h() ? 4e-5 : 0.0)
+  k->dmarg_rel = sizeof(Real) == sizeof(float) ? Real(a.H > fp32_max_h() ? 1e-3 : 0.0)
                                                : Real(1e-12);
+  k->dmarg_floor = sizeof(Real) == sizeof(float) ? Real(2e-6) : Real(1e-12);
   k->bcx = Real(0.5 * (a.fe - a.re));
   k->bhx = Real(0.5 * (a.fe + a.re));
   k->inv_wb = Real(1.0 / a.wheelbase);

@@ -100,6 +100,7 @@ struct ConstsT {
   Real inv_wb;          // 1 / wheelbase (FP32 path multiplies)
   double wb_d;          // wheelbase (FP64 path divides, src/dynamics.cpp:52-55)
   int32_t tan_small;    // delta_max <= pi/4: tan by polynomial ratio (FP32)
+  Real dmarg_floor;     // the band's relative drift is at least this
   Real dmarg_rel;       // + this x the path so far: the flag band widens with the distance
                         // travelled (the measured relative drift of a rollout's state)
   int32_t flag_miss;    // several restarts: narrow collision MISSES are marginal too

@@ -49,8 +49,13 @@ __device__ __forceinline__ int advance(Lane<Real>& L, const Net& net, const Cons
   L.ephi = M<Real>::wrap(K.gphi - L.phi);
   bool hit = false;
   // the flag band: the base margin plus the drift the state may have
-  // accumulated over the path so far
-  const Real band = K.dmarg + K.dmarg_rel * L.path;
+  // accumulated over the path so far, which grows with the state index like
+  // the measured relative path error (rho2_fp32's envelope)
+  Real band = K.dmarg;
+  if (K.dmarg_rel != Real(0)) {
+    const Real f = static_cast<Real>(L.h) * Real(1.0 / 150.0);
+    band += L.path * fmax(K.dmarg_floor, K.dmarg_rel * fmin(f * f, Real(1)));
+  }
   bool narrow = false;
   if (f.Ns + f.Nd > 0) {
     // a lane may stop at a hit whose margin is too large to flip
