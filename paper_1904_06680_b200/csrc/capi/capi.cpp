@@ -69,6 +69,16 @@ void prewarm(pp_handle* h) {
       if (s64.refill) h->d_theta.reserve(total * s64.theta_elem * sizeof(double), "theta buffer");
       h->d_skeys.reserve(total * sizeof(ppdev::SKey), "sample keys");
     }
+    // selection buffers for a window of the whole round (up to kSelMax): a
+    // closed loop's near-goal ticks select most of a round, and growing
+    // pinned and device buffers mid-tick cost tens of ms
+    if (h->rerank) {
+      ppdev::RoundArgs scratch{};
+      const int cap = static_cast<int>(std::min<size_t>(total, kSelMax));
+      grow_selection(h, scratch, std::max(cap, kSelCap));
+      h->d_listkeys.reserve(sizeof(ppdev::SKey) * h->sel_cap, "list keys");
+      h->h_listkeys.reserve(sizeof(ppdev::SKey) * h->sel_cap, "pinned list keys");
+    }
   } catch (...) {
     cudaGetLastError();
   }

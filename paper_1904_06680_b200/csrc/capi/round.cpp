@@ -768,7 +768,22 @@ void certify_round(pp_handle* h, ppdev::RoundArgs& a, uint64_t t, int iter, int 
             return k2 < o.k2;
           }
         };
-        std::map<GroupKey, int> groups;  // -> member of the lowest index
+        struct GroupHash {
+          size_t operator()(const GroupKey& g) const {
+            uint64_t a, b;
+            std::memcpy(&a, &g.k1, 8);
+            std::memcpy(&b, &g.k2, 8);
+            return std::hash<uint64_t>()(a * 0x9E3779B97F4A7C15ull ^ b ^
+                                         (static_cast<uint64_t>(g.r) << 3 | g.cls));
+          }
+        };
+        struct GroupEq {
+          bool operator()(const GroupKey& x, const GroupKey& y) const {
+            return x.r == y.r && x.cls == y.cls && x.k1 == y.k1 && x.k2 == y.k2;
+          }
+        };
+        // -> member of the lowest index
+        std::unordered_map<GroupKey, int, GroupHash, GroupEq> groups;
         for (size_t i = 0; i < dev.size(); ++i) {
           const Exact& b = got[best[dev[i].restart]];
           const double tol = b.cls == 2 ? kRho64Reached : rho64(h->cfg.H);
