@@ -66,6 +66,7 @@ int host_max() {
 // (path length of a reaching rollout, measured FP64 error <= 1.1e-13)
 double rho64(int H) { return H <= 60 ? 1e-9 : 1e-6; }
 constexpr double kRho64Reached = 1e-11;
+constexpr double kRho64ReachedFloor = 2e-14;
 
 // Occupancy of the rollout kernel for (precision, staged field size, grid
 // mode), queried once per handle.
@@ -200,7 +201,8 @@ void run_round_launch(pp_handle* h, uint64_t t, int iter, int r0, int rc, const 
     a.refine_grid = refine_grid(h);
     a.sel_rho = fp64 ? rho64(h->cfg.H) : h->sel_rho;
     a.sel_rho2 = fp64 ? kRho64Reached : h->sel_rho;
-    a.rho2_by_tgoal = fp64 ? 0 : 1;
+    a.sel_rho2_floor = fp64 ? kRho64ReachedFloor : 2e-6;
+    a.rho2_by_tgoal = 1;
     a.sel_alpha = fp64 ? 1e-13 : 1e-6;
   }
 
@@ -537,7 +539,9 @@ void certify_round(pp_handle* h, ppdev::RoundArgs& a, uint64_t t, int iter, int 
   }
   const double alpha = a.sel_alpha;
   const auto rho_of = [&](int cls, int t_goal) {
-    return cls != 2 ? a.sel_rho : (a.rho2_by_tgoal ? ppdev::rho2_fp32(a.sel_rho2, t_goal) : a.sel_rho2);
+    return cls != 2 ? a.sel_rho
+                    : (a.rho2_by_tgoal ? ppdev::rho2_of(a.sel_rho2, a.sel_rho2_floor, t_goal)
+                                       : a.sel_rho2);
   };
   const char* hres = static_cast<const char*>(h->h_round.p);
   std::vector<ppdev::SelBound> bound(rc);
@@ -786,7 +790,9 @@ void certify_round(pp_handle* h, ppdev::RoundArgs& a, uint64_t t, int iter, int 
         std::unordered_map<GroupKey, int, GroupHash, GroupEq> groups;
         for (size_t i = 0; i < dev.size(); ++i) {
           const Exact& b = got[best[dev[i].restart]];
-          const double tol = b.cls == 2 ? kRho64Reached : rho64(h->cfg.H);
+          const double tol =
+              b.cls == 2 ? ppdev::rho2_of(kRho64Reached, kRho64ReachedFloor, b.t_goal)
+                         : rho64(h->cfg.H);
           if (flagged[i]) {
             keep.push_back(static_cast<int>(i));
             continue;

@@ -43,16 +43,17 @@ PP_HD int meta_tgoal(uint32_t m) { return static_cast<int>((m >> 2) & 0x7fffu); 
 PP_HD uint32_t meta_mstep(uint32_t m) { return m >> 17; }
 PP_HD bool meta_flagged(uint32_t m) { return (m >> 17) != kNoStep; }
 
-// rho of an FP32 window anchored on a class-2 candidate reaching at t_goal
-// T. The relative error of a reaching rollout's path grows with T (measured,
-// profiles/r2_error_model*.json: 1.6e-7 at T <= 6, 3e-7 at T = 20-40, 1.3e-6
-// at T = 78, 2.1e-5 at T = 125): base (T / 150)^2, at least 2e-6 -- >= 8x the
-// measured error at every T. Host and device evaluate it alike (no FMA
-// contraction in either translation unit).
-PP_HD double rho2_fp32(double base, int T) {
+// rho of a window anchored on a class-2 candidate reaching at t_goal T. The
+// relative error of a reaching rollout's path grows with T (measured,
+// profiles/r2_error_model*.json; FP32: 1.6e-7 at T <= 6, 3e-7 at T = 20-40,
+// 1.3e-6 at T = 78, 2.1e-5 at T = 125; FP64: <= 1.1e-13): base (T / 150)^2,
+// at least `floor` -- FP32 base 1e-3, floor 2e-6; FP64 base 1e-11, floor
+// 2e-14 -- >= 8x the measured error at every T. Host and device evaluate it
+// alike (no FMA contraction in either translation unit).
+PP_HD double rho2_of(double base, double floor, int T) {
   const double f = static_cast<double>(T) / 150.0;
   const double r = base * (f * f < 1.0 ? f * f : 1.0);
-  return r > 2e-6 ? r : 2e-6;
+  return r > floor ? r : floor;
 }
 struct SKey32 {
   float cost;
@@ -191,7 +192,8 @@ struct RoundArgs {
   int32_t refine_grid;
   double sel_rho, sel_alpha;   // window: cost <= best * (1 + rho) + alpha
   double sel_rho2;             // rho of windows anchored on a class-2 (reached) candidate
-  int32_t rho2_by_tgoal;       // FP32: rho2 grows with the anchor's t_goal (sel_rho2_of)
+  int32_t rho2_by_tgoal;       // rho2 grows with the anchor's t_goal (rho2_of)
+  double sel_rho2_floor;
   // list rounds (the certification's FP64 re-evaluation of a wide window):
   // item i of the round is the flat candidate list[i] (restart-major over
   // list_count candidates per restart) of the round the list came from; the

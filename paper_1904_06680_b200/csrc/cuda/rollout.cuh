@@ -415,7 +415,7 @@ static __global__ void __launch_bounds__(256) select_kernel(const RoundArgs a) {
       bd.cls = u.cls;
       bd.t_goal = u.cls == 2 ? u.t_goal : 0;
       const double rho = u.cls != 2       ? a.sel_rho
-                         : a.rho2_by_tgoal ? rho2_fp32(a.sel_rho2, u.t_goal)
+                         : a.rho2_by_tgoal ? rho2_of(a.sel_rho2, a.sel_rho2_floor, u.t_goal)
                                            : a.sel_rho2;
       bd.thr = static_cast<double>(u.cost) * (1.0 + rho) + a.sel_alpha;
     } else {  // first pass: around the round winner (its best unflagged candidate)
@@ -423,7 +423,7 @@ static __global__ void __launch_bounds__(256) select_kernel(const RoundArgs a) {
       bd.cls = b.cls;
       bd.t_goal = b.cls == 2 ? static_cast<int>(-b.k1) : 0;
       const double rho = b.cls != 2       ? a.sel_rho
-                         : a.rho2_by_tgoal ? rho2_fp32(a.sel_rho2, bd.t_goal)
+                         : a.rho2_by_tgoal ? rho2_of(a.sel_rho2, a.sel_rho2_floor, bd.t_goal)
                                            : a.sel_rho2;
       bd.thr = (b.cls == 2 ? -b.k2 : -b.k1) * (1.0 + rho) + a.sel_alpha;
     }
