@@ -354,10 +354,11 @@ void run_round_launch(pp_handle* h, uint64_t t, int iter, int r0, int rc, const 
 // indices of the round `a`, restart-major over `count` candidates per
 // restart, candidates starting at c0): a list round of the FP64 generator +
 // refill rollout (the FP64 round's own kernels and per-candidate cost, at
-// full occupancy), keys only. dev[i] receives member i's FP64 key, flagged[i]
-// whether a discrete FP64 verdict came within the FP64 margin of flipping.
+// full occupancy), keys only. dev[i] receives member i's FP64 key, mstep[i]
+// the earliest state whose FP64 verdict came within the FP64 band of
+// flipping (ppdev::kNoStep: none).
 void eval_list_fp64(pp_handle* h, const ppdev::RoundArgs& a, int64_t n, int64_t count, int64_t c0,
-                    std::vector<ppdev::SelRec>& dev, std::vector<char>& flagged) {
+                    std::vector<ppdev::SelRec>& dev, std::vector<uint32_t>& mstep) {
   ppdev::RoundArgs L = a;
   L.list = static_cast<const int64_t*>(h->d_reflist.p);
   L.list_count = count;
@@ -411,7 +412,7 @@ void eval_list_fp64(pp_handle* h, const ppdev::RoundArgs& a, int64_t n, int64_t 
     const int tg = ppdev::meta_tgoal(k.meta);
     d.k1 = d.cls == 2 ? -static_cast<double>(tg) : -k.cost;
     d.k2 = d.cls == 2 ? -k.cost : 0.0;
-    flagged[static_cast<size_t>(i)] = ppdev::meta_flagged(k.meta);
+    mstep[static_cast<size_t>(i)] = ppdev::meta_mstep(k.meta);
   }
 }
 
@@ -717,9 +718,9 @@ void certify_round(pp_handle* h, ppdev::RoundArgs& a, uint64_t t, int iter, int 
                          cudaMemcpyHostToDevice, h->stream),
          "refine list H2D");
       std::vector<ppdev::SelRec> dev(list.size());
-      std::vector<char> flagged(list.size(), 0);
+      std::vector<uint32_t> mstep(list.size(), ppdev::kNoStep);
       if (launch_shape(h, true, 0, 0).refill) {
-        eval_list_fp64(h, a, static_cast<int64_t>(list.size()), count, c0, dev, flagged);
+        eval_list_fp64(h, a, static_cast<int64_t>(list.size()), count, c0, dev, mstep);
         for (size_t i = 0; i < list.size(); ++i) {
           dev[i].restart = static_cast<int32_t>(list[i] / count);
           dev[i].cand = static_cast<int32_t>(c0 + (list[i] - dev[i].restart * count));
@@ -760,11 +761,14 @@ void certify_round(pp_handle* h, ppdev::RoundArgs& a, uint64_t t, int iter, int 
       // (e.g. rollouts whose steering saturates identically: the same
       // trajectory) are one group: its lowest index is evaluated and the
       // others, identical rollouts that lose the index tie-break, dropped.
+      // Flagged members group the same way, by key and flagged state.
       std::vector<int> keep;
+      size_t n_flagged = 0;
       {
         struct GroupKey {
           int r, cls;
           double k1, k2;
+          uint32_t ms;
           bool operator<(const GroupKey& o) const {
             if (r != o.r) return r < o.r;
             if (cls != o.cls) return cls < o.cls;
@@ -778,12 +782,12 @@ void certify_round(pp_handle* h, ppdev::RoundArgs& a, uint64_t t, int iter, int 
             std::memcpy(&a, &g.k1, 8);
             std::memcpy(&b, &g.k2, 8);
             return std::hash<uint64_t>()(a * 0x9E3779B97F4A7C15ull ^ b ^
-                                         (static_cast<uint64_t>(g.r) << 3 | g.cls));
+                                         (static_cast<uint64_t>(g.r) << 20 | g.ms << 2 | g.cls));
           }
         };
         struct GroupEq {
           bool operator()(const GroupKey& x, const GroupKey& y) const {
-            return x.r == y.r && x.cls == y.cls && x.k1 == y.k1 && x.k2 == y.k2;
+            return x.r == y.r && x.cls == y.cls && x.k1 == y.k1 && x.k2 == y.k2 && x.ms == y.ms;
           }
         };
         // -> member of the lowest index
@@ -793,14 +797,13 @@ void certify_round(pp_handle* h, ppdev::RoundArgs& a, uint64_t t, int iter, int 
           const double tol =
               b.cls == 2 ? ppdev::rho2_of(kRho64Reached, kRho64ReachedFloor, b.t_goal)
                          : rho64(h->cfg.H);
-          if (flagged[i]) {
-            keep.push_back(static_cast<int>(i));
-            continue;
-          }
-          if (got[i].cls == b.cls &&
-              std::abs(got[i].k1 - b.k1) <= tol * std::max(1.0, std::abs(b.k1)) &&
-              std::abs(got[i].k2 - b.k2) <= tol * std::max(1.0, std::abs(b.k2))) {
-            const GroupKey g{dev[i].restart, got[i].cls, got[i].k1, got[i].k2};
+          const bool flag = mstep[i] != ppdev::kNoStep;
+          n_flagged += flag ? 1 : 0;
+          if (flag || (got[i].cls == b.cls &&
+                       std::abs(got[i].k1 - b.k1) <= tol * std::max(1.0, std::abs(b.k1)) &&
+                       std::abs(got[i].k2 - b.k2) <= tol * std::max(1.0, std::abs(b.k2)))) {
+            const GroupKey g{dev[i].restart, got[i].cls, got[i].k1, got[i].k2,
+                             flag ? mstep[i] : ppdev::kNoStep};
             auto it = groups.find(g);
             if (it == groups.end()) {
               groups.emplace(g, static_cast<int>(i));
@@ -824,8 +827,10 @@ void certify_round(pp_handle* h, ppdev::RoundArgs& a, uint64_t t, int iter, int 
         });
       }
       if (trace_on()) {
-        std::fprintf(stderr, "[paraplan]   wide window %zu: %zu FP64 near-tie groups / flags to "
-                             "the host\n", list.size(), keep.size());
+        std::fprintf(stderr, "[paraplan]   wide window %zu: %zu to the host (%zu FP64-flagged, "
+                             "the rest FP64 near-tie groups; best cls %d t_goal %d)\n",
+                     list.size(), keep.size(), n_flagged, best.empty() ? -1 : got[best[0]].cls,
+                     best.empty() ? -1 : got[best[0]].t_goal);
       }
       list.swap(kept_list);
       got.swap(kept_got);
