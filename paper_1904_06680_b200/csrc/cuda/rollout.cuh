@@ -58,6 +58,31 @@ constexpr int rec_width(int P) {
 template <typename Real>
 using Vec16 = typename std::conditional<sizeof(Real) == 4, float4, double2>::type;
 
+// One candidate's record: theta of restart r, local candidate `local`, and
+// its first action, written to record slot s.
+template <typename Real, class Net>
+__device__ __forceinline__ void generate_one(const RoundArgs& a, const Real s0[5], int r,
+                                             int64_t local, int64_t s) {
+  constexpr int P = Net::P;
+  constexpr int W = rec_width<Real>(P);
+  constexpr int V = W * static_cast<int>(sizeof(Real)) / 16;
+  Vec16<Real>* recs = static_cast<Vec16<Real>*>(a.theta_buf);
+  union {
+    Real v[W];
+    Vec16<Real> q[V];
+  } rec;
+  draw_theta<Real, P>(a, __ldg(a.key_prefix + r), a.injected ? local : a.cand_begin + local, P,
+                      [&](int i, Real v) { rec.v[i] = v; });
+  Net n;
+#pragma unroll
+  for (int i = 0; i < P; ++i) n.w[i] = rec.v[i];
+  n.eval(s0, rec.v[P], rec.v[P + 1]);  // first action (src/planner.cpp:130-132)
+#pragma unroll
+  for (int i = P + 2; i < W; ++i) rec.v[i] = Real(0);
+#pragma unroll
+  for (int j = 0; j < V; ++j) recs[s * V + j] = rec.q[j];
+}
+
 template <typename Real, class Net>
 __global__ void __launch_bounds__(256, PARAPLAN_GEN_MINB) generate_kernel(const RoundArgs a) {
   constexpr int P = Net::P;
@@ -66,6 +91,27 @@ __global__ void __launch_bounds__(256, PARAPLAN_GEN_MINB) generate_kernel(const 
   const Consts<Real>& K = consts_of<Real>(a);
   Real s0[5];
   start_features(K, s0);
+  if (a.overlap) {
+    // persistent warps, one 32-candidate batch each at a time, in batch
+    // order (the rollout claims batches in that order); the rollout grid
+    // may launch now and co-reside
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    const int lane = static_cast<int>(threadIdx.x & 31u);
+    const int n_warps = static_cast<int>((gridDim.x * blockDim.x) >> 5);
+    for (int b = static_cast<int>((blockIdx.x * blockDim.x + threadIdx.x) >> 5); b < a.n_tiles;
+         b += n_warps) {
+      const int r = b / a.tiles_per_restart;
+      const int64_t c = static_cast<int64_t>(b - r * a.tiles_per_restart) * 32 + lane;
+      if (c < a.count) generate_one<Real, Net>(a, s0, r, c, static_cast<int64_t>(r) * a.count + c);
+      __syncwarp();
+      if (lane == 0) {
+        __threadfence();  // the batch's records before its flag
+        asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a.ready + b), "r"(a.epoch)
+                     : "memory");
+      }
+    }
+    return;
+  }
   Vec16<Real>* recs = static_cast<Vec16<Real>*>(a.theta_buf);
   const int64_t total = a.count * a.restart_count;
   for (int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; s < total;
@@ -78,21 +124,9 @@ __global__ void __launch_bounds__(256, PARAPLAN_GEN_MINB) generate_kernel(const 
                       ? static_cast<int>(static_cast<uint32_t>(flat) / static_cast<uint32_t>(cnt))
                       : static_cast<int>(flat / cnt);
     const int64_t local = flat - static_cast<int64_t>(r) * cnt;
-    union {
-      Real v[W];
-      Vec16<Real> q[V];
-    } rec;
-    draw_theta<Real, P>(a, __ldg(a.key_prefix + r), a.injected ? local : a.cand_begin + local, P,
-                        [&](int i, Real v) { rec.v[i] = v; });
-    Net n;
-#pragma unroll
-    for (int i = 0; i < P; ++i) n.w[i] = rec.v[i];
-    n.eval(s0, rec.v[P], rec.v[P + 1]);  // first action (src/planner.cpp:130-132)
-#pragma unroll
-    for (int i = P + 2; i < W; ++i) rec.v[i] = Real(0);
-#pragma unroll
-    for (int j = 0; j < V; ++j) recs[s * V + j] = rec.q[j];
+    generate_one<Real, Net>(a, s0, r, local, s);
   }
+  (void)recs;
 }
 
 // ------------------------------------------------------ refill kernel ----
@@ -121,7 +155,8 @@ __global__ void __launch_bounds__(kBlock, refill_min_blocks<Real, Net>())
     (&table[0][0])[i] = empty_key();
   }
   const Field<Real> f = stage_field<Real, kGrid>(a, smem_raw);
-  wait_prior_grid();  // the generator's theta records
+  // the generator's theta records: all of them, or (overlap) batch by batch
+  if (!a.overlap) wait_prior_grid();
 
   const int bpr = a.tiles_per_restart;  // 32-candidate batches per restart
   const unsigned total_batches = static_cast<unsigned>(a.n_tiles);
@@ -157,6 +192,18 @@ __global__ void __launch_bounds__(kBlock, refill_min_blocks<Real, Net>())
         if (b >= total_batches) {
           exhausted = true;
         } else {
+          if (a.overlap) {  // the overlapped generator's flag of batch b
+            if (lane == 0) {
+              for (;;) {
+                uint32_t e;
+                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(e) : "l"(a.ready + b)
+                             : "memory");
+                if (e == a.epoch) break;
+                __nanosleep(64);
+              }
+            }
+            __syncwarp();
+          }
           q_r = static_cast<int>(b) / bpr;
           q_c0 = (static_cast<int>(b) - q_r * bpr) * 32;
           const int64_t left = a.count - q_c0;
@@ -177,7 +224,7 @@ __global__ void __launch_bounds__(kBlock, refill_min_blocks<Real, Net>())
             Vec16<Real> q[V];
           } rec;
 #pragma unroll
-          for (int j = 0; j < V; ++j) rec.q[j] = __ldg(recs + sidx * V + j);
+          for (int j = 0; j < V; ++j) rec.q[j] = __ldcg(recs + sidx * V + j);
 #pragma unroll
           for (int i = 0; i < P; ++i) net.w[i] = rec.v[i];
           L.start(K, rec.v[P], rec.v[P + 1]);
@@ -618,6 +665,11 @@ template <typename Real, class Net>
 int launch_generate_impl(const RoundArgs& a, void* stream) {
   if constexpr (Net::kP > 0) {
     if (refill_schedule<Net>()) {
+      if (a.overlap) {  // persistent: one CTA of 4 warps per SM, beside the rollout's
+        generate_kernel<Real, Net>
+            <<<std::max(a.sms, 1), 128, 0, static_cast<cudaStream_t>(stream)>>>(a);
+        return static_cast<int>(cudaGetLastError());
+      }
       const int64_t total = a.count * a.restart_count;
       const int gen_blocks = static_cast<int>((total + 255) / 256);
       generate_kernel<Real, Net><<<gen_blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(a);
