@@ -221,7 +221,7 @@ void pp_destroy(pp_handle* h) {
   for (DevBuf* b : {&h->d_field, &h->d_params, &h->d_round, &h->d_tiles, &h->d_movers, &h->d_bin,
                     &h->d_samples, &h->d_scratch, &h->d_injected, &h->d_theta, &h->d_skeys,
                     &h->d_sel, &h->d_bound, &h->d_field64, &h->d_selmore, &h->d_reflist,
-                    &h->d_listkeys, &h->d_listout, &h->d_ready}) {
+                    &h->d_listkeys, &h->d_listout}) {
     b->release();
   }
   for (HostBuf* b : {&h->h_field, &h->h_params, &h->h_round, &h->h_bound, &h->h_movers,

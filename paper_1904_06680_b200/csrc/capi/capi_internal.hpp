@@ -347,8 +347,7 @@ struct pp_handle {
   cudaEvent_t ev_field = nullptr;
   bool field_via_side = false, field_event = false;
   ppcapi::DevBuf d_field, d_params, d_round, d_tiles, d_samples, d_scratch, d_injected, d_theta, d_skeys,
-      d_sel, d_bound, d_movers, d_bin, d_selmore, d_reflist, d_listkeys, d_listout, d_ready;
-  uint32_t epoch = 0;  // overlapped generator: the round's flag value in d_ready
+      d_sel, d_bound, d_movers, d_bin, d_selmore, d_reflist, d_listkeys, d_listout;
   int sel_cap = 1 << 16;  // selection capacity of this handle (kSelCap, grown on overflow)
   ppcapi::HostBuf h_field, h_params, h_round, h_bound, h_movers, h_listkeys;
 

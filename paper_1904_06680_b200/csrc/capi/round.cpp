@@ -27,18 +27,6 @@ uint64_t key_prefix(uint64_t seed, uint64_t t, uint64_t r, uint64_t i) {
 
 constexpr int ppdev_warps() { return 4; }
 
-// PARAPLAN_OVERLAP=1 runs the generator as a persistent grid beside the
-// rollout (per-batch flags) instead of to completion before it. Off: the
-// measured A/B on B200 (C2, 2^20): 0.437 ms per round overlapped vs 0.287 ms
-// sequential -- the 4 generator warps per SM that fit beside 5 rollout CTAs
-// in the register file issue too slowly, and the rollout waits on them.
-bool overlap_on() {
-  static const bool v = [] {
-    const char* e = std::getenv("PARAPLAN_OVERLAP");
-    return e != nullptr && std::atoi(e) != 0;
-  }();
-  return v;
-}
 
 // Selection buffers of capacity `cap`: the indices beyond the round block's
 // first kSelFirst, the refine kernel's input list and its FP64 keys.
@@ -219,25 +207,6 @@ void run_round_launch(pp_handle* h, uint64_t t, int iter, int r0, int rc, const 
     a.sel_alpha = fp64 ? 1e-13 : 1e-6;
   }
 
-  // Overlapped generator (FP32 refill rounds): the generator runs as a
-  // persistent grid beside the rollout and flags each batch ready; the
-  // rollout launches at once and waits per batch (rollout.cuh). The batch
-  // tiling is fixed before the generator launch.
-  a.overlap = 0;
-  if (shape0.refill && !fp64 && overlap_on()) {
-    const int64_t tpr = (count + 31) / 32;
-    if (tpr * rc <= (int64_t{1} << 30)) {
-      a.tiles_per_restart = static_cast<int32_t>(tpr);
-      a.n_tiles = static_cast<int32_t>(tpr * rc);
-      if (h->d_ready.reserve(sizeof(uint32_t) * static_cast<size_t>(a.n_tiles), "batch flags")) {
-        ck(cudaMemsetAsync(h->d_ready.p, 0, h->d_ready.cap, h->stream), "batch flags");
-      }
-      a.ready = static_cast<uint32_t*>(h->d_ready.p);
-      if (++h->epoch == 0) h->epoch = 1;  // 0 is the cleared flag
-      a.epoch = h->epoch;
-      a.overlap = 1;
-    }
-  }
   phase("buffers");
   ck(cudaEventRecord(h->ev0, h->stream), "event");
   ck(static_cast<cudaError_t>(fp64 ? ppdev::launch_generate_f64(h->kind, a, h->stream)
@@ -274,11 +243,9 @@ void run_round_launch(pp_handle* h, uint64_t t, int iter, int r0, int rc, const 
   a.tiles_per_restart = static_cast<int32_t>(tpr64);
   a.n_tiles = static_cast<int32_t>(tpr64 * rc);
   a.block = shape.block;
-  // overlapped: one rollout CTA per SM fewer, so the generator's CTA fits
-  const int grid_cap = a.overlap ? std::max(h->sms, shape.grid - h->sms) : shape.grid;
-  a.grid = std::max(1, std::min(grid_cap, shape.refill ? (a.n_tiles + ppdev_warps() - 1) /
-                                                             ppdev_warps()
-                                                       : a.n_tiles));
+  a.grid = std::max(1, std::min(shape.grid, shape.refill ? (a.n_tiles + ppdev_warps() - 1) /
+                                                               ppdev_warps()
+                                                         : a.n_tiles));
   a.field_smem_bytes = field_smem;
   // tile records (x2 for keys_only: best and best unflagged)
   const size_t n_recs = shape.refill ? 2 * static_cast<size_t>(rc) * std::max(a.grid, h->sms * 4)

@@ -200,14 +200,7 @@ struct RoundArgs {
   // round itself is one "restart" of count = n items, keys_only
   const int64_t* list;
   int64_t list_count;
-  // overlapped generator (refill schedule): the generator is a persistent
-  // grid that lets the rollout launch at once (griddepcontrol
-  // .launch_dependents) and publishes each 32-candidate batch with
-  // ready[batch] = epoch; a rollout warp waits for its batch's flag instead
-  // of the whole generator grid
-  uint32_t* ready;
-  uint32_t epoch;
-  int32_t overlap;
+
   const SelBound* sel_bound;   // null: first pass (window around a.out)
   double dmarg32;              // FP32 marginal threshold (host side, copied into kf)
   int32_t sms;                 // multiprocessors of the device (launch sizing)

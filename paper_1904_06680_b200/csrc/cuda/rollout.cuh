@@ -91,27 +91,6 @@ __global__ void __launch_bounds__(256, PARAPLAN_GEN_MINB) generate_kernel(const 
   const Consts<Real>& K = consts_of<Real>(a);
   Real s0[5];
   start_features(K, s0);
-  if (a.overlap) {
-    // persistent warps, one 32-candidate batch each at a time, in batch
-    // order (the rollout claims batches in that order); the rollout grid
-    // may launch now and co-reside
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    const int lane = static_cast<int>(threadIdx.x & 31u);
-    const int n_warps = static_cast<int>((gridDim.x * blockDim.x) >> 5);
-    for (int b = static_cast<int>((blockIdx.x * blockDim.x + threadIdx.x) >> 5); b < a.n_tiles;
-         b += n_warps) {
-      const int r = b / a.tiles_per_restart;
-      const int64_t c = static_cast<int64_t>(b - r * a.tiles_per_restart) * 32 + lane;
-      if (c < a.count) generate_one<Real, Net>(a, s0, r, c, static_cast<int64_t>(r) * a.count + c);
-      __syncwarp();
-      if (lane == 0) {
-        __threadfence();  // the batch's records before its flag
-        asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a.ready + b), "r"(a.epoch)
-                     : "memory");
-      }
-    }
-    return;
-  }
   Vec16<Real>* recs = static_cast<Vec16<Real>*>(a.theta_buf);
   const int64_t total = a.count * a.restart_count;
   for (int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; s < total;
@@ -155,8 +134,7 @@ __global__ void __launch_bounds__(kBlock, refill_min_blocks<Real, Net>())
     (&table[0][0])[i] = empty_key();
   }
   const Field<Real> f = stage_field<Real, kGrid>(a, smem_raw);
-  // the generator's theta records: all of them, or (overlap) batch by batch
-  if (!a.overlap) wait_prior_grid();
+  wait_prior_grid();  // the generator's theta records
 
   const int bpr = a.tiles_per_restart;  // 32-candidate batches per restart
   const unsigned total_batches = static_cast<unsigned>(a.n_tiles);
@@ -192,18 +170,6 @@ __global__ void __launch_bounds__(kBlock, refill_min_blocks<Real, Net>())
         if (b >= total_batches) {
           exhausted = true;
         } else {
-          if (a.overlap) {  // the overlapped generator's flag of batch b
-            if (lane == 0) {
-              for (;;) {
-                uint32_t e;
-                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(e) : "l"(a.ready + b)
-                             : "memory");
-                if (e == a.epoch) break;
-                __nanosleep(64);
-              }
-            }
-            __syncwarp();
-          }
           q_r = static_cast<int>(b) / bpr;
           q_c0 = (static_cast<int>(b) - q_r * bpr) * 32;
           const int64_t left = a.count - q_c0;
@@ -665,11 +631,6 @@ template <typename Real, class Net>
 int launch_generate_impl(const RoundArgs& a, void* stream) {
   if constexpr (Net::kP > 0) {
     if (refill_schedule<Net>()) {
-      if (a.overlap) {  // persistent: one CTA of 4 warps per SM, beside the rollout's
-        generate_kernel<Real, Net>
-            <<<std::max(a.sms, 1), 128, 0, static_cast<cudaStream_t>(stream)>>>(a);
-        return static_cast<int>(cudaGetLastError());
-      }
       const int64_t total = a.count * a.restart_count;
       const int gen_blocks = static_cast<int>((total + 255) / 256);
       generate_kernel<Real, Net><<<gen_blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(a);
