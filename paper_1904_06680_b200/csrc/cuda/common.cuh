@@ -36,6 +36,9 @@ constexpr int kWarps = kBlock / 32;
 #ifndef PARAPLAN_GEN_MINB
 #define PARAPLAN_GEN_MINB 1  // theta generator: resident CTAs the register cap must allow
 #endif
+#ifndef PARAPLAN_REFILL64_MINB
+#define PARAPLAN_REFILL64_MINB 4  // FP64 [5,2,2]/[5,10,2]: <= 128 registers
+#endif
 #ifndef PARAPLAN_REFILL_MINB
 #define PARAPLAN_REFILL_MINB 6  // <= 85 registers: 6 CTAs (24 warps) per SM, no spills
 #endif
@@ -173,8 +176,17 @@ struct M<double> {
     const double r = remainder(a, kTwoPi);  // exact, identical to glibc
     return r <= -kPi ? r + kTwoPi : r;
   }
-  // true division, as the reference (src/planner.cpp:117-120, 186-189)
-  static __device__ __forceinline__ double ndiv(double a, double d, double) { return a / d; }
+  // the correctly rounded a / d of the reference (src/planner.cpp:117-120,
+  // 186-189) for a constant divisor d with inv = RN(1 / d) (the host's
+  // 1.0 / d): Markstein's correction, q = RN(a inv), r = a - q d exactly by
+  // FMA, RN(q + r inv) = RN(a / d) (no over/underflow in this range). Three
+  // DFMA/DMUL instead of div.rn.f64's iteration and special-case checks; a
+  // zero residual keeps q itself (the sign of a zero quotient)
+  static __device__ __forceinline__ double ndiv(double a, double d, double inv) {
+    const double q = a * inv;
+    const double r = fma(-q, d, a);
+    return r == 0.0 ? q : fma(r, inv, q);
+  }
 };
 
 template <typename Real>

@@ -114,7 +114,7 @@ __global__ void __launch_bounds__(256, PARAPLAN_GEN_MINB) generate_kernel(const 
 template <typename Real, class Net>
 constexpr int refill_min_blocks() {
   return sizeof(Real) == 4 ? (Net::kP <= 24 ? PARAPLAN_REFILL_MINB : (Net::kP <= 100 ? 3 : 2))
-                           : (Net::kP <= 24 ? 4 : 2);
+                           : (Net::kP <= 24 ? PARAPLAN_REFILL64_MINB : 2);
 }
 
 template <typename Real, class Net, int kGrid>
