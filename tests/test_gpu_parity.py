@@ -51,9 +51,11 @@ def check_stats(got, want, precision, min_frac=0.99):
                for k in ("path_length", "terminal_cost")},
             **{f"max_rel_{k}": float(_rel(got[k][same0], want[k][same0]).max(initial=0.0))
                for k in ("path_length", "terminal_cost")})
+    # FP32 discrete flips: measured <= 1 per test (1 of 1024 injected, 1 of
+    # 32768 at C2; profiles/r2_parity_log.jsonl); allowed: that + a margin
     for k in ("reached", "collided", "t_goal", "steps"):
         flips = np.count_nonzero(got[k] != want[k])
-        assert flips <= (0 if precision == 64 else max(1, len(want) // 200)), (k, flips)
+        assert flips <= (0 if precision == 64 else 2 + len(want) // 20000), (k, flips)
     same = (got["collided"] == want["collided"]) & (got["t_goal"] == want["t_goal"]) & \
            (got["steps"] == want["steps"])
     for k in ("path_length", "terminal_cost"):
