@@ -301,8 +301,8 @@ void reset(Binned& b, int rows, double cull) {
 
 Layout layout(const Binned& b, size_t elem) {
   Layout l;
-  l.dpts = align16(2 * elem * b.Ns);
-  l.sst = align16(l.dpts + 2 * elem * static_cast<size_t>(b.Nd) * b.rows);
+  l.dpts = align16(2 * elem * static_cast<size_t>(b.Ns + b.pad_s));
+  l.sst = align16(l.dpts + 2 * elem * static_cast<size_t>(b.Nd + b.pad_d) * b.rows);
   l.dst = align16(l.sst + sizeof(int32_t) * (b.cells() + 1));
   l.sbox = align16(l.dst + sizeof(int32_t) * static_cast<size_t>(b.rows) * (b.cells() + 1));
   l.cst = align16(l.sbox + (b.boxes ? 4 * elem * static_cast<size_t>(b.cells()) : 0));
@@ -482,10 +482,43 @@ void pack(const Binned& b, bool fp64, void* out, bool with_dynamic) {
       }
     });
   };
+  // sentinels: (1e30, 0) -- outside the chassis by ~0.7e30 at any heading
+  // (one of |cos|, |sin| >= 0.7), finite in FP32
+  const auto sentinels = [&](size_t off, int n) {
+    for (int i = 0; i < n; ++i) {
+      if (fp64) {
+        double* d = reinterpret_cast<double*>(base + off) + 2 * i;
+        d[0] = 1e30;
+        d[1] = 0.0;
+      } else {
+        float* f = reinterpret_cast<float*>(base + off) + 2 * i;
+        f[0] = 1e30f;
+        f[1] = 0.0f;
+      }
+    }
+  };
   put(0, b.spts);
+  sentinels(2 * elem * static_cast<size_t>(b.Ns), b.pad_s);
   std::memcpy(base + l.sst, b.sst.data(), b.sst.size() * sizeof(int32_t));
   if (with_dynamic) {
-    put(l.dpts, b.dpts);
+    if (b.pad_d == 0) {
+      put(l.dpts, b.dpts);
+    } else {  // rows of Nd points + pad_d sentinels
+      for (int r = 0; r < b.rows; ++r) {
+        const size_t row = l.dpts + 2 * elem * static_cast<size_t>(r) * (b.Nd + b.pad_d);
+        for (int i = 0; i < b.Nd; ++i) {
+          const double* src = b.dpts.data() + 2 * (static_cast<size_t>(r) * b.Nd + i);
+          if (fp64) {
+            std::memcpy(base + row + 2 * elem * i, src, 2 * sizeof(double));
+          } else {
+            float* f = reinterpret_cast<float*>(base + row) + 2 * i;
+            f[0] = static_cast<float>(src[0]);
+            f[1] = static_cast<float>(src[1]);
+          }
+        }
+        sentinels(row + 2 * elem * static_cast<size_t>(b.Nd), b.pad_d);
+      }
+    }
     std::memcpy(base + l.dst, b.dst.data(), b.dst.size() * sizeof(int32_t));
   }
   if (b.boxes) {

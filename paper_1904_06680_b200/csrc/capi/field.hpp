@@ -48,6 +48,12 @@ struct Binned {
   // image later (overlapped with the device round).
   std::vector<double> dbase;
   bool dyn_deferred = false;
+  // Device image only: sentinel points (far away, never inside the chassis)
+  // after the static part and after each dynamic row, so the single-part
+  // x-bucket scan (kernel kind 3) reads its window's points without a bounds
+  // select: a lane reads past its window into later buckets (outside the
+  // chassis box) or into the sentinels. Set by the upload (finish_field).
+  int pad_s = 0, pad_d = 0;
   int cells() const { return nx * ny; }
   // 0: x-buckets, 1: 2-D cells scanned by column, 2: 2-D cells with boxes
   int mode() const { return boxes ? 2 : (ny > 1 ? 1 : 0); }

@@ -221,6 +221,8 @@ void run_round_launch(pp_handle* h, uint64_t t, int iter, int r0, int rc, const 
     a.n_points = b.n_points;
     a.field_ns = b.field_ns;
     a.field_nd = b.field_nd;
+    a.field_dstride = b.field_dstride;
+    a.field_padded = b.field_padded;
     a.grid_nx = b.grid_nx;
     a.grid_ny = b.grid_ny;
     a.grid_mode = b.grid_mode;
@@ -235,7 +237,8 @@ void run_round_launch(pp_handle* h, uint64_t t, int iter, int r0, int rc, const 
   }
   const int field_smem = (force_fp64 && !h->fp64) ? 0 : h->field_smem_bytes;
   const ppdev::LaunchShape shape = launch_shape(
-      h, fp64, field_smem, ppdev::grid_kind(a.grid_mode, field_smem, a.field_ns, a.field_nd));
+      h, fp64, field_smem, ppdev::grid_kind(a.grid_mode, field_smem, a.field_ns, a.field_nd,
+                                        a.field_padded));
   // refill: 32-candidate batches; lockstep: one tile of `block` candidates
   const int unit = shape.refill ? 32 : shape.block;
   const int64_t tpr64 = (count + unit - 1) / unit;

@@ -70,9 +70,18 @@ void fill_consts(const ppdev::RoundArgs& a, ppdev::ConstsT<Real>* k) {
 // Device image of h->field in the compute precision (one H2D); the FP64 image
 // for the near-tie re-ranking is uploaded only when a round needs it.
 void finish_field(pp_handle* h, ppdev::RoundArgs& a) {
+  {  // single-part x-bucket fields: sentinel padding for kernel kind 3
+    ppfield::Binned& m = h->field;
+    const bool one_part = m.Ns == 0 || m.Nd == 0;
+    const bool pad = m.mode() == 0 && one_part && !m.dyn_deferred;
+    m.pad_s = pad && m.Nd == 0 ? m.Ns : 0;
+    m.pad_d = pad && m.Ns == 0 ? m.Nd : 0;
+  }
   const ppfield::Binned& b = h->field;
   a.field_ns = b.Ns;
   a.field_nd = b.Nd;
+  a.field_dstride = b.Nd + b.pad_d;
+  a.field_padded = (b.pad_s > 0 || b.pad_d > 0) ? 1 : 0;
   a.grid_nx = b.nx;
   a.grid_ny = b.ny;
   a.grid_x0 = b.x0;

@@ -149,6 +149,8 @@ struct RoundArgs {
   // cells, grid_mode 2 only], points in cell order.
   const void* field;
   int32_t field_ns, field_nd;  // static points, dynamic points per row
+  int32_t field_dstride;       // points per dynamic row in the image (Nd + sentinels)
+  int32_t field_padded;        // the image carries sentinels (kernel kind 3 needs them)
   int32_t grid_nx, grid_ny;    // cells (grid_ny == 1: x-buckets)
   int32_t grid_mode;           // 0 x-buckets, 1 2-D by column, 2 2-D with static cell boxes
   int32_t coop;                // 2-D grids: warps with few live lanes scan windows together
@@ -234,9 +236,9 @@ struct LaunchShape {
 #ifndef PARAPLAN_SMEM_FIELD
 #define PARAPLAN_SMEM_FIELD 1
 #endif
-inline int grid_kind(int mode, int field_smem_bytes, int ns, int nd) {
+inline int grid_kind(int mode, int field_smem_bytes, int ns, int nd, int padded = 1) {
 #if PARAPLAN_SMEM_FIELD
-  return mode == 0 && field_smem_bytes > 0 && (ns == 0 || nd == 0) ? 3 : mode;
+  return mode == 0 && field_smem_bytes > 0 && (ns == 0 || nd == 0) && padded ? 3 : mode;
 #else
   return mode;
 #endif

@@ -21,6 +21,7 @@ struct Field {
   const int* cst;                          // per cell: first chunk box
   const typename Vec2T<Real>::type* cbox;  // per chunk: (centre), (half extents)
   int Ns, Nd;
+  int dstride;  // points per dynamic row in the image (Nd + sentinels)
   int ncx, ncy;
   int coop;  // RoundArgs::coop
 };
@@ -34,8 +35,8 @@ __device__ __forceinline__ Field<Real> field_at(const RoundArgs& a, const void* 
                      reinterpret_cast<const int*>(p + l.sst),
                      reinterpret_cast<const int*>(p + l.dst),
                      reinterpret_cast<const R2*>(p + l.sbox), reinterpret_cast<const int*>(p + l.cst),
-                     reinterpret_cast<const R2*>(p + l.cbox), a.field_ns, a.field_nd, a.grid_nx,
-                     a.grid_ny, a.coop};
+                     reinterpret_cast<const R2*>(p + l.cbox), a.field_ns, a.field_nd,
+                     a.field_dstride, a.grid_nx, a.grid_ny, a.coop};
 }
 
 // Inside-margin of one point against the chassis at (x, y, phi):
@@ -82,7 +83,22 @@ __device__ __forceinline__ void scan_part(const typename Vec2T<Real>::type* pts,
                                           int ncy, int cx_lo, int cx_hi, int cy_lo, int cy_hi,
                                           const Consts<Real>& K, Real x, Real y, Real c, Real s,
                                           Real kx, Real ky, Real stop, Real& best) {
-  if constexpr (kGrid == 0 || kGrid == 3) {  // x-buckets: one contiguous range
+  if constexpr (kGrid == 3) {
+    // x-buckets of a sentinel-padded part (field.hpp pad_s / pad_d): every
+    // lane reads `rounds` consecutive points from its window's first. Points
+    // past its window lie in later buckets (outside the chassis box by more
+    // than the pad) or are sentinels, so their margins are negative and the
+    // max is the window's -- no bounds select, immediate-offset loads
+    const int lo = st[cx_lo];
+    const int cnt = st[cx_hi + 1] - lo;
+    const int rounds = __reduce_max_sync(kFull, cnt);
+    const auto* p = pts + lo;
+#pragma unroll 4
+    for (int j = 0; j < rounds; ++j) {
+      const auto m = p[j];
+      best = fmax(best, point_margin<Real>(K, x, y, c, s, kx, ky, m.x, m.y));
+    }
+  } else if constexpr (kGrid == 0) {  // x-buckets: one contiguous range
     const int lo = st[cx_lo];
     const int cnt = st[cx_hi + 1] - lo;
     const int rounds = __reduce_max_sync(kFull, cnt);
@@ -354,7 +370,7 @@ __device__ __forceinline__ Real collide_margin(const Field<Real>& f, const Const
   if constexpr (kGrid == 3) {
     // one part: all points static, or all dynamic (the row of state h)
     const bool dyn = f.Nd > 0;
-    const auto* pts = dyn ? f.dpts + h * f.Nd : f.spts;
+    const auto* pts = dyn ? f.dpts + h * f.dstride : f.spts;
     const int* st = dyn ? f.dst + h * (ncx + 1) : f.sst;
     // a lane whose rollout is over scans nothing (its window would only
     // lengthen the warp's point loop)
@@ -385,7 +401,7 @@ __device__ __forceinline__ Real collide_margin(const Field<Real>& f, const Const
                                                  qc, qs, qkx, qky, lane);
         }
         if (f.Nd > 0) {
-          m = fmax(m, coop_scan_cells<Real>(f.dpts + static_cast<size_t>(qh) * f.Nd,
+          m = fmax(m, coop_scan_cells<Real>(f.dpts + static_cast<size_t>(qh) * f.dstride,
                                             f.dst + static_cast<size_t>(qh) * row_cells, ncy, q0,
                                             q1, r0, r1, K, qx, qy, qc, qs, qkx, qky, lane));
         }
@@ -401,7 +417,7 @@ __device__ __forceinline__ Real collide_margin(const Field<Real>& f, const Const
   for (int part = 0; part < 2; ++part) {
     const bool dyn = part == 1;
     if ((dyn ? f.Nd : f.Ns) == 0) continue;
-    const auto* pts = dyn ? f.dpts + static_cast<size_t>(h) * f.Nd : f.spts;
+    const auto* pts = dyn ? f.dpts + static_cast<size_t>(h) * f.dstride : f.spts;
     const int* st = dyn ? f.dst + static_cast<size_t>(h) * row_cells : f.sst;
     if constexpr (kGrid == 2) {
       if (!dyn) {

@@ -646,7 +646,8 @@ int launch_generate_impl(const RoundArgs& a, void* stream) {
 template <typename Real, class Net>
 int launch_rollout_impl(const RoundArgs& a, void* stream) {
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  auto k = kernel_of<Real, Net>(grid_kind(a.grid_mode, a.field_smem_bytes, a.field_ns, a.field_nd));
+  auto k = kernel_of<Real, Net>(grid_kind(a.grid_mode, a.field_smem_bytes, a.field_ns, a.field_nd,
+                                               a.field_padded));
   const size_t smem = static_cast<size_t>(a.field_smem_bytes);
   if (smem > 32 * 1024) {
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
