@@ -387,9 +387,11 @@ def run_b200(a):
                 capi.lib().pp_last_timing(C.c_void_p(handle), C.byref(tm))
                 return tm
         else:
-            sp = ShardedPlanner.on_device(model, rank, world)
-
-            assert sp.exchange() == "nccl", sp.exchange()
+            if shared:  # ranks sharing a GPU: NCCL refuses; records over gloo
+                sp = ShardedPlanner.on_shared_device(model, rank, world)
+            else:
+                sp = ShardedPlanner.on_device(model, rank, world)
+                assert sp.exchange() == "nccl", sp.exchange()
 
             def e2e_step():
                 return sp.plan_step(w.snapshot, w.t).action[0]
