@@ -247,7 +247,7 @@ def spawn_ranks(a) -> int:
     way the driver does, after checking that N GPUs exist."""
     import torch
     n_dev = torch.cuda.device_count()
-    if n_dev < a.gpus:
+    if n_dev < a.gpus and not a.allow_shared:
         print(json.dumps({"error": f"--gpus {a.gpus} but only {n_dev} CUDA device(s) visible"}),
               flush=True)
         return 2
