@@ -24,19 +24,57 @@ struct Field {
   int dstride;  // points per dynamic row in the image (Nd + sentinels)
   int ncx, ncy;
   int coop;  // RoundArgs::coop
+  // kernel kind 3 (one x-bucket part staged in shared memory): 32-bit shared
+  // addresses of its points and starts, and the byte strides of a state row
+  // (0 for a static part), fixed once per CTA so a step's row base is one
+  // IMAD each instead of a generic-to-shared conversion
+  uint32_t s_pts, s_st, row_bytes, st_row_bytes;
 };
+
+// ld.shared of a staged field's point / start at a 32-bit shared address
+template <typename Real>
+__device__ __forceinline__ typename Vec2T<Real>::type lds_point(uint32_t a);
+template <>
+__device__ __forceinline__ float2 lds_point<float>(uint32_t a) {
+  float2 v;
+  asm("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(a));
+  return v;
+}
+template <>
+__device__ __forceinline__ double2 lds_point<double>(uint32_t a) {
+  double2 v;
+  asm("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ int lds_start(uint32_t a) {
+  int v;
+  asm("ld.shared.s32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
 
 template <typename Real>
 __device__ __forceinline__ Field<Real> field_at(const RoundArgs& a, const void* base,
                                                 const FieldLayout& l) {
   using R2 = typename Vec2T<Real>::type;
   const unsigned char* p = static_cast<const unsigned char*>(base);
-  return Field<Real>{reinterpret_cast<const R2*>(p), reinterpret_cast<const R2*>(p + l.dpts),
-                     reinterpret_cast<const int*>(p + l.sst),
-                     reinterpret_cast<const int*>(p + l.dst),
-                     reinterpret_cast<const R2*>(p + l.sbox), reinterpret_cast<const int*>(p + l.cst),
-                     reinterpret_cast<const R2*>(p + l.cbox), a.field_ns, a.field_nd,
-                     a.field_dstride, a.grid_nx, a.grid_ny, a.coop};
+  Field<Real> f{reinterpret_cast<const R2*>(p), reinterpret_cast<const R2*>(p + l.dpts),
+                reinterpret_cast<const int*>(p + l.sst), reinterpret_cast<const int*>(p + l.dst),
+                reinterpret_cast<const R2*>(p + l.sbox), reinterpret_cast<const int*>(p + l.cst),
+                reinterpret_cast<const R2*>(p + l.cbox), a.field_ns, a.field_nd,
+                a.field_dstride, a.grid_nx, a.grid_ny, a.coop, 0u, 0u, 0u, 0u};
+  return f;
+}
+
+// The kind-3 shared addressing of a field staged at `smem`.
+template <typename Real>
+__device__ __forceinline__ void bind_shared(Field<Real>& f, const unsigned char* smem,
+                                            const FieldLayout& l) {
+  const uint32_t s0 = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+  const bool dyn = f.Nd > 0;
+  f.s_pts = s0 + static_cast<uint32_t>(dyn ? l.dpts : 0);
+  f.s_st = s0 + static_cast<uint32_t>(dyn ? l.dst : l.sst);
+  f.row_bytes = dyn ? static_cast<uint32_t>(f.dstride * sizeof(typename Vec2T<Real>::type)) : 0u;
+  f.st_row_bytes = dyn ? static_cast<uint32_t>((f.ncx + 1) * sizeof(int)) : 0u;
 }
 
 // Inside-margin of one point against the chassis at (x, y, phi):
@@ -368,14 +406,24 @@ __device__ __forceinline__ Real collide_margin(const Field<Real>& f, const Const
   const Real ky = -s * x + c * y;
   Real best = Real(-1e30);
   if constexpr (kGrid == 3) {
-    // one part: all points static, or all dynamic (the row of state h)
-    const bool dyn = f.Nd > 0;
-    const auto* pts = dyn ? f.dpts + h * f.dstride : f.spts;
-    const int* st = dyn ? f.dst + h * (ncx + 1) : f.sst;
-    // a lane whose rollout is over scans nothing (its window would only
-    // lengthen the warp's point loop)
-    scan_part<Real, kGrid>(pts, st, ncy, cx_lo, live ? cx_hi : cx_lo - 1, cy_lo, cy_hi, K, x, y, c,
-                           s, kx, ky, stop, best);
+    // one part (all points static, or all dynamic: the row of state h),
+    // sentinel-padded, in shared memory: every lane reads `rounds`
+    // consecutive points from its window's first (see scan_part). A lane
+    // whose rollout is over scans nothing (its window would only lengthen the
+    // warp's point loop)
+    const uint32_t st = f.s_st + static_cast<uint32_t>(h) * f.st_row_bytes;
+    const uint32_t pr = f.s_pts + static_cast<uint32_t>(h) * f.row_bytes;
+    const int lo = lds_start(st + 4u * static_cast<uint32_t>(cx_lo));
+    const int cnt = live ? lds_start(st + 4u * static_cast<uint32_t>(cx_hi + 1)) - lo : 0;
+    const int rounds = __reduce_max_sync(kFull, cnt);
+    const uint32_t p0 = pr + static_cast<uint32_t>(lo) *
+                                 static_cast<uint32_t>(sizeof(typename Vec2T<Real>::type));
+#pragma unroll 4
+    for (int j = 0; j < rounds; ++j) {
+      const auto m = lds_point<Real>(
+          p0 + static_cast<uint32_t>(j) * static_cast<uint32_t>(sizeof(typename Vec2T<Real>::type)));
+      best = fmax(best, point_margin<Real>(K, x, y, c, s, kx, ky, m.x, m.y));
+    }
     return best;
   }
   const size_t row_cells = static_cast<size_t>(ncx) * ncy + 1;

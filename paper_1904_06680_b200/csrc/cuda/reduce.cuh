@@ -177,7 +177,9 @@ __device__ __forceinline__ Field<Real> stage_field(const RoundArgs& a, unsigned 
     // instantiation only then), so every field load is an LDS on a 32-bit
     // shared address instead of a generic 64-bit load
     bulk_stage(smem, a.field, static_cast<uint32_t>(a.field_smem_bytes), &stage_bar);
-    return field_at<Real>(a, smem, a.lay);
+    Field<Real> f = field_at<Real>(a, smem, a.lay);
+    bind_shared(f, smem, a.lay);
+    return f;
   }
   if (a.field_smem_bytes > 0 && a.n_points > 0) {
     bulk_stage(smem, a.field, static_cast<uint32_t>(a.field_smem_bytes), &stage_bar);
