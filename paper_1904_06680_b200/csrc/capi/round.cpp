@@ -362,7 +362,8 @@ void run_round_launch(pp_handle* h, uint64_t t, int iter, int r0, int rc, const 
 // the earliest state whose FP64 verdict came within the FP64 band of
 // flipping (ppdev::kNoStep: none).
 void eval_list_fp64(pp_handle* h, const ppdev::RoundArgs& a, int64_t n, int64_t count, int64_t c0,
-                    std::vector<ppdev::SelRec>& dev, std::vector<uint32_t>& mstep) {
+                    std::vector<ppdev::SelRec>& dev, std::vector<uint32_t>& mstep,
+                    std::vector<float>& mpath) {
   ppdev::RoundArgs L = a;
   L.list = static_cast<const int64_t*>(h->d_reflist.p);
   L.list_count = count;
@@ -417,6 +418,7 @@ void eval_list_fp64(pp_handle* h, const ppdev::RoundArgs& a, int64_t n, int64_t 
     d.k1 = d.cls == 2 ? -static_cast<double>(tg) : -k.cost;
     d.k2 = d.cls == 2 ? -k.cost : 0.0;
     mstep[static_cast<size_t>(i)] = ppdev::meta_mstep(k.meta);
+    mpath[static_cast<size_t>(i)] = ppdev::bits_float(k.mpath);
   }
 }
 
@@ -723,8 +725,9 @@ void certify_round(pp_handle* h, ppdev::RoundArgs& a, uint64_t t, int iter, int 
          "refine list H2D");
       std::vector<ppdev::SelRec> dev(list.size());
       std::vector<uint32_t> mstep(list.size(), ppdev::kNoStep);
+      std::vector<float> mpath(list.size(), 0.0f);
       if (launch_shape(h, true, 0, 0).refill) {
-        eval_list_fp64(h, a, static_cast<int64_t>(list.size()), count, c0, dev, mstep);
+        eval_list_fp64(h, a, static_cast<int64_t>(list.size()), count, c0, dev, mstep, mpath);
         for (size_t i = 0; i < list.size(); ++i) {
           dev[i].restart = static_cast<int32_t>(list[i] / count);
           dev[i].cand = static_cast<int32_t>(c0 + (list[i] - dev[i].restart * count));
@@ -767,7 +770,6 @@ void certify_round(pp_handle* h, ppdev::RoundArgs& a, uint64_t t, int iter, int 
       // others, identical rollouts that lose the index tie-break, dropped.
       // Flagged members group the same way, by key and flagged state.
       std::vector<int> keep;
-      size_t n_flagged = 0;
       {
         struct GroupKey {
           int r, cls;
@@ -802,7 +804,6 @@ void certify_round(pp_handle* h, ppdev::RoundArgs& a, uint64_t t, int iter, int 
               b.cls == 2 ? ppdev::rho2_of(kRho64Reached, kRho64ReachedFloor, b.t_goal)
                          : rho64(h->cfg.H);
           const bool flag = mstep[i] != ppdev::kNoStep;
-          n_flagged += flag ? 1 : 0;
           if (flag || (got[i].cls == b.cls &&
                        std::abs(got[i].k1 - b.k1) <= tol * std::max(1.0, std::abs(b.k1)) &&
                        std::abs(got[i].k2 - b.k2) <= tol * std::max(1.0, std::abs(b.k2)))) {
@@ -820,21 +821,69 @@ void certify_round(pp_handle* h, ppdev::RoundArgs& a, uint64_t t, int iter, int 
         std::sort(keep.begin(), keep.end(), [&](int x, int y) { return list[x] < list[y]; });
         keep.erase(std::unique(keep.begin(), keep.end()), keep.end());
       }
-      std::vector<int64_t> kept_list(keep.size());
-      for (size_t j = 0; j < keep.size(); ++j) kept_list[j] = list[keep[j]];
-      std::vector<Exact> kept_got(keep.size());
-      const int base = take_slots(keep.size());
-      {
+      // Phase A: the near-tie groups, exactly; their exact best per restart.
+      // Phase B: a flagged member is evaluated only if its most optimistic
+      // exact key could still beat (or tie) that best: a flip at its flagged
+      // state reaches there with the path so far (mpath, a lower bound; the
+      // path only grows), or its own FP64 key within the FP64 tolerance.
+      std::vector<int> ka, kb;
+      for (int i : keep) (mstep[i] == ppdev::kNoStep ? ka : kb).push_back(i);
+      const auto eval_exact = [&](const std::vector<int>& idx, std::vector<Exact>& out) {
+        out.resize(idx.size());
+        const int base = take_slots(idx.size());
         std::lock_guard<std::mutex> turn(shared_pool().mu);
-        h->pool->run(static_cast<int>(keep.size()), [&](int j) {
-          kept_got[j] = exact_of(kept_list[j], base < 0 ? -1 : base + j);
+        h->pool->run(static_cast<int>(idx.size()), [&](int j) {
+          out[j] = exact_of(list[idx[j]], base < 0 ? -1 : base + j);
         });
+      };
+      std::vector<Exact> got_a, got_b;
+      eval_exact(ka, got_a);
+      std::vector<int> estar(rc, -1);  // per restart: best of phase A (index into ka)
+      for (size_t j = 0; j < ka.size(); ++j) {
+        const int r = dev[ka[j]].restart;
+        const Exact& q = got_a[j];
+        if (estar[r] < 0 || key_better({q.cls, q.k1, q.k2},
+                                       {got_a[estar[r]].cls, got_a[estar[r]].k1,
+                                        got_a[estar[r]].k2})) {
+          estar[r] = static_cast<int>(j);
+        }
+      }
+      std::vector<int> kb_eval;
+      for (int i : kb) {
+        const int r = dev[i].restart;
+        if (estar[r] < 0) {
+          kb_eval.push_back(i);
+          continue;
+        }
+        const double tol = got[i].cls == 2
+                               ? ppdev::rho2_of(kRho64Reached, kRho64ReachedFloor, got[i].t_goal)
+                               : rho64(h->cfg.H);
+        const Key flip{2, -static_cast<double>(mstep[i]),
+                       -static_cast<double>(mpath[i]) * (1.0 - 1e-12)};
+        const Key own = got[i].cls == 2 ? Key{2, got[i].k1, -got[i].cost * (1.0 - tol)}
+                                        : Key{got[i].cls, -got[i].cost * (1.0 - tol), 0.0};
+        const Key opt = key_better(flip, own) ? flip : own;
+        const Exact& e = got_a[estar[r]];
+        if (!key_better({e.cls, e.k1, e.k2}, opt)) kb_eval.push_back(i);
+      }
+      eval_exact(kb_eval, got_b);
+      std::vector<std::pair<int64_t, Exact>> kept;
+      kept.reserve(ka.size() + kb_eval.size());
+      for (size_t j = 0; j < ka.size(); ++j) kept.emplace_back(list[ka[j]], got_a[j]);
+      for (size_t j = 0; j < kb_eval.size(); ++j) kept.emplace_back(list[kb_eval[j]], got_b[j]);
+      std::sort(kept.begin(), kept.end(),
+                [](const auto& x, const auto& y) { return x.first < y.first; });
+      std::vector<int64_t> kept_list(kept.size());
+      std::vector<Exact> kept_got(kept.size());
+      for (size_t j = 0; j < kept.size(); ++j) {
+        kept_list[j] = kept[j].first;
+        kept_got[j] = kept[j].second;
       }
       if (trace_on()) {
-        std::fprintf(stderr, "[paraplan]   wide window %zu: %zu to the host (%zu FP64-flagged, "
-                             "the rest FP64 near-tie groups; best cls %d t_goal %d)\n",
-                     list.size(), keep.size(), n_flagged, best.empty() ? -1 : got[best[0]].cls,
-                     best.empty() ? -1 : got[best[0]].t_goal);
+        std::fprintf(stderr, "[paraplan]   wide window %zu: %zu near-tie groups and %zu of %zu "
+                             "FP64-flagged members to the host (best cls %d t_goal %d)\n",
+                     list.size(), ka.size(), kb_eval.size(), kb.size(),
+                     best.empty() ? -1 : got[best[0]].cls, best.empty() ? -1 : got[best[0]].t_goal);
       }
       list.swap(kept_list);
       got.swap(kept_got);

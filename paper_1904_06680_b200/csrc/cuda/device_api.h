@@ -24,7 +24,7 @@ struct SampleOut {
 struct SKey {
   double cost;    // terminal cost (cls 0/1) or path length (cls 2)
   uint32_t meta;  // make_meta below
-  uint32_t pad;
+  uint32_t mpath; // FP64 rounds: float bits of the path up to the flagged state, rounded down
 };
 
 // meta of a sample key: cls (2 bits) | t_goal (15 bits, class 2) | the

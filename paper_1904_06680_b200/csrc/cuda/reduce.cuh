@@ -200,7 +200,10 @@ __device__ __forceinline__ void write_skey(const RoundArgs& a, int64_t slot, int
   if constexpr (sizeof(Real) == sizeof(float)) {
     static_cast<SKey32*>(a.skeys)[slot] = SKey32{cls == 2 ? L.path : term, meta};
   } else {
-    static_cast<SKey*>(a.skeys)[slot] = SKey{cls == 2 ? L.path : term, meta, 0u};
+    // pad: the path up to the flagged state, rounded down to float (a lower
+    // bound of the key a flip there would give; the wide-window pruning)
+    static_cast<SKey*>(a.skeys)[slot] =
+        SKey{cls == 2 ? L.path : term, meta, float_bits(__double2float_rd(L.mpath))};
   }
 }
 

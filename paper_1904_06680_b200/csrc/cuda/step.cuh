@@ -13,6 +13,7 @@ struct Lane {
   Real x, y, phi, v, act, pa0, path, f0, f1, ephi;
   int h;
   uint32_t mstep;  // earliest state of a verdict within the flag band (meta, kNoStep = none)
+  Real mpath;      // FP64: the path up to that state (a flip there reaches with this path)
   __device__ __forceinline__ void start(const Consts<Real>& K, Real first0, Real first1) {
     x = y = phi = Real(0);
     v = K.v0;
@@ -23,6 +24,7 @@ struct Lane {
     f1 = first1;
     h = 0;
     mstep = kNoStep;
+    mpath = Real(0);
   }
 };
 
@@ -80,6 +82,9 @@ __device__ __forceinline__ int advance(Lane<Real>& L, const Net& net, const Cons
   // step): its verdicts cannot order candidates, and the host decides them
   // exactly (host_stops_at_state0), so they are never flags
   narrow &= L.h > 0;
+  if constexpr (sizeof(Real) == sizeof(double)) {
+    if (narrow && L.mstep == kNoStep) L.mpath = L.path;
+  }
   L.mstep = narrow ? min(L.mstep, static_cast<uint32_t>(L.h)) : L.mstep;
   const int cls = hit ? 0 : (reached ? 2 : (L.h == H ? 1 : -1));
 
