@@ -77,7 +77,18 @@ void prewarm(pp_handle* h) {
       const int cap = static_cast<int>(std::min<size_t>(total, kSelMax));
       grow_selection(h, scratch, std::max(cap, kSelCap));
       h->d_listkeys.reserve(sizeof(ppdev::SKey) * h->sel_cap, "list keys");
-      h->h_listkeys.reserve(sizeof(ppdev::SKey) * h->sel_cap, "pinned list keys");
+      h->d_listout.reserve(sizeof(ppdev::Rec) * 2, "list winner");
+      h->d_listpick.reserve(1024 + sizeof(ppdev::ListPick) * h->sel_cap, "list picks");
+      // (the picks of a wide window are its near-ties and flagged members:
+      // few; a larger set grows the pinned buffer when it happens)
+      h->h_listkeys.reserve(sizeof(ppdev::ListPick) * std::min(h->sel_cap, 1 << 16),
+                            "pinned list picks");
+      // the filter's kernels load on first use: load them now (an empty list)
+      ppdev::ListFilterArgs f{};
+      f.list_count = 1;
+      f.sms = h->sms;
+      ck(static_cast<cudaError_t>(ppdev::launch_list_filter(f, h->stream)), "filter warm-up");
+      ck(cudaStreamSynchronize(h->stream), "filter warm-up");
     }
   } catch (...) {
     cudaGetLastError();
@@ -175,9 +186,12 @@ pp_status pp_create(const pp_model* m, pp_handle** out) {
     ck(cudaEventCreate(&hp->ev1), "event");
     ck(cudaStreamCreateWithFlags(&hp->side, cudaStreamNonBlocking), "stream");
     ck(cudaEventCreateWithFlags(&hp->ev_field, cudaEventDisableTiming), "event");
-    hp->d_round.reserve(kRoundBytes, "round block");
-    ck(cudaMemsetAsync(hp->d_round.p, 0, kRoundBytes, hp->stream), "round block");
-    hp->h_round.reserve(kRoundBytes, "pinned round block");
+    hp->d_round.reserve(kRoundAlloc, "round block");
+    ck(cudaMemsetAsync(hp->d_round.p, 0, kRoundAlloc, hp->stream), "round block");
+    ck(cudaMemsetAsync(static_cast<char*>(hp->d_round.p) + kCutOff, 0xff,
+                       sizeof(uint32_t) * ppdev::kMaxRestartsPerLaunch, hp->stream),
+       "goal cut");
+    hp->h_round.reserve(kRoundAlloc, "pinned round block");
     ck(cudaStreamSynchronize(hp->stream), "init");
     h = hp.release();
   });
@@ -221,7 +235,7 @@ void pp_destroy(pp_handle* h) {
   for (DevBuf* b : {&h->d_field, &h->d_params, &h->d_round, &h->d_tiles, &h->d_movers, &h->d_bin,
                     &h->d_samples, &h->d_scratch, &h->d_injected, &h->d_theta, &h->d_skeys,
                     &h->d_sel, &h->d_bound, &h->d_field64, &h->d_selmore, &h->d_reflist,
-                    &h->d_listkeys, &h->d_listout}) {
+                    &h->d_listkeys, &h->d_listout, &h->d_listpick}) {
     b->release();
   }
   for (HostBuf* b : {&h->h_field, &h->h_params, &h->h_round, &h->h_bound, &h->h_movers,

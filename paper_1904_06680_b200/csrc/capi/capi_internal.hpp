@@ -269,9 +269,39 @@ constexpr size_t kFreeOff = kRecOff + sizeof(ppdev::Rec) * ppdev::kMaxRestartsPe
 // (keypack.h), reduced across the shards in place
 constexpr size_t kPackOff =
     (kFreeOff + sizeof(ppdev::Rec) * ppdev::kMaxRestartsPerLaunch + 63) / 64 * 64;
-constexpr size_t kSelOff =
+// [uint32 x kMaxRestartsPerLaunch] goal-horizon cut state (kCutNone between
+// rounds) and [uint32 x kMaxRestartsPerLaunch] the round's final cut per
+// restart (device_api.h kCutTGoal)
+constexpr size_t kCutOff =
     (kPackOff + sizeof(uint64_t) * 2 * ppdev::kMaxRestartsPerLaunch + 63) / 64 * 64;
+constexpr size_t kCutPubOff = kCutOff + sizeof(uint32_t) * ppdev::kMaxRestartsPerLaunch;
+constexpr size_t kSelOff =
+    (kCutPubOff + sizeof(uint32_t) * ppdev::kMaxRestartsPerLaunch + 63) / 64 * 64;
+// rollouts of a restart stop cut_slack() states after its earliest t_goal
+// (PARAPLAN_GOAL_CUT=0: never; PARAPLAN_CUT_SLACK overrides the slack, a
+// negative one for tests of the redo path)
+inline int cut_slack() {
+  static const int v = [] {
+    const char* e = std::getenv("PARAPLAN_CUT_SLACK");
+    return e != nullptr ? std::atoi(e) : 2;
+  }();
+  return v;
+}
+inline bool goal_cut_enabled() {
+  static const bool v = [] {
+    const char* e = std::getenv("PARAPLAN_GOAL_CUT");
+    return e == nullptr || std::atoi(e) != 0;
+  }();
+  return v;
+}
 constexpr size_t kRoundBytes = kSelOff + sizeof(int64_t) * kSelFirst;
+// behind the round block (not in its D2H): an FP64 list round's final cut
+// per source restart [uint32 x kMaxRestartsPerLaunch] and its filter's pick
+// count, copied back by the certification
+constexpr size_t kListCutOff = kRoundBytes;
+constexpr size_t kListCountOff = kListCutOff + sizeof(uint32_t) * ppdev::kMaxRestartsPerLaunch;
+constexpr size_t kListTailBytes = 512;
+constexpr size_t kRoundAlloc = kRoundBytes + kListTailBytes;
 
 // FP32 rounds are certified for every class up to this horizon, beyond it for
 // class-2 (reaching) windows only (round.cpp: the error model).
@@ -296,7 +326,7 @@ inline bool trace_on() { return trace_level() > 0; }
 
 struct PhaseClock {
   std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
-  char buf[256] = {};
+  char buf[1024] = {};
   int len = 0;
   void mark(const char* what) {
     if (trace_level() < 2 || len >= static_cast<int>(sizeof(buf)) - 1) return;
@@ -337,6 +367,9 @@ struct pp_handle {
   // FP32 planner: the last certified round needed FP64 (class 0/1 anchors
   // beyond the FP32 error envelope); the next round starts in FP64
   bool prefer_fp64 = false;
+  // the next round runs every rollout to its end (a cut round whose
+  // certificate the cut would break is redone so)
+  bool no_cut = false;
 
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -347,7 +380,7 @@ struct pp_handle {
   cudaEvent_t ev_field = nullptr;
   bool field_via_side = false, field_event = false;
   ppcapi::DevBuf d_field, d_params, d_round, d_tiles, d_samples, d_scratch, d_injected, d_theta, d_skeys,
-      d_sel, d_bound, d_movers, d_bin, d_selmore, d_reflist, d_listkeys, d_listout;
+      d_sel, d_bound, d_movers, d_bin, d_selmore, d_reflist, d_listkeys, d_listout, d_listpick;
   int sel_cap = 1 << 16;  // selection capacity of this handle (kSelCap, grown on overflow)
   ppcapi::HostBuf h_field, h_params, h_round, h_bound, h_movers, h_listkeys;
 

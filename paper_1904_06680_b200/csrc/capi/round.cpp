@@ -25,7 +25,7 @@ uint64_t key_prefix(uint64_t seed, uint64_t t, uint64_t r, uint64_t i) {
   return hh;
 }
 
-constexpr int ppdev_warps() { return 4; }
+constexpr int ppdev_warps() { return 4; }  // warps per CTA (rollout.cuh kBlock / 32)
 
 
 // Selection buffers of capacity `cap`: the indices beyond the round block's
@@ -39,7 +39,7 @@ void grow_selection(pp_handle* h, ppdev::RoundArgs& a, int cap) {
   a.ref_list = static_cast<const int64_t*>(h->d_reflist.p);
   a.sel_out = static_cast<ppdev::SelRec*>(h->d_sel.p);
   a.sel_cap = h->sel_cap;
-}  // warps per CTA (rollout.cuh kBlock / 32)
+}
 
 // Windows up to this size are re-evaluated on the host pool (exact FP64
 // rollouts, 16 workers); wider ones get the FP64 device kernel first.
@@ -187,6 +187,12 @@ void run_round_launch(pp_handle* h, uint64_t t, int iter, int r0, int rc, const 
     a.theta_buf = h->d_theta.p;  // [total][theta_elem]: theta, first action, pad
     a.first_buf = nullptr;
   }
+  // goal-horizon cut (refill schedule; per-sample rounds keep every rollout)
+  const bool cut = shape0.refill && per_sample == nullptr && !h->no_cut && goal_cut_enabled();
+  a.goal_cut = cut ? reinterpret_cast<uint32_t*>(dres + kCutOff) : nullptr;
+  a.cut_pub = reinterpret_cast<uint32_t*>(dres + kCutPubOff);
+  a.cut_slack = cut_slack();
+  a.cut_slots = rc;
   // several restarts on the refill schedule: winners from the sample keys
   const bool keys_only = shape0.refill && rc > 1;
   a.keys_only = keys_only ? 1 : 0;
@@ -355,15 +361,20 @@ void run_round_launch(pp_handle* h, uint64_t t, int iter, int r0, int rc, const 
 }
 
 // FP64 re-evaluation of the n window members listed in h->d_reflist (flat
-// indices of the round `a`, restart-major over `count` candidates per
-// restart, candidates starting at c0): a list round of the FP64 generator +
-// refill rollout (the FP64 round's own kernels and per-candidate cost, at
-// full occupancy), keys only. dev[i] receives member i's FP64 key, mstep[i]
-// the earliest state whose FP64 verdict came within the FP64 band of
-// flipping (ppdev::kNoStep: none).
-void eval_list_fp64(pp_handle* h, const ppdev::RoundArgs& a, int64_t n, int64_t count, int64_t c0,
-                    std::vector<ppdev::SelRec>& dev, std::vector<uint32_t>& mstep,
-                    std::vector<float>& mpath) {
+// indices of the round `a`, rc restarts of `count` candidates, candidates
+// starting at c0): a list round of the FP64 generator + refill rollout (the
+// FP64 round's own kernels and per-candidate cost, at full occupancy, with the
+// goal-horizon cut per source restart), keys only, then the device filter
+// (launch_list_filter) keeps each restart's FP64 near-ties (within 2 x their
+// tolerance) and the FP64-flagged members. Only those come back: list[i] the
+// member, dev[i] its FP64 key, mstep[i] the earliest state whose FP64 verdict
+// came within the FP64 band of flipping (ppdev::kNoStep: none), mpath[i] the
+// path up to there. Returns the list round's cut per restart (kCutNone: none).
+std::vector<uint32_t> eval_list_fp64(pp_handle* h, const ppdev::RoundArgs& a, int64_t n,
+                                     int64_t count, int64_t c0, int rc,
+                                     std::vector<int64_t>& list,
+                                     std::vector<ppdev::SelRec>& dev,
+                                     std::vector<uint32_t>& mstep, std::vector<float>& mpath) {
   ppdev::RoundArgs L = a;
   L.list = static_cast<const int64_t*>(h->d_reflist.p);
   L.list_count = count;
@@ -380,8 +391,15 @@ void eval_list_fp64(pp_handle* h, const ppdev::RoundArgs& a, int64_t n, int64_t 
   L.sel_packed = 0;
   L.pkeys = nullptr;
   L.skey32 = 0;
+  char* dres = static_cast<char*>(h->d_round.p);
+  L.goal_cut = !h->no_cut && goal_cut_enabled() ? reinterpret_cast<uint32_t*>(dres + kCutOff)
+                                                 : nullptr;
+  L.cut_pub = reinterpret_cast<uint32_t*>(dres + kListCutOff);
+  L.cut_slack = cut_slack();
+  L.cut_slots = rc;
   // sized to the selection capacity: a closed loop's windows grow tick by tick
-  h->d_listkeys.reserve(sizeof(ppdev::SKey) * std::max<size_t>(n, h->sel_cap), "list keys");
+  const size_t cap = std::max<size_t>(n, h->sel_cap);
+  h->d_listkeys.reserve(sizeof(ppdev::SKey) * cap, "list keys");
   h->d_listout.reserve(sizeof(ppdev::Rec) * 2, "list winner");
   L.skeys = h->d_listkeys.p;
   L.out = static_cast<ppdev::Rec*>(h->d_listout.p);
@@ -403,23 +421,62 @@ void eval_list_fp64(pp_handle* h, const ppdev::RoundArgs& a, int64_t n, int64_t 
      "list generator launch");
   ck(static_cast<cudaError_t>(ppdev::launch_rollout_f64(h->kind, L, h->stream)),
      "list rollout launch");
-  h->h_listkeys.reserve(sizeof(ppdev::SKey) * std::max<size_t>(n, h->sel_cap), "pinned list keys");
-  const ppdev::SKey* keys = static_cast<const ppdev::SKey*>(h->h_listkeys.p);
-  ck(cudaMemcpyAsync(h->h_listkeys.p, h->d_listkeys.p, sizeof(ppdev::SKey) * n,
+  // the filter: scratch [rank u32 x 64][cost u64 x 64], then the picks
+  constexpr size_t kScratch = 1024;  // as the prewarm's reservation (capi.cpp)
+  h->d_listpick.reserve(kScratch + sizeof(ppdev::ListPick) * cap, "list picks");
+  char* dp = static_cast<char*>(h->d_listpick.p);
+  ck(cudaMemsetAsync(dp, 0xff, kScratch, h->stream), "list filter scratch");
+  ck(cudaMemsetAsync(dres + kListCountOff, 0, sizeof(uint32_t), h->stream), "list filter count");
+  ppdev::ListFilterArgs f{};
+  f.keys = static_cast<const ppdev::SKey*>(h->d_listkeys.p);
+  f.list = L.list;
+  f.n = n;
+  f.list_count = count;
+  f.rho = rho64(h->cfg.H);
+  f.rho2 = kRho64Reached;
+  f.rho2_floor = kRho64ReachedFloor;
+  f.rank = reinterpret_cast<uint32_t*>(dp);
+  f.cost = reinterpret_cast<unsigned long long*>(dp + 256);
+  f.count = reinterpret_cast<uint32_t*>(dres + kListCountOff);
+  f.out = reinterpret_cast<ppdev::ListPick*>(dp + kScratch);
+  f.sms = h->sms;
+  ck(static_cast<cudaError_t>(ppdev::launch_list_filter(f, h->stream)), "list filter launch");
+  char* hres = static_cast<char*>(h->h_round.p);
+  ck(cudaMemcpyAsync(hres + kListCutOff, dres + kListCutOff, kListTailBytes,
                      cudaMemcpyDeviceToHost, h->stream),
-     "list keys D2H");
+     "list cut D2H");
   ck(cudaStreamSynchronize(h->stream), "list round");
-  h->timing.launches += 3;
-  for (int64_t i = 0; i < n; ++i) {
-    const ppdev::SKey& k = keys[static_cast<size_t>(i)];
-    ppdev::SelRec& d = dev[static_cast<size_t>(i)];
+  h->timing.launches += 6;
+  const uint32_t m = *reinterpret_cast<const uint32_t*>(hres + kListCountOff);
+  std::vector<uint32_t> cut(rc, ppdev::kCutNone);
+  if (L.goal_cut != nullptr) {
+    std::memcpy(cut.data(), hres + kListCutOff, sizeof(uint32_t) * rc);
+  }
+  h->h_listkeys.reserve(sizeof(ppdev::ListPick) * std::max<size_t>(m, 1), "pinned list picks");
+  const ppdev::ListPick* picks = static_cast<const ppdev::ListPick*>(h->h_listkeys.p);
+  if (m > 0) {
+    ck(cudaMemcpyAsync(h->h_listkeys.p, f.out, sizeof(ppdev::ListPick) * m,
+                       cudaMemcpyDeviceToHost, h->stream),
+       "list picks D2H");
+    ck(cudaStreamSynchronize(h->stream), "list picks");
+  }
+  phase("list-gpu");
+  list.resize(m);
+  dev.resize(m);
+  mstep.resize(m);
+  mpath.resize(m);
+  for (uint32_t i = 0; i < m; ++i) {
+    const ppdev::SKey& k = picks[i].key;
+    ppdev::SelRec& d = dev[i];
+    list[i] = picks[i].flat;
     d.cls = ppdev::meta_cls(k.meta);
     const int tg = ppdev::meta_tgoal(k.meta);
     d.k1 = d.cls == 2 ? -static_cast<double>(tg) : -k.cost;
     d.k2 = d.cls == 2 ? -k.cost : 0.0;
-    mstep[static_cast<size_t>(i)] = ppdev::meta_mstep(k.meta);
-    mpath[static_cast<size_t>(i)] = ppdev::bits_float(k.mpath);
+    mstep[i] = ppdev::meta_mstep(k.meta);
+    mpath[i] = ppdev::bits_float(k.mpath);
   }
+  return cut;
 }
 
 // Certified re-ranking (PlannerConfig::refine). The FP32 keys are trusted
@@ -447,7 +504,7 @@ struct XBest {
   double cost, k1, k2;
   int64_t cand;       // candidate index within the restart
   int32_t overflow;   // the shard's window overflowed this pass
-  int32_t _pad;
+  uint32_t cut;       // the shard's goal-horizon cut of the restart (kCutNone: none)
 };
 
 }  // namespace
@@ -551,6 +608,7 @@ void certify_round(pp_handle* h, ppdev::RoundArgs& a, uint64_t t, int iter, int 
                                        : a.sel_rho2);
   };
   const char* hres = static_cast<const char*>(h->h_round.p);
+  const uint32_t* cut_pub = reinterpret_cast<const uint32_t*>(hres + kCutPubOff);
   std::vector<ppdev::SelBound> bound(rc);
   auto set_bound = [&](int r, int cls, int t_goal, double cost) {
     bound[r].cls = cls;
@@ -620,6 +678,9 @@ void certify_round(pp_handle* h, ppdev::RoundArgs& a, uint64_t t, int iter, int 
     }
   }
   std::vector<char> certified(rc, 0);
+  // per restart: the earliest cut of the round and of its list rounds
+  std::vector<uint32_t> cut_eff(rc, ppdev::kCutNone);
+  if (a.goal_cut != nullptr) std::copy(cut_pub, cut_pub + rc, cut_eff.begin());
   std::vector<int64_t> list;
   std::vector<XBest> xmine(rc), xall;
   bool widened = shard_mode == 2;  // no select ran yet
@@ -662,7 +723,12 @@ void certify_round(pp_handle* h, ppdev::RoundArgs& a, uint64_t t, int iter, int 
                    static_cast<unsigned long long>(t), iter, pass, n_sel);
     }
     list.clear();
-    if (!overflow) {
+    // a wide first-pass window stays on the device: the FP64 list round reads
+    // the selection in place and only the members the host must see return
+    const bool refill64 = launch_shape(h, true, 0, 0).refill != 0;
+    const bool dev_list =
+        !overflow && known.empty() && refill64 && n_sel > static_cast<uint32_t>(host_max());
+    if (!overflow && !dev_list) {
       std::vector<int64_t> sl(n_sel);
       std::memcpy(sl.data(), static_cast<const char*>(h->h_round.p) + kSelOff,
                   sizeof(int64_t) * std::min<uint32_t>(n_sel, kSelFirst));
@@ -684,7 +750,9 @@ void certify_round(pp_handle* h, ppdev::RoundArgs& a, uint64_t t, int iter, int 
       // after its FP64 pass, on the members it keeps
       if (list.size() <= static_cast<size_t>(host_max())) std::sort(list.begin(), list.end());
     }
-    h->timing.refined += static_cast<int32_t>(list.size());
+    const size_t n_new = dev_list ? n_sel : list.size();
+    h->timing.refined += static_cast<int32_t>(n_new);
+    phase("list");
     if (trace_level() >= 3 && !list.empty() && !fp64) {  // window composition
       std::vector<ppdev::SKey32> ks(list.size());
       for (size_t i = 0; i < list.size(); ++i) {
@@ -710,8 +778,9 @@ void certify_round(pp_handle* h, ppdev::RoundArgs& a, uint64_t t, int iter, int 
                    list.size(), m, bound[0].cls, bound[0].t_goal, bound[0].thr, flagged, ms_hist[0],
                    ms_hist[1], ms_hist[2], ms_hist[3], incost);
     }
-    std::vector<Exact> got(list.size());
-    if (list.size() <= static_cast<size_t>(host_max())) {
+    std::vector<Exact> got;
+    if (!dev_list && list.size() <= static_cast<size_t>(host_max())) {
+      got.resize(list.size());
       const int base = take_slots(list.size());
       std::lock_guard<std::mutex> turn(shared_pool().mu);
       h->pool->run(static_cast<int>(list.size()), [&](int i) {
@@ -719,20 +788,45 @@ void certify_round(pp_handle* h, ppdev::RoundArgs& a, uint64_t t, int iter, int 
       });
     } else {
       // wide window: FP64 keys from the device, exact host keys for the FP64
-      // near-ties of each restart's best
-      ck(cudaMemcpyAsync(h->d_reflist.p, list.data(), sizeof(int64_t) * list.size(),
-                         cudaMemcpyHostToDevice, h->stream),
-         "refine list H2D");
-      std::vector<ppdev::SelRec> dev(list.size());
-      std::vector<uint32_t> mstep(list.size(), ppdev::kNoStep);
-      std::vector<float> mpath(list.size(), 0.0f);
-      if (launch_shape(h, true, 0, 0).refill) {
-        eval_list_fp64(h, a, static_cast<int64_t>(list.size()), count, c0, dev, mstep, mpath);
+      // near-ties of each restart's best and the FP64-flagged members
+      if (dev_list) {  // the selection, in place: round block head + sel_more
+        const char* dsel = static_cast<const char*>(h->d_round.p) + kSelOff;
+        const size_t head = std::min<uint32_t>(n_sel, kSelFirst);
+        ck(cudaMemcpyAsync(h->d_reflist.p, dsel, sizeof(int64_t) * head,
+                           cudaMemcpyDeviceToDevice, h->stream),
+           "refine list D2D");
+        if (n_sel > static_cast<uint32_t>(kSelFirst)) {
+          ck(cudaMemcpyAsync(static_cast<int64_t*>(h->d_reflist.p) + kSelFirst, a.sel_more,
+                             sizeof(int64_t) * (n_sel - kSelFirst), cudaMemcpyDeviceToDevice,
+                             h->stream),
+             "refine list D2D");
+        }
+      } else {
+        ck(cudaMemcpyAsync(h->d_reflist.p, list.data(), sizeof(int64_t) * list.size(),
+                           cudaMemcpyHostToDevice, h->stream),
+           "refine list H2D");
+      }
+      std::vector<ppdev::SelRec> dev;
+      std::vector<uint32_t> mstep;
+      std::vector<float> mpath;
+      if (refill64) {
+        const size_t n_listed = n_new;
+        const std::vector<uint32_t> lcut =
+            eval_list_fp64(h, a, static_cast<int64_t>(n_listed), count, c0, rc, list, dev, mstep,
+                           mpath);
+        for (int r = 0; r < rc; ++r) cut_eff[r] = std::min(cut_eff[r], lcut[r]);
         for (size_t i = 0; i < list.size(); ++i) {
           dev[i].restart = static_cast<int32_t>(list[i] / count);
           dev[i].cand = static_cast<int32_t>(c0 + (list[i] - dev[i].restart * count));
         }
+        if (trace_on()) {
+          std::fprintf(stderr, "[paraplan]   wide window %zu: %zu picked on the device\n", n_listed,
+                       list.size());
+        }
       } else {  // generic architectures: one lockstep FP64 rollout per lane
+        dev.resize(list.size());
+        mstep.assign(list.size(), ppdev::kNoStep);
+        mpath.assign(list.size(), 0.0f);
         const uint32_t n_list = static_cast<uint32_t>(list.size());
         ck(cudaMemcpyAsync(a.counters + 2, &n_list, sizeof(uint32_t), cudaMemcpyHostToDevice,
                            h->stream),
@@ -746,6 +840,7 @@ void certify_round(pp_handle* h, ppdev::RoundArgs& a, uint64_t t, int iter, int 
         ck(cudaStreamSynchronize(h->stream), "refine kernel");
         h->timing.launches += 1;
       }
+      got.resize(list.size());
       phase("refine64");
       std::vector<int> best(rc, -1);
       for (size_t i = 0; i < dev.size(); ++i) {
@@ -769,6 +864,7 @@ void certify_round(pp_handle* h, ppdev::RoundArgs& a, uint64_t t, int iter, int 
       // trajectory) are one group: its lowest index is evaluated and the
       // others, identical rollouts that lose the index tie-break, dropped.
       // Flagged members group the same way, by key and flagged state.
+      phase("best");
       std::vector<int> keep;
       {
         struct GroupKey {
@@ -826,6 +922,7 @@ void certify_round(pp_handle* h, ppdev::RoundArgs& a, uint64_t t, int iter, int 
       // exact key could still beat (or tie) that best: a flip at its flagged
       // state reaches there with the path so far (mpath, a lower bound; the
       // path only grows), or its own FP64 key within the FP64 tolerance.
+      phase("groups");
       std::vector<int> ka, kb;
       for (int i : keep) (mstep[i] == ppdev::kNoStep ? ka : kb).push_back(i);
       const auto eval_exact = [&](const std::vector<int>& idx, std::vector<Exact>& out) {
@@ -838,6 +935,7 @@ void certify_round(pp_handle* h, ppdev::RoundArgs& a, uint64_t t, int iter, int 
       };
       std::vector<Exact> got_a, got_b;
       eval_exact(ka, got_a);
+      phase("exactA");
       std::vector<int> estar(rc, -1);  // per restart: best of phase A (index into ka)
       for (size_t j = 0; j < ka.size(); ++j) {
         const int r = dev[ka[j]].restart;
@@ -920,10 +1018,11 @@ void certify_round(pp_handle* h, ppdev::RoundArgs& a, uint64_t t, int iter, int 
     }
     for (int r = 0; r < rc; ++r) {
       const Exact* e = local[r];
+      const uint32_t cut = cut_eff[r];
       xmine[r] = e == nullptr
-                     ? XBest{-1, 0, 0.0, 0.0, 0.0, -1, overflow ? 1 : 0, 0}
+                     ? XBest{-1, 0, 0.0, 0.0, 0.0, -1, overflow ? 1 : 0, cut}
                      : XBest{e->cls, e->t_goal, e->cost, e->k1, e->k2,
-                             c0 + (local_win[r] - r * count), overflow ? 1 : 0, 0};
+                             c0 + (local_win[r] - r * count), overflow ? 1 : 0, cut};
     }
     bool any_overflow = overflow;
     std::vector<XBest> gbest(xmine);
@@ -931,20 +1030,23 @@ void certify_round(pp_handle* h, ppdev::RoundArgs& a, uint64_t t, int iter, int 
       xall.resize(static_cast<size_t>(rc) * xg->world);
       xg->allgather(xmine.data(), xall.data(), sizeof(XBest) * rc, h->stream);
       for (int r = 0; r < rc; ++r) {
-        XBest g{-1, 0, 0.0, 0.0, 0.0, -1, 0, 0};
+        XBest g{-1, 0, 0.0, 0.0, 0.0, -1, 0, ppdev::kCutNone};
+        uint32_t cut = ppdev::kCutNone;
         for (int w = 0; w < xg->world; ++w) {  // shard order = index order
           const XBest& q = xall[static_cast<size_t>(w) * rc + r];
           any_overflow = any_overflow || q.overflow != 0;
+          cut = std::min(cut, q.cut);
           if (q.cls < 0) continue;
           if (g.cls < 0 || key_better({q.cls, q.k1, q.k2}, {g.cls, g.k1, g.k2})) g = q;
         }
+        g.cut = cut;
         gbest[r] = g;
       }
     }
     if (any_overflow) break;
 
     // certify or widen each uncertified restart
-    bool all = true;
+    bool all = true, cut_broken = false;
     for (int r = 0; r < rc; ++r) {
       if (certified[r]) continue;
       const ppdev::SelBound& bd = bound[r];
@@ -959,6 +1061,17 @@ void certify_round(pp_handle* h, ppdev::RoundArgs& a, uint64_t t, int iter, int 
           ok = (bd.cls == 2 && e.t_goal < bd.t_goal) ||
                ((bd.cls != 2 || e.t_goal == bd.t_goal) && e.cost <= bd.thr - slack);
         }
+      }
+      // A cut rollout has not reached the goal by its restart's (shard's)
+      // earliest t_goal + cut_slack() (device_api.h), so no exact key places
+      // it ahead of an exact best that reaches by then -- unless it is
+      // flagged at or before the window's t_goal, and then it is in the
+      // window. An exact best reaching later (or not at all) has no such
+      // guarantee: the round is redone without the cut.
+      if (ok && e.cut != ppdev::kCutNone &&
+          !(e.cls == 2 && static_cast<int64_t>(e.t_goal) <= int64_t{e.cut} + cut_slack())) {
+        cut_broken = true;
+        ok = false;
       }
       if (ok) {
         certified[r] = 1;
@@ -991,6 +1104,21 @@ void certify_round(pp_handle* h, ppdev::RoundArgs& a, uint64_t t, int iter, int 
       const bool same = e.cls >= 0 && e.cls == bd.cls && (bd.cls != 2 || e.t_goal == bd.t_goal);
       const double wider = bd.thr * 1.25 + alpha;
       bound[r].thr = same ? std::max(e.cost * (1.0 + rho) + alpha, wider) : wider;
+    }
+    if (cut_broken) {
+      if (trace_on()) {
+        std::fprintf(stderr, "[paraplan] t=%llu iter=%d: the goal cut does not hold, round redone\n",
+                     static_cast<unsigned long long>(t), iter);
+      }
+      h->no_cut = true;
+      try {
+        run_round_launch(h, t, iter, r0, rc, center, c0, c1, injected, out, nullptr, fp64);
+      } catch (...) {
+        h->no_cut = false;
+        throw;
+      }
+      h->no_cut = false;
+      return;
     }
     if (trace_on()) {
       std::fprintf(stderr, "[paraplan] t=%llu iter=%d pass=%d selected=%u new=%zu certified=%s\n",

@@ -38,6 +38,13 @@ PP_HD uint32_t make_meta(int cls, int t_goal, uint32_t mstep) {
   return static_cast<uint32_t>(cls) | (static_cast<uint32_t>(cls == 2 ? t_goal : 0) << 2) |
          (mstep << 17);
 }
+// Goal-horizon cut (refill schedule): once a rollout of a restart reaches the
+// goal at state T, no candidate of that restart that has not reached it by
+// state T + slack can win (class 2 ranks first, then the earliest t_goal), so
+// its lane stops there. Its key is class 2 with t_goal kCutTGoal, behind
+// every real t_goal (H <= kMaxKeyHorizon); its flags up to the cut are kept.
+constexpr int kCutTGoal = 0x7fff;
+constexpr uint32_t kCutNone = 0xffffffffu;
 PP_HD int meta_cls(uint32_t m) { return static_cast<int>(m & 3u); }
 PP_HD int meta_tgoal(uint32_t m) { return static_cast<int>((m >> 2) & 0x7fffu); }
 PP_HD uint32_t meta_mstep(uint32_t m) { return m >> 17; }
@@ -213,6 +220,15 @@ struct RoundArgs {
   // GLOBAL best unflagged candidate (sel_packed != 0)
   int32_t sel_packed;
   uint64_t* pkeys;
+  // goal-horizon cut (kCutTGoal above; null: every rollout runs to its end):
+  // goal_cut[r] the earliest t_goal seen so far in restart r (kCutNone: none;
+  // a list round's slots are the restarts of the round the list came from),
+  // re-armed by the round's last block after copying slots [0, cut_slots)
+  // to cut_pub
+  uint32_t* goal_cut;
+  uint32_t* cut_pub;
+  int32_t cut_slack;
+  int32_t cut_slots;
 };
 
 // Architecture dispatch of the specialised kernels.
@@ -266,6 +282,28 @@ int launch_select(const RoundArgs& a, void* stream);
 // Packed keys of the round's per-restart winners into a.pkeys (a dependent
 // launch after the rollout / per-restart reduction).
 int launch_pack_keys(const RoundArgs& a, void* stream);
+// Wide-window filter after an FP64 list round (csrc/capi/round.cpp
+// certify_round): per source restart, the members' best rank (2 - cls,
+// t_goal) and the best cost at that rank; then every member that is flagged
+// or within 2 x tol of its restart's best (a superset of the host's FP64
+// near-ties, tol = rho of the best's class and t_goal) is appended to `out`.
+struct ListPick {
+  int64_t flat;  // the member (flat index of the listed round)
+  SKey key;      // its FP64 key
+};
+struct ListFilterArgs {
+  const SKey* keys;     // [n] the list round's keys
+  const int64_t* list;  // [n] flat indices, restart-major over list_count
+  int64_t n, list_count;
+  double rho;                // class 0/1 tolerance
+  double rho2, rho2_floor;   // class 2: rho2_of(rho2, rho2_floor, t_goal)
+  uint32_t* rank;            // [kMaxRestartsPerLaunch] scratch, 0xff..
+  unsigned long long* cost;  // [kMaxRestartsPerLaunch] scratch, 0xff..
+  uint32_t* count;           // picked members (0 on entry)
+  ListPick* out;             // [n]
+  int32_t sms;
+};
+int launch_list_filter(const ListFilterArgs& f, void* stream);
 // Copy `bytes` (a multiple of 16) of device memory into pinned host memory
 // with SM stores, after the previous kernel on `stream` (dependent launch).
 int launch_copy_out(const void* src, void* host_dst, size_t bytes, void* stream);

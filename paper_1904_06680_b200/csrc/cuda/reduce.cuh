@@ -194,9 +194,9 @@ __device__ __forceinline__ Field<Real> stage_field(const RoundArgs& a, unsigned 
 // | t_goal<<8.
 template <typename Real>
 __device__ __forceinline__ void write_skey(const RoundArgs& a, int64_t slot, int cls,
-                                           const Lane<Real>& L, Real term) {
+                                           const Lane<Real>& L, Real term, int t_goal = -1) {
   if (a.skeys == nullptr) return;
-  const uint32_t meta = make_meta(cls, L.h, L.mstep);
+  const uint32_t meta = make_meta(cls, t_goal < 0 ? L.h : t_goal, L.mstep);
   if constexpr (sizeof(Real) == sizeof(float)) {
     static_cast<SKey32*>(a.skeys)[slot] = SKey32{cls == 2 ? L.path : term, meta};
   } else {
@@ -301,6 +301,11 @@ __device__ __forceinline__ void publish_round(const RoundArgs& a) {
     a.counters[0] = 0;
     a.counters[1] = 0;
     a.counters[2] = 0;  // the window selection that follows counts from zero
+  }
+  if (a.goal_cut != nullptr) {
+    for (int r = threadIdx.x; r < a.cut_slots; r += blockDim.x) {
+      a.cut_pub[r] = atomicExch(&a.goal_cut[r], kCutNone);
+    }
   }
 }
 

@@ -158,6 +158,12 @@ __global__ void __launch_bounds__(kBlock, refill_min_blocks<Real, Net>())
   const bool track = a.keys_only == 0;  // lane bests (one restart) or keys only
   // lane bests can cross restarts only when a launch holds several
   const bool cross = track && a.restart_count > 1;
+  // goal-horizon cut: the lane's view of its restart's earliest t_goal,
+  // refreshed every 8 states and on every refill (loaded ahead of its use)
+  uint32_t* const goal_cut = a.goal_cut;
+  uint32_t cut_h = kCutNone;
+  unsigned iter = 0;
+  int cut_slot = 0;  // the lane's restart (list rounds: the listed member's)
 
   for (;;) {
     // -------- hand the warp's current batch to idle lanes --------
@@ -195,6 +201,11 @@ __global__ void __launch_bounds__(kBlock, refill_min_blocks<Real, Net>())
           for (int i = 0; i < P; ++i) net.w[i] = rec.v[i];
           L.start(K, rec.v[P], rec.v[P + 1]);
           active = true;
+          if (goal_cut != nullptr) {
+            cut_slot = a.list != nullptr ? static_cast<int>(__ldg(a.list + sidx) / a.list_count)
+                                         : my_r;
+            cut_h = __ldcv(goal_cut + cut_slot);
+          }
         }
         q_head += __popc(need) < avail ? __popc(need) : avail;
       }
@@ -202,8 +213,20 @@ __global__ void __launch_bounds__(kBlock, refill_min_blocks<Real, Net>())
     if (!__any_sync(kFull, active)) break;  // stream exhausted, all lanes done
 
     // -------- one rollout state per lane --------
+    if (goal_cut != nullptr && (++iter & 7u) == 0u && active) {
+      cut_h = min(cut_h, __ldcv(goal_cut + cut_slot));
+    }
     // every lane steps (idle lanes only at the stream tail, results unused)
-    const int cls = advance<Real, kGrid>(L, net, K, f, H, active);
+    int cls = advance<Real, kGrid>(L, net, K, f, H, active);
+    // cut: states 0..h checked without reaching, h >= the restart's earliest
+    // t_goal + slack (cut_h is never below the final earliest t_goal)
+    const bool cut = active && cls < 0 && cut_h != kCutNone &&
+                     L.h >= static_cast<int>(cut_h) + a.cut_slack;
+    if (goal_cut != nullptr && active && cls == 2 && static_cast<uint32_t>(L.h) < cut_h) {
+      cut_h = static_cast<uint32_t>(L.h);
+      atomicMin(goal_cut + cut_slot, cut_h);
+    }
+    if (cut) cls = 2;
     const bool done = active && cls >= 0;
     // lane bests are per restart: flush the old one before crossing over
     if (cross) {
@@ -212,9 +235,10 @@ __global__ void __launch_bounds__(kBlock, refill_min_blocks<Real, Net>())
     }
     if (done) {
       const Real term = terminal_cost(L, K);
+      const int tg = cut ? kCutTGoal : L.h;
       if (track) {
         const LaneKey<Real> k =
-            make_lane_key<Real>(cls, L.h, L.path, term, static_cast<int>(a.cand_begin + my_c));
+            make_lane_key<Real>(cls, tg, L.path, term, static_cast<int>(a.cand_begin + my_c));
         if (best.cls < 0 || prefer(k, best)) {
           best = k;
           best_r = my_r;
@@ -225,7 +249,7 @@ __global__ void __launch_bounds__(kBlock, refill_min_blocks<Real, Net>())
       if (a.per_sample != nullptr) {
         write_sample(a, static_cast<int64_t>(my_r) * a.count + my_c, cls, L, term);
       }
-      write_skey(a, static_cast<int64_t>(my_r) * a.count + my_c, cls, L, term);
+      write_skey(a, static_cast<int64_t>(my_r) * a.count + my_c, cls, L, term, tg);
       active = false;
     }
   }

@@ -83,6 +83,126 @@ int launch_copy_out(const void* src, void* host_dst, size_t bytes, void* stream)
                                              static_cast<uint4*>(dst), n16));
 }
 
+// ------------------------------------------------ wide-window filter ----
+namespace {
+
+__device__ __forceinline__ uint32_t pick_rank(uint32_t meta) {
+  const int cls = meta_cls(meta);
+  return (static_cast<uint32_t>(2 - cls) << 16) |
+         static_cast<uint32_t>(cls == 2 ? meta_tgoal(meta) : 0);
+}
+// order-preserving bits of a double (any sign)
+__device__ __forceinline__ unsigned long long cost_order(double c) {
+  const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(c));
+  return (b >> 63) ? ~b : (b | (1ull << 63));
+}
+__device__ __forceinline__ double order_cost(unsigned long long o) {
+  const unsigned long long b = (o >> 63) ? (o & ~(1ull << 63)) : ~o;
+  return __longlong_as_double(static_cast<long long>(b));
+}
+
+// Flush a thread's running minimum of restart r: one atomic per warp when the
+// warp agrees on r (the usual case: a window is one restart's or sorted).
+template <typename T>
+__device__ __forceinline__ void flush_min(T* dst, int r, T v) {
+  const int r0 = __shfl_sync(kFull, r, 0);
+  if (__all_sync(kFull, r == r0)) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const T w = __shfl_xor_sync(kFull, v, o);
+      v = w < v ? w : v;
+    }
+    if ((threadIdx.x & 31) == 0 && r0 >= 0) atomicMin(dst + r0, v);
+  } else if (r >= 0) {
+    atomicMin(dst + r, v);
+  }
+}
+
+// pass 0: best rank per restart; pass 1: best cost at that rank
+template <int kPass>
+__global__ void __launch_bounds__(256) list_best_kernel(const ListFilterArgs f) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const int64_t n_pad = (f.n + 31) / 32 * 32;  // whole warps for the shuffles
+  int r_cur = -1;
+  unsigned long long v_cur = ~0ull;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n_pad;
+       i += stride) {
+    int r = -1;
+    unsigned long long v = ~0ull;
+    if (i < f.n) {
+      r = static_cast<int>(__ldg(f.list + i) / f.list_count);
+      const SKey k = f.keys[i];
+      const uint32_t rank = pick_rank(k.meta);
+      if (kPass == 0) {
+        v = rank;
+      } else if (rank == f.rank[r]) {
+        v = cost_order(k.cost);
+      }
+    }
+    if (r != r_cur && r >= 0) {
+      if (r_cur >= 0) {
+        if (kPass == 0) {
+          atomicMin(f.rank + r_cur, static_cast<uint32_t>(v_cur));
+        } else {
+          atomicMin(f.cost + r_cur, v_cur);
+        }
+      }
+      r_cur = r;
+      v_cur = ~0ull;
+    }
+    if (r >= 0 && v < v_cur) v_cur = v;
+  }
+  if (kPass == 0) {
+    flush_min<uint32_t>(f.rank, r_cur, static_cast<uint32_t>(v_cur));
+  } else {
+    flush_min<unsigned long long>(f.cost, r_cur, v_cur);
+  }
+}
+
+__global__ void __launch_bounds__(256) list_pick_kernel(const ListFilterArgs f) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const int64_t n_pad = (f.n + 31) / 32 * 32;
+  const int lane = threadIdx.x & 31;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n_pad;
+       i += stride) {
+    bool keep = false;
+    int64_t flat = 0;
+    SKey k{};
+    if (i < f.n) {
+      flat = __ldg(f.list + i);
+      const int r = static_cast<int>(flat / f.list_count);
+      k = f.keys[i];
+      if (meta_flagged(k.meta)) {
+        keep = true;
+      } else if (pick_rank(k.meta) == f.rank[r]) {
+        const double b = order_cost(f.cost[r]);
+        const int cls = meta_cls(k.meta);
+        const double tol =
+            cls == 2 ? rho2_of(f.rho2, f.rho2_floor, meta_tgoal(k.meta)) : f.rho;
+        keep = fabs(k.cost - b) <= 2.0 * tol * fmax(1.0, fabs(b));
+      }
+    }
+    const unsigned m = __ballot_sync(kFull, keep);
+    if (m == 0u) continue;
+    unsigned base = 0;
+    if (lane == 0) base = atomicAdd(f.count, static_cast<unsigned>(__popc(m)));
+    base = __shfl_sync(kFull, base, 0);
+    if (keep) f.out[base + __popc(m & ((1u << lane) - 1u))] = ListPick{flat, k};
+  }
+}
+
+}  // namespace
+
+int launch_list_filter(const ListFilterArgs& f, void* stream) {
+  const cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int64_t blocks = std::min<int64_t>((f.n + 255) / 256, int64_t{f.sms} * 8);
+  const unsigned g = static_cast<unsigned>(std::max<int64_t>(1, blocks));
+  list_best_kernel<0><<<g, 256, 0, st>>>(f);
+  list_best_kernel<1><<<g, 256, 0, st>>>(f);
+  list_pick_kernel<<<g, 256, 0, st>>>(f);
+  return static_cast<int>(cudaGetLastError());
+}
+
 int refine_occupancy(NetKind k) {
   switch (k) {
     case NetKind::k5_2_2:
