@@ -184,7 +184,7 @@ void run_round_launch(pp_handle* h, uint64_t t, int iter, int r0, int rc, const 
   if (shape0.refill) {
     const size_t esz = fp64 ? sizeof(double) : sizeof(float);
     h->d_theta.reserve(total * shape0.theta_elem * esz, "theta buffer");
-    a.theta_buf = h->d_theta.p;  // [total][theta_elem]: theta, first action, pad
+    a.theta_buf = h->d_theta.p;  // [total][theta_elem]: theta, state 1, pad
     a.first_buf = nullptr;
   }
   // goal-horizon cut (refill schedule; per-sample rounds keep every rollout)

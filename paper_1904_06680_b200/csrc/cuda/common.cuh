@@ -39,6 +39,61 @@ constexpr int kWarps = kBlock / 32;
 #ifndef PARAPLAN_REFILL64_MINB
 #define PARAPLAN_REFILL64_MINB 4  // FP64 [5,2,2]/[5,10,2]: <= 128 registers
 #endif
+// L2 residency of the theta records between the generator and the rollout
+// (PARAPLAN_REC_L2=0: default caching): the generator stores them with an
+// evict_last policy, the rollout's single read demotes them (evict_first).
+#ifndef PARAPLAN_REC_L2
+#define PARAPLAN_REC_L2 1
+#endif
+__device__ __forceinline__ unsigned long long l2_keep_policy() {
+  unsigned long long p;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ unsigned long long l2_drop_policy() {
+  unsigned long long p;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void st_rec(float4* p, const float4& v, unsigned long long pol) {
+#if PARAPLAN_REC_L2
+  asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;"
+               :: "l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w), "l"(pol) : "memory");
+#else
+  *p = v;
+#endif
+}
+__device__ __forceinline__ void st_rec(double2* p, const double2& v, unsigned long long pol) {
+#if PARAPLAN_REC_L2
+  asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;"
+               :: "l"(p), "d"(v.x), "d"(v.y), "l"(pol) : "memory");
+#else
+  *p = v;
+#endif
+}
+__device__ __forceinline__ void prefetch_l1(const void* p) {
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
+__device__ __forceinline__ float4 ld_rec(const float4* p, unsigned long long pol) {
+#if PARAPLAN_REC_L2
+  float4 v;
+  asm("ld.global.L1::evict_first.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p), "l"(pol));
+  return v;
+#else
+  return __ldcg(p);
+#endif
+}
+__device__ __forceinline__ double2 ld_rec(const double2* p, unsigned long long pol) {
+#if PARAPLAN_REC_L2
+  double2 v;
+  asm("ld.global.L1::evict_first.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
+               : "=d"(v.x), "=d"(v.y) : "l"(p), "l"(pol));
+  return v;
+#else
+  return __ldcg(p);
+#endif
+}
 #ifndef PARAPLAN_REFILL_MINB
 #define PARAPLAN_REFILL_MINB 6  // <= 85 registers: 6 CTAs (24 warps) per SM, no spills
 #endif
@@ -128,6 +183,13 @@ struct M<float> {
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(e + 1.0f));
     return fmaf(-2.0f, r, 1.0f);
 #endif
+  }
+  // th of x / (2 log2 e): the prescaled weights' argument (nets.cuh prescale)
+  static __device__ __forceinline__ float th_pre(float x) {
+    float e, r;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(x));
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(e + 1.0f));
+    return fmaf(-2.0f, r, 1.0f);
   }
   static __device__ __forceinline__ float tn(float x) { return tanf(x); }
   // tan for |x| <= pi/4 (the steering range when delta_max <= pi/4)

@@ -45,15 +45,47 @@
 namespace ppdev {
 
 // --------------------------------------------------- generate kernel ----
-// theta (rounded to Real) and the first action of every candidate of the
-// round, one thread per candidate at full SIMT width: the FP64 RNG lives here
-// and not in the rollout kernel, so the rollout kernel stays register-light.
-// Layout: one record of kRecW(P) Reals per candidate, [theta 0..P-1][f0][f1]
-// [pad], so a refilling lane loads it with 16-byte vector loads; the flat
-// index is s = r * count + local (restart-major).
+// theta (rounded to Real), the first action and the state it leads to
+// (state 1) of every candidate of the round, one thread per candidate at full
+// SIMT width: the FP64 RNG lives here and not in the rollout kernel, so the
+// rollout kernel stays register-light, and a rollout starts at state 1.
+// Layout: one record of rec_width(P) Reals per candidate, [theta 0..P-1]
+// [x y phi v act pa0 path of state 1][f0 f1: the first action][pad], so a
+// refilling lane loads it with 16-byte vector loads; the flat index is
+// s = r * count + local (restart-major).
+constexpr int kRecState = 9;
 template <typename Real>
 constexpr int rec_width(int P) {
-  return ((P + 2) * static_cast<int>(sizeof(Real)) + 15) / 16 * 16 / static_cast<int>(sizeof(Real));
+  return ((P + kRecState) * static_cast<int>(sizeof(Real)) + 15) / 16 * 16 /
+         static_cast<int>(sizeof(Real));
+}
+template <typename Real>
+__device__ __forceinline__ void store_state(const Lane<Real>& L, Real* v) {
+  v[0] = L.x;
+  v[1] = L.y;
+  v[2] = L.phi;
+  v[3] = L.v;
+  v[4] = L.act;
+  v[5] = L.pa0;
+  v[6] = L.path;
+  v[7] = L.f0;
+  v[8] = L.f1;
+}
+// a lane at state 1 from its record
+template <typename Real>
+__device__ __forceinline__ void load_state(Lane<Real>& L, const Real* v) {
+  L.x = v[0];
+  L.y = v[1];
+  L.phi = v[2];
+  L.v = v[3];
+  L.act = v[4];
+  L.pa0 = v[5];
+  L.path = v[6];
+  L.f0 = v[7];
+  L.f1 = v[8];
+  L.h = 1;
+  L.mstep = kNoStep;
+  L.mpath = Real(0);
 }
 template <typename Real>
 using Vec16 = typename std::conditional<sizeof(Real) == 4, float4, double2>::type;
@@ -61,8 +93,8 @@ using Vec16 = typename std::conditional<sizeof(Real) == 4, float4, double2>::typ
 // One candidate's record: theta of restart r, local candidate `local`, and
 // its first action, written to record slot s.
 template <typename Real, class Net>
-__device__ __forceinline__ void generate_one(const RoundArgs& a, const Real s0[5], int r,
-                                             int64_t local, int64_t s) {
+__device__ __forceinline__ void generate_one(const RoundArgs& a, const Consts<Real>& K,
+                                             const Real s0[5], int r, int64_t local, int64_t s) {
   constexpr int P = Net::P;
   constexpr int W = rec_width<Real>(P);
   constexpr int V = W * static_cast<int>(sizeof(Real)) / 16;
@@ -76,11 +108,23 @@ __device__ __forceinline__ void generate_one(const RoundArgs& a, const Real s0[5
   Net n;
 #pragma unroll
   for (int i = 0; i < P; ++i) n.w[i] = rec.v[i];
-  n.eval(s0, rec.v[P], rec.v[P + 1]);  // first action (src/planner.cpp:130-132)
+  Real f0, f1;
+  n.eval(s0, f0, f1);  // first action (src/planner.cpp:130-132)
+  Lane<Real> L;
+  L.start(K, f0, f1);
+  first_step(L, K);
+  store_state(L, rec.v + P);
+  if constexpr (prescaled<Real, Net>(true)) {
+    const Real in_scale[5] = {K.inv_xi * Real(2.8853900817779268), K.inv_eta * Real(2.8853900817779268),
+                              K.inv_phi * Real(2.8853900817779268), K.inv_v * Real(2.8853900817779268),
+                              Real(2.8853900817779268)};
+    prescale<Net>(rec.v, in_scale);
+  }
 #pragma unroll
-  for (int i = P + 2; i < W; ++i) rec.v[i] = Real(0);
+  for (int i = P + kRecState; i < W; ++i) rec.v[i] = Real(0);
+  const unsigned long long keep = l2_keep_policy();
 #pragma unroll
-  for (int j = 0; j < V; ++j) recs[s * V + j] = rec.q[j];
+  for (int j = 0; j < V; ++j) st_rec(recs + s * V + j, rec.q[j], keep);
 }
 
 template <typename Real, class Net>
@@ -103,7 +147,7 @@ __global__ void __launch_bounds__(256, PARAPLAN_GEN_MINB) generate_kernel(const 
                       ? static_cast<int>(static_cast<uint32_t>(flat) / static_cast<uint32_t>(cnt))
                       : static_cast<int>(flat / cnt);
     const int64_t local = flat - static_cast<int64_t>(r) * cnt;
-    generate_one<Real, Net>(a, s0, r, local, s);
+    generate_one<Real, Net>(a, K, s0, r, local, s);
   }
   (void)recs;
 }
@@ -141,12 +185,20 @@ __global__ void __launch_bounds__(kBlock, refill_min_blocks<Real, Net>())
   constexpr int W = rec_width<Real>(P);
   constexpr int V = W * static_cast<int>(sizeof(Real)) / 16;
   const Vec16<Real>* recs = static_cast<const Vec16<Real>*>(a.theta_buf);
+  const unsigned long long drop = l2_drop_policy();
 
   Net net;
 #pragma unroll
   for (int i = 0; i < P; ++i) net.w[i] = Real(0);
+  // state 0 is every candidate's: its checks run once per thread (the
+  // verdicts every lane would compute); lanes start at state 1 (the
+  // generator's record), or, when state 0 already stops, end there
   Lane<Real> L;
   L.start(K, Real(0), Real(0));  // idle lanes step a valid (discarded) state
+  L.ephi = M<Real>::wrap(K.gphi - Real(0));
+  const int cls0 = check_state<Real, kGrid>(L, K, f, H, true, Real(0), Real(1));
+  L.mstep = kNoStep;
+  const Real ephi0 = L.ephi;
   bool active = false;
   int my_r = 0;
   int my_c = 0;  // local candidate index within [0, count)
@@ -158,12 +210,17 @@ __global__ void __launch_bounds__(kBlock, refill_min_blocks<Real, Net>())
   const bool track = a.keys_only == 0;  // lane bests (one restart) or keys only
   // lane bests can cross restarts only when a launch holds several
   const bool cross = track && a.restart_count > 1;
-  // goal-horizon cut: the lane's view of its restart's earliest t_goal,
-  // refreshed every 8 states and on every refill (loaded ahead of its use)
+  // goal-horizon cut: a lane stops at state cut_at = its restart's earliest
+  // t_goal (as this lane last saw it) + slack. The restart's value is loaded
+  // every 8 iterations before the step and folded in after it (no wait on
+  // the load); a lane that reaches lowers it at once. cut_slot: the lane's
+  // restart (list rounds: the listed member's); a lane moving to another
+  // restart forgets the old one's cut.
   uint32_t* const goal_cut = a.goal_cut;
-  uint32_t cut_h = kCutNone;
+  constexpr int kNoCut = 0x7fffffff;
+  int cut_at = kNoCut;
   unsigned iter = 0;
-  int cut_slot = 0;  // the lane's restart (list rounds: the listed member's)
+  int cut_slot = 0;
 
   for (;;) {
     // -------- hand the warp's current batch to idle lanes --------
@@ -181,6 +238,14 @@ __global__ void __launch_bounds__(kBlock, refill_min_blocks<Real, Net>())
           const int64_t left = a.count - q_c0;
           q_count = left < 32 ? static_cast<int>(left) : 32;
           q_head = 0;
+          // the batch's records into L1: the lanes refill from it over the
+          // next iterations (all but the first few hit L1)
+          if (lane < q_count) {
+            const char* rp = reinterpret_cast<const char*>(
+                recs + (static_cast<int64_t>(q_r) * a.count + q_c0 + lane) * V);
+            prefetch_l1(rp);
+            prefetch_l1(rp + W * static_cast<int>(sizeof(Real)) - 1);
+          }
         }
       }
       const int avail = q_count - q_head;
@@ -196,15 +261,24 @@ __global__ void __launch_bounds__(kBlock, refill_min_blocks<Real, Net>())
             Vec16<Real> q[V];
           } rec;
 #pragma unroll
-          for (int j = 0; j < V; ++j) rec.q[j] = __ldcg(recs + sidx * V + j);
+          for (int j = 0; j < V; ++j) rec.q[j] = ld_rec(recs + sidx * V + j, drop);
 #pragma unroll
           for (int i = 0; i < P; ++i) net.w[i] = rec.v[i];
-          L.start(K, rec.v[P], rec.v[P + 1]);
+          if (cls0 < 0) {
+            load_state(L, rec.v + P);
+          } else {
+            L.start(K, Real(0), Real(0));
+            L.ephi = ephi0;
+          }
           active = true;
           if (goal_cut != nullptr) {
-            cut_slot = a.list != nullptr ? static_cast<int>(__ldg(a.list + sidx) / a.list_count)
-                                         : my_r;
-            cut_h = __ldcv(goal_cut + cut_slot);
+            const int slot = a.list != nullptr
+                                 ? static_cast<int>(__ldg(a.list + sidx) / a.list_count)
+                                 : my_r;
+            if (slot != cut_slot) {
+              cut_slot = slot;
+              cut_at = kNoCut;
+            }
           }
         }
         q_head += __popc(need) < avail ? __popc(need) : avail;
@@ -213,18 +287,18 @@ __global__ void __launch_bounds__(kBlock, refill_min_blocks<Real, Net>())
     if (!__any_sync(kFull, active)) break;  // stream exhausted, all lanes done
 
     // -------- one rollout state per lane --------
-    if (goal_cut != nullptr && (++iter & 7u) == 0u && active) {
-      cut_h = min(cut_h, __ldcv(goal_cut + cut_slot));
-    }
+    const bool fresh = goal_cut != nullptr && (++iter & 7u) == 0u;
+    const uint32_t cut_ld = fresh ? __ldcv(goal_cut + cut_slot) : kCutNone;  // used after the step
     // every lane steps (idle lanes only at the stream tail, results unused)
-    int cls = advance<Real, kGrid>(L, net, K, f, H, active);
+    int cls = cls0 >= 0 ? (active ? cls0 : -1)
+                        : advance<Real, kGrid, Net, false>(L, net, K, f, H, active);
+    if (cut_ld != kCutNone) cut_at = min(cut_at, static_cast<int>(cut_ld) + a.cut_slack);
     // cut: states 0..h checked without reaching, h >= the restart's earliest
-    // t_goal + slack (cut_h is never below the final earliest t_goal)
-    const bool cut = active && cls < 0 && cut_h != kCutNone &&
-                     L.h >= static_cast<int>(cut_h) + a.cut_slack;
-    if (goal_cut != nullptr && active && cls == 2 && static_cast<uint32_t>(L.h) < cut_h) {
-      cut_h = static_cast<uint32_t>(L.h);
-      atomicMin(goal_cut + cut_slot, cut_h);
+    // t_goal + slack (a lane's view is never below the final earliest t_goal)
+    const bool cut = active && cls < 0 && L.h >= cut_at;
+    if (goal_cut != nullptr && active && cls == 2 && L.h + a.cut_slack < cut_at) {
+      cut_at = L.h + a.cut_slack;
+      atomicMin(goal_cut + cut_slot, static_cast<uint32_t>(L.h));
     }
     if (cut) cls = 2;
     const bool done = active && cls >= 0;

@@ -14,6 +14,7 @@ struct Lane {
   int h;
   uint32_t mstep;  // earliest state of a verdict within the flag band (meta, kNoStep = none)
   Real mpath;      // FP64: the path up to that state (a flip there reaches with this path)
+  // state 0 with the first action (first0, first1) still to apply
   __device__ __forceinline__ void start(const Consts<Real>& K, Real first0, Real first1) {
     x = y = phi = Real(0);
     v = K.v0;
@@ -38,25 +39,22 @@ __device__ __forceinline__ void start_features(const Consts<Real>& K, Real s[5])
   s[4] = K.pa0;
 }
 
-// One state of the rollout loop (src/planner.cpp:137-183). Returns -1 while
-// running, else the class (0 collided, 1 horizon, 2 reached at state h).
-// Warp-synchronous and branch-free: the checks and the next state are
-// computed for every lane and committed only by the lanes still running,
-// so the warp never splits into per-outcome paths.
-template <typename Real, int kGrid, class Net>
-__device__ __forceinline__ int advance(Lane<Real>& L, const Net& net, const Consts<Real>& K,
-                                       const Field<Real>& f, int H, bool live = true) {
-  Real sphi, cphi;
-  M<Real>::sc(L.phi, &sphi, &cphi);
-  L.ephi = M<Real>::wrap(K.gphi - L.phi);
+// The verdicts at the lane's state h (src/planner.cpp:137-152): collision
+// with field row h, the goal box, the horizon. Returns -1 while running, else
+// the class (0 collided, 1 horizon, 2 reached at state h); records the
+// earliest flagged state. Branch-free: every lane computes every check.
+template <typename Real, int kGrid>
+__device__ __forceinline__ int check_state(Lane<Real>& L, const Consts<Real>& K,
+                                           const Field<Real>& f, int H, bool live, Real sphi,
+                                           Real cphi) {
   bool hit = false;
   // the flag band: the base margin plus the drift the state may have
   // accumulated over the path so far, which grows with the state index like
   // the measured relative path error (rho2_fp32's envelope)
   Real band = K.dmarg;
   if (K.dmarg_rel != Real(0)) {
-    const Real f = static_cast<Real>(L.h) * Real(1.0 / 150.0);
-    band += L.path * fmax(K.dmarg_floor, K.dmarg_rel * fmin(f * f, Real(1)));
+    const Real q = static_cast<Real>(L.h) * Real(1.0 / 150.0);
+    band += L.path * fmax(K.dmarg_floor, K.dmarg_rel * fmin(q * q, Real(1)));
   }
   bool narrow = false;
   if (f.Ns + f.Nd > 0) {
@@ -86,68 +84,120 @@ __device__ __forceinline__ int advance(Lane<Real>& L, const Net& net, const Cons
     if (narrow && L.mstep == kNoStep) L.mpath = L.path;
   }
   L.mstep = narrow ? min(L.mstep, static_cast<uint32_t>(L.h)) : L.mstep;
-  const int cls = hit ? 0 : (reached ? 2 : (L.h == H ? 1 : -1));
+  return hit ? 0 : (reached ? 2 : (L.h == H ? 1 : -1));
+}
 
-  Real s[5];
-  s[0] = M<Real>::ndiv(gdx, K.d_xi, K.inv_xi);
-  s[1] = M<Real>::ndiv(gdy, K.d_eta, K.inv_eta);
-  s[2] = M<Real>::ndiv(L.ephi, K.d_phi, K.inv_phi);
-  s[3] = M<Real>::ndiv(K.gv - L.v, K.d_v, K.inv_v);
-  s[4] = L.pa0;
-  Real a0, a1;
-  net.eval(s, a0, a1);
-  if (L.h == 0) {  // the first action was computed before the loop
-    a0 = L.f0;
-    a1 = L.f1;
-  }
-  // map_controls (src/dynamics.cpp:30-43)
+// The transition from the lane's state h under action (a0, a1):
+// map_controls (src/dynamics.cpp:30-43) and the explicit Euler step
+// (src/dynamics.cpp:45-62), with the path segment (src/planner.cpp:177-179).
+template <typename Real>
+struct Next {
+  Real x, y, phi, v, act, seg;
+};
+template <typename Real>
+__device__ __forceinline__ Next<Real> transition(const Lane<Real>& L, const Consts<Real>& K,
+                                                 Real a0, Real a1, Real sphi, Real cphi) {
   const Real c0 = clampr(a0, Real(-1), Real(1));
   const Real c1 = clampr(a1, Real(-1), Real(1));
   Real delta = clampr(K.dmax * c0, L.act - K.window, L.act + K.window);
   delta = clampr(delta, -K.dmax, K.dmax);
-  // u_v = lerp(umin, umax, (c1 + 1) / 2) (src/dynamics.cpp:40-42); FP32 folds
-  // it with T_s into one FMA of the speed update below
-  Real u_v = Real(0);
-  if constexpr (sizeof(Real) == sizeof(double)) {
-    const Real w = Real(0.5) * (c1 + Real(1));
-    u_v = (Real(1) - w) * K.umin + w * K.umax;
-  }
-  // explicit Euler (src/dynamics.cpp:45-62)
   const Real tan_d = K.tan_small ? M<Real>::tn_small(delta) : M<Real>::tn(delta);
   const Real tb = M<Real>::ndiv(K.l_r * tan_d, K.wb_d, K.inv_wb);
   const Real tv = K.Ts * L.v;
   const Real ix = tv * (cphi - tb * sphi);
   const Real iy = tv * (sphi + tb * cphi);
-  const Real nx = L.x + ix;
-  const Real ny = L.y + iy;
-  const Real nphi = L.phi + M<Real>::ndiv(tv * tan_d, K.wb_d, K.inv_wb);
-  Real nv;
+  Next<Real> n;
+  n.x = L.x + ix;
+  n.y = L.y + iy;
+  n.phi = L.phi + M<Real>::ndiv(tv * tan_d, K.wb_d, K.inv_wb);
+  n.act = delta;
   if constexpr (sizeof(Real) == sizeof(double)) {
-    nv = L.v + K.Ts * u_v;
+    // u_v = lerp(umin, umax, (c1 + 1) / 2) (src/dynamics.cpp:40-42)
+    const Real w = Real(0.5) * (c1 + Real(1));
+    const Real u_v = (Real(1) - w) * K.umin + w * K.umax;
+    n.v = L.v + K.Ts * u_v;
+    // the reference's difference of the rounded positions
+    const Real dx = n.x - L.x, dy = n.y - L.y;
+    n.seg = M<Real>::sq(dx * dx + dy * dy);
   } else {
-    nv = fmaf(c1, K.ts_uhalf, L.v + K.ts_umid);
+    // FP32 folds the lerp with T_s into one FMA; the path takes the
+    // increment itself, since n.x - x cancels ~|x| / |dx| float ulps (1e-6
+    // relative per segment at 30 m), which the FP64 difference does not
+    n.v = fmaf(c1, K.ts_uhalf, L.v + K.ts_umid);
+    n.seg = M<Real>::sq(ix * ix + iy * iy);
   }
-  // path segment (src/planner.cpp:177-179): FP64 takes the reference's
-  // difference of the rounded positions; FP32 takes the increment itself,
-  // since nx - x cancels ~|x| / |dx| float ulps (1e-6 relative per segment at
-  // 30 m), which the FP64 difference does not
-  Real seg;
-  if constexpr (sizeof(Real) == sizeof(double)) {
-    const Real dx = nx - L.x, dy = ny - L.y;
-    seg = M<Real>::sq(dx * dx + dy * dy);
+  return n;
+}
+
+// Apply a transition: the lane moves to state h + 1 (a0: the action's first
+// component, the next state's feature).
+template <typename Real>
+__device__ __forceinline__ void commit(Lane<Real>& L, const Next<Real>& n, Real a0) {
+  L.path += n.seg;
+  L.x = n.x;
+  L.y = n.y;
+  L.phi = n.phi;
+  L.v = n.v;
+  L.act = n.act;
+  L.pa0 = a0;
+  ++L.h;
+}
+
+// State 1 of every candidate: state 0 under its first action (f0, f1), as
+// advance computes it. The refill schedule's generator applies it, so the
+// rollout starts at state 1 (the checks of state 0, the same for every
+// candidate, run once per rollout thread).
+template <typename Real>
+__device__ __forceinline__ void first_step(Lane<Real>& L, const Consts<Real>& K) {
+  const Next<Real> n = transition(L, K, L.f0, L.f1, Real(0), Real(1));
+  commit(L, n, L.f0);
+}
+
+// One state of the rollout loop (src/planner.cpp:137-183): the checks of
+// state h and, independent of them, the MLP and transition to state h + 1,
+// committed only by lanes still running. Returns -1 while running, else the
+// class at state h. Warp-synchronous and branch-free: the checks and the
+// next state are computed for every lane, so the warp never splits into
+// per-outcome paths.
+// Whether a refill-schedule net's weights are prescaled (nets.cuh prescale):
+// FP32 register nets with the fast tanh.
+template <typename Real, class Net>
+constexpr bool prescaled(bool refill) {
+  return refill && sizeof(Real) == sizeof(float) && Net::kP > 0 && !PARAPLAN_ACCURATE_TANH;
+}
+
+// kFromZero: lanes may be at state 0 (the lockstep schedules), whose action
+// is the precomputed first one; otherwise the lanes come from the refill
+// schedule's records (state >= 1, prescaled weights where prescaled()).
+template <typename Real, int kGrid, class Net, bool kFromZero = true>
+__device__ __forceinline__ int advance(Lane<Real>& L, const Net& net, const Consts<Real>& K,
+                                       const Field<Real>& f, int H, bool live = true) {
+  Real sphi, cphi;
+  M<Real>::sc(L.phi, &sphi, &cphi);
+  L.ephi = M<Real>::wrap(K.gphi - L.phi);
+  const int cls = check_state<Real, kGrid>(L, K, f, H, live, sphi, cphi);
+  Real s[5];
+  constexpr bool kPre = prescaled<Real, Net>(!kFromZero);
+  if constexpr (kPre) {  // the normalisation lives in the weights
+    s[0] = K.gx - L.x;
+    s[1] = K.gy - L.y;
+    s[2] = L.ephi;
+    s[3] = K.gv - L.v;
   } else {
-    seg = M<Real>::sq(ix * ix + iy * iy);
+    s[0] = M<Real>::ndiv(K.gx - L.x, K.d_xi, K.inv_xi);
+    s[1] = M<Real>::ndiv(K.gy - L.y, K.d_eta, K.inv_eta);
+    s[2] = M<Real>::ndiv(L.ephi, K.d_phi, K.inv_phi);
+    s[3] = M<Real>::ndiv(K.gv - L.v, K.d_v, K.inv_v);
   }
-  if (cls < 0) {
-    L.path += seg;
-    L.x = nx;
-    L.y = ny;
-    L.phi = nphi;
-    L.v = nv;
-    L.act = delta;
-    L.pa0 = a0;
-    ++L.h;
+  s[4] = L.pa0;
+  Real a0, a1;
+  net.template eval<kPre>(s, a0, a1);
+  if (kFromZero && L.h == 0) {  // the first action was computed before the loop
+    a0 = L.f0;
+    a1 = L.f1;
   }
+  const Next<Real> n = transition(L, K, a0, a1, sphi, cphi);
+  if (cls < 0) commit(L, n, a0);
   return cls;
 }
 
