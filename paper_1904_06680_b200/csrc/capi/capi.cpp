@@ -97,6 +97,7 @@ void prewarm(pp_handle* h) {
   h->snapshot = nullptr;
   h->timing = pp_timing{};
   h->prefer_fp64 = false;  // the warm-up's fake snapshot says nothing about real ticks
+  h->expect_reach = true;
 }
 
 // The exchange of an in-process sharded planner (PlannerConfig::devices):

@@ -370,6 +370,9 @@ struct pp_handle {
   // the next round runs every rollout to its end (a cut round whose
   // certificate the cut would break is redone so)
   bool no_cut = false;
+  // the last round's winner reached the goal: the next round runs the cut's
+  // kernel (round.cpp)
+  bool expect_reach = true;
 
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;

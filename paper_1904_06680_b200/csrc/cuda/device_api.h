@@ -222,9 +222,9 @@ struct RoundArgs {
   uint64_t* pkeys;
   // goal-horizon cut (kCutTGoal above; null: every rollout runs to its end):
   // goal_cut[r] the earliest t_goal seen so far in restart r (kCutNone: none;
-  // a list round's slots are the restarts of the round the list came from),
-  // re-armed by the round's last block after copying slots [0, cut_slots)
-  // to cut_pub
+  // a list round has one slot, and is cut only when its list comes from a
+  // round of one restart), re-armed by the round's last block after copying
+  // slots [0, cut_slots) to cut_pub
   uint32_t* goal_cut;
   uint32_t* cut_pub;
   int32_t cut_slack;

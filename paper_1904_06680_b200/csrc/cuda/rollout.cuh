@@ -161,7 +161,19 @@ constexpr int refill_min_blocks() {
                            : (Net::kP <= 24 ? PARAPLAN_REFILL64_MINB : 2);
 }
 
-template <typename Real, class Net, int kGrid>
+// A relaxed load of a restart's goal cut. Not a volatile access: the
+// compiler may schedule the loop's other memory operations across it (a
+// volatile load here cost ~9% of the C2 rollout); `tag` (loop-variant) keeps
+// it from being hoisted out of the loop.
+__device__ __forceinline__ uint32_t ld_cut(const uint32_t* p, int tag) {
+  uint32_t v;
+  asm("ld.relaxed.gpu.global.u32 %0, [%1]; // %2" : "=r"(v) : "l"(p), "r"(tag));
+  return v;
+}
+
+// kCut: with the goal-horizon cut (a.goal_cut set); without it the loop
+// carries none of its instructions (~6% of a C2 rollout that never reaches).
+template <typename Real, class Net, int kGrid, bool kCut>
 __global__ void __launch_bounds__(kBlock, refill_min_blocks<Real, Net>())
     refill_kernel(const RoundArgs a) {
   constexpr int P = Net::kP;
@@ -210,17 +222,16 @@ __global__ void __launch_bounds__(kBlock, refill_min_blocks<Real, Net>())
   const bool track = a.keys_only == 0;  // lane bests (one restart) or keys only
   // lane bests can cross restarts only when a launch holds several
   const bool cross = track && a.restart_count > 1;
-  // goal-horizon cut: a lane stops at state cut_at = its restart's earliest
-  // t_goal (as this lane last saw it) + slack. The restart's value is loaded
-  // every 8 iterations before the step and folded in after it (no wait on
-  // the load); a lane that reaches lowers it at once. cut_slot: the lane's
-  // restart (list rounds: the listed member's); a lane moving to another
-  // restart forgets the old one's cut.
-  uint32_t* const goal_cut = a.goal_cut;
+  // goal-horizon cut (kCut): a lane stops at state cut_at = its restart's
+  // earliest t_goal (as this lane last saw it) + slack. The restart's value
+  // is loaded every 8 iterations before the step and folded in after it (no
+  // wait on the load); a lane that reaches lowers it at once. With several
+  // restarts a lane forgets the cut when it takes a new candidate (a list
+  // round is one slot: the host cuts list rounds of one restart only).
+  uint32_t* const goal_cut = kCut ? a.goal_cut : nullptr;
   constexpr int kNoCut = 0x7fffffff;
   int cut_at = kNoCut;
   unsigned iter = 0;
-  int cut_slot = 0;
 
   for (;;) {
     // -------- hand the warp's current batch to idle lanes --------
@@ -271,15 +282,7 @@ __global__ void __launch_bounds__(kBlock, refill_min_blocks<Real, Net>())
             L.ephi = ephi0;
           }
           active = true;
-          if (goal_cut != nullptr) {
-            const int slot = a.list != nullptr
-                                 ? static_cast<int>(__ldg(a.list + sidx) / a.list_count)
-                                 : my_r;
-            if (slot != cut_slot) {
-              cut_slot = slot;
-              cut_at = kNoCut;
-            }
-          }
+          if (kCut && a.restart_count > 1) cut_at = kNoCut;
         }
         q_head += __popc(need) < avail ? __popc(need) : avail;
       }
@@ -287,20 +290,23 @@ __global__ void __launch_bounds__(kBlock, refill_min_blocks<Real, Net>())
     if (!__any_sync(kFull, active)) break;  // stream exhausted, all lanes done
 
     // -------- one rollout state per lane --------
-    const bool fresh = goal_cut != nullptr && (++iter & 7u) == 0u;
-    const uint32_t cut_ld = fresh ? __ldcv(goal_cut + cut_slot) : kCutNone;  // used after the step
+    uint32_t cut_ld = kCutNone;  // used after the step
+    if (kCut && (++iter & 7u) == 0u) cut_ld = ld_cut(goal_cut + my_r, static_cast<int>(iter));
     // every lane steps (idle lanes only at the stream tail, results unused)
     int cls = cls0 >= 0 ? (active ? cls0 : -1)
                         : advance<Real, kGrid, Net, false>(L, net, K, f, H, active);
-    if (cut_ld != kCutNone) cut_at = min(cut_at, static_cast<int>(cut_ld) + a.cut_slack);
-    // cut: states 0..h checked without reaching, h >= the restart's earliest
-    // t_goal + slack (a lane's view is never below the final earliest t_goal)
-    const bool cut = active && cls < 0 && L.h >= cut_at;
-    if (goal_cut != nullptr && active && cls == 2 && L.h + a.cut_slack < cut_at) {
-      cut_at = L.h + a.cut_slack;
-      atomicMin(goal_cut + cut_slot, static_cast<uint32_t>(L.h));
+    bool cut = false;
+    if constexpr (kCut) {
+      if (cut_ld != kCutNone) cut_at = min(cut_at, static_cast<int>(cut_ld) + a.cut_slack);
+      // cut: states 0..h checked without reaching, h >= the restart's
+      // earliest t_goal + slack (a lane's view is never below the final one)
+      cut = active && cls < 0 && L.h >= cut_at;
+      if (active && cls == 2 && L.h + a.cut_slack < cut_at) {
+        cut_at = L.h + a.cut_slack;
+        atomicMin(goal_cut + my_r, static_cast<uint32_t>(L.h));
+      }
+      if (cut) cls = 2;
     }
-    if (cut) cls = 2;
     const bool done = active && cls >= 0;
     // lane bests are per restart: flush the old one before crossing over
     if (cross) {
@@ -700,9 +706,11 @@ inline cudaError_t launch_dependent(KernelFn k, int grid, int block, size_t smem
 }
 
 template <typename Real, class Net, int kGrid>
-KernelFn kernel_of_g() {
+KernelFn kernel_of_g(bool cut) {
   if constexpr (Net::kP > 0) {
-    if (refill_schedule<Net>()) return refill_kernel<Real, Net, kGrid>;
+    if (refill_schedule<Net>()) {
+      return cut ? refill_kernel<Real, Net, kGrid, true> : refill_kernel<Real, Net, kGrid, false>;
+    }
   }
   return lockstep_kernel<Real, Net, kGrid>;
 }
@@ -710,16 +718,16 @@ KernelFn kernel_of_g() {
 // grid mode of the field (0 x-buckets, 1 2-D, 2 2-D with cell boxes) -- a
 // separate instantiation each, so the small-field kernel stays lean.
 template <typename Real, class Net>
-KernelFn kernel_of(int kind) {
+KernelFn kernel_of(int kind, bool cut = true) {
   switch (kind) {
     case 3:
-      return kernel_of_g<Real, Net, 3>();
+      return kernel_of_g<Real, Net, 3>(cut);
     case 2:
-      return kernel_of_g<Real, Net, 2>();
+      return kernel_of_g<Real, Net, 2>(cut);
     case 1:
-      return kernel_of_g<Real, Net, 1>();
+      return kernel_of_g<Real, Net, 1>(cut);
     default:
-      return kernel_of_g<Real, Net, 0>();
+      return kernel_of_g<Real, Net, 0>(cut);
   }
 }
 
@@ -745,7 +753,8 @@ template <typename Real, class Net>
 int launch_rollout_impl(const RoundArgs& a, void* stream) {
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   auto k = kernel_of<Real, Net>(grid_kind(a.grid_mode, a.field_smem_bytes, a.field_ns, a.field_nd,
-                                               a.field_padded));
+                                               a.field_padded),
+                                 a.goal_cut != nullptr);
   const size_t smem = static_cast<size_t>(a.field_smem_bytes);
   if (smem > 32 * 1024) {
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
