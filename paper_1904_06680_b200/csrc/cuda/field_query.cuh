@@ -97,13 +97,22 @@ __device__ __forceinline__ Real point_margin(const Consts<Real>& K, Real x, Real
 // bounding circle; the prefilter can only matter at the rear corners within
 // rounding -- a narrow hit, which the marginal flag sends to the exact
 // re-ranking).
+// The pair (bx, by) = (fma(c, mx, fma(s, my, -kx)), fma(-s, mx, fma(c, my, -ky)))
+// in two packed FFMA2 with the point coordinate as the broadcast operand
+// (sm_100 FFMA2 Ra.F32 form): bit-identical to the scalar FMAs, half the issue.
 template <>
 __device__ __forceinline__ float point_margin<float>(const Consts<float>& K, float, float,
                                                      float c, float s, float kx, float ky,
                                                      float mx, float my) {
+#if PARAPLAN_FFMA2
+  const float2 t = __ffma2_rn(make_float2(my, my), make_float2(s, c), make_float2(-kx, -ky));
+  const float2 b = __ffma2_rn(make_float2(mx, mx), make_float2(c, -s), t);
+  return fminf(K.bhx - fabsf(b.x), K.hw - fabsf(b.y));
+#else
   const float bx = fmaf(c, mx, fmaf(s, my, -kx));
   const float by = fmaf(-s, mx, fmaf(c, my, -ky));
   return fminf(K.bhx - fabsf(bx), K.hw - fabsf(by));
+#endif
 }
 
 // Collision of the chassis at (x, y, phi) with row h. Only the grid cells
