@@ -94,6 +94,9 @@ __device__ __forceinline__ double2 ld_rec(const double2* p, unsigned long long p
   return __ldcg(p);
 #endif
 }
+#ifndef PARAPLAN_FAST_BOXMULLER
+#define PARAPLAN_FAST_BOXMULLER 1  // FP32 generator: MUFU log2 / sqrt in Box-Muller
+#endif
 #ifndef PARAPLAN_FFMA2
 // packed FP32x2 FMAs in the point scan (sm_100 FFMA2): the kind-3 scan body
 // drops from 39 to 29 instructions per 4 points, but the C2 rollout measured

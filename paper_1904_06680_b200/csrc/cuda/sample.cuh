@@ -42,7 +42,19 @@ __device__ __forceinline__ void draw_theta(const RoundArgs& a, uint64_t prefix, 
       const uint64_t m1 = g.next() >> 11, m2 = g.next() >> 11;
       const float u1 = __ull2float_rn((1ull << 53) - m1) * 0x1.0p-53f;
       const float u2 = __ull2float_rn(m2) * 0x1.0p-53f;
+#if PARAPLAN_FAST_BOXMULLER
+      // r = sqrt(-2 ln u1) with MUFU lg2 / rsqrt: ~1e-7 relative for r of
+      // order 1; near u1 = 1 (r < 0.02, 1.5e-4 of the draws) the absolute
+      // error of lg2.approx (2^-22.6) leaves r within ~2e-5 absolute. The
+      // FP32 path only (certified; the host regenerates the winner in FP64).
+      float l2, rr;
+      asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l2) : "f"(u1));
+      const float t2 = -1.3862943611198906f * l2;  // -2 ln 2 log2(u1) = -2 ln(u1)
+      asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(rr) : "f"(fmaxf(t2, 0.0f)));
+      const float r = rr;
+#else
       const float r = sqrtf(-2.0f * logf(u1));
+#endif
       // sincos(2 pi u2): quarter-turn reduction t = 4 u2 - q is exact
       const float q = rintf(4.0f * u2);
       const float t = fmaf(4.0f, u2, -q) * 1.57079632679489662f;
