@@ -457,9 +457,11 @@ def run_b200(a):
             "e2e": {"value": e2e_value, "unit": UNIT, "ms_per_step": e2e_s / a.steps * 1e3,
                     "h2d_bytes_per_step": h2d // a.steps, "d2h_bytes_per_step": d2h // a.steps,
                     "api": "paraplan.Planner.plan_step" if world == 1 else
-                           "pp_plan_step on a pp_comm_init rank (C++ sharded planner: "
-                           "ncclAllReduce(min) of packed winner keys + ncclAllGather of "
-                           "exact bests)"},
+                           ("ShardedPlanner.plan_step on ranks sharing a GPU (winner records "
+                            "exchanged over gloo; NCCL refuses a shared device)" if shared else
+                            "pp_plan_step on a pp_comm_init rank (C++ sharded planner: "
+                            "ncclAllReduce(min) of packed winner keys + ncclAllGather of "
+                            "exact bests)")},
             "latency_ms": e2e_s / a.steps * 1e3,
             "gpu_launches": st["launches"],
             "nccl": ({"ranks": world, "version": ".".join(map(str, torch.cuda.nccl.version()))}
