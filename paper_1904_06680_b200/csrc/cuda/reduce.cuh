@@ -210,7 +210,7 @@ __device__ __forceinline__ void write_skey(const RoundArgs& a, int64_t slot, int
 // Per-sample debug/parity record.
 template <typename Real>
 __device__ __forceinline__ void write_sample(const RoundArgs& a, int64_t slot, int cls,
-                                             const Lane<Real>& L, Real term) {
+                                             const Lane<Real>& L, Real term, Real f0, Real f1) {
   SampleOut& so = a.per_sample[slot];
   so.reached = cls == 2;
   so.t_goal = cls == 2 ? L.h : -1;
@@ -218,8 +218,8 @@ __device__ __forceinline__ void write_sample(const RoundArgs& a, int64_t slot, i
   so.steps = L.h;
   so.path_length = static_cast<double>(L.path);
   so.terminal_cost = static_cast<double>(term);
-  so.first_a0 = static_cast<double>(L.f0);
-  so.first_a1 = static_cast<double>(L.f1);
+  so.first_a0 = static_cast<double>(f0);
+  so.first_a1 = static_cast<double>(f1);
 }
 
 // Last CTA: per-restart reduction of `n_src` records per restart (laid out

@@ -81,8 +81,6 @@ __device__ __forceinline__ void load_state(Lane<Real>& L, const Real* v) {
   L.act = v[4];
   L.pa0 = v[5];
   L.path = v[6];
-  L.f0 = v[7];
-  L.f1 = v[8];
   L.h = 1;
   L.mstep = kNoStep;
   L.mpath = Real(0);
@@ -218,7 +216,9 @@ __global__ void __launch_bounds__(kBlock, refill_min_blocks<Real, Net>())
   int best_r = -1;
   int q_head = 32, q_count = 0, q_r = 0, q_c0 = 0;
   bool exhausted = false;
-  unsigned n_steps = 0, n_states = 0;  // per lane: a few candidates x H
+  // per lane: a few candidates x H. The checked states are the steps plus
+  // one per candidate (L.h + 1 each), added once for the whole round
+  unsigned n_steps = 0;
   const bool track = a.keys_only == 0;  // lane bests (one restart) or keys only
   // lane bests can cross restarts only when a launch holds several
   const bool cross = track && a.restart_count > 1;
@@ -325,9 +325,11 @@ __global__ void __launch_bounds__(kBlock, refill_min_blocks<Real, Net>())
         }
       }
       n_steps += static_cast<unsigned>(L.h);
-      n_states += static_cast<unsigned>(L.h + 1);
       if (a.per_sample != nullptr) {
-        write_sample(a, static_cast<int64_t>(my_r) * a.count + my_c, cls, L, term);
+        // the first action from the record (not kept in the lane's registers)
+        const Real* rv = reinterpret_cast<const Real*>(recs) +
+                         (static_cast<int64_t>(my_r) * a.count + my_c) * W + P;
+        write_sample(a, static_cast<int64_t>(my_r) * a.count + my_c, cls, L, term, rv[7], rv[8]);
       }
       write_skey(a, static_cast<int64_t>(my_r) * a.count + my_c, cls, L, term, tg);
       active = false;
@@ -337,10 +339,11 @@ __global__ void __launch_bounds__(kBlock, refill_min_blocks<Real, Net>())
   // -------- flush lane bests, combine warps, publish CTA records --------
   mark_end(a);
   const unsigned long long steps = block_sum(static_cast<unsigned long long>(n_steps), red_sum);
-  const unsigned long long states = block_sum(static_cast<unsigned long long>(n_states), red_sum);
   if (threadIdx.x == 0) {
     atomicAdd(&a.exec[0], steps);
-    atomicAdd(&a.exec[1], states);
+    atomicAdd(&a.exec[1], steps + (blockIdx.x == 0 ? static_cast<unsigned long long>(
+                                                         a.count * a.restart_count)
+                                                   : 0ull));
   }
   if (!track) return;  // reduce_keys_kernel forms the winners
   bool flush = best.cls >= 0;
@@ -491,7 +494,7 @@ __global__ void __launch_bounds__(kBlock) lockstep_kernel(const RoundArgs a) {
       n_steps += static_cast<unsigned long long>(L.h);
       n_states += static_cast<unsigned long long>(L.h + 1);
       if (a.per_sample != nullptr) {
-        write_sample(a, static_cast<int64_t>(r) * a.count + local, cls, L, term);
+        write_sample(a, static_cast<int64_t>(r) * a.count + local, cls, L, term, L.f0, L.f1);
       }
       write_skey(a, static_cast<int64_t>(r) * a.count + local, cls, L, term);
     }
