@@ -99,7 +99,7 @@ __device__ __forceinline__ double2 ld_rec(const double2* p, unsigned long long p
 #endif
 #ifndef PARAPLAN_FFMA2
 // packed FP32x2 FMAs in the point scan (sm_100 FFMA2): the kind-3 scan body
-// drops from 39 to 29 instructions per 4 points, but the C2 rollout measured
+// drops from 39 to 33 instructions per 4 points, but the C2 rollout measured
 // 0.6% slower and C4/C5 unchanged (A/B on B200), so it is off by default
 #define PARAPLAN_FFMA2 0
 #endif
