@@ -6,6 +6,7 @@
 // N = 100k, 25% moving, H = 100): rows are binned in parallel on the host
 // cores, each row independent.
 #include "field.hpp"
+#include "host_pool.hpp"
 
 #include <algorithm>
 #include <atomic>
@@ -30,24 +31,25 @@ double env_or(const char* name, double dflt) {
   return v != nullptr ? std::atof(v) : dflt;
 }
 
-// f(i) for i in [0, n), on up to 16 host threads when `work` is large.
+// f(i) for i in [0, n), on the process's host pool (host_pool.hpp) when
+// `work` is large. Spawning threads per call instead cost ~1 ms per binning
+// pass at C5's 100k points (measured: 2.7 ms of a 6.3 ms plan step).
+// Loops nested in a parallel loop run serially on their worker.
+thread_local bool tl_in_par = false;
 template <class F>
 void par_for(int n, size_t work, F&& f) {
-  if (work < (size_t(1) << 17) || n <= 1) {
+  if (work < (size_t(1) << 17) || n <= 1 || tl_in_par) {
     for (int i = 0; i < n; ++i) f(i);
     return;
   }
-  static const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
-  const unsigned T = std::min<unsigned>({16u, hw, static_cast<unsigned>(n)});
-  std::atomic<int> next{0};
-  const auto body = [&] {
-    for (int i; (i = next.fetch_add(1)) < n;) f(i);
+  ppcapi::SharedPool& sp = ppcapi::shared_pool();
+  std::lock_guard<std::mutex> turn(sp.mu);
+  const std::function<void(int)> fn = [&](int i) {
+    tl_in_par = true;
+    f(i);
+    tl_in_par = false;
   };
-  std::vector<std::thread> th;
-  th.reserve(T - 1);
-  for (unsigned t = 1; t < T; ++t) th.emplace_back(body);
-  body();
-  for (auto& t : th) t.join();
+  sp.pool->run(n, fn);
 }
 
 struct BBox {
@@ -105,10 +107,45 @@ struct CellOf {
 };
 
 // Stable counting sort of n points (xy) into `out` (cell order) + starts.
+// Large inputs: per-block histograms, then each block scatters at its own
+// offsets (the same stable order).
 void bin(const Binned& b, const double* xy, int n, double* out, int32_t* starts,
          std::vector<int32_t>& cell) {
   const int cells = b.cells();
   const CellOf cell_of(b);
+  constexpr int kBinBlock = 8192;
+  if (n >= 4 * kBinBlock && !tl_in_par) {
+    const int nblk = (n + kBinBlock - 1) / kBinBlock;
+    cell.resize(n);
+    std::vector<int32_t> cnt(static_cast<size_t>(nblk) * cells, 0);
+    par_for(nblk, static_cast<size_t>(n) * 4, [&](int k) {
+      int32_t* ck = cnt.data() + static_cast<size_t>(k) * cells;
+      for (int j = k * kBinBlock; j < std::min(n, (k + 1) * kBinBlock); ++j) {
+        cell[j] = cell_of(xy[2 * j], xy[2 * j + 1]);
+        ++ck[cell[j]];
+      }
+    });
+    // starts, and per block its cursor into each cell (in place of cnt)
+    int32_t run = 0;
+    for (int c = 0; c < cells; ++c) {
+      starts[c] = run;
+      for (int k = 0; k < nblk; ++k) {
+        const int32_t v = cnt[static_cast<size_t>(k) * cells + c];
+        cnt[static_cast<size_t>(k) * cells + c] = run;
+        run += v;
+      }
+    }
+    starts[cells] = run;
+    par_for(nblk, static_cast<size_t>(n) * 4, [&](int k) {
+      int32_t* ck = cnt.data() + static_cast<size_t>(k) * cells;
+      for (int j = k * kBinBlock; j < std::min(n, (k + 1) * kBinBlock); ++j) {
+        const int at = ck[cell[j]]++;
+        out[2 * at] = xy[2 * j];
+        out[2 * at + 1] = xy[2 * j + 1];
+      }
+    });
+    return;
+  }
   cell.resize(n);
   std::fill(starts, starts + cells + 1, 0);
   for (int j = 0; j < n; ++j) {
@@ -190,10 +227,16 @@ void cell_boxes(Binned& b) {
         const double x = b.spts[2 * (j0 + k)], y = b.spts[2 * (j0 + k) + 1];
         uint32_t ix = static_cast<uint32_t>((x - (bx[0] - bx[2])) * sx);
         uint32_t iy = static_cast<uint32_t>((y - (bx[1] - bx[3])) * sy);
-        uint32_t z = 0;
-        for (int bit = 0; bit < 15; ++bit) {
-          z |= ((ix >> bit) & 1u) << (2 * bit) | ((iy >> bit) & 1u) << (2 * bit + 1);
-        }
+        // bit interleave (Morton) of the 15-bit coordinates
+        const auto spread = [](uint32_t v) {
+          v &= 0x7fffu;
+          v = (v | (v << 8)) & 0x00ff00ffu;
+          v = (v | (v << 4)) & 0x0f0f0f0fu;
+          v = (v | (v << 2)) & 0x33333333u;
+          v = (v | (v << 1)) & 0x55555555u;
+          return v;
+        };
+        const uint32_t z = spread(ix) | (spread(iy) << 1);
         key[k] = {z, k};
       }
       std::stable_sort(key.begin(), key.end(),

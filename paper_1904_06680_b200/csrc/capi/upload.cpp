@@ -114,6 +114,7 @@ void finish_field(pp_handle* h, ppdev::RoundArgs& a) {
       // the device bins the movers itself: upload the static parts and the
       // raw movers only (csrc/cuda/binning_f64.cu)
       ppfield::pack(b, h->fp64, h->h_field.p, false);
+      phase("packed");
       unsigned char* hf = static_cast<unsigned char*>(h->h_field.p);
       unsigned char* df = static_cast<unsigned char*>(h->d_field.p);
       const auto part = [&](size_t lo, size_t hi) {
@@ -248,6 +249,7 @@ void upload_points(pp_handle* h, const pp_snapshot_points& p, bool defer) {
     a.n_points = p.n_points;
     const double cull = std::sqrt(a.r2) + 1e-3;
     ppfield::from_points(h->field, p.points, p.n_points, h->cfg.H + 1, p.T_s, cull, defer);
+    phase("points-binned");
     if (h->field.dyn_deferred &&
         static_cast<int64_t>(h->field.Nd) * h->field.rows < device_bin_min()) {
       ppfield::bin_dynamic(h->field);  // small: the host bins it at once
