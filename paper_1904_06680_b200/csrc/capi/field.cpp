@@ -358,12 +358,16 @@ void from_rows(Binned& b, const double* xy, int rows, int N, double cull) {
   reset(b, rows, cull);
   const size_t len = 2 * static_cast<size_t>(N);
   std::vector<char> moving(N, 0);
-  for (int r = 1; r < rows; ++r) {
-    const double* row = xy + r * len;
-    for (int j = 0; j < N; ++j) {
-      moving[j] |= std::memcmp(row + 2 * j, xy + 2 * j, 2 * sizeof(double)) != 0;
+  constexpr int kPtBlock = 2048;  // a block's slice of a row: 32 KB
+  par_for((N + kPtBlock - 1) / kPtBlock, static_cast<size_t>(rows) * N, [&](int k) {
+    const int j0 = k * kPtBlock, j1 = std::min(N, (k + 1) * kPtBlock);
+    for (int r = 1; r < rows; ++r) {
+      const double* row = xy + r * len;
+      for (int j = j0; j < j1; ++j) {
+        moving[j] |= std::memcmp(row + 2 * j, xy + 2 * j, 2 * sizeof(double)) != 0;
+      }
     }
-  }
+  });
   // small mixed clouds stay one scan per state: every point dynamic
   if (N <= kSmall && std::count(moving.begin(), moving.end(), 1) > 0) {
     std::fill(moving.begin(), moving.end(), 1);
