@@ -98,6 +98,8 @@ void prewarm(pp_handle* h) {
   h->timing = pp_timing{};
   h->prefer_fp64 = false;  // the warm-up's fake snapshot says nothing about real ticks
   h->expect_reach = true;
+  h->flush_every = 3;
+  h->flush_min = 0;
 }
 
 // The exchange of an in-process sharded planner (PlannerConfig::devices):

@@ -194,6 +194,14 @@ inline int cut_slack() {
   }();
   return v;
 }
+// PARAPLAN_FLUSH_EVERY=k: a fixed flush period (A/B experiments only)
+inline int flush_every_fixed() {
+  static const int v = [] {
+    const char* e = std::getenv("PARAPLAN_FLUSH_EVERY");
+    return e != nullptr ? std::max(1, std::atoi(e)) : 0;
+  }();
+  return v;
+}
 inline bool goal_cut_enabled() {
   static const bool v = [] {
     const char* e = std::getenv("PARAPLAN_GOAL_CUT");
@@ -280,6 +288,10 @@ struct pp_handle {
   // the last round's winner reached the goal: the next round runs the cut's
   // kernel (round.cpp)
   bool expect_reach = true;
+  // rollout warps flush finished lanes every flush_every-th iteration, sized
+  // from the last round's mean rollout length (round.cpp)
+  int flush_every = 3;
+  int flush_min = 0;
 
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;

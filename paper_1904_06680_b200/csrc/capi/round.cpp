@@ -196,6 +196,8 @@ void run_round_launch(pp_handle* h, uint64_t t, int iter, int r0, int rc, const 
   a.cut_pub = reinterpret_cast<uint32_t*>(dres + kCutPubOff);
   a.cut_slack = cut_slack();
   a.cut_slots = rc;
+  a.flush_every = flush_every_fixed() > 0 ? flush_every_fixed() : h->flush_every;
+  a.flush_min = flush_every_fixed() > 0 ? 0 : h->flush_min;
   // several restarts on the refill schedule: winners from the sample keys
   const bool keys_only = shape0.refill && rc > 1;
   a.keys_only = keys_only ? 1 : 0;
@@ -341,6 +343,15 @@ void run_round_launch(pp_handle* h, uint64_t t, int iter, int r0, int rc, const 
   const char* hres = static_cast<const char*>(h->h_round.p);
   const unsigned long long* ex = reinterpret_cast<const unsigned long long*>(hres + kExecOff);
   h->timing.executed_steps += static_cast<int64_t>(ex[2]);
+  // the next round's flush rule, from this round's mean rollout length
+  // (measured on B200: rollouts of ~9 steps (C5 H=10) flush best every 2
+  // iterations, ~11-13 steps (C2, C5 H >= 30) every 3, ~20 and more (C4)
+  // once 6 lanes wait, else every 6)
+  if (count * rc > 0 && ex[2] > 0) {
+    const double mean = static_cast<double>(ex[2]) / static_cast<double>(count * rc);
+    h->flush_every = mean <= 10.0 ? 2 : (mean <= 16.0 ? 3 : 6);
+    h->flush_min = mean <= 16.0 ? 0 : 6;
+  }
   h->timing.checked_states += static_cast<int64_t>(ex[3]);
   h->timing.rollout_ms += 1e-6 * static_cast<double>(ex[6]);
   const ppdev::Rec* recs = reinterpret_cast<const ppdev::Rec*>(hres + kRecOff);

@@ -229,6 +229,11 @@ struct RoundArgs {
   uint32_t* cut_pub;
   int32_t cut_slack;
   int32_t cut_slots;
+  // refill schedule: a warp writes its finished lanes' keys and refills them
+  // every flush_every-th iteration (>= 1), or (flush_min > 0) as soon as
+  // flush_min of its lanes wait
+  int32_t flush_every;
+  int32_t flush_min;
 };
 
 // Architecture dispatch of the specialised kernels.

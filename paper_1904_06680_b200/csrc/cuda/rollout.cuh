@@ -233,61 +233,107 @@ __global__ void __launch_bounds__(kBlock, refill_min_blocks<Real, Net>())
   int cut_at = kNoCut;
   unsigned iter = 0;
 
+  // A lane whose rollout ends parks its class in `pend`; its keys are written
+  // and it is refilled at the warp's next flush, every a.flush_every-th
+  // iteration. The flush code runs for the whole warp whenever any lane
+  // needs it, so batching it trades parked lane-steps for fewer flushes
+  // (the host sizes it from the last round's mean rollout length).
+  int pend = -1;  // class of a finished rollout (| 4: cut) awaiting its keys
+  int flush_cd = 1;
   for (;;) {
-    // -------- hand the warp's current batch to idle lanes --------
-    const unsigned need = __ballot_sync(kFull, !active);
-    if (need != 0u) {
-      if (q_head >= q_count && !exhausted) {
-        unsigned b = 0;
-        if (lane == 0) b = atomicAdd(&a.counters[0], 1u);
-        b = __shfl_sync(kFull, b, 0);
-        if (b >= total_batches) {
-          exhausted = true;
-        } else {
-          q_r = static_cast<int>(b) / bpr;
-          q_c0 = (static_cast<int>(b) - q_r * bpr) * 32;
-          const int64_t left = a.count - q_c0;
-          q_count = left < 32 ? static_cast<int>(left) : 32;
-          q_head = 0;
-          // the batch's records into L1: the lanes refill from it over the
-          // next iterations (all but the first few hit L1)
-          if (lane < q_count) {
-            const char* rp = reinterpret_cast<const char*>(
-                recs + (static_cast<int64_t>(q_r) * a.count + q_c0 + lane) * V);
-            prefetch_l1(rp);
-            prefetch_l1(rp + W * static_cast<int>(sizeof(Real)) - 1);
-          }
-        }
+    // every a.flush_every-th iteration (a countdown); the goal-cut variant,
+    // whose rounds can hold long rollouts, also once a.flush_min lanes wait
+    bool flush_now = --flush_cd <= 0;
+    if (kCut && a.flush_min > 0) {
+      flush_now |= __popc(__ballot_sync(kFull, !active)) >= a.flush_min;
+    }
+    if (flush_now) flush_cd = a.flush_every;
+    if (flush_now) {
+      // -------- finished lanes: keys and lane bests --------
+      // lane bests are per restart: flush the old one before crossing over
+      if (cross) {
+        bool flush = pend >= 0 && best.cls >= 0 && best_r != my_r;
+        if (__any_sync(kFull, flush)) flush_bests(flush, best, best_r, table[warp], lane);
       }
-      const int avail = q_count - q_head;
-      if (avail > 0) {
-        const int rank = __popc(need & ((1u << lane) - 1u));
-        if (!active && rank < avail) {
-          my_r = q_r;
-          my_c = q_c0 + q_head + rank;
-          const int64_t sidx = static_cast<int64_t>(my_r) * a.count + my_c;
-          // contiguous 16-byte aligned record: V vector loads
-          union {
-            Real v[W];
-            Vec16<Real> q[V];
-          } rec;
-#pragma unroll
-          for (int j = 0; j < V; ++j) rec.q[j] = ld_rec(recs + sidx * V + j, drop);
-#pragma unroll
-          for (int i = 0; i < P; ++i) net.w[i] = rec.v[i];
-          if (cls0 < 0) {
-            load_state(L, rec.v + P);
-          } else {
-            L.start(K, Real(0), Real(0));
-            L.ephi = ephi0;
+      if (pend >= 0) {
+        const int cls = pend & 3;
+        const bool cut = (pend & 4) != 0;
+        const Real term = terminal_cost(L, K);
+        const int tg = cut ? kCutTGoal : L.h;
+        if (track) {
+          const LaneKey<Real> k =
+              make_lane_key<Real>(cls, tg, L.path, term, static_cast<int>(a.cand_begin + my_c));
+          if (best.cls < 0 || prefer(k, best)) {
+            best = k;
+            best_r = my_r;
           }
-          active = true;
-          if (kCut && a.restart_count > 1) cut_at = kNoCut;
         }
-        q_head += __popc(need) < avail ? __popc(need) : avail;
+        n_steps += static_cast<unsigned>(L.h);
+        if (a.per_sample != nullptr) {
+          // the first action from the record (not kept in the lane's registers)
+          const Real* rv = reinterpret_cast<const Real*>(recs) +
+                           (static_cast<int64_t>(my_r) * a.count + my_c) * W + P;
+          write_sample(a, static_cast<int64_t>(my_r) * a.count + my_c, cls, L, term, rv[7], rv[8]);
+        }
+        write_skey(a, static_cast<int64_t>(my_r) * a.count + my_c, cls, L, term, tg);
+        pend = -1;
+      }
+      // -------- hand the warp's current batch to idle lanes --------
+      const unsigned need = __ballot_sync(kFull, !active);
+      if (need != 0u) {
+        if (q_head >= q_count && !exhausted) {
+          unsigned b = 0;
+          if (lane == 0) b = atomicAdd(&a.counters[0], 1u);
+          b = __shfl_sync(kFull, b, 0);
+          if (b >= total_batches) {
+            exhausted = true;
+          } else {
+            q_r = static_cast<int>(b) / bpr;
+            q_c0 = (static_cast<int>(b) - q_r * bpr) * 32;
+            const int64_t left = a.count - q_c0;
+            q_count = left < 32 ? static_cast<int>(left) : 32;
+            q_head = 0;
+            // the batch's records into L1: the lanes refill from it over the
+            // next iterations (all but the first few hit L1)
+            if (lane < q_count) {
+              const char* rp = reinterpret_cast<const char*>(
+                  recs + (static_cast<int64_t>(q_r) * a.count + q_c0 + lane) * V);
+              prefetch_l1(rp);
+              prefetch_l1(rp + W * static_cast<int>(sizeof(Real)) - 1);
+            }
+          }
+        }
+        const int avail = q_count - q_head;
+        if (avail > 0) {
+          const int rank = __popc(need & ((1u << lane) - 1u));
+          if (!active && rank < avail) {
+            my_r = q_r;
+            my_c = q_c0 + q_head + rank;
+            const int64_t sidx = static_cast<int64_t>(my_r) * a.count + my_c;
+            // contiguous 16-byte aligned record: V vector loads
+            union {
+              Real v[W];
+              Vec16<Real> q[V];
+            } rec;
+#pragma unroll
+            for (int j = 0; j < V; ++j) rec.q[j] = ld_rec(recs + sidx * V + j, drop);
+#pragma unroll
+            for (int i = 0; i < P; ++i) net.w[i] = rec.v[i];
+            if (cls0 < 0) {
+              load_state(L, rec.v + P);
+            } else {
+              L.start(K, Real(0), Real(0));
+              L.ephi = ephi0;
+            }
+            active = true;
+            if (kCut && a.restart_count > 1) cut_at = kNoCut;
+          }
+          q_head += __popc(need) < avail ? __popc(need) : avail;
+        }
       }
     }
-    if (!__any_sync(kFull, active)) break;  // stream exhausted, all lanes done
+    // stream exhausted, all lanes done and flushed
+    if (!__any_sync(kFull, active || pend >= 0)) break;
 
     // -------- one rollout state per lane --------
     uint32_t cut_ld = kCutNone;  // used after the step
@@ -307,31 +353,8 @@ __global__ void __launch_bounds__(kBlock, refill_min_blocks<Real, Net>())
       }
       if (cut) cls = 2;
     }
-    const bool done = active && cls >= 0;
-    // lane bests are per restart: flush the old one before crossing over
-    if (cross) {
-      bool flush = done && best.cls >= 0 && best_r != my_r;
-      if (__any_sync(kFull, flush)) flush_bests(flush, best, best_r, table[warp], lane);
-    }
-    if (done) {
-      const Real term = terminal_cost(L, K);
-      const int tg = cut ? kCutTGoal : L.h;
-      if (track) {
-        const LaneKey<Real> k =
-            make_lane_key<Real>(cls, tg, L.path, term, static_cast<int>(a.cand_begin + my_c));
-        if (best.cls < 0 || prefer(k, best)) {
-          best = k;
-          best_r = my_r;
-        }
-      }
-      n_steps += static_cast<unsigned>(L.h);
-      if (a.per_sample != nullptr) {
-        // the first action from the record (not kept in the lane's registers)
-        const Real* rv = reinterpret_cast<const Real*>(recs) +
-                         (static_cast<int64_t>(my_r) * a.count + my_c) * W + P;
-        write_sample(a, static_cast<int64_t>(my_r) * a.count + my_c, cls, L, term, rv[7], rv[8]);
-      }
-      write_skey(a, static_cast<int64_t>(my_r) * a.count + my_c, cls, L, term, tg);
+    if (active && cls >= 0) {
+      pend = cls | (cut ? 4 : 0);
       active = false;
     }
   }

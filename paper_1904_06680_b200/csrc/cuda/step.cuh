@@ -153,12 +153,6 @@ __device__ __forceinline__ void first_step(Lane<Real>& L, const Consts<Real>& K)
   commit(L, n, L.f0);
 }
 
-// One state of the rollout loop (src/planner.cpp:137-183): the checks of
-// state h and, independent of them, the MLP and transition to state h + 1,
-// committed only by lanes still running. Returns -1 while running, else the
-// class at state h. Warp-synchronous and branch-free: the checks and the
-// next state are computed for every lane, so the warp never splits into
-// per-outcome paths.
 // Whether a refill-schedule net's weights are prescaled (nets.cuh prescale):
 // FP32 register nets with the fast tanh.
 template <typename Real, class Net>
@@ -166,6 +160,14 @@ constexpr bool prescaled(bool refill) {
   return refill && sizeof(Real) == sizeof(float) && Net::kP > 0 && !PARAPLAN_ACCURATE_TANH;
 }
 
+// One state of the rollout loop (src/planner.cpp:137-183): the checks of
+// state h and, independent of them, the MLP and transition to state h + 1,
+// committed only by lanes still running (live, and no verdict at h).
+// Returns -1 while running, else the class at state h. Warp-synchronous and
+// branch-free: the checks and the next state are computed for every lane, so
+// the warp never splits into per-outcome paths; a lane with live == false
+// (idle, or parked with a finished rollout until the warp's next flush) scans
+// no points and keeps its state.
 // kFromZero: lanes may be at state 0 (the lockstep schedules), whose action
 // is the precomputed first one; otherwise the lanes come from the refill
 // schedule's records (state >= 1, prescaled weights where prescaled()).
@@ -197,7 +199,7 @@ __device__ __forceinline__ int advance(Lane<Real>& L, const Net& net, const Cons
     a1 = L.f1;
   }
   const Next<Real> n = transition(L, K, a0, a1, sphi, cphi);
-  if (cls < 0) commit(L, n, a0);
+  if (live && cls < 0) commit(L, n, a0);  // a parked or idle lane keeps its state
   return cls;
 }
 
