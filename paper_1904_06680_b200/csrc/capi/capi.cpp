@@ -373,17 +373,9 @@ pp_status pp_draw_theta(pp_handle* h, const double* center, int32_t len, uint64_
     a.count = n;
     a.restart_count = 1;
     a.cand_begin = cand_begin;
-    const size_t pbytes = sizeof(uint64_t) + sizeof(double) * h->P;
-    h->h_params.reserve(pbytes, "pinned params");
-    h->d_params.reserve(pbytes, "device params");
-    uint64_t* hp = static_cast<uint64_t*>(h->h_params.p);
-    hp[0] = key_prefix(h->cfg.master_seed, t, static_cast<uint64_t>(restart),
-                       static_cast<uint64_t>(iter));
-    std::memcpy(hp + 1, center, sizeof(double) * h->P);
-    ck(cudaMemcpyAsync(h->d_params.p, h->h_params.p, pbytes, cudaMemcpyHostToDevice, h->stream),
-       "params H2D");
-    a.key_prefix = static_cast<const uint64_t*>(h->d_params.p);
-    a.center = reinterpret_cast<const double*>(static_cast<uint64_t*>(h->d_params.p) + 1);
+    const uint64_t prefix = key_prefix(h->cfg.master_seed, t, static_cast<uint64_t>(restart),
+                                       static_cast<uint64_t>(iter));
+    upload_params(h, a, &prefix, 1, center);
     const size_t esz = h->fp64 ? sizeof(double) : sizeof(float);
     const size_t bytes = esz * h->P * static_cast<size_t>(n);
     h->d_samples.reserve(bytes, "theta draws");

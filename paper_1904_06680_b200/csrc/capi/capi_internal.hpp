@@ -380,6 +380,8 @@ void upload_points(pp_handle* h, const pp_snapshot_points& p, bool defer = false
 void upload_snapshot(pp_handle* h, const pp_snapshot& s, bool defer = false);
 
 // round.cpp
+void upload_params(pp_handle* h, ppdev::RoundArgs& a, const uint64_t* prefix, int n_prefix,
+                   const double* center);
 void grow_selection(pp_handle* h, ppdev::RoundArgs& a, int cap);
 uint64_t key_prefix(uint64_t seed, uint64_t t, uint64_t r, uint64_t i);
 ppdev::LaunchShape launch_shape(pp_handle* h, bool fp64, int field_smem, int kind);

@@ -108,6 +108,32 @@ void consume_pending_field(pp_handle* h, bool side) {
 // With re-ranking on, the round is followed by the near-tie window select,
 // the FP64 re-evaluation of the window and a host re-rank of FP64 near-ties
 // in the reference's own arithmetic, so the winner is the reference's.
+// The round's params block, [prefix u64 x n_prefix][centre f64 x P][centre
+// rounded to f32 x P] (the FP32 generator adds sigma * N(0,1) to the float
+// centre; the host's (float) rounding is the device's), on the handle's
+// stream; a.key_prefix / a.center / a.center_f point into it.
+void upload_params(pp_handle* h, ppdev::RoundArgs& a, const uint64_t* prefix, int n_prefix,
+                   const double* center) {
+  const size_t pbytes = sizeof(uint64_t) * n_prefix + sizeof(double) * h->P + sizeof(float) * h->P;
+  h->h_params.reserve(pbytes, "pinned params");
+  h->d_params.reserve(pbytes, "device params");
+  uint64_t* hp = static_cast<uint64_t*>(h->h_params.p);
+  std::memcpy(hp, prefix, sizeof(uint64_t) * n_prefix);
+  double* hc = reinterpret_cast<double*>(hp + n_prefix);
+  float* hf = reinterpret_cast<float*>(hc + h->P);
+  for (int i = 0; i < h->P; ++i) {
+    hc[i] = center != nullptr ? center[i] : 0.0;
+    hf[i] = static_cast<float>(hc[i]);
+  }
+  ck(cudaMemcpyAsync(h->d_params.p, h->h_params.p, pbytes, cudaMemcpyHostToDevice, h->stream),
+     "params H2D");
+  h->timing.h2d_bytes += static_cast<int64_t>(pbytes);
+  const uint64_t* dp = static_cast<const uint64_t*>(h->d_params.p);
+  a.key_prefix = dp;
+  a.center = reinterpret_cast<const double*>(dp + n_prefix);
+  a.center_f = reinterpret_cast<const float*>(a.center + h->P);
+}
+
 void run_round_launch(pp_handle* h, uint64_t t, int iter, int r0, int rc, const double* center,
                       int64_t c0, int64_t c1, const double* injected, pp_record* out,
                       pp_rollout_stats* per_sample, bool force_fp64) {
@@ -137,26 +163,12 @@ void run_round_launch(pp_handle* h, uint64_t t, int iter, int r0, int rc, const 
   a.count = count;
   a.queue_bytes = 0;
 
-  // params block: [prefix u64 x rc][center f64 x P]
-  const size_t pbytes = sizeof(uint64_t) * rc + sizeof(double) * h->P;
-  h->h_params.reserve(pbytes, "pinned params");
-  h->d_params.reserve(pbytes, "device params");
-  uint64_t* hp = static_cast<uint64_t*>(h->h_params.p);
+  std::vector<uint64_t> prefixes(rc);
   for (int r = 0; r < rc; ++r) {
-    hp[r] = key_prefix(h->cfg.master_seed, t, static_cast<uint64_t>(r0 + r),
-                       static_cast<uint64_t>(iter));
+    prefixes[r] = key_prefix(h->cfg.master_seed, t, static_cast<uint64_t>(r0 + r),
+                             static_cast<uint64_t>(iter));
   }
-  double* hc = reinterpret_cast<double*>(hp + rc);
-  if (center != nullptr) {
-    std::memcpy(hc, center, sizeof(double) * h->P);
-  } else {
-    std::fill(hc, hc + h->P, 0.0);
-  }
-  ck(cudaMemcpyAsync(h->d_params.p, h->h_params.p, pbytes, cudaMemcpyHostToDevice, h->stream),
-     "params H2D");
-  h->timing.h2d_bytes += static_cast<int64_t>(pbytes);
-  a.key_prefix = static_cast<const uint64_t*>(h->d_params.p);
-  a.center = reinterpret_cast<const double*>(static_cast<uint64_t*>(h->d_params.p) + rc);
+  upload_params(h, a, prefixes.data(), rc, center);
 
   if (injected != nullptr) {
     const size_t ib = sizeof(double) * h->P * static_cast<size_t>(count);

@@ -149,6 +149,7 @@ struct RoundArgs {
   int64_t count;
   const uint64_t* key_prefix;  // device [restart_count]: fold^4(seed, t, r, iter)
   const double* center;        // device [n_params]
+  const float* center_f;       // device [n_params]: center rounded to float
   const double* injected;      // device [count * n_params] or null (RNG off)
   // Obstacle field image (see csrc/capi/field.hpp): [static pts Real2 x Ns]
   // [dynamic pts Real2 x (H+1) x Nd][static starts int32 x (cells+1)]

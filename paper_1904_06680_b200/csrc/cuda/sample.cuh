@@ -64,8 +64,8 @@ __device__ __forceinline__ void draw_theta(const RoundArgs& a, uint64_t prefix, 
       float cs = (qi & 1) ? sp : cp;
       sn = (qi & 2) ? -sn : sn;
       cs = ((qi + 1) & 2) ? -cs : cs;
-      put(i, Real(static_cast<float>(__ldg(center + i)) + sigma * (r * cs)));
-      if (i + 1 < P) put(i + 1, Real(static_cast<float>(__ldg(center + i + 1)) + sigma * (r * sn)));
+      put(i, Real(__ldg(a.center_f + i) + sigma * (r * cs)));
+      if (i + 1 < P) put(i + 1, Real(__ldg(a.center_f + i + 1) + sigma * (r * sn)));
     }
   } else {
     const double sigma = pow(10.0, a.sig_lo + unit53(g.next()) * a.sig_span);
