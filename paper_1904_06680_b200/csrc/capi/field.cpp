@@ -35,10 +35,15 @@ double env_or(const char* name, double dflt) {
 // `work` is large. Spawning threads per call instead cost ~1 ms per binning
 // pass at C5's 100k points (measured: 2.7 ms of a 6.3 ms plan step).
 // Loops nested in a parallel loop run serially on their worker.
+// PARAPLAN_FIELD_SERIAL=1: every pass serial (tests compare the two).
 thread_local bool tl_in_par = false;
+bool field_serial() {
+  static const bool v = env_or("PARAPLAN_FIELD_SERIAL", 0) != 0;
+  return v;
+}
 template <class F>
 void par_for(int n, size_t work, F&& f) {
-  if (work < (size_t(1) << 17) || n <= 1 || tl_in_par) {
+  if (work < (size_t(1) << 17) || n <= 1 || tl_in_par || field_serial()) {
     for (int i = 0; i < n; ++i) f(i);
     return;
   }
@@ -114,7 +119,7 @@ void bin(const Binned& b, const double* xy, int n, double* out, int32_t* starts,
   const int cells = b.cells();
   const CellOf cell_of(b);
   constexpr int kBinBlock = 8192;
-  if (n >= 4 * kBinBlock && !tl_in_par) {
+  if (n >= 4 * kBinBlock && !tl_in_par && !field_serial()) {
     const int nblk = (n + kBinBlock - 1) / kBinBlock;
     cell.resize(n);
     std::vector<int32_t> cnt(static_cast<size_t>(nblk) * cells, 0);

@@ -97,6 +97,9 @@ __device__ __forceinline__ double2 ld_rec(const double2* p, unsigned long long p
 #ifndef PARAPLAN_FAST_BOXMULLER
 #define PARAPLAN_FAST_BOXMULLER 1  // FP32 generator: MUFU log2 / sqrt in Box-Muller
 #endif
+#ifndef PARAPLAN_SELECT_BPS
+#define PARAPLAN_SELECT_BPS 16  // window select: blocks per SM
+#endif
 #ifndef PARAPLAN_FFMA2
 // packed FP32x2 FMAs in the point scan (sm_100 FFMA2): the kind-3 scan body
 // drops from 39 to 33 instructions per 4 points, but the C2 rollout measured

@@ -809,7 +809,7 @@ int launch_rollout_impl(const RoundArgs& a, void* stream) {
 // Near-tie window of a finished round (a dependent launch after the rollout).
 inline int launch_select_impl(const RoundArgs& a, void* stream) {
   const int64_t total = a.count * a.restart_count;
-  const int blocks = static_cast<int>(std::min<int64_t>((total + 255) / 256, std::max(a.sms, 1) * 16));
+  const int blocks = static_cast<int>(std::min<int64_t>((total + 255) / 256, std::max(a.sms, 1) * PARAPLAN_SELECT_BPS));
   return static_cast<int>(
       launch_dependent(select_kernel, blocks, 256, 0, static_cast<cudaStream_t>(stream), true, a));
 }
