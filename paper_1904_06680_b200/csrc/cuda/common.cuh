@@ -34,7 +34,10 @@ constexpr int kWarps = kBlock / 32;
 #define PARAPLAN_FAST_SQRT 1
 #endif
 #ifndef PARAPLAN_GEN_MINB
-#define PARAPLAN_GEN_MINB 1  // theta generator: resident CTAs the register cap must allow
+// theta generator of the small FP32 net ([5,2,2]): resident CTAs of 256 the
+// register cap must allow (6: 40 registers, no spills; measured 2% faster
+// than 4 CTAs at C2 once the Box-Muller runs in MUFU); other nets: 1
+#define PARAPLAN_GEN_MINB 6
 #endif
 #ifndef PARAPLAN_REFILL64_MINB
 #define PARAPLAN_REFILL64_MINB 4  // FP64 [5,2,2]/[5,10,2]: <= 128 registers

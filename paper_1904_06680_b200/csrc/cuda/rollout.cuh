@@ -126,7 +126,8 @@ __device__ __forceinline__ void generate_one(const RoundArgs& a, const Consts<Re
 }
 
 template <typename Real, class Net>
-__global__ void __launch_bounds__(256, PARAPLAN_GEN_MINB) generate_kernel(const RoundArgs a) {
+__global__ void __launch_bounds__(256, sizeof(Real) == 4 && Net::P <= 24 ? PARAPLAN_GEN_MINB : 1)
+    generate_kernel(const RoundArgs a) {
   constexpr int P = Net::P;
   constexpr int W = rec_width<Real>(P);
   constexpr int V = W * static_cast<int>(sizeof(Real)) / 16;
@@ -141,7 +142,8 @@ __global__ void __launch_bounds__(256, PARAPLAN_GEN_MINB) generate_kernel(const 
     // list round draws item s = candidate list[s] of the listed round
     const int64_t flat = a.list != nullptr ? a.list[s] : s;
     const int64_t cnt = a.list != nullptr ? a.list_count : a.count;
-    const int r = flat <= 0x7fffffff && cnt <= 0x7fffffff
+    const int r = flat < cnt ? 0  // one restart (and a list of one): no division
+                  : flat <= 0x7fffffff && cnt <= 0x7fffffff
                       ? static_cast<int>(static_cast<uint32_t>(flat) / static_cast<uint32_t>(cnt))
                       : static_cast<int>(flat / cnt);
     const int64_t local = flat - static_cast<int64_t>(r) * cnt;
