@@ -58,7 +58,8 @@ int host_max() {
 //   FP32, class 0/1 (cost = terminal cost), H <= 30:      <= 1.4e-6
 //   FP32, class 0/1, H >= 60:  up to 2.2e-2 (H 60) ... 0.5 (H 200): chaotic
 //                              amplification through saturated steering
-//   FP64 (device libm, no contraction), any H, class:     <= 5.1e-10
+//   FP64 (no contraction), class 0/1: <= 2e-12 (H <= 60), <= 5.6e-9 (H 200);
+//   class 2: <= 1.1e-13
 // So an FP32 round is certified with rho = 1e-3 only where that envelope
 // holds with a wide margin: every class up to H = fp32_max_h() (40), class 2
 // beyond. A longer round whose anchor is of class 0/1 is redone in FP64, and

@@ -103,6 +103,9 @@ __device__ __forceinline__ double2 ld_rec(const double2* p, unsigned long long p
 #ifndef PARAPLAN_SELECT_BPS
 #define PARAPLAN_SELECT_BPS 16  // window select: blocks per SM
 #endif
+#ifndef PARAPLAN_FAST_FP64
+#define PARAPLAN_FAST_FP64 1  // FP64 rollout: branch-free tanh, polynomial tan (|x| <= pi/4)
+#endif
 #ifndef PARAPLAN_FFMA2
 // packed FP32x2 FMAs in the point scan (sm_100 FFMA2): the kind-3 scan body
 // drops from 39 to 33 instructions per 4 points, but the C2 rollout measured
@@ -243,9 +246,37 @@ struct M<float> {
 
 template <>
 struct M<double> {
+#if PARAPLAN_FAST_FP64
+  // tanh(x) = sign(x) (1 - 2 / (exp(2|x|) + 1)): branch-free (libdevice's
+  // tanh takes a polynomial path below |x| = 0.55 and an exp path above, and
+  // a warp runs both), absolute error a few ulp of 1 (the policy's outputs
+  // are clamped actions: absolute accuracy is what propagates). The FP64
+  // rollout is certified against the reference's own arithmetic like the
+  // FP32 one; its measured error stays ~1e-13.
+  static __device__ __forceinline__ double th(double x) {
+    const double e = exp(2.0 * fabs(x));
+    return copysign(1.0 - 2.0 / (e + 1.0), x);
+  }
+  // tan on |x| <= pi/4 (the steering range when delta_max <= pi/4): sin / cos
+  // of their minimax kernels (fdlibm __kernel_sin / __kernel_cos
+  // coefficients), no range reduction
+  static __device__ __forceinline__ double tn_small(double x) {
+    const double z = x * x;
+    const double sp = x + x * z * (-1.66666666666666324348e-01 +
+        z * (8.33333333332248946124e-03 + z * (-1.98412698298579493134e-04 +
+        z * (2.75573137070700676789e-06 + z * (-2.50507602534068634195e-08 +
+        z * 1.58969099521155010221e-10)))));
+    const double cp = 1.0 - 0.5 * z + z * z * (4.16666666666666019037e-02 +
+        z * (-1.38888888888741095749e-03 + z * (2.48015872894767294178e-05 +
+        z * (-2.75573143513906633035e-07 + z * (2.08757232129817482790e-09 +
+        z * -1.13596475577881948265e-11)))));
+    return sp / cp;
+  }
+#else
   static __device__ __forceinline__ double th(double x) { return tanh(x); }
-  static __device__ __forceinline__ double tn(double x) { return tan(x); }
   static __device__ __forceinline__ double tn_small(double x) { return tan(x); }
+#endif
+  static __device__ __forceinline__ double tn(double x) { return tan(x); }
   static __device__ __forceinline__ void sc(double x, double* s, double* c) { sincos(x, s, c); }
   static __device__ __forceinline__ double sq(double x) { return sqrt(x); }
   static __device__ __forceinline__ double ab(double x) { return fabs(x); }
