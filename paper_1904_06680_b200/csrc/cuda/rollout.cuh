@@ -161,10 +161,9 @@ constexpr int refill_min_blocks() {
                            : (Net::kP <= 24 ? PARAPLAN_REFILL64_MINB : 2);
 }
 
-// A relaxed load of a restart's goal cut. Not a volatile access: the
-// compiler may schedule the loop's other memory operations across it (a
-// volatile load here cost ~9% of the C2 rollout); `tag` (loop-variant) keeps
-// it from being hoisted out of the loop.
+// A relaxed load of a restart's goal cut (the value other lanes lower with
+// atomicMin); `tag` (loop-variant) keeps it from being hoisted out of the
+// loop.
 __device__ __forceinline__ uint32_t ld_cut(const uint32_t* p, int tag) {
   uint32_t v;
   asm("ld.relaxed.gpu.global.u32 %0, [%1]; // %2" : "=r"(v) : "l"(p), "r"(tag));
