@@ -112,6 +112,13 @@ __device__ __forceinline__ double2 ld_rec(const double2* p, unsigned long long p
 // 0.6% slower and C4/C5 unchanged (A/B on B200), so it is off by default
 #define PARAPLAN_FFMA2 0
 #endif
+#ifndef PARAPLAN_REFILL_MINB_2D
+// 2-D grid kinds (C4, C5 dense: latency-bound chains of cell / chunk / point
+// loads): 8 CTAs/SM at 64 registers despite 180-280 B of spills beat 6 at 80
+// (measured on B200: C4 -6.5%, C5 100k -6..7%, C5 10k H=100 -5%, N=1k equal;
+// 10 CTAs helped 100k further but cost N=1k 4%)
+#define PARAPLAN_REFILL_MINB_2D 8
+#endif
 #ifndef PARAPLAN_REFILL_MINB
 #define PARAPLAN_REFILL_MINB 6  // <= 85 registers: 6 CTAs (24 warps) per SM, no spills
 #endif

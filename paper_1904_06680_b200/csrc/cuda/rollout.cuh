@@ -156,9 +156,11 @@ __global__ void __launch_bounds__(256, sizeof(Real) == 4 && Net::P <= 24 ? PARAP
 // Resident CTAs per SM the register allocation must allow: [5,2,2] in FP32
 // fits 6 (<= 85 registers), wider nets and FP64 need more registers.
 template <typename Real, class Net>
-constexpr int refill_min_blocks() {
-  return sizeof(Real) == 4 ? (Net::kP <= 24 ? PARAPLAN_REFILL_MINB : (Net::kP <= 100 ? 3 : 2))
-                           : (Net::kP <= 24 ? PARAPLAN_REFILL64_MINB : 2);
+constexpr int refill_min_blocks(int grid = 3) {
+  return sizeof(Real) == 4
+             ? (Net::kP <= 24 ? (grid == 1 || grid == 2 ? PARAPLAN_REFILL_MINB_2D : PARAPLAN_REFILL_MINB)
+                              : (Net::kP <= 100 ? 3 : 2))
+             : (Net::kP <= 24 ? PARAPLAN_REFILL64_MINB : 2);
 }
 
 // A relaxed load of a restart's goal cut (the value other lanes lower with
@@ -173,7 +175,7 @@ __device__ __forceinline__ uint32_t ld_cut(const uint32_t* p, int tag) {
 // kCut: with the goal-horizon cut (a.goal_cut set); without it the loop
 // carries none of its instructions (~6% of a C2 rollout that never reaches).
 template <typename Real, class Net, int kGrid, bool kCut>
-__global__ void __launch_bounds__(kBlock, refill_min_blocks<Real, Net>())
+__global__ void __launch_bounds__(kBlock, refill_min_blocks<Real, Net>(kGrid))
     refill_kernel(const RoundArgs a) {
   constexpr int P = Net::kP;
   extern __shared__ __align__(16) unsigned char smem_raw[];
