@@ -152,6 +152,7 @@ void finish_field(pp_handle* h, ppdev::RoundArgs& a) {
       h->timing.launches += 3;
     } else {
       ppfield::pack(b, h->fp64, h->h_field.p);
+      phase("field-packed");
       ck(cudaMemcpyAsync(h->d_field.p, h->h_field.p, l.bytes, cudaMemcpyHostToDevice, st),
          "field H2D");
       h->timing.h2d_bytes += static_cast<int64_t>(l.bytes);
@@ -339,6 +340,7 @@ void upload_field_rows(pp_handle* h, const pp_snapshot& s, ppdev::RoundArgs& a) 
   const double cull = std::sqrt(a.r2) + 1e-3;
   if (N > 0) {
     ppfield::from_rows(h->field, s.field_xy, cfg.H + 1, N, cull);
+    phase("rows-binned");
   } else {
     h->field = ppfield::Binned{};
     h->field.rows = cfg.H + 1;
