@@ -427,7 +427,7 @@ __device__ __forceinline__ Real collide_margin(const Field<Real>& f, const Const
     const int rounds = __reduce_max_sync(kFull, cnt);
     const uint32_t p0 = pr + static_cast<uint32_t>(lo) *
                                  static_cast<uint32_t>(sizeof(typename Vec2T<Real>::type));
-#pragma unroll 4
+PARAPLAN_PRAGMA_UNROLL(PARAPLAN_K3_UNROLL)
     for (int j = 0; j < rounds; ++j) {
       const auto m = lds_point<Real>(
           p0 + static_cast<uint32_t>(j) * static_cast<uint32_t>(sizeof(typename Vec2T<Real>::type)));
