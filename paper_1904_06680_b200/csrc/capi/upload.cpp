@@ -67,6 +67,13 @@ void fill_consts(const ppdev::RoundArgs& a, ppdev::ConstsT<Real>* k) {
   k->wb_d = a.wheelbase;
   k->tan_small = a.delta_max <= 0.785 ? 1 : 0;
   k->flag_miss = 0;  // per round (round.cpp)
+  k->H = a.H;
+  k->any_pts = a.field_ns + a.field_nd > 0 ? 1 : 0;
+  const bool dyn = a.field_nd > 0;  // field_query.cuh bind_shared: the staged part
+  k->k3_row_bytes = dyn ? static_cast<uint32_t>(a.field_dstride * 2 * sizeof(Real)) : 0u;
+  k->k3_st_row_bytes = dyn ? static_cast<uint32_t>((a.grid_nx + 1) * sizeof(int)) : 0u;
+  k->xtop = Real(a.grid_nx - 1);
+  k->ytop = Real(a.grid_ny - 1);
 }
 
 // Device image of h->field in the compute precision (one H2D); the FP64 image

@@ -91,27 +91,38 @@ struct Rec {
 // host and read by the kernels straight from the parameter (constant) bank,
 // so they cost no registers.
 template <typename Real>
-struct ConstsT {
-  Real gx, gy, gphi, gv, gcos, gsin;  // goal in the anchor frame (planner.cpp:70-81)
-  Real v0, act0, pa0;                 // initial carry (planner.cpp:123-125)
+struct alignas(16) ConstsT {
+  // The fields a rollout step reads come first, four to a 16-byte group in
+  // the order the step uses them, so the FP32 kernels fetch them from the
+  // parameter bank with few vector loads (LDCU.128) per iteration.
+  Real gx, gy, gcos, gsin;            // goal in the anchor frame (planner.cpp:70-81)
+  Real gphi, gv, eps_xi, eps_eta;     // + GoalTolerance
+  Real eps_phi, eps_v, dmax, window;  // VehicleParams-derived
+  Real l_r, Ts, inv_wb, ts_umid;      // inv_wb: 1 / wheelbase (FP32 path multiplies);
+  Real ts_uhalf;                      // ts_umid, ts_uhalf: T_s (umin + umax) / 2, T_s (umax - umin) / 2
+  Real bx0, binv, qpad;  // cell grid of the field: origin, 1 / cell size; box query pad: cell / 8
+  Real bcx, bhx, hw;     // rectangle centre offset (fe - re)/2, half length (fe + re)/2, half width
+  Real dmarg;            // |margin| below which a discrete verdict is "marginal"
+  Real dmarg_rel;        // + this x the path so far: the flag band widens with the distance
+                         // travelled (the measured relative drift of a rollout's state)
+  Real dmarg_floor;      // the band's relative drift is at least this
+  int32_t flag_miss;     // several restarts: narrow collision MISSES are marginal too
+  int32_t tan_small;     // delta_max <= pi/4: tan by polynomial ratio (FP32)
+  // round shape the step reads (copies of RoundArgs values, same group rule)
+  int32_t H;             // horizon
+  int32_t any_pts;       // field_ns + field_nd > 0
+  uint32_t k3_row_bytes;     // kernel kind 3: bytes of one dynamic point row (0: static part)
+  uint32_t k3_st_row_bytes;  // kernel kind 3: bytes of one row of cell starts (0: static part)
+  Real xtop, ytop;       // grid_nx - 1, grid_ny - 1 (the last cell column / row)
+  // the rest: start state, feature scales, FP64-only divisors
+  Real v0, act0, pa0;    // initial carry (planner.cpp:123-125)
   Real inv_xi, inv_eta, inv_phi, inv_v;
-  double d_xi, d_eta, d_phi, d_v;     // NormConstants (FP64 path divides)
-  Real eps_xi, eps_eta, eps_phi, eps_v;
-  Real dmax, window, l_r, wb, Ts, umin, umax;
-  Real ts_umid, ts_uhalf;  // T_s (umin + umax) / 2, T_s (umax - umin) / 2 (FP32 speed update)
-  Real fe, re, hw, r2;  // chassis half-planes, squared bounding radius
-  Real cull;            // collision x-window half width: bounding radius + 1e-3
-  Real bx0, by0, binv;  // cell grid of the field: origin, 1 / cell size
-  Real qpad;            // pad of the chassis bounding box query: cell size / 8
-  Real dmarg;           // |margin| below which a discrete verdict is "marginal"
-  Real bcx, bhx;        // rectangle centre offset (fe - re)/2 and half length (fe + re)/2
-  Real inv_wb;          // 1 / wheelbase (FP32 path multiplies)
-  double wb_d;          // wheelbase (FP64 path divides, src/dynamics.cpp:52-55)
-  int32_t tan_small;    // delta_max <= pi/4: tan by polynomial ratio (FP32)
-  Real dmarg_floor;     // the band's relative drift is at least this
-  Real dmarg_rel;       // + this x the path so far: the flag band widens with the distance
-                        // travelled (the measured relative drift of a rollout's state)
-  int32_t flag_miss;    // several restarts: narrow collision MISSES are marginal too
+  Real wb, umin, umax;
+  Real fe, re, r2;       // chassis half-planes, squared bounding radius
+  Real cull;             // collision x-window half width: bounding radius + 1e-3
+  Real by0;              // cell grid origin (y)
+  double d_xi, d_eta, d_phi, d_v;  // NormConstants (FP64 path divides)
+  double wb_d;           // wheelbase (FP64 path divides, src/dynamics.cpp:52-55)
 };
 
 // Byte offsets of the parts of a field image.

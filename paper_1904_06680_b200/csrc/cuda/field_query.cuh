@@ -25,10 +25,11 @@ struct Field {
   int ncx, ncy;
   int coop;  // RoundArgs::coop
   // kernel kind 3 (one x-bucket part staged in shared memory): 32-bit shared
-  // addresses of its points and starts, and the byte strides of a state row
-  // (0 for a static part), fixed once per CTA so a step's row base is one
-  // IMAD each instead of a generic-to-shared conversion
-  uint32_t s_pts, s_st, row_bytes, st_row_bytes;
+  // addresses of its points and starts, fixed once per CTA so a step's row
+  // base is one IMAD each instead of a generic-to-shared conversion (the byte
+  // strides of a state row, 0 for a static part, are the round constants
+  // Consts::k3_row_bytes / k3_st_row_bytes)
+  uint32_t s_pts, s_st;
 };
 
 // ld.shared of a staged field's point / start at a 32-bit shared address
@@ -61,7 +62,7 @@ __device__ __forceinline__ Field<Real> field_at(const RoundArgs& a, const void* 
                 reinterpret_cast<const int*>(p + l.sst), reinterpret_cast<const int*>(p + l.dst),
                 reinterpret_cast<const R2*>(p + l.sbox), reinterpret_cast<const int*>(p + l.cst),
                 reinterpret_cast<const R2*>(p + l.cbox), a.field_ns, a.field_nd,
-                a.field_dstride, a.grid_nx, a.grid_ny, a.coop, 0u, 0u, 0u, 0u};
+                a.field_dstride, a.grid_nx, a.grid_ny, a.coop, 0u, 0u};
   return f;
 }
 
@@ -73,8 +74,6 @@ __device__ __forceinline__ void bind_shared(Field<Real>& f, const unsigned char*
   const bool dyn = f.Nd > 0;
   f.s_pts = s0 + static_cast<uint32_t>(dyn ? l.dpts : 0);
   f.s_st = s0 + static_cast<uint32_t>(dyn ? l.dst : l.sst);
-  f.row_bytes = dyn ? static_cast<uint32_t>(f.dstride * sizeof(typename Vec2T<Real>::type)) : 0u;
-  f.st_row_bytes = dyn ? static_cast<uint32_t>((f.ncx + 1) * sizeof(int)) : 0u;
 }
 
 // Inside-margin of one point against the chassis at (x, y, phi):
@@ -397,7 +396,7 @@ __device__ __forceinline__ Real collide_margin(const Field<Real>& f, const Const
                                                bool live = true) {
   const int ncx = f.ncx, ncy = f.ncy;
   const Real ac = fabs(c), as = fabs(s);
-  const Real top = Real(ncx - 1);
+  const Real top = K.xtop;  // ncx - 1
   // rectangle centre (x, y) + bcx (c, s); half extents bhx |c| + hw |s| (x)
   const Real ox = x + K.bcx * c - K.bx0;
   const Real ex = K.bhx * ac + K.hw * as + K.qpad;
@@ -405,7 +404,7 @@ __device__ __forceinline__ Real collide_margin(const Field<Real>& f, const Const
   const int cx_hi = static_cast<int>(fmin(fmax((ox + ex) * K.binv, Real(0)), top));
   int cy_lo = 0, cy_hi = 0;
   if constexpr (kGrid == 1 || kGrid == 2) {
-    const Real ytop = Real(ncy - 1);
+    const Real ytop = K.ytop;  // ncy - 1
     const Real oy = y + K.bcx * s - K.by0;
     const Real ey = K.bhx * as + K.hw * ac + K.qpad;
     cy_lo = static_cast<int>(fmin(fmax((oy - ey) * K.binv, Real(0)), ytop));
@@ -420,8 +419,8 @@ __device__ __forceinline__ Real collide_margin(const Field<Real>& f, const Const
     // consecutive points from its window's first (see scan_part). A lane
     // whose rollout is over scans nothing (its window would only lengthen the
     // warp's point loop)
-    const uint32_t st = f.s_st + static_cast<uint32_t>(h) * f.st_row_bytes;
-    const uint32_t pr = f.s_pts + static_cast<uint32_t>(h) * f.row_bytes;
+    const uint32_t st = f.s_st + static_cast<uint32_t>(h) * K.k3_st_row_bytes;
+    const uint32_t pr = f.s_pts + static_cast<uint32_t>(h) * K.k3_row_bytes;
     const int lo = lds_start(st + 4u * static_cast<uint32_t>(cx_lo));
     const int cnt = live ? lds_start(st + 4u * static_cast<uint32_t>(cx_hi + 1)) - lo : 0;
     const int rounds = __reduce_max_sync(kFull, cnt);

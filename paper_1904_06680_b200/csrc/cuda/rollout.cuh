@@ -186,7 +186,7 @@ __global__ void __launch_bounds__(kBlock, refill_min_blocks<Real, Net>(kGrid))
   mark_start(a);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const Consts<Real>& K = consts_of<Real>(a);
-  const int H = a.H;
+  const int H = K.H;
   for (int i = threadIdx.x; i < kWarps * kMaxRestartsPerLaunch; i += blockDim.x) {
     (&table[0][0])[i] = empty_key();
   }
@@ -482,7 +482,7 @@ __global__ void __launch_bounds__(kBlock) lockstep_kernel(const RoundArgs a) {
 
   mark_start(a);
   const Consts<Real>& K = consts_of<Real>(a);
-  const int H = a.H;
+  const int H = K.H;
   const int P = a.n_params;
   const Field<Real> f = stage_field<Real, kGrid>(a, smem_raw);
   Real s0[5];

@@ -57,7 +57,7 @@ __device__ __forceinline__ int check_state(Lane<Real>& L, const Consts<Real>& K,
     band += L.path * fmax(K.dmarg_floor, K.dmarg_rel * fmin(q * q, Real(1)));
   }
   bool narrow = false;
-  if (f.Ns + f.Nd > 0) {
+  if (K.any_pts) {  // f.Ns + f.Nd > 0
     // a lane may stop at a hit whose margin is too large to flip
     const Real cm = collide_margin<Real, kGrid>(f, K, L.h, L.x, L.y, cphi, sphi, band, live);
     hit = cm > Real(0);
