@@ -43,6 +43,9 @@ JSON_DIRS = [
 
 HOST_FLAGS = ["-std=c++20", "-O3", "-fPIC", "-fno-math-errno", "-ffp-contract=off", "-pthread",
               "-Wall", "-Wno-unused-parameter"]
+# compile-time switches (PARAPLAN_NVCC_DEFS="-D..."): the -D ones reach the host
+# objects too, for constants both sides share (device_api.h)
+HOST_FLAGS += [d for d in os.environ.get("PARAPLAN_NVCC_DEFS", "").split() if d.startswith("-D")]
 NVCC_FLAGS = ["-std=c++17", "-O3", "-lineinfo", "-Xptxas", "-v", "-Xcompiler", "-fPIC",
               "--expt-relaxed-constexpr"] + ARCH + os.environ.get("PARAPLAN_NVCC_DEFS", "").split()
 

@@ -83,8 +83,10 @@ void finish_field(pp_handle* h, ppdev::RoundArgs& a) {
     ppfield::Binned& m = h->field;
     const bool one_part = m.Ns == 0 || m.Nd == 0;
     const bool pad = m.mode() == 0 && one_part && !m.dyn_deferred;
-    m.pad_s = pad && m.Nd == 0 ? m.Ns : 0;
-    m.pad_d = pad && m.Ns == 0 ? m.Nd : 0;
+    // a window starts at a point index <= N and the warp reads up to its
+    // longest window rounded up to a whole group: N + kK3Group - 1 sentinels
+    m.pad_s = pad && m.Nd == 0 ? m.Ns + ppdev::kK3Group - 1 : 0;
+    m.pad_d = pad && m.Ns == 0 ? m.Nd + ppdev::kK3Group - 1 : 0;
   }
   const ppfield::Binned& b = h->field;
   a.field_ns = b.Ns;

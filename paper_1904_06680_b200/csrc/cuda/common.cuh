@@ -112,13 +112,6 @@ __device__ __forceinline__ double2 ld_rec(const double2* p, unsigned long long p
 // 0.6% slower and C4/C5 unchanged (A/B on B200), so it is off by default
 #define PARAPLAN_FFMA2 0
 #endif
-#ifndef PARAPLAN_K3_UNROLL
-// kind-3 point loop unroll (C2 rollout on B200: 1 -> 176.6 us, 2 -> 173.0,
-// 3 -> 179.1, 4 -> 173.7, 8 -> 179.7; C4/C5 within noise)
-#define PARAPLAN_K3_UNROLL 2
-#endif
-#define PARAPLAN_STR_(x) #x
-#define PARAPLAN_PRAGMA_UNROLL(n) _Pragma(PARAPLAN_STR_(unroll n))
 #ifndef PARAPLAN_REFILL_MINB_2D
 // 2-D grid kinds (C4, C5 dense: latency-bound chains of cell / chunk / point
 // loads): 8 CTAs/SM at 64 registers despite 180-280 B of spills beat 6 at 80

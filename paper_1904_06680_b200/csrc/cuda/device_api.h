@@ -87,6 +87,14 @@ struct Rec {
   double k1, k2;
 };
 
+// Kernel kind 3 scans a lane's x-bucket window kK3Group points per step of
+// its loop, with no remainder pass: the sentinel padding after each part of
+// the staged image holds N + kK3Group - 1 points (csrc/capi/upload.cpp).
+#ifndef PARAPLAN_K3_GROUP
+#define PARAPLAN_K3_GROUP 2
+#endif
+constexpr int kK3Group = PARAPLAN_K3_GROUP;
+
 // Round constants in the compute precision, filled once per snapshot on the
 // host and read by the kernels straight from the parameter (constant) bank,
 // so they cost no registers.

@@ -424,13 +424,18 @@ __device__ __forceinline__ Real collide_margin(const Field<Real>& f, const Const
     const int lo = lds_start(st + 4u * static_cast<uint32_t>(cx_lo));
     const int cnt = live ? lds_start(st + 4u * static_cast<uint32_t>(cx_hi + 1)) - lo : 0;
     const int rounds = __reduce_max_sync(kFull, cnt);
-    const uint32_t p0 = pr + static_cast<uint32_t>(lo) *
-                                 static_cast<uint32_t>(sizeof(typename Vec2T<Real>::type));
-PARAPLAN_PRAGMA_UNROLL(PARAPLAN_K3_UNROLL)
-    for (int j = 0; j < rounds; ++j) {
-      const auto m = lds_point<Real>(
-          p0 + static_cast<uint32_t>(j) * static_cast<uint32_t>(sizeof(typename Vec2T<Real>::type)));
-      best = fmax(best, point_margin<Real>(K, x, y, c, s, kx, ky, m.x, m.y));
+    constexpr uint32_t kPt = sizeof(typename Vec2T<Real>::type);
+    // whole groups of kK3Group points (the padding covers the overrun: a
+    // point past a lane's window lies beyond its box in x, or is a sentinel)
+    const int groups = (rounds + kK3Group - 1) / kK3Group;
+    uint32_t p = pr + static_cast<uint32_t>(lo) * kPt;
+#pragma unroll 1
+    for (int j = 0; j < groups; ++j, p += kK3Group * kPt) {
+#pragma unroll
+      for (int u = 0; u < kK3Group; ++u) {
+        const auto m = lds_point<Real>(p + static_cast<uint32_t>(u) * kPt);
+        best = fmax(best, point_margin<Real>(K, x, y, c, s, kx, ky, m.x, m.y));
+      }
     }
     return best;
   }
