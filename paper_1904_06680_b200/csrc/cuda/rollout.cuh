@@ -334,9 +334,10 @@ __global__ void __launch_bounds__(kBlock, refill_min_blocks<Real, Net>(kGrid))
           q_head += __popc(need) < avail ? __popc(need) : avail;
         }
       }
+      // stream exhausted, all lanes done and flushed (only a flush can end
+      // the loop: between flushes a lane that stops parks in `pend`)
+      if (!__any_sync(kFull, active || pend >= 0)) break;
     }
-    // stream exhausted, all lanes done and flushed
-    if (!__any_sync(kFull, active || pend >= 0)) break;
 
     // -------- one rollout state per lane --------
     uint32_t cut_ld = kCutNone;  // used after the step
