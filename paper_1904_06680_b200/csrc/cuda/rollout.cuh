@@ -291,7 +291,7 @@ __global__ void __launch_bounds__(kBlock, refill_min_blocks<Real, Net>(kGrid))
           if (b >= total_batches) {
             exhausted = true;
           } else {
-            q_r = static_cast<int>(b) / bpr;
+            q_r = a.restart_count == 1 ? 0 : static_cast<int>(b) / bpr;
             q_c0 = (static_cast<int>(b) - q_r * bpr) * 32;
             const int64_t left = a.count - q_c0;
             q_count = left < 32 ? static_cast<int>(left) : 32;
@@ -342,9 +342,10 @@ __global__ void __launch_bounds__(kBlock, refill_min_blocks<Real, Net>(kGrid))
     // -------- one rollout state per lane --------
     uint32_t cut_ld = kCutNone;  // used after the step
     if (kCut && (++iter & 7u) == 0u) cut_ld = ld_cut(goal_cut + my_r, static_cast<int>(iter));
-    // every lane steps (idle lanes only at the stream tail, results unused)
-    int cls = cls0 >= 0 ? (active ? cls0 : -1)
-                        : advance<Real, kGrid, Net, false>(L, net, K, f, H, active);
+    // every lane steps (idle lanes only at the stream tail, results unused).
+    // When state 0 already stops (cls0 >= 0) the lanes hold state 0, whose
+    // checks give cls0 again and whose transition is not committed
+    int cls = advance<Real, kGrid, Net, false>(L, net, K, f, H, active);
     bool cut = false;
     if constexpr (kCut) {
       if (cut_ld != kCutNone) cut_at = min(cut_at, static_cast<int>(cut_ld) + a.cut_slack);
