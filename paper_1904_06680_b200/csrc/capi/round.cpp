@@ -348,6 +348,7 @@ void run_round_launch(pp_handle* h, uint64_t t, int iter, int r0, int rc, const 
   phase("synced");
   float ms = 0.f;
   ck(cudaEventElapsedTime(&ms, h->ev0, h->ev1), "event timing");
+  phase("evtime");
   if (trace_level() >= 2) std::fprintf(stderr, "[paraplan] round gpu us: %.1f\n", 1e3 * ms);
   h->timing.kernel_ms += ms;
   h->timing.launches += (shape.refill ? 2 : 1) + (rerank && (!sharded || packed) ? 1 : 0) +
@@ -381,6 +382,7 @@ void run_round_launch(pp_handle* h, uint64_t t, int iter, int r0, int rc, const 
   }
   if (!rerank) return;
 
+  phase("outs");
   n_sel = reinterpret_cast<const uint32_t*>(hres)[2];
   const auto c_t0 = std::chrono::steady_clock::now();
   certify_round(h, a, t, iter, r0, rc, center, c0, c1, injected, out, fp64, n_sel,
@@ -549,6 +551,7 @@ void certify_round(pp_handle* h, ppdev::RoundArgs& a, uint64_t t, int iter, int 
   Exchange* xg = shard_mode != 0 ? h->xchg.get() : nullptr;
   std::vector<double> ctr(h->P, 0.0);
   if (center != nullptr) ctr.assign(center, center + h->P);
+  phase("cert-enter");
   struct Exact {
     int cls;
     int t_goal;
@@ -606,6 +609,7 @@ void certify_round(pp_handle* h, ppdev::RoundArgs& a, uint64_t t, int iter, int 
     return e;
   };
   if (h->pool == nullptr) h->pool = shared_pool().pool.get();
+  phase("cert-setup");
   // Every rollout starts from the same state 0, so the checks at state 0
   // (collision with field row 0, then the goal box; src/planner.cpp:137-152)
   // do not depend on theta. If they stop the rollout there, every candidate
@@ -633,6 +637,7 @@ void certify_round(pp_handle* h, ppdev::RoundArgs& a, uint64_t t, int iter, int 
       return;
     }
   }
+  phase("state0");
   const double alpha = a.sel_alpha;
   const auto rho_of = [&](int cls, int t_goal) {
     return cls != 2 ? a.sel_rho
@@ -709,6 +714,7 @@ void certify_round(pp_handle* h, ppdev::RoundArgs& a, uint64_t t, int iter, int 
       return;
     }
   }
+  phase("bounds");
   std::vector<char> certified(rc, 0);
   // per restart: the earliest cut of the round and of its list rounds
   std::vector<uint32_t> cut_eff(rc, ppdev::kCutNone);
