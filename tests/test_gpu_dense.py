@@ -128,3 +128,33 @@ def test_small_fields_every_kernel_kind(n, movers, precision):
                         field=abi.extrapolate(pts, w.model.H))
     w.snapshot = snap
     _plan_equal(w)
+
+
+@pytest.mark.parametrize("precision", [32, 64])
+@pytest.mark.parametrize("n", [1, 2, 3, 5])
+def test_tiny_fields_scan_group_overrun(n, precision):
+    """Kind 3 scans whole groups of kK3Group points (device_api.h): the last
+    group of the warp's longest window reads past it, into points further in
+    x or into the sentinel padding (N + kK3Group - 1 sentinels after the
+    part). Tiny all-static clouds right on the road, odd and even N, so that
+    windows end at the image's last point: every rollout's outcome must be
+    the oracle's (FP64 exactly; FP32 within the flip budget of the other
+    per-sample tests), and the certified plan equal."""
+    rng = np.random.default_rng(77 + n)
+    pts = np.zeros((n, 4))
+    pts[:, 0] = rng.uniform(5.0, 15.0, n)
+    pts[:, 1] = rng.uniform(-1.0, 1.0, n)
+    w = workloads.c5(2048, 30, n, precision=precision)
+    w.snapshot = abi.Snapshot(ev=w.snapshot.ev, actuator_delta=w.snapshot.actuator_delta,
+                              prev_action=w.snapshot.prev_action, goal=w.snapshot.goal,
+                              field=abi.extrapolate(pts, w.model.H))
+    _plan_equal(w)
+    w.model.refine = 0
+    dp = capi.DevicePlanner(w.model)
+    _, got = dp.evaluate(w.snapshot, w.t, 0, 0, 1, None, 0, 2048, per_sample=True)
+    want = Port(w.model).eval_candidates(w.snapshot, w.t, 0, 0, np.zeros(18), 0, 2048)
+    assert want["collided"].any()  # the cloud is in the way
+    flips = np.count_nonzero(got["collided"] != want["collided"])
+    assert flips <= (0 if precision == 64 else 5)
+    if precision == 64:
+        assert np.array_equal(got["steps"], want["steps"])
