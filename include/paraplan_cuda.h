@@ -183,7 +183,9 @@ typedef struct pp_plan_output {
 
 /* Per-call device accounting (for the benchmark and the roofline). */
 typedef struct pp_timing {
-  double kernel_ms;        /* device time of the sampling kernels (CUDA events) */
+  double kernel_ms;        /* device time of the sampling rounds: first kernel start to the
+                              result store (%globaltimer; CUDA events around the launches
+                              when a round has no generator kernel) */
   int64_t executed_steps;  /* sum over samples of dynamics steps simulated */
   int64_t checked_states;  /* sum over samples of states tested (steps + 1) */
   int64_t samples;         /* candidates evaluated on the device */

@@ -324,7 +324,8 @@ void run_round_launch(pp_handle* h, uint64_t t, int iter, int r0, int rc, const 
   // dependent kernel right behind the last round kernel (no event between
   // them, which would break the programmatic dependency)
   ck(static_cast<cudaError_t>(
-         ppdev::launch_copy_out(h->d_round.p, h->h_round.p, (rbytes + 15) / 16 * 16, h->stream)),
+         ppdev::launch_copy_out(h->d_round.p, h->h_round.p, (rbytes + 15) / 16 * 16, kExecOff,
+                                h->stream)),
      "result D2H");
   ck(cudaEventRecord(h->ev1, h->stream), "event");
   phase("enqueued");
@@ -346,16 +347,22 @@ void run_round_launch(pp_handle* h, uint64_t t, int iter, int r0, int rc, const 
   }
   ck(cudaStreamSynchronize(h->stream), "sampling kernel");
   phase("synced");
-  float ms = 0.f;
-  ck(cudaEventElapsedTime(&ms, h->ev0, h->ev1), "event timing");
+  // the round's device span: first kernel start to the result store
+  // (copy_out_kernel), else the events around the launches (no generator)
+  const char* hres = static_cast<const char*>(h->h_round.p);
+  const unsigned long long* ex = reinterpret_cast<const unsigned long long*>(hres + kExecOff);
+  double ms = 1e-6 * static_cast<double>(ex[ppdev::kExecRoundT0]);
+  if (ex[ppdev::kExecRoundT0] == 0ull) {
+    float ems = 0.f;
+    ck(cudaEventElapsedTime(&ems, h->ev0, h->ev1), "event timing");
+    ms = ems;
+  }
   phase("evtime");
   if (trace_level() >= 2) std::fprintf(stderr, "[paraplan] round gpu us: %.1f\n", 1e3 * ms);
   h->timing.kernel_ms += ms;
   h->timing.launches += (shape.refill ? 2 : 1) + (rerank && (!sharded || packed) ? 1 : 0) +
                         (keys_only ? 1 : 0) + 1;
   h->timing.samples += count * rc;
-  const char* hres = static_cast<const char*>(h->h_round.p);
-  const unsigned long long* ex = reinterpret_cast<const unsigned long long*>(hres + kExecOff);
   h->timing.executed_steps += static_cast<int64_t>(ex[2]);
   // the next round's flush rule, from this round's mean rollout length
   // (measured on B200: rollouts of ~9 steps (C5 H=10) flush best every 2

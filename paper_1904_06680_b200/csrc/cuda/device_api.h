@@ -256,6 +256,9 @@ struct RoundArgs {
   int32_t flush_min;
 };
 
+// RoundArgs::exec slot of the round's device start stamp (generate_kernel)
+constexpr int kExecRoundT0 = 7;
+
 // Architecture dispatch of the specialised kernels.
 enum class NetKind : int { kGeneric = 0, k5_2_2 = 1, k5_10_2 = 2, k5_10_10_2 = 3 };
 NetKind classify(const int32_t* sizes, int32_t n_layers);
@@ -329,9 +332,13 @@ struct ListFilterArgs {
   int32_t sms;
 };
 int launch_list_filter(const ListFilterArgs& f, void* stream);
-// Copy `bytes` (a multiple of 16) of device memory into pinned host memory
-// with SM stores, after the previous kernel on `stream` (dependent launch).
-int launch_copy_out(const void* src, void* host_dst, size_t bytes, void* stream);
+// Copy `bytes` (a multiple of 16) of the device round block into pinned host
+// memory with SM stores, after the previous kernel on `stream` (dependent
+// launch behind the round's last kernel). Slot kExecRoundT0 of the
+// block's exec counters (at `exec_off` bytes) holds the device time the
+// round's first kernel started (0: no stamp); the host copy receives the
+// round's span in ns there instead, and the device slot is cleared.
+int launch_copy_out(const void* src, void* host_dst, size_t bytes, size_t exec_off, void* stream);
 // FP64 re-evaluation of the selected candidates into sel_out.
 int launch_refine(NetKind k, const RoundArgs& a, void* stream);
 // Resident refine_kernel CTAs of 128 threads per SM.

@@ -132,6 +132,8 @@ __global__ void __launch_bounds__(256, sizeof(Real) == 4 && Net::P <= 24 ? PARAP
   constexpr int W = rec_width<Real>(P);
   constexpr int V = W * static_cast<int>(sizeof(Real)) / 16;
   const Consts<Real>& K = consts_of<Real>(a);
+  // the round's device start (copy_out_kernel publishes the round's span)
+  if (blockIdx.x == 0 && threadIdx.x == 0 && a.exec != nullptr) a.exec[kExecRoundT0] = global_ns();
   Real s0[5];
   start_features(K, s0);
   Vec16<Real>* recs = static_cast<Vec16<Real>*>(a.theta_buf);
