@@ -75,15 +75,19 @@ __device__ __forceinline__ void draw_theta(const RoundArgs& a, uint64_t prefix, 
       if (i + 1 < P) put(i + 1, Real(__ldg(a.center_f + i + 1) + sigma * (r * sn)));
     }
   } else {
-    const double sigma = pow(10.0, a.sig_lo + unit53(g.next()) * a.sig_span);
+    // FP64 path: libdevice's exp10 and sincospi (sin / cos of pi * 2 u2, the
+    // product 2 u2 exact) instead of pow(10, .) and sincos(2 pi u2): theta
+    // stays within a few ulps of the reference's draw (the host regenerates
+    // the returned plan's theta in the reference's own arithmetic), and
+    // sincospi needs no multi-part reduction of 2 pi u2
+    const double sigma = exp10(a.sig_lo + unit53(g.next()) * a.sig_span);
 #pragma unroll
     for (int i = 0; i < P; i += 2) {
       const double u1 = 1.0 - unit53(g.next());
       const double u2 = unit53(g.next());
       const double r = sqrt(-2.0 * log(u1));
-      const double t = kTwoPi * u2;
       double sn, cs;
-      sincos(t, &sn, &cs);
+      sincospi(2.0 * u2, &sn, &cs);
       put(i, Real(__ldg(center + i) + sigma * (r * cs)));
       if (i + 1 < P) put(i + 1, Real(__ldg(center + i + 1) + sigma * (r * sn)));
     }
