@@ -39,6 +39,12 @@ constexpr int kWarps = kBlock / 32;
 // than 4 CTAs at C2 once the Box-Muller runs in MUFU); other nets: 1
 #define PARAPLAN_GEN_MINB 6
 #endif
+#ifndef PARAPLAN_GEN_MINB_MID
+#define PARAPLAN_GEN_MINB_MID 2  // theta generator of FP32 [5,10,2] (rollout.cuh gen_min_blocks)
+#endif
+#ifndef PARAPLAN_GEN_MID_MAXP
+#define PARAPLAN_GEN_MID_MAXP 96
+#endif
 #ifndef PARAPLAN_REFILL64_MINB
 #define PARAPLAN_REFILL64_MINB 4  // FP64 [5,2,2]/[5,10,2]: <= 128 registers
 #endif

@@ -125,8 +125,22 @@ __device__ __forceinline__ void generate_one(const RoundArgs& a, const Consts<Re
   for (int j = 0; j < V; ++j) st_rec(recs + s * V + j, rec.q[j], keep);
 }
 
+// Resident 256-thread CTAs per SM the generator's register cap must allow:
+// FP32 [5,2,2] PARAPLAN_GEN_MINB; FP32 [5,10,2] (a 91-float record)
+// PARAPLAN_GEN_MINB_MID (2: 128 registers, a little spill, measured on B200:
+// its C2 round 0.557 -> 0.453 ms against 1 CTA at 232 registers; 3 CTAs
+// spill 328 B and give 0.507); the rest 1 (FP64 [5,2,2] needs 102 registers,
+// 2 CTAs anyway; 3 CTAs measured no faster)
 template <typename Real, class Net>
-__global__ void __launch_bounds__(256, sizeof(Real) == 4 && Net::P <= 24 ? PARAPLAN_GEN_MINB : 1)
+constexpr int gen_min_blocks() {
+  return sizeof(Real) != 4 ? 1
+         : Net::P <= 24    ? PARAPLAN_GEN_MINB
+         : Net::P <= PARAPLAN_GEN_MID_MAXP ? PARAPLAN_GEN_MINB_MID
+                           : 1;
+}
+
+template <typename Real, class Net>
+__global__ void __launch_bounds__(256, gen_min_blocks<Real, Net>())
     generate_kernel(const RoundArgs a) {
   constexpr int P = Net::P;
   constexpr int W = rec_width<Real>(P);
