@@ -42,6 +42,11 @@ constexpr int kWarps = kBlock / 32;
 #ifndef PARAPLAN_GEN_MINB_MID
 #define PARAPLAN_GEN_MINB_MID 2  // theta generator of FP32 [5,10,2] (rollout.cuh gen_min_blocks)
 #endif
+#ifndef PARAPLAN_REFILL_MINB_MID
+// FP32 [5,10,2] rollout CTAs/SM (4: 128 registers, 8 B spill; its C2 round
+// 0.452 ms at 3 CTAs / 142 registers, 0.433 at 4, 0.52 at 5 with 168 B spills)
+#define PARAPLAN_REFILL_MINB_MID 4
+#endif
 #ifndef PARAPLAN_GEN_MID_MAXP
 #define PARAPLAN_GEN_MID_MAXP 96
 #endif
