@@ -47,6 +47,11 @@ constexpr int kWarps = kBlock / 32;
 // 0.452 ms at 3 CTAs / 142 registers, 0.433 at 4, 0.52 at 5 with 168 B spills)
 #define PARAPLAN_REFILL_MINB_MID 4
 #endif
+#ifndef PARAPLAN_REFILL_MINB_BIG
+// FP32 [5,10,10,2] rollout CTAs/SM (2: 255 registers; 3 spills 344 B and its
+// C2 round goes 1.06 -> 1.47 ms)
+#define PARAPLAN_REFILL_MINB_BIG 2
+#endif
 #ifndef PARAPLAN_GEN_MID_MAXP
 #define PARAPLAN_GEN_MID_MAXP 96
 #endif

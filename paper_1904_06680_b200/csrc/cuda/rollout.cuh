@@ -175,7 +175,7 @@ template <typename Real, class Net>
 constexpr int refill_min_blocks(int grid = 3) {
   return sizeof(Real) == 4
              ? (Net::kP <= 24 ? (grid == 1 || grid == 2 ? PARAPLAN_REFILL_MINB_2D : PARAPLAN_REFILL_MINB)
-                              : (Net::kP <= 100 ? PARAPLAN_REFILL_MINB_MID : 2))
+                              : (Net::kP <= 100 ? PARAPLAN_REFILL_MINB_MID : PARAPLAN_REFILL_MINB_BIG))
              : (Net::kP <= 24 ? PARAPLAN_REFILL64_MINB : 2);
 }
 
